@@ -1,0 +1,550 @@
+/* CPU oracle for the minibatch training step — see ember_oracle.h for scope and parity status.
+ * TEST INFRASTRUCTURE ONLY (the checker; never the measured or shipped path).
+ *
+ * Every function cites the reference line it restates. Arithmetic is fp32 storage with fp32
+ * accumulation in a fixed order (built with -ffp-contract=off), OpenMP over independent rows only,
+ * so results are bit-reproducible for any thread count.
+ */
+#include "ember_oracle.h"
+
+#include <float.h>
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+int orc_num_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+/* ---------------------------------------------------------------- RNG (common.h:51-117) */
+
+/* common.h:51-56 */
+uint64_t orc_splitmix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
+/* common.h:59 */
+uint64_t orc_mix_seed(uint64_t base, uint64_t salt) { return orc_splitmix64(base ^ orc_splitmix64(salt)); }
+/* common.h:60 */
+uint64_t orc_mix_seed3(uint64_t base, uint64_t a, uint64_t b) { return orc_mix_seed(orc_mix_seed(base, a), b); }
+
+typedef struct {
+    uint64_t s;
+} orc_rng;
+
+/* Rng::Rng, common.h:67 */
+static inline orc_rng rng_make(uint64_t seed) {
+    orc_rng r = {orc_splitmix64(seed ^ 0x2545f4914f6cdd1dULL)};
+    return r;
+}
+/* Rng::next, common.h:69-72 */
+static inline uint64_t rng_next(orc_rng* r) {
+    r->s = orc_splitmix64(r->s);
+    return r->s;
+}
+/* Rng::uniform_below, common.h:75-87 (Lemire multiply-shift with rejection) */
+static inline uint64_t rng_below(orc_rng* r, uint64_t n) {
+    for (;;) {
+        uint64_t x = rng_next(r);
+        unsigned __int128 m = (unsigned __int128)x * n;
+        uint64_t lo = (uint64_t)m;
+        if (lo < n) {
+            uint64_t threshold = (0ULL - n) % n;
+            if (lo < threshold) continue;
+        }
+        return (uint64_t)(m >> 64);
+    }
+}
+/* Rng::uniform01 / uniform, common.h:90-92 */
+static inline float rng_uniform(orc_rng* r, float lo, float hi) {
+    double u = (double)(rng_next(r) >> 11) * (1.0 / 9007199254740992.0);
+    return lo + (float)u * (hi - lo);
+}
+
+void orc_rng_next(uint64_t seed, uint32_t k, uint64_t* out) {
+    orc_rng r = rng_make(seed);
+    for (uint32_t i = 0; i < k; ++i) out[i] = rng_next(&r);
+}
+void orc_rng_uniform_below(uint64_t seed, uint64_t n, uint32_t k, uint64_t* out) {
+    orc_rng r = rng_make(seed);
+    for (uint32_t i = 0; i < k; ++i) out[i] = rng_below(&r, n);
+}
+void orc_rng_uniform(uint64_t seed, float lo, float hi, uint32_t k, float* out) {
+    orc_rng r = rng_make(seed);
+    for (uint32_t i = 0; i < k; ++i) out[i] = rng_uniform(&r, lo, hi);
+}
+
+/* ---------------------------------------------------------------- partitions */
+
+uint64_t orc_part_offset(uint64_t V, uint32_t p, uint32_t k) {
+    uint64_t q = V / p, rem = V % p;
+    return (uint64_t)k * q + (k < rem ? k : rem);
+}
+uint64_t orc_part_size(uint64_t V, uint32_t p, uint32_t k) {
+    uint64_t q = V / p, rem = V % p;
+    return q + (k < rem ? 1 : 0);
+}
+
+/* ---------------------------------------------------------------- model */
+
+/* Per-edge "adjusted" vectors so that every score is a plain dot product:
+ *   destination corruption: f(s, r, x) = adj_dst(s, r) . x
+ *   source corruption:      f(x, r, t) = adj_src(r, t) . x
+ * Dot:      adj_dst = s,        adj_src = t
+ * DistMult: adj_dst = s*r,      adj_src = r*t
+ * ComplEx (halves [re | im]): f = Re(<s, r, conj(t)>)
+ *           adj_dst = s*r (complex product) as [re | im]
+ *           adj_src = [Re(r conj t) | -Im(r conj t)]                                        */
+static void adjust_dst(int32_t kind, uint32_t d, const float* s, const float* r, float* out) {
+    if (kind == ORC_DOT) {
+        memcpy(out, s, d * sizeof(float));
+    } else if (kind == ORC_DISTMULT) {
+        for (uint32_t k = 0; k < d; ++k) out[k] = s[k] * r[k];
+    } else {
+        uint32_t h = d / 2;
+        for (uint32_t k = 0; k < h; ++k) {
+            float a = s[k], b = s[h + k], c = r[k], e = r[h + k];
+            out[k] = a * c - b * e;
+            out[h + k] = a * e + b * c;
+        }
+    }
+}
+
+static void adjust_src(int32_t kind, uint32_t d, const float* r, const float* t, float* out) {
+    if (kind == ORC_DOT) {
+        memcpy(out, t, d * sizeof(float));
+    } else if (kind == ORC_DISTMULT) {
+        for (uint32_t k = 0; k < d; ++k) out[k] = r[k] * t[k];
+    } else {
+        uint32_t h = d / 2;
+        for (uint32_t k = 0; k < h; ++k) {
+            float c = r[k], e = r[h + k], x = t[k], y = t[h + k];
+            out[k] = c * x + e * y;
+            out[h + k] = c * y - e * x;
+        }
+    }
+}
+
+static inline float dotf(const float* a, const float* b, uint32_t d) {
+    float acc = 0.f;
+    for (uint32_t k = 0; k < d; ++k) acc += a[k] * b[k];
+    return acc;
+}
+
+/* SPEC.md:139-147 */
+float orc_score(int32_t kind, uint32_t dim, const float* s, const float* r, const float* d) {
+    float* tmp = (float*)malloc(dim * sizeof(float));
+    adjust_dst(kind, dim, s, r, tmp);
+    float f = dotf(tmp, d, dim);
+    free(tmp);
+    return f;
+}
+
+/* SPEC.md:175-183. One Rng stream per global row keeps init order-independent and
+ * identical between the GPU initializer and this oracle. */
+void orc_init_rows(uint64_t seed, uint32_t dim, uint64_t row_begin, uint64_t rows, float* theta) {
+    const float a = (float)(1.0 / sqrt((double)dim));
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < (int64_t)rows; ++r) {
+        orc_rng g = rng_make(orc_mix_seed(seed, row_begin + (uint64_t)r));
+        float* out = theta + (uint64_t)r * dim;
+        for (uint32_t k = 0; k < dim; ++k) out[k] = rng_uniform(&g, -a, a);
+    }
+}
+
+/* SPEC.md:148-156 + design decisions SPEC.md:194-195, 425 (negatives from the resident
+ * partitions: destination side from the dst partition, source side from the src partition).
+ * Counter-based stream: every slot owns Rng(mix_seed(mix_seed(seed, epoch, bucket_step),
+ * batch_in_bucket, (chunk*2 + side)*n_t + slot)), so slots are independent of each other
+ * and of evaluation order. */
+void orc_sample_negatives(const orc_model* m, uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket,
+                          const uint32_t* bucket_edges, uint64_t bucket_n, uint64_t src_off, uint64_t src_size,
+                          uint64_t dst_off, uint64_t dst_size, uint32_t* out) {
+    const uint32_t nt = m->num_negatives;
+    const uint32_t n_deg = (uint32_t)ceil((double)m->alpha * (double)nt);
+    const uint64_t base = orc_mix_seed(orc_mix_seed3(m->neg_seed, epoch, bucket_step), batch_in_bucket);
+    const uint32_t chunks = m->num_chunks ? m->num_chunks : 1;
+    for (uint32_t q = 0; q < chunks; ++q) {
+        for (uint32_t side = 0; side < 2; ++side) {
+            for (uint32_t k = 0; k < nt; ++k) {
+                uint64_t slot = ((uint64_t)q * 2 + side) * nt + k;
+                orc_rng g = rng_make(orc_mix_seed(base, slot));
+                uint32_t id;
+                if (k < n_deg && bucket_n > 0) {
+                    uint64_t e = rng_below(&g, bucket_n);
+                    id = side == 0 ? bucket_edges[3 * e + 2] : bucket_edges[3 * e + 0];
+                } else if (side == 0) {
+                    id = (uint32_t)(dst_off + rng_below(&g, dst_size));
+                } else {
+                    id = (uint32_t)(src_off + rng_below(&g, src_size));
+                }
+                out[slot] = id;
+            }
+        }
+    }
+}
+
+typedef struct {
+    uint32_t key;
+    uint32_t idx;
+} kv;
+
+static int kv_cmp(const void* a, const void* b) {
+    const kv* x = (const kv*)a;
+    const kv* y = (const kv*)b;
+    if (x->key != y->key) return x->key < y->key ? -1 : 1;
+    return x->idx < y->idx ? -1 : (x->idx > y->idx);
+}
+
+/* Sums gradient rows per id in ascending (id, occurrence) order; returns #unique. */
+static uint32_t reduce_rows(const uint32_t* keys, uint32_t n, const float* rows, uint32_t d, uint32_t* ids_out,
+                            float* rows_out) {
+    kv* v = (kv*)malloc((size_t)n * sizeof(kv));
+    for (uint32_t i = 0; i < n; ++i) {
+        v[i].key = keys[i];
+        v[i].idx = i;
+    }
+    qsort(v, n, sizeof(kv), kv_cmp);
+    uint32_t* seg = (uint32_t*)malloc(((size_t)n + 1) * sizeof(uint32_t));
+    uint32_t nu = 0;
+    for (uint32_t i = 0; i < n; ++i)
+        if (i == 0 || v[i].key != v[i - 1].key) seg[nu++] = i;
+    seg[nu] = n;
+#pragma omp parallel for schedule(static)
+    for (int64_t u = 0; u < (int64_t)nu; ++u) {
+        float* out = rows_out ? rows_out + (uint64_t)u * d : NULL;
+        if (ids_out) ids_out[u] = v[seg[u]].key;
+        if (!out) continue;
+        memset(out, 0, d * sizeof(float));
+        for (uint32_t i = seg[u]; i < seg[u + 1]; ++i) {
+            const float* g = rows + (uint64_t)v[i].idx * d;
+            for (uint32_t k = 0; k < d; ++k) out[k] += g[k];
+        }
+    }
+    free(seg);
+    free(v);
+    return nu;
+}
+
+/* SPEC.md:157-165 with the sign fix of SPEC.md:192: per edge and corruption side
+ *   loss = -f + log(e^f + sum_k e^{f'_k})  (max-subtracted), total = mean over positives;
+ * dL/df = (p0 - 1)/nb, dL/df'_k = p_k/nb; chain rule through the adjusted vectors. */
+double orc_loss_and_grad(const orc_model* m, const uint32_t* edges, uint32_t nb, const uint32_t* negs,
+                         const float* node_theta, const float* rel_theta, float* fpos_out, float* lse_out,
+                         uint32_t* node_ids, float* node_rows, uint32_t* n_node, uint32_t* rel_ids, float* rel_rows,
+                         uint32_t* n_rel) {
+    const uint32_t d = m->dim, nt = m->num_negatives;
+    const uint32_t chunks = m->num_chunks ? m->num_chunks : 1;
+    const int32_t kind = m->kind;
+    const float inv_b = 1.0f / (float)nb;
+    const uint32_t chunk_rows = (nb + chunks - 1) / chunks;
+    const uint64_t nneg = (uint64_t)chunks * 2 * nt;
+
+    float* A = (float*)malloc((size_t)2 * nb * d * sizeof(float));   /* [side][edge][d] adjusted */
+    float* dA = (float*)calloc((size_t)2 * nb * d, sizeof(float));   /* [side][edge][d] */
+    float* P = (float*)malloc((size_t)2 * nb * (nt ? nt : 1) * sizeof(float)); /* [side][edge][k] */
+    float* N = (float*)malloc((nneg ? nneg : 1) * d * sizeof(float));  /* negative rows */
+    float* dN = (float*)calloc((nneg ? nneg : 1) * d, sizeof(float));
+    float* fpos = (float*)malloc((size_t)nb * sizeof(float));
+    float* g0 = (float*)malloc((size_t)2 * nb * sizeof(float));
+    double* loss_e = (double*)malloc((size_t)nb * sizeof(double));
+    int bad = 0;
+
+    for (uint64_t i = 0; i < nneg; ++i) memcpy(N + i * d, node_theta + (uint64_t)negs[i] * d, d * sizeof(float));
+
+    /* gather + adjust + positive score (Alg.1 formBatch) */
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < (int64_t)nb; ++e) {
+        const uint32_t s = edges[3 * e], r = edges[3 * e + 1], t = edges[3 * e + 2];
+        const float* ts = node_theta + (uint64_t)s * d;
+        const float* tt = node_theta + (uint64_t)t * d;
+        const float* tr = kind == ORC_DOT ? NULL : rel_theta + (uint64_t)r * d;
+        adjust_dst(kind, d, ts, tr, A + (uint64_t)e * d);
+        adjust_src(kind, d, tr, tt, A + ((uint64_t)nb + e) * d);
+        fpos[e] = dotf(A + (uint64_t)e * d, tt, d);
+    }
+
+    /* scores vs shared negatives, log-sum-exp, dA */
+#pragma omp parallel for schedule(static) reduction(| : bad)
+    for (int64_t e = 0; e < (int64_t)nb; ++e) {
+        const uint32_t q = (uint32_t)(e / chunk_rows);
+        double le = 0.0;
+        for (uint32_t side = 0; side < 2; ++side) {
+            const float* a = A + ((uint64_t)side * nb + e) * d;
+            const float* Ns = N + ((uint64_t)q * 2 + side) * nt * d;
+            float* p = P + ((uint64_t)side * nb + e) * nt;
+            const float f = fpos[e];
+            float mx = f;
+            for (uint32_t k = 0; k < nt; ++k) {
+                p[k] = dotf(a, Ns + (uint64_t)k * d, d);
+                if (!(p[k] == p[k]) || isinf(p[k])) bad = 1;
+                if (p[k] > mx) mx = p[k];
+            }
+            float z = expf(f - mx);
+            for (uint32_t k = 0; k < nt; ++k) z += expf(p[k] - mx);
+            const float lse = mx + logf(z);
+            if (lse_out) lse_out[(uint64_t)side * nb + e] = lse;
+            le += (double)(lse - f);
+            const float p0 = expf(f - lse);
+            const float gpos = (p0 - 1.0f) * inv_b;
+            g0[(uint64_t)side * nb + e] = gpos;
+            float* da = dA + ((uint64_t)side * nb + e) * d;
+            /* d f / d adj = the "other" endpoint: t for dst corruption, s for src corruption */
+            const float* other = node_theta + (uint64_t)edges[3 * e + (side == 0 ? 2 : 0)] * d;
+            for (uint32_t j = 0; j < d; ++j) da[j] = gpos * other[j];
+            for (uint32_t k = 0; k < nt; ++k) {
+                const float pk = expf(p[k] - lse) * inv_b;
+                p[k] = pk;
+                const float* nk = Ns + (uint64_t)k * d;
+                for (uint32_t j = 0; j < d; ++j) da[j] += pk * nk[j];
+            }
+        }
+        loss_e[e] = le;
+    }
+
+    /* dN = P^T A per chunk and side, fixed edge order */
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < (int64_t)nneg; ++i) {
+        const uint32_t q = (uint32_t)(i / (2 * nt));
+        const uint32_t side = (uint32_t)((i / nt) % 2);
+        const uint32_t k = (uint32_t)(i % nt);
+        const uint32_t e0 = q * chunk_rows;
+        const uint32_t e1 = e0 + chunk_rows < nb ? e0 + chunk_rows : nb;
+        float* out = dN + (uint64_t)i * d;
+        for (uint32_t e = e0; e < e1; ++e) {
+            const float pk = P[((uint64_t)side * nb + e) * nt + k];
+            const float* a = A + ((uint64_t)side * nb + e) * d;
+            for (uint32_t j = 0; j < d; ++j) out[j] += pk * a[j];
+        }
+    }
+
+    /* chain rule back through adjust (per edge: src row, dst row, rel row) */
+    float* Gs = (float*)calloc((size_t)nb * d, sizeof(float));
+    float* Gt = (float*)calloc((size_t)nb * d, sizeof(float));
+    float* Gr = (float*)calloc((size_t)nb * d, sizeof(float));
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < (int64_t)nb; ++e) {
+        const uint32_t s = edges[3 * e], r = edges[3 * e + 1], t = edges[3 * e + 2];
+        const float* ts = node_theta + (uint64_t)s * d;
+        const float* tt = node_theta + (uint64_t)t * d;
+        const float* tr = kind == ORC_DOT ? NULL : rel_theta + (uint64_t)r * d;
+        const float* ad = A + (uint64_t)e * d;
+        const float* as = A + ((uint64_t)nb + e) * d;
+        const float* u = dA + (uint64_t)e * d;          /* grad wrt adj_dst */
+        const float* w = dA + ((uint64_t)nb + e) * d;   /* grad wrt adj_src */
+        const float gd = g0[e], gs = g0[(uint64_t)nb + e];
+        float* gS = Gs + (uint64_t)e * d;
+        float* gT = Gt + (uint64_t)e * d;
+        float* gR = Gr + (uint64_t)e * d;
+        /* positive-score terms: f = adj_dst . t  and  f = adj_src . s */
+        for (uint32_t j = 0; j < d; ++j) {
+            gT[j] = gd * ad[j];
+            gS[j] = gs * as[j];
+        }
+        if (kind == ORC_DOT) {
+            for (uint32_t j = 0; j < d; ++j) {
+                gS[j] += u[j];
+                gT[j] += w[j];
+            }
+        } else if (kind == ORC_DISTMULT) {
+            for (uint32_t j = 0; j < d; ++j) {
+                gS[j] += u[j] * tr[j];
+                gR[j] = u[j] * ts[j] + w[j] * tt[j];
+                gT[j] += w[j] * tr[j];
+            }
+        } else {
+            const uint32_t h = d / 2;
+            for (uint32_t j = 0; j < h; ++j) {
+                const float a = ts[j], b = ts[h + j], c = tr[j], ee = tr[h + j], x = tt[j], y = tt[h + j];
+                const float u0 = u[j], u1 = u[h + j], w0 = w[j], w1 = w[h + j];
+                gS[j] += u0 * c + u1 * ee;
+                gS[h + j] += u1 * c - u0 * ee;
+                gR[j] = (u0 * a + u1 * b) + (w0 * x + w1 * y);
+                gR[h + j] = (u1 * a - u0 * b) + (w0 * y - w1 * x);
+                gT[j] += w0 * c - w1 * ee;
+                gT[h + j] += w0 * ee + w1 * c;
+            }
+        }
+    }
+
+    /* GradientDelta: one summed row per unique id */
+    const uint32_t nkeys = 2 * nb + (uint32_t)nneg;
+    uint32_t* keys = (uint32_t*)malloc((size_t)nkeys * sizeof(uint32_t));
+    float* rows = (float*)malloc((size_t)nkeys * d * sizeof(float));
+    for (uint32_t e = 0; e < nb; ++e) {
+        keys[e] = edges[3 * e];
+        keys[nb + e] = edges[3 * e + 2];
+    }
+    memcpy(rows, Gs, (size_t)nb * d * sizeof(float));
+    memcpy(rows + (size_t)nb * d, Gt, (size_t)nb * d * sizeof(float));
+    for (uint64_t i = 0; i < nneg; ++i) keys[2 * nb + i] = negs[i];
+    memcpy(rows + (size_t)2 * nb * d, dN, nneg * d * sizeof(float));
+    uint32_t nu = reduce_rows(keys, nkeys, rows, d, node_ids, node_rows);
+    if (n_node) *n_node = nu;
+    if (kind != ORC_DOT) {
+        uint32_t* rk = (uint32_t*)malloc((size_t)nb * sizeof(uint32_t));
+        for (uint32_t e = 0; e < nb; ++e) rk[e] = edges[3 * e + 1];
+        uint32_t nr = reduce_rows(rk, nb, Gr, d, rel_ids, rel_rows);
+        if (n_rel) *n_rel = nr;
+        free(rk);
+    } else if (n_rel) {
+        *n_rel = 0;
+    }
+
+    double loss = 0.0;
+    for (uint32_t e = 0; e < nb; ++e) loss += loss_e[e];
+    loss /= (double)nb;
+    if (fpos_out) memcpy(fpos_out, fpos, (size_t)nb * sizeof(float));
+
+    free(keys);
+    free(rows);
+    free(Gs);
+    free(Gt);
+    free(Gr);
+    free(A);
+    free(dA);
+    free(P);
+    free(N);
+    free(dN);
+    free(fpos);
+    free(g0);
+    free(loss_e);
+    return bad ? NAN : loss;
+}
+
+/* SPEC.md:166-174 */
+void orc_adagrad_apply(uint32_t d, float lr, float eps, const uint32_t* ids, const float* rows, uint32_t n,
+                       float* theta, float* acc) {
+#pragma omp parallel for schedule(static)
+    for (int64_t u = 0; u < (int64_t)n; ++u) {
+        float* th = theta + (uint64_t)ids[u] * d;
+        float* ac = acc + (uint64_t)ids[u] * d;
+        const float* g = rows + (uint64_t)u * d;
+        for (uint32_t k = 0; k < d; ++k) {
+            const float a = ac[k] + g[k] * g[k];
+            ac[k] = a;
+            th[k] -= lr * g[k] / (sqrtf(a) + eps);
+        }
+    }
+}
+
+/* Algorithm 1, one batch: getBatchEdges -> sample -> formBatch ->
+ * computeGradients -> updateGpuParameters (relations) -> updateCpuParameters (nodes). */
+double orc_train_batch(const orc_model* m, uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket,
+                       const uint32_t* bucket_edges, uint64_t bucket_n, uint64_t batch_begin, uint32_t nb,
+                       uint64_t src_off, uint64_t src_size, uint64_t dst_off, uint64_t dst_size, float* node_theta,
+                       float* node_acc, float* rel_theta, float* rel_acc) {
+    const uint32_t chunks = m->num_chunks ? m->num_chunks : 1;
+    const uint64_t nneg = (uint64_t)chunks * 2 * m->num_negatives;
+    uint32_t* negs = (uint32_t*)malloc((nneg ? nneg : 1) * sizeof(uint32_t));
+    orc_sample_negatives(m, epoch, bucket_step, batch_in_bucket, bucket_edges, bucket_n, src_off, src_size, dst_off,
+                         dst_size, negs);
+    const uint32_t cap = 2 * nb + (uint32_t)nneg;
+    uint32_t* ids = (uint32_t*)malloc((size_t)cap * sizeof(uint32_t));
+    float* rows = (float*)malloc((size_t)cap * m->dim * sizeof(float));
+    uint32_t* rids = (uint32_t*)malloc((size_t)nb * sizeof(uint32_t));
+    float* rrows = (float*)malloc((size_t)nb * m->dim * sizeof(float));
+    uint32_t nu = 0, nr = 0;
+    double loss = orc_loss_and_grad(m, bucket_edges + 3 * batch_begin, nb, negs, node_theta, rel_theta, NULL, NULL,
+                                    ids, rows, &nu, rids, rrows, &nr);
+    if (nr) orc_adagrad_apply(m->dim, m->lr, m->eps, rids, rrows, nr, rel_theta, rel_acc);
+    orc_adagrad_apply(m->dim, m->lr, m->eps, ids, rows, nu, node_theta, node_acc);
+    free(negs);
+    free(ids);
+    free(rows);
+    free(rids);
+    free(rrows);
+    return loss;
+}
+
+/* ---------------------------------------------------------------- eval */
+
+static int key_in(const uint64_t* keys, uint64_t n, uint64_t k) {
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        uint64_t mid = (lo + hi) / 2;
+        if (keys[mid] < k)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo < n && keys[lo] == k;
+}
+
+static inline uint64_t pack_key(uint64_t s, uint64_t r, uint64_t t) { return (s << 40) | (r << 24) | t; }
+
+void orc_eval_ranks(int32_t kind, uint32_t d, const float* node_theta, const float* rel_theta, uint64_t V,
+                    const uint32_t* test, uint32_t n_test, int filtered, const uint64_t* fkeys, uint64_t n_filter,
+                    const uint32_t* train, uint64_t n_train, uint32_t n_eval_neg, float alpha_eval, uint32_t block,
+                    uint64_t eval_seed, uint32_t* ranks_out) {
+    if (block == 0) block = 1;
+    uint32_t nblocks = (n_test + block - 1) / block;
+    uint32_t* negs = NULL;
+    if (!filtered) {
+        orc_model em;
+        memset(&em, 0, sizeof em);
+        em.num_negatives = n_eval_neg;
+        em.alpha = alpha_eval;
+        em.num_chunks = 1;
+        em.neg_seed = eval_seed;
+        negs = (uint32_t*)malloc((size_t)nblocks * 2 * (n_eval_neg ? n_eval_neg : 1) * sizeof(uint32_t));
+        for (uint32_t q = 0; q < nblocks; ++q)
+            orc_sample_negatives(&em, 0, 0, q, train, n_train, 0, V, 0, V, negs + (size_t)q * 2 * n_eval_neg);
+    }
+#pragma omp parallel
+    {
+        float* a = (float*)malloc(d * sizeof(float));
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t e = 0; e < (int64_t)n_test; ++e) {
+            const uint32_t s = test[3 * e], r = test[3 * e + 1], t = test[3 * e + 2];
+            const float* ts = node_theta + (uint64_t)s * d;
+            const float* tt = node_theta + (uint64_t)t * d;
+            const float* tr = kind == ORC_DOT ? NULL : rel_theta + (uint64_t)r * d;
+            for (uint32_t side = 0; side < 2; ++side) {
+                if (side == 0)
+                    adjust_dst(kind, d, ts, tr, a);
+                else
+                    adjust_src(kind, d, tr, tt, a);
+                const float pos = dotf(a, side == 0 ? tt : ts, d);
+                uint32_t rank = 1;
+                if (filtered) {
+                    for (uint64_t c = 0; c < V; ++c) {
+                        if (c == (side == 0 ? t : s)) continue;
+                        uint64_t key = side == 0 ? pack_key(s, r, c) : pack_key(c, r, t);
+                        float sc = dotf(a, node_theta + c * d, d);
+                        if (sc >= pos && !key_in(fkeys, n_filter, key)) ++rank;
+                    }
+                } else {
+                    const uint32_t* ng = negs + ((size_t)(e / block) * 2 + side) * n_eval_neg;
+                    for (uint32_t k = 0; k < n_eval_neg; ++k)
+                        if (dotf(a, node_theta + (uint64_t)ng[k] * d, d) >= pos) ++rank;
+                }
+                ranks_out[(uint64_t)side * n_test + e] = rank;
+            }
+        }
+        free(a);
+    }
+    free(negs);
+}
+
+/* SPEC.md:461-467 */
+void orc_aggregate(const uint32_t* ranks, uint64_t n, const uint32_t* ks, uint32_t nk, double* out) {
+    double mrr = 0.0;
+    for (uint32_t j = 0; j < nk; ++j) out[1 + j] = 0.0;
+    for (uint64_t i = 0; i < n; ++i) {
+        mrr += 1.0 / (double)ranks[i];
+        for (uint32_t j = 0; j < nk; ++j) out[1 + j] += ranks[i] <= ks[j] ? 1.0 : 0.0;
+    }
+    out[0] = n ? mrr / (double)n : 0.0;
+    for (uint32_t j = 0; j < nk; ++j) out[1 + j] = n ? out[1 + j] / (double)n : 0.0;
+}
