@@ -1,0 +1,190 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * ember_gpu.h — the C-ABI drop-in boundary of the B200-native minibatch training step.
+ *
+ * The reference (proj/, namespace ember) declares its trainer only as SPEC operations;
+ * proj/src/model.cpp and pipeline.cpp are listed in proj/src/CMakeLists.txt:5,8 but absent.
+ * Each entry point below names the SPEC/paper operation it replaces. Plain C types only:
+ * device pointers are `T*` into memory on the context's device, host pointers are marked.
+ * Every call returns EMBER_OK (0), EMBER_EUSER (1: bad config/arguments, the reference's
+ * ConfigError) or EMBER_EINTERNAL (2: CUDA/IO failure, non-finite score);
+ * ember_last_error() returns the thread-local message (SPEC.md:552 exit codes).
+ * No exceptions cross this boundary. One context per GPU, not thread-safe, all work is
+ * enqueued on the context's stream ("the model computation stage only uses a
+ * single worker").
+ */
+#ifndef EMBER_GPU_H
+#define EMBER_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EMBER_OK 0
+#define EMBER_EUSER 1
+#define EMBER_EINTERNAL 2
+
+/* ModelKind */
+#define EMBER_DOT 0
+#define EMBER_DISTMULT 1
+#define EMBER_COMPLEX 2
+
+/* Contraction engine for the shared-negative scores.
+ * TC_BF16X3: tcgen05 tensor cores, operands split hi+lo in bf16 (3 products, fp32 accumulate),
+ *            ~2^-17 relative per product — inside the 1e-4 parity tolerance.
+ * SIMT_FP32: CUDA-core fp32 tiles (correctness baseline). */
+#define EMBER_ENGINE_SIMT_FP32 0
+#define EMBER_ENGINE_TC_BF16X3 1
+
+/* OrderingKind (reference ordering.h:14) */
+#define EMBER_ORDER_ELIMINATION 0
+#define EMBER_ORDER_HILBERT 1
+#define EMBER_ORDER_HILBERT_SYMMETRIC 2
+#define EMBER_ORDER_RANDOM 3
+
+typedef struct ember_ctx ember_ctx;
+
+/* Hyper-parameters of the step: SPEC RunConfig subset + NegativeSampleSpec
+ * (SPEC.md:129-132). num_chunks: the batch is cut into num_chunks contiguous chunks, each scored
+ * against its own n_t shared negatives per corruption side (1 = whole batch shares). */
+typedef struct {
+    int32_t kind;
+    uint32_t dim;
+    float lr;
+    float eps;
+    uint32_t batch_size;    /* b: max edges per step */
+    uint32_t num_negatives; /* n_t per chunk per side */
+    float alpha;            /* degree-based fraction */
+    uint32_t num_chunks;
+    uint64_t neg_seed;
+    int32_t engine;         /* EMBER_ENGINE_* */
+    uint32_t reserved;
+} ember_model_desc;
+
+/* GraphMeta subset. Partition k owns global rows
+ * [k*floor(V/p) + min(k, V%p), +floor(V/p) + (k < V%p)). */
+typedef struct {
+    uint64_t num_nodes;
+    uint32_t num_relations;
+    uint32_t num_partitions;
+} ember_graph_desc;
+
+typedef struct {
+    double loss_sum;        /* sum of per-batch mean losses */
+    uint64_t batches;
+    uint64_t edges;
+    uint64_t unique_nodes;  /* node rows updated (sum over batches), filled when stats requested */
+    uint64_t unique_rels;
+} ember_step_stats;
+
+/* ---- lifecycle -------------------------------------------------------------------------- */
+/* stream: a cudaStream_t to enqueue on (NULL -> the context creates its own). */
+int ember_ctx_create(int device, const ember_model_desc* model, const ember_graph_desc* graph, void* stream,
+                     ember_ctx** out);
+int ember_ctx_destroy(ember_ctx* ctx);
+void* ember_ctx_stream(ember_ctx* ctx);
+const char* ember_last_error(void);
+int ember_version(void);
+
+/* ---- parameter storage (PartitionBlock; ParameterSlice SPEC.md:125) ------------
+ * Caller-owned device memory, borrowed: theta and acc are [rows x dim] f32 row-major for the
+ * partition's rows (the on-disk node_part_<k>.bin layout). */
+int ember_tables_bind(ember_ctx* ctx, uint32_t part, float* theta_dev, float* acc_dev);
+int ember_relations_bind(ember_ctx* ctx, float* theta_dev, float* acc_dev);
+/* init_embeddings for one bound partition / the relation table:
+ * global row g <- Rng(mix_seed(seed, g)).uniform(-1/sqrt(d), 1/sqrt(d)) x d; acc <- 0.
+ * Relations use seed ^ 0x52454c (row = relation id). */
+int ember_init_partition(ember_ctx* ctx, uint32_t part, uint64_t seed);
+int ember_init_relations(ember_ctx* ctx, uint64_t seed);
+
+/* ---- the training step (Algorithm 1; Stage 1+3+5 of Fig. 4) --------------
+ * One batch = edges [batch_begin, batch_begin+nb) of bucket (i, j) whose edges live at
+ * bucket_edges_dev (bucket_n EdgeTriples, device). Negatives are drawn from the bucket
+ * (degree part) and partitions j (dst side) / i (src side). Relations and nodes are updated
+ * in place with Adagrad before the call's work completes on the stream.
+ * loss_dev (nullable): device float receiving this batch's mean loss. */
+int ember_train_batch(ember_ctx* ctx, const uint32_t* bucket_edges_dev, uint64_t bucket_n, uint64_t batch_begin,
+                      uint32_t nb, uint32_t i, uint32_t j, uint64_t epoch, uint32_t bucket_step,
+                      uint32_t batch_in_bucket, float* loss_dev);
+/* trainEdgeBucket (Algorithm 2): all batches of one bucket, in order.
+ * stats (host, nullable) is filled after a stream sync when non-NULL. */
+int ember_train_bucket(ember_ctx* ctx, const uint32_t* bucket_edges_dev, uint64_t bucket_n, uint32_t i, uint32_t j,
+                       uint64_t epoch, uint32_t bucket_step, ember_step_stats* stats);
+/* Same step with the nb positives in HOST memory (pinned recommended), copied in on the
+ * context stream. The degree-based sampler still reads the bucket (bucket_edges_dev), which
+ * stays device-resident. loss_host (nullable; pinned for an asynchronous copy) receives the
+ * loss on the context stream: synchronise the stream before reading it. */
+int ember_train_batch_host(ember_ctx* ctx, const uint32_t* bucket_edges_dev, uint64_t bucket_n,
+                           const uint32_t* host_batch, uint32_t nb, uint32_t i, uint32_t j, uint64_t epoch,
+                           uint32_t bucket_step, uint32_t batch_in_bucket, float* loss_host);
+
+/* ---- per-op entry points (SPEC model ops), for parity tests ------------------------------ */
+/* sample_negatives: negs_dev receives num_chunks*2*n_t ids [chunk][side][slot]. */
+int ember_sample_negatives(ember_ctx* ctx, const uint32_t* bucket_edges_dev, uint64_t bucket_n, uint32_t i, uint32_t j,
+                           uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket, uint32_t* negs_dev);
+/* loss_and_grad: no parameter update. Outputs (device, nullable): fpos[nb],
+ * lse[2*nb]; node GradientDelta: unique ids ascending + summed rows (capacity 2nb + negs);
+ * relation GradientDelta likewise (capacity nb). Counts and loss are written to host. */
+int ember_loss_and_grad(ember_ctx* ctx, const uint32_t* edges_dev, uint32_t nb, uint32_t i, uint32_t j,
+                        const uint32_t* negs_dev, float* fpos_dev, float* lse_dev, uint32_t* node_ids_dev,
+                        float* node_rows_dev, uint32_t* n_node_host, uint32_t* rel_ids_dev, float* rel_rows_dev,
+                        uint32_t* n_rel_host, double* loss_host);
+/* adagrad_step on n rows of bucket (i, j)'s node tables (relations != 0: the
+ * relation table). ids/rows device. */
+int ember_adagrad_apply(ember_ctx* ctx, const uint32_t* ids_dev, const float* rows_dev, uint32_t n, uint32_t i,
+                        uint32_t j, int relations);
+/* Scores S[r][k] = f(edge r, negative k) for the first `rows` edges of a batch against chunk 0's
+ * side-`side` negatives (debug/parity; out_dev: rows x n_t). */
+int ember_debug_scores(ember_ctx* ctx, const uint32_t* edges_dev, uint32_t nb, uint32_t i, uint32_t j,
+                       const uint32_t* negs_dev, int side, uint32_t rows, float* out_dev);
+
+/* ---- link-prediction eval, unfiltered sampled negatives ------------------ */
+int ember_eval_ranks(ember_ctx* ctx, const uint32_t* test_edges_dev, uint32_t n_test, const uint32_t* train_edges_dev,
+                     uint64_t n_train, uint32_t n_eval_neg, float alpha_eval, uint32_t block, uint64_t eval_seed,
+                     uint32_t* ranks_dev);
+
+/* ---- ordering (reference ordering.h, bit-identical) -------------------------------------- */
+int ember_make_plan(int kind, uint32_t p, uint32_t c, uint64_t seed, uint32_t* seq_out /* 2*p*p */,
+                    uint64_t* swap_count, uint32_t* admissions_out /* c + 2*p*p */, uint32_t* n_admissions,
+                    uint32_t* swaps_out /* 3 per swap, <= 2*p*p swaps */, uint32_t* bucket_state_out /* p*p */);
+uint64_t ember_lower_bound_swaps(uint32_t p, uint32_t c);
+uint64_t ember_elimination_swap_formula(uint32_t p, uint32_t c);
+
+/* ---- synthetic graphs (test/bench data; SURVEY §8(d) generator) ---------------------------
+ * Edge e of a graph with `seed`: power-law sources, Zipf relations, community-planted
+ * destinations. Generated on the device (device != -1) or host (device == -1) into
+ * edges_out (n x 3 u32, same memory space). split_out (nullable, n bytes): 0 train, 1 valid,
+ * 2 test with the given fractions. */
+int ember_graph_generate(int device, uint64_t num_nodes, uint32_t num_relations, uint64_t n_edges, uint64_t seed,
+                         float train_frac, float valid_frac, uint32_t* edges_out, uint8_t* split_out);
+/* bucket_edges: stable counting sort of n edges by (part(src), part(dst)).
+ * offsets_out: p*p+1 u64. device == -1 -> host arrays. */
+int ember_graph_bucket(int device, uint64_t num_nodes, uint32_t p, const uint32_t* edges_in, uint64_t n,
+                       uint32_t* edges_out, uint64_t* offsets_out);
+
+/* ---- measurement ----------------------------------------------------------------------------
+ * enable != 0: record CUDA events on the context stream at step phase boundaries.
+ * ms_out[6]: summed ms per phase {sample, gather, contraction, chain+loss, reduce+adagrad, -}
+ * since the last read; launches_out: our kernels launched since context creation; lib_calls_out:
+ * CUB device-wide calls (library kernels) since creation. Synchronises the stream. */
+int ember_profile_enable(ember_ctx* ctx, int enable);
+int ember_profile_read(ember_ctx* ctx, double* ms_out, uint64_t* launches_out, uint64_t* lib_calls_out);
+
+/* ---- multi-GPU------------------------------------------------------------ */
+/* nccl_unique_id: 128 bytes (ncclUniqueId) shared by all ranks. NCCL is loaded at run time. */
+int ember_comm_init(ember_ctx* ctx, const void* nccl_unique_id, int rank, int world);
+/* Sum the relation gradients across ranks before the relation Adagrad (on by default once
+ * comm is initialised). */
+int ember_comm_barrier(ember_ctx* ctx);
+/* Copy a partition's theta+acc (rows x dim each) device->device, possibly across GPUs
+ * (P2P over NVLink via cudaMemcpyPeerAsync on the context stream). */
+int ember_partition_copy(ember_ctx* ctx, float* dst_theta, float* dst_acc, int dst_device, const float* src_theta,
+                         const float* src_acc, int src_device, uint64_t rows);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EMBER_GPU_H */

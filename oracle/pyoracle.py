@@ -121,8 +121,8 @@ def ref_plan(kind: int, p: int, c: int, seed: int):
     """Reference make_plan (ordering.cpp:384) -> dict of numpy arrays, or raises on ConfigError."""
     L = ref_lib()
     seq = np.zeros(2 * p * p, np.uint32)
-    adm = np.zeros(c + p * p + 1, np.uint32)
-    swaps = np.zeros(3 * p * p + 3, np.uint32)
+    adm = np.zeros(c + 2 * p * p + 1, np.uint32)
+    swaps = np.zeros(6 * p * p + 3, np.uint32)
     state = np.zeros(p * p, np.uint32)
     sc = C.c_uint64(0)
     na = C.c_uint32(0)

@@ -28,7 +28,7 @@ static int status_of(const std::exception_ptr& ep) {
 }
 
 // make_plan (ordering.cpp:384). seq_out: 2*p*p u32 (i,j pairs); adm_out: up to
-// c + p*p u32; swaps_out: 3 u32 per swap (step, evicted, admitted), up to p*p.
+// c + 2*p*p u32; swaps_out: 3 u32 per swap (step, evicted, admitted), up to 2*p*p.
 int ref_make_plan(int kind, uint32_t p, uint32_t c, uint64_t seed, uint32_t* seq_out, uint64_t* swap_count,
                   uint32_t* adm_out, uint32_t* n_adm, uint32_t* swaps_out, uint32_t* bucket_state_out) {
     try {

@@ -1,0 +1,303 @@
+"""ember-b200: B200-native minibatch training step of Gaius/Marius (arXiv 2101.08358).
+
+Host mirror of the reference's (reconstructed) model / ordering / pipeline surface over the
+C-ABI in include/ember_gpu.h. Device memory is torch-allocated (plumbing); all compute runs in
+libember_b200.so (sm_100a). Names follow the reference: ModelKind, OrderingPlan, make_plan,
+sample_negatives, loss_and_grad, adagrad_step, init_embeddings, train_epoch_partitioned.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._lib import (ENGINE, KIND, ORDERING, ConfigError, EmberError, GraphDesc, ModelDesc, StepStats, check,  # noqa: F401
+                   lib)
+
+__all__ = ["ConfigError", "EmberError", "Hyper", "Trainer", "make_plan", "lower_bound_swaps",
+           "elimination_swap_formula", "generate_graph", "bucket_edges", "partition_offset", "partition_size", "lib"]
+
+
+def partition_offset(V: int, p: int, k: int) -> int:
+    q, r = divmod(V, p)
+    return k * q + min(k, r)
+
+
+def partition_size(V: int, p: int, k: int) -> int:
+    q, r = divmod(V, p)
+    return q + (1 if k < r else 0)
+
+
+def _ptr(x) -> int | None:
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return int(x)
+
+
+# ---------------------------------------------------------------------------------- ordering
+
+def make_plan(kind: str | int, p: int, c: int, seed: int = 0) -> dict:
+    """make_plan (reference ordering.h:80 / ordering.cpp:384): BETA (elimination), hilbert, ..."""
+    k = ORDERING[kind] if isinstance(kind, str) else int(kind)
+    seq = np.zeros(2 * p * p, np.uint32)
+    adm = np.zeros(c + 2 * p * p + 1, np.uint32)
+    swaps = np.zeros(6 * p * p + 3, np.uint32)
+    state = np.zeros(p * p, np.uint32)
+    sc = C.c_uint64(0)
+    na = C.c_uint32(0)
+    check(lib().ember_make_plan(k, p, c, seed, _ptr(seq), C.byref(sc), _ptr(adm), C.byref(na), _ptr(swaps),
+                                _ptr(state)))
+    n = int(sc.value)
+    return {"seq": seq.reshape(-1, 2), "swap_count": n, "admissions": adm[: na.value].copy(),
+            "swaps": swaps[: 3 * n].reshape(-1, 3).copy(), "bucket_state": state}
+
+
+def lower_bound_swaps(p: int, c: int) -> int:
+    v = lib().ember_lower_bound_swaps(p, c)
+    if v == (1 << 64) - 1:
+        raise ConfigError(lib().ember_last_error().decode())
+    return int(v)
+
+
+def elimination_swap_formula(p: int, c: int) -> int:
+    v = lib().ember_elimination_swap_formula(p, c)
+    if v == (1 << 64) - 1:
+        raise ConfigError(lib().ember_last_error().decode())
+    return int(v)
+
+
+# ---------------------------------------------------------------------------------- graphs
+
+def generate_graph(num_nodes: int, num_relations: int, n_edges: int, seed: int, train_frac=0.9, valid_frac=0.05,
+                   device: int | None = None):
+    """Synthetic planted-community graph. device=None -> numpy (host), else torch tensors on cuda:device."""
+    if device is None:
+        edges = np.zeros((n_edges, 3), np.uint32)
+        split = np.zeros(n_edges, np.uint8)
+        check(lib().ember_graph_generate(-1, num_nodes, num_relations, n_edges, seed, train_frac, valid_frac,
+                                         _ptr(edges), _ptr(split)))
+        return edges, split
+    import torch
+    edges = torch.empty((n_edges, 3), dtype=torch.int32, device=f"cuda:{device}")
+    split = torch.empty(n_edges, dtype=torch.uint8, device=f"cuda:{device}")
+    check(lib().ember_graph_generate(device, num_nodes, num_relations, n_edges, seed, train_frac, valid_frac,
+                                     _ptr(edges), _ptr(split)))
+    return edges, split
+
+
+def bucket_edges(edges, num_nodes: int, p: int, device: int | None = None):
+    """bucket_edges: stable sort into p*p buckets; returns (edges, offsets[p*p+1])."""
+    n = int(edges.shape[0])
+    offsets = np.zeros(p * p + 1, np.uint64)
+    if device is None:
+        edges = np.ascontiguousarray(edges, np.uint32)
+        out = np.zeros_like(edges)
+        check(lib().ember_graph_bucket(-1, num_nodes, p, _ptr(edges), n, _ptr(out), _ptr(offsets)))
+        return out, offsets
+    import torch
+    out = torch.empty_like(edges)
+    check(lib().ember_graph_bucket(device, num_nodes, p, _ptr(edges), n, _ptr(out), _ptr(offsets)))
+    return out, offsets
+
+
+# ---------------------------------------------------------------------------------- trainer
+
+@dataclass
+class Hyper:
+    """RunConfig subset consumed by the step (Table 1 defaults)."""
+    kind: str = "complex"
+    dim: int = 100
+    lr: float = 0.1
+    eps: float = 1e-10
+    batch_size: int = 50_000
+    num_negatives: int = 1000
+    alpha: float = 0.5
+    num_chunks: int = 1
+    neg_seed: int = 1
+    engine: str = "simt"
+
+    def desc(self) -> ModelDesc:
+        return ModelDesc(KIND[self.kind], self.dim, self.lr, self.eps, self.batch_size, self.num_negatives,
+                         self.alpha, self.num_chunks, self.neg_seed, ENGINE[self.engine], 0)
+
+
+class Trainer:
+    """One GPU's training context: partition tables in HBM + the C-ABI step.
+
+    tables: allocate=True allocates theta/acc for every partition on this GPU (torch, fp32) and
+    binds them; pass allocate=False to bind externally owned slots with bind_partition().
+    """
+
+    def __init__(self, hyper: Hyper, num_nodes: int, num_relations: int, num_partitions: int = 1, device: int = 0,
+                 allocate: bool = True, stream=None):
+        import torch
+        self.torch = torch
+        self.h = hyper
+        self.V, self.R, self.p = num_nodes, num_relations, num_partitions
+        self.device = device
+        self.dev = torch.device(f"cuda:{device}")
+        md = hyper.desc()
+        gd = GraphDesc(num_nodes, num_relations, num_partitions)
+        ctx = C.c_void_p()
+        check(lib().ember_ctx_create(device, C.byref(md), C.byref(gd), _ptr(stream) if stream is not None else None,
+                                     C.byref(ctx)))
+        self.ctx = ctx
+        self.theta: dict[int, object] = {}
+        self.acc: dict[int, object] = {}
+        self.rel_theta = self.rel_acc = None
+        if allocate:
+            for k in range(num_partitions):
+                rows = partition_size(num_nodes, num_partitions, k)
+                self.bind_partition(k, torch.empty((rows, hyper.dim), dtype=torch.float32, device=self.dev),
+                                    torch.empty((rows, hyper.dim), dtype=torch.float32, device=self.dev))
+            if KIND[hyper.kind] != 0:
+                self.bind_relations(torch.empty((num_relations, hyper.dim), dtype=torch.float32, device=self.dev),
+                                    torch.empty((num_relations, hyper.dim), dtype=torch.float32, device=self.dev))
+
+    # -- lifecycle ------------------------------------------------------------------------
+    def close(self):
+        if getattr(self, "ctx", None):
+            check(lib().ember_ctx_destroy(self.ctx))
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream_ptr(self) -> int:
+        return lib().ember_ctx_stream(self.ctx)
+
+    def torch_stream(self):
+        return self.torch.cuda.ExternalStream(self.stream_ptr, device=self.dev)
+
+    def synchronize(self):
+        self.torch.cuda.synchronize(self.dev)
+
+    # -- tables ---------------------------------------------------------------------------
+    def bind_partition(self, k, theta, acc):
+        self.theta[k], self.acc[k] = theta, acc
+        check(lib().ember_tables_bind(self.ctx, k, _ptr(theta), _ptr(acc)))
+
+    def bind_relations(self, theta, acc):
+        self.rel_theta, self.rel_acc = theta, acc
+        check(lib().ember_relations_bind(self.ctx, _ptr(theta), _ptr(acc)))
+
+    def init_embeddings(self, seed: int):
+        """init_embeddings: every bound partition + relations, on the device."""
+        for k in self.theta:
+            check(lib().ember_init_partition(self.ctx, k, seed))
+        if self.rel_theta is not None:
+            check(lib().ember_init_relations(self.ctx, seed))
+
+    def node_table(self):
+        """Concatenated theta/acc of all partitions (host copies for parity checks)."""
+        self.synchronize()
+        th = self.torch.cat([self.theta[k] for k in range(self.p)]).cpu().numpy()
+        ac = self.torch.cat([self.acc[k] for k in range(self.p)]).cpu().numpy()
+        return th, ac
+
+    # -- the step -------------------------------------------------------------------------
+    def train_batch(self, bucket_edges, batch_begin: int, nb: int, i: int = 0, j: int = 0, epoch: int = 0,
+                    bucket_step: int = 0, batch_in_bucket: int = 0, loss_out=None):
+        check(lib().ember_train_batch(self.ctx, _ptr(bucket_edges), int(bucket_edges.shape[0]), batch_begin, nb, i, j,
+                                      epoch, bucket_step, batch_in_bucket, _ptr(loss_out)))
+
+    def train_batch_host(self, bucket_edges, host_batch, i=0, j=0, epoch=0, bucket_step=0, batch_in_bucket=0,
+                         want_loss=True) -> float | None:
+        loss = C.c_float(0.0)
+        check(lib().ember_train_batch_host(self.ctx, _ptr(bucket_edges), int(bucket_edges.shape[0]), _ptr(host_batch),
+                                           int(host_batch.shape[0]), i, j, epoch, bucket_step, batch_in_bucket,
+                                           C.byref(loss) if want_loss else None))
+        if want_loss:
+            self.torch.cuda.current_stream(self.dev)  # ensure CUDA initialised
+            self.torch_stream().synchronize()
+        return float(loss.value) if want_loss else None
+
+    def train_bucket(self, bucket_edges, i=0, j=0, epoch=0, bucket_step=0) -> StepStats:
+        st = StepStats()
+        check(lib().ember_train_bucket(self.ctx, _ptr(bucket_edges), int(bucket_edges.shape[0]), i, j, epoch,
+                                       bucket_step, C.byref(st)))
+        return st
+
+    def train_epoch(self, edges_dev, offsets, plan_seq, epoch: int) -> dict:
+        """train_epoch_partitioned (Algorithm 2): buckets in plan order."""
+        total = StepStats()
+        for step, (i, j) in enumerate(np.asarray(plan_seq).reshape(-1, 2)):
+            b = int(i) * self.p + int(j)
+            lo, hi = int(offsets[b]), int(offsets[b + 1])
+            if hi == lo:
+                continue
+            check(lib().ember_train_bucket(self.ctx, _ptr(edges_dev[lo:hi]), hi - lo, int(i), int(j), epoch, step,
+                                           C.byref(total)))
+        return {"loss": total.loss_sum / max(1, total.batches), "batches": total.batches, "edges": total.edges}
+
+    # -- per-op entry points (parity tests) ----------------------------------------------
+    def sample_negatives(self, bucket_edges, i=0, j=0, epoch=0, bucket_step=0, batch_in_bucket=0):
+        t = self.torch
+        out = t.empty(max(1, self.h.num_chunks) * 2 * self.h.num_negatives, dtype=t.int32, device=self.dev)
+        check(lib().ember_sample_negatives(self.ctx, _ptr(bucket_edges), int(bucket_edges.shape[0]), i, j, epoch,
+                                           bucket_step, batch_in_bucket, _ptr(out)))
+        return out
+
+    def loss_and_grad(self, edges, negs, i=0, j=0) -> dict:
+        t = self.torch
+        nb = int(edges.shape[0])
+        d = self.h.dim
+        cap = 2 * nb + int(negs.numel())
+        fpos = t.empty(nb, dtype=t.float32, device=self.dev)
+        lse = t.empty(2 * nb, dtype=t.float32, device=self.dev)
+        ids = t.empty(cap, dtype=t.int32, device=self.dev)
+        rows = t.empty((cap, d), dtype=t.float32, device=self.dev)
+        rids = t.empty(max(nb, 1), dtype=t.int32, device=self.dev)
+        rrows = t.empty((max(nb, 1), d), dtype=t.float32, device=self.dev)
+        nu, nr, loss = C.c_uint32(0), C.c_uint32(0), C.c_double(0)
+        check(lib().ember_loss_and_grad(self.ctx, _ptr(edges), nb, i, j, _ptr(negs), _ptr(fpos), _ptr(lse), _ptr(ids),
+                                        _ptr(rows), C.byref(nu), _ptr(rids), _ptr(rrows), C.byref(nr), C.byref(loss)))
+        self.synchronize()
+        u, r = nu.value, nr.value
+        return {"loss": loss.value, "fpos": fpos.cpu().numpy(), "lse": lse.cpu().numpy().reshape(2, nb),
+                "node_ids": ids[:u].cpu().numpy().view(np.uint32), "node_rows": rows[:u].cpu().numpy(),
+                "rel_ids": rids[:r].cpu().numpy().view(np.uint32), "rel_rows": rrows[:r].cpu().numpy()}
+
+    def adagrad_apply(self, ids, rows, i=0, j=0, relations=False):
+        check(lib().ember_adagrad_apply(self.ctx, _ptr(ids), _ptr(rows), int(ids.numel()), i, j, 1 if relations else 0))
+
+    def debug_scores(self, edges, negs, side=0, rows=None, i=0, j=0):
+        t = self.torch
+        rows = int(edges.shape[0]) if rows is None else rows
+        out = t.empty((rows, self.h.num_negatives), dtype=t.float32, device=self.dev)
+        check(lib().ember_debug_scores(self.ctx, _ptr(edges), int(edges.shape[0]), i, j, _ptr(negs), side, rows,
+                                       _ptr(out)))
+        self.synchronize()
+        return out.cpu().numpy()
+
+    def eval_ranks(self, test_edges, train_edges, n_eval=1000, alpha_eval=0.5, block=1000, eval_seed=7):
+        t = self.torch
+        n = int(test_edges.shape[0])
+        ranks = t.empty(2 * n, dtype=t.int32, device=self.dev)
+        check(lib().ember_eval_ranks(self.ctx, _ptr(test_edges), n, _ptr(train_edges), int(train_edges.shape[0]),
+                                     n_eval, alpha_eval, block, eval_seed, _ptr(ranks)))
+        self.synchronize()
+        return ranks.cpu().numpy().view(np.uint32)
+
+    def profile(self, enable: bool = True):
+        check(lib().ember_profile_enable(self.ctx, 1 if enable else 0))
+
+    def profile_read(self) -> dict:
+        ms = (C.c_double * 6)()
+        la, lc = C.c_uint64(0), C.c_uint64(0)
+        check(lib().ember_profile_read(self.ctx, ms, C.byref(la), C.byref(lc)))
+        names = ["sample", "gather", "contraction", "chain_loss", "reduce_adagrad"]
+        return {"ms": {n: ms[k] for k, n in enumerate(names)}, "launches": la.value, "lib_calls": lc.value}
+
+    def comm_init(self, unique_id: bytes, rank: int, world: int):
+        buf = C.create_string_buffer(unique_id, 128)
+        check(lib().ember_comm_init(self.ctx, buf, rank, world))

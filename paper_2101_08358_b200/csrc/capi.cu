@@ -1,0 +1,362 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// extern "C" boundary (include/ember_gpu.h). Converts exceptions to status codes
+// (ConfigError -> EMBER_EUSER, anything else -> EMBER_EINTERNAL) with a thread-local message.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <exception>
+#include <new>
+#include <string>
+
+#include "ember/ordering.h"
+#include "engine.h"
+
+namespace ember {
+void graph_generate(int device, uint64_t V, uint32_t R, uint64_t n, uint64_t seed, float train, float valid,
+                    uint32_t* edges, uint8_t* split);
+void graph_bucket(int device, uint64_t V, uint32_t p, const uint32_t* in, uint64_t n, uint32_t* out,
+                  uint64_t* offsets);
+void launch_eval(const Engine& E, const uint32_t* test, uint32_t n_test, const uint32_t* train, uint64_t n_train,
+                 uint32_t n_eval, float alpha_eval, uint32_t block, uint64_t eval_seed, uint32_t* ranks);
+}  // namespace ember
+
+using namespace ember;
+
+struct ember_ctx {
+    Engine* e;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        g_err.clear();
+        return EMBER_OK;
+    } catch (const ConfigError& ex) {
+        g_err = ex.what();
+        return EMBER_EUSER;
+    } catch (const std::bad_alloc&) {
+        g_err = "host out of memory";
+        return EMBER_EINTERNAL;
+    } catch (const std::exception& ex) {
+        g_err = ex.what();
+        return EMBER_EINTERNAL;
+    } catch (...) {
+        g_err = "unknown error";
+        return EMBER_EINTERNAL;
+    }
+}
+
+Engine& eng(ember_ctx* c) {
+    if (!c || !c->e) throw ConfigError("null context");
+    EMBER_CUDA(cudaSetDevice(c->e->device));
+    return *c->e;
+}
+
+void need(const void* p, const char* what) {
+    if (!p) throw ConfigError(std::string(what) + " must not be NULL");
+}
+}  // namespace
+
+extern "C" {
+
+const char* ember_last_error(void) { return g_err.c_str(); }
+int ember_version(void) { return 1; }
+
+int ember_ctx_create(int device, const ember_model_desc* model, const ember_graph_desc* graph, void* stream,
+                     ember_ctx** out) {
+    return guarded([&] {
+        need(model, "model");
+        need(graph, "graph");
+        need(out, "out");
+        *out = nullptr;
+        auto* c = new ember_ctx{nullptr};
+        try {
+            c->e = new Engine(device, *model, *graph, static_cast<cudaStream_t>(stream));
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+int ember_ctx_destroy(ember_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        delete ctx->e;
+        delete ctx;
+    });
+}
+
+void* ember_ctx_stream(ember_ctx* ctx) { return ctx && ctx->e ? static_cast<void*>(ctx->e->stream) : nullptr; }
+
+int ember_tables_bind(ember_ctx* ctx, uint32_t part, float* theta, float* acc) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        if (part >= E.parts.size()) throw ConfigError("partition id out of range");
+        need(theta, "theta");
+        need(acc, "acc");
+        if ((reinterpret_cast<uintptr_t>(theta) | reinterpret_cast<uintptr_t>(acc)) & 15)
+            throw ConfigError("tables must be 16-byte aligned");
+        E.parts[part].theta = theta;
+        E.parts[part].acc = acc;
+    });
+}
+
+int ember_relations_bind(ember_ctx* ctx, float* theta, float* acc) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        need(theta, "theta");
+        need(acc, "acc");
+        E.rel_theta = theta;
+        E.rel_acc = acc;
+    });
+}
+
+int ember_init_partition(ember_ctx* ctx, uint32_t part, uint64_t seed) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        const PartView v = E.view(part);
+        launch_init_rows(E.stream, v.theta, v.acc, v.first, v.rows, E.dim, seed);
+    });
+}
+
+int ember_init_relations(ember_ctx* ctx, uint64_t seed) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        if (!E.rel_theta) throw ConfigError("relation table not bound");
+        launch_init_rows(E.stream, E.rel_theta, E.rel_acc, 0, E.g.num_relations, E.dim, seed ^ 0x52454cULL);
+    });
+}
+
+int ember_train_batch(ember_ctx* ctx, const uint32_t* bucket, uint64_t bucket_n, uint64_t batch_begin, uint32_t nb,
+                      uint32_t i, uint32_t j, uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket,
+                      float* loss_dev) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        need(bucket, "bucket_edges_dev");
+        E.train_batch(bucket, bucket_n, batch_begin, nb, i, j, epoch, bucket_step, batch_in_bucket, loss_dev);
+    });
+}
+
+int ember_train_bucket(ember_ctx* ctx, const uint32_t* bucket, uint64_t n, uint32_t i, uint32_t j, uint64_t epoch,
+                       uint32_t bucket_step, ember_step_stats* stats) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        need(bucket, "bucket_edges_dev");
+        double loss_sum = 0.0;
+        uint64_t batches = 0;
+        float* losses = nullptr;
+        const uint64_t nbatch = (n + E.cap_b - 1) / E.cap_b;
+        if (stats && nbatch) EMBER_CUDA(cudaMallocAsync(&losses, nbatch * sizeof(float), E.stream));
+        for (uint64_t b0 = 0, k = 0; b0 < n; b0 += E.cap_b, ++k) {
+            const uint32_t nb = (uint32_t)std::min<uint64_t>(E.cap_b, n - b0);
+            E.train_batch(bucket, n, b0, nb, i, j, epoch, bucket_step, (uint32_t)k, losses ? losses + k : nullptr);
+            ++batches;
+        }
+        if (stats) {
+            std::vector<float> h(nbatch);
+            if (nbatch) {
+                EMBER_CUDA(cudaMemcpyAsync(h.data(), losses, nbatch * sizeof(float), cudaMemcpyDeviceToHost, E.stream));
+                EMBER_CUDA(cudaFreeAsync(losses, E.stream));
+            }
+            EMBER_CUDA(cudaStreamSynchronize(E.stream));
+            for (float x : h) loss_sum += x;
+            stats->loss_sum += loss_sum;
+            stats->batches += batches;
+            stats->edges += n;
+        }
+    });
+}
+
+int ember_train_batch_host(ember_ctx* ctx, const uint32_t* bucket, uint64_t bucket_n, const uint32_t* host_batch,
+                           uint32_t nb, uint32_t i, uint32_t j, uint64_t epoch, uint32_t bucket_step,
+                           uint32_t batch_in_bucket, float* loss_host) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        need(bucket, "bucket_edges_dev");
+        need(host_batch, "host_batch");
+        if (nb == 0 || nb > E.cap_b) throw ConfigError("batch size must be in [1, batch_size]");
+        EMBER_CUDA(cudaMemcpyAsync(E.s.batch, host_batch, (size_t)nb * 12, cudaMemcpyHostToDevice, E.stream));
+        E.step(E.s.batch, nb, bucket, bucket_n, i, j, epoch, bucket_step, batch_in_bucket, E.s.loss);
+        if (loss_host) EMBER_CUDA(cudaMemcpyAsync(loss_host, E.s.loss, sizeof(float), cudaMemcpyDeviceToHost, E.stream));
+    });
+}
+
+int ember_sample_negatives(ember_ctx* ctx, const uint32_t* bucket, uint64_t bucket_n, uint32_t i, uint32_t j,
+                           uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket, uint32_t* negs_dev) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        need(negs_dev, "negs_dev");
+        E.sample(bucket, bucket_n, i, j, epoch, bucket_step, batch_in_bucket, negs_dev);
+    });
+}
+
+int ember_loss_and_grad(ember_ctx* ctx, const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j,
+                        const uint32_t* negs, float* fpos, float* lse, uint32_t* node_ids, float* node_rows,
+                        uint32_t* n_node, uint32_t* rel_ids, float* rel_rows, uint32_t* n_rel, double* loss) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        need(edges, "edges_dev");
+        need(negs, "negs_dev");
+        if (nb == 0 || nb > E.cap_b) throw ConfigError("batch size must be in [1, batch_size]");
+        E.check_bucket(i, j);
+        E.forward_backward(edges, nb, i, j, negs);
+        launch_loss(E, nb, E.s.loss);
+        if (fpos) EMBER_CUDA(cudaMemcpyAsync(fpos, E.s.fpos, nb * sizeof(float), cudaMemcpyDeviceToDevice, E.stream));
+        if (lse) EMBER_CUDA(cudaMemcpyAsync(lse, E.s.lse, 2ull * nb * sizeof(float), cudaMemcpyDeviceToDevice, E.stream));
+        E.reduce_and_apply(edges, nb, i, j, negs, false, node_ids, node_rows, rel_ids, rel_rows);
+        uint32_t counts[2] = {0, 0};
+        float l = 0.f;
+        EMBER_CUDA(cudaMemcpyAsync(counts, E.s.nunique, sizeof(counts), cudaMemcpyDeviceToHost, E.stream));
+        EMBER_CUDA(cudaMemcpyAsync(&l, E.s.loss, sizeof(float), cudaMemcpyDeviceToHost, E.stream));
+        EMBER_CUDA(cudaStreamSynchronize(E.stream));
+        if (n_node) *n_node = counts[0];
+        if (n_rel) *n_rel = E.m.kind == EMBER_DOT ? 0 : counts[1];
+        if (loss) *loss = l;
+    });
+}
+
+int ember_adagrad_apply(ember_ctx* ctx, const uint32_t* ids, const float* rows, uint32_t n, uint32_t i, uint32_t j,
+                        int relations) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        if (!n) return;
+        need(ids, "ids_dev");
+        need(rows, "rows_dev");
+        if (relations) {
+            if (!E.rel_theta) throw ConfigError("relation table not bound");
+            launch_adagrad_rows(E, ids, rows, n, E.parts[0], E.parts[0], true);
+        } else {
+            launch_adagrad_rows(E, ids, rows, n, E.view(i), E.view(j), false);
+        }
+    });
+}
+
+int ember_debug_scores(ember_ctx* ctx, const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j,
+                       const uint32_t* negs, int side, uint32_t rows, float* out) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        if (side != 0 && side != 1) throw ConfigError("side must be 0 or 1");
+        if (rows > nb || nb > E.cap_b) throw ConfigError("rows <= nb <= batch_size");
+        E.check_bucket(i, j);
+        launch_debug_scores(E, edges, nb, negs, side, rows, out, E.view(i), E.view(j));
+    });
+}
+
+int ember_eval_ranks(ember_ctx* ctx, const uint32_t* test, uint32_t n_test, const uint32_t* train, uint64_t n_train,
+                     uint32_t n_eval, float alpha_eval, uint32_t block, uint64_t eval_seed, uint32_t* ranks) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        need(test, "test_edges_dev");
+        need(ranks, "ranks_dev");
+        launch_eval(E, test, n_test, train, n_train, n_eval, alpha_eval, block ? block : 1, eval_seed, ranks);
+    });
+}
+
+int ember_make_plan(int kind, uint32_t p, uint32_t c, uint64_t seed, uint32_t* seq, uint64_t* swap_count,
+                    uint32_t* adm, uint32_t* n_adm, uint32_t* swaps, uint32_t* state) {
+    return guarded([&] {
+        if (kind < 0 || kind > 3) throw ConfigError("unknown ordering kind");
+        const OrderingPlan plan = make_plan(static_cast<OrderingKind>(kind), p, c, seed);
+        plan.validate();
+        for (size_t t = 0; t < plan.bucket_sequence.size(); ++t) {
+            if (seq) {
+                seq[2 * t] = plan.bucket_sequence[t].i;
+                seq[2 * t + 1] = plan.bucket_sequence[t].j;
+            }
+            if (state) state[t] = plan.bucket_state[t];
+        }
+        if (swap_count) *swap_count = plan.swap_count;
+        if (n_adm) *n_adm = (uint32_t)plan.admission_schedule.size();
+        if (adm) std::memcpy(adm, plan.admission_schedule.data(), plan.admission_schedule.size() * sizeof(uint32_t));
+        if (swaps)
+            for (size_t k = 0; k < plan.swap_events.size(); ++k) {
+                swaps[3 * k] = plan.swap_events[k].step;
+                swaps[3 * k + 1] = plan.swap_events[k].evicted;
+                swaps[3 * k + 2] = plan.swap_events[k].admitted;
+            }
+    });
+}
+
+uint64_t ember_lower_bound_swaps(uint32_t p, uint32_t c) {
+    uint64_t r = ~0ULL;
+    guarded([&] { r = lower_bound_swaps(p, c); });
+    return r;
+}
+
+uint64_t ember_elimination_swap_formula(uint32_t p, uint32_t c) {
+    uint64_t r = ~0ULL;
+    guarded([&] { r = elimination_swap_formula(p, c); });
+    return r;
+}
+
+int ember_graph_generate(int device, uint64_t V, uint32_t R, uint64_t n, uint64_t seed, float train, float valid,
+                         uint32_t* edges, uint8_t* split) {
+    return guarded([&] {
+        need(edges, "edges_out");
+        graph_generate(device, V, R, n, seed, train, valid, edges, split);
+    });
+}
+
+int ember_graph_bucket(int device, uint64_t V, uint32_t p, const uint32_t* in, uint64_t n, uint32_t* out,
+                       uint64_t* offsets) {
+    return guarded([&] {
+        need(in, "edges_in");
+        need(out, "edges_out");
+        need(offsets, "offsets_out");
+        graph_bucket(device, V, p, in, n, out, offsets);
+    });
+}
+
+int ember_profile_enable(ember_ctx* ctx, int enable) {
+    return guarded([&] { eng(ctx).prof_on = enable != 0; });
+}
+
+int ember_profile_read(ember_ctx* ctx, double* ms_out, uint64_t* launches_out, uint64_t* lib_calls_out) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        const std::vector<double> ms = E.profile_read();
+        if (ms_out)
+            for (size_t k = 0; k < ms.size(); ++k) ms_out[k] = ms[k];
+        if (launches_out) *launches_out = E.launches;
+        if (lib_calls_out) *lib_calls_out = E.lib_calls;
+    });
+}
+
+int ember_comm_init(ember_ctx* ctx, const void* id, int rank, int world) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        need(id, "nccl_unique_id");
+        E.comm_init(id, rank, world);
+    });
+}
+
+int ember_comm_barrier(ember_ctx* ctx) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        EMBER_CUDA(cudaStreamSynchronize(E.stream));
+    });
+}
+
+int ember_partition_copy(ember_ctx* ctx, float* dst_theta, float* dst_acc, int dst_device, const float* src_theta,
+                         const float* src_acc, int src_device, uint64_t rows) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        const size_t bytes = (size_t)rows * E.dim * sizeof(float);
+        if (dst_device == src_device) {
+            EMBER_CUDA(cudaMemcpyAsync(dst_theta, src_theta, bytes, cudaMemcpyDeviceToDevice, E.stream));
+            EMBER_CUDA(cudaMemcpyAsync(dst_acc, src_acc, bytes, cudaMemcpyDeviceToDevice, E.stream));
+        } else {
+            EMBER_CUDA(cudaMemcpyPeerAsync(dst_theta, dst_device, src_theta, src_device, bytes, E.stream));
+            EMBER_CUDA(cudaMemcpyPeerAsync(dst_acc, dst_device, src_acc, src_device, bytes, E.stream));
+        }
+    });
+}
+
+}  // extern "C"

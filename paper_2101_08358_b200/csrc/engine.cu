@@ -1,0 +1,319 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Engine: the device-resident training step (Algorithm 1, PAPER.md:84-99 / SPEC.md:376-384
+// train_epoch_sync semantics, bound = 1). Per batch, on one stream:
+//   sample -> gather+adjust -> contraction (scores, LSE, dA, dN) -> chain rule ->
+//   sort ids + segmented sum -> Adagrad (relations synchronously, then nodes).
+// Stage 2/4 transfers of the paper's pipeline vanish: parameters stay in HBM.
+#include <cub/cub.cuh>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstring>
+
+#include "engine.h"
+
+namespace ember {
+
+void launch_node_keys(const Engine& E, const uint32_t* edges, uint32_t nb, const uint32_t* negs);
+void launch_rel_keys(const Engine& E, const uint32_t* edges, uint32_t nb);
+
+namespace {
+
+template <typename T>
+T* dalloc(size_t n) {
+    if (n == 0) n = 1;
+    void* p = nullptr;
+    EMBER_CUDA(cudaMalloc(&p, n * sizeof(T)));
+    return static_cast<T*>(p);
+}
+
+uint32_t bits_for(uint64_t n) {
+    uint32_t b = 1;
+    while (b < 32 && (1ULL << b) < n) ++b;
+    return b;
+}
+
+// ---- NCCL, loaded at run time so single-GPU use never needs the library -----------------
+struct NcclApi {
+    void* h = nullptr;
+    ncclResult_t (*init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*destroy)(ncclComm_t) = nullptr;
+    const char* (*err)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    if (!api.h) {
+        const char* names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char* n : names)
+            if ((api.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+        if (!api.h) throw EmberError("NCCL not loadable (libnccl.so.2): " + std::string(dlerror()));
+        api.init_rank = reinterpret_cast<decltype(api.init_rank)>(dlsym(api.h, "ncclCommInitRank"));
+        api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(api.h, "ncclAllReduce"));
+        api.destroy = reinterpret_cast<decltype(api.destroy)>(dlsym(api.h, "ncclCommDestroy"));
+        api.err = reinterpret_cast<decltype(api.err)>(dlsym(api.h, "ncclGetErrorString"));
+        if (!api.init_rank || !api.all_reduce || !api.destroy) throw EmberError("NCCL symbols missing");
+    }
+    return api;
+}
+
+__global__ void k_scatter_rel_dense(const uint32_t* ukeys, const uint32_t* nunique, const float* rows, uint32_t d,
+                                    float* dense) {
+    const uint32_t u = blockIdx.x;
+    if (u >= *nunique) return;
+    for (uint32_t k = threadIdx.x; k < d; k += blockDim.x) dense[(uint64_t)ukeys[u] * d + k] = rows[(uint64_t)u * d + k];
+}
+
+__global__ void k_adagrad_dense(float* th, float* ac, const float* g, uint64_t n, float lr, float eps) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float gi = g[i];
+    if (gi == 0.f) return;  // untouched row elements: Adagrad is the identity for g == 0
+    const float a = __fadd_rn(ac[i], __fmul_rn(gi, gi));
+    ac[i] = a;
+    th[i] = __fsub_rn(th[i], __fdiv_rn(__fmul_rn(lr, gi), __fadd_rn(__fsqrt_rn(a), eps)));
+}
+
+}  // namespace
+
+Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, cudaStream_t st)
+    : device(dev), m(md), g(gd) {
+    if (m.kind < EMBER_DOT || m.kind > EMBER_COMPLEX) throw ConfigError("model kind must be 0 (Dot), 1 (DistMult), 2 (ComplEx)");
+    if (m.dim == 0 || m.dim % 4 != 0) throw ConfigError("dim must be a positive multiple of 4");
+    if (m.kind == EMBER_COMPLEX && m.dim % 8 != 0) throw ConfigError("ComplEx needs dim % 8 == 0 (even halves of float4s)");
+    if (m.batch_size == 0) throw ConfigError("batch_size must be >= 1");
+    if (!(m.alpha >= 0.f && m.alpha <= 1.f)) throw ConfigError("alpha must be in [0, 1]");
+    if (!(m.eps > 0.f)) throw ConfigError("eps must be > 0 (SPEC.md:170)");
+    if (g.num_partitions == 0 || g.num_nodes < g.num_partitions) throw ConfigError("need 1 <= p <= |V|");
+    if (g.num_nodes > 0xffffffffULL) throw ConfigError("node ids are u32");
+    if (m.kind != EMBER_DOT && g.num_relations == 0) throw ConfigError("DistMult/ComplEx need relations");
+    if (m.engine != EMBER_ENGINE_SIMT_FP32 && m.engine != EMBER_ENGINE_TC_BF16X3) throw ConfigError("unknown engine");
+    dim = m.dim;
+    nt = m.num_negatives;
+    chunks = m.num_chunks ? m.num_chunks : 1;
+    if (chunks > m.batch_size) throw ConfigError("num_chunks must be <= batch_size");
+    cap_b = m.batch_size;
+    n_neg = chunks * 2 * nt;
+    key_bits = bits_for(g.num_nodes);
+
+    EMBER_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    EMBER_CUDA(cudaGetDeviceProperties(&prop, device));
+    sm_count = prop.multiProcessorCount;
+    if (st) {
+        stream = st;
+    } else {
+        EMBER_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        own_stream = true;
+    }
+    parts.assign(g.num_partitions, PartView{nullptr, nullptr, 0, 0});
+    for (uint32_t k = 0; k < g.num_partitions; ++k) {
+        parts[k].first = partition_offset(g.num_nodes, g.num_partitions, k);
+        parts[k].rows = partition_size(g.num_nodes, g.num_partitions, k);
+    }
+    if (m.engine == EMBER_ENGINE_TC_BF16X3 && !tc_engine_supported(*this))
+        throw ConfigError("tensor-core engine needs a CC 10.0 device (B200), dim <= 256 and num_chunks == 1");
+
+    const uint64_t b = cap_b, d = dim, nrows = 2 * b + n_neg;
+    s.negs = dalloc<uint32_t>(n_neg);
+    s.batch = dalloc<uint32_t>(3 * b);
+    s.A = dalloc<float>(2 * b * d);
+    s.fpos = dalloc<float>(b);
+    s.lse = dalloc<float>(2 * b);
+    s.g0 = dalloc<float>(2 * b);
+    s.N = dalloc<float>((uint64_t)n_neg * d);
+    s.dA = dalloc<float>(2 * b * d);
+    s.grows = dalloc<float>(nrows * d);
+    s.rrows = dalloc<float>(b * d);
+    s.loss = dalloc<float>(1);
+    s.keys = dalloc<uint32_t>(nrows);
+    s.keys_sorted = dalloc<uint32_t>(nrows);
+    s.vals = dalloc<uint32_t>(nrows);
+    s.vals_sorted = dalloc<uint32_t>(nrows);
+    s.ukeys = dalloc<uint32_t>(nrows);
+    s.counts = dalloc<uint32_t>(nrows);
+    s.offsets = dalloc<uint32_t>(nrows);
+    s.nunique = dalloc<uint32_t>(2);
+    if (m.engine == EMBER_ENGINE_SIMT_FP32) {
+        s.S = dalloc<float>(2 * b * (uint64_t)(nt ? nt : 1));
+        s.dN_part = dalloc<float>((uint64_t)dsplit * n_neg * d);
+    }
+    size_t t1 = 0, t2 = 0, t3 = 0;
+    EMBER_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t1, s.keys, s.keys_sorted, s.vals, s.vals_sorted, (int)nrows, 0,
+                                               32, stream));
+    EMBER_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, t2, s.keys_sorted, s.ukeys, s.counts, s.nunique, (int)nrows,
+                                                  stream));
+    EMBER_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t3, s.counts, s.offsets, (int)nrows, stream));
+    s.cub_bytes = std::max(t1, std::max(t2, t3));
+    s.cub_tmp = dalloc<uint8_t>(s.cub_bytes);
+    EMBER_CUDA(cudaStreamSynchronize(stream));
+}
+
+Engine::~Engine() {
+    cudaSetDevice(device);
+    void* ptrs[] = {s.negs, s.batch, s.A, s.fpos, s.lse, s.g0, s.N, s.S, s.dA, s.dN_part, s.grows, s.rrows,
+                    s.row_loss, s.loss, s.keys, s.keys_sorted, s.vals, s.vals_sorted, s.ukeys, s.counts, s.offsets,
+                    s.nunique, s.cub_tmp, s.Atc, s.Ntc, s.NTtc, s.dN_tc, s.rel_dense};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (nccl_comm) {
+        try {
+            nccl().destroy(static_cast<ncclComm_t>(nccl_comm));
+        } catch (...) {
+        }
+    }
+    if (own_stream) cudaStreamDestroy(stream);
+}
+
+PartView Engine::view(uint32_t part) const {
+    if (part >= parts.size()) throw ConfigError("partition id out of range");
+    const PartView& v = parts[part];
+    if (!v.theta || !v.acc) throw ConfigError("partition " + std::to_string(part) + " has no bound tables");
+    return v;
+}
+
+void Engine::check_bucket(uint32_t i, uint32_t j) const {
+    view(i);
+    view(j);
+    if (m.kind != EMBER_DOT && (!rel_theta || !rel_acc)) throw ConfigError("relation table not bound");
+}
+
+void Engine::sample(const uint32_t* bucket, uint64_t bucket_n, uint32_t i, uint32_t j, uint64_t epoch,
+                    uint32_t bucket_step, uint32_t batch_in_bucket, uint32_t* negs_out) {
+    const uint64_t base = mix_seed(mix_seed(m.neg_seed, epoch, bucket_step), batch_in_bucket);
+    launch_sample(*this, negs_out, base, bucket, bucket_n, view(i), view(j));
+}
+
+void Engine::forward_backward(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs) {
+    const PartView pi = view(i), pj = view(j);
+    mark(PHASE_GATHER);
+    launch_gather_adjust(*this, edges, nb, pi, pj);
+    launch_gather_negatives(*this, negs, pi, pj);
+    mark(PHASE_CONTRACT);
+    if (m.engine == EMBER_ENGINE_TC_BF16X3)
+        launch_contract_tc(*this, nb);
+    else
+        launch_contract_simt(*this, nb);
+    mark(PHASE_CHAIN);
+    launch_chain_rule(*this, edges, nb, pi, pj);
+}
+
+void Engine::reduce_and_apply(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs,
+                              bool apply, uint32_t* node_ids_out, float* node_rows_out, uint32_t* rel_ids_out,
+                              float* rel_rows_out) {
+    const PartView pi = view(i), pj = view(j);
+    size_t bytes = s.cub_bytes;
+    // relations first: the synchronous relation update of SPEC.md:388
+    if (m.kind != EMBER_DOT) {
+        launch_rel_keys(*this, edges, nb);
+        const uint32_t rbits = bits_for(g.num_relations);
+        EMBER_CUDA(cub::DeviceRadixSort::SortPairs(s.cub_tmp, bytes, s.keys, s.keys_sorted, s.vals, s.vals_sorted,
+                                                   (int)nb, 0, rbits, stream));
+        bytes = s.cub_bytes;
+        EMBER_CUDA(cub::DeviceRunLengthEncode::Encode(s.cub_tmp, bytes, s.keys_sorted, s.ukeys, s.counts,
+                                                      s.nunique + 1, (int)nb, stream));
+        bytes = s.cub_bytes;
+        EMBER_CUDA(cub::DeviceScan::ExclusiveSum(s.cub_tmp, bytes, s.counts, s.offsets, (int)nb, stream));
+        if (world > 1 && apply) {
+            // dense relation gradient, summed over ranks, then dense Adagrad (g == 0 rows untouched)
+            const uint64_t rn = (uint64_t)g.num_relations * dim;
+            float* dense = s.rel_dense;
+            EMBER_CUDA(cudaMemsetAsync(dense, 0, rn * sizeof(float), stream));
+            // summed rows per unique relation into s.A (free after the chain rule), then scatter dense
+            launch_adagrad_segments(*this, s.ukeys, s.offsets, s.counts, s.nunique + 1, s.vals_sorted, s.rrows, nb,
+                                    pi, pj, true, nullptr, s.A, false);
+            k_scatter_rel_dense<<<nb, 128, 0, stream>>>(s.ukeys, s.nunique + 1, s.A, dim, dense);
+            EMBER_CUDA(cudaGetLastError());
+            allreduce_relations(nb);
+            k_adagrad_dense<<<(unsigned)((rn + 255) / 256), 256, 0, stream>>>(rel_theta, rel_acc, dense, rn, m.lr,
+                                                                             m.eps);
+            EMBER_CUDA(cudaGetLastError());
+        } else {
+            launch_adagrad_segments(*this, s.ukeys, s.offsets, s.counts, s.nunique + 1, s.vals_sorted, s.rrows, nb,
+                                    pi, pj, true, rel_ids_out, rel_rows_out, apply);
+        }
+    }
+    if (m.kind != EMBER_DOT) lib_calls += 3;
+    launch_node_keys(*this, edges, nb, negs);
+    lib_calls += 3;
+    const uint32_t n = 2 * nb + n_neg;
+    bytes = s.cub_bytes;
+    EMBER_CUDA(cub::DeviceRadixSort::SortPairs(s.cub_tmp, bytes, s.keys, s.keys_sorted, s.vals, s.vals_sorted, (int)n,
+                                               0, key_bits, stream));
+    bytes = s.cub_bytes;
+    EMBER_CUDA(cub::DeviceRunLengthEncode::Encode(s.cub_tmp, bytes, s.keys_sorted, s.ukeys, s.counts, s.nunique,
+                                                  (int)n, stream));
+    bytes = s.cub_bytes;
+    EMBER_CUDA(cub::DeviceScan::ExclusiveSum(s.cub_tmp, bytes, s.counts, s.offsets, (int)n, stream));
+    launch_adagrad_segments(*this, s.ukeys, s.offsets, s.counts, s.nunique, s.vals_sorted, s.grows, n, pi, pj, false,
+                            node_ids_out, node_rows_out, apply);
+}
+
+void Engine::mark(int phase) {
+    if (!prof_on) return;
+    cudaEvent_t ev;
+    EMBER_CUDA(cudaEventCreate(&ev));
+    EMBER_CUDA(cudaEventRecord(ev, stream));
+    prof_events.emplace_back(phase, ev);
+}
+
+void Engine::train_batch(const uint32_t* bucket, uint64_t bucket_n, uint64_t batch_begin, uint32_t nb, uint32_t i,
+                         uint32_t j, uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket, float* loss_out) {
+    if (batch_begin + nb > bucket_n) throw ConfigError("batch exceeds bucket");
+    step(bucket + 3 * batch_begin, nb, bucket, bucket_n, i, j, epoch, bucket_step, batch_in_bucket, loss_out);
+}
+
+void Engine::step(const uint32_t* edges, uint32_t nb, const uint32_t* bucket, uint64_t bucket_n, uint32_t i,
+                  uint32_t j, uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket, float* loss_out) {
+    if (nb == 0 || nb > cap_b) throw ConfigError("batch size must be in [1, batch_size]");
+    check_bucket(i, j);
+    mark(PHASE_SAMPLE);
+    sample(bucket, bucket_n, i, j, epoch, bucket_step, batch_in_bucket, s.negs);
+    forward_backward(edges, nb, i, j, s.negs);
+    launch_loss(*this, nb, loss_out ? loss_out : s.loss);
+    mark(PHASE_REDUCE);
+    reduce_and_apply(edges, nb, i, j, s.negs, true, nullptr, nullptr, nullptr, nullptr);
+    mark(PHASE_END);
+}
+
+std::vector<double> Engine::profile_read() {
+    std::vector<double> ms(PHASE_END + 1, 0.0);
+    EMBER_CUDA(cudaStreamSynchronize(stream));
+    for (size_t k = 0; k + 1 < prof_events.size(); ++k) {
+        if (prof_events[k].first == PHASE_END) continue;
+        float t = 0.f;
+        EMBER_CUDA(cudaEventElapsedTime(&t, prof_events[k].second, prof_events[k + 1].second));
+        ms[prof_events[k].first] += t;
+    }
+    for (auto& pe : prof_events) cudaEventDestroy(pe.second);
+    prof_events.clear();
+    return ms;
+}
+
+void Engine::comm_init(const void* unique_id, int r, int w) {
+    if (w < 1 || r < 0 || r >= w) throw ConfigError("bad rank/world");
+    rank = r;
+    world = w;
+    if (w == 1) return;
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof(id));
+    ncclComm_t comm = nullptr;
+    EMBER_CUDA(cudaSetDevice(device));
+    ncclResult_t res = nccl().init_rank(&comm, w, id, r);
+    if (res != ncclSuccess) throw EmberError(std::string("ncclCommInitRank failed: ") + (nccl().err ? nccl().err(res) : "?"));
+    nccl_comm = comm;
+    if (m.kind != EMBER_DOT && !s.rel_dense) s.rel_dense = dalloc<float>((uint64_t)g.num_relations * dim);
+}
+
+void Engine::allreduce_relations(uint32_t) {
+    if (!nccl_comm) return;
+    const uint64_t rn = (uint64_t)g.num_relations * dim;
+    ncclResult_t r = nccl().all_reduce(s.rel_dense, s.rel_dense, rn, ncclFloat32, ncclSum, static_cast<ncclComm_t>(nccl_comm), stream);
+    if (r != ncclSuccess) throw EmberError(std::string("ncclAllReduce failed: ") + (nccl().err ? nccl().err(r) : "?"));
+}
+
+}  // namespace ember

@@ -1,0 +1,95 @@
+"""CPU checks of the C-ABI library: it loads, exports exactly what include/ember_gpu.h declares,
+maps errors to status codes without a GPU, and the host-side data plumbing (synthetic graph,
+bucketing) behaves per SPEC.md:70-78."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_2101_08358_b200 as eb
+from paper_2101_08358_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "ember_gpu.h")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ember_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = eb.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 25
+    for s in syms:
+        assert hasattr(L, s), s
+    nm = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (ember_\w+)", nm))
+    assert set(syms) <= exported
+    assert exported <= set(syms), f"undeclared exports: {exported - set(syms)}"
+
+
+def test_python_binding_declares_all_symbols():
+    assert set(declared_symbols()) <= _sig_names()
+
+
+def _sig_names():
+    src = open(_lib.__file__).read()
+    return set(re.findall(r'"(ember_\w+)"', src))
+
+
+def test_sm100a_code_in_library():
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_errors_map_to_status_codes_without_gpu():
+    L = eb.lib()
+    md = _lib.ModelDesc(7, 100, 0.1, 1e-10, 10, 10, 0.5, 1, 1, 0, 0)  # bad kind
+    gd = _lib.GraphDesc(100, 1, 1)
+    ctx = C.c_void_p()
+    st = L.ember_ctx_create(0, C.byref(md), C.byref(gd), None, C.byref(ctx))
+    assert st == _lib.EMBER_EUSER and b"kind" in L.ember_last_error()
+    md.kind = 0
+    md.dim = 6  # not a multiple of 4
+    assert L.ember_ctx_create(0, C.byref(md), C.byref(gd), None, C.byref(ctx)) == _lib.EMBER_EUSER
+    assert L.ember_ctx_create(0, None, C.byref(gd), None, C.byref(ctx)) == _lib.EMBER_EUSER
+    assert L.ember_ctx_destroy(None) == _lib.EMBER_OK
+    with pytest.raises(eb.ConfigError):
+        _lib.check(L.ember_tables_bind(None, 0, None, None))
+
+
+def test_host_graph_generation_is_deterministic_and_in_range():
+    e1, s1 = eb.generate_graph(10_000, 50, 20_000, seed=3, train_frac=0.8, valid_frac=0.1)
+    e2, s2 = eb.generate_graph(10_000, 50, 20_000, seed=3, train_frac=0.8, valid_frac=0.1)
+    assert (e1 == e2).all() and (s1 == s2).all()
+    assert e1[:, 0].max() < 10_000 and e1[:, 2].max() < 10_000 and e1[:, 1].max() < 50
+    frac = np.bincount(s1, minlength=3) / len(s1)
+    assert abs(frac[0] - 0.8) < 0.02 and abs(frac[1] - 0.1) < 0.02
+    # power-law degrees: the top 1% of nodes carry a large share of endpoints
+    deg = np.bincount(np.concatenate([e1[:, 0], e1[:, 2]]), minlength=10_000)
+    top = np.sort(deg)[::-1][:100].sum() / deg.sum()
+    assert top > 0.05
+    # relations Zipf: relation 0 most frequent
+    assert np.bincount(e1[:, 1]).argmax() == 0
+
+
+def test_bucketing_is_a_stable_partition_of_the_edges():
+    V, p = 1000, 4
+    edges, _ = eb.generate_graph(V, 5, 5000, seed=1)
+    out, off = eb.bucket_edges(edges, V, p)
+    assert off[0] == 0 and off[-1] == len(edges) and (np.diff(off.astype(np.int64)) >= 0).all()
+    part = lambda x: np.searchsorted([eb.partition_offset(V, p, k) for k in range(1, p)], x, side="right")
+    for b in range(p * p):
+        seg = out[off[b]:off[b + 1]]
+        assert (part(seg[:, 0]) == b // p).all() and (part(seg[:, 2]) == b % p).all()
+        # stable: same relative order as in the input
+        key = part(edges[:, 0]) * p + part(edges[:, 2])
+        assert (seg == edges[key == b]).all()
+    # multiset equality
+    assert sorted(map(tuple, out.tolist())) == sorted(map(tuple, edges.tolist()))

@@ -1,0 +1,157 @@
+"""GPU parity through the C-ABI against the CPU oracle on identical seeded inputs.
+
+Bars (BASELINE.json north_star): negative ids, init and bucket order bit-exact; per-step scores,
+losses and gradients within 1e-4 relative (tolerance stated per assert); Adagrad bit-exact for
+identical gradients.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2101_08358_b200 as eb  # noqa: E402
+from oracle import pyoracle as po  # noqa: E402
+
+from gpu_helpers import host_tables, make_graph, make_trainer, oracle_model, rel_err, row_rel_err  # noqa: E402
+
+TOL = 1e-4  # per-step scores and gradients, relative (north_star)
+ENGINES = ["simt"]
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).cuda()
+
+
+@pytest.fixture(scope="module")
+def graph():
+    return make_graph(V=3000, R=20, E=20000, p=2)
+
+
+def test_init_bit_exact_vs_oracle():
+    tr = make_trainer("complex", dim=40, V=3000, p=2)
+    th, ac, rt, _ = host_tables(tr)
+    assert (ac == 0).all()
+    ref = po.init_rows(11, 40, 0, 3000)
+    assert th.tobytes() == ref.tobytes()
+    assert rt.tobytes() == po.init_rows(11 ^ 0x52454C, 40, 0, 20).tobytes()
+
+
+@pytest.mark.parametrize("chunks,alpha", [(1, 0.5), (3, 0.0), (2, 1.0)])
+def test_negative_ids_bit_exact(graph, chunks, alpha):
+    edges, off, _ = graph
+    tr = make_trainer("distmult", nt=257, chunks=chunks, alpha=alpha, p=2)
+    m = oracle_model(tr)
+    for (i, j) in [(0, 0), (0, 1), (1, 0)]:
+        b = i * 2 + j
+        bucket = edges[off[b]:off[b + 1]]
+        got = tr.sample_negatives(_dev(bucket), i, j, epoch=3, bucket_step=5, batch_in_bucket=7)
+        exp = po.sample_negatives(m, 3, 5, 7, bucket, eb.partition_offset(3000, 2, i), eb.partition_size(3000, 2, i),
+                                  eb.partition_offset(3000, 2, j), eb.partition_size(3000, 2, j))
+        assert (got.cpu().numpy().view(np.uint32) == exp).all()
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("kind,chunks,nb", [("dot", 1, 512), ("distmult", 1, 512), ("complex", 1, 512),
+                                            ("complex", 4, 509), ("distmult", 2, 77)])
+def test_loss_and_grad_match_oracle(graph, engine, kind, chunks, nb):
+    edges, off, _ = graph
+    tr = make_trainer(kind, dim=32, nt=64, chunks=chunks, p=2, engine=engine)
+    th, _, rt, _ = host_tables(tr)
+    i, j = 0, 1
+    bucket = edges[off[1]:off[2]]
+    negs = tr.sample_negatives(_dev(bucket), i, j, 0, 0, 0)
+    batch = bucket[:nb]
+    got = tr.loss_and_grad(_dev(batch), negs, i, j)
+    exp = po.loss_and_grad(oracle_model(tr), batch, negs.cpu().numpy().view(np.uint32), th, rt)
+    assert abs(got["loss"] - exp["loss"]) <= TOL * abs(exp["loss"])
+    assert rel_err(got["fpos"], exp["fpos"]) <= TOL
+    assert rel_err(got["lse"], exp["lse"]) <= TOL
+    assert (got["node_ids"] == exp["node_ids"]).all()
+    assert row_rel_err(got["node_rows"], exp["node_rows"]) <= TOL
+    assert rel_err(got["node_rows"], exp["node_rows"]) <= TOL
+    assert (got["rel_ids"] == exp["rel_ids"]).all()
+    if kind != "dot":
+        assert row_rel_err(got["rel_rows"], exp["rel_rows"]) <= TOL
+
+
+def test_scores_match_oracle(graph):
+    edges, off, _ = graph
+    tr = make_trainer("complex", dim=32, nt=64, p=2)
+    th, _, rt, _ = host_tables(tr)
+    bucket = edges[off[1]:off[2]]
+    negs = tr.sample_negatives(_dev(bucket), 0, 1)
+    batch = bucket[:100]
+    for side in (0, 1):
+        got = tr.debug_scores(_dev(batch), negs, side=side, rows=50, i=0, j=1)
+        nn = negs.cpu().numpy().view(np.uint32)[side * 64:(side + 1) * 64]
+        exp = np.zeros((50, 64), np.float32)
+        for r in range(50):
+            s, rel, t = batch[r]
+            for k in range(64):
+                trip = (nn[k], rel, t) if side == 1 else (s, rel, nn[k])
+                exp[r, k] = po.lib().orc_score(2, 32, th[trip[0]].copy(), rt[trip[1]].copy(), th[trip[2]].copy())
+        assert rel_err(got, exp) <= TOL
+
+
+def test_adagrad_bit_exact():
+    tr = make_trainer("distmult", dim=32, p=1)
+    th0, ac0, rt0, ra0 = host_tables(tr)
+    rng = np.random.default_rng(0)
+    ids = np.unique(rng.integers(0, 3000, 300)).astype(np.uint32)
+    rows = rng.standard_normal((len(ids), 32)).astype(np.float32)
+    tr.adagrad_apply(_dev(ids), torch.from_numpy(rows).cuda())
+    tr.adagrad_apply(_dev(ids), torch.from_numpy(rows * 0.5).cuda())
+    th, ac, _, _ = host_tables(tr)
+    po.adagrad_apply(32, 0.1, 1e-10, ids, rows, th0, ac0)
+    po.adagrad_apply(32, 0.1, 1e-10, ids, rows * 0.5, th0, ac0)
+    assert th.tobytes() == th0.tobytes() and ac.tobytes() == ac0.tobytes()
+    rid = np.array([0, 5, 19], np.uint32)
+    rrows = rng.standard_normal((3, 32)).astype(np.float32)
+    tr.adagrad_apply(_dev(rid), torch.from_numpy(rrows).cuda(), relations=True)
+    po.adagrad_apply(32, 0.1, 1e-10, rid, rrows, rt0, ra0)
+    _, _, rt, ra = host_tables(tr)
+    assert rt.tobytes() == rt0.tobytes() and ra.tobytes() == ra0.tobytes()
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_training_trajectory_matches_oracle(graph, engine):
+    """A few full steps (sample -> grads -> Adagrad) over two buckets; losses within 1e-4, tables
+    close (Adagrad's first step is ~ -lr*sign(g), so elements whose gradient is at rounding level can
+    legitimately flip: allow < 0.01% of elements)."""
+    edges, off, _ = graph
+    tr = make_trainer("complex", dim=32, b=256, nt=64, p=2, engine=engine)
+    th, ac, rt, ra = host_tables(tr)
+    m = oracle_model(tr)
+    V, p = 3000, 2
+    for step, (i, j) in enumerate([(0, 1), (1, 1)]):
+        b = i * p + j
+        bucket = edges[off[b]:off[b + 1]]
+        dbucket = _dev(bucket)
+        loss_dev = torch.zeros(1, device="cuda")
+        for k in range(2):
+            tr.train_batch(dbucket, k * 256, 256, i, j, epoch=1, bucket_step=step, batch_in_bucket=k,
+                           loss_out=loss_dev)
+            l_gpu = float(loss_dev.item())
+            l_cpu = po.train_batch(m, 1, step, k, bucket, k * 256, 256, eb.partition_offset(V, p, i),
+                                   eb.partition_size(V, p, i), eb.partition_offset(V, p, j),
+                                   eb.partition_size(V, p, j), th, ac, rt, ra)
+            assert abs(l_gpu - l_cpu) <= TOL * abs(l_cpu), (step, k, l_gpu, l_cpu)
+    gth, gac, grt, gra = host_tables(tr)
+    for a, b_ in ((gth, th), (grt, rt)):
+        bad = np.abs(a - b_) > 1e-3
+        assert bad.mean() < 1e-4, bad.sum()
+    assert rel_err(gac, ac) <= 1e-3 and rel_err(gra, ra) <= 1e-3
+
+
+def test_eval_ranks_match_oracle(graph):
+    edges, off, test = graph
+    tr = make_trainer("distmult", dim=32, p=2)
+    th, _, rt, _ = host_tables(tr)
+    train = edges
+    got = tr.eval_ranks(_dev(test), _dev(train), n_eval=200, alpha_eval=0.5, block=100, eval_seed=9)
+    exp = po.eval_ranks("distmult", 32, th, rt, 3000, test, train_edges=train, n_eval_neg=200, alpha_eval=0.5,
+                        block=100, eval_seed=9)
+    assert (np.abs(got.astype(np.int64) - exp.astype(np.int64)) <= 1).mean() > 0.999
+    a, b = po.aggregate(got), po.aggregate(exp)
+    assert abs(a["mrr"] - b["mrr"]) < 1e-3
