@@ -84,7 +84,6 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     : device(dev), m(md), g(gd) {
     if (m.kind < EMBER_DOT || m.kind > EMBER_COMPLEX) throw ConfigError("model kind must be 0 (Dot), 1 (DistMult), 2 (ComplEx)");
     if (m.dim == 0 || m.dim % 4 != 0) throw ConfigError("dim must be a positive multiple of 4");
-    if (m.kind == EMBER_COMPLEX && m.dim % 8 != 0) throw ConfigError("ComplEx needs dim % 8 == 0 (even halves of float4s)");
     if (m.batch_size == 0) throw ConfigError("batch_size must be >= 1");
     if (!(m.alpha >= 0.f && m.alpha <= 1.f)) throw ConfigError("alpha must be in [0, 1]");
     if (!(m.eps > 0.f)) throw ConfigError("eps must be > 0 (SPEC.md:170)");
@@ -138,6 +137,9 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     s.counts = dalloc<uint32_t>(nrows);
     s.offsets = dalloc<uint32_t>(nrows);
     s.nunique = dalloc<uint32_t>(2);
+    s.cc = dalloc<uint32_t>(nrows);
+    s.coff = dalloc<uint32_t>(nrows);
+    s.partial = dalloc<float>(nrows * d);
     if (m.engine == EMBER_ENGINE_SIMT_FP32) {
         s.S = dalloc<float>(2 * b * (uint64_t)(nt ? nt : 1));
         s.dN_part = dalloc<float>((uint64_t)dsplit * n_neg * d);
@@ -157,7 +159,7 @@ Engine::~Engine() {
     cudaSetDevice(device);
     void* ptrs[] = {s.negs, s.batch, s.A, s.fpos, s.lse, s.g0, s.N, s.S, s.dA, s.dN_part, s.grows, s.rrows,
                     s.row_loss, s.loss, s.keys, s.keys_sorted, s.vals, s.vals_sorted, s.ukeys, s.counts, s.offsets,
-                    s.nunique, s.cub_tmp, s.Atc, s.Ntc, s.NTtc, s.dN_tc, s.rel_dense};
+                    s.nunique, s.cub_tmp, s.Atc, s.Ntc, s.NTtc, s.dN_tc, s.rel_dense, s.cc, s.coff, s.partial};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (nccl_comm) {

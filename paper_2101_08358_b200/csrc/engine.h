@@ -81,6 +81,9 @@ struct Scratch {
     uint16_t* NTtc = nullptr;
     float* dN_tc = nullptr;
     float* rel_dense = nullptr;  // [R][dim] relation gradient summed over ranks (world > 1)
+    uint32_t* cc = nullptr;      // chunks per unique id (segmented reduction)
+    uint32_t* coff = nullptr;    // exclusive scan of cc
+    float* partial = nullptr;    // [2b + negs][dim] per-chunk partial sums
 };
 
 struct Engine {

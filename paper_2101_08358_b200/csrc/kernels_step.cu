@@ -10,6 +10,8 @@
 // Rows are dim floats (dim % 4 == 0) and are moved warp-per-row with 128-bit accesses.
 #include <cuda_runtime.h>
 
+#include <cub/cub.cuh>
+
 #include "engine.h"
 
 namespace ember {
@@ -198,15 +200,62 @@ __device__ __forceinline__ float adagrad_elem(float& th, float& ac, float g, flo
     return th;
 }
 
-// One warp per unique id: sum its gradient rows in sorted (stable) order, then Adagrad.
-__global__ void k_adagrad_segs(const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ offsets,
+// Segmented sum in two deterministic passes so hot ids (Zipf relations, power-law nodes) are not
+// serialised on one warp: every segment is cut into chunks of <= kChunk sorted rows.
+constexpr uint32_t kChunk = 32;
+
+__global__ void k_chunk_counts(const uint32_t* __restrict__ counts, const uint32_t* __restrict__ nunique, uint32_t n,
+                               uint32_t* cc) {
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n) return;
+    cc[u] = u < *nunique ? (counts[u] + kChunk - 1) / kChunk : 0u;
+}
+
+// Pass 1: one warp per chunk sums its rows (ascending sorted position) into partial[chunk].
+__global__ void k_chunk_sum(const uint32_t* __restrict__ coff, const uint32_t* __restrict__ offsets,
+                            const uint32_t* __restrict__ counts, const uint32_t* __restrict__ nunique,
+                            const uint32_t* __restrict__ vals, const float* __restrict__ rows, uint32_t d,
+                            float* __restrict__ partial) {
+    const uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const uint32_t nu = *nunique;
+    if (nu == 0) return;
+    const uint32_t total = coff[nu - 1] + (counts[nu - 1] + kChunk - 1) / kChunk;
+    if (g >= total) return;
+    uint32_t lo = 0, hi = nu - 1;  // last segment whose first chunk is <= g
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (coff[mid] <= g) lo = mid;
+        else hi = mid - 1;
+    }
+    const uint32_t r0 = offsets[lo] + (g - coff[lo]) * kChunk;
+    const uint32_t r1 = min(r0 + kChunk, offsets[lo] + counts[lo]);
+    const uint32_t cnt = r1 - r0;
+    const uint32_t my = lane < cnt ? vals[r0 + lane] : 0u;
+    for (uint32_t base = 0; base < d / 4; base += 32) {  // all lanes stay converged for the shuffles
+        const uint32_t c4 = base + lane;
+        const bool live = c4 < d / 4;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+        for (uint32_t c = 0; c < cnt; ++c) {
+            const uint32_t idx = __shfl_sync(0xffffffffu, my, c);
+            if (live) {
+                const float4 x = ldg4(rows + (uint64_t)idx * d + 4 * c4);
+                acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+            }
+        }
+        if (live) reinterpret_cast<float4*>(partial + (uint64_t)g * d)[c4] = acc;
+    }
+}
+
+// Pass 2: one warp per unique id sums its chunk partials in order, then Adagrad (or exports).
+__global__ void k_adagrad_segs(const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ coff,
                                const uint32_t* __restrict__ counts, const uint32_t* __restrict__ nunique,
-                               const uint32_t* __restrict__ vals, const float* __restrict__ rows, uint32_t d,
-                               PartView pi, PartView pj, int relations, float* rel_theta, float* rel_acc, float lr,
-                               float eps, uint32_t* ids_out, float* rows_out, int apply) {
+                               const float* __restrict__ partial, uint32_t d, PartView pi, PartView pj, int relations,
+                               float* rel_theta, float* rel_acc, float lr, float eps, uint32_t* ids_out,
+                               float* rows_out, int apply) {
     const uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (u >= *nunique) return;
-    const uint32_t key = ukeys[u], beg = offsets[u], cnt = counts[u];
+    const uint32_t key = ukeys[u], beg = coff[u], cnt = (counts[u] + kChunk - 1) / kChunk;
     float* th;
     float* ac;
     if (relations) {
@@ -220,8 +269,9 @@ __global__ void k_adagrad_segs(const uint32_t* __restrict__ ukeys, const uint32_
     if (ids_out && lane == 0) ids_out[u] = key;
     for (uint32_t c4 = lane; c4 < d / 4; c4 += 32) {
         float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
         for (uint32_t c = 0; c < cnt; ++c) {
-            const float4 x = ldg4(rows + (uint64_t)vals[beg + c] * d + 4 * c4);
+            const float4 x = ldg4(partial + (uint64_t)(beg + c) * d + 4 * c4);
             g.x += x.x; g.y += x.y; g.z += x.z; g.w += x.w;
         }
         if (rows_out) reinterpret_cast<float4*>(rows_out + (uint64_t)u * d)[c4] = g;
@@ -340,9 +390,18 @@ void launch_adagrad_segments(const Engine& E, const uint32_t* ukeys, const uint3
                              const PartView& pi, const PartView& pj, bool relations, uint32_t* ids_out,
                              float* rows_out, bool apply) {
     if (!max_u) return;
-    k_adagrad_segs<<<(max_u * 32 + 255) / 256, 256, 0, E.stream>>>(
-        ukeys, offsets, counts, nunique, vals_sorted, rows, E.dim, pi, pj, relations ? 1 : 0, E.rel_theta, E.rel_acc,
-        E.m.lr, E.m.eps, ids_out, rows_out, apply ? 1 : 0);
+    const unsigned wblocks = (max_u * 32 + 255) / 256;
+    k_chunk_counts<<<(max_u + 255) / 256, 256, 0, E.stream>>>(counts, nunique, max_u, E.s.cc);
+    EMBER_LAUNCHED(E);
+    size_t bytes = E.s.cub_bytes;
+    EMBER_CUDA(cub::DeviceScan::ExclusiveSum(E.s.cub_tmp, bytes, E.s.cc, E.s.coff, (int)max_u, E.stream));
+    ++E.lib_calls;
+    k_chunk_sum<<<wblocks, 256, 0, E.stream>>>(E.s.coff, offsets, counts, nunique, vals_sorted, rows, E.dim,
+                                               E.s.partial);
+    EMBER_LAUNCHED(E);
+    k_adagrad_segs<<<wblocks, 256, 0, E.stream>>>(ukeys, E.s.coff, counts, nunique, E.s.partial, E.dim, pi, pj,
+                                                  relations ? 1 : 0, E.rel_theta, E.rel_acc, E.m.lr, E.m.eps, ids_out,
+                                                  rows_out, apply ? 1 : 0);
     EMBER_LAUNCHED(E);
 }
 
