@@ -172,6 +172,9 @@ int ember_graph_bucket(int device, uint64_t num_nodes, uint32_t p, const uint32_
  * CUB device-wide calls (library kernels) since creation. Synchronises the stream. */
 int ember_profile_enable(ember_ctx* ctx, int enable);
 int ember_profile_read(ember_ctx* ctx, double* ms_out, uint64_t* launches_out, uint64_t* lib_calls_out);
+/* Self-test of the tcgen05 building blocks on `device` (one 128 x N x K bf16 product vs a double
+ * host product); max_rel_err_out = max|err| / max|ref|. mode: see csrc/tc_selftest.cu. */
+int ember_tc_selftest(int device, int mode, int K, int N, uint64_t seed, double* max_rel_err_out);
 
 /* ---- multi-GPU------------------------------------------------------------ */
 /* nccl_unique_id: 128 bytes (ncclUniqueId) shared by all ranks. NCCL is loaded at run time. */

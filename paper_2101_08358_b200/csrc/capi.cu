@@ -17,6 +17,7 @@ void graph_generate(int device, uint64_t V, uint32_t R, uint64_t n, uint64_t see
                     uint32_t* edges, uint8_t* split);
 void graph_bucket(int device, uint64_t V, uint32_t p, const uint32_t* in, uint64_t n, uint32_t* out,
                   uint64_t* offsets);
+double tc_selftest(int device, int mode, int K, int N, uint64_t seed);
 void launch_eval(const Engine& E, const uint32_t* test, uint32_t n_test, const uint32_t* train, uint64_t n_train,
                  uint32_t n_eval, float alpha_eval, uint32_t block, uint64_t eval_seed, uint32_t* ranks);
 }  // namespace ember
@@ -311,6 +312,13 @@ int ember_graph_bucket(int device, uint64_t V, uint32_t p, const uint32_t* in, u
         need(out, "edges_out");
         need(offsets, "offsets_out");
         graph_bucket(device, V, p, in, n, out, offsets);
+    });
+}
+
+int ember_tc_selftest(int device, int mode, int K, int N, uint64_t seed, double* err) {
+    return guarded([&] {
+        need(err, "max_rel_err_out");
+        *err = tc_selftest(device, mode, K, N, seed);
     });
 }
 
