@@ -187,10 +187,12 @@ def bench_ours(args, rank, world, local_rank):
     clocks.start()
     time.sleep(0.3)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.profiler.start()  # ncu --profile-from-start off captures exactly the timed steps
     e0.record(stream)
     edges = W.run_steps(start_at + args.warmup, args.steps)
     e1.record(stream)
     torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
     ms = e0.elapsed_time(e1)
     clk = clocks.stop()
     prof = tr.profile_read()
