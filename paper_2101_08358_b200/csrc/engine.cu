@@ -152,11 +152,13 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     EMBER_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t3, s.counts, s.offsets, (int)nrows, stream));
     s.cub_bytes = std::max(t1, std::max(t2, t3));
     s.cub_tmp = dalloc<uint8_t>(s.cub_bytes);
+    if (m.engine == EMBER_ENGINE_TC_BF16X3) tc_setup(*this);
     EMBER_CUDA(cudaStreamSynchronize(stream));
 }
 
 Engine::~Engine() {
     cudaSetDevice(device);
+    tc_release(*this);
     void* ptrs[] = {s.negs, s.batch, s.A, s.fpos, s.lse, s.g0, s.N, s.S, s.dA, s.dN_part, s.grows, s.rrows,
                     s.row_loss, s.loss, s.keys, s.keys_sorted, s.vals, s.vals_sorted, s.ukeys, s.counts, s.offsets,
                     s.nunique, s.cub_tmp, s.Atc, s.Ntc, s.NTtc, s.dN_tc, s.rel_dense, s.cc, s.coff, s.partial};

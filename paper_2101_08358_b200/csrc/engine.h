@@ -86,6 +86,8 @@ struct Scratch {
     float* partial = nullptr;    // [2b + negs][dim] per-chunk partial sums
 };
 
+struct TcState;  // tensor-core engine state (tc_score.cu)
+
 struct Engine {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -103,6 +105,7 @@ struct Engine {
     float* rel_theta = nullptr;
     float* rel_acc = nullptr;
     Scratch s;
+    TcState* tc = nullptr;
     int sm_count = 148;
     // multi-GPU
     void* nccl_comm = nullptr;
@@ -163,5 +166,7 @@ void launch_debug_scores(const Engine& E, const uint32_t* edges, uint32_t nb, co
 void launch_eval_ranks(const Engine& E, const uint32_t* test, uint32_t n_test, const uint32_t* negs, uint32_t n_eval,
                        uint32_t block, uint32_t* ranks);
 bool tc_engine_supported(const Engine& E);
+void tc_setup(Engine& E);
+void tc_release(Engine& E);
 
 }  // namespace ember

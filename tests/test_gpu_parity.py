@@ -16,7 +16,7 @@ from oracle import pyoracle as po  # noqa: E402
 from gpu_helpers import host_tables, make_graph, make_trainer, oracle_model, rel_err, row_rel_err  # noqa: E402
 
 TOL = 1e-4  # per-step scores and gradients, relative (north_star)
-ENGINES = ["simt"]
+ENGINES = ["simt", "tc"]
 
 
 def _dev(a):
@@ -55,6 +55,8 @@ def test_negative_ids_bit_exact(graph, chunks, alpha):
 @pytest.mark.parametrize("kind,chunks,nb", [("dot", 1, 512), ("distmult", 1, 512), ("complex", 1, 512),
                                             ("complex", 4, 509), ("distmult", 2, 77)])
 def test_loss_and_grad_match_oracle(graph, engine, kind, chunks, nb):
+    if engine == "tc" and chunks > 1:
+        pytest.skip("tensor-core engine shares one negative set per batch (num_chunks == 1)")
     edges, off, _ = graph
     tr = make_trainer(kind, dim=32, nt=64, chunks=chunks, p=2, engine=engine)
     th, _, rt, _ = host_tables(tr)
@@ -155,3 +157,28 @@ def test_eval_ranks_match_oracle(graph):
     assert (np.abs(got.astype(np.int64) - exp.astype(np.int64)) <= 1).mean() > 0.999
     a, b = po.aggregate(got), po.aggregate(exp)
     assert abs(a["mrr"] - b["mrr"]) < 1e-3
+
+
+@pytest.mark.parametrize("kind,dim,nt,nb,tau", [("complex", 100, 1000, 3000, None), ("dot", 100, 1000, 1500, None),
+                                              ("distmult", 40, 100, 333, None), ("complex", 64, 200, 700, "0"),
+                                              ("distmult", 128, 300, 1000, None), ("complex", 16, 17, 5, None)])
+def test_tc_engine_headline_shapes(graph, monkeypatch, kind, dim, nt, nb, tau):
+    """Tensor-core contraction at the headline d=100 / n_t=1000 shape (smaller b), ragged tiles
+    (nb, n_t not multiples of the 128/64 tiles), d at the 128 limit, and tau=0 (the lazy-rescale
+    path taken on every negative tile) — all within 1e-4 of the oracle."""
+    if tau is not None:
+        monkeypatch.setenv("EMBER_TC_TAU", tau)
+    edges, off, _ = graph
+    tr = make_trainer(kind, dim=dim, b=max(nb, 16), nt=nt, p=2, engine="tc")
+    th, _, rt, _ = host_tables(tr)
+    bucket = edges[off[1]:off[2]]
+    negs = tr.sample_negatives(_dev(bucket), 0, 1, 0, 0, 0)
+    batch = bucket[:nb]
+    got = tr.loss_and_grad(_dev(batch), negs, 0, 1)
+    exp = po.loss_and_grad(oracle_model(tr), batch, negs.cpu().numpy().view(np.uint32), th, rt)
+    assert abs(got["loss"] - exp["loss"]) <= TOL * abs(exp["loss"])
+    assert rel_err(got["lse"], exp["lse"]) <= TOL
+    assert (got["node_ids"] == exp["node_ids"]).all()
+    assert row_rel_err(got["node_rows"], exp["node_rows"]) <= TOL
+    if kind != "dot":
+        assert row_rel_err(got["rel_rows"], exp["rel_rows"]) <= TOL
