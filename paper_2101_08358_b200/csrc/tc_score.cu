@@ -9,22 +9,30 @@
 // a product uses the three terms hi*hi + hi*lo + lo*hi (fp32 accumulate in TMEM), ~2^-16
 // relative per product — inside the 1e-4 per-step tolerance of the north_star.
 //
-// Operand layout in HBM (written by k_pack_*): per side, [2*CB column blocks][rows][8 bf16],
-// CB = KP/8 (KP = dim rounded up to 16), hi blocks then lo blocks. Any row range of it is one
-// TMA box {8, R, 2CB} that lands in shared memory as the canonical no-swizzle K-major UMMA
-// tile [cb][R][16 B] (tc_common.cuh), and the same bytes serve as the MN-major operand of the
-// transposed products.
+// Operand layout in HBM (written by k_pack): per side, [2*CB column blocks][rows][8 bf16],
+// CB = KP/8 (KP = dim rounded up to 16), hi blocks then lo blocks. Any row range is one TMA
+// box {8, R, 2CB} that lands in shared memory as the canonical no-swizzle K-major UMMA tile
+// [cb][R][16 B] (tc_common.cuh); the same bytes are the MN-major operand of the transposed
+// product.
 //
-// Per side, with A = adjusted vectors [nb x d], N = shared negatives [nt x d], b = nb:
-//   k_tc_rows  (row-parallel, FlashAttention-forward shape): for each 128-row tile,
-//              S = A N^T streamed over 64-negative tiles (TMEM, double-buffered), online
-//              row max/sum with lazy rescaling, P = exp(S - m) in bf16 hi/lo to smem, and
-//              dA += P N accumulated in TMEM. Epilogue: lse, g0 = (p_pos - 1)/b, dA /= Z*b.
-//   k_tc_negs  (negative-parallel, FA-backward dK shape): for each 128-negative tile and a
-//              chunk of 64-row sub-tiles, S^T = N A^T, P^T = exp(S^T - lse)/b, and
-//              dN += P^T A in TMEM; partial dN per chunk, summed in fixed order by k_dn_reduce.
-// Warp roles (both kernels): warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer
-// (one thread), warps 2..5 = epilogue (TMEM lane quadrant = warp % 4).
+// One kernel template, two modes, per side (A = adjusted vectors [nb x d], N = shared
+// negatives [nt x d], b = nb):
+//   MODE_ROWS  item = 128-row tile of A (resident), streamed over 64-negative tiles of N:
+//              S = A N^T, P = exp(S - f_pos) (the positive's score is the fixed row shift: it
+//              is part of every row's log-sum-exp, so no online rescaling is needed), dA += P N.
+//              Item end: lse = f_pos + log(1 + sum P), g0 = (exp(f_pos - lse) - 1)/b, dA/(Z b).
+//              Rows whose sum overflows the safe range are listed and recomputed exactly by
+//              k_tc_fixup before anything reads lse.
+//   MODE_NEGS  item = 128-negative tile of N (resident) x a chunk of 64-row tiles of A:
+//              S^T = N A^T, P^T = exp(S^T - lse)/b, dN += P^T A; per-chunk partials are summed
+//              in a fixed order by k_dn_reduce (deterministic).
+// TMEM (512 columns): [0,128) two 64-column S buffers, each overwritten in place by P as bf16
+// hi|lo pairs (the A operand of the second product, TS mode); [128,128+KP) the accumulator;
+// [256,384) / [384,512) the double-buffered resident operand (hi|lo pairs), so every MMA reads
+// only its B operand from shared memory.
+// Warps: 0 = TMA producer, 1 = TMEM owner + MMA issuer (one thread), 2..9 = two epilogue
+// warpgroups that take alternate streamed tiles (ping-pong); group 0 also stages the next
+// item's resident operand smem -> TMEM.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -40,361 +48,178 @@
 namespace ember {
 namespace {
 
-constexpr int RT = 128;      // k_tc_rows: rows per tile (MMA M)
-constexpr int NT1 = 64;      // k_tc_rows: negatives per tile (S: MMA N; P.N: K)
-constexpr int NS1 = 3;       // k_tc_rows: negative-tile ring depth
-constexpr int MT2 = 128;     // k_tc_negs: negatives per item (MMA M)
-constexpr int RS2 = 64;      // k_tc_negs: rows per sub-tile
-constexpr int NS2 = 3;       // k_tc_negs: row-sub-tile ring depth
+enum { MODE_ROWS = 0, MODE_NEGS = 1 };
+constexpr int RES = 128;     // resident rows per item (MMA M)
+constexpr int TILE = 64;     // streamed rows per tile (first product's N, second product's K)
+constexpr int NSTAGE = 4;    // streamed-tile ring depth
 constexpr int KPMAX = 128;   // largest padded dim
-constexpr uint32_t TCOLS = 256;  // TMEM columns: S double buffer (2 x 64) + accumulator (<= 128)
-constexpr int NTHREADS = 192;
+constexpr int NTHREADS = 320;
+constexpr uint32_t TCOLS = 512;
+constexpr uint32_t T_ACC = 128, T_RES = 256;
+constexpr float L2E = 1.4426950408889634f;
 
 struct TcArgs {
-    int KP, CB, d, nb, nt, n_pad;
-    float inv_b, tau;
+    int KP, CB, d, nb, nt, n_pad, b_cap, chunks2;
+    float inv_b, log2_inv_b, zmax;
     const float* fpos;
-    float* lse;
-    float* g0;
-    float* dA;       // [2][nb][d]
-    float* dN_part;  // [chunks][2][n_pad][d]
-    int chunks2;
+    float* lse;       // [2][nb]
+    float* lse_pad;   // [2][b_cap], +inf past nb
+    float* g0;        // [2][nb]
+    float* dA;        // [2][nb][d]
+    float* dN_part;   // [chunks][2][n_pad][d]
+    uint32_t* flags;  // [0] = count, [1..] = side * b_cap + row
 };
 
-// Shared-memory carve-up (bytes), identical for both kernels:
-//   big   : resident tile, 128 rows x KP x (hi, lo) bf16   = 512*KP
-//   ring  : 3 stages of 64 rows x KP x (hi, lo)             = 3*256*KP
-//   P     : 2 buffers of 128 x 64 x (hi, lo) bf16           = 2*32 KB
-//   bars  : mbarriers + TMEM slot
-struct Smem {
-    uint8_t* big;
-    uint8_t* ring[3];
-    uint8_t* P[2];
-    uint64_t* bars;
-};
-__host__ __device__ constexpr size_t big_bytes(int KP) { return (size_t)512 * KP; }
-__host__ __device__ constexpr size_t stage_bytes(int KP) { return (size_t)256 * KP; }
-constexpr size_t P_BYTES = 128 * 64 * 4;
+// ---- shared memory ------------------------------------------------------------------------
+__host__ __device__ constexpr size_t res_bytes(int KP) { return (size_t)RES * KP * 4; }
+__host__ __device__ constexpr size_t stage_bytes(int KP) { return ((size_t)TILE * KP * 4 + 256 + 1023) & ~size_t(1023); }
 __host__ __device__ constexpr size_t smem_total(int KP) {
-    return 1024 + big_bytes(KP) + 3 * stage_bytes(KP) + 2 * P_BYTES + 256;
+    return 1024 + res_bytes(KP) + NSTAGE * stage_bytes(KP) + 2 * 2 * RES * 4 + 256;
 }
+
+enum {
+    B_RES_FULL = 0, B_RES_EMPTY = 1,
+    B_RING_FULL = 2,                 // + NSTAGE
+    B_RING_EMPTY = 2 + NSTAGE,       // + NSTAGE
+    B_S_FULL = 2 + 2 * NSTAGE,       // + 2
+    B_P_FULL = 4 + 2 * NSTAGE,       // + 2
+    B_R_READY = 6 + 2 * NSTAGE,      // + 2
+    B_ACC_FULL = 8 + 2 * NSTAGE, B_ACC_EMPTY = 9 + 2 * NSTAGE,
+    B_TMEM_SLOT = 10 + 2 * NSTAGE,
+};
+
+struct Smem {
+    uint8_t* res;
+    uint8_t* ring;  // NSTAGE x stage_bytes; a stage = tile [2CB][64][16 B] then 64 floats (lse)
+    float* zbuf;    // [2 items][2 groups][128]
+    uint64_t* bars;
+    size_t sbytes;
+    __device__ uint8_t* stage(int st) const { return ring + (size_t)st * sbytes; }
+};
 
 __device__ __forceinline__ Smem carve(uint8_t* raw, int KP) {
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
     Smem s;
-    s.big = base;
-    uint8_t* p = base + big_bytes(KP);
-    for (int i = 0; i < 3; ++i, p += stage_bytes(KP)) s.ring[i] = p;
-    s.P[0] = p;
-    s.P[1] = p + P_BYTES;
-    s.bars = reinterpret_cast<uint64_t*>(p + 2 * P_BYTES);
+    s.sbytes = stage_bytes(KP);
+    s.res = base;
+    s.ring = base + res_bytes(KP);
+    s.zbuf = reinterpret_cast<float*>(s.ring + NSTAGE * s.sbytes);
+    s.bars = reinterpret_cast<uint64_t*>(s.zbuf + 2 * 2 * RES);
     return s;
 }
-
-// barrier slots
-enum {
-    B_BIG_FULL = 0, B_BIG_EMPTY = 1,
-    B_RING_FULL = 2,   // +3
-    B_RING_EMPTY = 5,  // +3
-    B_S_FULL = 8,      // +2
-    B_S_EMPTY = 10,    // +2
-    B_P_FULL = 12,     // +2
-    B_P_EMPTY = 14,    // +2
-    B_ACC_FULL = 16, B_ACC_EMPTY = 17,
-    B_TMEM_SLOT = 18,  // uint32 slot lives here
-    NBARS = 19
-};
-
-__device__ __forceinline__ uint32_t u32_of(float f) { return __float_as_uint(f); }
 
 // Descriptor of a canonical K-major tile [cb][R][16 B] at k-step s (16 elements = 2 blocks).
 __device__ __forceinline__ uint64_t kdesc(const uint8_t* tile, int R, int s, int cb0) {
     return tc::sdesc(tc::smem_addr(tile) + (uint32_t)((cb0 + 2 * s) * R * 16), (uint32_t)(R * 16), 128u);
 }
-// Same bytes read as the MN-major operand of the transposed product: K = R rows, k-step s.
+// The same bytes read as the MN-major operand of the transposed product: K = R rows.
 __device__ __forceinline__ uint64_t mndesc(const uint8_t* tile, int R, int s, int cb0) {
     return tc::sdesc(tc::smem_addr(tile) + (uint32_t)(cb0 * R * 16 + s * 256), 128u, (uint32_t)(R * 16));
 }
 
-__device__ __forceinline__ void init_bars(uint64_t* bars) {
-    tc::mbar_init(&bars[B_BIG_FULL], 1);
-    tc::mbar_init(&bars[B_BIG_EMPTY], 1);
-    for (int i = 0; i < 3; ++i) {
-        tc::mbar_init(&bars[B_RING_FULL + i], 1);
-        tc::mbar_init(&bars[B_RING_EMPTY + i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-        tc::mbar_init(&bars[B_S_FULL + i], 1);
-        tc::mbar_init(&bars[B_S_EMPTY + i], 128);
-        tc::mbar_init(&bars[B_P_FULL + i], 128);
-        tc::mbar_init(&bars[B_P_EMPTY + i], 1);
-    }
-    tc::mbar_init(&bars[B_ACC_FULL], 1);
-    tc::mbar_init(&bars[B_ACC_EMPTY], 128);
-    tc::fence_mbar_init();
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+// ---- item geometry -------------------------------------------------------------------------
+struct Item {
+    int side, r0, t0, T, chunk, ntile;
+};
+
+template <int MODE>
+__device__ __forceinline__ int n_items(const TcArgs& g) {
+    if (MODE == MODE_ROWS) return 2 * ((g.nb + RES - 1) / RES);
+    return 2 * (g.n_pad / RES) * g.chunks2;
 }
 
-// Every epilogue thread arrives (count 128): its own TMEM reads / smem writes are ordered
-// before its own release-arrive.
-__device__ __forceinline__ void epi_arrive(uint64_t* bar) { tc::mbar_arrive(bar); }
+template <int MODE>
+__device__ __forceinline__ Item item_geo(const TcArgs& g, int item) {
+    Item it;
+    if (MODE == MODE_ROWS) {
+        const int row_tiles = (g.nb + RES - 1) / RES;
+        it.side = item / row_tiles;
+        it.r0 = (item % row_tiles) * RES;
+        it.t0 = 0;
+        it.T = (g.nt + TILE - 1) / TILE;
+        it.chunk = it.ntile = 0;
+    } else {
+        const int ntl = g.n_pad / RES, nsub = (g.nb + TILE - 1) / TILE;
+        it.side = item / (ntl * g.chunks2);
+        const int rem = item % (ntl * g.chunks2);
+        it.ntile = rem / g.chunks2;
+        it.chunk = rem % g.chunks2;
+        const int u0 = (int)((long long)it.chunk * nsub / g.chunks2);
+        it.T = (int)((long long)(it.chunk + 1) * nsub / g.chunks2) - u0;
+        it.r0 = it.ntile * RES;
+        it.t0 = u0 * TILE;
+    }
+    return it;
+}
 
-// Loads 64 fp32 TMEM columns of this warp's lane quadrant.
-__device__ __forceinline__ void ld64(uint32_t taddr, float (&v)[64]) {
-    uint32_t a[32], b[32];
-    tc::tmem_ld32(taddr, a);
-    tc::tmem_ld32(taddr + 32, b);
-    tc::tmem_ld_wait();
+// Group 0: resident tile (smem, canonical K-major [2CB][128][16 B]) -> TMEM columns
+// [tR, tR + KP) as bf16 pairs: block cb -> columns 4cb..4cb+3 (hi blocks first, then lo).
+__device__ __forceinline__ void stage_resident(const Smem& sm, uint64_t* bars, int CB, uint32_t it, int r,
+                                               uint32_t t_row) {
+    tc::mbar_wait(&bars[B_RES_FULL], it & 1);
+    const uint32_t tR = t_row + T_RES + (it & 1) * 128;
+    for (int c0 = 0; c0 < 2 * CB; c0 += 4) {
+        uint32_t v[16];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int cb = c0 + i;
+            uint4 x = make_uint4(0, 0, 0, 0);
+            if (cb < 2 * CB) x = *reinterpret_cast<const uint4*>(sm.res + (size_t)cb * RES * 16 + r * 16);
+            v[4 * i] = x.x;
+            v[4 * i + 1] = x.y;
+            v[4 * i + 2] = x.z;
+            v[4 * i + 3] = x.w;
+        }
+        tc::tmem_st16(tR + 4 * c0, v);
+    }
+    tc::tmem_st_wait();
+    tc::fence_before();
+    tc::mbar_arrive(&bars[B_RES_EMPTY]);
+    tc::mbar_arrive(&bars[B_R_READY + (it & 1)]);
+}
+
+// Splits 64 fp32 values into 32 bf16x2 hi pairs and 32 lo pairs.
+__device__ __forceinline__ void split64(const float (&p)[64], uint32_t (&hi)[32], uint32_t (&lo)[32]) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-        v[i] = __uint_as_float(a[i]);
-        v[32 + i] = __uint_as_float(b[i]);
+        const __nv_bfloat162 h = __floats2bfloat162_rn(p[2 * i], p[2 * i + 1]);
+        const float2 hf = __bfloat1622float2(h);
+        hi[i] = *reinterpret_cast<const uint32_t*>(&h);
+        lo[i] = tc::pack_bf16x2(p[2 * i] - hf.x, p[2 * i + 1] - hf.y);
     }
 }
 
-// Writes row `r` of a 128-row K-major bf16 hi/lo operand tile (64 K-elements) from 64 values.
-__device__ __forceinline__ void store_p_row(uint8_t* P, int r, const float (&p)[64]) {
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
-        float x[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) x[i] = p[8 * g + i];
-        uint4 hi, lo;
-        tc::split8(x, hi, lo);
-        *reinterpret_cast<uint4*>(P + g * (128 * 16) + r * 16) = hi;
-        *reinterpret_cast<uint4*>(P + 16384 + g * (128 * 16) + r * 16) = lo;
-    }
-}
-
-// =========================================================================================
-// k_tc_rows: scores, online LSE and dA for 128-row tiles (items = 2 sides x row tiles).
-// =========================================================================================
+template <int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
-    k_tc_rows(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapN, TcArgs g) {
+    k_tc(const __grid_constant__ CUtensorMap mapR, const __grid_constant__ CUtensorMap mapT, TcArgs g) {
     extern __shared__ uint8_t smem_raw[];
     const Smem sm = carve(smem_raw, g.KP);
     uint64_t* bars = sm.bars;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(&bars[B_TMEM_SLOT]);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int KP = g.KP, CB = g.CB;
-    const int row_tiles = (g.nb + RT - 1) / RT;
-    const int n_items = 2 * row_tiles;
-    const int J = (g.nt + NT1 - 1) / NT1;  // negative tiles
-    const int KS = KP / 16;                // k-steps of the score product
-
-    if (threadIdx.x == 0) {
-        init_bars(bars);
-        tc::tmap_prefetch(&mapA);
-        tc::tmap_prefetch(&mapN);
-    }
-    if (warp == 1) tc::tmem_alloc(tslot, TCOLS);
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
-    const uint32_t tbase = *tslot;
-
-    if (warp == 0) {
-        if (lane == 0) {  // ---------------------------------------------------- TMA producer
-            uint32_t it = 0, gn = 0;
-            const uint32_t bytesA = (uint32_t)(RT * KP * 4), bytesN = (uint32_t)(NT1 * KP * 4);
-            for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-                const int side = item / row_tiles, tile = item % row_tiles;
-                tc::mbar_wait(&bars[B_BIG_EMPTY], (it & 1) ^ 1);
-                tc::mbar_expect_tx(&bars[B_BIG_FULL], bytesA);
-                tc::tma_load_4d(sm.big, &mapA, 0, tile * RT, 0, side, &bars[B_BIG_FULL]);
-                for (int j = 0; j < J; ++j, ++gn) {
-                    const int st = gn % NS1;
-                    tc::mbar_wait(&bars[B_RING_EMPTY + st], ((gn / NS1) & 1) ^ 1);
-                    tc::mbar_expect_tx(&bars[B_RING_FULL + st], bytesN);
-                    tc::tma_load_4d(sm.ring[st], &mapN, 0, j * NT1, 0, side, &bars[B_RING_FULL + st]);
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ----------------------------------------------------- MMA issuer
-            const uint32_t id_s = tc::idesc_bf16(128, NT1, false, false);
-            const uint32_t id_pn = tc::idesc_bf16(128, KP, false, true);
-            const uint32_t t_acc = tbase + 2 * NT1;
-            uint32_t it = 0, gn = 0, gs = 0, gp = 0;
-            for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-                tc::mbar_wait(&bars[B_BIG_FULL], it & 1);
-                tc::fence_after();
-                int prev_st = 0;
-                for (int j = 0; j <= J; ++j) {
-                    int st = 0;
-                    if (j < J) {  // S_j = A . N_j^T
-                        st = gn % NS1;
-                        tc::mbar_wait(&bars[B_RING_FULL + st], (gn / NS1) & 1);
-                        const int sb = gs & 1;
-                        tc::mbar_wait(&bars[B_S_EMPTY + sb], ((gs >> 1) & 1) ^ 1);
-                        tc::fence_after();
-                        const uint32_t t_s = tbase + sb * NT1;
-                        const uint8_t* Nt = sm.ring[st];
-                        for (int s = 0; s < KS; ++s) {
-                            const uint64_t ah = kdesc(sm.big, RT, s, 0), al = kdesc(sm.big, RT, s, CB);
-                            const uint64_t nh = kdesc(Nt, NT1, s, 0), nl = kdesc(Nt, NT1, s, CB);
-                            tc::mma_ss(t_s, al, nh, id_s, s > 0 ? 1u : 0u);
-                            tc::mma_ss(t_s, ah, nl, id_s, 1u);
-                            tc::mma_ss(t_s, ah, nh, id_s, 1u);
-                        }
-                        tc::mma_commit(&bars[B_S_FULL + sb]);
-                        ++gs;
-                        ++gn;
-                    }
-                    if (j > 0) {  // dA += P_{j-1} . N_{j-1}
-                        const int pb = gp & 1;
-                        tc::mbar_wait(&bars[B_P_FULL + pb], (gp >> 1) & 1);
-                        if (j == 1) tc::mbar_wait(&bars[B_ACC_EMPTY], (it & 1) ^ 1);
-                        tc::fence_after();
-                        const uint8_t* Nt = sm.ring[prev_st];
-                        const uint8_t* Pt = sm.P[pb];
-                        for (int s = 0; s < NT1 / 16; ++s) {
-                            const uint64_t ph = kdesc(Pt, 128, s, 0), pl = kdesc(Pt, 128, s, 8);
-                            const uint64_t nh = mndesc(Nt, NT1, s, 0), nl = mndesc(Nt, NT1, s, CB);
-                            tc::mma_ss(t_acc, pl, nh, id_pn, (j > 1 || s > 0) ? 1u : 0u);
-                            tc::mma_ss(t_acc, ph, nl, id_pn, 1u);
-                            tc::mma_ss(t_acc, ph, nh, id_pn, 1u);
-                        }
-                        tc::mma_commit(&bars[B_P_EMPTY + pb]);
-                        tc::mma_commit(&bars[B_RING_EMPTY + prev_st]);
-                        ++gp;
-                    }
-                    prev_st = st;
-                }
-                tc::mma_commit(&bars[B_ACC_FULL]);
-                tc::mma_commit(&bars[B_BIG_EMPTY]);
-            }
-        }
-    } else {  // ------------------------------------------------------------------ epilogue
-        const int q = warp & 3;
-        const int r = 32 * q + lane;
-        const uint32_t lane_off = (uint32_t)(32 * q) << 16;
-        const uint32_t t_acc = tbase + 2 * NT1 + lane_off;
-        const float L2E = 1.4426950408889634f;
-        uint32_t it = 0, gs = 0, gp = 0;
-        for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-            const int side = item / row_tiles, tile = item % row_tiles;
-            const int row = tile * RT + r;
-            const bool valid = row < g.nb;
-            const float fp = valid ? g.fpos[row] : 0.f;
-            float m = fp, z = 0.f;
-            for (int j = 0; j < J; ++j) {
-                const int sb = gs & 1;
-                tc::mbar_wait(&bars[B_S_FULL + sb], (gs >> 1) & 1);
-                tc::fence_after();
-                float v[64];
-                ld64(tbase + sb * NT1 + lane_off, v);
-                tc::fence_before();
-                epi_arrive(&bars[B_S_EMPTY + sb]);
-                ++gs;
-                const int k0 = j * NT1;
-                float tm = -INFINITY;
-#pragma unroll
-                for (int c = 0; c < 64; ++c) {
-                    if (k0 + c >= g.nt) v[c] = -INFINITY;
-                    tm = fmaxf(tm, v[c]);
-                }
-                if (j == 0) {
-                    m = fmaxf(m, tm);
-                } else {
-                    const bool need = tm > m + g.tau;
-                    if (__any_sync(0xffffffffu, need)) {
-                        // lazy rescale: wait until P.N of tile j-1 has landed in the accumulator
-                        const uint32_t u = gp - 1;
-                        tc::mbar_wait(&bars[B_P_EMPTY + (u & 1)], (u >> 1) & 1);
-                        tc::fence_after();
-                        const float mn = need ? tm : m;
-                        const float f = __expf(m - mn);
-                        for (int c0 = 0; c0 < KP; c0 += 16) {
-                            uint32_t a[16];
-                            tc::tmem_ld16(t_acc + c0, a);
-                            tc::tmem_ld_wait();
-#pragma unroll
-                            for (int i = 0; i < 16; ++i) a[i] = u32_of(__uint_as_float(a[i]) * f);
-                            tc::tmem_st16(t_acc + c0, a);
-                        }
-                        tc::tmem_st_wait();
-                        z *= f;
-                        m = mn;
-                    }
-                }
-                const float mL = m * L2E;
-#pragma unroll
-                for (int c = 0; c < 64; ++c) {
-                    const float p = exp2f(fmaf(v[c], L2E, -mL));  // 0 for masked columns
-                    v[c] = p;
-                    z += p;
-                }
-                const int pb = gp & 1;
-                tc::mbar_wait(&bars[B_P_EMPTY + pb], ((gp >> 1) & 1) ^ 1);
-                store_p_row(sm.P[pb], r, v);
-                tc::fence_async_smem();
-                tc::fence_before();
-                epi_arrive(&bars[B_P_FULL + pb]);
-                ++gp;
-            }
-            // accumulator epilogue
-            tc::mbar_wait(&bars[B_ACC_FULL], it & 1);
-            tc::fence_after();
-            const float Z = z + __expf(fp - m);
-            const float l = m + __logf(Z);
-            const float scale = g.inv_b / Z;
-            float* out = g.dA + ((size_t)side * g.nb + (valid ? row : 0)) * g.d;
-            for (int c0 = 0; c0 < KP; c0 += 16) {
-                uint32_t a[16];
-                tc::tmem_ld16(t_acc + c0, a);
-                tc::tmem_ld_wait();
-                if (valid) {
-#pragma unroll
-                    for (int i = 0; i < 16; i += 4)
-                        if (c0 + i < g.d)
-                            *reinterpret_cast<float4*>(out + c0 + i) =
-                                make_float4(__uint_as_float(a[i]) * scale, __uint_as_float(a[i + 1]) * scale,
-                                            __uint_as_float(a[i + 2]) * scale, __uint_as_float(a[i + 3]) * scale);
-                }
-            }
-            tc::fence_before();
-            epi_arrive(&bars[B_ACC_EMPTY]);
-            if (valid) {
-                g.lse[(size_t)side * g.nb + row] = l;
-                g.g0[(size_t)side * g.nb + row] = (expf(fp - l) - 1.0f) * g.inv_b;
-            }
-        }
-    }
-    tc::fence_before();
-    __syncthreads();
-    if (warp == 1) tc::tmem_dealloc(tbase, TCOLS);
-}
-
-// =========================================================================================
-// k_tc_negs: dN partials for (side, 128-negative tile, row chunk) items.
-// =========================================================================================
-__device__ __forceinline__ void negs_item(int item, int ntl, int chunks, int nsub, int& side, int& ntile, int& chunk,
-                                          int& u0, int& U) {
-    side = item / (ntl * chunks);
-    const int rem = item % (ntl * chunks);
-    ntile = rem / chunks;
-    chunk = rem % chunks;
-    u0 = (int)((long long)chunk * nsub / chunks);
-    U = (int)((long long)(chunk + 1) * nsub / chunks) - u0;
-}
-
-__global__ void __launch_bounds__(NTHREADS, 1)
-    k_tc_negs(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapN, TcArgs g) {
-    extern __shared__ uint8_t smem_raw[];
-    const Smem sm = carve(smem_raw, g.KP);
-    uint64_t* bars = sm.bars;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(&bars[B_TMEM_SLOT]);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int KP = g.KP, CB = g.CB;
-    const int ntl = g.n_pad / MT2;
-    const int nsub = (g.nb + RS2 - 1) / RS2;
-    const int n_items = 2 * ntl * g.chunks2;
+    const int items = n_items<MODE>(g);
     const int KS = KP / 16;
 
     if (threadIdx.x == 0) {
-        init_bars(bars);
-        tc::tmap_prefetch(&mapA);
-        tc::tmap_prefetch(&mapN);
+        tc::mbar_init(&bars[B_RES_FULL], 1);
+        tc::mbar_init(&bars[B_RES_EMPTY], 128);
+        for (int i = 0; i < NSTAGE; ++i) {
+            tc::mbar_init(&bars[B_RING_FULL + i], 1);
+            tc::mbar_init(&bars[B_RING_EMPTY + i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            tc::mbar_init(&bars[B_S_FULL + i], 1);
+            tc::mbar_init(&bars[B_P_FULL + i], 128);
+            tc::mbar_init(&bars[B_R_READY + i], 128);
+        }
+        tc::mbar_init(&bars[B_ACC_FULL], 1);
+        tc::mbar_init(&bars[B_ACC_EMPTY], 256);
+        tc::fence_mbar_init();
+        tc::tmap_prefetch(&mapR);
+        tc::tmap_prefetch(&mapT);
     }
     if (warp == 1) tc::tmem_alloc(tslot, TCOLS);
     tc::fence_before();
@@ -403,154 +228,255 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t tbase = *tslot;
 
     if (warp == 0) {
-        if (lane == 0) {  // ---------------------------------------------------- TMA producer
-            uint32_t it = 0, ga = 0;
-            const uint32_t bytesN = (uint32_t)(MT2 * KP * 4), bytesA = (uint32_t)(RS2 * KP * 4);
-            for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-                int side, ntile, chunk, u0, U;
-                negs_item(item, ntl, g.chunks2, nsub, side, ntile, chunk, u0, U);
-                if (U == 0) continue;
-                tc::mbar_wait(&bars[B_BIG_EMPTY], (it & 1) ^ 1);
-                tc::mbar_expect_tx(&bars[B_BIG_FULL], bytesN);
-                tc::tma_load_4d(sm.big, &mapN, 0, ntile * MT2, 0, side, &bars[B_BIG_FULL]);
-                for (int u = 0; u < U; ++u, ++ga) {
-                    const int st = ga % NS2;
-                    tc::mbar_wait(&bars[B_RING_EMPTY + st], ((ga / NS2) & 1) ^ 1);
-                    tc::mbar_expect_tx(&bars[B_RING_FULL + st], bytesA);
-                    tc::tma_load_4d(sm.ring[st], &mapA, 0, (u0 + u) * RS2, 0, side, &bars[B_RING_FULL + st]);
+        if (lane == 0) {  // ------------------------------------------------------ TMA producer
+            const uint32_t bytesR = (uint32_t)res_bytes(KP);
+            const uint32_t bytesT = (uint32_t)(TILE * KP * 4) + (MODE == MODE_NEGS ? 256u : 0u);
+            uint32_t it = 0, gt = 0;
+            for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+                const Item I = item_geo<MODE>(g, item);
+                tc::mbar_wait(&bars[B_RES_EMPTY], (it & 1) ^ 1);
+                tc::mbar_expect_tx(&bars[B_RES_FULL], bytesR);
+                tc::tma_load_4d(sm.res, &mapR, 0, I.r0, 0, I.side, &bars[B_RES_FULL]);
+                for (int k = 0; k < I.T; ++k, ++gt) {
+                    const int st = gt % NSTAGE;
+                    tc::mbar_wait(&bars[B_RING_EMPTY + st], ((gt / NSTAGE) & 1) ^ 1);
+                    tc::mbar_expect_tx(&bars[B_RING_FULL + st], bytesT);
+                    uint8_t* dst = sm.stage(st);
+                    const int row = I.t0 + k * TILE;
+                    tc::tma_load_4d(dst, &mapT, 0, row, 0, I.side, &bars[B_RING_FULL + st]);
+                    if (MODE == MODE_NEGS)
+                        tc::bulk_g2s(dst + TILE * KP * 4, g.lse_pad + (size_t)I.side * g.b_cap + row, 256,
+                                     &bars[B_RING_FULL + st]);
                 }
-                ++it;
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ----------------------------------------------------- MMA issuer
-            const uint32_t id_s = tc::idesc_bf16(128, RS2, false, false);
-            const uint32_t id_dn = tc::idesc_bf16(128, KP, false, true);
-            const uint32_t t_acc = tbase + 2 * RS2;
-            uint32_t it = 0, ga = 0, gs = 0, gp = 0;
-            for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-                int side, ntile, chunk, u0, U;
-                negs_item(item, ntl, g.chunks2, nsub, side, ntile, chunk, u0, U);
-                if (U == 0) continue;
-                tc::mbar_wait(&bars[B_BIG_FULL], it & 1);
+        if (lane == 0) {  // ------------------------------------------------------- MMA issuer
+            const uint32_t id_s = tc::idesc_bf16(128, TILE, false, false);
+            const uint32_t id_a = tc::idesc_bf16(128, KP, false, true);
+            const uint32_t t_acc = tbase + T_ACC;
+            uint32_t it = 0, gt = 0;
+            for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+                const Item I = item_geo<MODE>(g, item);
+                tc::mbar_wait(&bars[B_R_READY + (it & 1)], (it >> 1) & 1);
                 tc::fence_after();
+                const uint32_t tR = tbase + T_RES + (it & 1) * 128;
                 int prev_st = 0;
-                for (int u = 0; u <= U; ++u) {
+                for (int k = 0; k <= I.T; ++k) {
                     int st = 0;
-                    if (u < U) {
-                        st = ga % NS2;
-                        tc::mbar_wait(&bars[B_RING_FULL + st], (ga / NS2) & 1);
-                        const int sb = gs & 1;
-                        tc::mbar_wait(&bars[B_S_EMPTY + sb], ((gs >> 1) & 1) ^ 1);
+                    if (k < I.T) {  // S_k = R . T_k^T   (R from TMEM, T_k K-major from smem)
+                        const uint32_t q = gt + k;
+                        st = q % NSTAGE;
+                        tc::mbar_wait(&bars[B_RING_FULL + st], (q / NSTAGE) & 1);
                         tc::fence_after();
-                        const uint32_t t_s = tbase + sb * RS2;
-                        const uint8_t* At = sm.ring[st];
+                        const uint32_t tS = tbase + (q & 1) * 64;
+                        const uint8_t* Tt = sm.stage(st);
                         for (int s = 0; s < KS; ++s) {
-                            const uint64_t nh = kdesc(sm.big, MT2, s, 0), nl = kdesc(sm.big, MT2, s, CB);
-                            const uint64_t ah = kdesc(At, RS2, s, 0), al = kdesc(At, RS2, s, CB);
-                            tc::mma_ss(t_s, nl, ah, id_s, s > 0 ? 1u : 0u);
-                            tc::mma_ss(t_s, nh, al, id_s, 1u);
-                            tc::mma_ss(t_s, nh, ah, id_s, 1u);
+                            const uint32_t rh = tR + s * 8, rl = tR + KP / 2 + s * 8;
+                            const uint64_t th = kdesc(Tt, TILE, s, 0), tl = kdesc(Tt, TILE, s, CB);
+                            tc::mma_ts(tS, rl, th, id_s, s > 0 ? 1u : 0u);
+                            tc::mma_ts(tS, rh, tl, id_s, 1u);
+                            tc::mma_ts(tS, rh, th, id_s, 1u);
                         }
-                        tc::mma_commit(&bars[B_S_FULL + sb]);
-                        ++gs;
-                        ++ga;
+                        tc::mma_commit(&bars[B_S_FULL + (q & 1)]);
                     }
-                    if (u > 0) {  // dN += P^T_{u-1} . A_{u-1}
-                        const int pb = gp & 1;
-                        tc::mbar_wait(&bars[B_P_FULL + pb], (gp >> 1) & 1);
-                        if (u == 1) tc::mbar_wait(&bars[B_ACC_EMPTY], (it & 1) ^ 1);
+                    if (k > 0) {  // acc += P_{k-1} . T_{k-1}   (P from TMEM, T MN-major from smem)
+                        const uint32_t q = gt + k - 1;
+                        tc::mbar_wait(&bars[B_P_FULL + (q & 1)], (q >> 1) & 1);
+                        if (k == 1) tc::mbar_wait(&bars[B_ACC_EMPTY], (it & 1) ^ 1);
                         tc::fence_after();
-                        const uint8_t* At = sm.ring[prev_st];
-                        const uint8_t* Pt = sm.P[pb];
-                        for (int s = 0; s < RS2 / 16; ++s) {
-                            const uint64_t ph = kdesc(Pt, 128, s, 0), pl = kdesc(Pt, 128, s, 8);
-                            const uint64_t ah = mndesc(At, RS2, s, 0), al = mndesc(At, RS2, s, CB);
-                            tc::mma_ss(t_acc, pl, ah, id_dn, (u > 1 || s > 0) ? 1u : 0u);
-                            tc::mma_ss(t_acc, ph, al, id_dn, 1u);
-                            tc::mma_ss(t_acc, ph, ah, id_dn, 1u);
+                        const uint32_t tP = tbase + (q & 1) * 64;
+                        const uint8_t* Tt = sm.stage(prev_st);
+                        for (int s = 0; s < TILE / 16; ++s) {
+                            const uint32_t ph = tP + s * 8, pl = tP + 32 + s * 8;
+                            const uint64_t th = mndesc(Tt, TILE, s, 0), tl = mndesc(Tt, TILE, s, CB);
+                            tc::mma_ts(t_acc, pl, th, id_a, (k > 1 || s > 0) ? 1u : 0u);
+                            tc::mma_ts(t_acc, ph, tl, id_a, 1u);
+                            tc::mma_ts(t_acc, ph, th, id_a, 1u);
                         }
-                        tc::mma_commit(&bars[B_P_EMPTY + pb]);
                         tc::mma_commit(&bars[B_RING_EMPTY + prev_st]);
-                        ++gp;
                     }
                     prev_st = st;
                 }
                 tc::mma_commit(&bars[B_ACC_FULL]);
-                tc::mma_commit(&bars[B_BIG_EMPTY]);
-                ++it;
+                gt += I.T;
             }
         }
-    } else {  // ------------------------------------------------------------------ epilogue
-        const int q = warp & 3;
-        const int n = 32 * q + lane;  // negative within the tile
-        const uint32_t lane_off = (uint32_t)(32 * q) << 16;
-        const uint32_t t_acc = tbase + 2 * RS2 + lane_off;
-        const float L2E = 1.4426950408889634f;
-        const float log2_inv_b = log2f(g.inv_b);
-        uint32_t it = 0, gs = 0, gp = 0;
-        for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-            int side, ntile, chunk, u0, U;
-            negs_item(item, ntl, g.chunks2, nsub, side, ntile, chunk, u0, U);
-            float* out = g.dN_part + (((size_t)chunk * 2 + side) * g.n_pad + (size_t)ntile * MT2 + n) * g.d;
-            if (U == 0) {
-                for (int c = 0; c < g.d; c += 4) *reinterpret_cast<float4*>(out + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-                continue;
-            }
-            const float* lse = g.lse + (size_t)side * g.nb;
-            for (int u = 0; u < U; ++u) {
-                const int sb = gs & 1;
-                tc::mbar_wait(&bars[B_S_FULL + sb], (gs >> 1) & 1);
+    } else {  // -------------------------------------------------------------------- epilogue
+        const int G = (warp - 2) >> 2;          // ping-pong group: takes streamed tiles with q % 2 == G
+        const int qd = warp & 3;                // TMEM lane quadrant
+        const int r = 32 * qd + lane;           // resident row (MODE_ROWS: batch row; NEGS: negative)
+        const uint32_t t_row = tbase + ((uint32_t)(32 * qd) << 16);
+        const int nch = KP / 16, half = (nch + 1) / 2;
+        const int c_lo = G == 0 ? 0 : half, c_hi = G == 0 ? half : nch;
+        uint32_t it = 0, gt = 0;
+        if (G == 0 && (int)blockIdx.x < items) stage_resident(sm, bars, CB, 0, r, t_row);
+        for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+            const Item I = item_geo<MODE>(g, item);
+            const int row = I.r0 + r;
+            float fp = 0.f, z = 0.f;
+            if (MODE == MODE_ROWS) fp = row < g.nb ? g.fpos[row] : 0.f;
+            const float cshift = -fp * L2E;
+            for (int k = 0; k < I.T; ++k) {
+                const uint32_t q = gt + k;
+                if ((int)(q & 1) != G) continue;
+                const uint32_t tS = t_row + (q & 1) * 64;
+                const int st = q % NSTAGE;
+                if (MODE == MODE_NEGS) tc::mbar_wait(&bars[B_RING_FULL + st], (q / NSTAGE) & 1);
+                tc::mbar_wait(&bars[B_S_FULL + (q & 1)], (q >> 1) & 1);
                 tc::fence_after();
                 float v[64];
-                ld64(tbase + sb * RS2 + lane_off, v);
-                tc::fence_before();
-                epi_arrive(&bars[B_S_EMPTY + sb]);
-                ++gs;
-                const int row0 = (u0 + u) * RS2;
+                {
+                    uint32_t a[32], b[32];
+                    tc::tmem_ld32(tS, a);
+                    tc::tmem_ld32(tS + 32, b);
+                    tc::tmem_ld_wait();
 #pragma unroll
-                for (int c = 0; c < 64; ++c) {
-                    const int row = row0 + c;
-                    // P^T = exp(S - lse) / b, folded into one exp2; rows past the batch -> 0
-                    const float l = row < g.nb ? __ldg(lse + row) : INFINITY;
-                    v[c] = exp2f(fmaf(v[c], L2E, fmaf(-l, L2E, log2_inv_b)));
+                    for (int i = 0; i < 32; ++i) {
+                        v[i] = __uint_as_float(a[i]);
+                        v[32 + i] = __uint_as_float(b[i]);
+                    }
                 }
-                const int pb = gp & 1;
-                tc::mbar_wait(&bars[B_P_EMPTY + pb], ((gp >> 1) & 1) ^ 1);
-                store_p_row(sm.P[pb], n, v);
-                tc::fence_async_smem();
+                if (MODE == MODE_ROWS) {
+                    const int k0 = k * TILE;
+                    if (k0 + TILE <= g.nt) {
+#pragma unroll
+                        for (int c = 0; c < 64; ++c) {
+                            v[c] = exp2f(fmaf(v[c], L2E, cshift));
+                            z += v[c];
+                        }
+                    } else {  // last tile: negatives past n_t contribute nothing
+#pragma unroll
+                        for (int c = 0; c < 64; ++c) {
+                            v[c] = (k0 + c < g.nt) ? exp2f(fmaf(v[c], L2E, cshift)) : 0.f;
+                            z += v[c];
+                        }
+                    }
+                } else {
+                    const float4* L = reinterpret_cast<const float4*>(sm.stage(st) + TILE * KP * 4);
+#pragma unroll
+                    for (int c4 = 0; c4 < 16; ++c4) {
+                        const float4 l = L[c4];  // broadcast; +inf past the batch -> P = 0
+                        v[4 * c4 + 0] = exp2f(fmaf(v[4 * c4 + 0], L2E, fmaf(-l.x, L2E, g.log2_inv_b)));
+                        v[4 * c4 + 1] = exp2f(fmaf(v[4 * c4 + 1], L2E, fmaf(-l.y, L2E, g.log2_inv_b)));
+                        v[4 * c4 + 2] = exp2f(fmaf(v[4 * c4 + 2], L2E, fmaf(-l.z, L2E, g.log2_inv_b)));
+                        v[4 * c4 + 3] = exp2f(fmaf(v[4 * c4 + 3], L2E, fmaf(-l.w, L2E, g.log2_inv_b)));
+                    }
+                }
+                uint32_t hi[32], lo[32];
+                split64(v, hi, lo);
+                tc::tmem_st32(tS, hi);  // P overwrites S in place: hi pairs, then lo pairs
+                tc::tmem_st32(tS + 32, lo);
+                tc::tmem_st_wait();
                 tc::fence_before();
-                epi_arrive(&bars[B_P_FULL + pb]);
-                ++gp;
+                tc::mbar_arrive(&bars[B_P_FULL + (q & 1)]);
             }
+            // group 0 stages the next item's resident operand while the tail of this one drains
+            if (G == 0 && item + (int)gridDim.x < items) stage_resident(sm, bars, CB, it + 1, r, t_row);
             tc::mbar_wait(&bars[B_ACC_FULL], it & 1);
             tc::fence_after();
-            for (int c0 = 0; c0 < KP; c0 += 16) {
-                uint32_t a[16];
-                tc::tmem_ld16(t_acc + c0, a);
-                tc::tmem_ld_wait();
+            if (MODE == MODE_ROWS) {
+                float* zb = sm.zbuf + (it & 1) * 256;
+                zb[G * 128 + r] = z;
+                epi_sync();
+                const float Z = 1.0f + zb[r] + zb[128 + r];  // exp(f_pos - f_pos) = 1: the positive
+                const bool valid = row < g.nb;
+                const float lse = fp + __logf(Z);
+                const bool bad = !(Z < g.zmax);
+                const float scale = g.inv_b / Z;
+                float* out = g.dA + ((size_t)I.side * g.nb + (valid ? row : 0)) * g.d;
+                for (int c = c_lo; c < c_hi; ++c) {
+                    uint32_t a[16];
+                    tc::tmem_ld16(t_row + T_ACC + 16 * c, a);
+                    tc::tmem_ld_wait();
+                    if (valid) {
 #pragma unroll
-                for (int i = 0; i < 16; i += 4)
-                    if (c0 + i < g.d)
-                        *reinterpret_cast<float4*>(out + c0 + i) = make_float4(
-                            __uint_as_float(a[i]), __uint_as_float(a[i + 1]), __uint_as_float(a[i + 2]),
-                            __uint_as_float(a[i + 3]));
+                        for (int i = 0; i < 16; i += 4)
+                            if (16 * c + i < g.d)
+                                *reinterpret_cast<float4*>(out + 16 * c + i) =
+                                    make_float4(__uint_as_float(a[i]) * scale, __uint_as_float(a[i + 1]) * scale,
+                                                __uint_as_float(a[i + 2]) * scale, __uint_as_float(a[i + 3]) * scale);
+                    }
+                }
+                if (G == 0) {
+                    if (valid) {
+                        g.lse[(size_t)I.side * g.nb + row] = lse;
+                        g.g0[(size_t)I.side * g.nb + row] = (__expf(fp - lse) - 1.0f) * g.inv_b;
+                        if (bad) g.flags[1 + atomicAdd(g.flags, 1u)] = (uint32_t)(I.side * g.b_cap + row);
+                    }
+                    g.lse_pad[(size_t)I.side * g.b_cap + row] = valid ? lse : INFINITY;
+                }
+            } else {
+                float* out = g.dN_part + (((size_t)I.chunk * 2 + I.side) * g.n_pad + row) * g.d;
+                for (int c = c_lo; c < c_hi; ++c) {
+                    uint32_t a[16];
+                    tc::tmem_ld16(t_row + T_ACC + 16 * c, a);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 16; i += 4)
+                        if (16 * c + i < g.d)
+                            *reinterpret_cast<float4*>(out + 16 * c + i) = make_float4(
+                                __uint_as_float(a[i]), __uint_as_float(a[i + 1]), __uint_as_float(a[i + 2]),
+                                __uint_as_float(a[i + 3]));
+                }
             }
             tc::fence_before();
-            epi_arrive(&bars[B_ACC_EMPTY]);
-            ++it;
+            tc::mbar_arrive(&bars[B_ACC_EMPTY]);
+            gt += I.T;
         }
     }
     tc::fence_before();
     __syncthreads();
     if (warp == 1) tc::tmem_dealloc(tbase, TCOLS);
+}
+
+// Exact two-pass recomputation (fp32, CUDA cores) of the rows k_tc<MODE_ROWS> flagged because
+// sum exp(S - f_pos) left the safe range (a negative scoring > f_pos + ~55). One block; normally
+// the list is empty and the kernel exits at once. Resets the list for the next step.
+__global__ void k_tc_fixup(TcArgs g, const float* __restrict__ A, const float* __restrict__ N) {
+    const uint32_t n = *(volatile uint32_t*)g.flags;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (uint32_t f = warp; f < n; f += nw) {
+        const uint32_t code = g.flags[1 + f];
+        const int side = (int)(code / g.b_cap), row = (int)(code % g.b_cap);
+        const float* a = A + ((size_t)side * g.nb + row) * g.d;
+        const float* Nn = N + (size_t)side * g.nt * g.d;
+        const float fp = g.fpos[row];
+        float mx = fp;
+        for (int k = 0; k < g.nt; ++k) {
+            float s = 0.f;
+            for (int c = lane; c < g.d; c += 32) s += a[c] * Nn[(size_t)k * g.d + c];
+            for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            mx = fmaxf(mx, s);
+        }
+        float z = expf(fp - mx), acc[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int k = 0; k < g.nt; ++k) {
+            float s = 0.f;
+            for (int c = lane; c < g.d; c += 32) s += a[c] * Nn[(size_t)k * g.d + c];
+            for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            const float p = expf(s - mx);
+            z += p;
+            for (int c = lane, i = 0; c < g.d; c += 32, ++i) acc[i] += p * Nn[(size_t)k * g.d + c];
+        }
+        const float lse = mx + logf(z);
+        const float scale = g.inv_b / z;
+        float* out = g.dA + ((size_t)side * g.nb + row) * g.d;
+        for (int c = lane, i = 0; c < g.d; c += 32, ++i) out[c] = acc[i] * scale;
+        if (lane == 0) {
+            g.lse[(size_t)side * g.nb + row] = lse;
+            g.lse_pad[(size_t)side * g.b_cap + row] = lse;
+            g.g0[(size_t)side * g.nb + row] = (expf(fp - lse) - 1.0f) * g.inv_b;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && n) *g.flags = 0u;
 }
 
 // =========================================================================================
 // Operand packing and the dN reduction (memory-bound helpers).
 // =========================================================================================
 
-// src [2 sides][rows][d] fp32 (side stride side_stride rows) -> dst [2][2CB][cap][8] bf16 hi|lo.
+// src [2 sides][rows][d] fp32 (side stride side_stride floats) -> dst [2][2CB][cap][8] bf16 hi|lo.
 // One thread per (side, cb, row); rows in [0, rows_pad) (zero past `rows`).
 __global__ void k_pack(const float* __restrict__ src, uint64_t side_stride, int rows, int rows_pad, int cap, int d,
                        int CB, uint16_t* __restrict__ dst) {
@@ -624,8 +550,10 @@ struct TcState {
     uint16_t* A = nullptr;   // [2][2CB][b_cap][8]
     uint16_t* N = nullptr;   // [2][2CB][n_pad][8]
     float* dN_part = nullptr;
+    float* lse_pad = nullptr;
+    uint32_t* flags = nullptr;
     CUtensorMap mA128, mA64, mN64, mN128;
-    float tau = 30.f;
+    float zmax = 1e24f;
 };
 
 bool tc_engine_supported(const Engine& E) {
@@ -639,21 +567,24 @@ void tc_setup(Engine& E) {
     auto* t = new TcState();
     t->KP = (int)((E.dim + 15) / 16 * 16);
     t->CB = t->KP / 8;
-    t->b_cap = (int)((E.cap_b + RT - 1) / RT * RT);
-    t->n_pad = (int)((E.nt + MT2 - 1) / MT2 * MT2);
-    const int ntl = t->n_pad / MT2;
+    t->b_cap = (int)((E.cap_b + RES - 1) / RES * RES);
+    t->n_pad = (int)((E.nt + RES - 1) / RES * RES);
+    const int ntl = t->n_pad / RES;
     t->chunks2 = std::max(1, E.sm_count / (2 * ntl));
-    if (const char* s = getenv("EMBER_TC_TAU")) t->tau = (float)atof(s);
+    if (const char* s = getenv("EMBER_TC_ZMAX")) t->zmax = (float)atof(s);  // test hook: 0 flags every row
     EMBER_CUDA(cudaMalloc(&t->A, (size_t)2 * 2 * t->CB * t->b_cap * 16));
     EMBER_CUDA(cudaMalloc(&t->N, (size_t)2 * 2 * t->CB * t->n_pad * 16));
     EMBER_CUDA(cudaMalloc(&t->dN_part, (size_t)t->chunks2 * 2 * t->n_pad * E.dim * sizeof(float)));
-    t->mA128 = make_map(t->A, t->b_cap, t->CB, RT);
-    t->mA64 = make_map(t->A, t->b_cap, t->CB, RS2);
-    t->mN64 = make_map(t->N, t->n_pad, t->CB, NT1);
-    t->mN128 = make_map(t->N, t->n_pad, t->CB, MT2);
+    EMBER_CUDA(cudaMalloc(&t->lse_pad, (size_t)2 * t->b_cap * sizeof(float)));
+    EMBER_CUDA(cudaMalloc(&t->flags, (size_t)(1 + 2 * t->b_cap) * sizeof(uint32_t)));
+    EMBER_CUDA(cudaMemset(t->flags, 0, sizeof(uint32_t)));
+    t->mA128 = make_map(t->A, t->b_cap, t->CB, RES);
+    t->mA64 = make_map(t->A, t->b_cap, t->CB, TILE);
+    t->mN64 = make_map(t->N, t->n_pad, t->CB, TILE);
+    t->mN128 = make_map(t->N, t->n_pad, t->CB, RES);
     const size_t smem = smem_total(t->KP);
-    EMBER_CUDA(cudaFuncSetAttribute(k_tc_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    EMBER_CUDA(cudaFuncSetAttribute(k_tc_negs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    EMBER_CUDA(cudaFuncSetAttribute(k_tc<MODE_ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    EMBER_CUDA(cudaFuncSetAttribute(k_tc<MODE_NEGS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     E.tc = t;
 }
 
@@ -662,6 +593,8 @@ void tc_release(Engine& E) {
     cudaFree(E.tc->A);
     cudaFree(E.tc->N);
     cudaFree(E.tc->dN_part);
+    cudaFree(E.tc->lse_pad);
+    cudaFree(E.tc->flags);
     delete E.tc;
     E.tc = nullptr;
 }
@@ -670,7 +603,7 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
     TcState& t = *E.tc;
     const int d = (int)E.dim, nt = (int)E.nt;
     Scratch& s = E.s;
-    const int rows_pad = (int)((nb + RT - 1) / RT * RT);
+    const int rows_pad = (int)((nb + RES - 1) / RES * RES);
     {
         const int64_t n = (int64_t)2 * t.CB * rows_pad;
         k_pack<<<(unsigned)((n + 255) / 256), 256, 0, E.stream>>>(s.A, (uint64_t)nb * d, (int)nb, rows_pad, t.b_cap, d,
@@ -688,21 +621,27 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
     a.nb = (int)nb;
     a.nt = nt;
     a.n_pad = t.n_pad;
+    a.b_cap = t.b_cap;
     a.inv_b = 1.0f / (float)nb;
-    a.tau = t.tau;
+    a.log2_inv_b = log2f(a.inv_b);
+    a.zmax = t.zmax;
     a.fpos = s.fpos;
     a.lse = s.lse;
+    a.lse_pad = t.lse_pad;
     a.g0 = s.g0;
     a.dA = s.dA;
     a.dN_part = t.dN_part;
-    const int nsub = (int)((nb + RS2 - 1) / RS2);
+    a.flags = t.flags;
+    const int nsub = (int)((nb + TILE - 1) / TILE);
     a.chunks2 = std::min(t.chunks2, nsub);
     const size_t smem = smem_total(t.KP);
-    const int items1 = 2 * (rows_pad / RT);
-    k_tc_rows<<<std::min(items1, E.sm_count), NTHREADS, smem, E.stream>>>(t.mA128, t.mN64, a);
+    const int items1 = 2 * (rows_pad / RES);
+    k_tc<MODE_ROWS><<<std::min(items1, E.sm_count), NTHREADS, smem, E.stream>>>(t.mA128, t.mN64, a);
     EMBER_LAUNCHED(E);
-    const int items2 = 2 * (t.n_pad / MT2) * a.chunks2;
-    k_tc_negs<<<std::min(items2, E.sm_count), NTHREADS, smem, E.stream>>>(t.mA64, t.mN128, a);
+    k_tc_fixup<<<1, 1024, 0, E.stream>>>(a, s.A, s.N);
+    EMBER_LAUNCHED(E);
+    const int items2 = 2 * (t.n_pad / RES) * a.chunks2;
+    k_tc<MODE_NEGS><<<std::min(items2, E.sm_count), NTHREADS, smem, E.stream>>>(t.mN128, t.mA64, a);
     EMBER_LAUNCHED(E);
     const int64_t r = (int64_t)2 * nt * d;
     k_dn_reduce<<<(unsigned)((r + 255) / 256), 256, 0, E.stream>>>(t.dN_part, a.chunks2, nt, t.n_pad, d,

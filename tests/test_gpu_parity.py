@@ -159,15 +159,15 @@ def test_eval_ranks_match_oracle(graph):
     assert abs(a["mrr"] - b["mrr"]) < 1e-3
 
 
-@pytest.mark.parametrize("kind,dim,nt,nb,tau", [("complex", 100, 1000, 3000, None), ("dot", 100, 1000, 1500, None),
+@pytest.mark.parametrize("kind,dim,nt,nb,zmax", [("complex", 100, 1000, 3000, None), ("dot", 100, 1000, 1500, None),
                                               ("distmult", 40, 100, 333, None), ("complex", 64, 200, 700, "0"),
                                               ("distmult", 128, 300, 1000, None), ("complex", 16, 17, 5, None)])
-def test_tc_engine_headline_shapes(graph, monkeypatch, kind, dim, nt, nb, tau):
+def test_tc_engine_headline_shapes(graph, monkeypatch, kind, dim, nt, nb, zmax):
     """Tensor-core contraction at the headline d=100 / n_t=1000 shape (smaller b), ragged tiles
-    (nb, n_t not multiples of the 128/64 tiles), d at the 128 limit, and tau=0 (the lazy-rescale
-    path taken on every negative tile) — all within 1e-4 of the oracle."""
-    if tau is not None:
-        monkeypatch.setenv("EMBER_TC_TAU", tau)
+    (nb, n_t not multiples of the 128/64 tiles), d at the 128 limit, and zmax=0 (every row sent
+    through the exact overflow fixup, k_tc_fixup) — all within 1e-4 of the oracle."""
+    if zmax is not None:
+        monkeypatch.setenv("EMBER_TC_ZMAX", zmax)
     edges, off, _ = graph
     tr = make_trainer(kind, dim=dim, b=max(nb, 16), nt=nt, p=2, engine="tc")
     th, _, rt, _ = host_tables(tr)
