@@ -225,7 +225,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
+    // All 512 columns belong to this CTA (one CTA per SM), so the allocation starts at lane 0,
+    // column 0: the MMA issuer uses compile-time TMEM addresses.
     const uint32_t tbase = *tslot;
+    if (tbase != 0) __trap();
 
     if (warp == 0) {
         if (lane == 0) {  // ------------------------------------------------------ TMA producer
@@ -250,57 +253,58 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
             }
         }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ------------------------------------------------------- MMA issuer
-            const uint32_t id_s = tc::idesc_bf16(128, TILE, false, false);
-            const uint32_t id_a = tc::idesc_bf16(128, KP, false, true);
-            const uint32_t t_acc = tbase + T_ACC;
-            uint32_t it = 0, gt = 0;
-            for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
-                const Item I = item_geo<MODE>(g, item);
-                tc::mbar_wait(&bars[B_R_READY + (it & 1)], (it >> 1) & 1);
-                tc::fence_after();
-                const uint32_t tR = tbase + T_RES + (it & 1) * 128;
-                int prev_st = 0;
-                for (int k = 0; k <= I.T; ++k) {
-                    int st = 0;
-                    if (k < I.T) {  // S_k = R . T_k^T   (R from TMEM, T_k K-major from smem)
-                        const uint32_t q = gt + k;
-                        st = q % NSTAGE;
-                        tc::mbar_wait(&bars[B_RING_FULL + st], (q / NSTAGE) & 1);
-                        tc::fence_after();
-                        const uint32_t tS = tbase + (q & 1) * 64;
-                        const uint8_t* Tt = sm.stage(st);
-                        for (int s = 0; s < KS; ++s) {
-                            const uint32_t rh = tR + s * 8, rl = tR + KP / 2 + s * 8;
-                            const uint64_t th = kdesc(Tt, TILE, s, 0), tl = kdesc(Tt, TILE, s, CB);
-                            tc::mma_ts(tS, rl, th, id_s, s > 0 ? 1u : 0u);
-                            tc::mma_ts(tS, rh, tl, id_s, 1u);
-                            tc::mma_ts(tS, rh, th, id_s, 1u);
-                        }
-                        tc::mma_commit(&bars[B_S_FULL + (q & 1)]);
+    } else if (warp == 1) {  // ------------------------------------------------- MMA issuer
+        // The whole warp runs this loop converged (all values warp-uniform, held in uniform
+        // registers); one elected lane issues each tcgen05 instruction.
+        const uint32_t id_s = tc::idesc_bf16(128, TILE, false, false);
+        const uint32_t id_a = tc::idesc_bf16(128, KP, false, true);
+        uint32_t it = 0, gt = 0;
+        for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+            const Item I = item_geo<MODE>(g, item);
+            tc::mbar_wait(&bars[B_R_READY + (it & 1)], (it >> 1) & 1);
+            tc::fence_after();
+            const uint32_t tR = T_RES + (it & 1) * 128;
+            int prev_st = 0;
+            for (int k = 0; k <= I.T; ++k) {
+                int st = 0;
+                if (k < I.T) {  // S_k = R . T_k^T   (R from TMEM, T_k K-major from smem)
+                    const uint32_t q = gt + k;
+                    st = q % NSTAGE;
+                    tc::mbar_wait(&bars[B_RING_FULL + st], (q / NSTAGE) & 1);
+                    tc::fence_after();
+                    const uint32_t tS = (q & 1) * 64;
+                    const uint64_t t0 = kdesc(sm.stage(st), TILE, 0, 0);
+                    const uint64_t lo_off = (uint64_t)((CB * TILE * 16) >> 4);
+                    for (int s = 0; s < KS; ++s) {
+                        const uint32_t rh = tR + s * 8, rl = tR + KP / 2 + s * 8;
+                        const uint64_t th = t0 + (uint64_t)((2 * s * TILE * 16) >> 4), tl = th + lo_off;
+                        tc::mma_ts_elect(tS, rl, th, id_s, s > 0 ? 1u : 0u);
+                        tc::mma_ts_elect(tS, rh, tl, id_s, 1u);
+                        tc::mma_ts_elect(tS, rh, th, id_s, 1u);
                     }
-                    if (k > 0) {  // acc += P_{k-1} . T_{k-1}   (P from TMEM, T MN-major from smem)
-                        const uint32_t q = gt + k - 1;
-                        tc::mbar_wait(&bars[B_P_FULL + (q & 1)], (q >> 1) & 1);
-                        if (k == 1) tc::mbar_wait(&bars[B_ACC_EMPTY], (it & 1) ^ 1);
-                        tc::fence_after();
-                        const uint32_t tP = tbase + (q & 1) * 64;
-                        const uint8_t* Tt = sm.stage(prev_st);
-                        for (int s = 0; s < TILE / 16; ++s) {
-                            const uint32_t ph = tP + s * 8, pl = tP + 32 + s * 8;
-                            const uint64_t th = mndesc(Tt, TILE, s, 0), tl = mndesc(Tt, TILE, s, CB);
-                            tc::mma_ts(t_acc, pl, th, id_a, (k > 1 || s > 0) ? 1u : 0u);
-                            tc::mma_ts(t_acc, ph, tl, id_a, 1u);
-                            tc::mma_ts(t_acc, ph, th, id_a, 1u);
-                        }
-                        tc::mma_commit(&bars[B_RING_EMPTY + prev_st]);
-                    }
-                    prev_st = st;
+                    tc::mma_commit_elect(&bars[B_S_FULL + (q & 1)]);
                 }
-                tc::mma_commit(&bars[B_ACC_FULL]);
-                gt += I.T;
+                if (k > 0) {  // acc += P_{k-1} . T_{k-1}   (P from TMEM, T MN-major from smem)
+                    const uint32_t q = gt + k - 1;
+                    tc::mbar_wait(&bars[B_P_FULL + (q & 1)], (q >> 1) & 1);
+                    if (k == 1) tc::mbar_wait(&bars[B_ACC_EMPTY], (it & 1) ^ 1);
+                    tc::fence_after();
+                    const uint32_t tP = (q & 1) * 64;
+                    const uint64_t t0 = mndesc(sm.stage(prev_st), TILE, 0, 0);
+                    const uint64_t lo_off = (uint64_t)((CB * TILE * 16) >> 4);
+                    for (int s = 0; s < TILE / 16; ++s) {
+                        const uint32_t ph = tP + s * 8, pl = tP + 32 + s * 8;
+                        const uint64_t th = t0 + (uint64_t)((s * 256) >> 4), tl = th + lo_off;
+                        tc::mma_ts_elect(T_ACC, pl, th, id_a, (k > 1 || s > 0) ? 1u : 0u);
+                        tc::mma_ts_elect(T_ACC, ph, tl, id_a, 1u);
+                        tc::mma_ts_elect(T_ACC, ph, th, id_a, 1u);
+                    }
+                    tc::mma_commit_elect(&bars[B_RING_EMPTY + prev_st]);
+                }
+                prev_st = st;
             }
+            tc::mma_commit_elect(&bars[B_ACC_FULL]);
+            gt += I.T;
         }
     } else {  // -------------------------------------------------------------------- epilogue
         const int G = (warp - 2) >> 2;          // ping-pong group: takes streamed tiles with q % 2 == G
