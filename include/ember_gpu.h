@@ -175,6 +175,10 @@ int ember_profile_read(ember_ctx* ctx, double* ms_out, uint64_t* launches_out, u
 /* Self-test of the tcgen05 building blocks on `device` (one 128 x N x K bf16 product vs a double
  * host product); max_rel_err_out = max|err| / max|ref|. mode: see csrc/tc_selftest.cu. */
 int ember_tc_selftest(int device, int mode, int K, int N, uint64_t seed, double* max_rel_err_out);
+/* Microbenchmark: cycles per back-to-back tcgen05.mma (M=128, K=16, bf16, N columns) issued by one
+ * thread. mode %16: 0 SS, 1 TS (A in TMEM), 2 TS with MN-major B, 3 SS with MN-major B; mode / 16 + 1
+ * independent accumulators are cycled round-robin (N * count <= 256 columns). */
+int ember_tc_mmabench(int device, int mode, int N, int iters, double* cycles_per_mma);
 
 /* ---- multi-GPU------------------------------------------------------------ */
 /* nccl_unique_id: 128 bytes (ncclUniqueId) shared by all ranks. NCCL is loaded at run time. */

@@ -71,6 +71,7 @@ def _declare(L):
         "ember_graph_generate": (C.c_int, [i32, u64, u32, u64, u64, f32, f32, vp, vp]),
         "ember_graph_bucket": (C.c_int, [i32, u64, u32, vp, u64, vp, vp]),
         "ember_tc_selftest": (C.c_int, [i32, i32, i32, i32, u64, C.POINTER(C.c_double)]),
+        "ember_tc_mmabench": (C.c_int, [i32, i32, i32, i32, C.POINTER(C.c_double)]),
         "ember_profile_enable": (C.c_int, [vp, i32]),
         "ember_profile_read": (C.c_int, [vp, vp, C.POINTER(u64), C.POINTER(u64)]),
         "ember_comm_init": (C.c_int, [vp, vp, i32, i32]),

@@ -18,6 +18,7 @@ void graph_generate(int device, uint64_t V, uint32_t R, uint64_t n, uint64_t see
 void graph_bucket(int device, uint64_t V, uint32_t p, const uint32_t* in, uint64_t n, uint32_t* out,
                   uint64_t* offsets);
 double tc_selftest(int device, int mode, int K, int N, uint64_t seed);
+double tc_mmabench(int device, int mode, int N, int iters, int nacc);
 void launch_eval(const Engine& E, const uint32_t* test, uint32_t n_test, const uint32_t* train, uint64_t n_train,
                  uint32_t n_eval, float alpha_eval, uint32_t block, uint64_t eval_seed, uint32_t* ranks);
 }  // namespace ember
@@ -319,6 +320,14 @@ int ember_tc_selftest(int device, int mode, int K, int N, uint64_t seed, double*
     return guarded([&] {
         need(err, "max_rel_err_out");
         *err = tc_selftest(device, mode, K, N, seed);
+    });
+}
+
+int ember_tc_mmabench(int device, int mode, int N, int iters, double* cycles_per_mma) {
+    return guarded([&] {
+        need(cycles_per_mma, "cycles_per_mma");
+        if (N % 16 || N < 16 || N > 256 || iters < 1) throw ConfigError("mmabench: N multiple of 16 in [16, 256]");
+        *cycles_per_mma = tc_mmabench(device, mode % 16, N, iters, mode / 16 + 1);
     });
 }
 

@@ -55,6 +55,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
+// Warp-uniform wait for a converged warp: the exit condition is a warp vote, so ptxas keeps the
+// code after it in uniform control flow (descriptor math stays in uniform registers).
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_addr(bar);
+    uint32_t n = 0;
+    while (!__all_sync(0xffffffffu, mbar_try(a, parity))) {
+        if (++n == (1u << 24)) __trap();
+    }
+}
+
 // ---- TMA tensor copies (cp.async.bulk.tensor, tensor map in kernel-param space) -------------
 __device__ __forceinline__ void tmap_prefetch(const void* tmap) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
@@ -175,6 +185,14 @@ __device__ __forceinline__ void mma_ts_elect(uint32_t d_tmem, uint32_t a_tmem, u
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+__device__ __forceinline__ void mma_ss_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate) {
+    asm volatile(
+        "{ .reg .pred p, e; elect.sync _|e, 0xffffffff; setp.ne.b32 p, %4, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
 __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
     asm volatile(
         "{ .reg .pred e; elect.sync _|e, 0xffffffff;\n"
@@ -199,6 +217,13 @@ __device__ __forceinline__ uint32_t pack2(uint16_t lo_k, uint16_t hi_k) {
     return static_cast<uint32_t>(lo_k) | (static_cast<uint32_t>(hi_k) << 16);
 }
 
+// 2^x on the SFU, one MUFU.EX2 (flushes results below 2^-126 to zero; callers only feed it
+// log-probabilities, for which such terms are far below fp32 resolution of the row sums).
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 // Two fp32 -> packed bf16 pair (element 2i in the low half).
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo_k, float hi_k) {
     const __nv_bfloat162 v = __floats2bfloat162_rn(lo_k, hi_k);

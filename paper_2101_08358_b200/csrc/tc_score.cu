@@ -10,29 +10,33 @@
 // relative per product — inside the 1e-4 per-step tolerance of the north_star.
 //
 // Operand layout in HBM (written by k_pack): per side, [2*CB column blocks][rows][8 bf16],
-// CB = KP/8 (KP = dim rounded up to 16), hi blocks then lo blocks. Any row range is one TMA
-// box {8, R, 2CB} that lands in shared memory as the canonical no-swizzle K-major UMMA tile
-// [cb][R][16 B] (tc_common.cuh); the same bytes are the MN-major operand of the transposed
-// product.
+// CB = KP/8 (KP = dim rounded up to 16), hi blocks then lo blocks. A 128-row range is one TMA box
+// that lands in shared memory as the canonical no-swizzle K-major UMMA tile [cb][128][16 B]
+// (tc_common.cuh); the same bytes are the MN-major operand of the transposed product.
 //
 // One kernel template, two modes, per side (A = adjusted vectors [nb x d], N = shared
 // negatives [nt x d], b = nb):
-//   MODE_ROWS  item = 128-row tile of A (resident), streamed over 64-negative tiles of N:
+//   MODE_ROWS  item = 128-row tile of A (resident), streamed over 128-negative tiles of N:
 //              S = A N^T, P = exp(S - f_pos) (the positive's score is the fixed row shift: it
 //              is part of every row's log-sum-exp, so no online rescaling is needed), dA += P N.
 //              Item end: lse = f_pos + log(1 + sum P), g0 = (exp(f_pos - lse) - 1)/b, dA/(Z b).
 //              Rows whose sum overflows the safe range are listed and recomputed exactly by
 //              k_tc_fixup before anything reads lse.
-//   MODE_NEGS  item = 128-negative tile of N (resident) x a chunk of 64-row tiles of A:
+//   MODE_NEGS  item = 128-negative tile of N (resident) x a chunk of 128-row tiles of A:
 //              S^T = N A^T, P^T = exp(S^T - lse)/b, dN += P^T A; per-chunk partials are summed
 //              in a fixed order by k_dn_reduce (deterministic).
-// TMEM (512 columns): [0,128) two 64-column S buffers, each overwritten in place by P as bf16
-// hi|lo pairs (the A operand of the second product, TS mode); [128,128+KP) the accumulator;
-// [256,384) / [384,512) the double-buffered resident operand (hi|lo pairs), so every MMA reads
-// only its B operand from shared memory.
-// Warps: 0 = TMA producer, 1 = TMEM owner + MMA issuer (one thread), 2..9 = two epilogue
-// warpgroups that take alternate streamed tiles (ping-pong); group 0 also stages the next
-// item's resident operand smem -> TMEM.
+// TMEM (512 columns): [0,128) and [128,256) two S buffers of 128 fp32 columns, each overwritten
+// in place by P as bf16 pairs (per 64-column half: 32 hi columns then 32 lo columns) — the A
+// operand of the second product (TS mode); [256,256+KP) the accumulator; [384,384+KP) the
+// resident operand (hi|lo pairs), copied smem -> TMEM by tcgen05.cp in the MMA pipe, so every
+// MMA reads only its B operand from shared memory.
+// Warps: 0 = TMA producer, 1 = MMA issuer (whole warp converged, one elected lane issues; also
+// owns TMEM), 2..9 = two epilogue warpgroups that take alternate streamed tiles (ping-pong).
+//
+// MMA ordering: tcgen05.mma / tcgen05.cp from one thread execute in issue order, which the
+// kernel relies on for the two write-after-read reuses of TMEM: S_{k+2} overwrites the buffer
+// that P_k.T_k read, and the next item's tcgen05.cp overwrites the resident operand that this
+// item's last S read (the same convention as CUTLASS's sm100 FMHA S/P aliasing).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -41,6 +45,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "engine.h"
 #include "tc_common.cuh"
@@ -49,62 +54,87 @@ namespace ember {
 namespace {
 
 enum { MODE_ROWS = 0, MODE_NEGS = 1 };
-constexpr int RES = 128;     // resident rows per item (MMA M)
-constexpr int TILE = 64;     // streamed rows per tile (first product's N, second product's K)
-constexpr int NSTAGE = 4;    // streamed-tile ring depth
-constexpr int KPMAX = 128;   // largest padded dim
+constexpr int RES = 128;       // resident rows per item (MMA M)
+constexpr int TILE = 128;      // streamed rows per tile (first product's N, second product's K)
+constexpr int NSTAGE_MAX = 3;  // streamed-tile ring depth (as many as fit in shared memory)
+constexpr int KPMAX = 128;     // largest padded dim
 constexpr int NTHREADS = 320;
 constexpr uint32_t TCOLS = 512;
-constexpr uint32_t T_ACC = 128, T_RES = 256;
+constexpr uint32_t T_ACC = 256, T_RES = 384;
 constexpr float L2E = 1.4426950408889634f;
 
 struct TcArgs {
-    int KP, CB, d, nb, nt, n_pad, b_cap, chunks2;
+    int KP, CB, d, nb, nt, n_pad, b_cap, chunks2, nstage;
     float inv_b, log2_inv_b, zmax;
     const float* fpos;
     float* lse;       // [2][nb]
-    float* lse_pad;   // [2][b_cap], +inf past nb
+    float* lse_pad;   // [2][b_cap]: log2(1/b) - lse*log2(e), -inf past nb
     float* g0;        // [2][nb]
     float* dA;        // [2][nb][d]
     float* dN_part;   // [chunks][2][n_pad][d]
     uint32_t* flags;  // [0] = count, [1..] = side * b_cap + row
+    unsigned long long* trace;  // debug timeline of CTA 0 (EMBER_TC_TRACE), nullptr normally
 };
 
+// Debug timeline: (clock64, event << 32 | arg) records from CTA 0's producer, MMA issuer and one
+// warp of each epilogue group, each role writing its own region with a register counter
+// (fire-and-forget stores: no atomics on the issuing threads' critical path).
+constexpr int TRACE_ROLE = 4096;  // records per role
+#define TC_TRACE(ev, arg)                                                                              \
+    do {                                                                                               \
+        if (g.trace && blockIdx.x == 0 && lane == 0 && tr_n < TRACE_ROLE) {                            \
+            unsigned long long* p_ = g.trace + 2 * ((size_t)tr_role * TRACE_ROLE + tr_n++);            \
+            p_[0] = clock64();                                                                         \
+            p_[1] = ((unsigned long long)(ev) << 32) | (uint32_t)(arg);                                \
+        }                                                                                              \
+    } while (0)
+
 // ---- shared memory ------------------------------------------------------------------------
+// [res: 128 x KP hi|lo][ring: nstage x (TILE x KP hi|lo + lse trailer)][zbuf][bars]
 __host__ __device__ constexpr size_t res_bytes(int KP) { return (size_t)RES * KP * 4; }
-__host__ __device__ constexpr size_t stage_bytes(int KP) { return ((size_t)TILE * KP * 4 + 256 + 1023) & ~size_t(1023); }
-__host__ __device__ constexpr size_t smem_total(int KP) {
-    return 1024 + res_bytes(KP) + NSTAGE * stage_bytes(KP) + 2 * 2 * RES * 4 + 256;
+__host__ __device__ constexpr size_t trailer_bytes(int mode) { return mode == MODE_NEGS ? TILE * 4 : 0; }
+__host__ __device__ constexpr size_t stage_bytes(int KP, int mode) {
+    return (size_t)TILE * KP * 4 + trailer_bytes(mode);
+}
+__host__ __device__ constexpr size_t zbuf_bytes(int mode) { return mode == MODE_ROWS ? 2 * 2 * RES * 4 : 0; }
+__host__ __device__ constexpr size_t smem_total(int KP, int nstage, int mode) {
+    return 128 + res_bytes(KP) + nstage * stage_bytes(KP, mode) + zbuf_bytes(mode) + 256;
+}
+constexpr size_t SMEM_LIMIT = 232448;
+inline int stages_for(int KP) {
+    int n = NSTAGE_MAX;
+    while (n > 2 && std::max(smem_total(KP, n, MODE_ROWS), smem_total(KP, n, MODE_NEGS)) > SMEM_LIMIT) --n;
+    return n;
 }
 
 enum {
     B_RES_FULL = 0, B_RES_EMPTY = 1,
-    B_RING_FULL = 2,                 // + NSTAGE
-    B_RING_EMPTY = 2 + NSTAGE,       // + NSTAGE
-    B_S_FULL = 2 + 2 * NSTAGE,       // + 2
-    B_P_FULL = 4 + 2 * NSTAGE,       // + 2
-    B_R_READY = 6 + 2 * NSTAGE,      // + 2
-    B_ACC_FULL = 8 + 2 * NSTAGE, B_ACC_EMPTY = 9 + 2 * NSTAGE,
-    B_TMEM_SLOT = 10 + 2 * NSTAGE,
+    B_RING_FULL = 2,                     // + NSTAGE_MAX
+    B_RING_EMPTY = 2 + NSTAGE_MAX,       // + NSTAGE_MAX
+    B_S_FULL = 2 + 2 * NSTAGE_MAX,       // + 2
+    B_P_FULL = 4 + 2 * NSTAGE_MAX,       // + 2
+    B_ACC_FULL = 6 + 2 * NSTAGE_MAX, B_ACC_EMPTY = 7 + 2 * NSTAGE_MAX,
+    B_TMEM_SLOT = 8 + 2 * NSTAGE_MAX,
 };
 
 struct Smem {
     uint8_t* res;
-    uint8_t* ring;  // NSTAGE x stage_bytes; a stage = tile [2CB][64][16 B] then 64 floats (lse)
-    float* zbuf;    // [2 items][2 groups][128]
+    uint8_t* ring;  // nstage x stage; a stage = tile [2CB][TILE][16 B] (+ TILE floats in MODE_NEGS)
+    float* zbuf;    // [2 items][2 groups][128]   (MODE_ROWS)
     uint64_t* bars;
-    size_t sbytes;
+    uint32_t sbytes;
     __device__ uint8_t* stage(int st) const { return ring + (size_t)st * sbytes; }
 };
 
-__device__ __forceinline__ Smem carve(uint8_t* raw, int KP) {
-    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+template <int MODE>
+__device__ __forceinline__ Smem carve(uint8_t* raw, int KP, int nstage) {
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 127) & ~uintptr_t(127));
     Smem s;
-    s.sbytes = stage_bytes(KP);
+    s.sbytes = (uint32_t)stage_bytes(KP, MODE);
     s.res = base;
     s.ring = base + res_bytes(KP);
-    s.zbuf = reinterpret_cast<float*>(s.ring + NSTAGE * s.sbytes);
-    s.bars = reinterpret_cast<uint64_t*>(s.zbuf + 2 * 2 * RES);
+    s.zbuf = reinterpret_cast<float*>(s.ring + (size_t)nstage * s.sbytes);
+    s.bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(s.zbuf) + zbuf_bytes(MODE));
     return s;
 }
 
@@ -118,6 +148,14 @@ __device__ __forceinline__ uint64_t mndesc(const uint8_t* tile, int R, int s, in
 }
 
 __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+    asm volatile(
+        "{ .reg .pred e; elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.cp.cta_group::1.128x256b [%0], %1; }" ::"r"(taddr),
+        "l"(sdesc)
+        : "memory");
+}
 
 // ---- item geometry -------------------------------------------------------------------------
 struct Item {
@@ -154,32 +192,6 @@ __device__ __forceinline__ Item item_geo(const TcArgs& g, int item) {
     return it;
 }
 
-// Group 0: resident tile (smem, canonical K-major [2CB][128][16 B]) -> TMEM columns
-// [tR, tR + KP) as bf16 pairs: block cb -> columns 4cb..4cb+3 (hi blocks first, then lo).
-__device__ __forceinline__ void stage_resident(const Smem& sm, uint64_t* bars, int CB, uint32_t it, int r,
-                                               uint32_t t_row) {
-    tc::mbar_wait(&bars[B_RES_FULL], it & 1);
-    const uint32_t tR = t_row + T_RES + (it & 1) * 128;
-    for (int c0 = 0; c0 < 2 * CB; c0 += 4) {
-        uint32_t v[16];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int cb = c0 + i;
-            uint4 x = make_uint4(0, 0, 0, 0);
-            if (cb < 2 * CB) x = *reinterpret_cast<const uint4*>(sm.res + (size_t)cb * RES * 16 + r * 16);
-            v[4 * i] = x.x;
-            v[4 * i + 1] = x.y;
-            v[4 * i + 2] = x.z;
-            v[4 * i + 3] = x.w;
-        }
-        tc::tmem_st16(tR + 4 * c0, v);
-    }
-    tc::tmem_st_wait();
-    tc::fence_before();
-    tc::mbar_arrive(&bars[B_RES_EMPTY]);
-    tc::mbar_arrive(&bars[B_R_READY + (it & 1)]);
-}
-
 // Splits 64 fp32 values into 32 bf16x2 hi pairs and 32 lo pairs.
 __device__ __forceinline__ void split64(const float (&p)[64], uint32_t (&hi)[32], uint32_t (&lo)[32]) {
 #pragma unroll
@@ -194,26 +206,28 @@ __device__ __forceinline__ void split64(const float (&p)[64], uint32_t (&hi)[32]
 template <int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_tc(const __grid_constant__ CUtensorMap mapR, const __grid_constant__ CUtensorMap mapT, TcArgs g) {
-    extern __shared__ uint8_t smem_raw[];
-    const Smem sm = carve(smem_raw, g.KP);
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    const Smem sm = carve<MODE>(smem_raw, g.KP, g.nstage);
+    const int NSTAGE = g.nstage;
     uint64_t* bars = sm.bars;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(&bars[B_TMEM_SLOT]);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int KP = g.KP, CB = g.CB;
     const int items = n_items<MODE>(g);
     const int KS = KP / 16;
+    const int tr_role = warp == 0 ? 0 : warp == 1 ? 1 : warp == 2 ? 2 : 3;  // TC_TRACE region
+    int tr_n = 0;
 
     if (threadIdx.x == 0) {
         tc::mbar_init(&bars[B_RES_FULL], 1);
-        tc::mbar_init(&bars[B_RES_EMPTY], 128);
-        for (int i = 0; i < NSTAGE; ++i) {
+        tc::mbar_init(&bars[B_RES_EMPTY], 1);
+        for (int i = 0; i < g.nstage; ++i) {
             tc::mbar_init(&bars[B_RING_FULL + i], 1);
             tc::mbar_init(&bars[B_RING_EMPTY + i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             tc::mbar_init(&bars[B_S_FULL + i], 1);
             tc::mbar_init(&bars[B_P_FULL + i], 128);
-            tc::mbar_init(&bars[B_R_READY + i], 128);
         }
         tc::mbar_init(&bars[B_ACC_FULL], 1);
         tc::mbar_init(&bars[B_ACC_EMPTY], 256);
@@ -233,73 +247,97 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (warp == 0) {
         if (lane == 0) {  // ------------------------------------------------------ TMA producer
             const uint32_t bytesR = (uint32_t)res_bytes(KP);
-            const uint32_t bytesT = (uint32_t)(TILE * KP * 4) + (MODE == MODE_NEGS ? 256u : 0u);
+            const uint32_t bytesT = (uint32_t)stage_bytes(KP, MODE);
             uint32_t it = 0, gt = 0;
             for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
                 const Item I = item_geo<MODE>(g, item);
+                // resident tile of this item: its previous occupant was copied to TMEM (RES_EMPTY)
                 tc::mbar_wait(&bars[B_RES_EMPTY], (it & 1) ^ 1);
                 tc::mbar_expect_tx(&bars[B_RES_FULL], bytesR);
-                tc::tma_load_4d(sm.res, &mapR, 0, I.r0, 0, I.side, &bars[B_RES_FULL]);
+                tc::tma_load_4d(sm.res, &mapR, 0, I.r0 / 32, 0, I.side, &bars[B_RES_FULL]);
+                TC_TRACE(1, it);
                 for (int k = 0; k < I.T; ++k, ++gt) {
                     const int st = gt % NSTAGE;
                     tc::mbar_wait(&bars[B_RING_EMPTY + st], ((gt / NSTAGE) & 1) ^ 1);
+                    TC_TRACE(2, gt);
                     tc::mbar_expect_tx(&bars[B_RING_FULL + st], bytesT);
                     uint8_t* dst = sm.stage(st);
                     const int row = I.t0 + k * TILE;
-                    tc::tma_load_4d(dst, &mapT, 0, row, 0, I.side, &bars[B_RING_FULL + st]);
+                    tc::tma_load_4d(dst, &mapT, 0, row / 32, 0, I.side, &bars[B_RING_FULL + st]);
                     if (MODE == MODE_NEGS)
-                        tc::bulk_g2s(dst + TILE * KP * 4, g.lse_pad + (size_t)I.side * g.b_cap + row, 256,
+                        tc::bulk_g2s(dst + TILE * KP * 4, g.lse_pad + (size_t)I.side * g.b_cap + row, TILE * 4,
                                      &bars[B_RING_FULL + st]);
                 }
             }
         }
     } else if (warp == 1) {  // ------------------------------------------------- MMA issuer
-        // The whole warp runs this loop converged (all values warp-uniform, held in uniform
-        // registers); one elected lane issues each tcgen05 instruction.
+        // The whole warp runs this loop converged (warp-uniform waits and values, held in
+        // uniform registers); one elected lane issues each tcgen05 instruction.
         const uint32_t id_s = tc::idesc_bf16(128, TILE, false, false);
         const uint32_t id_a = tc::idesc_bf16(128, KP, false, true);
+        const uint64_t lo_off = (uint64_t)((CB * TILE * 16) >> 4);  // lo blocks follow hi blocks
         uint32_t it = 0, gt = 0;
         for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
             const Item I = item_geo<MODE>(g, item);
-            tc::mbar_wait(&bars[B_R_READY + (it & 1)], (it >> 1) & 1);
+            // resident operand smem -> TMEM, in the MMA pipe after the previous item's last S
+            tc::mbar_wait_warp(&bars[B_RES_FULL], it & 1);
+            TC_TRACE(10, it);
             tc::fence_after();
-            const uint32_t tR = T_RES + (it & 1) * 128;
+#pragma unroll
+            for (int s = 0; s < KPMAX / 16; ++s) {
+                if (s < KS) {
+                    tmem_cp_128x256b(T_RES + s * 8, kdesc(sm.res, RES, s, 0));
+                    tmem_cp_128x256b(T_RES + KP / 2 + s * 8, kdesc(sm.res, RES, s, CB));
+                }
+            }
+            tc::mma_commit_elect(&bars[B_RES_EMPTY]);
             int prev_st = 0;
             for (int k = 0; k <= I.T; ++k) {
                 int st = 0;
                 if (k < I.T) {  // S_k = R . T_k^T   (R from TMEM, T_k K-major from smem)
                     const uint32_t q = gt + k;
                     st = q % NSTAGE;
-                    tc::mbar_wait(&bars[B_RING_FULL + st], (q / NSTAGE) & 1);
+                    TC_TRACE(16, q);
+                    tc::mbar_wait_warp(&bars[B_RING_FULL + st], (q / NSTAGE) & 1);
+                    TC_TRACE(11, q);
                     tc::fence_after();
-                    const uint32_t tS = (q & 1) * 64;
+                    const uint32_t tS = (q & 1) * 128;
                     const uint64_t t0 = kdesc(sm.stage(st), TILE, 0, 0);
-                    const uint64_t lo_off = (uint64_t)((CB * TILE * 16) >> 4);
-                    for (int s = 0; s < KS; ++s) {
-                        const uint32_t rh = tR + s * 8, rl = tR + KP / 2 + s * 8;
-                        const uint64_t th = t0 + (uint64_t)((2 * s * TILE * 16) >> 4), tl = th + lo_off;
-                        tc::mma_ts_elect(tS, rl, th, id_s, s > 0 ? 1u : 0u);
-                        tc::mma_ts_elect(tS, rh, tl, id_s, 1u);
-                        tc::mma_ts_elect(tS, rh, th, id_s, 1u);
+#pragma unroll
+                    for (int s = 0; s < KPMAX / 16; ++s) {
+                        if (s < KS) {
+                            const uint32_t rh = T_RES + s * 8, rl = T_RES + KP / 2 + s * 8;
+                            const uint64_t th = t0 + (uint64_t)(s * ((2 * TILE * 16) >> 4)), tl = th + lo_off;
+                            tc::mma_ts_elect(tS, rl, th, id_s, s > 0 ? 1u : 0u);
+                            tc::mma_ts_elect(tS, rh, tl, id_s, 1u);
+                            tc::mma_ts_elect(tS, rh, th, id_s, 1u);
+                        }
                     }
                     tc::mma_commit_elect(&bars[B_S_FULL + (q & 1)]);
+                    TC_TRACE(12, q);
                 }
                 if (k > 0) {  // acc += P_{k-1} . T_{k-1}   (P from TMEM, T MN-major from smem)
                     const uint32_t q = gt + k - 1;
-                    tc::mbar_wait(&bars[B_P_FULL + (q & 1)], (q >> 1) & 1);
-                    if (k == 1) tc::mbar_wait(&bars[B_ACC_EMPTY], (it & 1) ^ 1);
+                    TC_TRACE(17, q);
+                    tc::mbar_wait_warp(&bars[B_P_FULL + (q & 1)], (q >> 1) & 1);
+                    TC_TRACE(13, q);
+                    if (k == 1) tc::mbar_wait_warp(&bars[B_ACC_EMPTY], (it & 1) ^ 1);
+                    if (k == 1) TC_TRACE(15, it);
                     tc::fence_after();
-                    const uint32_t tP = (q & 1) * 64;
+                    const uint32_t tP = (q & 1) * 128;
                     const uint64_t t0 = mndesc(sm.stage(prev_st), TILE, 0, 0);
-                    const uint64_t lo_off = (uint64_t)((CB * TILE * 16) >> 4);
+                    const uint32_t acc0 = k > 1 ? 1u : 0u;
+#pragma unroll
                     for (int s = 0; s < TILE / 16; ++s) {
-                        const uint32_t ph = tP + s * 8, pl = tP + 32 + s * 8;
-                        const uint64_t th = t0 + (uint64_t)((s * 256) >> 4), tl = th + lo_off;
-                        tc::mma_ts_elect(T_ACC, pl, th, id_a, (k > 1 || s > 0) ? 1u : 0u);
+                        // k-step s covers streamed rows 16s..16s+15: half h = s/4 of the P buffer
+                        const uint32_t ph = tP + (s >> 2) * 64 + (s & 3) * 8, pl = ph + 32;
+                        const uint64_t th = t0 + (uint64_t)(s * (256 >> 4)), tl = th + lo_off;
+                        tc::mma_ts_elect(T_ACC, pl, th, id_a, s > 0 ? 1u : acc0);
                         tc::mma_ts_elect(T_ACC, ph, tl, id_a, 1u);
                         tc::mma_ts_elect(T_ACC, ph, th, id_a, 1u);
                     }
                     tc::mma_commit_elect(&bars[B_RING_EMPTY + prev_st]);
+                    TC_TRACE(14, q);
                 }
                 prev_st = st;
             }
@@ -314,7 +352,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int nch = KP / 16, half = (nch + 1) / 2;
         const int c_lo = G == 0 ? 0 : half, c_hi = G == 0 ? half : nch;
         uint32_t it = 0, gt = 0;
-        if (G == 0 && (int)blockIdx.x < items) stage_resident(sm, bars, CB, 0, r, t_row);
         for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
             const Item I = item_geo<MODE>(g, item);
             const int row = I.r0 + r;
@@ -324,60 +361,67 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int k = 0; k < I.T; ++k) {
                 const uint32_t q = gt + k;
                 if ((int)(q & 1) != G) continue;
-                const uint32_t tS = t_row + (q & 1) * 64;
+                const uint32_t tS = t_row + (q & 1) * 128;
                 const int st = q % NSTAGE;
                 if (MODE == MODE_NEGS) tc::mbar_wait(&bars[B_RING_FULL + st], (q / NSTAGE) & 1);
                 tc::mbar_wait(&bars[B_S_FULL + (q & 1)], (q >> 1) & 1);
+                if (qd == 2) TC_TRACE(20 + G, q);
                 tc::fence_after();
-                float v[64];
-                {
-                    uint32_t a[32], b[32];
-                    tc::tmem_ld32(tS, a);
-                    tc::tmem_ld32(tS + 32, b);
-                    tc::tmem_ld_wait();
+#pragma unroll 1
+                for (int h = 0; h < 2; ++h) {  // 64-column halves: S half h -> P half h in place
+                    float v[64];
+                    {
+                        uint32_t a[32], b[32];
+                        tc::tmem_ld32(tS + 64 * h, a);
+                        tc::tmem_ld32(tS + 64 * h + 32, b);
+                        tc::tmem_ld_wait();
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        v[i] = __uint_as_float(a[i]);
-                        v[32 + i] = __uint_as_float(b[i]);
-                    }
-                }
-                if (MODE == MODE_ROWS) {
-                    const int k0 = k * TILE;
-                    if (k0 + TILE <= g.nt) {
-#pragma unroll
-                        for (int c = 0; c < 64; ++c) {
-                            v[c] = exp2f(fmaf(v[c], L2E, cshift));
-                            z += v[c];
-                        }
-                    } else {  // last tile: negatives past n_t contribute nothing
-#pragma unroll
-                        for (int c = 0; c < 64; ++c) {
-                            v[c] = (k0 + c < g.nt) ? exp2f(fmaf(v[c], L2E, cshift)) : 0.f;
-                            z += v[c];
+                        for (int i = 0; i < 32; ++i) {
+                            v[i] = __uint_as_float(a[i]);
+                            v[32 + i] = __uint_as_float(b[i]);
                         }
                     }
-                } else {
-                    const float4* L = reinterpret_cast<const float4*>(sm.stage(st) + TILE * KP * 4);
+                    if (MODE == MODE_ROWS) {
+                        const int k0 = k * TILE + 64 * h;
+                        if (k0 + 64 <= g.nt) {
 #pragma unroll
-                    for (int c4 = 0; c4 < 16; ++c4) {
-                        const float4 l = L[c4];  // broadcast; +inf past the batch -> P = 0
-                        v[4 * c4 + 0] = exp2f(fmaf(v[4 * c4 + 0], L2E, fmaf(-l.x, L2E, g.log2_inv_b)));
-                        v[4 * c4 + 1] = exp2f(fmaf(v[4 * c4 + 1], L2E, fmaf(-l.y, L2E, g.log2_inv_b)));
-                        v[4 * c4 + 2] = exp2f(fmaf(v[4 * c4 + 2], L2E, fmaf(-l.z, L2E, g.log2_inv_b)));
-                        v[4 * c4 + 3] = exp2f(fmaf(v[4 * c4 + 3], L2E, fmaf(-l.w, L2E, g.log2_inv_b)));
+                            for (int c = 0; c < 64; ++c) {
+                                v[c] = tc::ex2(fmaf(v[c], L2E, cshift));
+                                z += v[c];
+                            }
+                        } else {  // last tile: negatives past n_t contribute nothing
+#pragma unroll
+                            for (int c = 0; c < 64; ++c) {
+                                v[c] = (k0 + c < g.nt) ? tc::ex2(fmaf(v[c], L2E, cshift)) : 0.f;
+                                z += v[c];
+                            }
+                        }
+                    } else {
+                        // per batch row: log2(1/b) - lse*log2(e) (k_tc<ROWS> stores it; -inf past
+                        // the batch), from the stage's trailer (TMA'd with the tile)
+                        const float4* L =
+                            reinterpret_cast<const float4*>(sm.stage(st) + TILE * KP * 4) + 16 * h;
+#pragma unroll
+                        for (int c4 = 0; c4 < 16; ++c4) {
+                            const float4 l = L[c4];  // broadcast read
+                            v[4 * c4 + 0] = tc::ex2(fmaf(v[4 * c4 + 0], L2E, l.x));
+                            v[4 * c4 + 1] = tc::ex2(fmaf(v[4 * c4 + 1], L2E, l.y));
+                            v[4 * c4 + 2] = tc::ex2(fmaf(v[4 * c4 + 2], L2E, l.z));
+                            v[4 * c4 + 3] = tc::ex2(fmaf(v[4 * c4 + 3], L2E, l.w));
+                        }
                     }
+                    uint32_t hi[32], lo[32];
+                    split64(v, hi, lo);
+                    tc::tmem_st32(tS + 64 * h, hi);  // P overwrites S half h in place: hi, then lo
+                    tc::tmem_st32(tS + 64 * h + 32, lo);
                 }
-                uint32_t hi[32], lo[32];
-                split64(v, hi, lo);
-                tc::tmem_st32(tS, hi);  // P overwrites S in place: hi pairs, then lo pairs
-                tc::tmem_st32(tS + 32, lo);
                 tc::tmem_st_wait();
                 tc::fence_before();
                 tc::mbar_arrive(&bars[B_P_FULL + (q & 1)]);
+                if (qd == 2) TC_TRACE(22 + G, q);
             }
-            // group 0 stages the next item's resident operand while the tail of this one drains
-            if (G == 0 && item + (int)gridDim.x < items) stage_resident(sm, bars, CB, it + 1, r, t_row);
             tc::mbar_wait(&bars[B_ACC_FULL], it & 1);
+            if (qd == 2) TC_TRACE(26 + G, it);
             tc::fence_after();
             if (MODE == MODE_ROWS) {
                 float* zb = sm.zbuf + (it & 1) * 256;
@@ -408,7 +452,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         g.g0[(size_t)I.side * g.nb + row] = (__expf(fp - lse) - 1.0f) * g.inv_b;
                         if (bad) g.flags[1 + atomicAdd(g.flags, 1u)] = (uint32_t)(I.side * g.b_cap + row);
                     }
-                    g.lse_pad[(size_t)I.side * g.b_cap + row] = valid ? lse : INFINITY;
+                    g.lse_pad[(size_t)I.side * g.b_cap + row] = valid ? fmaf(-lse, L2E, g.log2_inv_b) : -INFINITY;
                 }
             } else {
                 float* out = g.dN_part + (((size_t)I.chunk * 2 + I.side) * g.n_pad + row) * g.d;
@@ -426,6 +470,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             tc::fence_before();
             tc::mbar_arrive(&bars[B_ACC_EMPTY]);
+            if (qd == 2) TC_TRACE(28 + G, it);
             gt += I.T;
         }
     }
@@ -468,7 +513,7 @@ __global__ void k_tc_fixup(TcArgs g, const float* __restrict__ A, const float* _
         for (int c = lane, i = 0; c < g.d; c += 32, ++i) out[c] = acc[i] * scale;
         if (lane == 0) {
             g.lse[(size_t)side * g.nb + row] = lse;
-            g.lse_pad[(size_t)side * g.b_cap + row] = lse;
+            g.lse_pad[(size_t)side * g.b_cap + row] = fmaf(-lse, L2E, g.log2_inv_b);
             g.g0[(size_t)side * g.nb + row] = (expf(fp - lse) - 1.0f) * g.inv_b;
         }
     }
@@ -532,12 +577,16 @@ EncodeTiled encode_fn() {
     return fn;
 }
 
-// 4-D view {8 bf16, rows (cap), 2CB blocks, 2 sides} of a packed operand; box {8, box_rows, 2CB, 1}.
+// 4-D view of a packed operand [2 sides][2CB blocks][cap rows][8 bf16]: within one column block,
+// 32 consecutive rows are one contiguous 512-byte run, so the view is {256 elements, cap/32 row
+// groups, 2CB blocks, 2 sides} and a box {256, box_rows/32, 2CB, 1} moves 512-byte rows (a 16-byte
+// inner box would cost one TMA request per 16 B). It lands in smem as [cb][box_rows][16 B], the
+// canonical K-major tile. Coordinates: (0, row/32, 0, side).
 CUtensorMap make_map(uint16_t* base, int cap, int CB, int box_rows) {
     CUtensorMap m;
-    const cuuint64_t dims[4] = {8, (cuuint64_t)cap, (cuuint64_t)(2 * CB), 2};
-    const cuuint64_t strides[3] = {16, (cuuint64_t)cap * 16, (cuuint64_t)cap * 16 * 2 * CB};
-    const cuuint32_t box[4] = {8, (cuuint32_t)box_rows, (cuuint32_t)(2 * CB), 1};
+    const cuuint64_t dims[4] = {256, (cuuint64_t)(cap / 32), (cuuint64_t)(2 * CB), 2};
+    const cuuint64_t strides[3] = {512, (cuuint64_t)cap * 16, (cuuint64_t)cap * 16 * 2 * CB};
+    const cuuint32_t box[4] = {256, (cuuint32_t)(box_rows / 32), (cuuint32_t)(2 * CB), 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, estr,
                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -550,14 +599,18 @@ CUtensorMap make_map(uint16_t* base, int cap, int CB, int box_rows) {
 
 // Engine-side state of the tensor-core engine (allocated once per context).
 struct TcState {
-    int KP = 0, CB = 0, b_cap = 0, n_pad = 0, chunks2 = 1;
+    int KP = 0, CB = 0, b_cap = 0, n_pad = 0, chunks2 = 1, nstage = 4;
     uint16_t* A = nullptr;   // [2][2CB][b_cap][8]
     uint16_t* N = nullptr;   // [2][2CB][n_pad][8]
     float* dN_part = nullptr;
     float* lse_pad = nullptr;
     uint32_t* flags = nullptr;
-    CUtensorMap mA128, mA64, mN64, mN128;
+    CUtensorMap mA, mN;  // 128-row boxes (RES == TILE)
     float zmax = 1e24f;
+    int max_grid = 0;  // test hook (EMBER_TC_MAXGRID): several items per CTA at small sizes
+    unsigned long long* trace = nullptr;  // EMBER_TC_TRACE=<file prefix>: CTA-0 timeline dump
+    std::string trace_path;
+    int trace_calls = 0;
 };
 
 bool tc_engine_supported(const Engine& E) {
@@ -575,20 +628,25 @@ void tc_setup(Engine& E) {
     t->n_pad = (int)((E.nt + RES - 1) / RES * RES);
     const int ntl = t->n_pad / RES;
     t->chunks2 = std::max(1, E.sm_count / (2 * ntl));
+    t->nstage = stages_for(t->KP);
     if (const char* s = getenv("EMBER_TC_ZMAX")) t->zmax = (float)atof(s);  // test hook: 0 flags every row
+    if (const char* s = getenv("EMBER_TC_MAXGRID")) t->max_grid = atoi(s);
+    if (const char* s = getenv("EMBER_TC_TRACE")) {
+        t->trace_path = s;
+        EMBER_CUDA(cudaMalloc(&t->trace, (size_t)2 * 4 * TRACE_ROLE * 8));
+    }
     EMBER_CUDA(cudaMalloc(&t->A, (size_t)2 * 2 * t->CB * t->b_cap * 16));
     EMBER_CUDA(cudaMalloc(&t->N, (size_t)2 * 2 * t->CB * t->n_pad * 16));
     EMBER_CUDA(cudaMalloc(&t->dN_part, (size_t)t->chunks2 * 2 * t->n_pad * E.dim * sizeof(float)));
     EMBER_CUDA(cudaMalloc(&t->lse_pad, (size_t)2 * t->b_cap * sizeof(float)));
     EMBER_CUDA(cudaMalloc(&t->flags, (size_t)(1 + 2 * t->b_cap) * sizeof(uint32_t)));
     EMBER_CUDA(cudaMemset(t->flags, 0, sizeof(uint32_t)));
-    t->mA128 = make_map(t->A, t->b_cap, t->CB, RES);
-    t->mA64 = make_map(t->A, t->b_cap, t->CB, TILE);
-    t->mN64 = make_map(t->N, t->n_pad, t->CB, TILE);
-    t->mN128 = make_map(t->N, t->n_pad, t->CB, RES);
-    const size_t smem = smem_total(t->KP);
-    EMBER_CUDA(cudaFuncSetAttribute(k_tc<MODE_ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    EMBER_CUDA(cudaFuncSetAttribute(k_tc<MODE_NEGS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    t->mA = make_map(t->A, t->b_cap, t->CB, RES);
+    t->mN = make_map(t->N, t->n_pad, t->CB, RES);
+    EMBER_CUDA(cudaFuncSetAttribute(k_tc<MODE_ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem_total(t->KP, t->nstage, MODE_ROWS)));
+    EMBER_CUDA(cudaFuncSetAttribute(k_tc<MODE_NEGS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem_total(t->KP, t->nstage, MODE_NEGS)));
     E.tc = t;
 }
 
@@ -599,6 +657,7 @@ void tc_release(Engine& E) {
     cudaFree(E.tc->dN_part);
     cudaFree(E.tc->lse_pad);
     cudaFree(E.tc->flags);
+    if (E.tc->trace) cudaFree(E.tc->trace);
     delete E.tc;
     E.tc = nullptr;
 }
@@ -636,17 +695,41 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
     a.dA = s.dA;
     a.dN_part = t.dN_part;
     a.flags = t.flags;
+    a.trace = nullptr;
     const int nsub = (int)((nb + TILE - 1) / TILE);
     a.chunks2 = std::min(t.chunks2, nsub);
-    const size_t smem = smem_total(t.KP);
+    a.nstage = t.nstage;
     const int items1 = 2 * (rows_pad / RES);
-    k_tc<MODE_ROWS><<<std::min(items1, E.sm_count), NTHREADS, smem, E.stream>>>(t.mA128, t.mN64, a);
+    const int gmax = t.max_grid > 0 ? std::min(t.max_grid, E.sm_count) : E.sm_count;
+    const bool tr = t.trace && t.trace_calls++ == 4;  // one warmed-up call per process
+    auto dump = [&](const char* tag) {
+        EMBER_CUDA(cudaStreamSynchronize(E.stream));
+        std::vector<unsigned long long> buf((size_t)2 * 4 * TRACE_ROLE);
+        EMBER_CUDA(cudaMemcpy(buf.data(), t.trace, buf.size() * 8, cudaMemcpyDeviceToHost));
+        FILE* f = fopen((t.trace_path + tag).c_str(), "wb");
+        if (f) {
+            fwrite(buf.data(), 8, buf.size(), f);
+            fclose(f);
+        }
+    };
+    if (tr) {
+        EMBER_CUDA(cudaMemsetAsync(t.trace, 0, (size_t)2 * 4 * TRACE_ROLE * 8, E.stream));
+        a.trace = t.trace;
+    }
+    k_tc<MODE_ROWS><<<std::min(items1, gmax), NTHREADS, smem_total(t.KP, t.nstage, MODE_ROWS), E.stream>>>(
+        t.mA, t.mN, a);
     EMBER_LAUNCHED(E);
+    if (tr) {
+        dump(".rows.bin");
+        EMBER_CUDA(cudaMemsetAsync(t.trace, 0, (size_t)2 * 4 * TRACE_ROLE * 8, E.stream));
+    }
     k_tc_fixup<<<1, 1024, 0, E.stream>>>(a, s.A, s.N);
     EMBER_LAUNCHED(E);
     const int items2 = 2 * (t.n_pad / RES) * a.chunks2;
-    k_tc<MODE_NEGS><<<std::min(items2, E.sm_count), NTHREADS, smem, E.stream>>>(t.mN128, t.mA64, a);
+    k_tc<MODE_NEGS><<<std::min(items2, gmax), NTHREADS, smem_total(t.KP, t.nstage, MODE_NEGS), E.stream>>>(
+        t.mN, t.mA, a);
     EMBER_LAUNCHED(E);
+    if (tr) dump(".negs.bin");
     const int64_t r = (int64_t)2 * nt * d;
     k_dn_reduce<<<(unsigned)((r + 255) / 256), 256, 0, E.stream>>>(t.dN_part, a.chunks2, nt, t.n_pad, d,
                                                                     s.grows + (size_t)2 * nb * d);

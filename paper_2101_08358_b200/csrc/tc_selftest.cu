@@ -7,6 +7,7 @@
 //   2  as 1 with lbo/sbo swapped
 //   3  TS: A in TMEM (lane = row, column c = bf16 pair (2c, 2c+1)), B as in mode 1
 //   4  TS: A in TMEM, B K-major as in mode 0
+//   5  as 4, A copied smem -> TMEM by tcgen05.cp.128x256b (one k-step of 16 per copy) in the MMA pipe
 #include <cuda_bf16.h>
 
 #include <cmath>
@@ -52,8 +53,8 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     tc::fence_after();
     const uint32_t taddr = tslot;
-    const bool a_tmem = (mode == 3 || mode == 4);
-    if (a_tmem && warp >= 4) {
+    const bool a_tmem = (mode == 3 || mode == 4 || mode == 5);
+    if ((mode == 3 || mode == 4) && warp >= 4) {
         const int r = 32 * (warp % 4) + lane;
         for (int c0 = 0; c0 < K / 2; c0 += 32) {
             uint32_t v[32];
@@ -76,6 +77,10 @@ __global__ void __launch_bounds__(256, 1)
             if (mode == 1 || mode == 3) bd = tc::sdesc(b0 + s * 256, 128, K * 16);
             else if (mode == 2) bd = tc::sdesc(b0 + s * 256, K * 16, 128);
             else bd = tc::sdesc(b0 + s * 2 * N * 16, N * 16, 128);
+            if (mode == 5)
+                asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr + 128 + s * 8),
+                             "l"(tc::sdesc(a0 + s * 2 * 128 * 16, 128 * 16, 128))
+                             : "memory");
             if (a_tmem)
                 tc::mma_ts(taddr, taddr + 128 + s * 8, bd, id, s > 0);
             else
@@ -154,4 +159,98 @@ double tc_selftest(int device, int mode, int K, int N, uint64_t seed) {
     return maxerr / std::max(maxref, 1e-30);
 }
 
+}  // namespace ember
+
+// ---- MMA issue-throughput microbenchmark ------------------------------------------------------
+// One CTA, one elected thread issues `iters` back-to-back tcgen05.mma (M=128, K=16, bf16) into one
+// accumulator and waits for completion; returns cycles per MMA. mode: 0 SS (A, B K-major smem),
+// 1 TS (A in TMEM, B K-major), 2 TS with B MN-major, 3 SS with B MN-major. Operand contents are
+// irrelevant (zeros); only the timing is reported.
+namespace ember {
+namespace {
+__global__ void __launch_bounds__(128, 1) k_tc_mmabench(int mode, int N, int iters, int nacc, long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tslot;
+    const int warp = threadIdx.x / 32;
+    for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
+    if (threadIdx.x == 0) {
+        tc::mbar_init(&bar, 1);
+        tc::fence_mbar_init();
+    }
+    tc::fence_async_smem();
+    __syncthreads();
+    if (warp == 0) tc::tmem_alloc(&tslot, 512);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t t = tslot;
+    if (warp == 0) {
+        const bool b_mn = (mode == 2 || mode == 3);
+        const uint32_t id = tc::idesc_bf16(128, N, false, b_mn);
+        const uint32_t a0 = tc::smem_addr(smem), b0 = tc::smem_addr(smem + 32768);
+        const uint64_t ad = tc::sdesc(a0, 128 * 16, 128);
+        const uint64_t bd = b_mn ? tc::sdesc(b0, 128, 16 * 16) : tc::sdesc(b0, N * 16, 128);
+        __syncwarp();
+        const uint32_t d1 = t + (nacc > 1 ? (uint32_t)N : 0u), d2 = t + (nacc > 2 ? 2u * N : 0u),
+                       d3 = t + (nacc > 3 ? 3u * N : 0u);
+        const long long c0 = clock64();
+        // 8 MMAs per trip, accumulators cycled t, d1, d2, d3 (nacc distinct values), no per-MMA math
+        if (mode == 1 || mode == 2) {
+            tc::mma_ts_elect(t, t + 256, bd, id, 0u);
+            tc::mma_ts_elect(d1, t + 256, bd, id, 0u);
+            tc::mma_ts_elect(d2, t + 256, bd, id, 0u);
+            tc::mma_ts_elect(d3, t + 256, bd, id, 0u);
+            for (int i = 0; i < iters; i += 8) {
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    tc::mma_ts_elect(t, t + 256, bd, id, 1u);
+                    tc::mma_ts_elect(d1, t + 256, bd, id, 1u);
+                    tc::mma_ts_elect(d2, t + 256, bd, id, 1u);
+                    tc::mma_ts_elect(d3, t + 256, bd, id, 1u);
+                }
+            }
+        } else {
+            tc::mma_ss_elect(t, ad, bd, id, 0u);
+            tc::mma_ss_elect(d1, ad, bd, id, 0u);
+            tc::mma_ss_elect(d2, ad, bd, id, 0u);
+            tc::mma_ss_elect(d3, ad, bd, id, 0u);
+            for (int i = 0; i < iters; i += 8) {
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    tc::mma_ss_elect(t, ad, bd, id, 1u);
+                    tc::mma_ss_elect(d1, ad, bd, id, 1u);
+                    tc::mma_ss_elect(d2, ad, bd, id, 1u);
+                    tc::mma_ss_elect(d3, ad, bd, id, 1u);
+                }
+            }
+        }
+        tc::mma_commit_elect(&bar);
+        tc::mbar_wait(&bar, 0);
+        const long long c1 = clock64();
+        if (threadIdx.x == 0) *out = c1 - c0;
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(t, 512);
+}
+}  // namespace
+
+double tc_mmabench(int device, int mode, int N, int iters, int nacc) {
+    EMBER_CUDA(cudaSetDevice(device));
+    long long* d;
+    EMBER_CUDA(cudaMalloc(&d, 8));
+    EMBER_CUDA(cudaFuncSetAttribute(k_tc_mmabench, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+    long long best = -1;
+    for (int rep = 0; rep < 3; ++rep) {
+        k_tc_mmabench<<<1, 128, 65536>>>(mode, N, iters, nacc < 1 ? 1 : nacc, d);
+        EMBER_CUDA(cudaGetLastError());
+        EMBER_CUDA(cudaDeviceSynchronize());
+        long long h;
+        EMBER_CUDA(cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost));
+        if (best < 0 || h < best) best = h;
+    }
+    cudaFree(d);
+    return (double)best / iters;
+}
 }  // namespace ember

@@ -159,15 +159,21 @@ def test_eval_ranks_match_oracle(graph):
     assert abs(a["mrr"] - b["mrr"]) < 1e-3
 
 
-@pytest.mark.parametrize("kind,dim,nt,nb,zmax", [("complex", 100, 1000, 3000, None), ("dot", 100, 1000, 1500, None),
-                                              ("distmult", 40, 100, 333, None), ("complex", 64, 200, 700, "0"),
-                                              ("distmult", 128, 300, 1000, None), ("complex", 16, 17, 5, None)])
-def test_tc_engine_headline_shapes(graph, monkeypatch, kind, dim, nt, nb, zmax):
+@pytest.mark.parametrize("kind,dim,nt,nb,zmax,grid", [("complex", 100, 1000, 3000, None, None),
+                                                   ("complex", 100, 1000, 3000, None, "5"),
+                                                   ("dot", 100, 1000, 1500, None, "2"),
+                                                   ("distmult", 40, 100, 333, None, None),
+                                                   ("complex", 64, 200, 700, "0", "3"),
+                                                   ("distmult", 128, 300, 1000, None, "1"),
+                                                   ("complex", 16, 17, 5, None, None)])
+def test_tc_engine_headline_shapes(graph, monkeypatch, kind, dim, nt, nb, zmax, grid):
     """Tensor-core contraction at the headline d=100 / n_t=1000 shape (smaller b), ragged tiles
     (nb, n_t not multiples of the 128/64 tiles), d at the 128 limit, and zmax=0 (every row sent
-    through the exact overflow fixup, k_tc_fixup) — all within 1e-4 of the oracle."""
+    through the exact overflow fixup, k_tc_fixup), and capped grids (several items per CTA) — all within 1e-4 of the oracle."""
     if zmax is not None:
         monkeypatch.setenv("EMBER_TC_ZMAX", zmax)
+    if grid is not None:  # few CTAs: every CTA walks several items (resident-operand hand-over)
+        monkeypatch.setenv("EMBER_TC_MAXGRID", grid)
     edges, off, _ = graph
     tr = make_trainer(kind, dim=dim, b=max(nb, 16), nt=nt, p=2, engine="tc")
     th, _, rt, _ = host_tables(tr)
