@@ -394,7 +394,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="fb86m", choices=sorted(CONFIGS))
-    ap.add_argument("--engine", default=os.environ.get("EMBER_ENGINE", "simt"), choices=["simt", "tc"])
+    ap.add_argument("--engine", default=os.environ.get("EMBER_ENGINE", "tc"), choices=["simt", "tc"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--cpu-rows", type=int, default=5000)
     ap.add_argument("--no-cpu", action="store_true")

@@ -212,7 +212,7 @@ int ember_loss_and_grad(ember_ctx* ctx, const uint32_t* edges, uint32_t nb, uint
         launch_loss(E, nb, E.s.loss);
         if (fpos) EMBER_CUDA(cudaMemcpyAsync(fpos, E.s.fpos, nb * sizeof(float), cudaMemcpyDeviceToDevice, E.stream));
         if (lse) EMBER_CUDA(cudaMemcpyAsync(lse, E.s.lse, 2ull * nb * sizeof(float), cudaMemcpyDeviceToDevice, E.stream));
-        E.reduce_and_apply(edges, nb, i, j, negs, false, node_ids, node_rows, rel_ids, rel_rows);
+        E.reduce_and_apply(nb, i, j, false, node_ids, node_rows, rel_ids, rel_rows);
         uint32_t counts[2] = {0, 0};
         float l = 0.f;
         EMBER_CUDA(cudaMemcpyAsync(counts, E.s.nunique, sizeof(counts), cudaMemcpyDeviceToHost, E.stream));

@@ -1,10 +1,15 @@
 // SPDX-License-Identifier: Apache-2.0
 //
 // Engine: the device-resident training step (Algorithm 1, PAPER.md:84-99 / SPEC.md:376-384
-// train_epoch_sync semantics, bound = 1). Per batch, on one stream:
-//   sample -> gather+adjust -> contraction (scores, LSE, dA, dN) -> chain rule ->
-//   sort ids + segmented sum -> Adagrad (relations synchronously, then nodes).
-// Stage 2/4 transfers of the paper's pipeline vanish: parameters stay in HBM.
+// train_epoch_sync semantics, bound = 1). Per batch:
+//   step stream:   sample -+-> gather+adjust -> contraction (scores, LSE, dA, dN) -> chain rule
+//                          |                                  (join) ^           -> loss
+//   helper stream:         +-> gradient-slot keys -> radix sort -> runs -> rank -+
+//   then one segmented sum over the sorted gradient rows -> Adagrad (relations and nodes;
+//   relations synchronously, after an NCCL all-reduce when world > 1).
+// The helper stream only overlaps work that the step stream would otherwise serialise; the
+// result is identical to a single-stream order. Stage 2/4 transfers of the paper's pipeline
+// vanish: parameters stay in HBM.
 #include <cub/cub.cuh>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -15,9 +20,6 @@
 #include "engine.h"
 
 namespace ember {
-
-void launch_node_keys(const Engine& E, const uint32_t* edges, uint32_t nb, const uint32_t* negs);
-void launch_rel_keys(const Engine& E, const uint32_t* edges, uint32_t nb);
 
 namespace {
 
@@ -61,13 +63,6 @@ NcclApi& nccl() {
     return api;
 }
 
-__global__ void k_scatter_rel_dense(const uint32_t* ukeys, const uint32_t* nunique, const float* rows, uint32_t d,
-                                    float* dense) {
-    const uint32_t u = blockIdx.x;
-    if (u >= *nunique) return;
-    for (uint32_t k = threadIdx.x; k < d; k += blockDim.x) dense[(uint64_t)ukeys[u] * d + k] = rows[(uint64_t)u * d + k];
-}
-
 __global__ void k_adagrad_dense(float* th, float* ac, const float* g, uint64_t n, float lr, float eps) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -97,7 +92,7 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     if (chunks > m.batch_size) throw ConfigError("num_chunks must be <= batch_size");
     cap_b = m.batch_size;
     n_neg = chunks * 2 * nt;
-    key_bits = bits_for(g.num_nodes);
+    cap_rows = 3 * cap_b + n_neg;
 
     EMBER_CUDA(cudaSetDevice(device));
     cudaDeviceProp prop;
@@ -109,59 +104,77 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
         EMBER_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
         own_stream = true;
     }
+    EMBER_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    EMBER_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    EMBER_CUDA(cudaEventCreateWithFlags(&ev_sorted, cudaEventDisableTiming));
     parts.assign(g.num_partitions, PartView{nullptr, nullptr, 0, 0});
     for (uint32_t k = 0; k < g.num_partitions; ++k) {
         parts[k].first = partition_offset(g.num_nodes, g.num_partitions, k);
         parts[k].rows = partition_size(g.num_nodes, g.num_partitions, k);
     }
-    if (m.engine == EMBER_ENGINE_TC_BF16X3 && !tc_engine_supported(*this))
-        throw ConfigError("tensor-core engine needs a CC 10.0 device (B200), dim <= 256 and num_chunks == 1");
+    if (tc_engine() && !tc_engine_supported(*this))
+        throw ConfigError("tensor-core engine needs a CC 10.0 device (B200), dim <= 128 and num_chunks == 1");
 
-    const uint64_t b = cap_b, d = dim, nrows = 2 * b + n_neg;
+    const uint64_t b = cap_b, d = dim;
     s.negs = dalloc<uint32_t>(n_neg);
     s.batch = dalloc<uint32_t>(3 * b);
     s.A = dalloc<float>(2 * b * d);
+    s.N = dalloc<float>((uint64_t)n_neg * d);
     s.fpos = dalloc<float>(b);
     s.lse = dalloc<float>(2 * b);
     s.g0 = dalloc<float>(2 * b);
-    s.N = dalloc<float>((uint64_t)n_neg * d);
     s.dA = dalloc<float>(2 * b * d);
-    s.grows = dalloc<float>(nrows * d);
-    s.rrows = dalloc<float>(b * d);
+    s.grows = dalloc<float>((uint64_t)cap_rows * d);
     s.loss = dalloc<float>(1);
-    s.keys = dalloc<uint32_t>(nrows);
-    s.keys_sorted = dalloc<uint32_t>(nrows);
-    s.vals = dalloc<uint32_t>(nrows);
-    s.vals_sorted = dalloc<uint32_t>(nrows);
-    s.ukeys = dalloc<uint32_t>(nrows);
-    s.counts = dalloc<uint32_t>(nrows);
-    s.offsets = dalloc<uint32_t>(nrows);
+    s.loss_part = reinterpret_cast<float*>(dalloc<double>(b / 4096 + 2));
+    s.loss_done = dalloc<uint32_t>(1);
+    EMBER_CUDA(cudaMemset(s.loss_done, 0, sizeof(uint32_t)));
+    s.keys = dalloc<uint32_t>(cap_rows);
+    s.keys_sorted = dalloc<uint32_t>(cap_rows);
+    s.vals = dalloc<uint32_t>(cap_rows);
+    s.vals_sorted = dalloc<uint32_t>(cap_rows);
+    s.rank = dalloc<uint32_t>(cap_rows);
+    s.ukeys = dalloc<uint32_t>(cap_rows);
+    s.counts = dalloc<uint32_t>(cap_rows);
+    s.offsets = dalloc<uint32_t>(cap_rows);
+    s.nruns = dalloc<uint32_t>(1);
     s.nunique = dalloc<uint32_t>(2);
-    s.cc = dalloc<uint32_t>(nrows);
-    s.coff = dalloc<uint32_t>(nrows);
-    s.partial = dalloc<float>(nrows * d);
+    s.longs = dalloc<uint32_t>(1 + cap_rows);
+    EMBER_CUDA(cudaMemset(s.nunique, 0, 2 * sizeof(uint32_t)));
+    EMBER_CUDA(cudaMemset(s.longs, 0, sizeof(uint32_t)));
     if (m.engine == EMBER_ENGINE_SIMT_FP32) {
         s.S = dalloc<float>(2 * b * (uint64_t)(nt ? nt : 1));
         s.dN_part = dalloc<float>((uint64_t)dsplit * n_neg * d);
     }
+    if (tc_engine()) {  // packed operand geometry: dim padded to 16, rows to 128-row tiles
+        KP = (int)((dim + 15) / 16 * 16);
+        CB = KP / 8;
+        b_cap = (int)((cap_b + 127) / 128 * 128);
+        n_pad = (int)((nt + 127) / 128 * 128);
+        s.Apk = dalloc<uint16_t>((size_t)2 * 2 * CB * b_cap * 8);
+        s.Npk = dalloc<uint16_t>((size_t)2 * 2 * CB * n_pad * 8);
+    }
     size_t t1 = 0, t2 = 0, t3 = 0;
-    EMBER_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t1, s.keys, s.keys_sorted, s.vals, s.vals_sorted, (int)nrows, 0,
-                                               32, stream));
-    EMBER_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, t2, s.keys_sorted, s.ukeys, s.counts, s.nunique, (int)nrows,
-                                                  stream));
-    EMBER_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t3, s.counts, s.offsets, (int)nrows, stream));
+    EMBER_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t1, s.keys, s.keys_sorted, s.vals, s.vals_sorted,
+                                               (int)cap_rows, 0, 32, side));
+    EMBER_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, t2, s.keys_sorted, s.ukeys, s.counts, s.nruns,
+                                                  (int)cap_rows, side));
+    EMBER_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t3, s.counts, s.offsets, (int)cap_rows, side));
     s.cub_bytes = std::max(t1, std::max(t2, t3));
     s.cub_tmp = dalloc<uint8_t>(s.cub_bytes);
-    if (m.engine == EMBER_ENGINE_TC_BF16X3) tc_setup(*this);
+    if (tc_engine()) tc_setup(*this);
     EMBER_CUDA(cudaStreamSynchronize(stream));
 }
 
 Engine::~Engine() {
     cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    if (side) cudaStreamSynchronize(side);
     tc_release(*this);
-    void* ptrs[] = {s.negs, s.batch, s.A, s.fpos, s.lse, s.g0, s.N, s.S, s.dA, s.dN_part, s.grows, s.rrows,
-                    s.row_loss, s.loss, s.keys, s.keys_sorted, s.vals, s.vals_sorted, s.ukeys, s.counts, s.offsets,
-                    s.nunique, s.cub_tmp, s.Atc, s.Ntc, s.NTtc, s.dN_tc, s.rel_dense, s.cc, s.coff, s.partial};
+    void* ptrs[] = {s.negs,  s.batch,       s.A,    s.N,          s.Apk,       s.Npk,   s.fpos,   s.lse,
+                    s.g0,    s.S,           s.dA,   s.dN_part,    s.grows,     s.loss,  s.loss_part,
+                    s.loss_done, s.keys,    s.keys_sorted, s.vals, s.vals_sorted, s.rank, s.ukeys,  s.counts,
+                    s.offsets, s.nruns,     s.nunique, s.longs,   s.cub_tmp,   s.rel_dense};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (nccl_comm) {
@@ -170,6 +183,9 @@ Engine::~Engine() {
         } catch (...) {
         }
     }
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_sorted) cudaEventDestroy(ev_sorted);
+    if (side) cudaStreamDestroy(side);
     if (own_stream) cudaStreamDestroy(stream);
 }
 
@@ -186,75 +202,78 @@ void Engine::check_bucket(uint32_t i, uint32_t j) const {
     if (m.kind != EMBER_DOT && (!rel_theta || !rel_acc)) throw ConfigError("relation table not bound");
 }
 
+KeySpace Engine::keyspace(uint32_t i, uint32_t j) const {
+    KeySpace ks;
+    ks.lo = view(std::min(i, j));
+    ks.hi = view(std::max(i, j));
+    ks.node_range = ks.lo.rows + (i != j ? ks.hi.rows : 0);
+    const uint64_t n_keys = ks.node_range + (m.kind != EMBER_DOT ? g.num_relations : 0);
+    ks.bits = bits_for(n_keys);
+    return ks;
+}
+
 void Engine::sample(const uint32_t* bucket, uint64_t bucket_n, uint32_t i, uint32_t j, uint64_t epoch,
                     uint32_t bucket_step, uint32_t batch_in_bucket, uint32_t* negs_out) {
     const uint64_t base = mix_seed(mix_seed(m.neg_seed, epoch, bucket_step), batch_in_bucket);
     launch_sample(*this, negs_out, base, bucket, bucket_n, view(i), view(j));
 }
 
+void Engine::sort_keys(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs) {
+    const KeySpace ks = keyspace(i, j);
+    const uint32_t n = slots(nb);
+    EMBER_CUDA(cudaEventRecord(ev_fork, stream));
+    EMBER_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+    launch_keys(*this, edges, nb, negs, ks);
+    size_t bytes = s.cub_bytes;
+    EMBER_CUDA(cub::DeviceRadixSort::SortPairs(s.cub_tmp, bytes, s.keys, s.keys_sorted, s.vals, s.vals_sorted, (int)n,
+                                               0, (int)ks.bits, side));
+    bytes = s.cub_bytes;
+    EMBER_CUDA(cub::DeviceRunLengthEncode::Encode(s.cub_tmp, bytes, s.keys_sorted, s.ukeys, s.counts, s.nruns, (int)n,
+                                                  side));
+    bytes = s.cub_bytes;
+    EMBER_CUDA(cub::DeviceScan::ExclusiveSum(s.cub_tmp, bytes, s.counts, s.offsets, (int)n, side));
+    lib_calls += 3;
+    launch_rank(*this, n);
+    EMBER_CUDA(cudaEventRecord(ev_sorted, side));
+    sorted_pending = true;
+}
+
+void Engine::join_sorted() {
+    if (!sorted_pending) return;
+    EMBER_CUDA(cudaStreamWaitEvent(stream, ev_sorted, 0));
+    sorted_pending = false;
+}
+
 void Engine::forward_backward(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs) {
     const PartView pi = view(i), pj = view(j);
+    sort_keys(edges, nb, i, j, negs);  // helper stream, overlapped with the gathers and the contraction
     mark(PHASE_GATHER);
-    launch_gather_adjust(*this, edges, nb, pi, pj);
-    launch_gather_negatives(*this, negs, pi, pj);
+    launch_gather_adjust(*this, edges, nb, pi, pj, tc_engine());
+    launch_gather_negatives(*this, negs, pi, pj, tc_engine());
     mark(PHASE_CONTRACT);
-    if (m.engine == EMBER_ENGINE_TC_BF16X3)
-        launch_contract_tc(*this, nb);
+    if (tc_engine())
+        launch_contract_tc(*this, nb);  // joins the sort before scattering dN rows
     else
         launch_contract_simt(*this, nb);
     mark(PHASE_CHAIN);
+    join_sorted();
     launch_chain_rule(*this, edges, nb, pi, pj);
 }
 
-void Engine::reduce_and_apply(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs,
-                              bool apply, uint32_t* node_ids_out, float* node_rows_out, uint32_t* rel_ids_out,
-                              float* rel_rows_out) {
-    const PartView pi = view(i), pj = view(j);
-    size_t bytes = s.cub_bytes;
-    // relations first: the synchronous relation update of SPEC.md:388
-    if (m.kind != EMBER_DOT) {
-        launch_rel_keys(*this, edges, nb);
-        const uint32_t rbits = bits_for(g.num_relations);
-        EMBER_CUDA(cub::DeviceRadixSort::SortPairs(s.cub_tmp, bytes, s.keys, s.keys_sorted, s.vals, s.vals_sorted,
-                                                   (int)nb, 0, rbits, stream));
-        bytes = s.cub_bytes;
-        EMBER_CUDA(cub::DeviceRunLengthEncode::Encode(s.cub_tmp, bytes, s.keys_sorted, s.ukeys, s.counts,
-                                                      s.nunique + 1, (int)nb, stream));
-        bytes = s.cub_bytes;
-        EMBER_CUDA(cub::DeviceScan::ExclusiveSum(s.cub_tmp, bytes, s.counts, s.offsets, (int)nb, stream));
-        if (world > 1 && apply) {
-            // dense relation gradient, summed over ranks, then dense Adagrad (g == 0 rows untouched)
-            const uint64_t rn = (uint64_t)g.num_relations * dim;
-            float* dense = s.rel_dense;
-            EMBER_CUDA(cudaMemsetAsync(dense, 0, rn * sizeof(float), stream));
-            // summed rows per unique relation into s.A (free after the chain rule), then scatter dense
-            launch_adagrad_segments(*this, s.ukeys, s.offsets, s.counts, s.nunique + 1, s.vals_sorted, s.rrows, nb,
-                                    pi, pj, true, nullptr, s.A, false);
-            k_scatter_rel_dense<<<nb, 128, 0, stream>>>(s.ukeys, s.nunique + 1, s.A, dim, dense);
-            EMBER_CUDA(cudaGetLastError());
-            allreduce_relations(nb);
-            k_adagrad_dense<<<(unsigned)((rn + 255) / 256), 256, 0, stream>>>(rel_theta, rel_acc, dense, rn, m.lr,
-                                                                             m.eps);
-            EMBER_CUDA(cudaGetLastError());
-        } else {
-            launch_adagrad_segments(*this, s.ukeys, s.offsets, s.counts, s.nunique + 1, s.vals_sorted, s.rrows, nb,
-                                    pi, pj, true, rel_ids_out, rel_rows_out, apply);
-        }
+void Engine::reduce_and_apply(uint32_t nb, uint32_t i, uint32_t j, bool apply, uint32_t* node_ids_out,
+                              float* node_rows_out, uint32_t* rel_ids_out, float* rel_rows_out) {
+    const KeySpace ks = keyspace(i, j);
+    const bool dense = world > 1 && apply && m.kind != EMBER_DOT;
+    if (dense) EMBER_CUDA(cudaMemsetAsync(s.rel_dense, 0, (size_t)g.num_relations * dim * sizeof(float), stream));
+    // nodes apply in place; relations either in place (world == 1) or into the dense buffer
+    launch_segments(*this, slots(nb), ks, apply, dense, node_ids_out, node_rows_out, rel_ids_out, rel_rows_out);
+    if (dense) {
+        allreduce_relations();
+        const uint64_t rn = (uint64_t)g.num_relations * dim;
+        k_adagrad_dense<<<(unsigned)((rn + 255) / 256), 256, 0, stream>>>(rel_theta, rel_acc, s.rel_dense, rn, m.lr,
+                                                                         m.eps);
+        EMBER_LAUNCHED(*this);
     }
-    if (m.kind != EMBER_DOT) lib_calls += 3;
-    launch_node_keys(*this, edges, nb, negs);
-    lib_calls += 3;
-    const uint32_t n = 2 * nb + n_neg;
-    bytes = s.cub_bytes;
-    EMBER_CUDA(cub::DeviceRadixSort::SortPairs(s.cub_tmp, bytes, s.keys, s.keys_sorted, s.vals, s.vals_sorted, (int)n,
-                                               0, key_bits, stream));
-    bytes = s.cub_bytes;
-    EMBER_CUDA(cub::DeviceRunLengthEncode::Encode(s.cub_tmp, bytes, s.keys_sorted, s.ukeys, s.counts, s.nunique,
-                                                  (int)n, stream));
-    bytes = s.cub_bytes;
-    EMBER_CUDA(cub::DeviceScan::ExclusiveSum(s.cub_tmp, bytes, s.counts, s.offsets, (int)n, stream));
-    launch_adagrad_segments(*this, s.ukeys, s.offsets, s.counts, s.nunique, s.vals_sorted, s.grows, n, pi, pj, false,
-                            node_ids_out, node_rows_out, apply);
 }
 
 void Engine::mark(int phase) {
@@ -280,7 +299,7 @@ void Engine::step(const uint32_t* edges, uint32_t nb, const uint32_t* bucket, ui
     forward_backward(edges, nb, i, j, s.negs);
     launch_loss(*this, nb, loss_out ? loss_out : s.loss);
     mark(PHASE_REDUCE);
-    reduce_and_apply(edges, nb, i, j, s.negs, true, nullptr, nullptr, nullptr, nullptr);
+    reduce_and_apply(nb, i, j, true, nullptr, nullptr, nullptr, nullptr);
     mark(PHASE_END);
 }
 
@@ -313,7 +332,7 @@ void Engine::comm_init(const void* unique_id, int r, int w) {
     if (m.kind != EMBER_DOT && !s.rel_dense) s.rel_dense = dalloc<float>((uint64_t)g.num_relations * dim);
 }
 
-void Engine::allreduce_relations(uint32_t) {
+void Engine::allreduce_relations() {
     if (!nccl_comm) return;
     const uint64_t rn = (uint64_t)g.num_relations * dim;
     ncclResult_t r = nccl().all_reduce(s.rel_dense, s.rel_dense, rn, ncclFloat32, ncclSum, static_cast<ncclComm_t>(nccl_comm), stream);

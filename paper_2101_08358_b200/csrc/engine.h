@@ -2,8 +2,8 @@
 //
 // Engine: one GPU's training context behind the C-ABI (include/ember_gpu.h).
 // Owns the step's device scratch, sized once for the configured batch; borrows the
-// partition tables. All work goes to one CUDA stream (the single compute worker of
-// SPEC.md:372).
+// partition tables. All work is ordered on one CUDA stream (the single compute worker of
+// SPEC.md:372); internally the key sort forks onto a helper stream and joins back.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -40,50 +40,60 @@ struct PartView {
     uint64_t rows;
 };
 
-// Scratch for one step. Layouts (row-major, dim-wide rows unless noted):
+// Gradient-row keys of one batch of bucket (i, j). Node ids live in partitions lo = min(i, j)
+// and hi = max(i, j); key = id - first_lo for the lo partition, rows_lo + (id - first_hi) for
+// the hi one (so ascending keys = ascending global ids), relation r -> node_range + r. With
+// p = 16 this is a 24-bit key: three 8-bit radix passes.
+struct KeySpace {
+    PartView lo, hi;
+    uint64_t node_range;
+    uint32_t bits;
+};
+
+// Gradient-row production index ("slot") of one batch: [0, nb) source rows, [nb, 2nb)
+// destination rows, [2nb, 2nb + n_neg) negative rows, [2nb + n_neg, 3nb + n_neg) relation rows.
+// rank[slot] = the slot's position after sorting by (key, slot); producers write each gradient
+// row straight to grows[rank[slot]], so every key's rows are contiguous and in slot order.
+//
+// Scratch layouts (row-major, dim-wide rows unless noted):
 //   negs   [chunks][2][nt]             sampled negative ids (side 0 = dst corruption)
-//   A      [2][b][dim]                 adjusted vectors (side 0: adj_dst, side 1: adj_src)
-//   fpos   [b]                         positive scores
-//   lse,g0 [2][b]                      log-sum-exp per row, dL/dfpos per side
-//   N      [chunks*2*nt][dim]          gathered negative rows
-//   S      [2][b][nt]                  scores, overwritten by P/b (SIMT engine only)
-//   dA     [2][b][dim]
-//   grows  [2b + chunks*2*nt][dim]     node gradient rows: src rows, dst rows, negative rows (= dN)
-//   rrows  [b][dim]                    relation gradient rows
+//   A      [2][b][dim]                 adjusted vectors, fp32 (SIMT engine / debug scores)
+//   N      [chunks*2*nt][dim]          negative rows, fp32 (SIMT engine / debug scores)
+//   Apk    [2][2CB][b_cap][8] bf16     adjusted vectors split hi|lo (tensor-core engine)
+//   Npk    [2][2CB][n_pad][8] bf16     negative rows split hi|lo (tensor-core engine)
+//   fpos   [b]; lse, g0 [2][b]; dA [2][b][dim]
+//   grows  [3b + n_neg][dim]           gradient rows in sorted (key, slot) order
 struct Scratch {
     uint32_t* negs = nullptr;
     uint32_t* batch = nullptr;  // staging for host batches [b][3]
     float* A = nullptr;
+    float* N = nullptr;
+    uint16_t* Apk = nullptr;
+    uint16_t* Npk = nullptr;
     float* fpos = nullptr;
     float* lse = nullptr;
     float* g0 = nullptr;
-    float* N = nullptr;
-    float* S = nullptr;
+    float* S = nullptr;       // SIMT engine: [2][b][nt] scores -> P/b
     float* dA = nullptr;
-    float* dN_part = nullptr;
+    float* dN_part = nullptr; // SIMT engine split-K partials
     float* grows = nullptr;
-    float* rrows = nullptr;
-    float* row_loss = nullptr;
-    float* loss = nullptr;      // [1]
+    float* loss = nullptr;       // [1]
+    float* loss_part = nullptr;  // per-block partial sums of the loss reduction
+    uint32_t* loss_done = nullptr;
     uint32_t* keys = nullptr;
     uint32_t* keys_sorted = nullptr;
     uint32_t* vals = nullptr;
     uint32_t* vals_sorted = nullptr;
+    uint32_t* rank = nullptr;
     uint32_t* ukeys = nullptr;
     uint32_t* counts = nullptr;
     uint32_t* offsets = nullptr;
-    uint32_t* nunique = nullptr;  // [2]: nodes, relations
+    uint32_t* nruns = nullptr;    // [1] unique keys (RLE)
+    uint32_t* nunique = nullptr;  // [2] unique node keys, unique relation keys
+    uint32_t* longs = nullptr;    // [1 + cap] count, then indices of long segments
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
-    // bf16 hi/lo operand tiles for the tensor-core engine
-    uint16_t* Atc = nullptr;
-    uint16_t* Ntc = nullptr;
-    uint16_t* NTtc = nullptr;
-    float* dN_tc = nullptr;
     float* rel_dense = nullptr;  // [R][dim] relation gradient summed over ranks (world > 1)
-    uint32_t* cc = nullptr;      // chunks per unique id (segmented reduction)
-    uint32_t* coff = nullptr;    // exclusive scan of cc
-    float* partial = nullptr;    // [2b + negs][dim] per-chunk partial sums
 };
 
 struct TcState;  // tensor-core engine state (tc_score.cu)
@@ -91,7 +101,10 @@ struct TcState;  // tensor-core engine state (tc_score.cu)
 struct Engine {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;  // key sort runs here, overlapped with gather + contraction
+    cudaEvent_t ev_fork = nullptr, ev_sorted = nullptr;
     bool own_stream = false;
+    bool sorted_pending = false;
     ember_model_desc m{};
     ember_graph_desc g{};
     uint32_t dim = 0;
@@ -99,13 +112,15 @@ struct Engine {
     uint32_t chunks = 1;
     uint32_t cap_b = 0;
     uint32_t n_neg = 0;     // chunks * 2 * nt
+    uint32_t cap_rows = 0;  // 3 * cap_b + n_neg gradient slots
     uint32_t dsplit = 16;   // split-K factor for dN in the SIMT engine
-    uint32_t key_bits = 32;
     std::vector<PartView> parts;
     float* rel_theta = nullptr;
     float* rel_acc = nullptr;
     Scratch s;
     TcState* tc = nullptr;
+    // packed-operand geometry (tensor-core engine)
+    int KP = 0, CB = 0, b_cap = 0, n_pad = 0;
     int sm_count = 148;
     // multi-GPU
     void* nccl_comm = nullptr;
@@ -122,22 +137,27 @@ struct Engine {
 
     PartView view(uint32_t part) const;
     void check_bucket(uint32_t i, uint32_t j) const;
+    KeySpace keyspace(uint32_t i, uint32_t j) const;
+    bool tc_engine() const { return m.engine == EMBER_ENGINE_TC_BF16X3; }
+    uint32_t slots(uint32_t nb) const { return 2 * nb + n_neg + (m.kind != EMBER_DOT ? nb : 0); }
 
     // pipeline stages
     void sample(const uint32_t* bucket, uint64_t bucket_n, uint32_t i, uint32_t j, uint64_t epoch,
                 uint32_t bucket_step, uint32_t batch_in_bucket, uint32_t* negs_out);
-    // Computes loss and node/relation gradient rows for one batch into scratch (grows, rrows).
+    // Keys of the batch's gradient slots, sorted on the helper stream (forked here).
+    void sort_keys(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs);
+    void join_sorted();  // the step stream waits for sort_keys' results
+    // Computes loss and gradient rows for one batch into grows (sorted order).
     void forward_backward(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs);
-    // Dedupe + segmented sum of the gradient rows, then Adagrad (or export the deltas).
-    void reduce_and_apply(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs,
-                          bool apply, uint32_t* node_ids_out, float* node_rows_out, uint32_t* rel_ids_out,
-                          float* rel_rows_out);
+    // Segmented sum of the sorted gradient rows, then Adagrad (or export of the deltas).
+    void reduce_and_apply(uint32_t nb, uint32_t i, uint32_t j, bool apply, uint32_t* node_ids_out,
+                          float* node_rows_out, uint32_t* rel_ids_out, float* rel_rows_out);
     void train_batch(const uint32_t* bucket, uint64_t bucket_n, uint64_t batch_begin, uint32_t nb, uint32_t i,
                      uint32_t j, uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket, float* loss_out);
     // One Algorithm-1 step on nb positives at `edges` (device) of bucket (i, j).
     void step(const uint32_t* edges, uint32_t nb, const uint32_t* bucket, uint64_t bucket_n, uint32_t i, uint32_t j,
               uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket, float* loss_out);
-    void allreduce_relations(uint32_t nb);
+    void allreduce_relations();
     void comm_init(const void* nccl_unique_id, int rank, int world);
     std::vector<double> profile_read();  // ms per phase summed over marked batches
 };
@@ -147,16 +167,18 @@ enum Phase { PHASE_SAMPLE = 0, PHASE_GATHER = 1, PHASE_CONTRACT = 2, PHASE_CHAIN
 // kernel launchers (kernels_step.cu, gemm_simt.cu, tc_score.cu, graph.cu)
 void launch_sample(const Engine& E, uint32_t* out, uint64_t base_seed, const uint32_t* bucket, uint64_t bucket_n,
                    const PartView& src, const PartView& dst);
-void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj);
-void launch_gather_negatives(const Engine& E, const uint32_t* negs, const PartView& pi, const PartView& pj);
+// packed: write the tensor-core engine's bf16 hi|lo operands (Apk/Npk), else fp32 A / N.
+void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj,
+                          bool packed);
+void launch_gather_negatives(const Engine& E, const uint32_t* negs, const PartView& pi, const PartView& pj, bool packed);
+void launch_keys(const Engine& E, const uint32_t* edges, uint32_t nb, const uint32_t* negs, const KeySpace& ks);
+void launch_rank(const Engine& E, uint32_t n);
 void launch_contract_simt(Engine& E, uint32_t nb);
 void launch_contract_tc(Engine& E, uint32_t nb);
 void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj);
 void launch_loss(const Engine& E, uint32_t nb, float* loss_out);
-void launch_adagrad_segments(const Engine& E, const uint32_t* ukeys, const uint32_t* offsets, const uint32_t* counts,
-                             const uint32_t* nunique, const uint32_t* vals_sorted, const float* rows, uint32_t max_u,
-                             const PartView& pi, const PartView& pj, bool relations, uint32_t* ids_out,
-                             float* rows_out, bool apply);
+void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool apply, bool rel_dense,
+                     uint32_t* node_ids_out, float* node_rows_out, uint32_t* rel_ids_out, float* rel_rows_out);
 void launch_adagrad_rows(const Engine& E, const uint32_t* ids, const float* rows, uint32_t n, const PartView& pi,
                          const PartView& pj, bool relations);
 void launch_init_rows(cudaStream_t st, float* theta, float* acc, uint64_t first_row, uint64_t rows, uint32_t dim,

@@ -129,12 +129,14 @@ __global__ void k_softmax_rows(float* S, const float* fpos, float* lse, float* g
     }
 }
 
-__global__ void k_sum_parts(const float* parts, uint32_t nparts, uint64_t stride, uint64_t n, float* out) {
+// dN row k (negative slot 2nb + k) -> its sorted gradient position grows[rank[2nb + k]].
+__global__ void k_sum_parts(const float* parts, uint32_t nparts, uint64_t stride, uint64_t n, uint32_t d,
+                            const uint32_t* __restrict__ rank, uint32_t slot0, float* out) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     float acc = 0.f;
     for (uint32_t k = 0; k < nparts; ++k) acc += parts[k * stride + i];
-    out[i] = acc;
+    out[(uint64_t)rank[slot0 + i / d] * d + i % d] = acc;
 }
 
 }  // namespace
@@ -191,8 +193,9 @@ void launch_contract_simt(Engine& E, uint32_t nb) {
     n.ksplit = ks; n.part_stride = (int64_t)E.n_neg * d; n.alpha = 1.f;
     run_gemm(E, n, batches, st);
     const uint64_t total = (uint64_t)E.n_neg * d;
-    float* dN = s.grows + (uint64_t)2 * nb * d;
-    k_sum_parts<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(s.dN_part, ks, total, total, dN);
+    E.join_sorted();
+    k_sum_parts<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(s.dN_part, ks, total, total, (uint32_t)d, s.rank,
+                                                                  2 * nb, s.grows);
     EMBER_LAUNCHED(E);
 }
 

@@ -2,17 +2,19 @@
 //
 // Memory-bound kernels of the training step (everything but the dense contraction):
 //   k_sample          sample_negatives, SPEC.md:148-156 (counter-based, bit-exact with the oracle)
-//   k_gather_adjust   formBatch gather + "adjust" to per-side dot-product operands
-//   k_gather_negs     negative rows
-//   k_chain_rule      chain rule back through adjust
-//   k_batch_loss      deterministic loss reduction
-//   k_adagrad_segs    segmented sum of sorted gradient rows + sparse Adagrad
+//   k_gather_adjust   formBatch gather + "adjust" to per-side dot-product operands,
+//                     written as fp32 (SIMT engine) or straight into the tensor-core engine's
+//                     bf16 hi|lo operand layout
+//   k_gather_negs     negative rows, fp32 or packed
+//   k_keys / k_rank   gradient-slot keys for the (key, slot) sort and its inverse permutation
+//   k_chain_rule      chain rule back through adjust, rows written in sorted order
+//   k_loss            deterministic loss reduction (fixed-order partials, last block finishes)
+//   k_segments(_long) segmented sum of the sorted gradient rows + sparse Adagrad
 // Rows are dim floats (dim % 4 == 0) and are moved warp-per-row with 128-bit accesses.
 #include <cuda_runtime.h>
 
-#include <cub/cub.cuh>
-
 #include "engine.h"
+#include "tc_common.cuh"
 
 namespace ember {
 namespace {
@@ -48,14 +50,55 @@ __global__ void k_sample(uint32_t* out, uint32_t nt, uint32_t n_deg, uint32_t to
     out[slot] = id;
 }
 
-// One warp per edge: A[0][e] = adj_dst(s, r), A[1][e] = adj_src(r, t), fpos[e] = adj_dst . t.
-__global__ void k_gather_adjust(const uint32_t* __restrict__ edges, uint32_t nb, PartView pi, PartView pj,
-                                const float* __restrict__ rel, int kind, uint32_t d, float* __restrict__ A,
+// Adjusted vectors at coordinate k (ss/sr/st = source, relation, destination rows):
+//   ad = the row the destination is scored against (s o r; ComplEx s * r),
+//   as = the row the source is scored against      (r o t; ComplEx r * conj(t)),
+// so that f(s, r, t) = ad . t = s . as (ComplEx halves [re | im]).
+// Products are rounded individually (no FMA contraction), like the oracle.
+__device__ __forceinline__ void adjust_at(int kind, uint32_t d, uint32_t k, const float* ss, const float* sr,
+                                          const float* st, float& ad, float& as) {
+    if (k >= d) {
+        ad = as = 0.f;
+    } else if (kind == EMBER_DOT) {
+        ad = ss[k];
+        as = st[k];
+    } else if (kind == EMBER_DISTMULT) {
+        ad = __fmul_rn(ss[k], sr[k]);
+        as = __fmul_rn(sr[k], st[k]);
+    } else {
+        const uint32_t h = d / 2, kk = k < h ? k : k - h;
+        const float a = ss[kk], b = ss[h + kk], c = sr[kk], e = sr[h + kk], x = st[kk], y = st[h + kk];
+        if (k < h) {
+            ad = __fsub_rn(__fmul_rn(a, c), __fmul_rn(b, e));
+            as = __fadd_rn(__fmul_rn(c, x), __fmul_rn(e, y));
+        } else {
+            ad = __fadd_rn(__fmul_rn(a, e), __fmul_rn(b, c));
+            as = __fsub_rn(__fmul_rn(c, y), __fmul_rn(e, x));
+        }
+    }
+}
+
+// One warp per edge (rows up to rows_pad: the packed layout is zero-padded to 128-row tiles).
+// PACKED: lane l < KP/8 owns coordinates 8l..8l+7 and writes their bf16 hi|lo 16-byte core-matrix
+// rows for both sides; else fp32 rows A[0][e] = ad, A[1][e] = as. fpos[e] = ad . t.
+template <bool PACKED>
+__global__ void k_gather_adjust(const uint32_t* __restrict__ edges, uint32_t nb, uint32_t rows_pad, PartView pi,
+                                PartView pj, const float* __restrict__ rel, int kind, uint32_t d, uint32_t CB,
+                                uint32_t cap, float* __restrict__ A, uint16_t* __restrict__ Apk,
                                 float* __restrict__ fpos) {
     extern __shared__ float sm[];
     const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t e = blockIdx.x * (blockDim.x >> 5) + wib;
-    if (e >= nb) return;
+    if (e >= (PACKED ? rows_pad : nb)) return;
+    uint4* P = reinterpret_cast<uint4*>(Apk);
+    if (PACKED && e >= nb) {  // zero padding rows of the last 128-row tile
+        const uint4 z = make_uint4(0, 0, 0, 0);
+        for (uint32_t c = lane; c < 4 * CB; c += 32) {
+            const uint32_t side = c / (2 * CB), cb = c % (2 * CB);
+            P[((uint64_t)side * 2 * CB + cb) * cap + e] = z;
+        }
+        return;
+    }
     float* ss = sm + wib * 3 * d;
     float* sr = ss + d;
     float* st = sr + d;
@@ -64,52 +107,107 @@ __global__ void k_gather_adjust(const uint32_t* __restrict__ edges, uint32_t nb,
     warp_load_row(st, node_row(pj, t, d), d, lane);
     if (kind != EMBER_DOT) warp_load_row(sr, rel + (uint64_t)r * d, d, lane);
     __syncwarp();
-    float* ad = A + (uint64_t)e * d;
-    float* as = A + ((uint64_t)nb + e) * d;
     float part = 0.f;
-    if (kind == EMBER_COMPLEX) {
-        const uint32_t h = d / 2;
-        for (uint32_t k = lane; k < h; k += 32) {
-            const float a = ss[k], b = ss[h + k], c = sr[k], x = st[k], y = st[h + k];
-            const float ee = sr[h + k];
-            const float re = __fsub_rn(__fmul_rn(a, c), __fmul_rn(b, ee));
-            const float im = __fadd_rn(__fmul_rn(a, ee), __fmul_rn(b, c));
-            ad[k] = re;
-            ad[h + k] = im;
-            as[k] = __fadd_rn(__fmul_rn(c, x), __fmul_rn(ee, y));
-            as[h + k] = __fsub_rn(__fmul_rn(c, y), __fmul_rn(ee, x));
-            part += re * x + im * y;
+    if (PACKED) {
+        if (lane < CB) {
+            float xd[8], xs[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint32_t k = 8 * lane + i;
+                adjust_at(kind, d, k, ss, sr, st, xd[i], xs[i]);
+                part += k < d ? xd[i] * st[k] : 0.f;
+            }
+            uint4 h, l;
+            tc::split8(xd, h, l);
+            P[((uint64_t)0 * 2 * CB + lane) * cap + e] = h;
+            P[((uint64_t)0 * 2 * CB + CB + lane) * cap + e] = l;
+            tc::split8(xs, h, l);
+            P[((uint64_t)1 * 2 * CB + lane) * cap + e] = h;
+            P[((uint64_t)1 * 2 * CB + CB + lane) * cap + e] = l;
         }
     } else {
+        float* ad = A + (uint64_t)e * d;
+        float* as = A + ((uint64_t)nb + e) * d;
         for (uint32_t k = lane; k < d; k += 32) {
-            const float v = kind == EMBER_DOT ? ss[k] : __fmul_rn(ss[k], sr[k]);
-            ad[k] = v;
-            as[k] = kind == EMBER_DOT ? st[k] : __fmul_rn(sr[k], st[k]);
-            part += v * st[k];
+            float x, y;
+            adjust_at(kind, d, k, ss, sr, st, x, y);
+            ad[k] = x;
+            as[k] = y;
+            part += x * st[k];
         }
     }
     for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
     if (lane == 0) fpos[e] = part;
 }
 
-// Negative rows: slot -> N[slot] (side 0 rows come from partition j, side 1 from i).
-__global__ void k_gather_negs(const uint32_t* __restrict__ negs, uint32_t n, uint32_t nt, PartView pi, PartView pj,
-                              uint32_t d, float* __restrict__ N) {
+// Negative rows: slot -> row (side 0 rows come from partition j, side 1 from i).
+// PACKED: slots [0, 2 n_pad), zero past n_t per side; else fp32 N[slot] for slots < n.
+template <bool PACKED>
+__global__ void k_gather_negs(const uint32_t* __restrict__ negs, uint32_t n, uint32_t nt, uint32_t n_pad, PartView pi,
+                              PartView pj, uint32_t d, uint32_t CB, float* __restrict__ N, uint16_t* __restrict__ Npk) {
     const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (w >= n) return;
-    const uint32_t side = (w / nt) & 1u;
-    const float* src = node_row(side == 0 ? pj : pi, negs[w], d);
-    float4* dst = reinterpret_cast<float4*>(N + (uint64_t)w * d);
-    for (uint32_t v = lane; v < d / 4; v += 32) dst[v] = ldg4(src + 4 * v);
+    if (!PACKED) {
+        if (w >= n) return;
+        const uint32_t side = (w / nt) & 1u;
+        const float* src = node_row(side == 0 ? pj : pi, negs[w], d);
+        float4* dst = reinterpret_cast<float4*>(N + (uint64_t)w * d);
+        for (uint32_t v = lane; v < d / 4; v += 32) dst[v] = ldg4(src + 4 * v);
+        return;
+    }
+    if (w >= 2 * n_pad || lane >= CB) return;
+    const uint32_t side = w / n_pad, slot = w % n_pad;
+    float x[8];
+    if (slot < nt) {
+        const float* src = node_row(side == 0 ? pj : pi, negs[side * nt + slot], d);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = 8 * lane + i < d ? __ldg(src + 8 * lane + i) : 0.f;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = 0.f;
+    }
+    uint4 h, l;
+    tc::split8(x, h, l);
+    uint4* P = reinterpret_cast<uint4*>(Npk);
+    P[((uint64_t)side * 2 * CB + lane) * n_pad + slot] = h;
+    P[((uint64_t)side * 2 * CB + CB + lane) * n_pad + slot] = l;
 }
 
-// Chain rule (one warp per edge). dA excludes the positive term, added here:
-//   grad adj_dst = g0_dst * t + (P N)_dst,  grad adj_src = g0_src * s + (P N)_src
+__device__ __forceinline__ uint32_t node_key(const KeySpace& ks, uint32_t id) {
+    const uint64_t o = (uint64_t)id - ks.lo.first;
+    return o < ks.lo.rows ? (uint32_t)o : (uint32_t)(ks.lo.rows + ((uint64_t)id - ks.hi.first));
+}
+
+// keys[slot], vals[slot] = slot (slot layout: engine.h).
+__global__ void k_keys(const uint32_t* __restrict__ edges, uint32_t nb, const uint32_t* __restrict__ negs,
+                       uint32_t n_neg, uint32_t n_slots, KeySpace ks, uint32_t* keys, uint32_t* vals,
+                       uint32_t* longs) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) *longs = 0u;  // long-segment list of this step's reduction
+    if (i >= n_slots) return;
+    uint32_t k;
+    if (i < nb) k = node_key(ks, edges[3 * i]);
+    else if (i < 2 * nb) k = node_key(ks, edges[3 * (i - nb) + 2]);
+    else if (i < 2 * nb + n_neg) k = node_key(ks, negs[i - 2 * nb]);
+    else k = (uint32_t)ks.node_range + edges[3 * (i - 2 * nb - n_neg) + 1];
+    keys[i] = k;
+    vals[i] = i;
+}
+
+__global__ void k_rank(const uint32_t* __restrict__ vals_sorted, uint32_t n, uint32_t* __restrict__ rank) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) rank[vals_sorted[p]] = p;
+}
+
+// Chain rule (one warp per edge), adjusted vectors recomputed from the staged rows. dA excludes
+// the positive term, added here:
+//   grad adj_dst = g0_dst * t + dA_dst,  grad adj_src = g0_src * s + dA_src,
 //   grad t += g0_dst * adj_dst (positive score = adj_dst . t), grad s += g0_src * adj_src.
-__global__ void k_chain_rule(const uint32_t* __restrict__ edges, uint32_t nb, PartView pi, PartView pj,
-                             const float* __restrict__ rel, int kind, uint32_t d, const float* __restrict__ A,
-                             const float* __restrict__ dA, const float* __restrict__ g0, float* __restrict__ grows,
-                             float* __restrict__ rrows) {
+// Rows go to their sorted positions: source -> grows[rank[e]], destination -> grows[rank[nb + e]],
+// relation -> grows[rank[2nb + n_neg + e]].
+__global__ void k_chain_rule(const uint32_t* __restrict__ edges, uint32_t nb, uint32_t n_neg, PartView pi,
+                             PartView pj, const float* __restrict__ rel, int kind, uint32_t d,
+                             const float* __restrict__ dA, const float* __restrict__ g0,
+                             const uint32_t* __restrict__ rank, float* __restrict__ grows) {
     extern __shared__ float sm[];
     const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t e = blockIdx.x * (blockDim.x >> 5) + wib;
@@ -123,46 +221,55 @@ __global__ void k_chain_rule(const uint32_t* __restrict__ edges, uint32_t nb, Pa
     if (kind != EMBER_DOT) warp_load_row(sr, rel + (uint64_t)r * d, d, lane);
     __syncwarp();
     const float gd = g0[e], gs = g0[(uint64_t)nb + e];
-    const float* ad = A + (uint64_t)e * d;
-    const float* as = A + ((uint64_t)nb + e) * d;
     const float* u = dA + (uint64_t)e * d;
     const float* w = dA + ((uint64_t)nb + e) * d;
-    float* gS = grows + (uint64_t)e * d;
-    float* gT = grows + ((uint64_t)nb + e) * d;
-    float* gR = rrows + (uint64_t)e * d;
+    float* gS = grows + (uint64_t)rank[e] * d;
+    float* gT = grows + (uint64_t)rank[nb + e] * d;
     if (kind == EMBER_COMPLEX) {
+        float* gR = grows + (uint64_t)rank[2 * nb + n_neg + e] * d;
         const uint32_t h = d / 2;
         for (uint32_t k = lane; k < h; k += 32) {
             const float a = ss[k], b = ss[h + k], c = sr[k], ee = sr[h + k], x = st[k], y = st[h + k];
+            float ad0, as0, ad1, as1;
+            adjust_at(kind, d, k, ss, sr, st, ad0, as0);
+            adjust_at(kind, d, h + k, ss, sr, st, ad1, as1);
             const float u0 = u[k] + gd * x, u1 = u[h + k] + gd * y;
             const float w0 = w[k] + gs * a, w1 = w[h + k] + gs * b;
-            gS[k] = gs * as[k] + (u0 * c + u1 * ee);
-            gS[h + k] = gs * as[h + k] + (u1 * c - u0 * ee);
+            gS[k] = gs * as0 + (u0 * c + u1 * ee);
+            gS[h + k] = gs * as1 + (u1 * c - u0 * ee);
             gR[k] = (u0 * a + u1 * b) + (w0 * x + w1 * y);
             gR[h + k] = (u1 * a - u0 * b) + (w0 * y - w1 * x);
-            gT[k] = gd * ad[k] + (w0 * c - w1 * ee);
-            gT[h + k] = gd * ad[h + k] + (w0 * ee + w1 * c);
+            gT[k] = gd * ad0 + (w0 * c - w1 * ee);
+            gT[h + k] = gd * ad1 + (w0 * ee + w1 * c);
         }
     } else if (kind == EMBER_DISTMULT) {
+        float* gR = grows + (uint64_t)rank[2 * nb + n_neg + e] * d;
         for (uint32_t k = lane; k < d; k += 32) {
+            float ad, as;
+            adjust_at(kind, d, k, ss, sr, st, ad, as);
             const float uk = u[k] + gd * st[k], wk = w[k] + gs * ss[k];
-            gS[k] = gs * as[k] + uk * sr[k];
+            gS[k] = gs * as + uk * sr[k];
             gR[k] = uk * ss[k] + wk * st[k];
-            gT[k] = gd * ad[k] + wk * sr[k];
+            gT[k] = gd * ad + wk * sr[k];
         }
     } else {
         for (uint32_t k = lane; k < d; k += 32) {
-            gS[k] = gs * as[k] + (u[k] + gd * st[k]);
-            gT[k] = gd * ad[k] + (w[k] + gs * ss[k]);
+            gS[k] = gs * st[k] + (u[k] + gd * st[k]);
+            gT[k] = gd * ss[k] + (w[k] + gs * ss[k]);
         }
     }
 }
 
-// loss = (1/nb) sum_e (lse_dst - f) + (lse_src - f), one block, fixed order.
-__global__ void k_batch_loss(const float* lse, const float* fpos, uint32_t nb, float* out) {
-    __shared__ double red[1024];
+// loss = (1/nb) sum_e (lse_dst - f) + (lse_src - f): each block sums a contiguous range in a fixed
+// order, the last block to finish adds the block partials in index order (deterministic).
+constexpr uint32_t LOSS_THREADS = 512;
+__global__ void k_loss(const float* __restrict__ lse, const float* __restrict__ fpos, uint32_t nb, uint32_t per_block,
+                       double* __restrict__ part, uint32_t* __restrict__ done, float* __restrict__ out) {
+    __shared__ double red[LOSS_THREADS];
+    __shared__ bool last;
+    const uint32_t b0 = blockIdx.x * per_block, b1 = min(nb, b0 + per_block);
     double acc = 0.0;
-    for (uint32_t e = threadIdx.x; e < nb; e += blockDim.x)
+    for (uint32_t e = b0 + threadIdx.x; e < b1; e += blockDim.x)
         acc += (double)(lse[e] - fpos[e]) + (double)(lse[(uint64_t)nb + e] - fpos[e]);
     red[threadIdx.x] = acc;
     __syncthreads();
@@ -170,27 +277,18 @@ __global__ void k_batch_loss(const float* lse, const float* fpos, uint32_t nb, f
         if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
         __syncthreads();
     }
-    if (threadIdx.x == 0) out[0] = (float)(red[0] / (double)nb);
-}
-
-__global__ void k_node_keys(const uint32_t* __restrict__ edges, uint32_t nb, const uint32_t* __restrict__ negs,
-                            uint32_t n_neg, uint32_t* keys, uint32_t* vals) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t n = 2 * nb + n_neg;
-    if (i >= n) return;
-    uint32_t k;
-    if (i < nb) k = edges[3 * i];
-    else if (i < 2 * nb) k = edges[3 * (i - nb) + 2];
-    else k = negs[i - 2 * nb];
-    keys[i] = k;
-    vals[i] = i;
-}
-
-__global__ void k_rel_keys(const uint32_t* __restrict__ edges, uint32_t nb, uint32_t* keys, uint32_t* vals) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nb) return;
-    keys[i] = edges[3 * i + 1];
-    vals[i] = i;
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = red[0];
+        __threadfence();
+        last = atomicAdd(done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    __threadfence();
+    double tot = 0.0;
+    for (uint32_t b = 0; b < gridDim.x; ++b) tot += ((volatile double*)part)[b];
+    out[0] = (float)(tot / (double)nb);
+    *done = 0u;
 }
 
 __device__ __forceinline__ float adagrad_elem(float& th, float& ac, float g, float lr, float eps) {
@@ -200,90 +298,157 @@ __device__ __forceinline__ float adagrad_elem(float& th, float& ac, float g, flo
     return th;
 }
 
-// Segmented sum in two deterministic passes so hot ids (Zipf relations, power-law nodes) are not
-// serialised on one warp: every segment is cut into chunks of <= kChunk sorted rows.
-constexpr uint32_t kChunk = 32;
+struct SegArgs {
+    const uint32_t* ukeys;
+    const uint32_t* offsets;
+    const uint32_t* counts;
+    const uint32_t* nruns;
+    uint32_t* nunique;   // [2] written: node uniques, relation uniques
+    uint32_t* longs;     // [0] count, [1..] unique indices of long segments
+    const float* rows;   // sorted gradient rows
+    KeySpace ks;
+    float* rel_theta;
+    float* rel_acc;
+    float* rel_dense;    // non-null: relation sums go here (summed over ranks later), no Adagrad
+    uint32_t d;
+    float lr, eps;
+    int apply;
+    uint32_t* node_ids_out;
+    float* node_rows_out;
+    uint32_t* rel_ids_out;
+    float* rel_rows_out;
+};
 
-__global__ void k_chunk_counts(const uint32_t* __restrict__ counts, const uint32_t* __restrict__ nunique, uint32_t n,
-                               uint32_t* cc) {
-    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= n) return;
-    cc[u] = u < *nunique ? (counts[u] + kChunk - 1) / kChunk : 0u;
-}
+constexpr uint32_t LONG_SEG = 48;  // longer segments go to the block-per-segment kernel
 
-// Pass 1: one warp per chunk sums its rows (ascending sorted position) into partial[chunk].
-__global__ void k_chunk_sum(const uint32_t* __restrict__ coff, const uint32_t* __restrict__ offsets,
-                            const uint32_t* __restrict__ counts, const uint32_t* __restrict__ nunique,
-                            const uint32_t* __restrict__ vals, const float* __restrict__ rows, uint32_t d,
-                            float* __restrict__ partial) {
-    const uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    const uint32_t nu = *nunique;
-    if (nu == 0) return;
-    const uint32_t total = coff[nu - 1] + (counts[nu - 1] + kChunk - 1) / kChunk;
-    if (g >= total) return;
-    uint32_t lo = 0, hi = nu - 1;  // last segment whose first chunk is <= g
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi + 1) >> 1;
-        if (coff[mid] <= g) lo = mid;
-        else hi = mid - 1;
-    }
-    const uint32_t r0 = offsets[lo] + (g - coff[lo]) * kChunk;
-    const uint32_t r1 = min(r0 + kChunk, offsets[lo] + counts[lo]);
-    const uint32_t cnt = r1 - r0;
-    const uint32_t my = lane < cnt ? vals[r0 + lane] : 0u;
-    for (uint32_t base = 0; base < d / 4; base += 32) {  // all lanes stay converged for the shuffles
-        const uint32_t c4 = base + lane;
-        const bool live = c4 < d / 4;
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 4
-        for (uint32_t c = 0; c < cnt; ++c) {
-            const uint32_t idx = __shfl_sync(0xffffffffu, my, c);
-            if (live) {
-                const float4 x = ldg4(rows + (uint64_t)idx * d + 4 * c4);
-                acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
-            }
-        }
-        if (live) reinterpret_cast<float4*>(partial + (uint64_t)g * d)[c4] = acc;
-    }
-}
-
-// Pass 2: one warp per unique id sums its chunk partials in order, then Adagrad (or exports).
-__global__ void k_adagrad_segs(const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ coff,
-                               const uint32_t* __restrict__ counts, const uint32_t* __restrict__ nunique,
-                               const float* __restrict__ partial, uint32_t d, PartView pi, PartView pj, int relations,
-                               float* rel_theta, float* rel_acc, float lr, float eps, uint32_t* ids_out,
-                               float* rows_out, int apply) {
-    const uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (u >= *nunique) return;
-    const uint32_t key = ukeys[u], beg = coff[u], cnt = (counts[u] + kChunk - 1) / kChunk;
+// Where unique key u's summed row goes: Adagrad target (th, ac) or export/dense destination.
+struct SegTarget {
     float* th;
     float* ac;
-    if (relations) {
-        th = rel_theta + (uint64_t)key * d;
-        ac = rel_acc + (uint64_t)key * d;
-    } else {
-        const PartView& v = (key - pi.first < pi.rows) ? pi : pj;
-        th = v.theta + (uint64_t)(key - v.first) * d;
-        ac = v.acc + (uint64_t)(key - v.first) * d;
+    float* out;  // export / dense row (may be null)
+    bool node;
+};
+
+__device__ __forceinline__ uint32_t n_node_unique(const SegArgs& a, uint32_t nr) {
+    uint32_t lo = 0, hi = nr;  // first u with key >= node_range
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (a.ukeys[mid] < a.ks.node_range) lo = mid + 1;
+        else hi = mid;
     }
-    if (ids_out && lane == 0) ids_out[u] = key;
-    for (uint32_t c4 = lane; c4 < d / 4; c4 += 32) {
-        float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 4
-        for (uint32_t c = 0; c < cnt; ++c) {
-            const float4 x = ldg4(partial + (uint64_t)(beg + c) * d + 4 * c4);
-            g.x += x.x; g.y += x.y; g.z += x.z; g.w += x.w;
+    return lo;
+}
+
+__device__ __forceinline__ SegTarget seg_target(const SegArgs& a, uint32_t u, uint32_t nr, bool write_id) {
+    SegTarget t{nullptr, nullptr, nullptr, true};
+    const uint32_t key = a.ukeys[u];
+    const uint32_t d = a.d;
+    if (key < a.ks.node_range) {
+        const bool lo = key < a.ks.lo.rows;
+        const PartView& v = lo ? a.ks.lo : a.ks.hi;
+        const uint64_t row = lo ? key : key - a.ks.lo.rows;
+        t.th = v.theta + row * d;
+        t.ac = v.acc + row * d;
+        if (!a.apply) {
+            if (a.node_rows_out) t.out = a.node_rows_out + (uint64_t)u * d;
+            if (write_id && a.node_ids_out) a.node_ids_out[u] = (uint32_t)(v.first + row);
         }
-        if (rows_out) reinterpret_cast<float4*>(rows_out + (uint64_t)u * d)[c4] = g;
-        if (!apply) continue;
-        float4 t = reinterpret_cast<float4*>(th)[c4];
-        float4 a = reinterpret_cast<float4*>(ac)[c4];
-        adagrad_elem(t.x, a.x, g.x, lr, eps);
-        adagrad_elem(t.y, a.y, g.y, lr, eps);
-        adagrad_elem(t.z, a.z, g.z, lr, eps);
-        adagrad_elem(t.w, a.w, g.w, lr, eps);
-        reinterpret_cast<float4*>(th)[c4] = t;
-        reinterpret_cast<float4*>(ac)[c4] = a;
+    } else {
+        t.node = false;
+        const uint32_t r = key - (uint32_t)a.ks.node_range;
+        t.th = a.rel_theta + (uint64_t)r * d;
+        t.ac = a.rel_acc + (uint64_t)r * d;
+        if (a.rel_dense) {
+            t.out = a.rel_dense + (uint64_t)r * d;
+        } else if (!a.apply) {
+            const uint32_t k = u - n_node_unique(a, nr);
+            if (a.rel_rows_out) t.out = a.rel_rows_out + (uint64_t)k * d;
+            if (write_id && a.rel_ids_out) a.rel_ids_out[k] = r;
+        }
+    }
+    return t;
+}
+
+__device__ __forceinline__ void seg_finish(const SegArgs& a, const SegTarget& t, uint32_t c4, float4 g) {
+    if (t.out) reinterpret_cast<float4*>(t.out)[c4] = g;
+    const bool do_apply = a.apply && !(!t.node && a.rel_dense);
+    if (!do_apply) return;
+    float4 th = reinterpret_cast<float4*>(t.th)[c4];
+    float4 ac = reinterpret_cast<float4*>(t.ac)[c4];
+    adagrad_elem(th.x, ac.x, g.x, a.lr, a.eps);
+    adagrad_elem(th.y, ac.y, g.y, a.lr, a.eps);
+    adagrad_elem(th.z, ac.z, g.z, a.lr, a.eps);
+    adagrad_elem(th.w, ac.w, g.w, a.lr, a.eps);
+    reinterpret_cast<float4*>(t.th)[c4] = th;
+    reinterpret_cast<float4*>(t.ac)[c4] = ac;
+}
+
+// One warp per unique key: sum its contiguous rows (slot order) and apply Adagrad / export.
+__global__ void k_segments(SegArgs a) {
+    const uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const uint32_t nr = *a.nruns;
+    if (u >= nr) return;
+    const uint32_t key = a.ukeys[u];
+    if (lane == 0 && key < a.ks.node_range && (u + 1 == nr || a.ukeys[u + 1] >= a.ks.node_range)) {
+        a.nunique[0] = u + 1;
+        a.nunique[1] = nr - (u + 1);
+    }
+    const uint32_t off = a.offsets[u], cnt = a.counts[u];
+    if (cnt > LONG_SEG) {
+        if (lane == 0) a.longs[1 + atomicAdd(a.longs, 1u)] = u;
+        return;
+    }
+    const SegTarget t = seg_target(a, u, nr, lane == 0);
+    const float* base = a.rows + (uint64_t)off * a.d;
+    for (uint32_t c4 = lane; c4 < a.d / 4; c4 += 32) {
+        float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (uint32_t r = 0; r < cnt; ++r) {  // fixed (slot) order
+            const float4 x = ldg4(base + (uint64_t)r * a.d + 4 * c4);
+            s0.x += x.x;
+            s0.y += x.y;
+            s0.z += x.z;
+            s0.w += x.w;
+        }
+        seg_finish(a, t, c4, s0);
+    }
+}
+
+// One block (8 warps) per long segment: warp w sums rows w, w + 8, ... (fixed order), then the 8
+// partials are added in warp order. Hot relations (Zipf) and hub nodes land here.
+__global__ void __launch_bounds__(256) k_segments_long(SegArgs a) {
+    extern __shared__ float4 part[];  // [8][d/4]
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t n_long = *(volatile uint32_t*)a.longs, nr = *a.nruns;
+    const uint32_t d4 = a.d / 4;
+    for (uint32_t li = blockIdx.x; li < n_long; li += gridDim.x) {
+        const uint32_t u = a.longs[1 + li];
+        const uint32_t off = a.offsets[u], cnt = a.counts[u];
+        const float* base = a.rows + (uint64_t)off * a.d;
+        for (uint32_t c4 = lane; c4 < d4; c4 += 32) {
+            float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (uint32_t r = warp; r < cnt; r += 8) {
+                const float4 x = ldg4(base + (uint64_t)r * a.d + 4 * c4);
+                s0.x += x.x;
+                s0.y += x.y;
+                s0.z += x.z;
+                s0.w += x.w;
+            }
+            part[warp * d4 + c4] = s0;
+        }
+        __syncthreads();
+        const SegTarget t = seg_target(a, u, nr, threadIdx.x == 0);
+        for (uint32_t c4 = threadIdx.x; c4 < d4; c4 += blockDim.x) {
+            float4 g = part[c4];
+            for (uint32_t w = 1; w < 8; ++w) {
+                const float4 x = part[w * d4 + c4];
+                g.x += x.x;
+                g.y += x.y;
+                g.z += x.z;
+                g.w += x.w;
+            }
+            seg_finish(a, t, c4, g);
+        }
+        __syncthreads();
     }
 }
 
@@ -346,62 +511,89 @@ void launch_sample(const Engine& E, uint32_t* out, uint64_t base, const uint32_t
     EMBER_LAUNCHED(E);
 }
 
-void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj) {
+void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj,
+                          bool packed) {
     const uint32_t warps = 8;
     const size_t sm = (size_t)warps * 3 * E.dim * sizeof(float);
-    k_gather_adjust<<<(nb + warps - 1) / warps, warps * 32, sm, E.stream>>>(edges, nb, pi, pj, E.rel_theta, E.m.kind,
-                                                                             E.dim, E.s.A, E.s.fpos);
+    if (packed) {
+        const uint32_t rows_pad = (nb + 127) / 128 * 128;
+        k_gather_adjust<true><<<(rows_pad + warps - 1) / warps, warps * 32, sm, E.stream>>>(
+            edges, nb, rows_pad, pi, pj, E.rel_theta, E.m.kind, E.dim, E.CB, E.b_cap, nullptr, E.s.Apk, E.s.fpos);
+    } else {
+        k_gather_adjust<false><<<(nb + warps - 1) / warps, warps * 32, sm, E.stream>>>(
+            edges, nb, nb, pi, pj, E.rel_theta, E.m.kind, E.dim, 0, 0, E.s.A, nullptr, E.s.fpos);
+    }
     EMBER_LAUNCHED(E);
 }
 
-void launch_gather_negatives(const Engine& E, const uint32_t* negs, const PartView& pi, const PartView& pj) {
+void launch_gather_negatives(const Engine& E, const uint32_t* negs, const PartView& pi, const PartView& pj,
+                             bool packed) {
     if (!E.n_neg) return;
-    k_gather_negs<<<(E.n_neg * 32 + 255) / 256, 256, 0, E.stream>>>(negs, E.n_neg, E.nt, pi, pj, E.dim, E.s.N);
+    const uint32_t warps = packed ? 2 * E.n_pad : E.n_neg;
+    if (packed)
+        k_gather_negs<true><<<(warps * 32 + 255) / 256, 256, 0, E.stream>>>(negs, E.n_neg, E.nt, E.n_pad, pi, pj, E.dim,
+                                                                            E.CB, nullptr, E.s.Npk);
+    else
+        k_gather_negs<false><<<(warps * 32 + 255) / 256, 256, 0, E.stream>>>(negs, E.n_neg, E.nt, 0, pi, pj, E.dim, 0,
+                                                                             E.s.N, nullptr);
+    EMBER_LAUNCHED(E);
+}
+
+void launch_keys(const Engine& E, const uint32_t* edges, uint32_t nb, const uint32_t* negs, const KeySpace& ks) {
+    const uint32_t n = E.slots(nb);
+    k_keys<<<(n + 255) / 256, 256, 0, E.side>>>(edges, nb, negs, E.n_neg, n, ks, E.s.keys, E.s.vals, E.s.longs);
+    EMBER_LAUNCHED(E);
+}
+
+void launch_rank(const Engine& E, uint32_t n) {
+    k_rank<<<(n + 255) / 256, 256, 0, E.side>>>(E.s.vals_sorted, n, E.s.rank);
     EMBER_LAUNCHED(E);
 }
 
 void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj) {
     const uint32_t warps = 8;
     const size_t sm = (size_t)warps * 3 * E.dim * sizeof(float);
-    k_chain_rule<<<(nb + warps - 1) / warps, warps * 32, sm, E.stream>>>(edges, nb, pi, pj, E.rel_theta, E.m.kind,
-                                                                          E.dim, E.s.A, E.s.dA, E.s.g0, E.s.grows,
-                                                                          E.s.rrows);
+    k_chain_rule<<<(nb + warps - 1) / warps, warps * 32, sm, E.stream>>>(edges, nb, E.n_neg, pi, pj, E.rel_theta,
+                                                                          E.m.kind, E.dim, E.s.dA, E.s.g0, E.s.rank,
+                                                                          E.s.grows);
     EMBER_LAUNCHED(E);
 }
 
 void launch_loss(const Engine& E, uint32_t nb, float* loss_out) {
-    k_batch_loss<<<1, 1024, 0, E.stream>>>(E.s.lse, E.s.fpos, nb, loss_out);
+    const uint32_t per = 4096;
+    const uint32_t blocks = (nb + per - 1) / per;
+    k_loss<<<blocks, LOSS_THREADS, 0, E.stream>>>(E.s.lse, E.s.fpos, nb, per, reinterpret_cast<double*>(E.s.loss_part),
+                                                 E.s.loss_done, loss_out);
     EMBER_LAUNCHED(E);
 }
 
-void launch_node_keys(const Engine& E, const uint32_t* edges, uint32_t nb, const uint32_t* negs) {
-    const uint32_t n = 2 * nb + E.n_neg;
-    k_node_keys<<<(n + 255) / 256, 256, 0, E.stream>>>(edges, nb, negs, E.n_neg, E.s.keys, E.s.vals);
+void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool apply, bool rel_dense,
+                     uint32_t* node_ids_out, float* node_rows_out, uint32_t* rel_ids_out, float* rel_rows_out) {
+    if (!n_slots) return;
+    SegArgs a{};
+    a.ukeys = E.s.ukeys;
+    a.offsets = E.s.offsets;
+    a.counts = E.s.counts;
+    a.nruns = E.s.nruns;
+    a.nunique = E.s.nunique;
+    a.longs = E.s.longs;
+    a.rows = E.s.grows;
+    a.ks = ks;
+    a.rel_theta = E.rel_theta;
+    a.rel_acc = E.rel_acc;
+    a.rel_dense = rel_dense ? E.s.rel_dense : nullptr;
+    a.d = E.dim;
+    a.lr = E.m.lr;
+    a.eps = E.m.eps;
+    a.apply = apply ? 1 : 0;
+    a.node_ids_out = node_ids_out;
+    a.node_rows_out = node_rows_out;
+    a.rel_ids_out = rel_ids_out;
+    a.rel_rows_out = rel_rows_out;
+    k_segments<<<(n_slots * 32 + 255) / 256, 256, 0, E.stream>>>(a);
     EMBER_LAUNCHED(E);
-}
-
-void launch_rel_keys(const Engine& E, const uint32_t* edges, uint32_t nb) {
-    k_rel_keys<<<(nb + 255) / 256, 256, 0, E.stream>>>(edges, nb, E.s.keys, E.s.vals);
-    EMBER_LAUNCHED(E);
-}
-
-void launch_adagrad_segments(const Engine& E, const uint32_t* ukeys, const uint32_t* offsets, const uint32_t* counts,
-                             const uint32_t* nunique, const uint32_t* vals_sorted, const float* rows, uint32_t max_u,
-                             const PartView& pi, const PartView& pj, bool relations, uint32_t* ids_out,
-                             float* rows_out, bool apply) {
-    if (!max_u) return;
-    const unsigned wblocks = (max_u * 32 + 255) / 256;
-    k_chunk_counts<<<(max_u + 255) / 256, 256, 0, E.stream>>>(counts, nunique, max_u, E.s.cc);
-    EMBER_LAUNCHED(E);
-    size_t bytes = E.s.cub_bytes;
-    EMBER_CUDA(cub::DeviceScan::ExclusiveSum(E.s.cub_tmp, bytes, E.s.cc, E.s.coff, (int)max_u, E.stream));
-    ++E.lib_calls;
-    k_chunk_sum<<<wblocks, 256, 0, E.stream>>>(E.s.coff, offsets, counts, nunique, vals_sorted, rows, E.dim,
-                                               E.s.partial);
-    EMBER_LAUNCHED(E);
-    k_adagrad_segs<<<wblocks, 256, 0, E.stream>>>(ukeys, E.s.coff, counts, nunique, E.s.partial, E.dim, pi, pj,
-                                                  relations ? 1 : 0, E.rel_theta, E.rel_acc, E.m.lr, E.m.eps, ids_out,
-                                                  rows_out, apply ? 1 : 0);
+    const size_t sm = (size_t)8 * E.dim * sizeof(float);
+    k_segments_long<<<2 * E.sm_count, 256, sm, E.stream>>>(a);
     EMBER_LAUNCHED(E);
 }
 
@@ -423,8 +615,8 @@ void launch_init_rows(cudaStream_t st, float* theta, float* acc, uint64_t first,
 
 void launch_debug_scores(const Engine& E, const uint32_t* edges, uint32_t nb, const uint32_t* negs, int side,
                          uint32_t rows, float* out, const PartView& pi, const PartView& pj) {
-    launch_gather_adjust(E, edges, nb, pi, pj);
-    launch_gather_negatives(E, negs, pi, pj);
+    launch_gather_adjust(E, edges, nb, pi, pj, false);
+    launch_gather_negatives(E, negs, pi, pj, false);
     const float* A = E.s.A + (uint64_t)side * nb * E.dim;
     const float* N = E.s.N + (uint64_t)side * E.nt * E.dim;
     const uint32_t w = rows * E.nt;

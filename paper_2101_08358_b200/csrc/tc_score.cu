@@ -482,35 +482,44 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 // Exact two-pass recomputation (fp32, CUDA cores) of the rows k_tc<MODE_ROWS> flagged because
 // sum exp(S - f_pos) left the safe range (a negative scoring > f_pos + ~55). One block; normally
 // the list is empty and the kernel exits at once. Resets the list for the next step.
-__global__ void k_tc_fixup(TcArgs g, const float* __restrict__ A, const float* __restrict__ N) {
+__device__ __forceinline__ float packed_at(const uint16_t* pk, int cap, int CB, int side, int row, int c) {
+    const size_t hi = (((size_t)side * 2 * CB + c / 8) * cap + row) * 8 + c % 8;
+    const size_t lo = hi + (size_t)CB * cap * 8;
+    return __bfloat162float(__ushort_as_bfloat16(pk[hi])) + __bfloat162float(__ushort_as_bfloat16(pk[lo]));
+}
+
+__global__ void k_tc_fixup(TcArgs g, const uint16_t* __restrict__ Apk, const uint16_t* __restrict__ Npk) {
     const uint32_t n = *(volatile uint32_t*)g.flags;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (uint32_t f = warp; f < n; f += nw) {
         const uint32_t code = g.flags[1 + f];
         const int side = (int)(code / g.b_cap), row = (int)(code % g.b_cap);
-        const float* a = A + ((size_t)side * g.nb + row) * g.d;
-        const float* Nn = N + (size_t)side * g.nt * g.d;
+        // operands as the tensor cores saw them (hi + lo), rows of at most 128 floats: 4 per lane
+        float a[4], nv[4];
+        for (int c = lane, i = 0; i < 4; c += 32, ++i) a[i] = c < g.d ? packed_at(Apk, g.b_cap, g.CB, side, row, c) : 0.f;
         const float fp = g.fpos[row];
-        float mx = fp;
-        for (int k = 0; k < g.nt; ++k) {
+        auto score = [&](int k) {
             float s = 0.f;
-            for (int c = lane; c < g.d; c += 32) s += a[c] * Nn[(size_t)k * g.d + c];
+            for (int c = lane, i = 0; i < 4; c += 32, ++i) {
+                nv[i] = c < g.d ? packed_at(Npk, g.n_pad, g.CB, side, k, c) : 0.f;
+                s += a[i] * nv[i];
+            }
             for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            mx = fmaxf(mx, s);
-        }
+            return s;
+        };
+        float mx = fp;
+        for (int k = 0; k < g.nt; ++k) mx = fmaxf(mx, score(k));
         float z = expf(fp - mx), acc[4] = {0.f, 0.f, 0.f, 0.f};
         for (int k = 0; k < g.nt; ++k) {
-            float s = 0.f;
-            for (int c = lane; c < g.d; c += 32) s += a[c] * Nn[(size_t)k * g.d + c];
-            for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            const float p = expf(s - mx);
+            const float p = expf(score(k) - mx);
             z += p;
-            for (int c = lane, i = 0; c < g.d; c += 32, ++i) acc[i] += p * Nn[(size_t)k * g.d + c];
+            for (int i = 0; i < 4; ++i) acc[i] += p * nv[i];
         }
         const float lse = mx + logf(z);
         const float scale = g.inv_b / z;
         float* out = g.dA + ((size_t)side * g.nb + row) * g.d;
-        for (int c = lane, i = 0; c < g.d; c += 32, ++i) out[c] = acc[i] * scale;
+        for (int c = lane, i = 0; i < 4; c += 32, ++i)
+            if (c < g.d) out[c] = acc[i] * scale;
         if (lane == 0) {
             g.lse[(size_t)side * g.nb + row] = lse;
             g.lse_pad[(size_t)side * g.b_cap + row] = fmaf(-lse, L2E, g.log2_inv_b);
@@ -522,33 +531,13 @@ __global__ void k_tc_fixup(TcArgs g, const float* __restrict__ A, const float* _
 }
 
 // =========================================================================================
-// Operand packing and the dN reduction (memory-bound helpers).
+// The dN reduction (memory-bound helper; the operands are packed by the gathers, kernels_step.cu).
 // =========================================================================================
 
-// src [2 sides][rows][d] fp32 (side stride side_stride floats) -> dst [2][2CB][cap][8] bf16 hi|lo.
-// One thread per (side, cb, row); rows in [0, rows_pad) (zero past `rows`).
-__global__ void k_pack(const float* __restrict__ src, uint64_t side_stride, int rows, int rows_pad, int cap, int d,
-                       int CB, uint16_t* __restrict__ dst) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t per_side = (int64_t)CB * rows_pad;
-    if (t >= 2 * per_side) return;
-    const int side = (int)(t / per_side);
-    const int rem = (int)(t % per_side);
-    const int cb = rem / rows_pad, row = rem % rows_pad;
-    float x[8];
-    const float* p = src + side * side_stride + (size_t)row * d + cb * 8;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = (row < rows && cb * 8 + i < d) ? p[i] : 0.f;
-    uint4 hi, lo;
-    tc::split8(x, hi, lo);
-    uint4* out = reinterpret_cast<uint4*>(dst);
-    const size_t base = (size_t)side * 2 * CB * cap;
-    out[base + (size_t)cb * cap + row] = hi;
-    out[base + (size_t)(CB + cb) * cap + row] = lo;
-}
-
+// dN rows summed over chunks in fixed order; row (side, n) is gradient slot 2nb + side*nt + n and
+// goes to its sorted position grows[rank[slot]].
 __global__ void k_dn_reduce(const float* __restrict__ part, int chunks, int nt, int n_pad, int d,
-                            float* __restrict__ out) {
+                            const uint32_t* __restrict__ rank, uint32_t slot0, float* __restrict__ out) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t per_side = (int64_t)nt * d;
     if (t >= 2 * per_side) return;
@@ -557,7 +546,7 @@ __global__ void k_dn_reduce(const float* __restrict__ part, int chunks, int nt, 
     const int n = rem / d, k = rem % d;
     float acc = 0.f;
     for (int c = 0; c < chunks; ++c) acc += part[(((size_t)c * 2 + side) * n_pad + n) * d + k];
-    out[t] = acc;
+    out[(size_t)rank[slot0 + side * nt + n] * d + k] = acc;
 }
 
 // ---- tensor maps (driver entry point fetched through the runtime: no libcuda link) ---------
@@ -600,8 +589,6 @@ CUtensorMap make_map(uint16_t* base, int cap, int CB, int box_rows) {
 // Engine-side state of the tensor-core engine (allocated once per context).
 struct TcState {
     int KP = 0, CB = 0, b_cap = 0, n_pad = 0, chunks2 = 1, nstage = 4;
-    uint16_t* A = nullptr;   // [2][2CB][b_cap][8]
-    uint16_t* N = nullptr;   // [2][2CB][n_pad][8]
     float* dN_part = nullptr;
     float* lse_pad = nullptr;
     uint32_t* flags = nullptr;
@@ -622,10 +609,10 @@ bool tc_engine_supported(const Engine& E) {
 
 void tc_setup(Engine& E) {
     auto* t = new TcState();
-    t->KP = (int)((E.dim + 15) / 16 * 16);
-    t->CB = t->KP / 8;
-    t->b_cap = (int)((E.cap_b + RES - 1) / RES * RES);
-    t->n_pad = (int)((E.nt + RES - 1) / RES * RES);
+    t->KP = E.KP;  // packed operands (E.s.Apk / E.s.Npk) are allocated by the engine
+    t->CB = E.CB;
+    t->b_cap = E.b_cap;
+    t->n_pad = E.n_pad;
     const int ntl = t->n_pad / RES;
     t->chunks2 = std::max(1, E.sm_count / (2 * ntl));
     t->nstage = stages_for(t->KP);
@@ -635,14 +622,12 @@ void tc_setup(Engine& E) {
         t->trace_path = s;
         EMBER_CUDA(cudaMalloc(&t->trace, (size_t)2 * 4 * TRACE_ROLE * 8));
     }
-    EMBER_CUDA(cudaMalloc(&t->A, (size_t)2 * 2 * t->CB * t->b_cap * 16));
-    EMBER_CUDA(cudaMalloc(&t->N, (size_t)2 * 2 * t->CB * t->n_pad * 16));
     EMBER_CUDA(cudaMalloc(&t->dN_part, (size_t)t->chunks2 * 2 * t->n_pad * E.dim * sizeof(float)));
     EMBER_CUDA(cudaMalloc(&t->lse_pad, (size_t)2 * t->b_cap * sizeof(float)));
     EMBER_CUDA(cudaMalloc(&t->flags, (size_t)(1 + 2 * t->b_cap) * sizeof(uint32_t)));
     EMBER_CUDA(cudaMemset(t->flags, 0, sizeof(uint32_t)));
-    t->mA = make_map(t->A, t->b_cap, t->CB, RES);
-    t->mN = make_map(t->N, t->n_pad, t->CB, RES);
+    t->mA = make_map(E.s.Apk, t->b_cap, t->CB, RES);
+    t->mN = make_map(E.s.Npk, t->n_pad, t->CB, RES);
     EMBER_CUDA(cudaFuncSetAttribute(k_tc<MODE_ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem_total(t->KP, t->nstage, MODE_ROWS)));
     EMBER_CUDA(cudaFuncSetAttribute(k_tc<MODE_NEGS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -652,8 +637,6 @@ void tc_setup(Engine& E) {
 
 void tc_release(Engine& E) {
     if (!E.tc) return;
-    cudaFree(E.tc->A);
-    cudaFree(E.tc->N);
     cudaFree(E.tc->dN_part);
     cudaFree(E.tc->lse_pad);
     cudaFree(E.tc->flags);
@@ -667,16 +650,6 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
     const int d = (int)E.dim, nt = (int)E.nt;
     Scratch& s = E.s;
     const int rows_pad = (int)((nb + RES - 1) / RES * RES);
-    {
-        const int64_t n = (int64_t)2 * t.CB * rows_pad;
-        k_pack<<<(unsigned)((n + 255) / 256), 256, 0, E.stream>>>(s.A, (uint64_t)nb * d, (int)nb, rows_pad, t.b_cap, d,
-                                                                  t.CB, t.A);
-        EMBER_LAUNCHED(E);
-        const int64_t m = (int64_t)2 * t.CB * t.n_pad;
-        k_pack<<<(unsigned)((m + 255) / 256), 256, 0, E.stream>>>(s.N, (uint64_t)nt * d, nt, t.n_pad, t.n_pad, d, t.CB,
-                                                                  t.N);
-        EMBER_LAUNCHED(E);
-    }
     TcArgs a{};
     a.KP = t.KP;
     a.CB = t.CB;
@@ -723,7 +696,7 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
         dump(".rows.bin");
         EMBER_CUDA(cudaMemsetAsync(t.trace, 0, (size_t)2 * 4 * TRACE_ROLE * 8, E.stream));
     }
-    k_tc_fixup<<<1, 1024, 0, E.stream>>>(a, s.A, s.N);
+    k_tc_fixup<<<1, 1024, 0, E.stream>>>(a, s.Apk, s.Npk);
     EMBER_LAUNCHED(E);
     const int items2 = 2 * (t.n_pad / RES) * a.chunks2;
     k_tc<MODE_NEGS><<<std::min(items2, gmax), NTHREADS, smem_total(t.KP, t.nstage, MODE_NEGS), E.stream>>>(
@@ -731,8 +704,9 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
     EMBER_LAUNCHED(E);
     if (tr) dump(".negs.bin");
     const int64_t r = (int64_t)2 * nt * d;
-    k_dn_reduce<<<(unsigned)((r + 255) / 256), 256, 0, E.stream>>>(t.dN_part, a.chunks2, nt, t.n_pad, d,
-                                                                    s.grows + (size_t)2 * nb * d);
+    E.join_sorted();
+    k_dn_reduce<<<(unsigned)((r + 255) / 256), 256, 0, E.stream>>>(t.dN_part, a.chunks2, nt, t.n_pad, d, s.rank,
+                                                                    2 * nb, s.grows);
     EMBER_LAUNCHED(E);
 }
 

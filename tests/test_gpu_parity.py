@@ -134,6 +134,7 @@ def test_training_trajectory_matches_oracle(graph, engine):
         for k in range(2):
             tr.train_batch(dbucket, k * 256, 256, i, j, epoch=1, bucket_step=step, batch_in_bucket=k,
                            loss_out=loss_dev)
+            tr.synchronize()  # the step runs on the context's own (non-blocking) stream
             l_gpu = float(loss_dev.item())
             l_cpu = po.train_batch(m, 1, step, k, bucket, k * 256, 256, eb.partition_offset(V, p, i),
                                    eb.partition_size(V, p, i), eb.partition_offset(V, p, j),
