@@ -1,0 +1,86 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// ember/gpu.hpp — header-only C++ RAII binding of the C-ABI (include/ember_gpu.h) for the
+// reference's own C++ code (namespace ember, proj/). It is what proj/src/pipeline.cpp's
+// train_epoch_sync / train_epoch_partitioned would call instead of a CPU
+// model: status codes become the reference's exception types (common.h:36-49; ConfigError for
+// status 1, EmberError otherwise), the context is owned by a movable handle.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "ember/common.h"
+#include "ember_gpu.h"
+
+namespace ember {
+namespace gpu {
+
+inline void check(int status) {
+    if (status == EMBER_OK) return;
+    const std::string msg = ember_last_error();
+    if (status == EMBER_EUSER) throw ConfigError(msg);
+    throw EmberError(msg);
+}
+
+// One GPU's training context (one compute worker, one stream).
+class Context {
+public:
+    Context(int device, const ember_model_desc& model, const ember_graph_desc& graph, void* stream = nullptr) {
+        check(ember_ctx_create(device, &model, &graph, stream, &ctx_));
+    }
+    Context(const Context&) = delete;
+    Context& operator=(const Context&) = delete;
+    Context(Context&& o) noexcept : ctx_(std::exchange(o.ctx_, nullptr)) {}
+    Context& operator=(Context&& o) noexcept {
+        if (this != &o) {
+            reset();
+            ctx_ = std::exchange(o.ctx_, nullptr);
+        }
+        return *this;
+    }
+    ~Context() { reset(); }
+
+    ember_ctx* get() const { return ctx_; }
+    void* stream() const { return ember_ctx_stream(ctx_); }
+
+    // ParameterSlice storage: caller-owned device rows, borrowed.
+    void bind_partition(uint32_t part, float* theta_dev, float* acc_dev) {
+        check(ember_tables_bind(ctx_, part, theta_dev, acc_dev));
+    }
+    void bind_relations(float* theta_dev, float* acc_dev) { check(ember_relations_bind(ctx_, theta_dev, acc_dev)); }
+    // init_embeddings
+    void init_partition(uint32_t part, uint64_t seed) { check(ember_init_partition(ctx_, part, seed)); }
+    void init_relations(uint64_t seed) { check(ember_init_relations(ctx_, seed)); }
+
+    // trainEdgeBucket (Algorithm 2): every batch of one bucket, in order.
+    ember_step_stats train_bucket(const uint32_t* bucket_edges_dev, uint64_t n, uint32_t i, uint32_t j,
+                                  uint64_t epoch, uint32_t bucket_step, bool want_stats = true) {
+        ember_step_stats st{};
+        check(ember_train_bucket(ctx_, bucket_edges_dev, n, i, j, epoch, bucket_step, want_stats ? &st : nullptr));
+        return st;
+    }
+
+private:
+    void reset() {
+        if (ctx_) ember_ctx_destroy(ctx_);
+        ctx_ = nullptr;
+    }
+    ember_ctx* ctx_ = nullptr;
+};
+
+// make_plan (ordering.h:80) through the C-ABI: the bucket sequence as (i, j) pairs.
+inline std::vector<std::pair<uint32_t, uint32_t>> bucket_sequence(int kind, uint32_t p, uint32_t c, uint64_t seed) {
+    std::vector<uint32_t> seq(2ull * p * p), adm(c + 2ull * p * p + 1), swaps(6ull * p * p + 3), state(1ull * p * p);
+    uint64_t swap_count = 0;
+    uint32_t n_adm = 0;
+    check(ember_make_plan(kind, p, c, seed, seq.data(), &swap_count, adm.data(), &n_adm, swaps.data(), state.data()));
+    std::vector<std::pair<uint32_t, uint32_t>> out(1ull * p * p);
+    for (size_t t = 0; t < out.size(); ++t) out[t] = {seq[2 * t], seq[2 * t + 1]};
+    return out;
+}
+
+}  // namespace gpu
+}  // namespace ember

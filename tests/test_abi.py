@@ -93,3 +93,36 @@ def test_bucketing_is_a_stable_partition_of_the_edges():
         assert (seg == edges[key == b]).all()
     # multiset equality
     assert sorted(map(tuple, out.tolist())) == sorted(map(tuple, edges.tolist()))
+
+
+def test_cpp_binding_compiles_and_maps_errors(tmp_path):
+    """include/ember/gpu.hpp (the binding the reference's C++ trainer would use) compiles against
+    the reference-compatible headers, links the library, and turns status 1 into ConfigError."""
+    src = tmp_path / "use_binding.cpp"
+    src.write_text(r'''
+#include <cstdio>
+#include "ember/gpu.hpp"
+int main() {
+    ember_model_desc m{};  // kind 7: rejected before any device work
+    m.kind = 7; m.dim = 100; m.lr = 0.1f; m.eps = 1e-10f; m.batch_size = 8; m.num_negatives = 8;
+    m.alpha = 0.5f; m.num_chunks = 1;
+    ember_graph_desc g{100, 1, 1};
+    try {
+        ember::gpu::Context ctx(0, m, g);
+        return 2;
+    } catch (const ember::ConfigError& e) {
+        std::printf("ConfigError: %s\n", e.what());
+    }
+    auto seq = ember::gpu::bucket_sequence(EMBER_ORDER_ELIMINATION, 4, 2, 42);
+    std::printf("buckets %zu first %u,%u\n", seq.size(), seq[0].first, seq[0].second);
+    return seq.size() == 16 ? 0 : 3;
+}
+''')
+    exe = tmp_path / "use_binding"
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    cc = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+    subprocess.run([cc, "-std=c++17", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe),
+                    f"-L{libdir}", "-l:libember_b200.so", f"-Wl,-rpath,{libdir}"], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "ConfigError" in out.stdout and "buckets 16 first 0,0" in out.stdout
