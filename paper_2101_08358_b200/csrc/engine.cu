@@ -15,6 +15,7 @@
 #include <nccl.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "engine.h"
@@ -104,7 +105,10 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
         EMBER_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
         own_stream = true;
     }
-    EMBER_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    if (getenv("EMBER_SERIAL_SORT"))  // A/B switch: sort on the step stream (no overlap)
+        side = stream;
+    else
+        EMBER_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
     EMBER_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     EMBER_CUDA(cudaEventCreateWithFlags(&ev_sorted, cudaEventDisableTiming));
     parts.assign(g.num_partitions, PartView{nullptr, nullptr, 0, 0});
@@ -139,9 +143,11 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     s.offsets = dalloc<uint32_t>(cap_rows);
     s.nruns = dalloc<uint32_t>(1);
     s.nunique = dalloc<uint32_t>(2);
-    s.longs = dalloc<uint32_t>(1 + cap_rows);
+    s.longs = dalloc<uint32_t>(2 + 3 * (cap_rows / 64 + 1));
+    s.long_owner = dalloc<uint32_t>(cap_rows / 64 + cap_rows / 64 + 2);
+    s.long_partial = dalloc<float>((uint64_t)(cap_rows / 64 + cap_rows / 64 + 2) * d);
     EMBER_CUDA(cudaMemset(s.nunique, 0, 2 * sizeof(uint32_t)));
-    EMBER_CUDA(cudaMemset(s.longs, 0, sizeof(uint32_t)));
+    EMBER_CUDA(cudaMemset(s.longs, 0, 2 * sizeof(uint32_t)));
     if (m.engine == EMBER_ENGINE_SIMT_FP32) {
         s.S = dalloc<float>(2 * b * (uint64_t)(nt ? nt : 1));
         s.dN_part = dalloc<float>((uint64_t)dsplit * n_neg * d);
@@ -169,12 +175,12 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
 Engine::~Engine() {
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
-    if (side) cudaStreamSynchronize(side);
+    if (side && side != stream) cudaStreamSynchronize(side);
     tc_release(*this);
     void* ptrs[] = {s.negs,  s.batch,       s.A,    s.N,          s.Apk,       s.Npk,   s.fpos,   s.lse,
                     s.g0,    s.S,           s.dA,   s.dN_part,    s.grows,     s.loss,  s.loss_part,
                     s.loss_done, s.keys,    s.keys_sorted, s.vals, s.vals_sorted, s.rank, s.ukeys,  s.counts,
-                    s.offsets, s.nruns,     s.nunique, s.longs,   s.cub_tmp,   s.rel_dense};
+                    s.offsets, s.nruns,     s.nunique, s.longs,   s.long_owner, s.long_partial, s.cub_tmp, s.rel_dense};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (nccl_comm) {
@@ -185,7 +191,7 @@ Engine::~Engine() {
     }
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_sorted) cudaEventDestroy(ev_sorted);
-    if (side) cudaStreamDestroy(side);
+    if (side && side != stream) cudaStreamDestroy(side);
     if (own_stream) cudaStreamDestroy(stream);
 }
 

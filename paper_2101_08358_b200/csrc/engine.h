@@ -90,7 +90,9 @@ struct Scratch {
     uint32_t* offsets = nullptr;
     uint32_t* nruns = nullptr;    // [1] unique keys (RLE)
     uint32_t* nunique = nullptr;  // [2] unique node keys, unique relation keys
-    uint32_t* longs = nullptr;    // [1 + cap] count, then indices of long segments
+    uint32_t* longs = nullptr;        // [2 + 3 * cap]: long segments, chunk slots, then (u, base, nch)
+    uint32_t* long_owner = nullptr;   // chunk slot -> long segment
+    float* long_partial = nullptr;    // chunk slot -> partial row
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
     float* rel_dense = nullptr;  // [R][dim] relation gradient summed over ranks (world > 1)

@@ -9,7 +9,8 @@
 //   k_keys / k_rank   gradient-slot keys for the (key, slot) sort and its inverse permutation
 //   k_chain_rule      chain rule back through adjust, rows written in sorted order
 //   k_loss            deterministic loss reduction (fixed-order partials, last block finishes)
-//   k_segments(_long) segmented sum of the sorted gradient rows + sparse Adagrad
+//   k_segments, k_long_partial, k_long_final
+//                     segmented sum of the sorted gradient rows + sparse Adagrad
 // Rows are dim floats (dim % 4 == 0) and are moved warp-per-row with 128-bit accesses.
 #include <cuda_runtime.h>
 
@@ -109,21 +110,30 @@ __global__ void k_gather_adjust(const uint32_t* __restrict__ edges, uint32_t nb,
     __syncwarp();
     float part = 0.f;
     if (PACKED) {
-        if (lane < CB) {
-            float xd[8], xs[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const uint32_t k = 8 * lane + i;
-                adjust_at(kind, d, k, ss, sr, st, xd[i], xs[i]);
-                part += k < d ? xd[i] * st[k] : 0.f;
+        // all lanes compute the adjusted rows (coalesced smem reads) into the source-row slot and
+        // the spare slot, then lanes < 2CB pack 8 consecutive coordinates each
+        const uint32_t kp = 8 * CB;  // padded dim
+        float* xd = sm + (blockDim.x >> 5) * 3 * d + wib * 2 * kp;
+        float* xs = xd + kp;
+        for (uint32_t k = lane; k < kp; k += 32) {
+            float x = 0.f, y = 0.f;
+            if (k < d) {
+                adjust_at(kind, d, k, ss, sr, st, x, y);
+                part += x * st[k];
             }
+            xd[k] = x;
+            xs[k] = y;
+        }
+        __syncwarp();
+        if (lane < 2 * CB) {
+            const uint32_t cb = lane % CB, side = lane / CB;
+            const float4* src = reinterpret_cast<const float4*>((side == 0 ? xd : xs) + 8 * cb);
+            const float4 v0 = src[0], v1 = src[1];  // zero past d (written above, up to KP)
+            float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
             uint4 h, l;
-            tc::split8(xd, h, l);
-            P[((uint64_t)0 * 2 * CB + lane) * cap + e] = h;
-            P[((uint64_t)0 * 2 * CB + CB + lane) * cap + e] = l;
-            tc::split8(xs, h, l);
-            P[((uint64_t)1 * 2 * CB + lane) * cap + e] = h;
-            P[((uint64_t)1 * 2 * CB + CB + lane) * cap + e] = l;
+            tc::split8(v, h, l);
+            P[((uint64_t)side * 2 * CB + cb) * cap + e] = h;
+            P[((uint64_t)side * 2 * CB + CB + cb) * cap + e] = l;
         }
     } else {
         float* ad = A + (uint64_t)e * d;
@@ -182,7 +192,10 @@ __global__ void k_keys(const uint32_t* __restrict__ edges, uint32_t nb, const ui
                        uint32_t n_neg, uint32_t n_slots, KeySpace ks, uint32_t* keys, uint32_t* vals,
                        uint32_t* longs) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0) *longs = 0u;  // long-segment list of this step's reduction
+    if (i == 0) {  // long-segment list of this step's reduction
+        longs[0] = 0u;
+        longs[1] = 0u;
+    }
     if (i >= n_slots) return;
     uint32_t k;
     if (i < nb) k = node_key(ks, edges[3 * i]);
@@ -304,7 +317,10 @@ struct SegArgs {
     const uint32_t* counts;
     const uint32_t* nruns;
     uint32_t* nunique;   // [2] written: node uniques, relation uniques
-    uint32_t* longs;     // [0] count, [1..] unique indices of long segments
+    uint32_t* longs;     // [0] long segments, [1] chunk slots; then u, base, nch per long (3 x cap)
+    uint32_t* owner;     // chunk slot -> long index
+    float* partial;      // chunk slot -> partial sum row
+    uint32_t long_cap;
     const float* rows;   // sorted gradient rows
     KeySpace ks;
     float* rel_theta;
@@ -319,7 +335,10 @@ struct SegArgs {
     float* rel_rows_out;
 };
 
-constexpr uint32_t LONG_SEG = 48;  // longer segments go to the block-per-segment kernel
+// Segments longer than LONG_SEG rows (hot relations, hub nodes) are cut into LONG_CHUNK-row chunks
+// summed by separate warps, then the chunk partials are added in chunk order (deterministic).
+constexpr uint32_t LONG_SEG = 64;
+constexpr uint32_t LONG_CHUNK = 64;
 
 // Where unique key u's summed row goes: Adagrad target (th, ac) or export/dense destination.
 struct SegTarget {
@@ -369,18 +388,46 @@ __device__ __forceinline__ SegTarget seg_target(const SegArgs& a, uint32_t u, ui
     return t;
 }
 
-__device__ __forceinline__ void seg_finish(const SegArgs& a, const SegTarget& t, uint32_t c4, float4 g) {
+__device__ __forceinline__ bool seg_applies(const SegArgs& a, const SegTarget& t) {
+    return a.apply && !(!t.node && a.rel_dense);
+}
+
+// g: the summed gradient of columns 4*c4..4*c4+3; th/ac: the preloaded parameter/accumulator.
+__device__ __forceinline__ void seg_finish(const SegArgs& a, const SegTarget& t, uint32_t c4, float4 g, float4 th,
+                                           float4 ac) {
     if (t.out) reinterpret_cast<float4*>(t.out)[c4] = g;
-    const bool do_apply = a.apply && !(!t.node && a.rel_dense);
-    if (!do_apply) return;
-    float4 th = reinterpret_cast<float4*>(t.th)[c4];
-    float4 ac = reinterpret_cast<float4*>(t.ac)[c4];
+    if (!seg_applies(a, t)) return;
     adagrad_elem(th.x, ac.x, g.x, a.lr, a.eps);
     adagrad_elem(th.y, ac.y, g.y, a.lr, a.eps);
     adagrad_elem(th.z, ac.z, g.z, a.lr, a.eps);
     adagrad_elem(th.w, ac.w, g.w, a.lr, a.eps);
     reinterpret_cast<float4*>(t.th)[c4] = th;
     reinterpret_cast<float4*>(t.ac)[c4] = ac;
+}
+
+__device__ __forceinline__ void add4(float4& s, const float4& x) {
+    s.x += x.x;
+    s.y += x.y;
+    s.z += x.z;
+    s.w += x.w;
+}
+
+// Sum of rows [0, cnt) (stride d floats) at column block c4, in row order, 4 loads in flight.
+__device__ __forceinline__ float4 sum_rows(const float* base, uint32_t cnt, uint32_t d, uint32_t c4) {
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t r = 0;
+    for (; r + 4 <= cnt; r += 4) {
+        const float4 x0 = ldg4(base + (uint64_t)r * d + 4 * c4);
+        const float4 x1 = ldg4(base + (uint64_t)(r + 1) * d + 4 * c4);
+        const float4 x2 = ldg4(base + (uint64_t)(r + 2) * d + 4 * c4);
+        const float4 x3 = ldg4(base + (uint64_t)(r + 3) * d + 4 * c4);
+        add4(s, x0);
+        add4(s, x1);
+        add4(s, x2);
+        add4(s, x3);
+    }
+    for (; r < cnt; ++r) add4(s, ldg4(base + (uint64_t)r * d + 4 * c4));
+    return s;
 }
 
 // One warp per unique key: sum its contiguous rows (slot order) and apply Adagrad / export.
@@ -394,61 +441,66 @@ __global__ void k_segments(SegArgs a) {
         a.nunique[1] = nr - (u + 1);
     }
     const uint32_t off = a.offsets[u], cnt = a.counts[u];
-    if (cnt > LONG_SEG) {
-        if (lane == 0) a.longs[1 + atomicAdd(a.longs, 1u)] = u;
+    if (cnt > LONG_SEG) {  // reserve chunk slots for the long path
+        const uint32_t nch = (cnt + LONG_CHUNK - 1) / LONG_CHUNK;
+        uint32_t li = 0, base = 0;
+        if (lane == 0) {
+            li = atomicAdd(&a.longs[0], 1u);
+            base = atomicAdd(&a.longs[1], nch);
+            uint32_t* rec = a.longs + 2 + 3 * li;
+            rec[0] = u;
+            rec[1] = base;
+            rec[2] = nch;
+        }
+        li = __shfl_sync(0xffffffffu, li, 0);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        for (uint32_t c = lane; c < nch; c += 32) a.owner[base + c] = li;
         return;
     }
     const SegTarget t = seg_target(a, u, nr, lane == 0);
+    const bool app = seg_applies(a, t);
     const float* base = a.rows + (uint64_t)off * a.d;
     for (uint32_t c4 = lane; c4 < a.d / 4; c4 += 32) {
-        float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (uint32_t r = 0; r < cnt; ++r) {  // fixed (slot) order
-            const float4 x = ldg4(base + (uint64_t)r * a.d + 4 * c4);
-            s0.x += x.x;
-            s0.y += x.y;
-            s0.z += x.z;
-            s0.w += x.w;
+        float4 th = make_float4(0.f, 0.f, 0.f, 0.f), ac = th;
+        if (app) {  // issue the parameter loads before the row sum
+            th = reinterpret_cast<const float4*>(t.th)[c4];
+            ac = reinterpret_cast<const float4*>(t.ac)[c4];
         }
-        seg_finish(a, t, c4, s0);
+        seg_finish(a, t, c4, sum_rows(base, cnt, a.d, c4), th, ac);
     }
 }
 
-// One block (8 warps) per long segment: warp w sums rows w, w + 8, ... (fixed order), then the 8
-// partials are added in warp order. Hot relations (Zipf) and hub nodes land here.
-__global__ void __launch_bounds__(256) k_segments_long(SegArgs a) {
-    extern __shared__ float4 part[];  // [8][d/4]
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t n_long = *(volatile uint32_t*)a.longs, nr = *a.nruns;
-    const uint32_t d4 = a.d / 4;
-    for (uint32_t li = blockIdx.x; li < n_long; li += gridDim.x) {
-        const uint32_t u = a.longs[1 + li];
-        const uint32_t off = a.offsets[u], cnt = a.counts[u];
-        const float* base = a.rows + (uint64_t)off * a.d;
-        for (uint32_t c4 = lane; c4 < d4; c4 += 32) {
-            float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (uint32_t r = warp; r < cnt; r += 8) {
-                const float4 x = ldg4(base + (uint64_t)r * a.d + 4 * c4);
-                s0.x += x.x;
-                s0.y += x.y;
-                s0.z += x.z;
-                s0.w += x.w;
+// One warp per chunk slot of the long segments: partial[slot] = sum of its <= LONG_CHUNK rows.
+__global__ void k_long_partial(SegArgs a) {
+    const uint32_t lane = threadIdx.x & 31, nw = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t n_slots = *(volatile uint32_t*)&a.longs[1];
+    for (uint32_t sl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < n_slots; sl += nw) {
+        const uint32_t* rec = a.longs + 2 + 3 * a.owner[sl];
+        const uint32_t u = rec[0], c = sl - rec[1];
+        const uint32_t r0 = c * LONG_CHUNK, cnt = min(LONG_CHUNK, a.counts[u] - r0);
+        const float* base = a.rows + ((uint64_t)a.offsets[u] + r0) * a.d;
+        for (uint32_t c4 = lane; c4 < a.d / 4; c4 += 32)
+            reinterpret_cast<float4*>(a.partial + (uint64_t)sl * a.d)[c4] = sum_rows(base, cnt, a.d, c4);
+    }
+}
+
+// One warp per long segment: chunk partials added in chunk order, then Adagrad / export.
+__global__ void k_long_final(SegArgs a) {
+    const uint32_t lane = threadIdx.x & 31, nw = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t n_long = *(volatile uint32_t*)&a.longs[0], nr = *a.nruns;
+    for (uint32_t li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < n_long; li += nw) {
+        const uint32_t* rec = a.longs + 2 + 3 * li;
+        const uint32_t u = rec[0], base = rec[1], nch = rec[2];
+        const SegTarget t = seg_target(a, u, nr, lane == 0);
+        const bool app = seg_applies(a, t);
+        for (uint32_t c4 = lane; c4 < a.d / 4; c4 += 32) {
+            float4 th = make_float4(0.f, 0.f, 0.f, 0.f), ac = th;
+            if (app) {
+                th = reinterpret_cast<const float4*>(t.th)[c4];
+                ac = reinterpret_cast<const float4*>(t.ac)[c4];
             }
-            part[warp * d4 + c4] = s0;
+            seg_finish(a, t, c4, sum_rows(a.partial + (uint64_t)base * a.d, nch, a.d, c4), th, ac);
         }
-        __syncthreads();
-        const SegTarget t = seg_target(a, u, nr, threadIdx.x == 0);
-        for (uint32_t c4 = threadIdx.x; c4 < d4; c4 += blockDim.x) {
-            float4 g = part[c4];
-            for (uint32_t w = 1; w < 8; ++w) {
-                const float4 x = part[w * d4 + c4];
-                g.x += x.x;
-                g.y += x.y;
-                g.z += x.z;
-                g.w += x.w;
-            }
-            seg_finish(a, t, c4, g);
-        }
-        __syncthreads();
     }
 }
 
@@ -517,7 +569,8 @@ void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, c
     const size_t sm = (size_t)warps * 3 * E.dim * sizeof(float);
     if (packed) {
         const uint32_t rows_pad = (nb + 127) / 128 * 128;
-        k_gather_adjust<true><<<(rows_pad + warps - 1) / warps, warps * 32, sm, E.stream>>>(
+        const size_t smp = sm + (size_t)warps * 2 * E.KP * sizeof(float);
+        k_gather_adjust<true><<<(rows_pad + warps - 1) / warps, warps * 32, smp, E.stream>>>(
             edges, nb, rows_pad, pi, pj, E.rel_theta, E.m.kind, E.dim, E.CB, E.b_cap, nullptr, E.s.Apk, E.s.fpos);
     } else {
         k_gather_adjust<false><<<(nb + warps - 1) / warps, warps * 32, sm, E.stream>>>(
@@ -577,6 +630,8 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
     a.nruns = E.s.nruns;
     a.nunique = E.s.nunique;
     a.longs = E.s.longs;
+    a.owner = E.s.long_owner;
+    a.partial = E.s.long_partial;
     a.rows = E.s.grows;
     a.ks = ks;
     a.rel_theta = E.rel_theta;
@@ -592,8 +647,9 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
     a.rel_rows_out = rel_rows_out;
     k_segments<<<(n_slots * 32 + 255) / 256, 256, 0, E.stream>>>(a);
     EMBER_LAUNCHED(E);
-    const size_t sm = (size_t)8 * E.dim * sizeof(float);
-    k_segments_long<<<2 * E.sm_count, 256, sm, E.stream>>>(a);
+    k_long_partial<<<2 * E.sm_count, 256, 0, E.stream>>>(a);
+    EMBER_LAUNCHED(E);
+    k_long_final<<<E.sm_count, 256, 0, E.stream>>>(a);
     EMBER_LAUNCHED(E);
 }
 
