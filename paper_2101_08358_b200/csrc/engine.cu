@@ -127,7 +127,7 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     s.fpos = dalloc<float>(b);
     s.lse = dalloc<float>(2 * b);
     s.g0 = dalloc<float>(2 * b);
-    s.dA = dalloc<float>(2 * b * d);
+    s.dA = dalloc<float>(2 * (uint64_t)std::max<uint64_t>(b, (uint64_t)pad_rows(cap_b)) * d);
     s.grows = dalloc<float>((uint64_t)cap_rows * d);
     s.loss = dalloc<float>(1);
     s.loss_part = reinterpret_cast<float*>(dalloc<double>(b / 4096 + 2));
@@ -152,11 +152,11 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
         s.S = dalloc<float>(2 * b * (uint64_t)(nt ? nt : 1));
         s.dN_part = dalloc<float>((uint64_t)dsplit * n_neg * d);
     }
-    if (tc_engine()) {  // packed operand geometry: dim padded to 16, rows to 128-row tiles
+    if (tc_engine()) {  // packed operand geometry: dim padded to 16, rows to 128- and 96-row tiles
         KP = (int)((dim + 15) / 16 * 16);
         CB = KP / 8;
-        b_cap = (int)((cap_b + 127) / 128 * 128);
-        n_pad = (int)((nt + 127) / 128 * 128);
+        b_cap = pad_rows(cap_b);
+        n_pad = pad_rows(nt);
         s.Apk = dalloc<uint16_t>((size_t)2 * 2 * CB * b_cap * 8);
         s.Npk = dalloc<uint16_t>((size_t)2 * 2 * CB * n_pad * 8);
     }

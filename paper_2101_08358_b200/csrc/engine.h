@@ -8,6 +8,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -142,6 +143,12 @@ struct Engine {
     KeySpace keyspace(uint32_t i, uint32_t j) const;
     bool tc_engine() const { return m.engine == EMBER_ENGINE_TC_BF16X3; }
     uint32_t slots(uint32_t nb) const { return 2 * nb + n_neg + (m.kind != EMBER_DOT ? nb : 0); }
+    // Rows of a packed operand holding n rows: whole 128-row resident tiles and whole 96-row
+    // streamed tiles of the tensor-core engine (zero / -inf padded).
+    static int pad_rows(uint32_t n) {
+        const uint32_t a = (n + 127) / 128 * 128, b = (n + 95) / 96 * 96;
+        return (int)((std::max(a, b) + 31) / 32 * 32);
+    }
 
     // pipeline stages
     void sample(const uint32_t* bucket, uint64_t bucket_n, uint32_t i, uint32_t j, uint64_t epoch,

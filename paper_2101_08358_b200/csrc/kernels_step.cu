@@ -79,7 +79,7 @@ __device__ __forceinline__ void adjust_at(int kind, uint32_t d, uint32_t k, cons
     }
 }
 
-// One warp per edge (rows up to rows_pad: the packed layout is zero-padded to 128-row tiles).
+// One warp per edge (rows up to rows_pad: the packed layout is zero-padded to whole tiles).
 // PACKED: lane l < KP/8 owns coordinates 8l..8l+7 and writes their bf16 hi|lo 16-byte core-matrix
 // rows for both sides; else fp32 rows A[0][e] = ad, A[1][e] = as. fpos[e] = ad . t.
 template <bool PACKED>
@@ -92,7 +92,7 @@ __global__ void k_gather_adjust(const uint32_t* __restrict__ edges, uint32_t nb,
     const uint32_t e = blockIdx.x * (blockDim.x >> 5) + wib;
     if (e >= (PACKED ? rows_pad : nb)) return;
     uint4* P = reinterpret_cast<uint4*>(Apk);
-    if (PACKED && e >= nb) {  // zero padding rows of the last 128-row tile
+    if (PACKED && e >= nb) {  // zero padding rows of the last tiles
         const uint4 z = make_uint4(0, 0, 0, 0);
         for (uint32_t c = lane; c < 4 * CB; c += 32) {
             const uint32_t side = c / (2 * CB), cb = c % (2 * CB);
@@ -217,25 +217,37 @@ __global__ void k_rank(const uint32_t* __restrict__ vals_sorted, uint32_t n, uin
 //   grad t += g0_dst * adj_dst (positive score = adj_dst . t), grad s += g0_src * adj_src.
 // Rows go to their sorted positions: source -> grows[rank[e]], destination -> grows[rank[nb + e]],
 // relation -> grows[rank[2nb + n_neg + e]].
+// dA is row-major [2][nb][d] (SIMT engine) or column-blocked [2][d/4][dcap][4] (tensor-core
+// engine, dcap = its padded row capacity): the rows are staged in shared memory either way.
 __global__ void k_chain_rule(const uint32_t* __restrict__ edges, uint32_t nb, uint32_t n_neg, PartView pi,
                              PartView pj, const float* __restrict__ rel, int kind, uint32_t d,
-                             const float* __restrict__ dA, const float* __restrict__ g0,
+                             const float* __restrict__ dA, uint32_t dcap, const float* __restrict__ g0,
                              const uint32_t* __restrict__ rank, float* __restrict__ grows) {
     extern __shared__ float sm[];
     const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t e = blockIdx.x * (blockDim.x >> 5) + wib;
     if (e >= nb) return;
-    float* ss = sm + wib * 3 * d;
+    float* ss = sm + wib * 5 * d;
     float* sr = ss + d;
     float* st = sr + d;
+    float* u = st + d;  // dA of the destination side
+    float* w = u + d;   // dA of the source side
     const uint32_t s = edges[3 * e], r = edges[3 * e + 1], t = edges[3 * e + 2];
     warp_load_row(ss, node_row(pi, s, d), d, lane);
     warp_load_row(st, node_row(pj, t, d), d, lane);
     if (kind != EMBER_DOT) warp_load_row(sr, rel + (uint64_t)r * d, d, lane);
+    if (dcap) {
+        const float4* D = reinterpret_cast<const float4*>(dA);
+        for (uint32_t c4 = lane; c4 < d / 4; c4 += 32) {
+            reinterpret_cast<float4*>(u)[c4] = __ldg(D + (uint64_t)c4 * dcap + e);
+            reinterpret_cast<float4*>(w)[c4] = __ldg(D + ((uint64_t)(d / 4) + c4) * dcap + e);
+        }
+    } else {
+        warp_load_row(u, dA + (uint64_t)e * d, d, lane);
+        warp_load_row(w, dA + ((uint64_t)nb + e) * d, d, lane);
+    }
     __syncwarp();
     const float gd = g0[e], gs = g0[(uint64_t)nb + e];
-    const float* u = dA + (uint64_t)e * d;
-    const float* w = dA + ((uint64_t)nb + e) * d;
     float* gS = grows + (uint64_t)rank[e] * d;
     float* gT = grows + (uint64_t)rank[nb + e] * d;
     if (kind == EMBER_COMPLEX) {
@@ -568,7 +580,7 @@ void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, c
     const uint32_t warps = 8;
     const size_t sm = (size_t)warps * 3 * E.dim * sizeof(float);
     if (packed) {
-        const uint32_t rows_pad = (nb + 127) / 128 * 128;
+        const uint32_t rows_pad = (uint32_t)Engine::pad_rows(nb);
         const size_t smp = sm + (size_t)warps * 2 * E.KP * sizeof(float);
         k_gather_adjust<true><<<(rows_pad + warps - 1) / warps, warps * 32, smp, E.stream>>>(
             edges, nb, rows_pad, pi, pj, E.rel_theta, E.m.kind, E.dim, E.CB, E.b_cap, nullptr, E.s.Apk, E.s.fpos);
@@ -605,10 +617,10 @@ void launch_rank(const Engine& E, uint32_t n) {
 
 void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj) {
     const uint32_t warps = 8;
-    const size_t sm = (size_t)warps * 3 * E.dim * sizeof(float);
-    k_chain_rule<<<(nb + warps - 1) / warps, warps * 32, sm, E.stream>>>(edges, nb, E.n_neg, pi, pj, E.rel_theta,
-                                                                          E.m.kind, E.dim, E.s.dA, E.s.g0, E.s.rank,
-                                                                          E.s.grows);
+    const size_t sm = (size_t)warps * 5 * E.dim * sizeof(float);
+    k_chain_rule<<<(nb + warps - 1) / warps, warps * 32, sm, E.stream>>>(
+        edges, nb, E.n_neg, pi, pj, E.rel_theta, E.m.kind, E.dim, E.s.dA, E.tc_engine() ? (uint32_t)E.b_cap : 0u,
+        E.s.g0, E.s.rank, E.s.grows);
     EMBER_LAUNCHED(E);
 }
 

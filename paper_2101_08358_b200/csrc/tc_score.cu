@@ -26,12 +26,13 @@
 //              S^T = N A^T, P^T = exp(S^T - lse)/b, dN += P^T A; per-chunk partials are summed
 //              in a fixed order by k_dn_reduce (deterministic).
 // TMEM (512 columns): [0,128) and [128,256) two S buffers of 128 fp32 columns, each overwritten
-// in place by P as bf16 pairs (per 64-column half: 32 hi columns then 32 lo columns) — the A
+// in place by P as bf16 pairs (per 32-column chunk: 16 hi columns then 16 lo columns) — the A
 // operand of the second product (TS mode); [256,256+KP) the accumulator; [384,384+KP) the
 // resident operand (hi|lo pairs), copied smem -> TMEM by tcgen05.cp in the MMA pipe, so every
 // MMA reads only its B operand from shared memory.
-// Warps: 0 = TMA producer, 1 = MMA issuer (whole warp converged, one elected lane issues; also
-// owns TMEM), 2..9 = two epilogue warpgroups that take alternate streamed tiles (ping-pong).
+// Warps: 0 = TMA producer, 1 = S issuer (+ TMEM owner, R staging), 2 = P.T issuer (whole warps
+// converged, one elected lane issues), 3..10 = two epilogue warpgroups that take alternate
+// streamed tiles (ping-pong).
 //
 // MMA ordering: tcgen05.mma / tcgen05.cp from one thread execute in issue order, which the
 // kernel relies on for the two write-after-read reuses of TMEM: S_{k+2} overwrites the buffer
@@ -55,23 +56,24 @@ namespace {
 
 enum { MODE_ROWS = 0, MODE_NEGS = 1 };
 constexpr int RES = 128;       // resident rows per item (MMA M)
-constexpr int TILE = 128;      // streamed rows per tile (first product's N, second product's K)
-constexpr int NSTAGE_MAX = 3;  // streamed-tile ring depth (as many as fit in shared memory)
+constexpr int TILE = 96;       // streamed rows per tile (first product's N, second product's K)
+constexpr int NSTAGE_MAX = 4;  // streamed-tile ring depth (as many as fit in shared memory)
 constexpr int KPMAX = 128;     // largest padded dim
-constexpr int NTHREADS = 320;
+constexpr int NTHREADS = 352;  // producer, S issuer, P.T issuer, 2 x 4 epilogue warps
 constexpr uint32_t TCOLS = 512;
-constexpr uint32_t T_ACC = 256, T_RES = 384;
+constexpr int NSP_MAX = 4;     // S/P buffers: (512 - 2 KP) / TILE of them fit next to acc and R
 constexpr float L2E = 1.4426950408889634f;
 
 struct TcArgs {
-    int KP, CB, d, nb, nt, n_pad, b_cap, chunks2, nstage;
+    int KP, CB, d, nb, nt, n_pad, b_cap, chunks2, nstage, nsp;
+    int rows128, rows_pad;  // batch rows covered by the 128-row items / by the packed padding
     float inv_b, log2_inv_b, zmax;
     const float* fpos;
     float* lse;       // [2][nb]
     float* lse_pad;   // [2][b_cap]: log2(1/b) - lse*log2(e), -inf past nb
     float* g0;        // [2][nb]
-    float* dA;        // [2][nb][d]
-    float* dN_part;   // [chunks][2][n_pad][d]
+    float* dA;        // column-blocked [2][d/4][b_cap] float4
+    float* dN_part;   // column-blocked [chunks][2][d/4][n_pad] float4
     uint32_t* flags;  // [0] = count, [1..] = side * b_cap + row
     unsigned long long* trace;  // debug timeline of CTA 0 (EMBER_TC_TRACE), nullptr normally
 };
@@ -90,13 +92,13 @@ constexpr int TRACE_ROLE = 4096;  // records per role
     } while (0)
 
 // ---- shared memory ------------------------------------------------------------------------
-// [res: 128 x KP hi|lo][ring: nstage x (TILE x KP hi|lo + lse trailer)][zbuf][bars]
+// [res: 128-row resident tile][ring: nstage x (TILE-row tile + lse trailer in MODE_NEGS)][zbuf][bars]
 __host__ __device__ constexpr size_t res_bytes(int KP) { return (size_t)RES * KP * 4; }
 __host__ __device__ constexpr size_t trailer_bytes(int mode) { return mode == MODE_NEGS ? TILE * 4 : 0; }
 __host__ __device__ constexpr size_t stage_bytes(int KP, int mode) {
-    return (size_t)TILE * KP * 4 + trailer_bytes(mode);
+    return ((size_t)TILE * KP * 4 + trailer_bytes(mode) + 127) & ~size_t(127);
 }
-__host__ __device__ constexpr size_t zbuf_bytes(int mode) { return mode == MODE_ROWS ? 2 * 2 * RES * 4 : 0; }
+__host__ __device__ constexpr size_t zbuf_bytes(int mode) { return mode == MODE_ROWS ? 4 * RES * 4 : 0; }
 __host__ __device__ constexpr size_t smem_total(int KP, int nstage, int mode) {
     return 128 + res_bytes(KP) + nstage * stage_bytes(KP, mode) + zbuf_bytes(mode) + 256;
 }
@@ -111,16 +113,22 @@ enum {
     B_RES_FULL = 0, B_RES_EMPTY = 1,
     B_RING_FULL = 2,                     // + NSTAGE_MAX
     B_RING_EMPTY = 2 + NSTAGE_MAX,       // + NSTAGE_MAX
-    B_S_FULL = 2 + 2 * NSTAGE_MAX,       // + 2
-    B_P_FULL = 4 + 2 * NSTAGE_MAX,       // + 2
-    B_ACC_FULL = 6 + 2 * NSTAGE_MAX, B_ACC_EMPTY = 7 + 2 * NSTAGE_MAX,
-    B_TMEM_SLOT = 8 + 2 * NSTAGE_MAX,
+    // Every barrier below has exactly one consumer that waits each of its phases in order, so a
+    // waiter can never see a phase two completions ahead (mbarrier parity aliasing).
+    B_S_FULL = 2 + 2 * NSTAGE_MAX,                   // + 2 * NSP_MAX: [epilogue group][S buffer]
+    B_P_FULL = 2 + 2 * NSTAGE_MAX + 2 * NSP_MAX,     // + NSP_MAX (consumer: P.T issuer)
+    B_PN_DONE = 2 + 2 * NSTAGE_MAX + 3 * NSP_MAX,    // + NSP_MAX: P.T of a buffer completed (S issuer)
+    B_ACC_FULL = 2 + 2 * NSTAGE_MAX + 4 * NSP_MAX,   // consumer: epilogue group 1 (item tails)
+    B_ACC_EMPTY = 3 + 2 * NSTAGE_MAX + 4 * NSP_MAX,  // consumer: P.T issuer
+    B_Z_READY = 4 + 2 * NSTAGE_MAX + 4 * NSP_MAX,    // + 4: group 0's row sums of item i in zbuf[i % 4]
+    B_ZB_FREE = 8 + 2 * NSTAGE_MAX + 4 * NSP_MAX,    // + 4: group 1 has read zbuf[i % 4]
+    B_TMEM_SLOT = 12 + 2 * NSTAGE_MAX + 4 * NSP_MAX,
 };
 
 struct Smem {
-    uint8_t* res;
+    uint8_t* res;   // the item's resident tile (TMA landing zone, copied to TMEM by tcgen05.cp)
     uint8_t* ring;  // nstage x stage; a stage = tile [2CB][TILE][16 B] (+ TILE floats in MODE_NEGS)
-    float* zbuf;    // [2 items][2 groups][128]   (MODE_ROWS)
+    float* zbuf;    // [4 items][128]: group 0's partial row sums (MODE_ROWS)
     uint64_t* bars;
     uint32_t sbytes;
     __device__ uint8_t* stage(int st) const { return ring + (size_t)st * sbytes; }
@@ -165,7 +173,7 @@ struct Item {
 template <int MODE>
 __device__ __forceinline__ int n_items(const TcArgs& g) {
     if (MODE == MODE_ROWS) return 2 * ((g.nb + RES - 1) / RES);
-    return 2 * (g.n_pad / RES) * g.chunks2;
+    return 2 * ((g.nt + RES - 1) / RES) * g.chunks2;
 }
 
 template <int MODE>
@@ -179,7 +187,7 @@ __device__ __forceinline__ Item item_geo(const TcArgs& g, int item) {
         it.T = (g.nt + TILE - 1) / TILE;
         it.chunk = it.ntile = 0;
     } else {
-        const int ntl = g.n_pad / RES, nsub = (g.nb + TILE - 1) / TILE;
+        const int ntl = (g.nt + RES - 1) / RES, nsub = (g.nb + TILE - 1) / TILE;
         it.side = item / (ntl * g.chunks2);
         const int rem = item % (ntl * g.chunks2);
         it.ntile = rem / g.chunks2;
@@ -192,14 +200,65 @@ __device__ __forceinline__ Item item_geo(const TcArgs& g, int item) {
     return it;
 }
 
-// Splits 64 fp32 values into 32 bf16x2 hi pairs and 32 lo pairs.
-__device__ __forceinline__ void split64(const float (&p)[64], uint32_t (&hi)[32], uint32_t (&lo)[32]) {
+// Epilogue body for NC 32-column chunks of an S buffer starting at column c0: P = exp(...) in bf16
+// hi|lo pairs written back in place (per 32-column chunk: 16 hi columns, then 16 lo columns).
+template <int MODE, int NC>
+__device__ __forceinline__ void epi_chunk(uint32_t tS, int c0, int k, const TcArgs& g, const Smem& sm, int st, int KP,
+                                          float cshift, float& z) {
+    float v[32 * NC];
+    {
+        uint32_t a[NC][32];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        const __nv_bfloat162 h = __floats2bfloat162_rn(p[2 * i], p[2 * i + 1]);
-        const float2 hf = __bfloat1622float2(h);
-        hi[i] = *reinterpret_cast<const uint32_t*>(&h);
-        lo[i] = tc::pack_bf16x2(p[2 * i] - hf.x, p[2 * i + 1] - hf.y);
+        for (int j = 0; j < NC; ++j) tc::tmem_ld32(tS + c0 + 32 * j, a[j]);
+        tc::tmem_ld_wait();  // the registers are valid only after the wait
+#pragma unroll
+        for (int j = 0; j < NC; ++j)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[32 * j + i] = __uint_as_float(a[j][i]);
+    }
+    if (MODE == MODE_ROWS) {
+        const int k0 = k * TILE + c0;
+        float zz[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent sums (latency)
+        if (k0 + 32 * NC <= g.nt) {
+#pragma unroll
+            for (int c = 0; c < 32 * NC; ++c) {
+                v[c] = tc::ex2(fmaf(v[c], L2E, cshift));
+                zz[c & 3] += v[c];
+            }
+        } else {  // last tile: negatives past n_t contribute nothing
+#pragma unroll
+            for (int c = 0; c < 32 * NC; ++c) {
+                v[c] = (k0 + c < g.nt) ? tc::ex2(fmaf(v[c], L2E, cshift)) : 0.f;
+                zz[c & 3] += v[c];
+            }
+        }
+        z += (zz[0] + zz[1]) + (zz[2] + zz[3]);
+    } else {
+        // per batch row: log2(1/b) - lse*log2(e) (k_tc<ROWS> stores it; -inf past the batch), from
+        // the stage's trailer (TMA'd with the tile)
+        const float4* L = reinterpret_cast<const float4*>(sm.stage(st) + TILE * KP * 4) + c0 / 4;
+#pragma unroll
+        for (int c4 = 0; c4 < 8 * NC; ++c4) {
+            const float4 l = L[c4];  // broadcast read
+            v[4 * c4 + 0] = tc::ex2(fmaf(v[4 * c4 + 0], L2E, l.x));
+            v[4 * c4 + 1] = tc::ex2(fmaf(v[4 * c4 + 1], L2E, l.y));
+            v[4 * c4 + 2] = tc::ex2(fmaf(v[4 * c4 + 2], L2E, l.z));
+            v[4 * c4 + 3] = tc::ex2(fmaf(v[4 * c4 + 3], L2E, l.w));
+        }
+    }
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) {
+        uint32_t hi[16], lo[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const float x0 = v[32 * cc + 2 * i], x1 = v[32 * cc + 2 * i + 1];
+            const __nv_bfloat162 hh = __floats2bfloat162_rn(x0, x1);
+            const float2 hf = __bfloat1622float2(hh);
+            hi[i] = *reinterpret_cast<const uint32_t*>(&hh);
+            lo[i] = tc::pack_bf16x2(x0 - hf.x, x1 - hf.y);
+        }
+        tc::tmem_st16(tS + c0 + 32 * cc, hi);  // P overwrites S in place
+        tc::tmem_st16(tS + c0 + 32 * cc + 16, lo);
     }
 }
 
@@ -215,7 +274,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int KP = g.KP, CB = g.CB;
     const int items = n_items<MODE>(g);
     const int KS = KP / 16;
-    const int tr_role = warp == 0 ? 0 : warp == 1 ? 1 : warp == 2 ? 2 : 3;  // TC_TRACE region
+    const int NSP = g.nsp;
+    const uint64_t lo_off = (uint64_t)((CB * TILE * 16) >> 4);  // lo blocks follow hi blocks (descriptor units)
+    // TMEM columns: S/P buffer b at b*TILE, accumulator, then the resident operand (KP each)
+    const uint32_t T_ACC = (uint32_t)(NSP * TILE), T_RES = T_ACC + (uint32_t)KP;
+    const int tr_role = warp == 0 ? 0 : warp == 1 ? 1 : warp == 2 ? 4 : (warp - 3) < 4 ? 2 : 3;  // TC_TRACE region
     int tr_n = 0;
 
     if (threadIdx.x == 0) {
@@ -225,12 +288,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tc::mbar_init(&bars[B_RING_FULL + i], 1);
             tc::mbar_init(&bars[B_RING_EMPTY + i], 1);
         }
-        for (int i = 0; i < 2; ++i) {
-            tc::mbar_init(&bars[B_S_FULL + i], 1);
+        for (int i = 0; i < 2 * NSP_MAX; ++i) tc::mbar_init(&bars[B_S_FULL + i], 1);
+        for (int i = 0; i < g.nsp; ++i) {
             tc::mbar_init(&bars[B_P_FULL + i], 128);
+            tc::mbar_init(&bars[B_PN_DONE + i], 1);
         }
         tc::mbar_init(&bars[B_ACC_FULL], 1);
-        tc::mbar_init(&bars[B_ACC_EMPTY], 256);
+        tc::mbar_init(&bars[B_ACC_EMPTY], 128);
+        for (int i = 0; i < 4; ++i) {
+            tc::mbar_init(&bars[B_Z_READY + i], 128);
+            tc::mbar_init(&bars[B_ZB_FREE + i], 128);
+        }
         tc::fence_mbar_init();
         tc::tmap_prefetch(&mapR);
         tc::tmap_prefetch(&mapT);
@@ -247,19 +315,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (warp == 0) {
         if (lane == 0) {  // ------------------------------------------------------ TMA producer
             const uint32_t bytesR = (uint32_t)res_bytes(KP);
-            const uint32_t bytesT = (uint32_t)stage_bytes(KP, MODE);
-            uint32_t it = 0, gt = 0;
+            const uint32_t bytesT = (uint32_t)(TILE * KP * 4 + trailer_bytes(MODE));  // TMA'd bytes per tile
+            uint32_t it = 0, gr = 0;  // gr: streamed-tile ring slots used
             for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
                 const Item I = item_geo<MODE>(g, item);
-                // resident tile of this item: its previous occupant was copied to TMEM (RES_EMPTY)
+                // resident tile: its previous occupant has been copied into TMEM (RES_EMPTY)
                 tc::mbar_wait(&bars[B_RES_EMPTY], (it & 1) ^ 1);
                 tc::mbar_expect_tx(&bars[B_RES_FULL], bytesR);
                 tc::tma_load_4d(sm.res, &mapR, 0, I.r0 / 32, 0, I.side, &bars[B_RES_FULL]);
                 TC_TRACE(1, it);
-                for (int k = 0; k < I.T; ++k, ++gt) {
-                    const int st = gt % NSTAGE;
-                    tc::mbar_wait(&bars[B_RING_EMPTY + st], ((gt / NSTAGE) & 1) ^ 1);
-                    TC_TRACE(2, gt);
+                for (int k = 0; k < I.T; ++k, ++gr) {
+                    const int st = gr % NSTAGE;
+                    tc::mbar_wait(&bars[B_RING_EMPTY + st], ((gr / NSTAGE) & 1) ^ 1);
+                    TC_TRACE(2, gr);
                     tc::mbar_expect_tx(&bars[B_RING_FULL + st], bytesT);
                     uint8_t* dst = sm.stage(st);
                     const int row = I.t0 + k * TILE;
@@ -270,206 +338,188 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
             }
         }
-    } else if (warp == 1) {  // ------------------------------------------------- MMA issuer
-        // The whole warp runs this loop converged (warp-uniform waits and values, held in
-        // uniform registers); one elected lane issues each tcgen05 instruction.
+    } else if (warp == 1) {  // ---------------------------------------------- S issuer (+ R staging)
+        // Warps 1 and 2 run their loops converged (warp-uniform waits and values in uniform
+        // registers); one elected lane issues each tcgen05 instruction. Splitting the two products
+        // over two issuing warps lets each warp's barrier waits hide behind the other's issue.
         const uint32_t id_s = tc::idesc_bf16(128, TILE, false, false);
+        uint32_t it = 0, gt = 0;  // gt: streamed tiles (S/P buffers and ring slots)
+        for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+            const Item I = item_geo<MODE>(g, item);
+            {  // resident operand smem -> TMEM, in this warp's MMA stream after the previous item's last S
+                tc::mbar_wait_warp(&bars[B_RES_FULL], it & 1);
+                TC_TRACE(10, it);
+                tc::fence_after();
+#pragma unroll
+                for (int s = 0; s < KPMAX / 16; ++s) {
+                    if (s < KS) {
+                        tmem_cp_128x256b(T_RES + s * 8, kdesc(sm.res, RES, s, 0));
+                        tmem_cp_128x256b(T_RES + KP / 2 + s * 8, kdesc(sm.res, RES, s, CB));
+                    }
+                }
+                tc::mma_commit_elect(&bars[B_RES_EMPTY]);
+            }
+            for (int k = 0; k < I.T; ++k) {  // S_k = R . T_k^T   (R from TMEM, T_k K-major from smem)
+                const uint32_t q = gt + k;
+                const int st = q % NSTAGE;
+                const uint32_t b = q % NSP;
+                if (q >= (uint32_t)NSP)  // buffer b free: P.T of tile q - NSP has completed
+                    tc::mbar_wait_warp(&bars[B_PN_DONE + b], (q / NSP - 1) & 1);
+                TC_TRACE(16, q);
+                tc::mbar_wait_warp(&bars[B_RING_FULL + st], (q / NSTAGE) & 1);
+                TC_TRACE(11, q);
+                tc::fence_after();
+                const uint32_t tS = b * TILE;
+                const uint64_t t0 = kdesc(sm.stage(st), TILE, 0, 0);
+#pragma unroll
+                for (int s = 0; s < KPMAX / 16; ++s) {
+                    if (s < KS) {
+                        const uint32_t rh = T_RES + s * 8, rl = T_RES + KP / 2 + s * 8;
+                        const uint64_t th = t0 + (uint64_t)(s * ((2 * TILE * 16) >> 4)), tl = th + lo_off;
+                        tc::mma_ts_elect(tS, rl, th, id_s, s > 0 ? 1u : 0u);
+                        tc::mma_ts_elect(tS, rh, tl, id_s, 1u);
+                        tc::mma_ts_elect(tS, rh, th, id_s, 1u);
+                    }
+                }
+                tc::mma_commit_elect(&bars[B_S_FULL + (k & 1) * NSP_MAX + b]);  // tile k of an item -> group k & 1
+                TC_TRACE(12, q);
+            }
+            gt += I.T;
+        }
+    } else if (warp == 2) {  // ----------------------------------------------------- P.T issuer
         const uint32_t id_a = tc::idesc_bf16(128, KP, false, true);
-        const uint64_t lo_off = (uint64_t)((CB * TILE * 16) >> 4);  // lo blocks follow hi blocks
         uint32_t it = 0, gt = 0;
         for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
             const Item I = item_geo<MODE>(g, item);
-            // resident operand smem -> TMEM, in the MMA pipe after the previous item's last S
-            tc::mbar_wait_warp(&bars[B_RES_FULL], it & 1);
-            TC_TRACE(10, it);
-            tc::fence_after();
+            for (int k = 0; k < I.T; ++k) {  // acc += P_k . T_k   (P from TMEM, T MN-major from smem)
+                const uint32_t q = gt + k;
+                const int st = q % NSTAGE;
+                const uint32_t b = q % NSP;
+                TC_TRACE(17, q);
+                tc::mbar_wait_warp(&bars[B_P_FULL + b], (q / NSP) & 1);
+                TC_TRACE(13, q);
+                if (k == 0) tc::mbar_wait_warp(&bars[B_ACC_EMPTY], (it & 1) ^ 1);
+                if (k == 0) TC_TRACE(15, it);
+                tc::fence_after();
+                const uint32_t tP = b * TILE;
+                const uint64_t t0 = mndesc(sm.stage(st), TILE, 0, 0);
+                const uint32_t acc0 = k > 0 ? 1u : 0u;
 #pragma unroll
-            for (int s = 0; s < KPMAX / 16; ++s) {
-                if (s < KS) {
-                    tmem_cp_128x256b(T_RES + s * 8, kdesc(sm.res, RES, s, 0));
-                    tmem_cp_128x256b(T_RES + KP / 2 + s * 8, kdesc(sm.res, RES, s, CB));
+                for (int s = 0; s < TILE / 16; ++s) {
+                    // k-step s covers streamed rows 16s..16s+15: 32-column chunk s/2 of the P buffer
+                    // holds 16 hi pair columns then 16 lo pair columns
+                    const uint32_t ph = tP + (s >> 1) * 32 + (s & 1) * 8, pl = ph + 16;
+                    const uint64_t th = t0 + (uint64_t)(s * (256 >> 4)), tl = th + lo_off;
+                    tc::mma_ts_elect(T_ACC, pl, th, id_a, s > 0 ? 1u : acc0);
+                    tc::mma_ts_elect(T_ACC, ph, tl, id_a, 1u);
+                    tc::mma_ts_elect(T_ACC, ph, th, id_a, 1u);
                 }
-            }
-            tc::mma_commit_elect(&bars[B_RES_EMPTY]);
-            int prev_st = 0;
-            for (int k = 0; k <= I.T; ++k) {
-                int st = 0;
-                if (k < I.T) {  // S_k = R . T_k^T   (R from TMEM, T_k K-major from smem)
-                    const uint32_t q = gt + k;
-                    st = q % NSTAGE;
-                    TC_TRACE(16, q);
-                    tc::mbar_wait_warp(&bars[B_RING_FULL + st], (q / NSTAGE) & 1);
-                    TC_TRACE(11, q);
-                    tc::fence_after();
-                    const uint32_t tS = (q & 1) * 128;
-                    const uint64_t t0 = kdesc(sm.stage(st), TILE, 0, 0);
-#pragma unroll
-                    for (int s = 0; s < KPMAX / 16; ++s) {
-                        if (s < KS) {
-                            const uint32_t rh = T_RES + s * 8, rl = T_RES + KP / 2 + s * 8;
-                            const uint64_t th = t0 + (uint64_t)(s * ((2 * TILE * 16) >> 4)), tl = th + lo_off;
-                            tc::mma_ts_elect(tS, rl, th, id_s, s > 0 ? 1u : 0u);
-                            tc::mma_ts_elect(tS, rh, tl, id_s, 1u);
-                            tc::mma_ts_elect(tS, rh, th, id_s, 1u);
-                        }
-                    }
-                    tc::mma_commit_elect(&bars[B_S_FULL + (q & 1)]);
-                    TC_TRACE(12, q);
-                }
-                if (k > 0) {  // acc += P_{k-1} . T_{k-1}   (P from TMEM, T MN-major from smem)
-                    const uint32_t q = gt + k - 1;
-                    TC_TRACE(17, q);
-                    tc::mbar_wait_warp(&bars[B_P_FULL + (q & 1)], (q >> 1) & 1);
-                    TC_TRACE(13, q);
-                    if (k == 1) tc::mbar_wait_warp(&bars[B_ACC_EMPTY], (it & 1) ^ 1);
-                    if (k == 1) TC_TRACE(15, it);
-                    tc::fence_after();
-                    const uint32_t tP = (q & 1) * 128;
-                    const uint64_t t0 = mndesc(sm.stage(prev_st), TILE, 0, 0);
-                    const uint32_t acc0 = k > 1 ? 1u : 0u;
-#pragma unroll
-                    for (int s = 0; s < TILE / 16; ++s) {
-                        // k-step s covers streamed rows 16s..16s+15: half h = s/4 of the P buffer
-                        const uint32_t ph = tP + (s >> 2) * 64 + (s & 3) * 8, pl = ph + 32;
-                        const uint64_t th = t0 + (uint64_t)(s * (256 >> 4)), tl = th + lo_off;
-                        tc::mma_ts_elect(T_ACC, pl, th, id_a, s > 0 ? 1u : acc0);
-                        tc::mma_ts_elect(T_ACC, ph, tl, id_a, 1u);
-                        tc::mma_ts_elect(T_ACC, ph, th, id_a, 1u);
-                    }
-                    tc::mma_commit_elect(&bars[B_RING_EMPTY + prev_st]);
-                    TC_TRACE(14, q);
-                }
-                prev_st = st;
+                tc::mma_commit_elect(&bars[B_RING_EMPTY + st]);
+                tc::mma_commit_elect(&bars[B_PN_DONE + b]);
+                TC_TRACE(14, q);
             }
             tc::mma_commit_elect(&bars[B_ACC_FULL]);
             gt += I.T;
         }
     } else {  // -------------------------------------------------------------------- epilogue
-        const int G = (warp - 2) >> 2;          // ping-pong group: takes streamed tiles with q % 2 == G
+        const int G = (warp - 3) >> 2;          // ping-pong group: takes tiles k of an item with k % 2 == G
         const int qd = warp & 3;                // TMEM lane quadrant
         const int r = 32 * qd + lane;           // resident row (MODE_ROWS: batch row; NEGS: negative)
         const uint32_t t_row = tbase + ((uint32_t)(32 * qd) << 16);
-        const int nch = KP / 16, half = (nch + 1) / 2;
-        const int c_lo = G == 0 ? 0 : half, c_hi = G == 0 ? half : nch;
+        // Tile k of every item goes to group k & 1 (group 0 always starts an item); group 1 also
+        // does every item tail, so group 0 moves straight on to the next item's first tile.
         uint32_t it = 0, gt = 0;
+        uint32_t sphase = 0;  // bit b: parity of this group's next wait on S_FULL[G][b]
         for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
             const Item I = item_geo<MODE>(g, item);
             const int row = I.r0 + r;
             float fp = 0.f, z = 0.f;
             if (MODE == MODE_ROWS) fp = row < g.nb ? g.fpos[row] : 0.f;
             const float cshift = -fp * L2E;
-            for (int k = 0; k < I.T; ++k) {
+            for (int k = G; k < I.T; k += 2) {
                 const uint32_t q = gt + k;
-                if ((int)(q & 1) != G) continue;
-                const uint32_t tS = t_row + (q & 1) * 128;
+                const uint32_t b = q % NSP;
+                const uint32_t tS = t_row + b * TILE;
                 const int st = q % NSTAGE;
                 if (MODE == MODE_NEGS) tc::mbar_wait(&bars[B_RING_FULL + st], (q / NSTAGE) & 1);
-                tc::mbar_wait(&bars[B_S_FULL + (q & 1)], (q >> 1) & 1);
+                tc::mbar_wait(&bars[B_S_FULL + G * NSP_MAX + b], (sphase >> b) & 1);
+                sphase ^= 1u << b;
                 if (qd == 2) TC_TRACE(20 + G, q);
                 tc::fence_after();
-#pragma unroll 1
-                for (int h = 0; h < 2; ++h) {  // 64-column halves: S half h -> P half h in place
-                    float v[64];
-                    {
-                        uint32_t a[32], b[32];
-                        tc::tmem_ld32(tS + 64 * h, a);
-                        tc::tmem_ld32(tS + 64 * h + 32, b);
-                        tc::tmem_ld_wait();
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) {
-                            v[i] = __uint_as_float(a[i]);
-                            v[32 + i] = __uint_as_float(b[i]);
-                        }
-                    }
-                    if (MODE == MODE_ROWS) {
-                        const int k0 = k * TILE + 64 * h;
-                        if (k0 + 64 <= g.nt) {
-#pragma unroll
-                            for (int c = 0; c < 64; ++c) {
-                                v[c] = tc::ex2(fmaf(v[c], L2E, cshift));
-                                z += v[c];
-                            }
-                        } else {  // last tile: negatives past n_t contribute nothing
-#pragma unroll
-                            for (int c = 0; c < 64; ++c) {
-                                v[c] = (k0 + c < g.nt) ? tc::ex2(fmaf(v[c], L2E, cshift)) : 0.f;
-                                z += v[c];
-                            }
-                        }
-                    } else {
-                        // per batch row: log2(1/b) - lse*log2(e) (k_tc<ROWS> stores it; -inf past
-                        // the batch), from the stage's trailer (TMA'd with the tile)
-                        const float4* L =
-                            reinterpret_cast<const float4*>(sm.stage(st) + TILE * KP * 4) + 16 * h;
-#pragma unroll
-                        for (int c4 = 0; c4 < 16; ++c4) {
-                            const float4 l = L[c4];  // broadcast read
-                            v[4 * c4 + 0] = tc::ex2(fmaf(v[4 * c4 + 0], L2E, l.x));
-                            v[4 * c4 + 1] = tc::ex2(fmaf(v[4 * c4 + 1], L2E, l.y));
-                            v[4 * c4 + 2] = tc::ex2(fmaf(v[4 * c4 + 2], L2E, l.z));
-                            v[4 * c4 + 3] = tc::ex2(fmaf(v[4 * c4 + 3], L2E, l.w));
-                        }
-                    }
-                    uint32_t hi[32], lo[32];
-                    split64(v, hi, lo);
-                    tc::tmem_st32(tS + 64 * h, hi);  // P overwrites S half h in place: hi, then lo
-                    tc::tmem_st32(tS + 64 * h + 32, lo);
-                }
+                // 64 columns per TMEM round trip, then the 32-column remainder (TILE = 96)
+                epi_chunk<MODE, 2>(tS, 0, k, g, sm, st, KP, cshift, z);
+                epi_chunk<MODE, 1>(tS, 64, k, g, sm, st, KP, cshift, z);
                 tc::tmem_st_wait();
                 tc::fence_before();
-                tc::mbar_arrive(&bars[B_P_FULL + (q & 1)]);
+                tc::mbar_arrive(&bars[B_P_FULL + b]);
                 if (qd == 2) TC_TRACE(22 + G, q);
+            }
+            if (G == 0) {  // hand the row sums to group 1 (4 slots, each reused in order)
+                if (MODE == MODE_ROWS) {
+                    const uint32_t zs = it & 3;
+                    tc::mbar_wait(&bars[B_ZB_FREE + zs], ((it >> 2) & 1) ^ 1);
+                    sm.zbuf[zs * 128 + r] = z;
+                    tc::mbar_arrive(&bars[B_Z_READY + zs]);
+                }
+                gt += I.T;
+                continue;
             }
             tc::mbar_wait(&bars[B_ACC_FULL], it & 1);
             if (qd == 2) TC_TRACE(26 + G, it);
             tc::fence_after();
+            // Accumulator row in two batches of <= 4 chunks of 16 columns; the accumulator is released
+            // right after the last TMEM read, before the last batch's stores.
+            const int nchunks = KP / 16;
+            float scale = 1.0f, lse = 0.f, Z = 1.f;
+            const bool valid = MODE == MODE_NEGS || row < g.nb;
             if (MODE == MODE_ROWS) {
-                float* zb = sm.zbuf + (it & 1) * 256;
-                zb[G * 128 + r] = z;
-                epi_sync();
-                const float Z = 1.0f + zb[r] + zb[128 + r];  // exp(f_pos - f_pos) = 1: the positive
-                const bool valid = row < g.nb;
-                const float lse = fp + __logf(Z);
-                const bool bad = !(Z < g.zmax);
-                const float scale = g.inv_b / Z;
-                float* out = g.dA + ((size_t)I.side * g.nb + (valid ? row : 0)) * g.d;
-                for (int c = c_lo; c < c_hi; ++c) {
-                    uint32_t a[16];
-                    tc::tmem_ld16(t_row + T_ACC + 16 * c, a);
-                    tc::tmem_ld_wait();
-                    if (valid) {
-#pragma unroll
-                        for (int i = 0; i < 16; i += 4)
-                            if (16 * c + i < g.d)
-                                *reinterpret_cast<float4*>(out + 16 * c + i) =
-                                    make_float4(__uint_as_float(a[i]) * scale, __uint_as_float(a[i + 1]) * scale,
-                                                __uint_as_float(a[i + 2]) * scale, __uint_as_float(a[i + 3]) * scale);
-                    }
-                }
-                if (G == 0) {
-                    if (valid) {
-                        g.lse[(size_t)I.side * g.nb + row] = lse;
-                        g.g0[(size_t)I.side * g.nb + row] = (__expf(fp - lse) - 1.0f) * g.inv_b;
-                        if (bad) g.flags[1 + atomicAdd(g.flags, 1u)] = (uint32_t)(I.side * g.b_cap + row);
-                    }
-                    g.lse_pad[(size_t)I.side * g.b_cap + row] = valid ? fmaf(-lse, L2E, g.log2_inv_b) : -INFINITY;
-                }
-            } else {
-                float* out = g.dN_part + (((size_t)I.chunk * 2 + I.side) * g.n_pad + row) * g.d;
-                for (int c = c_lo; c < c_hi; ++c) {
-                    uint32_t a[16];
-                    tc::tmem_ld16(t_row + T_ACC + 16 * c, a);
-                    tc::tmem_ld_wait();
-#pragma unroll
-                    for (int i = 0; i < 16; i += 4)
-                        if (16 * c + i < g.d)
-                            *reinterpret_cast<float4*>(out + 16 * c + i) = make_float4(
-                                __uint_as_float(a[i]), __uint_as_float(a[i + 1]), __uint_as_float(a[i + 2]),
-                                __uint_as_float(a[i + 3]));
-                }
+                const uint32_t zs = it & 3;
+                tc::mbar_wait(&bars[B_Z_READY + zs], (it >> 2) & 1);
+                Z = 1.0f + z + sm.zbuf[zs * 128 + r];  // + exp(f_pos - f_pos) = 1: the positive
+                tc::mbar_arrive(&bars[B_ZB_FREE + zs]);
+                lse = fp + __logf(Z);
+                scale = g.inv_b / Z;
             }
-            tc::fence_before();
-            tc::mbar_arrive(&bars[B_ACC_EMPTY]);
+            // column-blocked outputs: float4 block c4 of row e at [..][c4][e]
+            float4* out = MODE == MODE_ROWS
+                              ? reinterpret_cast<float4*>(g.dA) + (size_t)I.side * (g.d / 4) * g.b_cap + row
+                              : reinterpret_cast<float4*>(g.dN_part) +
+                                    ((size_t)I.chunk * 2 + I.side) * (g.d / 4) * g.n_pad + row;
+            const size_t cstride = MODE == MODE_ROWS ? (size_t)g.b_cap : (size_t)g.n_pad;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                uint32_t accv[4][16];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (4 * half + i < nchunks) tc::tmem_ld16(t_row + T_ACC + 16 * (4 * half + i), accv[i]);
+                tc::tmem_ld_wait();
+                if (half == 1 || nchunks <= 4) {
+                    tc::fence_before();
+                    if (half == 1 || nchunks <= 4) tc::mbar_arrive(&bars[B_ACC_EMPTY]);
+                }
+                if (valid) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int c = 4 * half + i;
+                        if (c >= nchunks) continue;
+#pragma unroll
+                        for (int j = 0; j < 16; j += 4)
+                            if (16 * c + j < g.d)
+                                out[(size_t)((16 * c + j) / 4) * cstride] = make_float4(
+                                    __uint_as_float(accv[i][j]) * scale, __uint_as_float(accv[i][j + 1]) * scale,
+                                    __uint_as_float(accv[i][j + 2]) * scale, __uint_as_float(accv[i][j + 3]) * scale);
+                    }
+                }
+                if (nchunks <= 4) break;
+            }
+            if (MODE == MODE_ROWS) {
+                if (valid) {
+                    g.lse[(size_t)I.side * g.nb + row] = lse;
+                    g.g0[(size_t)I.side * g.nb + row] = (__expf(fp - lse) - 1.0f) * g.inv_b;
+                    if (!(Z < g.zmax)) g.flags[1 + atomicAdd(g.flags, 1u)] = (uint32_t)(I.side * g.b_cap + row);
+                }
+                g.lse_pad[(size_t)I.side * g.b_cap + row] = valid ? fmaf(-lse, L2E, g.log2_inv_b) : -INFINITY;
+            }
             if (qd == 2) TC_TRACE(28 + G, it);
             gt += I.T;
         }
@@ -517,14 +567,19 @@ __global__ void k_tc_fixup(TcArgs g, const uint16_t* __restrict__ Apk, const uin
         }
         const float lse = mx + logf(z);
         const float scale = g.inv_b / z;
-        float* out = g.dA + ((size_t)side * g.nb + row) * g.d;
+        float* out = g.dA + (size_t)side * g.d * g.b_cap;  // column-blocked [side][c/4][row][c%4]
         for (int c = lane, i = 0; i < 4; c += 32, ++i)
-            if (c < g.d) out[c] = acc[i] * scale;
+            if (c < g.d) out[((size_t)(c / 4) * g.b_cap + row) * 4 + c % 4] = acc[i] * scale;
         if (lane == 0) {
             g.lse[(size_t)side * g.nb + row] = lse;
             g.lse_pad[(size_t)side * g.b_cap + row] = fmaf(-lse, L2E, g.log2_inv_b);
             g.g0[(size_t)side * g.nb + row] = (expf(fp - lse) - 1.0f) * g.inv_b;
         }
+    }
+    // streamed 96-row tiles may reach past the last 128-row item: those rows never score
+    for (int i = threadIdx.x; i < 2 * (g.rows_pad - g.rows128); i += blockDim.x) {
+        const int side = i / (g.rows_pad - g.rows128), row = g.rows128 + i % (g.rows_pad - g.rows128);
+        g.lse_pad[(size_t)side * g.b_cap + row] = -INFINITY;
     }
     __syncthreads();
     if (threadIdx.x == 0 && n) *g.flags = 0u;
@@ -545,7 +600,8 @@ __global__ void k_dn_reduce(const float* __restrict__ part, int chunks, int nt, 
     const int rem = (int)(t % per_side);
     const int n = rem / d, k = rem % d;
     float acc = 0.f;
-    for (int c = 0; c < chunks; ++c) acc += part[(((size_t)c * 2 + side) * n_pad + n) * d + k];
+    for (int c = 0; c < chunks; ++c)  // column-blocked partials [chunk][side][k/4][n][k%4]
+        acc += part[((((size_t)c * 2 + side) * (d / 4) + k / 4) * n_pad + n) * 4 + k % 4];
     out[(size_t)rank[slot0 + side * nt + n] * d + k] = acc;
 }
 
@@ -588,11 +644,11 @@ CUtensorMap make_map(uint16_t* base, int cap, int CB, int box_rows) {
 
 // Engine-side state of the tensor-core engine (allocated once per context).
 struct TcState {
-    int KP = 0, CB = 0, b_cap = 0, n_pad = 0, chunks2 = 1, nstage = 4;
+    int KP = 0, CB = 0, b_cap = 0, n_pad = 0, chunks2 = 1, nstage = 4, nsp = 2;
     float* dN_part = nullptr;
     float* lse_pad = nullptr;
     uint32_t* flags = nullptr;
-    CUtensorMap mA, mN;  // 128-row boxes (RES == TILE)
+    CUtensorMap mA128, mA96, mN128, mN96;  // resident (RES rows) and streamed (TILE rows) boxes
     float zmax = 1e24f;
     int max_grid = 0;  // test hook (EMBER_TC_MAXGRID): several items per CTA at small sizes
     unsigned long long* trace = nullptr;  // EMBER_TC_TRACE=<file prefix>: CTA-0 timeline dump
@@ -613,21 +669,25 @@ void tc_setup(Engine& E) {
     t->CB = E.CB;
     t->b_cap = E.b_cap;
     t->n_pad = E.n_pad;
-    const int ntl = t->n_pad / RES;
+    const int ntl = (int)((E.nt + RES - 1) / RES);
+    t->nsp = std::min(NSP_MAX, (512 - 2 * t->KP) / TILE);
+    if (t->nsp < 2) throw ConfigError("tensor-core engine: dim too large for the TMEM layout");
     t->chunks2 = std::max(1, E.sm_count / (2 * ntl));
     t->nstage = stages_for(t->KP);
     if (const char* s = getenv("EMBER_TC_ZMAX")) t->zmax = (float)atof(s);  // test hook: 0 flags every row
     if (const char* s = getenv("EMBER_TC_MAXGRID")) t->max_grid = atoi(s);
     if (const char* s = getenv("EMBER_TC_TRACE")) {
         t->trace_path = s;
-        EMBER_CUDA(cudaMalloc(&t->trace, (size_t)2 * 4 * TRACE_ROLE * 8));
+        EMBER_CUDA(cudaMalloc(&t->trace, (size_t)2 * 5 * TRACE_ROLE * 8));
     }
     EMBER_CUDA(cudaMalloc(&t->dN_part, (size_t)t->chunks2 * 2 * t->n_pad * E.dim * sizeof(float)));
     EMBER_CUDA(cudaMalloc(&t->lse_pad, (size_t)2 * t->b_cap * sizeof(float)));
     EMBER_CUDA(cudaMalloc(&t->flags, (size_t)(1 + 2 * t->b_cap) * sizeof(uint32_t)));
     EMBER_CUDA(cudaMemset(t->flags, 0, sizeof(uint32_t)));
-    t->mA = make_map(E.s.Apk, t->b_cap, t->CB, RES);
-    t->mN = make_map(E.s.Npk, t->n_pad, t->CB, RES);
+    t->mA128 = make_map(E.s.Apk, t->b_cap, t->CB, RES);
+    t->mA96 = make_map(E.s.Apk, t->b_cap, t->CB, TILE);
+    t->mN128 = make_map(E.s.Npk, t->n_pad, t->CB, RES);
+    t->mN96 = make_map(E.s.Npk, t->n_pad, t->CB, TILE);
     EMBER_CUDA(cudaFuncSetAttribute(k_tc<MODE_ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem_total(t->KP, t->nstage, MODE_ROWS)));
     EMBER_CUDA(cudaFuncSetAttribute(k_tc<MODE_NEGS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -649,7 +709,7 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
     TcState& t = *E.tc;
     const int d = (int)E.dim, nt = (int)E.nt;
     Scratch& s = E.s;
-    const int rows_pad = (int)((nb + RES - 1) / RES * RES);
+    const int rows_pad = (int)((nb + RES - 1) / RES * RES);  // 128-row items of k_tc<ROWS>
     TcArgs a{};
     a.KP = t.KP;
     a.CB = t.CB;
@@ -672,12 +732,15 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
     const int nsub = (int)((nb + TILE - 1) / TILE);
     a.chunks2 = std::min(t.chunks2, nsub);
     a.nstage = t.nstage;
+    a.nsp = t.nsp;
+    a.rows128 = rows_pad;
+    a.rows_pad = E.pad_rows(nb);
     const int items1 = 2 * (rows_pad / RES);
     const int gmax = t.max_grid > 0 ? std::min(t.max_grid, E.sm_count) : E.sm_count;
     const bool tr = t.trace && t.trace_calls++ == 4;  // one warmed-up call per process
     auto dump = [&](const char* tag) {
         EMBER_CUDA(cudaStreamSynchronize(E.stream));
-        std::vector<unsigned long long> buf((size_t)2 * 4 * TRACE_ROLE);
+        std::vector<unsigned long long> buf((size_t)2 * 5 * TRACE_ROLE);
         EMBER_CUDA(cudaMemcpy(buf.data(), t.trace, buf.size() * 8, cudaMemcpyDeviceToHost));
         FILE* f = fopen((t.trace_path + tag).c_str(), "wb");
         if (f) {
@@ -686,21 +749,21 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
         }
     };
     if (tr) {
-        EMBER_CUDA(cudaMemsetAsync(t.trace, 0, (size_t)2 * 4 * TRACE_ROLE * 8, E.stream));
+        EMBER_CUDA(cudaMemsetAsync(t.trace, 0, (size_t)2 * 5 * TRACE_ROLE * 8, E.stream));
         a.trace = t.trace;
     }
     k_tc<MODE_ROWS><<<std::min(items1, gmax), NTHREADS, smem_total(t.KP, t.nstage, MODE_ROWS), E.stream>>>(
-        t.mA, t.mN, a);
+        t.mA128, t.mN96, a);
     EMBER_LAUNCHED(E);
     if (tr) {
         dump(".rows.bin");
-        EMBER_CUDA(cudaMemsetAsync(t.trace, 0, (size_t)2 * 4 * TRACE_ROLE * 8, E.stream));
+        EMBER_CUDA(cudaMemsetAsync(t.trace, 0, (size_t)2 * 5 * TRACE_ROLE * 8, E.stream));
     }
     k_tc_fixup<<<1, 1024, 0, E.stream>>>(a, s.Apk, s.Npk);
     EMBER_LAUNCHED(E);
-    const int items2 = 2 * (t.n_pad / RES) * a.chunks2;
+    const int items2 = 2 * ((nt + RES - 1) / RES) * a.chunks2;
     k_tc<MODE_NEGS><<<std::min(items2, gmax), NTHREADS, smem_total(t.KP, t.nstage, MODE_NEGS), E.stream>>>(
-        t.mN, t.mA, a);
+        t.mN128, t.mA96, a);
     EMBER_LAUNCHED(E);
     if (tr) dump(".negs.bin");
     const int64_t r = (int64_t)2 * nt * d;
