@@ -180,7 +180,65 @@ int ember_tc_selftest(int device, int mode, int K, int N, uint64_t seed, double*
  * independent accumulators are cycled round-robin (N * count <= 256 columns). */
 int ember_tc_mmabench(int device, int mode, int N, int iters, double* cycles_per_mma);
 
+/* ---- device partition buffer (§4.2, Algorithm 2) ------------------
+ * HBM holds `capacity` resident partition slots + 2 staging slots; pinned host memory is the
+ * backing store (host_theta[k], host_acc[k]: partition k's [rows_k x dim] f32 arrays, pinned
+ * for asynchronous copies). The buffer replays one epoch's bucket sequence (seq: 2*steps ids,
+ * steps = p*p, from ember_make_plan) with Belady eviction (furthest next use, ties to the
+ * lower id), prefetching each admission on a copy stream and writing evicted partitions back
+ * asynchronously; misses per epoch == the plan's swap_count. While the buffer is attached it
+ * binds the context's partition tables itself (ember_tables_bind must not be used). */
+typedef struct ember_buffer ember_buffer;
+typedef struct {
+    uint64_t reads;          /* partition loads (initial fill + admissions) */
+    uint64_t writes;         /* partition writebacks (evictions + epoch-end flush) */
+    uint64_t bytes_read;
+    uint64_t bytes_written;
+    uint64_t swaps_per_epoch;
+    uint64_t epochs;         /* completed epochs */
+    uint32_t stalls;         /* admissions the compute stream had to wait for */
+    uint32_t slots;          /* device slots allocated (capacity + 2 when capacity < p) */
+    double stall_ms;         /* device time the compute stream waited on loads */
+    uint64_t slot_bytes;
+} ember_buffer_report;
+
+int ember_buffer_create(ember_ctx* ctx, uint32_t capacity, const uint32_t* seq, uint32_t steps,
+                        float* const* host_theta, float* const* host_acc, ember_buffer** out);
+int ember_buffer_destroy(ember_buffer* buf);
+/* acquire_pair: bucket seq[step] becomes resident for work enqueued after this call
+ * on the context stream; steps are acquired in plan order, an epoch starts at step 0.
+ * i_out/j_out (nullable) receive the bucket. */
+int ember_buffer_acquire(ember_buffer* buf, uint32_t step, uint32_t* i_out, uint32_t* j_out);
+/* The bucket's work has been enqueued: evictees whose last use this was start writing back.
+ * Releasing the last step ends the epoch (all residents are written back). */
+int ember_buffer_release(ember_buffer* buf, uint32_t step);
+/* Waits until every writeback has landed in host memory (between epochs). */
+int ember_buffer_flush(ember_buffer* buf);
+int ember_buffer_stats(ember_buffer* buf, ember_buffer_report* out);
+/* The eviction decisions of one epoch: 3 u32 per swap (step, evicted, admitted); *n = swaps. */
+int ember_buffer_decisions(ember_buffer* buf, uint32_t* out, uint32_t* n);
+/* train_epoch_partitioned (Algorithm 2) through the buffer: every bucket of
+ * the plan in order (acquire -> all batches of the bucket -> release). edges_dev: bucketed
+ * edges (device), offsets_host: p*p+1 u64 bucket offsets (host). stats nullable. */
+int ember_train_epoch_buffered(ember_ctx* ctx, ember_buffer* buf, const uint32_t* edges_dev,
+                               const uint64_t* offsets_host, uint64_t epoch, ember_step_stats* stats);
+
 /* ---- multi-GPU------------------------------------------------------------ */
+/* Conflict-free round schedule (csrc/host/rounds.cpp): circle-method perfect
+ * matchings of the p partitions, p/(2*world) pairs per GPU per round, buckets (a,b),(b,a) per
+ * pair and the self-buckets in round 0. p even and world | p/2 (or p == world == 1).
+ * order/round/rank: p*p u32 each — bucket id i*p+j in global schedule order, its round, its
+ * GPU. holder: rounds*p u32 — GPU holding partition x in round r. *n_rounds = p-1 (1 if p==1).
+ * The global position of a bucket is its bucket_step for the sampler seeds. */
+int ember_make_rounds(uint32_t p, uint32_t world, uint32_t* order, uint32_t* round, uint32_t* rank, uint32_t* holder,
+                      uint32_t* n_rounds);
+/* External relation reduction: with grad_dev != NULL every training step zeroes grad_dev
+ * ([R x dim] f32, device) and writes the batch's summed relation gradients into it instead of
+ * updating the relation table; the caller reduces it across ranks (e.g. an NCCL all-reduce on the
+ * context stream) and applies it with ember_relations_apply_dense (the relation Adagrad of
+ * SPEC.md:166 over all rows; rows with zero gradient are unchanged). NULL: in-place updates. */
+int ember_relations_external(ember_ctx* ctx, float* grad_dev);
+int ember_relations_apply_dense(ember_ctx* ctx, const float* grad_dev);
 /* nccl_unique_id: 128 bytes (ncclUniqueId) shared by all ranks. NCCL is loaded at run time. */
 int ember_comm_init(ember_ctx* ctx, const void* nccl_unique_id, int rank, int world);
 /* Sum the relation gradients across ranks before the relation Adagrad (on by default once

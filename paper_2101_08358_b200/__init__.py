@@ -12,10 +12,10 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from ._lib import (ENGINE, KIND, ORDERING, ConfigError, EmberError, GraphDesc, ModelDesc, StepStats, check,  # noqa: F401
-                   lib)
+from ._lib import (ENGINE, KIND, ORDERING, BufferReport, ConfigError, EmberError, GraphDesc, ModelDesc,  # noqa: F401
+                   StepStats, check, lib)
 
-__all__ = ["ConfigError", "EmberError", "Hyper", "Trainer", "make_plan", "lower_bound_swaps",
+__all__ = ["ConfigError", "EmberError", "Hyper", "Trainer", "PartitionBuffer", "make_plan", "lower_bound_swaps",
            "elimination_swap_formula", "generate_graph", "bucket_edges", "partition_offset", "partition_size", "lib"]
 
 
@@ -155,9 +155,9 @@ class Trainer:
                 rows = partition_size(num_nodes, num_partitions, k)
                 self.bind_partition(k, torch.empty((rows, hyper.dim), dtype=torch.float32, device=self.dev),
                                     torch.empty((rows, hyper.dim), dtype=torch.float32, device=self.dev))
-            if KIND[hyper.kind] != 0:
-                self.bind_relations(torch.empty((num_relations, hyper.dim), dtype=torch.float32, device=self.dev),
-                                    torch.empty((num_relations, hyper.dim), dtype=torch.float32, device=self.dev))
+        if KIND[hyper.kind] != 0:  # relations are always HBM-resident (5.9 MB at FB86m)
+            self.bind_relations(torch.empty((num_relations, hyper.dim), dtype=torch.float32, device=self.dev),
+                                torch.empty((num_relations, hyper.dim), dtype=torch.float32, device=self.dev))
 
     # -- lifecycle ------------------------------------------------------------------------
     def close(self):
@@ -301,3 +301,92 @@ class Trainer:
     def comm_init(self, unique_id: bytes, rank: int, world: int):
         buf = C.create_string_buffer(unique_id, 128)
         check(lib().ember_comm_init(self.ctx, buf, rank, world))
+
+
+class PartitionBuffer:
+    """PartitionBuffer on the device: `capacity` HBM slots (+2 staging) over a
+    pinned-host backing store holding every partition's theta and acc. Replays the plan's bucket
+    sequence with Belady eviction, prefetch and asynchronous writeback (csrc/buffer.cu).
+
+    The trainer must be created with allocate=False: the buffer binds its partition tables."""
+
+    def __init__(self, trainer: Trainer, capacity: int, plan_seq, host_theta=None, host_acc=None):
+        t = trainer.torch
+        self.tr, self.c = trainer, capacity
+        p, d = trainer.p, trainer.h.dim
+        self.seq = np.ascontiguousarray(np.asarray(plan_seq, dtype=np.uint32).reshape(-1))
+        if host_theta is None:
+            host_theta = [t.empty((partition_size(trainer.V, p, k), d), dtype=t.float32).pin_memory() for k in range(p)]
+            host_acc = [t.empty((partition_size(trainer.V, p, k), d), dtype=t.float32).pin_memory() for k in range(p)]
+        self.host_theta, self.host_acc = host_theta, host_acc
+        th = (C.c_void_p * p)(*[_ptr(x) for x in host_theta])
+        ac = (C.c_void_p * p)(*[_ptr(x) for x in host_acc])
+        buf = C.c_void_p()
+        check(lib().ember_buffer_create(trainer.ctx, capacity, _ptr(self.seq), len(self.seq) // 2, th, ac,
+                                        C.byref(buf)))
+        self.buf = buf
+
+    def init_backing(self, seed: int):
+        """init_embeddings of every partition, computed on the device and stored to
+        the host backing store (bit-identical to a resident init)."""
+        t, tr = self.tr.torch, self.tr
+        rows = max(x.shape[0] for x in self.host_theta)
+        th = t.empty((rows, tr.h.dim), dtype=t.float32, device=tr.dev)
+        ac = t.empty((rows, tr.h.dim), dtype=t.float32, device=tr.dev)
+        for k in range(tr.p):
+            check(lib().ember_tables_bind(tr.ctx, k, _ptr(th), _ptr(ac)))
+            check(lib().ember_init_partition(tr.ctx, k, seed))
+            tr.torch_stream().synchronize()
+            n = self.host_theta[k].shape[0]
+            self.host_theta[k].copy_(th[:n])
+            self.host_acc[k].copy_(ac[:n])
+        if tr.rel_theta is not None:
+            check(lib().ember_init_relations(tr.ctx, seed))
+        tr.torch_stream().synchronize()
+
+    def train_epoch(self, edges_dev, offsets, epoch: int) -> dict:
+        """train_epoch_partitioned through the buffer."""
+        st = StepStats()
+        off = np.ascontiguousarray(np.asarray(offsets, dtype=np.uint64))
+        check(lib().ember_train_epoch_buffered(self.tr.ctx, self.buf, _ptr(edges_dev), _ptr(off), epoch, C.byref(st)))
+        return {"loss": st.loss_sum / max(1, st.batches), "batches": st.batches, "edges": st.edges}
+
+    def acquire(self, step: int) -> tuple[int, int]:
+        i, j = C.c_uint32(0), C.c_uint32(0)
+        check(lib().ember_buffer_acquire(self.buf, step, C.byref(i), C.byref(j)))
+        return i.value, j.value
+
+    def release(self, step: int):
+        check(lib().ember_buffer_release(self.buf, step))
+
+    def flush(self):
+        check(lib().ember_buffer_flush(self.buf))
+
+    def stats(self) -> dict:
+        r = BufferReport()
+        check(lib().ember_buffer_stats(self.buf, C.byref(r)))
+        return {f: getattr(r, f) for f, _ in BufferReport._fields_}
+
+    def decisions(self) -> np.ndarray:
+        n = C.c_uint32(0)
+        check(lib().ember_buffer_decisions(self.buf, None, C.byref(n)))
+        out = np.zeros(3 * max(1, n.value), dtype=np.uint32)
+        check(lib().ember_buffer_decisions(self.buf, _ptr(out), C.byref(n)))
+        return out[:3 * n.value].reshape(-1, 3)
+
+    def node_table(self):
+        """Concatenated host backing store (after flush)."""
+        self.flush()
+        return (np.concatenate([x.numpy() for x in self.host_theta]),
+                np.concatenate([x.numpy() for x in self.host_acc]))
+
+    def close(self):
+        if getattr(self, "buf", None):
+            check(lib().ember_buffer_destroy(self.buf))
+            self.buf = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

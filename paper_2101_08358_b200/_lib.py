@@ -33,6 +33,12 @@ class StepStats(C.Structure):
                 ("unique_nodes", C.c_uint64), ("unique_rels", C.c_uint64)]
 
 
+class BufferReport(C.Structure):
+    _fields_ = [("reads", C.c_uint64), ("writes", C.c_uint64), ("bytes_read", C.c_uint64),
+                ("bytes_written", C.c_uint64), ("swaps_per_epoch", C.c_uint64), ("epochs", C.c_uint64),
+                ("stalls", C.c_uint32), ("slots", C.c_uint32), ("stall_ms", C.c_double), ("slot_bytes", C.c_uint64)]
+
+
 class EmberError(RuntimeError):
     pass
 
@@ -74,6 +80,14 @@ def _declare(L):
         "ember_tc_mmabench": (C.c_int, [i32, i32, i32, i32, C.POINTER(C.c_double)]),
         "ember_profile_enable": (C.c_int, [vp, i32]),
         "ember_profile_read": (C.c_int, [vp, vp, C.POINTER(u64), C.POINTER(u64)]),
+        "ember_buffer_create": (C.c_int, [vp, u32, vp, u32, vp, vp, C.POINTER(vp)]),
+        "ember_buffer_destroy": (C.c_int, [vp]),
+        "ember_buffer_acquire": (C.c_int, [vp, u32, C.POINTER(u32), C.POINTER(u32)]),
+        "ember_buffer_release": (C.c_int, [vp, u32]),
+        "ember_buffer_flush": (C.c_int, [vp]),
+        "ember_buffer_stats": (C.c_int, [vp, C.POINTER(BufferReport)]),
+        "ember_buffer_decisions": (C.c_int, [vp, vp, C.POINTER(u32)]),
+        "ember_train_epoch_buffered": (C.c_int, [vp, vp, vp, vp, u64, C.POINTER(StepStats)]),
         "ember_comm_init": (C.c_int, [vp, vp, i32, i32]),
         "ember_comm_barrier": (C.c_int, [vp]),
         "ember_partition_copy": (C.c_int, [vp, vp, vp, i32, vp, vp, i32, u64]),

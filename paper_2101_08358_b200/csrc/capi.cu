@@ -11,6 +11,7 @@
 
 #include "ember/ordering.h"
 #include "engine.h"
+#include "host/rounds.h"
 
 namespace ember {
 void graph_generate(int device, uint64_t V, uint32_t R, uint64_t n, uint64_t seed, float train, float valid,
@@ -19,6 +20,16 @@ void graph_bucket(int device, uint64_t V, uint32_t p, const uint32_t* in, uint64
                   uint64_t* offsets);
 double tc_selftest(int device, int mode, int K, int N, uint64_t seed);
 double tc_mmabench(int device, int mode, int N, int iters, int nacc);
+struct PartitionBuffer;
+PartitionBuffer* buffer_create(Engine& E, uint32_t c, const uint32_t* seq, uint32_t steps, float* const* host_theta,
+                               float* const* host_acc);
+void buffer_destroy(PartitionBuffer* B);
+void buffer_acquire(PartitionBuffer* B, uint32_t step, uint32_t* i, uint32_t* j);
+void buffer_release(PartitionBuffer* B, uint32_t step);
+void buffer_flush(PartitionBuffer* B);
+void buffer_stats(PartitionBuffer* B, ember_buffer_report* out);
+uint32_t buffer_decisions(PartitionBuffer* B, uint32_t* out);
+Engine& buffer_engine(PartitionBuffer* B);
 void launch_eval(const Engine& E, const uint32_t* test, uint32_t n_test, const uint32_t* train, uint64_t n_train,
                  uint32_t n_eval, float alpha_eval, uint32_t block, uint64_t eval_seed, uint32_t* ranks);
 }  // namespace ember
@@ -27,6 +38,11 @@ using namespace ember;
 
 struct ember_ctx {
     Engine* e;
+};
+
+struct ember_buffer {
+    PartitionBuffer* b;
+    ember_ctx* ctx;
 };
 
 namespace {
@@ -57,6 +73,12 @@ Engine& eng(ember_ctx* c) {
     if (!c || !c->e) throw ConfigError("null context");
     EMBER_CUDA(cudaSetDevice(c->e->device));
     return *c->e;
+}
+
+PartitionBuffer& buf(ember_buffer* b) {
+    if (!b || !b->b) throw ConfigError("null buffer");
+    eng(b->ctx);
+    return *b->b;
 }
 
 void need(const void* p, const char* what) {
@@ -146,11 +168,10 @@ int ember_train_batch(ember_ctx* ctx, const uint32_t* bucket, uint64_t bucket_n,
     });
 }
 
-int ember_train_bucket(ember_ctx* ctx, const uint32_t* bucket, uint64_t n, uint32_t i, uint32_t j, uint64_t epoch,
-                       uint32_t bucket_step, ember_step_stats* stats) {
-    return guarded([&] {
-        Engine& E = eng(ctx);
-        need(bucket, "bucket_edges_dev");
+namespace {
+// Algorithm 2 trainEdgeBucket: all batches of one bucket; per-batch losses summed into stats.
+void train_bucket(Engine& E, const uint32_t* bucket, uint64_t n, uint32_t i, uint32_t j, uint64_t epoch,
+                  uint32_t bucket_step, ember_step_stats* stats) {
         double loss_sum = 0.0;
         uint64_t batches = 0;
         float* losses = nullptr;
@@ -173,6 +194,15 @@ int ember_train_bucket(ember_ctx* ctx, const uint32_t* bucket, uint64_t n, uint3
             stats->batches += batches;
             stats->edges += n;
         }
+}
+}  // namespace
+
+int ember_train_bucket(ember_ctx* ctx, const uint32_t* bucket, uint64_t n, uint32_t i, uint32_t j, uint64_t epoch,
+                       uint32_t bucket_step, ember_step_stats* stats) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        need(bucket, "bucket_edges_dev");
+        train_bucket(E, bucket, n, i, j, epoch, bucket_step, stats);
     });
 }
 
@@ -343,6 +373,126 @@ int ember_profile_read(ember_ctx* ctx, double* ms_out, uint64_t* launches_out, u
             for (size_t k = 0; k < ms.size(); ++k) ms_out[k] = ms[k];
         if (launches_out) *launches_out = E.launches;
         if (lib_calls_out) *lib_calls_out = E.lib_calls;
+    });
+}
+
+int ember_buffer_create(ember_ctx* ctx, uint32_t capacity, const uint32_t* seq, uint32_t steps,
+                        float* const* host_theta, float* const* host_acc, ember_buffer** out) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        need(seq, "seq");
+        need(host_theta, "host_theta");
+        need(host_acc, "host_acc");
+        need(out, "out");
+        *out = nullptr;
+        PartitionBuffer* B = buffer_create(E, capacity, seq, steps, host_theta, host_acc);
+        *out = new ember_buffer{B, ctx};
+    });
+}
+
+int ember_buffer_destroy(ember_buffer* b) {
+    return guarded([&] {
+        if (!b) return;
+        if (b->b) buffer_destroy(b->b);
+        delete b;
+    });
+}
+
+int ember_buffer_acquire(ember_buffer* b, uint32_t step, uint32_t* i, uint32_t* j) {
+    return guarded([&] { buffer_acquire(&buf(b), step, i, j); });
+}
+
+int ember_buffer_release(ember_buffer* b, uint32_t step) {
+    return guarded([&] { buffer_release(&buf(b), step); });
+}
+
+int ember_buffer_flush(ember_buffer* b) {
+    return guarded([&] { buffer_flush(&buf(b)); });
+}
+
+int ember_buffer_stats(ember_buffer* b, ember_buffer_report* out) {
+    return guarded([&] {
+        need(out, "out");
+        buffer_stats(&buf(b), out);
+    });
+}
+
+int ember_buffer_decisions(ember_buffer* b, uint32_t* out, uint32_t* n) {
+    return guarded([&] {
+        const uint32_t k = buffer_decisions(&buf(b), out);
+        if (n) *n = k;
+    });
+}
+
+int ember_train_epoch_buffered(ember_ctx* ctx, ember_buffer* b, const uint32_t* edges, const uint64_t* offsets,
+                               uint64_t epoch, ember_step_stats* stats) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        PartitionBuffer& B = buf(b);
+        if (&buffer_engine(&B) != &E) throw ConfigError("buffer belongs to another context");
+        need(edges, "edges_dev");
+        need(offsets, "offsets_host");
+        const uint32_t p = E.g.num_partitions;
+        uint64_t nbatch = 0, n_edges = 0;
+        for (uint64_t k = 0; k < (uint64_t)p * p; ++k) {
+            if (offsets[k + 1] < offsets[k]) throw ConfigError("offsets must be non-decreasing");
+            nbatch += (offsets[k + 1] - offsets[k] + E.cap_b - 1) / E.cap_b;
+        }
+        n_edges = offsets[(size_t)p * p] - offsets[0];
+        float* losses = nullptr;  // one slot per batch, read once at the end (no per-bucket sync)
+        if (stats && nbatch) EMBER_CUDA(cudaMallocAsync(&losses, nbatch * sizeof(float), E.stream));
+        uint64_t slot = 0;
+        for (uint32_t t = 0; t < p * p; ++t) {
+            uint32_t i = 0, j = 0;
+            buffer_acquire(&B, t, &i, &j);
+            const uint64_t lo = offsets[(size_t)i * p + j], hi = offsets[(size_t)i * p + j + 1];
+            for (uint64_t b0 = 0, k = 0; lo + b0 < hi; b0 += E.cap_b, ++k) {
+                const uint32_t nb = (uint32_t)std::min<uint64_t>(E.cap_b, hi - lo - b0);
+                E.train_batch(edges + 3 * lo, hi - lo, b0, nb, i, j, epoch, t, (uint32_t)k,
+                              losses ? losses + slot : nullptr);
+                ++slot;
+            }
+            buffer_release(&B, t);
+        }
+        if (stats) {
+            std::vector<float> h(nbatch);
+            if (nbatch) {
+                EMBER_CUDA(cudaMemcpyAsync(h.data(), losses, nbatch * sizeof(float), cudaMemcpyDeviceToHost, E.stream));
+                EMBER_CUDA(cudaFreeAsync(losses, E.stream));
+            }
+            EMBER_CUDA(cudaStreamSynchronize(E.stream));
+            for (float x : h) stats->loss_sum += x;
+            stats->batches += nbatch;
+            stats->edges += n_edges;
+        }
+    });
+}
+
+int ember_make_rounds(uint32_t p, uint32_t world, uint32_t* order, uint32_t* round, uint32_t* rank, uint32_t* holder,
+                      uint32_t* n_rounds) {
+    return guarded([&] {
+        const RoundSchedule S = make_rounds(p, world);
+        if (order) std::memcpy(order, S.order.data(), S.order.size() * sizeof(uint32_t));
+        if (round) std::memcpy(round, S.round.data(), S.round.size() * sizeof(uint32_t));
+        if (rank) std::memcpy(rank, S.rank.data(), S.rank.size() * sizeof(uint32_t));
+        if (holder) std::memcpy(holder, S.holder.data(), S.holder.size() * sizeof(uint32_t));
+        if (n_rounds) *n_rounds = S.rounds;
+    });
+}
+
+int ember_relations_external(ember_ctx* ctx, float* grad) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        if (grad && (reinterpret_cast<uintptr_t>(grad) & 15)) throw ConfigError("grad_dev must be 16-byte aligned");
+        E.rel_ext = grad;
+    });
+}
+
+int ember_relations_apply_dense(ember_ctx* ctx, const float* grad) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        need(grad, "grad_dev");
+        E.apply_relations_dense(grad);
     });
 }
 

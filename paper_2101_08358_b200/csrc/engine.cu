@@ -269,17 +269,26 @@ void Engine::forward_backward(const uint32_t* edges, uint32_t nb, uint32_t i, ui
 void Engine::reduce_and_apply(uint32_t nb, uint32_t i, uint32_t j, bool apply, uint32_t* node_ids_out,
                               float* node_rows_out, uint32_t* rel_ids_out, float* rel_rows_out) {
     const KeySpace ks = keyspace(i, j);
-    const bool dense = world > 1 && apply && m.kind != EMBER_DOT;
-    if (dense) EMBER_CUDA(cudaMemsetAsync(s.rel_dense, 0, (size_t)g.num_relations * dim * sizeof(float), stream));
-    // nodes apply in place; relations either in place (world == 1) or into the dense buffer
+    // Relations: in place (1 GPU), or summed into a dense [R][dim] buffer that is all-reduced
+    // (internal NCCL comm) or handed to the caller (rel_ext: external reduction, then
+    // ember_relations_apply_dense) before the relation Adagrad.
+    const bool ext = rel_ext != nullptr;
+    const bool dense = apply && m.kind != EMBER_DOT && (world > 1 || ext);
+    float* buf = ext ? rel_ext : s.rel_dense;
+    if (dense) EMBER_CUDA(cudaMemsetAsync(buf, 0, (size_t)g.num_relations * dim * sizeof(float), stream));
     launch_segments(*this, slots(nb), ks, apply, dense, node_ids_out, node_rows_out, rel_ids_out, rel_rows_out);
-    if (dense) {
+    if (dense && !ext) {
         allreduce_relations();
-        const uint64_t rn = (uint64_t)g.num_relations * dim;
-        k_adagrad_dense<<<(unsigned)((rn + 255) / 256), 256, 0, stream>>>(rel_theta, rel_acc, s.rel_dense, rn, m.lr,
-                                                                         m.eps);
-        EMBER_LAUNCHED(*this);
+        apply_relations_dense(s.rel_dense);
     }
+}
+
+void Engine::apply_relations_dense(const float* grad) {
+    if (m.kind == EMBER_DOT) return;
+    if (!rel_theta || !rel_acc) throw ConfigError("relation table not bound");
+    const uint64_t rn = (uint64_t)g.num_relations * dim;
+    k_adagrad_dense<<<(unsigned)((rn + 255) / 256), 256, 0, stream>>>(rel_theta, rel_acc, grad, rn, m.lr, m.eps);
+    EMBER_LAUNCHED(*this);
 }
 
 void Engine::mark(int phase) {

@@ -128,6 +128,7 @@ struct Engine {
     // multi-GPU
     void* nccl_comm = nullptr;
     int rank = 0, world = 1;
+    float* rel_ext = nullptr;  // caller-owned [R][dim] relation-gradient buffer (external reduction)
     // profiling: CUDA events at phase boundaries on the step stream + our own kernel launches
     bool prof_on = false;
     std::vector<std::pair<int, cudaEvent_t>> prof_events;
@@ -167,6 +168,7 @@ struct Engine {
     void step(const uint32_t* edges, uint32_t nb, const uint32_t* bucket, uint64_t bucket_n, uint32_t i, uint32_t j,
               uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket, float* loss_out);
     void allreduce_relations();
+    void apply_relations_dense(const float* grad);  // dense relation Adagrad (zero rows are no-ops)
     void comm_init(const void* nccl_unique_id, int rank, int world);
     std::vector<double> profile_read();  // ms per phase summed over marked batches
 };

@@ -648,7 +648,7 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
     a.ks = ks;
     a.rel_theta = E.rel_theta;
     a.rel_acc = E.rel_acc;
-    a.rel_dense = rel_dense ? E.s.rel_dense : nullptr;
+    a.rel_dense = rel_dense ? (E.rel_ext ? E.rel_ext : E.s.rel_dense) : nullptr;
     a.d = E.dim;
     a.lr = E.m.lr;
     a.eps = E.m.eps;

@@ -1,0 +1,202 @@
+"""Multi-GPU path on CPU: the conflict-free round schedule (C-ABI, host code) and the
+DistributedTrainer orchestration (lockstep relation all-reduce, P2P partition handoff) with gloo,
+world_size 2, over the CPU oracle backend (tests/dist_oracle_backend.py).
+
+Bars: the schedule covers every bucket exactly once with no partition on two ranks in a round;
+a 2-rank epoch leaves every parameter bit-identical to a serial replay of the same lockstep
+schedule (node updates on disjoint partitions; relation gradients summed g0 + g1, fp32 addition
+being commutative), and the relation replicas bit-identical across ranks.
+"""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_2101_08358_b200 as eb  # noqa: E402
+from paper_2101_08358_b200 import distributed as ed  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.mark.parametrize("p,world", [(2, 1), (4, 1), (4, 2), (8, 2), (8, 4), (16, 1), (16, 2), (16, 4), (16, 8),
+                                     (32, 8), (1, 1)])
+def test_round_schedule_is_conflict_free_cover(p, world):
+    plan = ed.make_rounds(p, world)
+    assert plan.rounds == max(1, p - 1)
+    assert sorted(plan.order.tolist()) == list(range(p * p)), "every bucket exactly once"
+    for r in range(plan.rounds):
+        assert set(np.unique(plan.holder[r]).tolist()) == set(range(world))
+        counts = []
+        for g in range(world):
+            held = set(plan.partitions(r, g))
+            assert len(held) == p // world
+            bk = plan.buckets(r, g)
+            counts.append(len(bk))
+            for _, i, j in bk:
+                assert i in held and j in held, "bucket trained on a rank that does not hold its partitions"
+        assert len(set(counts)) == 1, "rounds balanced across ranks (bucket count)"
+    # self-buckets at first residency (round 0)
+    for s in range(p * p):
+        i, j = divmod(int(plan.order[s]), p)
+        if i == j:
+            assert plan.round[s] == 0
+    # positions are grouped by round, then rank
+    assert (np.diff(plan.round.astype(np.int64)) >= 0).all()
+
+
+def test_round_schedule_handoff_volume():
+    """p=16 over 8 GPUs: every round moves at most 2 partitions into each GPU (and the greedy
+    assignment keeps at least one partition in place for most GPUs)."""
+    plan = ed.make_rounds(16, 8)
+    for r in range(plan.rounds - 1):
+        moves = plan.transfers(r)
+        into = np.bincount([dst for _, _, dst in moves], minlength=8)
+        assert into.max() <= 2
+        assert len(moves) <= 16
+
+
+def test_round_schedule_errors():
+    for p, w in [(3, 1), (4, 3), (16, 3), (1, 2), (0, 1)]:
+        with pytest.raises(eb.ConfigError):
+            ed.make_rounds(p, w)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+CFG = dict(kind="distmult", dim=16, V=1200, R=6, p=4, nt=32, alpha=0.5, neg_seed=3, b=150, seed=11, epochs=2)
+
+
+def _graph():
+    edges, split = eb.generate_graph(CFG["V"], CFG["R"], 4000, seed=5, train_frac=0.9, valid_frac=0.05)
+    return eb.bucket_edges(edges[split == 0], CFG["V"], CFG["p"])
+
+
+def _backend(edges):
+    sys.path.insert(0, HERE)
+    from dist_oracle_backend import OracleBackend
+    return OracleBackend(CFG["kind"], CFG["dim"], CFG["V"], CFG["R"], CFG["p"], CFG["nt"], CFG["alpha"],
+                         CFG["neg_seed"], edges)
+
+
+def _worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    edges, off = _graph()
+    be = _backend(edges)
+    tr = ed.DistributedTrainer(be, CFG["p"], off, CFG["b"], rank, world, relations=True, dist=dist)
+    tr.init_embeddings(CFG["seed"])
+    n = 0
+    for ep in range(CFG["epochs"]):
+        n += tr.train_epoch(ep)["edges"]
+    held = sorted(be.held)
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), held=np.array(held), theta=be.theta, acc=be.acc,
+             rel_theta=be.rel_theta, rel_acc=be.rel_acc, edges=np.array([n]), hb=np.array([tr.handoff_bytes]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _serial_replay(world):
+    """The same lockstep schedule in one process: all ranks' batches of a step, node updates in
+    place, relation gradients summed in rank order before one relation Adagrad."""
+    edges, off = _graph()
+    be = _backend(edges)
+    for x in range(CFG["p"]):
+        be.init_partition(x, CFG["seed"])
+    be.init_relations(CFG["seed"])
+    plan = ed.make_rounds(CFG["p"], world)
+    n = 0
+    for ep in range(CFG["epochs"]):
+        for r in range(plan.rounds):
+            lists = [ed.round_batches(plan, off, CFG["b"], r, g) for g in range(world)]
+            for s in range(max(len(x) for x in lists)):
+                total = torch.zeros_like(be.rel_grad_t)
+                for g in range(world):
+                    if s < len(lists[g]):
+                        pos, i, j, k, lo, hi, begin, nb = lists[g][s]
+                        be.train_batch(pos, i, j, k, lo, hi, begin, nb, ep)
+                        total = total + be.rel_grad_t  # fp32, rank order
+                        n += nb
+                be.rel_grad_t.copy_(total)
+                be.apply_relations()
+    return be, n, off
+
+
+def test_two_rank_epochs_bit_identical_to_serial_replay(tmp_path):
+    import torch.multiprocessing as mp
+    world = 2
+    port = _free_port()
+    mp.start_processes(_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True, start_method="spawn")
+    ref, n_ref, off = _serial_replay(world)
+    assert n_ref == CFG["epochs"] * int(off[-1])
+    got_theta = np.full_like(ref.theta, np.nan)
+    got_acc = np.full_like(ref.acc, np.nan)
+    total_edges = 0
+    rel = []
+    for g in range(world):
+        z = np.load(tmp_path / f"rank{g}.npz")
+        total_edges += int(z["edges"][0])
+        for x in z["held"]:
+            o, sz = eb.partition_offset(CFG["V"], CFG["p"], int(x)), eb.partition_size(CFG["V"], CFG["p"], int(x))
+            got_theta[o:o + sz] = z["theta"][o:o + sz]
+            got_acc[o:o + sz] = z["acc"][o:o + sz]
+        rel.append((z["rel_theta"], z["rel_acc"]))
+        assert int(z["hb"][0]) > 0, "partitions were handed off between rounds"
+    assert total_edges == n_ref, "every training edge consumed exactly once per epoch"
+    assert not np.isnan(got_theta).any(), "every partition ends on exactly one rank"
+    assert got_theta.tobytes() == ref.theta.tobytes()
+    assert got_acc.tobytes() == ref.acc.tobytes()
+    assert rel[0][0].tobytes() == rel[1][0].tobytes() == ref.rel_theta.tobytes(), "relation replicas identical"
+    assert rel[0][1].tobytes() == rel[1][1].tobytes() == ref.rel_acc.tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["complex", "dot"])
+def test_gpu_backend_single_rank_matches_direct_training(kind):
+    """The product backend (GpuBackend: C-ABI step, external relation reduction through an NCCL
+    all-reduce on the context stream, dense relation Adagrad) on a 1-rank NCCL group leaves every
+    parameter bit-identical to training the same bucket sequence directly (in-place relations)."""
+    import torch.distributed as dist
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    V, R, p, d = 3000, 12, 4, 32
+    edges, split = eb.generate_graph(V, R, 20000, seed=5, train_frac=0.9, valid_frac=0.05)
+    bucketed, off = eb.bucket_edges(edges[split == 0], V, p)
+    dev_edges = torch.from_numpy(bucketed.view(np.int32)).cuda()
+    h = eb.Hyper(kind=kind, dim=d, batch_size=300, num_negatives=64, neg_seed=3, engine="tc")
+    port = _free_port()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda:0"))
+    try:
+        tr = eb.Trainer(h, V, R, p, device=0, allocate=False)
+        be = ed.GpuBackend(tr, dev_edges)
+        D = ed.DistributedTrainer(be, p, off, 300, 0, 1, relations=kind != "dot", dist=dist)
+        D.init_embeddings(11)
+        for ep in range(2):
+            D.train_epoch(ep)
+        torch.cuda.synchronize()
+        ref = eb.Trainer(h, V, R, p, device=0)
+        ref.init_embeddings(11)
+        seq = np.stack([D.plan.order // p, D.plan.order % p], 1)
+        for ep in range(2):
+            ref.train_epoch(dev_edges, off, seq, ep)
+        th_ref, ac_ref = ref.node_table()
+        tabs = D.local_tables()
+        th = np.concatenate([tabs[x][0].cpu().numpy() for x in range(p)])
+        ac = np.concatenate([tabs[x][1].cpu().numpy() for x in range(p)])
+        assert th.tobytes() == th_ref.tobytes()
+        assert ac.tobytes() == ac_ref.tobytes()
+        if kind != "dot":
+            assert tr.rel_theta.cpu().numpy().tobytes() == ref.rel_theta.cpu().numpy().tobytes()
+            assert tr.rel_acc.cpu().numpy().tobytes() == ref.rel_acc.cpu().numpy().tobytes()
+    finally:
+        dist.destroy_process_group()
