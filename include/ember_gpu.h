@@ -146,6 +146,12 @@ int ember_eval_ranks(ember_ctx* ctx, const uint32_t* test_edges_dev, uint32_t n_
                      uint64_t n_train, uint32_t n_eval_neg, float alpha_eval, uint32_t block, uint64_t eval_seed,
                      uint32_t* ranks_dev);
 
+/* Filtered protocol (FB15k-type configs): all nodes are
+ * candidates, candidates forming a known triple are skipped; filter_keys_dev: n_keys u64 sorted
+ * ascending, key = s<<40 | r<<24 | t. ranks_dev: 2*n_test (dst corruption ranks, then src). */
+int ember_eval_ranks_filtered(ember_ctx* ctx, const uint32_t* test_edges_dev, uint32_t n_test,
+                              const uint64_t* filter_keys_dev, uint64_t n_keys, uint32_t* ranks_dev);
+
 /* ---- ordering (reference ordering.h, bit-identical) -------------------------------------- */
 int ember_make_plan(int kind, uint32_t p, uint32_t c, uint64_t seed, uint32_t* seq_out /* 2*p*p */,
                     uint64_t* swap_count, uint32_t* admissions_out /* c + 2*p*p */, uint32_t* n_admissions,
@@ -212,7 +218,7 @@ int ember_buffer_acquire(ember_buffer* buf, uint32_t step, uint32_t* i_out, uint
 /* The bucket's work has been enqueued: evictees whose last use this was start writing back.
  * Releasing the last step ends the epoch (all residents are written back). */
 int ember_buffer_release(ember_buffer* buf, uint32_t step);
-/* Waits until every writeback has landed in host memory (between epochs). */
+/* Between epochs: the context stream and the host wait until every writeback has landed in host memory. */
 int ember_buffer_flush(ember_buffer* buf);
 int ember_buffer_stats(ember_buffer* buf, ember_buffer_report* out);
 /* The eviction decisions of one epoch: 3 u32 per swap (step, evicted, admitted); *n = swaps. */

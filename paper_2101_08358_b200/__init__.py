@@ -288,6 +288,17 @@ class Trainer:
         self.synchronize()
         return ranks.cpu().numpy().view(np.uint32)
 
+    def eval_ranks_filtered(self, test_edges, filter_keys):
+        """Filtered ranks against every node; filter_keys: sorted packed u64
+        keys (s<<40 | r<<24 | t) of the known triples, on the device (int64 tensor)."""
+        t = self.torch
+        n = int(test_edges.shape[0])
+        ranks = t.empty(2 * n, dtype=t.int32, device=self.dev)
+        check(lib().ember_eval_ranks_filtered(self.ctx, _ptr(test_edges), n, _ptr(filter_keys),
+                                              int(filter_keys.numel()), _ptr(ranks)))
+        self.synchronize()
+        return ranks.cpu().numpy().view(np.uint32)
+
     def profile(self, enable: bool = True):
         check(lib().ember_profile_enable(self.ctx, 1 if enable else 0))
 

@@ -71,6 +71,7 @@ def _declare(L):
         "ember_adagrad_apply": (C.c_int, [vp, vp, vp, u32, u32, u32, i32]),
         "ember_debug_scores": (C.c_int, [vp, vp, u32, u32, u32, vp, i32, u32, vp]),
         "ember_eval_ranks": (C.c_int, [vp, vp, u32, vp, u64, u32, f32, u32, u64, vp]),
+        "ember_eval_ranks_filtered": (C.c_int, [vp, vp, u32, vp, u64, vp]),
         "ember_make_plan": (C.c_int, [i32, u32, u32, u64, vp, C.POINTER(u64), vp, C.POINTER(u32), vp, vp]),
         "ember_lower_bound_swaps": (u64, [u32, u32]),
         "ember_elimination_swap_formula": (u64, [u32, u32]),
@@ -88,6 +89,9 @@ def _declare(L):
         "ember_buffer_stats": (C.c_int, [vp, C.POINTER(BufferReport)]),
         "ember_buffer_decisions": (C.c_int, [vp, vp, C.POINTER(u32)]),
         "ember_train_epoch_buffered": (C.c_int, [vp, vp, vp, vp, u64, C.POINTER(StepStats)]),
+        "ember_make_rounds": (C.c_int, [u32, u32, vp, vp, vp, vp, C.POINTER(u32)]),
+        "ember_relations_external": (C.c_int, [vp, vp]),
+        "ember_relations_apply_dense": (C.c_int, [vp, vp]),
         "ember_comm_init": (C.c_int, [vp, vp, i32, i32]),
         "ember_comm_barrier": (C.c_int, [vp]),
         "ember_partition_copy": (C.c_int, [vp, vp, vp, i32, vp, vp, i32, u64]),

@@ -17,7 +17,9 @@
 //   compute at the eviction step t_k waits on load k.
 //
 // Loads are issued as soon as their dependencies are issued, so each prefetch runs ahead of
-// the computation while at most c + 2 slots exist. All copies and waits
+// the computation while at most c + 2 slots exist. The epoch's initial
+// fill is waited for per partition at its first use, and the epoch-end flush of each final
+// resident starts right after its last use, so both overlap the computation as well. All copies and waits
 // are stream-ordered; the host blocks only in flush() and stats(). Stall time = compute waiting
 // on a load, measured on the device (event on the compute stream before the wait vs the load's
 // completion event).
@@ -51,6 +53,8 @@ struct PartitionBuffer {
     std::vector<uint32_t> fill;            // first c admissions, in order (slot m <- fill[m])
     std::vector<Swap> swaps;
     std::vector<std::vector<uint32_t>> wb_at;  // step -> swaps whose evictee is released there
+    std::vector<std::vector<uint32_t>> flush_at;  // step -> final residents whose last use it is
+    std::vector<int> final_slot;                  // partition -> slot at epoch end (-1: not resident)
 
     // per-epoch progress
     uint32_t cursor = 0;
@@ -59,7 +63,8 @@ struct PartitionBuffer {
     std::vector<int> slot_of;  // partition -> slot while resident (plan state), -1 otherwise
     std::vector<uint8_t> wb_ready;  // swap -> its writeback has been issued
     std::vector<uint8_t> waited;    // swap -> the compute stream waited on its load, stall not yet read
-    std::vector<cudaEvent_t> ev_release, ev_wb, ev_load, ev_need, ev_fill;
+    std::vector<uint8_t> fill_pending;  // partition -> compute has not yet waited for its fill load
+    std::vector<cudaEvent_t> ev_release, ev_wb, ev_load, ev_need, ev_fill, ev_fillm;
 
     uint64_t reads = 0, writes = 0, bytes_read = 0, bytes_written = 0, epochs = 0;
     double stall_ms = 0.0;
@@ -128,6 +133,11 @@ struct PartitionBuffer {
                 where[need] = (int)s.slot;
             }
         }
+        // epoch-end flush: each final resident is written back right after its last use
+        flush_at.assign(steps, {});
+        final_slot = where;
+        for (uint32_t x = 0; x < p; ++x)
+            if (where[x] >= 0) flush_at[uses[x].back()].push_back(x);
     }
 
     void bind(uint32_t part, int s) {
@@ -176,16 +186,24 @@ struct PartitionBuffer {
         waited.assign(swaps.size(), 0);
         slot_of.assign(p, -1);
         for (uint32_t k = 0; k < p; ++k) bind(k, -1);
-        // the initial fill on the load stream, then the first two prefetches
-        EMBER_CUDA(cudaEventRecord(ev_fill[0], E->stream));  // previous work on the tables done
-        EMBER_CUDA(cudaStreamWaitEvent(load_st, ev_fill[0], 0));
+        // The initial fill on the load stream, each partition with its own completion event (the
+        // compute stream waits per partition at its first use). The loads wait for the previous
+        // epoch's flush (host read-after-write, slot write-after-read) or, in the first epoch,
+        // for the work enqueued before (init).
+        if (epochs == 0) {
+            EMBER_CUDA(cudaEventRecord(ev_fill[0], E->stream));
+            EMBER_CUDA(cudaStreamWaitEvent(load_st, ev_fill[0], 0));
+        } else {
+            EMBER_CUDA(cudaStreamWaitEvent(load_st, ev_fill[3], 0));
+        }
+        fill_pending.assign(p, 0);
         for (uint32_t m = 0; m < fill.size(); ++m) {
             copy_in(fill[m], m, load_st);
+            EMBER_CUDA(cudaEventRecord(ev_fillm[m], load_st));
             slot_of[fill[m]] = (int)m;
+            fill_pending[fill[m]] = 1;
+            bind(fill[m], (int)m);
         }
-        EMBER_CUDA(cudaEventRecord(ev_fill[1], load_st));
-        EMBER_CUDA(cudaStreamWaitEvent(E->stream, ev_fill[1], 0));
-        for (uint32_t m = 0; m < fill.size(); ++m) bind(fill[m], (int)m);
         pump_loads();
         in_epoch = true;
     }
@@ -214,6 +232,11 @@ struct PartitionBuffer {
         }
         const uint32_t i = seq[2 * step], j = seq[2 * step + 1];
         if (slot_of[i] < 0 || slot_of[j] < 0) throw EmberError("buffer: bucket partition not resident");
+        for (uint32_t x : {i, j})
+            if (fill_pending[x]) {
+                EMBER_CUDA(cudaStreamWaitEvent(E->stream, ev_fillm[(uint32_t)slot_of[x]], 0));
+                fill_pending[x] = 0;
+            }
         if (i_out) *i_out = i;
         if (j_out) *j_out = j;
     }
@@ -230,19 +253,19 @@ struct PartitionBuffer {
             EMBER_CUDA(cudaEventRecord(ev_wb[k], wb_st));
             wb_ready[k] = 1;
         }
+        for (uint32_t x : flush_at[step]) {  // epoch-end writeback of a final resident, overlapped
+            EMBER_CUDA(cudaStreamWaitEvent(wb_st, ev_release[step], 0));
+            copy_out(x, (uint32_t)final_slot[x], wb_st);
+        }
         pump_loads();
         ++cursor;
         if (cursor == steps) end_epoch();
     }
 
-    // Epoch end: every resident (dirty) partition is written back.
+    // Epoch end: every resident (dirty) partition has been written back after its last use
+    // (SPEC.md:326, :334); the next epoch's loads wait for these writes, the compute stream does not.
     void end_epoch() {
-        EMBER_CUDA(cudaEventRecord(ev_fill[2], E->stream));
-        EMBER_CUDA(cudaStreamWaitEvent(wb_st, ev_fill[2], 0));
-        for (uint32_t x = 0; x < p; ++x)
-            if (slot_of[x] >= 0) copy_out(x, (uint32_t)slot_of[x], wb_st);
         EMBER_CUDA(cudaEventRecord(ev_fill[3], wb_st));
-        EMBER_CUDA(cudaStreamWaitEvent(E->stream, ev_fill[3], 0));  // next epoch's fill reads host
         for (uint32_t x = 0; x < p; ++x) bind(x, -1);
         in_epoch = false;
         ++epochs;
@@ -266,10 +289,11 @@ struct PartitionBuffer {
         }
     }
 
+    // The context stream (and the host) wait until every writeback has landed in host memory.
     void flush() {
         if (in_epoch) throw ConfigError("buffer: flush in the middle of an epoch");
+        if (epochs) EMBER_CUDA(cudaStreamWaitEvent(E->stream, ev_fill[3], 0));
         EMBER_CUDA(cudaStreamSynchronize(E->stream));
-        EMBER_CUDA(cudaStreamSynchronize(wb_st));
     }
 
     ~PartitionBuffer() {
@@ -279,7 +303,7 @@ struct PartitionBuffer {
         if (wb_st) cudaStreamSynchronize(wb_st);
         if (in_epoch)
             for (uint32_t x = 0; x < p; ++x) bind(x, -1);
-        for (auto* v : {&ev_release, &ev_wb, &ev_load, &ev_need, &ev_fill})
+        for (auto* v : {&ev_release, &ev_wb, &ev_load, &ev_need, &ev_fill, &ev_fillm})
             for (cudaEvent_t e : *v) cudaEventDestroy(e);
         for (char* s : slot) cudaFree(s);
         if (load_st) cudaStreamDestroy(load_st);
@@ -326,6 +350,7 @@ PartitionBuffer* buffer_create(Engine& E, uint32_t c, const uint32_t* seq, uint3
         mk(B->ev_load, B->swaps.size(), true);
         mk(B->ev_need, B->swaps.size(), true);
         mk(B->ev_fill, 4, false);
+        mk(B->ev_fillm, c, false);
     } catch (...) {
         delete B;
         throw;

@@ -20,6 +20,8 @@ void graph_bucket(int device, uint64_t V, uint32_t p, const uint32_t* in, uint64
                   uint64_t* offsets);
 double tc_selftest(int device, int mode, int K, int N, uint64_t seed);
 double tc_mmabench(int device, int mode, int N, int iters, int nacc);
+void launch_eval_filtered(const Engine& E, const uint32_t* test, uint32_t n_test, const uint64_t* keys, uint64_t n_keys,
+                          uint32_t* ranks);
 struct PartitionBuffer;
 PartitionBuffer* buffer_create(Engine& E, uint32_t c, const uint32_t* seq, uint32_t steps, float* const* host_theta,
                                float* const* host_acc);
@@ -288,6 +290,17 @@ int ember_eval_ranks(ember_ctx* ctx, const uint32_t* test, uint32_t n_test, cons
         need(test, "test_edges_dev");
         need(ranks, "ranks_dev");
         launch_eval(E, test, n_test, train, n_train, n_eval, alpha_eval, block ? block : 1, eval_seed, ranks);
+    });
+}
+
+int ember_eval_ranks_filtered(ember_ctx* ctx, const uint32_t* test, uint32_t n_test, const uint64_t* keys,
+                              uint64_t n_keys, uint32_t* ranks) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        need(test, "test_edges_dev");
+        need(ranks, "ranks_dev");
+        if (n_keys) need(keys, "filter_keys_dev");
+        launch_eval_filtered(E, test, n_test, keys, n_keys, ranks);
     });
 }
 

@@ -91,7 +91,149 @@ __global__ void k_eval_rank(Tables T, const float* __restrict__ rel, int kind, u
     if (lane == 0) ranks[(uint64_t)side * n_test + e] = 1 + cnt;
 }
 
+// Filtered protocol: every node is a candidate for the corrupted slot, known
+// true triples (sorted packed keys s<<40 | r<<24 | t) are skipped, ties count against the
+// positive (rank = 1 + #{c != true : score(c) >= score(true), (c) not a known triple}).
+// One CTA ranks QB query vectors (test edge x side) against all nodes, streaming candidate rows
+// through shared memory in CB-row tiles; each thread owns a 4-query x 8-candidate register tile.
+constexpr int FQ = 64, FC = 128, FT = 256;
+
+__device__ __forceinline__ bool key_known(const uint64_t* __restrict__ keys, uint64_t n, uint64_t k) {
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (keys[mid] < k) lo = mid + 1; else hi = mid;
+    }
+    return lo < n && keys[lo] == k;
+}
+
+__global__ void __launch_bounds__(FT) k_eval_filtered(Tables T, const float* __restrict__ rel, int kind, uint32_t d,
+                                                      const uint32_t* __restrict__ test, uint32_t n_test,
+                                                      const uint64_t* __restrict__ keys, uint64_t n_keys,
+                                                      uint32_t* ranks) {
+    extern __shared__ float sm[];
+    const uint32_t ld = d + 1;  // padded row stride: conflict-free candidate reads
+    float* As = sm;                       // [FQ][ld]
+    float* Cs = As + FQ * ld;             // [FC][ld]
+    float* pos = Cs + FC * ld;            // [FQ]
+    uint32_t* meta = reinterpret_cast<uint32_t*>(pos + FQ);  // [FQ][4]: s, r, t, side|valid
+    const uint32_t tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+    const uint32_t nq = 2 * n_test, q0 = blockIdx.x * FQ;
+    const uint32_t h = d / 2;
+    for (uint32_t qq = wib; qq < FQ; qq += FT / 32) {
+        const uint32_t q = q0 + qq;
+        float* a = As + qq * ld;
+        if (q >= nq) {
+            for (uint32_t k = lane; k < d; k += 32) a[k] = 0.f;
+            if (lane == 0) meta[4 * qq + 3] = 0;
+            continue;
+        }
+        const uint32_t side = q / n_test, e = q % n_test;
+        const uint32_t s = test[3 * e], r = test[3 * e + 1], t = test[3 * e + 2];
+        const float* ts = row_any(T, s, d);
+        const float* tt = row_any(T, t, d);
+        const float* tr = kind == EMBER_DOT ? nullptr : rel + (uint64_t)r * d;
+        for (uint32_t k = lane; k < (kind == EMBER_COMPLEX ? h : d); k += 32) {
+            if (kind == EMBER_DOT) {
+                a[k] = side == 0 ? ts[k] : tt[k];
+            } else if (kind == EMBER_DISTMULT) {
+                a[k] = side == 0 ? ts[k] * tr[k] : tr[k] * tt[k];
+            } else {
+                const float c = tr[k], ee = tr[h + k];
+                if (side == 0) {
+                    a[k] = ts[k] * c - ts[h + k] * ee;
+                    a[h + k] = ts[k] * ee + ts[h + k] * c;
+                } else {
+                    a[k] = c * tt[k] + ee * tt[h + k];
+                    a[h + k] = c * tt[h + k] - ee * tt[k];
+                }
+            }
+        }
+        __syncwarp();
+        const float* other = side == 0 ? tt : ts;
+        float ps = 0.f;
+        for (uint32_t k = lane; k < d; k += 32) ps += a[k] * other[k];
+        for (int o = 16; o; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+        if (lane == 0) {
+            pos[qq] = ps;
+            meta[4 * qq] = s;
+            meta[4 * qq + 1] = r;
+            meta[4 * qq + 2] = t;
+            meta[4 * qq + 3] = 2 | side;
+        }
+    }
+    const uint32_t tq = tid >> 4, tc = tid & 15;  // queries tq*4 .. +3, candidates tc + 16*m
+    uint32_t cnt[4] = {0, 0, 0, 0};
+    for (uint64_t c0 = 0; c0 < T.V; c0 += FC) {
+        __syncthreads();
+        for (uint32_t x = tid; x < FC * d; x += FT) {
+            const uint32_t cr = x / d, k = x % d;
+            const uint64_t c = c0 + cr;
+            Cs[cr * ld + k] = c < T.V ? row_any(T, (uint32_t)c, d)[k] : 0.f;
+        }
+        __syncthreads();
+        float acc[4][8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+        for (uint32_t k = 0; k < d; ++k) {
+            float av[4], cv[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = As[(tq * 4 + i) * ld + k];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) cv[j] = Cs[(tc + 16 * j) * ld + k];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], cv[j], acc[i][j]);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t qq = tq * 4 + i;
+            const uint32_t mt = meta[4 * qq + 3];
+            if (!(mt & 2)) continue;
+            const uint32_t side = mt & 1, s = meta[4 * qq], r = meta[4 * qq + 1], t = meta[4 * qq + 2];
+            const float ps = pos[qq];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint64_t c = c0 + tc + 16 * j;
+                if (c >= T.V || acc[i][j] < ps) continue;
+                if (c == (side == 0 ? t : s)) continue;
+                const uint64_t key = side == 0 ? ((uint64_t)s << 40 | (uint64_t)r << 24 | c)
+                                               : (c << 40 | (uint64_t)r << 24 | t);
+                if (!key_known(keys, n_keys, key)) ++cnt[i];
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        uint32_t v = cnt[i];
+        for (int o = 8; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        const uint32_t q = q0 + tq * 4 + i;
+        if (tc == 0 && q < nq) ranks[q] = 1 + v;  // q = side * n_test + e
+    }
+}
+
 }  // namespace
+
+void launch_eval_filtered(const Engine& E, const uint32_t* test, uint32_t n_test, const uint64_t* keys, uint64_t n_keys,
+                          uint32_t* ranks) {
+    if (!n_test) return;
+    for (uint32_t k = 0; k < E.parts.size(); ++k) E.view(k);
+    if (E.m.kind != EMBER_DOT && !E.rel_theta) throw ConfigError("relation table not bound");
+    PartView* parts = nullptr;
+    EMBER_CUDA(cudaMallocAsync(&parts, E.parts.size() * sizeof(PartView), E.stream));
+    EMBER_CUDA(cudaMemcpyAsync(parts, E.parts.data(), E.parts.size() * sizeof(PartView), cudaMemcpyHostToDevice,
+                               E.stream));
+    Tables T{parts, E.g.num_nodes, E.g.num_partitions};
+    const size_t smem = ((size_t)(FQ + FC) * (E.dim + 1) + FQ) * sizeof(float) + FQ * 4 * sizeof(uint32_t);
+    EMBER_CUDA(cudaFuncSetAttribute(k_eval_filtered, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const uint32_t blocks = (2 * n_test + FQ - 1) / FQ;
+    k_eval_filtered<<<blocks, FT, smem, E.stream>>>(T, E.rel_theta, E.m.kind, E.dim, test, n_test, keys, n_keys, ranks);
+    EMBER_LAUNCHED(E);
+    EMBER_CUDA(cudaFreeAsync(parts, E.stream));
+}
 
 void launch_eval(const Engine& E, const uint32_t* test, uint32_t n_test, const uint32_t* train, uint64_t n_train,
                  uint32_t n_eval, float alpha_eval, uint32_t block, uint64_t eval_seed, uint32_t* ranks) {
