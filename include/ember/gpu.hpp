@@ -71,6 +71,38 @@ private:
     ember_ctx* ctx_ = nullptr;
 };
 
+// PartitionBuffer on the device: capacity HBM slots over pinned host backing,
+// replaying one plan per epoch (Belady eviction, prefetch, async writeback).
+class PartitionBuffer {
+public:
+    PartitionBuffer(Context& ctx, uint32_t capacity, const std::vector<uint32_t>& seq,
+                    const std::vector<float*>& host_theta, const std::vector<float*>& host_acc) : ctx_(&ctx) {
+        check(ember_buffer_create(ctx.get(), capacity, seq.data(), (uint32_t)(seq.size() / 2), host_theta.data(),
+                                  host_acc.data(), &buf_));
+    }
+    PartitionBuffer(const PartitionBuffer&) = delete;
+    PartitionBuffer& operator=(const PartitionBuffer&) = delete;
+    ~PartitionBuffer() {
+        if (buf_) ember_buffer_destroy(buf_);
+    }
+    // train_epoch_partitioned through the buffer
+    ember_step_stats train_epoch(const uint32_t* edges_dev, const std::vector<uint64_t>& offsets, uint64_t epoch) {
+        ember_step_stats st{};
+        check(ember_train_epoch_buffered(ctx_->get(), buf_, edges_dev, offsets.data(), epoch, &st));
+        return st;
+    }
+    void flush() { check(ember_buffer_flush(buf_)); }
+    ember_buffer_report report() {
+        ember_buffer_report r{};
+        check(ember_buffer_stats(buf_, &r));
+        return r;
+    }
+
+private:
+    Context* ctx_;
+    ember_buffer* buf_ = nullptr;
+};
+
 // make_plan (ordering.h:80) through the C-ABI: the bucket sequence as (i, j) pairs.
 inline std::vector<std::pair<uint32_t, uint32_t>> bucket_sequence(int kind, uint32_t p, uint32_t c, uint64_t seed) {
     std::vector<uint32_t> seq(2ull * p * p), adm(c + 2ull * p * p + 1), swaps(6ull * p * p + 3), state(1ull * p * p);

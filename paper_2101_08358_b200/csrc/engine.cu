@@ -102,7 +102,12 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     if (st) {
         stream = st;
     } else {
-        EMBER_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        // The step stream gets the highest priority: when the helper stream's sort blocks and the
+        // step's kernels compete for SMs, the block scheduler dispatches the step's blocks first.
+        int least = 0, greatest = 0;
+        EMBER_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        const char* pr = getenv("EMBER_STREAM_PRIORITY");
+        EMBER_CUDA(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, pr && atoi(pr) == 0 ? least : greatest));
         own_stream = true;
     }
     if (getenv("EMBER_SERIAL_SORT"))  // A/B switch: sort on the step stream (no overlap)
@@ -130,7 +135,7 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     s.dA = dalloc<float>(2 * (uint64_t)std::max<uint64_t>(b, (uint64_t)pad_rows(cap_b)) * d);
     s.grows = dalloc<float>((uint64_t)cap_rows * d);
     s.loss = dalloc<float>(1);
-    s.loss_part = reinterpret_cast<float*>(dalloc<double>(b / 4096 + 2));
+    s.loss_part = reinterpret_cast<float*>(dalloc<double>(b / 512 + 2));  // one per k_loss block
     s.loss_done = dalloc<uint32_t>(1);
     EMBER_CUDA(cudaMemset(s.loss_done, 0, sizeof(uint32_t)));
     s.keys = dalloc<uint32_t>(cap_rows);
@@ -143,9 +148,12 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     s.offsets = dalloc<uint32_t>(cap_rows);
     s.nruns = dalloc<uint32_t>(1);
     s.nunique = dalloc<uint32_t>(2);
-    s.longs = dalloc<uint32_t>(2 + 3 * (cap_rows / 64 + 1));
-    s.long_owner = dalloc<uint32_t>(cap_rows / 64 + cap_rows / 64 + 2);
-    s.long_partial = dalloc<float>((uint64_t)(cap_rows / 64 + cap_rows / 64 + 2) * d);
+    // at most cap_rows / LONG_SEG long segments, each with <= len / LONG_CHUNK + 1 chunks
+    const uint32_t max_long = cap_rows / EMBER_LONG_SEG + 1;
+    const uint32_t max_chunks = cap_rows / EMBER_LONG_CHUNK + max_long;
+    s.longs = dalloc<uint32_t>(2 + 3 * max_long);
+    s.long_owner = dalloc<uint32_t>(max_chunks);
+    s.long_partial = dalloc<float>((uint64_t)max_chunks * d);
     EMBER_CUDA(cudaMemset(s.nunique, 0, 2 * sizeof(uint32_t)));
     EMBER_CUDA(cudaMemset(s.longs, 0, 2 * sizeof(uint32_t)));
     if (m.engine == EMBER_ENGINE_SIMT_FP32) {

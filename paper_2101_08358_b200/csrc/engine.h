@@ -18,6 +18,11 @@
 
 namespace ember {
 
+// Segmented reduction: keys with more than EMBER_LONG_SEG gradient rows take the chunked path
+// (EMBER_LONG_CHUNK-row chunk partials, kernels_step.cu).
+#define EMBER_LONG_SEG 64
+#define EMBER_LONG_CHUNK 32
+
 #define EMBER_CUDA(call)                                                                        \
     do {                                                                                        \
         cudaError_t e_ = (call);                                                                \

@@ -26,11 +26,6 @@ __device__ __forceinline__ const float* node_row(const PartView& v, uint32_t id,
 
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 
-// Loads a dim-float row into shared memory with float4 lanes.
-__device__ __forceinline__ void warp_load_row(float* dst, const float* src, uint32_t d, uint32_t lane) {
-    for (uint32_t v = lane; v < d / 4; v += 32) reinterpret_cast<float4*>(dst)[v] = ldg4(src + 4 * v);
-}
-
 __global__ void k_sample(uint32_t* out, uint32_t nt, uint32_t n_deg, uint32_t total, uint64_t base,
                          const uint32_t* __restrict__ bucket, uint64_t bucket_n, uint64_t src_first, uint64_t src_rows,
                          uint64_t dst_first, uint64_t dst_rows) {
@@ -51,37 +46,68 @@ __global__ void k_sample(uint32_t* out, uint32_t nt, uint32_t n_deg, uint32_t to
     out[slot] = id;
 }
 
-// Adjusted vectors at coordinate k (ss/sr/st = source, relation, destination rows):
-//   ad = the row the destination is scored against (s o r; ComplEx s * r),
-//   as = the row the source is scored against      (r o t; ComplEx r * conj(t)),
-// so that f(s, r, t) = ad . t = s . as (ComplEx halves [re | im]).
-// Products are rounded individually (no FMA contraction), like the oracle.
-__device__ __forceinline__ void adjust_at(int kind, uint32_t d, uint32_t k, const float* ss, const float* sr,
-                                          const float* st, float& ad, float& as) {
-    if (k >= d) {
-        ad = as = 0.f;
-    } else if (kind == EMBER_DOT) {
-        ad = ss[k];
-        as = st[k];
-    } else if (kind == EMBER_DISTMULT) {
-        ad = __fmul_rn(ss[k], sr[k]);
-        as = __fmul_rn(sr[k], st[k]);
+// Coordinates are handled in quads: quad q of a row is {4q .. 4q+3} for Dot/DistMult and, for
+// ComplEx ([re | im] halves of h = d/2), the two complex pairs {2q, 2q+1} (re) and
+// {h+2q, h+2q+1} (im), so that every lane loads its rows' quads straight into registers with
+// 16- or 8-byte loads (d % 4 == 0 keeps both aligned) and computes ComplEx products locally.
+struct Quad {
+    float v[4];
+};
+
+__device__ __forceinline__ Quad load_quad(const float* row, int kind, uint32_t h, uint32_t q) {
+    Quad x;
+    if (kind == EMBER_COMPLEX) {
+        const float2 a = __ldg(reinterpret_cast<const float2*>(row + 2 * q));
+        const float2 b = __ldg(reinterpret_cast<const float2*>(row + h + 2 * q));
+        x.v[0] = a.x, x.v[1] = a.y, x.v[2] = b.x, x.v[3] = b.y;
     } else {
-        const uint32_t h = d / 2, kk = k < h ? k : k - h;
-        const float a = ss[kk], b = ss[h + kk], c = sr[kk], e = sr[h + kk], x = st[kk], y = st[h + kk];
-        if (k < h) {
-            ad = __fsub_rn(__fmul_rn(a, c), __fmul_rn(b, e));
-            as = __fadd_rn(__fmul_rn(c, x), __fmul_rn(e, y));
-        } else {
-            ad = __fadd_rn(__fmul_rn(a, e), __fmul_rn(b, c));
-            as = __fsub_rn(__fmul_rn(c, y), __fmul_rn(e, x));
+        const float4 a = ldg4(row + 4 * q);
+        x.v[0] = a.x, x.v[1] = a.y, x.v[2] = a.z, x.v[3] = a.w;
+    }
+    return x;
+}
+
+__device__ __forceinline__ void store_quad(float* row, int kind, uint32_t h, uint32_t q, const Quad& x) {
+    if (kind == EMBER_COMPLEX) {
+        *reinterpret_cast<float2*>(row + 2 * q) = make_float2(x.v[0], x.v[1]);
+        *reinterpret_cast<float2*>(row + h + 2 * q) = make_float2(x.v[2], x.v[3]);
+    } else {
+        *reinterpret_cast<float4*>(row + 4 * q) = make_float4(x.v[0], x.v[1], x.v[2], x.v[3]);
+    }
+}
+
+// Adjusted quads: ad = the row the destination is scored against (s o r; ComplEx s * r), as = the
+// row the source is scored against (r o t; ComplEx r * conj(t)), so that f(s, r, t) = ad . t = s . as
+// (ComplEx halves [re | im]). Products are rounded individually (no
+// FMA contraction), like the oracle.
+__device__ __forceinline__ void adjust_quad(int kind, const Quad& S, const Quad& R, const Quad& T, Quad& ad,
+                                            Quad& as) {
+    if (kind == EMBER_DOT) {
+        ad = S;
+        as = T;
+    } else if (kind == EMBER_DISTMULT) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            ad.v[i] = __fmul_rn(S.v[i], R.v[i]);
+            as.v[i] = __fmul_rn(R.v[i], T.v[i]);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {  // i: re index i, im index 2 + i
+            const float a = S.v[i], b = S.v[2 + i], c = R.v[i], e = R.v[2 + i], x = T.v[i], y = T.v[2 + i];
+            ad.v[i] = __fsub_rn(__fmul_rn(a, c), __fmul_rn(b, e));
+            as.v[i] = __fadd_rn(__fmul_rn(c, x), __fmul_rn(e, y));
+            ad.v[2 + i] = __fadd_rn(__fmul_rn(a, e), __fmul_rn(b, c));
+            as.v[2 + i] = __fsub_rn(__fmul_rn(c, y), __fmul_rn(e, x));
         }
     }
 }
 
 // One warp per edge (rows up to rows_pad: the packed layout is zero-padded to whole tiles).
-// PACKED: lane l < KP/8 owns coordinates 8l..8l+7 and writes their bf16 hi|lo 16-byte core-matrix
-// rows for both sides; else fp32 rows A[0][e] = ad, A[1][e] = as. fpos[e] = ad . t.
+// Lanes load their quads of the source, relation and destination rows into registers and form
+// the adjusted quads. PACKED: the adjusted rows are staged in shared memory (2 x KP floats per
+// warp), then lane l < 2CB packs 8 consecutive coordinates into their bf16 hi|lo 16-byte
+// core-matrix rows; else fp32 rows A[0][e] = ad, A[1][e] = as. fpos[e] = ad . t.
 template <bool PACKED>
 __global__ void k_gather_adjust(const uint32_t* __restrict__ edges, uint32_t nb, uint32_t rows_pad, PartView pi,
                                 PartView pj, const float* __restrict__ rel, int kind, uint32_t d, uint32_t CB,
@@ -92,7 +118,8 @@ __global__ void k_gather_adjust(const uint32_t* __restrict__ edges, uint32_t nb,
     const uint32_t e = blockIdx.x * (blockDim.x >> 5) + wib;
     if (e >= (PACKED ? rows_pad : nb)) return;
     uint4* P = reinterpret_cast<uint4*>(Apk);
-    if (PACKED && e >= nb) {  // zero padding rows of the last tiles
+    const uint32_t kp = 8 * CB;  // padded dim (packed)
+    if (PACKED && e >= nb) {     // zero padding rows of the last tiles
         const uint4 z = make_uint4(0, 0, 0, 0);
         for (uint32_t c = lane; c < 4 * CB; c += 32) {
             const uint32_t side = c / (2 * CB), cb = c % (2 * CB);
@@ -100,50 +127,41 @@ __global__ void k_gather_adjust(const uint32_t* __restrict__ edges, uint32_t nb,
         }
         return;
     }
-    float* ss = sm + wib * 3 * d;
-    float* sr = ss + d;
-    float* st = sr + d;
     const uint32_t s = edges[3 * e], r = edges[3 * e + 1], t = edges[3 * e + 2];
-    warp_load_row(ss, node_row(pi, s, d), d, lane);
-    warp_load_row(st, node_row(pj, t, d), d, lane);
-    if (kind != EMBER_DOT) warp_load_row(sr, rel + (uint64_t)r * d, d, lane);
-    __syncwarp();
+    const float* ss = node_row(pi, s, d);
+    const float* st = node_row(pj, t, d);
+    const float* sr = kind != EMBER_DOT ? rel + (uint64_t)r * d : nullptr;
+    const uint32_t h = d / 2, nq = d / 4;
+    float* xd = sm + wib * 2 * kp;
+    float* xs = xd + kp;
     float part = 0.f;
-    if (PACKED) {
-        // all lanes compute the adjusted rows (coalesced smem reads) into the source-row slot and
-        // the spare slot, then lanes < 2CB pack 8 consecutive coordinates each
-        const uint32_t kp = 8 * CB;  // padded dim
-        float* xd = sm + (blockDim.x >> 5) * 3 * d + wib * 2 * kp;
-        float* xs = xd + kp;
-        for (uint32_t k = lane; k < kp; k += 32) {
-            float x = 0.f, y = 0.f;
-            if (k < d) {
-                adjust_at(kind, d, k, ss, sr, st, x, y);
-                part += x * st[k];
-            }
-            xd[k] = x;
-            xs[k] = y;
+    for (uint32_t q = lane; q < nq; q += 32) {
+        const Quad S = load_quad(ss, kind, h, q), T = load_quad(st, kind, h, q);
+        const Quad R = sr ? load_quad(sr, kind, h, q) : S;
+        Quad ad, as;
+        adjust_quad(kind, S, R, T, ad, as);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) part += ad.v[i] * T.v[i];
+        if (PACKED) {
+            store_quad(xd, kind, h, q, ad);
+            store_quad(xs, kind, h, q, as);
+        } else {
+            store_quad(A + (uint64_t)e * d, kind, h, q, ad);
+            store_quad(A + ((uint64_t)nb + e) * d, kind, h, q, as);
         }
+    }
+    if (PACKED) {
+        for (uint32_t k = d + lane; k < kp; k += 32) xd[k] = xs[k] = 0.f;  // K padding
         __syncwarp();
         if (lane < 2 * CB) {
             const uint32_t cb = lane % CB, side = lane / CB;
             const float4* src = reinterpret_cast<const float4*>((side == 0 ? xd : xs) + 8 * cb);
-            const float4 v0 = src[0], v1 = src[1];  // zero past d (written above, up to KP)
+            const float4 v0 = src[0], v1 = src[1];
             float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-            uint4 h, l;
-            tc::split8(v, h, l);
-            P[((uint64_t)side * 2 * CB + cb) * cap + e] = h;
-            P[((uint64_t)side * 2 * CB + CB + cb) * cap + e] = l;
-        }
-    } else {
-        float* ad = A + (uint64_t)e * d;
-        float* as = A + ((uint64_t)nb + e) * d;
-        for (uint32_t k = lane; k < d; k += 32) {
-            float x, y;
-            adjust_at(kind, d, k, ss, sr, st, x, y);
-            ad[k] = x;
-            as[k] = y;
-            part += x * st[k];
+            uint4 hq, lq;
+            tc::split8(v, hq, lq);
+            P[((uint64_t)side * 2 * CB + cb) * cap + e] = hq;
+            P[((uint64_t)side * 2 * CB + CB + cb) * cap + e] = lq;
         }
     }
     for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
@@ -211,77 +229,86 @@ __global__ void k_rank(const uint32_t* __restrict__ vals_sorted, uint32_t n, uin
     if (p < n) rank[vals_sorted[p]] = p;
 }
 
-// Chain rule (one warp per edge), adjusted vectors recomputed from the staged rows. dA excludes
-// the positive term, added here:
+// dA quad q of (side, edge e): column-blocked [2][d/4][dcap][4] (tensor-core engine) or
+// row-major [2][nb][d] (SIMT engine, dcap == 0).
+__device__ __forceinline__ Quad load_dA_quad(const float* __restrict__ dA, uint32_t dcap, uint32_t nb, uint32_t side,
+                                             uint32_t e, int kind, uint32_t d, uint32_t q) {
+    const uint32_t h = d / 2;
+    if (!dcap) return load_quad(dA + ((uint64_t)side * nb + e) * d, kind, h, q);
+    const float* base = dA + (uint64_t)side * (d / 4) * dcap * 4;
+    auto at = [&](uint32_t c) { return base + ((uint64_t)(c / 4) * dcap + e) * 4 + c % 4; };
+    Quad x;
+    if (kind == EMBER_COMPLEX) {
+        const float2 a = __ldg(reinterpret_cast<const float2*>(at(2 * q)));
+        const float2 b = __ldg(reinterpret_cast<const float2*>(at(h + 2 * q)));
+        x.v[0] = a.x, x.v[1] = a.y, x.v[2] = b.x, x.v[3] = b.y;
+    } else {
+        const float4 a = ldg4(at(4 * q));
+        x.v[0] = a.x, x.v[1] = a.y, x.v[2] = a.z, x.v[3] = a.w;
+    }
+    return x;
+}
+
+// Chain rule (one warp per edge, lanes on quads in registers), adjusted vectors recomputed from
+// the rows. dA excludes the positive term, added here:
 //   grad adj_dst = g0_dst * t + dA_dst,  grad adj_src = g0_src * s + dA_src,
 //   grad t += g0_dst * adj_dst (positive score = adj_dst . t), grad s += g0_src * adj_src.
 // Rows go to their sorted positions: source -> grows[rank[e]], destination -> grows[rank[nb + e]],
 // relation -> grows[rank[2nb + n_neg + e]].
-// dA is row-major [2][nb][d] (SIMT engine) or column-blocked [2][d/4][dcap][4] (tensor-core
-// engine, dcap = its padded row capacity): the rows are staged in shared memory either way.
-__global__ void k_chain_rule(const uint32_t* __restrict__ edges, uint32_t nb, uint32_t n_neg, PartView pi,
+__global__ void __launch_bounds__(256, 4) k_chain_rule(const uint32_t* __restrict__ edges, uint32_t nb, uint32_t n_neg, PartView pi,
                              PartView pj, const float* __restrict__ rel, int kind, uint32_t d,
                              const float* __restrict__ dA, uint32_t dcap, const float* __restrict__ g0,
                              const uint32_t* __restrict__ rank, float* __restrict__ grows) {
-    extern __shared__ float sm[];
     const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t e = blockIdx.x * (blockDim.x >> 5) + wib;
     if (e >= nb) return;
-    float* ss = sm + wib * 5 * d;
-    float* sr = ss + d;
-    float* st = sr + d;
-    float* u = st + d;  // dA of the destination side
-    float* w = u + d;   // dA of the source side
     const uint32_t s = edges[3 * e], r = edges[3 * e + 1], t = edges[3 * e + 2];
-    warp_load_row(ss, node_row(pi, s, d), d, lane);
-    warp_load_row(st, node_row(pj, t, d), d, lane);
-    if (kind != EMBER_DOT) warp_load_row(sr, rel + (uint64_t)r * d, d, lane);
-    if (dcap) {
-        const float4* D = reinterpret_cast<const float4*>(dA);
-        for (uint32_t c4 = lane; c4 < d / 4; c4 += 32) {
-            reinterpret_cast<float4*>(u)[c4] = __ldg(D + (uint64_t)c4 * dcap + e);
-            reinterpret_cast<float4*>(w)[c4] = __ldg(D + ((uint64_t)(d / 4) + c4) * dcap + e);
-        }
-    } else {
-        warp_load_row(u, dA + (uint64_t)e * d, d, lane);
-        warp_load_row(w, dA + ((uint64_t)nb + e) * d, d, lane);
-    }
-    __syncwarp();
+    const float* ss = node_row(pi, s, d);
+    const float* st = node_row(pj, t, d);
+    const float* sr = kind != EMBER_DOT ? rel + (uint64_t)r * d : nullptr;
     const float gd = g0[e], gs = g0[(uint64_t)nb + e];
     float* gS = grows + (uint64_t)rank[e] * d;
     float* gT = grows + (uint64_t)rank[nb + e] * d;
-    if (kind == EMBER_COMPLEX) {
-        float* gR = grows + (uint64_t)rank[2 * nb + n_neg + e] * d;
-        const uint32_t h = d / 2;
-        for (uint32_t k = lane; k < h; k += 32) {
-            const float a = ss[k], b = ss[h + k], c = sr[k], ee = sr[h + k], x = st[k], y = st[h + k];
-            float ad0, as0, ad1, as1;
-            adjust_at(kind, d, k, ss, sr, st, ad0, as0);
-            adjust_at(kind, d, h + k, ss, sr, st, ad1, as1);
-            const float u0 = u[k] + gd * x, u1 = u[h + k] + gd * y;
-            const float w0 = w[k] + gs * a, w1 = w[h + k] + gs * b;
-            gS[k] = gs * as0 + (u0 * c + u1 * ee);
-            gS[h + k] = gs * as1 + (u1 * c - u0 * ee);
-            gR[k] = (u0 * a + u1 * b) + (w0 * x + w1 * y);
-            gR[h + k] = (u1 * a - u0 * b) + (w0 * y - w1 * x);
-            gT[k] = gd * ad0 + (w0 * c - w1 * ee);
-            gT[h + k] = gd * ad1 + (w0 * ee + w1 * c);
+    float* gR = kind != EMBER_DOT ? grows + (uint64_t)rank[2 * nb + n_neg + e] * d : nullptr;
+    const uint32_t h = d / 2, nq = d / 4;
+    for (uint32_t q = lane; q < nq; q += 32) {
+        const Quad S = load_quad(ss, kind, h, q), T = load_quad(st, kind, h, q);
+        const Quad R = sr ? load_quad(sr, kind, h, q) : S;
+        const Quad U = load_dA_quad(dA, dcap, nb, 0, e, kind, d, q);  // destination side
+        const Quad W = load_dA_quad(dA, dcap, nb, 1, e, kind, d, q);  // source side
+        Quad ad, as, oS, oR, oT;
+        adjust_quad(kind, S, R, T, ad, as);
+        if (kind == EMBER_COMPLEX) {
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const float a = S.v[i], b = S.v[2 + i], c = R.v[i], ee = R.v[2 + i], x = T.v[i], y = T.v[2 + i];
+                const float u0 = U.v[i] + gd * x, u1 = U.v[2 + i] + gd * y;
+                const float w0 = W.v[i] + gs * a, w1 = W.v[2 + i] + gs * b;
+                oS.v[i] = gs * as.v[i] + (u0 * c + u1 * ee);
+                oS.v[2 + i] = gs * as.v[2 + i] + (u1 * c - u0 * ee);
+                oR.v[i] = (u0 * a + u1 * b) + (w0 * x + w1 * y);
+                oR.v[2 + i] = (u1 * a - u0 * b) + (w0 * y - w1 * x);
+                oT.v[i] = gd * ad.v[i] + (w0 * c - w1 * ee);
+                oT.v[2 + i] = gd * ad.v[2 + i] + (w0 * ee + w1 * c);
+            }
+        } else if (kind == EMBER_DISTMULT) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float uk = U.v[i] + gd * T.v[i], wk = W.v[i] + gs * S.v[i];
+                oS.v[i] = gs * as.v[i] + uk * R.v[i];
+                oR.v[i] = uk * S.v[i] + wk * T.v[i];
+                oT.v[i] = gd * ad.v[i] + wk * R.v[i];
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                oS.v[i] = gs * T.v[i] + (U.v[i] + gd * T.v[i]);
+                oT.v[i] = gd * S.v[i] + (W.v[i] + gs * S.v[i]);
+            }
         }
-    } else if (kind == EMBER_DISTMULT) {
-        float* gR = grows + (uint64_t)rank[2 * nb + n_neg + e] * d;
-        for (uint32_t k = lane; k < d; k += 32) {
-            float ad, as;
-            adjust_at(kind, d, k, ss, sr, st, ad, as);
-            const float uk = u[k] + gd * st[k], wk = w[k] + gs * ss[k];
-            gS[k] = gs * as + uk * sr[k];
-            gR[k] = uk * ss[k] + wk * st[k];
-            gT[k] = gd * ad + wk * sr[k];
-        }
-    } else {
-        for (uint32_t k = lane; k < d; k += 32) {
-            gS[k] = gs * st[k] + (u[k] + gd * st[k]);
-            gT[k] = gd * ss[k] + (w[k] + gs * ss[k]);
-        }
+        store_quad(gS, kind, h, q, oS);
+        store_quad(gT, kind, h, q, oT);
+        if (gR) store_quad(gR, kind, h, q, oR);
     }
 }
 
@@ -308,12 +335,21 @@ __global__ void k_loss(const float* __restrict__ lse, const float* __restrict__ 
         last = atomicAdd(done, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (!last || threadIdx.x != 0) return;
+    if (!last) return;
     __threadfence();
-    double tot = 0.0;
-    for (uint32_t b = 0; b < gridDim.x; ++b) tot += ((volatile double*)part)[b];
-    out[0] = (float)(tot / (double)nb);
-    *done = 0u;
+    // the last block adds the block partials: loaded in parallel, reduced in a fixed tree order
+    double v = 0.0;
+    for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) v += ((volatile double*)part)[b];
+    red[threadIdx.x] = v;
+    __syncthreads();
+    for (uint32_t s = blockDim.x / 2; s; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out[0] = (float)(red[0] / (double)nb);
+        *done = 0u;
+    }
 }
 
 __device__ __forceinline__ float adagrad_elem(float& th, float& ac, float g, float lr, float eps) {
@@ -348,9 +384,11 @@ struct SegArgs {
 };
 
 // Segments longer than LONG_SEG rows (hot relations, hub nodes) are cut into LONG_CHUNK-row chunks
-// summed by separate warps, then the chunk partials are added in chunk order (deterministic).
-constexpr uint32_t LONG_SEG = 64;
-constexpr uint32_t LONG_CHUNK = 64;
+// summed by separate warps; a block per long segment then adds the chunk partials in a fixed
+// order (warp w takes chunks w, w+8, ...; the 8 warp sums are added in warp order): deterministic.
+constexpr uint32_t LONG_SEG = EMBER_LONG_SEG;
+constexpr uint32_t LONG_CHUNK = EMBER_LONG_CHUNK;
+constexpr uint32_t LONG_WARPS = 8;
 
 // Where unique key u's summed row goes: Adagrad target (th, ac) or export/dense destination.
 struct SegTarget {
@@ -442,13 +480,46 @@ __device__ __forceinline__ float4 sum_rows(const float* base, uint32_t cnt, uint
     return s;
 }
 
-// One warp per unique key: sum its contiguous rows (slot order) and apply Adagrad / export.
-__global__ void k_segments(SegArgs a) {
-    const uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+// Sum of rows [0, cnt) at column blocks c4a and c4b (c4b valid iff hasb), in row order, 4 loads
+// in flight.
+__device__ __forceinline__ void sum_rows2(const float* base, uint32_t cnt, uint32_t d, uint32_t c4a, uint32_t c4b,
+                                          bool hasb, float4& sa, float4& sb) {
+    sa = make_float4(0.f, 0.f, 0.f, 0.f);
+    sb = sa;
+    uint32_t r = 0;
+    for (; r + 2 <= cnt; r += 2) {
+        const float4 x0 = ldg4(base + (uint64_t)r * d + 4 * c4a);
+        const float4 x1 = ldg4(base + (uint64_t)(r + 1) * d + 4 * c4a);
+        float4 y0 = sb, y1 = sb;
+        if (hasb) {
+            y0 = ldg4(base + (uint64_t)r * d + 4 * c4b);
+            y1 = ldg4(base + (uint64_t)(r + 1) * d + 4 * c4b);
+        }
+        add4(sa, x0);
+        add4(sa, x1);
+        if (hasb) {
+            add4(sb, y0);
+            add4(sb, y1);
+        }
+    }
+    if (r < cnt) {
+        add4(sa, ldg4(base + (uint64_t)r * d + 4 * c4a));
+        if (hasb) add4(sb, ldg4(base + (uint64_t)r * d + 4 * c4b));
+    }
+}
+
+// Two unique keys per warp, one per 16-lane half (more independent rows in flight per warp): the
+// half sums its key's contiguous rows (slot order) and applies Adagrad / export. A lane owns
+// column blocks c4 and c4 + 16 (d <= 128; larger d loops).
+constexpr uint32_t SEG_LANES = 16;
+__global__ void __launch_bounds__(256, 4) k_segments(SegArgs a) {
+    const uint32_t lane = threadIdx.x & 31, hl = lane & (SEG_LANES - 1);
+    const uint32_t u = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 2 + (lane >> 4);
+    const uint32_t hmask = lane < SEG_LANES ? 0x0000ffffu : 0xffff0000u;
     const uint32_t nr = *a.nruns;
     if (u >= nr) return;
     const uint32_t key = a.ukeys[u];
-    if (lane == 0 && key < a.ks.node_range && (u + 1 == nr || a.ukeys[u + 1] >= a.ks.node_range)) {
+    if (hl == 0 && key < a.ks.node_range && (u + 1 == nr || a.ukeys[u + 1] >= a.ks.node_range)) {
         a.nunique[0] = u + 1;
         a.nunique[1] = nr - (u + 1);
     }
@@ -456,7 +527,7 @@ __global__ void k_segments(SegArgs a) {
     if (cnt > LONG_SEG) {  // reserve chunk slots for the long path
         const uint32_t nch = (cnt + LONG_CHUNK - 1) / LONG_CHUNK;
         uint32_t li = 0, base = 0;
-        if (lane == 0) {
+        if (hl == 0) {
             li = atomicAdd(&a.longs[0], 1u);
             base = atomicAdd(&a.longs[1], nch);
             uint32_t* rec = a.longs + 2 + 3 * li;
@@ -464,21 +535,31 @@ __global__ void k_segments(SegArgs a) {
             rec[1] = base;
             rec[2] = nch;
         }
-        li = __shfl_sync(0xffffffffu, li, 0);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        for (uint32_t c = lane; c < nch; c += 32) a.owner[base + c] = li;
+        li = __shfl_sync(hmask, li, 0, SEG_LANES);
+        base = __shfl_sync(hmask, base, 0, SEG_LANES);
+        for (uint32_t c = hl; c < nch; c += SEG_LANES) a.owner[base + c] = li;
         return;
     }
-    const SegTarget t = seg_target(a, u, nr, lane == 0);
+    const SegTarget t = seg_target(a, u, nr, hl == 0);
     const bool app = seg_applies(a, t);
     const float* base = a.rows + (uint64_t)off * a.d;
-    for (uint32_t c4 = lane; c4 < a.d / 4; c4 += 32) {
-        float4 th = make_float4(0.f, 0.f, 0.f, 0.f), ac = th;
-        if (app) {  // issue the parameter loads before the row sum
-            th = reinterpret_cast<const float4*>(t.th)[c4];
-            ac = reinterpret_cast<const float4*>(t.ac)[c4];
+    const uint32_t d4 = a.d / 4;
+    for (uint32_t c4 = hl; c4 < d4; c4 += 2 * SEG_LANES) {
+        const uint32_t c4b = c4 + SEG_LANES;
+        const bool hasb = c4b < d4;
+        float4 tha = make_float4(0.f, 0.f, 0.f, 0.f), aca = tha, thb = tha, acb = tha;
+        if (app) {  // issue the parameter loads before the row sums
+            tha = reinterpret_cast<const float4*>(t.th)[c4];
+            aca = reinterpret_cast<const float4*>(t.ac)[c4];
+            if (hasb) {
+                thb = reinterpret_cast<const float4*>(t.th)[c4b];
+                acb = reinterpret_cast<const float4*>(t.ac)[c4b];
+            }
         }
-        seg_finish(a, t, c4, sum_rows(base, cnt, a.d, c4), th, ac);
+        float4 ga, gb;
+        sum_rows2(base, cnt, a.d, c4, c4b, hasb, ga, gb);
+        seg_finish(a, t, c4, ga, tha, aca);
+        if (hasb) seg_finish(a, t, c4b, gb, thb, acb);
     }
 }
 
@@ -496,23 +577,43 @@ __global__ void k_long_partial(SegArgs a) {
     }
 }
 
-// One warp per long segment: chunk partials added in chunk order, then Adagrad / export.
-__global__ void k_long_final(SegArgs a) {
-    const uint32_t lane = threadIdx.x & 31, nw = (gridDim.x * blockDim.x) >> 5;
+// One block per long segment: chunk partials added in the fixed two-level order, then Adagrad.
+__global__ void __launch_bounds__(32 * LONG_WARPS) k_long_final(SegArgs a) {
+    extern __shared__ float4 wsum[];  // [LONG_WARPS][d/4]
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, d4 = a.d / 4;
     const uint32_t n_long = *(volatile uint32_t*)&a.longs[0], nr = *a.nruns;
-    for (uint32_t li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < n_long; li += nw) {
+    for (uint32_t li = blockIdx.x; li < n_long; li += gridDim.x) {
         const uint32_t* rec = a.longs + 2 + 3 * li;
         const uint32_t u = rec[0], base = rec[1], nch = rec[2];
-        const SegTarget t = seg_target(a, u, nr, lane == 0);
-        const bool app = seg_applies(a, t);
-        for (uint32_t c4 = lane; c4 < a.d / 4; c4 += 32) {
-            float4 th = make_float4(0.f, 0.f, 0.f, 0.f), ac = th;
-            if (app) {
-                th = reinterpret_cast<const float4*>(t.th)[c4];
-                ac = reinterpret_cast<const float4*>(t.ac)[c4];
+        for (uint32_t c4 = lane; c4 < d4; c4 += 32) {
+            float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f), s5 = s4;
+            uint32_t c = w;
+            for (; c + LONG_WARPS < nch; c += 2 * LONG_WARPS) {  // two loads in flight
+                const float4 x = ldg4(a.partial + (uint64_t)(base + c) * a.d + 4 * c4);
+                const float4 y = ldg4(a.partial + (uint64_t)(base + c + LONG_WARPS) * a.d + 4 * c4);
+                add4(s4, x);
+                add4(s5, y);
             }
-            seg_finish(a, t, c4, sum_rows(a.partial + (uint64_t)base * a.d, nch, a.d, c4), th, ac);
+            if (c < nch) add4(s4, ldg4(a.partial + (uint64_t)(base + c) * a.d + 4 * c4));
+            add4(s4, s5);
+            wsum[w * d4 + c4] = s4;
         }
+        __syncthreads();
+        if (w == 0) {
+            const SegTarget t = seg_target(a, u, nr, lane == 0);
+            const bool app = seg_applies(a, t);
+            for (uint32_t c4 = lane; c4 < d4; c4 += 32) {
+                float4 th = make_float4(0.f, 0.f, 0.f, 0.f), ac = th;
+                if (app) {
+                    th = reinterpret_cast<const float4*>(t.th)[c4];
+                    ac = reinterpret_cast<const float4*>(t.ac)[c4];
+                }
+                float4 g = wsum[c4];
+                for (uint32_t k = 1; k < LONG_WARPS; ++k) add4(g, wsum[k * d4 + c4]);
+                seg_finish(a, t, c4, g, th, ac);
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -578,14 +679,13 @@ void launch_sample(const Engine& E, uint32_t* out, uint64_t base, const uint32_t
 void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj,
                           bool packed) {
     const uint32_t warps = 8;
-    const size_t sm = (size_t)warps * 3 * E.dim * sizeof(float);
     if (packed) {
         const uint32_t rows_pad = (uint32_t)Engine::pad_rows(nb);
-        const size_t smp = sm + (size_t)warps * 2 * E.KP * sizeof(float);
+        const size_t smp = (size_t)warps * 2 * E.KP * sizeof(float);
         k_gather_adjust<true><<<(rows_pad + warps - 1) / warps, warps * 32, smp, E.stream>>>(
             edges, nb, rows_pad, pi, pj, E.rel_theta, E.m.kind, E.dim, E.CB, E.b_cap, nullptr, E.s.Apk, E.s.fpos);
     } else {
-        k_gather_adjust<false><<<(nb + warps - 1) / warps, warps * 32, sm, E.stream>>>(
+        k_gather_adjust<false><<<(nb + warps - 1) / warps, warps * 32, 0, E.stream>>>(
             edges, nb, nb, pi, pj, E.rel_theta, E.m.kind, E.dim, 0, 0, E.s.A, nullptr, E.s.fpos);
     }
     EMBER_LAUNCHED(E);
@@ -617,15 +717,14 @@ void launch_rank(const Engine& E, uint32_t n) {
 
 void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj) {
     const uint32_t warps = 8;
-    const size_t sm = (size_t)warps * 5 * E.dim * sizeof(float);
-    k_chain_rule<<<(nb + warps - 1) / warps, warps * 32, sm, E.stream>>>(
+    k_chain_rule<<<(nb + warps - 1) / warps, warps * 32, 0, E.stream>>>(
         edges, nb, E.n_neg, pi, pj, E.rel_theta, E.m.kind, E.dim, E.s.dA, E.tc_engine() ? (uint32_t)E.b_cap : 0u,
         E.s.g0, E.s.rank, E.s.grows);
     EMBER_LAUNCHED(E);
 }
 
 void launch_loss(const Engine& E, uint32_t nb, float* loss_out) {
-    const uint32_t per = 4096;
+    const uint32_t per = LOSS_THREADS;  // ~100 blocks at b = 5e4: latency, not bandwidth
     const uint32_t blocks = (nb + per - 1) / per;
     k_loss<<<blocks, LOSS_THREADS, 0, E.stream>>>(E.s.lse, E.s.fpos, nb, per, reinterpret_cast<double*>(E.s.loss_part),
                                                  E.s.loss_done, loss_out);
@@ -657,11 +756,11 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
     a.node_rows_out = node_rows_out;
     a.rel_ids_out = rel_ids_out;
     a.rel_rows_out = rel_rows_out;
-    k_segments<<<(n_slots * 32 + 255) / 256, 256, 0, E.stream>>>(a);
+    k_segments<<<(n_slots * 16 + 255) / 256, 256, 0, E.stream>>>(a);  // 2 keys per warp
     EMBER_LAUNCHED(E);
     k_long_partial<<<2 * E.sm_count, 256, 0, E.stream>>>(a);
     EMBER_LAUNCHED(E);
-    k_long_final<<<E.sm_count, 256, 0, E.stream>>>(a);
+    k_long_final<<<E.sm_count, 32 * LONG_WARPS, LONG_WARPS * E.dim * sizeof(float), E.stream>>>(a);
     EMBER_LAUNCHED(E);
 }
 

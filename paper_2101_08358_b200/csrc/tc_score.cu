@@ -590,19 +590,32 @@ __global__ void k_tc_fixup(TcArgs g, const uint16_t* __restrict__ Apk, const uin
 // =========================================================================================
 
 // dN rows summed over chunks in fixed order; row (side, n) is gradient slot 2nb + side*nt + n and
-// goes to its sorted position grows[rank[slot]].
-__global__ void k_dn_reduce(const float* __restrict__ part, int chunks, int nt, int n_pad, int d,
+// goes to its sorted position grows[rank[slot]]. Thread per (side, column block, negative): the
+// column-blocked partials [chunk][side][d/4][n_pad] float4 are read coalesced along n.
+__global__ void k_dn_reduce(const float4* __restrict__ part, int chunks, int nt, int n_pad, int d,
                             const uint32_t* __restrict__ rank, uint32_t slot0, float* __restrict__ out) {
+    const int d4 = d / 4;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t per_side = (int64_t)nt * d;
-    if (t >= 2 * per_side) return;
-    const int side = (int)(t / per_side);
-    const int rem = (int)(t % per_side);
-    const int n = rem / d, k = rem % d;
-    float acc = 0.f;
-    for (int c = 0; c < chunks; ++c)  // column-blocked partials [chunk][side][k/4][n][k%4]
-        acc += part[((((size_t)c * 2 + side) * (d / 4) + k / 4) * n_pad + n) * 4 + k % 4];
-    out[(size_t)rank[slot0 + side * nt + n] * d + k] = acc;
+    if (t >= (int64_t)2 * d4 * nt) return;
+    const int n = (int)(t % nt);
+    const int c4 = (int)((t / nt) % d4);
+    const int side = (int)(t / ((int64_t)nt * d4));
+    const float4* p = part + ((size_t)side * d4 + c4) * n_pad + n;
+    const size_t cstride = (size_t)2 * d4 * n_pad;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int c = 0;
+    for (; c + 4 <= chunks; c += 4) {  // 4 loads in flight, added in chunk order
+        float4 x[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) x[i] = __ldg(p + (size_t)(c + i) * cstride);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc.x += x[i].x, acc.y += x[i].y, acc.z += x[i].z, acc.w += x[i].w;
+    }
+    for (; c < chunks; ++c) {
+        const float4 x = __ldg(p + (size_t)c * cstride);
+        acc.x += x.x, acc.y += x.y, acc.z += x.z, acc.w += x.w;
+    }
+    reinterpret_cast<float4*>(out + (size_t)rank[slot0 + side * nt + n] * d)[c4] = acc;
 }
 
 // ---- tensor maps (driver entry point fetched through the runtime: no libcuda link) ---------
@@ -766,10 +779,11 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
         t.mN128, t.mA96, a);
     EMBER_LAUNCHED(E);
     if (tr) dump(".negs.bin");
-    const int64_t r = (int64_t)2 * nt * d;
+    const int64_t r = (int64_t)2 * nt * (d / 4);
     E.join_sorted();
-    k_dn_reduce<<<(unsigned)((r + 255) / 256), 256, 0, E.stream>>>(t.dN_part, a.chunks2, nt, t.n_pad, d, s.rank,
-                                                                    2 * nb, s.grows);
+    k_dn_reduce<<<(unsigned)((r + 255) / 256), 256, 0, E.stream>>>(reinterpret_cast<const float4*>(t.dN_part),
+                                                                    a.chunks2, nt, t.n_pad, d, s.rank, 2 * nb,
+                                                                    s.grows);
     EMBER_LAUNCHED(E);
 }
 
