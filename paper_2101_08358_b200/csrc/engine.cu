@@ -74,6 +74,12 @@ __global__ void k_adagrad_dense(float* th, float* ac, const float* g, uint64_t n
     th[i] = __fsub_rn(th[i], __fdiv_rn(__fmul_rn(lr, gi), __fadd_rn(__fsqrt_rn(a), eps)));
 }
 
+// A/B switch: EMBER_NO_DIRECT=1 sends every gradient row through the segmented reduction.
+bool getenv_direct() {
+    const char* v = getenv("EMBER_NO_DIRECT");
+    return !(v && v[0] == '1');
+}
+
 }  // namespace
 
 Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, cudaStream_t st)
@@ -319,10 +325,12 @@ void Engine::step(const uint32_t* edges, uint32_t nb, const uint32_t* bucket, ui
     check_bucket(i, j);
     mark(PHASE_SAMPLE);
     sample(bucket, bucket_n, i, j, epoch, bucket_step, batch_in_bucket, s.negs);
+    direct_hi = getenv_direct() ? 2 * nb : 0;
     forward_backward(edges, nb, i, j, s.negs);
     launch_loss(*this, nb, loss_out ? loss_out : s.loss);
     mark(PHASE_REDUCE);
     reduce_and_apply(nb, i, j, true, nullptr, nullptr, nullptr, nullptr);
+    direct_hi = 0;
     mark(PHASE_END);
 }
 

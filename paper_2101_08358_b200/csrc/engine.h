@@ -20,7 +20,7 @@ namespace ember {
 
 // Segmented reduction: keys with more than EMBER_LONG_SEG gradient rows take the chunked path
 // (EMBER_LONG_CHUNK-row chunk partials, kernels_step.cu).
-#define EMBER_LONG_SEG 64
+#define EMBER_LONG_SEG 16
 #define EMBER_LONG_CHUNK 32
 
 #define EMBER_CUDA(call)                                                                        \
@@ -134,6 +134,10 @@ struct Engine {
     void* nccl_comm = nullptr;
     int rank = 0, world = 1;
     float* rel_ext = nullptr;  // caller-owned [R][dim] relation-gradient buffer (external reduction)
+    // Training steps apply Adagrad to source/destination rows whose key occurs once in the batch
+    // right in the chain rule (slots < direct_hi = 2nb); 0: every row goes through the segmented
+    // reduction.
+    uint32_t direct_hi = 0;
     // profiling: CUDA events at phase boundaries on the step stream + our own kernel launches
     bool prof_on = false;
     std::vector<std::pair<int, cudaEvent_t>> prof_events;

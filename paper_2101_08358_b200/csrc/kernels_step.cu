@@ -229,6 +229,27 @@ __global__ void k_rank(const uint32_t* __restrict__ vals_sorted, uint32_t n, uin
     if (p < n) rank[vals_sorted[p]] = p;
 }
 
+// The sorted position p holds a key that occurs exactly once among the batch's gradient slots.
+__device__ __forceinline__ bool slot_unique(const uint32_t* __restrict__ ks, uint32_t n, uint32_t p) {
+    const uint32_t k = ks[p];
+    return (p == 0 || ks[p - 1] != k) && (p + 1 == n || ks[p + 1] != k);
+}
+
+__device__ __forceinline__ void adagrad_one(float& th, float& ac, float g, float lr, float eps) {
+    const float a = __fadd_rn(ac, __fmul_rn(g, g));
+    ac = a;
+    th = __fsub_rn(th, __fdiv_rn(__fmul_rn(lr, g), __fadd_rn(__fsqrt_rn(a), eps)));
+}
+
+// Adagrad of one quad of a row whose parameters Th were already loaded.
+__device__ __forceinline__ void adagrad_quad(float* th_row, float* ac_row, int kind, uint32_t h, uint32_t q,
+                                             Quad Th, Quad Ac, const Quad& G, float lr, float eps) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) adagrad_one(Th.v[i], Ac.v[i], G.v[i], lr, eps);
+    store_quad(th_row, kind, h, q, Th);
+    store_quad(ac_row, kind, h, q, Ac);
+}
+
 // dA quad q of (side, edge e): column-blocked [2][d/4][dcap][4] (tensor-core engine) or
 // row-major [2][nb][d] (SIMT engine, dcap == 0).
 __device__ __forceinline__ Quad load_dA_quad(const float* __restrict__ dA, uint32_t dcap, uint32_t nb, uint32_t side,
@@ -258,7 +279,9 @@ __device__ __forceinline__ Quad load_dA_quad(const float* __restrict__ dA, uint3
 __global__ void __launch_bounds__(256, 4) k_chain_rule(const uint32_t* __restrict__ edges, uint32_t nb, uint32_t n_neg, PartView pi,
                              PartView pj, const float* __restrict__ rel, int kind, uint32_t d,
                              const float* __restrict__ dA, uint32_t dcap, const float* __restrict__ g0,
-                             const uint32_t* __restrict__ rank, float* __restrict__ grows) {
+                             const uint32_t* __restrict__ rank, float* __restrict__ grows,
+                             const uint32_t* __restrict__ keys_sorted, uint32_t n_slots, int direct, float lr,
+                             float eps) {
     const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t e = blockIdx.x * (blockDim.x >> 5) + wib;
     if (e >= nb) return;
@@ -267,15 +290,27 @@ __global__ void __launch_bounds__(256, 4) k_chain_rule(const uint32_t* __restric
     const float* st = node_row(pj, t, d);
     const float* sr = kind != EMBER_DOT ? rel + (uint64_t)r * d : nullptr;
     const float gd = g0[e], gs = g0[(uint64_t)nb + e];
-    float* gS = grows + (uint64_t)rank[e] * d;
-    float* gT = grows + (uint64_t)rank[nb + e] * d;
+    const uint32_t ps = rank[e], pt = rank[nb + e];
+    // A node row whose key occurs once in the batch (the common case) is final here: Adagrad is
+    // applied in place (the row was just read), skipping the sorted-row round trip.
+    const bool us = direct && slot_unique(keys_sorted, n_slots, ps);
+    const bool ut = direct && slot_unique(keys_sorted, n_slots, pt);
+    float* gS = grows + (uint64_t)ps * d;
+    float* gT = grows + (uint64_t)pt * d;
     float* gR = kind != EMBER_DOT ? grows + (uint64_t)rank[2 * nb + n_neg + e] * d : nullptr;
+    float* aS = pi.acc + (uint64_t)(s - pi.first) * d;
+    float* aT = pj.acc + (uint64_t)(t - pj.first) * d;
     const uint32_t h = d / 2, nq = d / 4;
     for (uint32_t q = lane; q < nq; q += 32) {
         const Quad S = load_quad(ss, kind, h, q), T = load_quad(st, kind, h, q);
         const Quad R = sr ? load_quad(sr, kind, h, q) : S;
         const Quad U = load_dA_quad(dA, dcap, nb, 0, e, kind, d, q);  // destination side
         const Quad W = load_dA_quad(dA, dcap, nb, 1, e, kind, d, q);  // source side
+        Quad AS, AT;  // accumulators, loaded with the rows (speculatively: used when the key is unique)
+        if (direct) {
+            AS = load_quad(aS, kind, h, q);
+            AT = load_quad(aT, kind, h, q);
+        }
         Quad ad, as, oS, oR, oT;
         adjust_quad(kind, S, R, T, ad, as);
         if (kind == EMBER_COMPLEX) {
@@ -306,8 +341,10 @@ __global__ void __launch_bounds__(256, 4) k_chain_rule(const uint32_t* __restric
                 oT.v[i] = gd * S.v[i] + (W.v[i] + gs * S.v[i]);
             }
         }
-        store_quad(gS, kind, h, q, oS);
-        store_quad(gT, kind, h, q, oT);
+        if (us) adagrad_quad(const_cast<float*>(ss), aS, kind, h, q, S, AS, oS, lr, eps);
+        else store_quad(gS, kind, h, q, oS);
+        if (ut) adagrad_quad(const_cast<float*>(st), aT, kind, h, q, T, AT, oT, lr, eps);
+        else store_quad(gT, kind, h, q, oT);
         if (gR) store_quad(gR, kind, h, q, oR);
     }
 }
@@ -353,9 +390,7 @@ __global__ void k_loss(const float* __restrict__ lse, const float* __restrict__ 
 }
 
 __device__ __forceinline__ float adagrad_elem(float& th, float& ac, float g, float lr, float eps) {
-    const float a = __fadd_rn(ac, __fmul_rn(g, g));
-    ac = a;
-    th = __fsub_rn(th, __fdiv_rn(__fmul_rn(lr, g), __fadd_rn(__fsqrt_rn(a), eps)));
+    adagrad_one(th, ac, g, lr, eps);
     return th;
 }
 
@@ -374,6 +409,8 @@ struct SegArgs {
     float* rel_theta;
     float* rel_acc;
     float* rel_dense;    // non-null: relation sums go here (summed over ranks later), no Adagrad
+    const uint32_t* vals_sorted;  // sorted position -> gradient slot
+    uint32_t direct_hi;  // node keys occurring once with slot < direct_hi were applied by their producer
     uint32_t d;
     float lr, eps;
     int apply;
@@ -385,10 +422,11 @@ struct SegArgs {
 
 // Segments longer than LONG_SEG rows (hot relations, hub nodes) are cut into LONG_CHUNK-row chunks
 // summed by separate warps; a block per long segment then adds the chunk partials in a fixed
-// order (warp w takes chunks w, w+8, ...; the 8 warp sums are added in warp order): deterministic.
+// order (stream s of 2 LONG_WARPS takes chunks s, s + 2 LONG_WARPS, ...; the stream sums are then added
+// in stream order): deterministic.
 constexpr uint32_t LONG_SEG = EMBER_LONG_SEG;
 constexpr uint32_t LONG_CHUNK = EMBER_LONG_CHUNK;
-constexpr uint32_t LONG_WARPS = 8;
+constexpr uint32_t LONG_WARPS = 16;
 
 // Where unique key u's summed row goes: Adagrad target (th, ac) or export/dense destination.
 struct SegTarget {
@@ -524,6 +562,7 @@ __global__ void __launch_bounds__(256, 4) k_segments(SegArgs a) {
         a.nunique[1] = nr - (u + 1);
     }
     const uint32_t off = a.offsets[u], cnt = a.counts[u];
+    if (cnt == 1 && key < a.ks.node_range && a.vals_sorted[off] < a.direct_hi) return;  // applied already
     if (cnt > LONG_SEG) {  // reserve chunk slots for the long path
         const uint32_t nch = (cnt + LONG_CHUNK - 1) / LONG_CHUNK;
         uint32_t li = 0, base = 0;
@@ -563,43 +602,71 @@ __global__ void __launch_bounds__(256, 4) k_segments(SegArgs a) {
     }
 }
 
-// One warp per chunk slot of the long segments: partial[slot] = sum of its <= LONG_CHUNK rows.
+// Sum of rows r = r0, r0 + step, ... < cnt at column block c4, 4 loads in flight, in row order.
+__device__ __forceinline__ float4 sum_rows_strided(const float* base, uint32_t r0, uint32_t step, uint32_t cnt,
+                                                   uint32_t d, uint32_t c4) {
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t r = r0;
+    for (; r + 3 * step < cnt; r += 4 * step) {
+        const float4 x0 = ldg4(base + (uint64_t)r * d + 4 * c4);
+        const float4 x1 = ldg4(base + (uint64_t)(r + step) * d + 4 * c4);
+        const float4 x2 = ldg4(base + (uint64_t)(r + 2 * step) * d + 4 * c4);
+        const float4 x3 = ldg4(base + (uint64_t)(r + 3 * step) * d + 4 * c4);
+        add4(s, x0);
+        add4(s, x1);
+        add4(s, x2);
+        add4(s, x3);
+    }
+    for (; r < cnt; r += step) add4(s, ldg4(base + (uint64_t)r * d + 4 * c4));
+    return s;
+}
+
+__device__ __forceinline__ float4 shfl_xor4(float4 v, int m) {
+    v.x = __shfl_xor_sync(0xffffffffu, v.x, m);
+    v.y = __shfl_xor_sync(0xffffffffu, v.y, m);
+    v.z = __shfl_xor_sync(0xffffffffu, v.z, m);
+    v.w = __shfl_xor_sync(0xffffffffu, v.w, m);
+    return v;
+}
+
+// One warp per chunk slot of the long segments: partial[slot] = sum of its <= LONG_CHUNK rows;
+// the two half-warps take the even and the odd rows, then even + odd (fixed order).
 __global__ void k_long_partial(SegArgs a) {
-    const uint32_t lane = threadIdx.x & 31, nw = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31, hl = lane & 15, half = lane >> 4;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5, d4 = a.d / 4;
     const uint32_t n_slots = *(volatile uint32_t*)&a.longs[1];
     for (uint32_t sl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < n_slots; sl += nw) {
         const uint32_t* rec = a.longs + 2 + 3 * a.owner[sl];
         const uint32_t u = rec[0], c = sl - rec[1];
         const uint32_t r0 = c * LONG_CHUNK, cnt = min(LONG_CHUNK, a.counts[u] - r0);
         const float* base = a.rows + ((uint64_t)a.offsets[u] + r0) * a.d;
-        for (uint32_t c4 = lane; c4 < a.d / 4; c4 += 32)
-            reinterpret_cast<float4*>(a.partial + (uint64_t)sl * a.d)[c4] = sum_rows(base, cnt, a.d, c4);
+        for (uint32_t c0 = 0; c0 < d4; c0 += 16) {  // warp-uniform trip count (shuffles below)
+            const uint32_t c4 = c0 + hl;
+            float4 v = c4 < d4 ? sum_rows_strided(base, half, 2, cnt, a.d, c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 o = shfl_xor4(v, 16);
+            if (half == 0 && c4 < d4) {
+                add4(v, o);  // even rows + odd rows
+                reinterpret_cast<float4*>(a.partial + (uint64_t)sl * a.d)[c4] = v;
+            }
+        }
     }
 }
 
-// One block per long segment: chunk partials added in the fixed two-level order, then Adagrad.
+// One block per long segment: 2 * LONG_WARPS half-warp streams each add the chunk partials
+// c = stream, stream + 2 LONG_WARPS, ... (in order); warp 0 then adds the stream sums in stream
+// order (a fixed two-level order: deterministic) and applies Adagrad / export.
 __global__ void __launch_bounds__(32 * LONG_WARPS) k_long_final(SegArgs a) {
-    extern __shared__ float4 wsum[];  // [LONG_WARPS][d/4]
-    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, d4 = a.d / 4;
+    extern __shared__ float4 wsum[];  // [2 * LONG_WARPS][d/4]
+    const uint32_t lane = threadIdx.x & 31, hl = lane & 15, stream = threadIdx.x >> 4, d4 = a.d / 4;
+    const uint32_t NS = 2 * LONG_WARPS;
     const uint32_t n_long = *(volatile uint32_t*)&a.longs[0], nr = *a.nruns;
     for (uint32_t li = blockIdx.x; li < n_long; li += gridDim.x) {
         const uint32_t* rec = a.longs + 2 + 3 * li;
         const uint32_t u = rec[0], base = rec[1], nch = rec[2];
-        for (uint32_t c4 = lane; c4 < d4; c4 += 32) {
-            float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f), s5 = s4;
-            uint32_t c = w;
-            for (; c + LONG_WARPS < nch; c += 2 * LONG_WARPS) {  // two loads in flight
-                const float4 x = ldg4(a.partial + (uint64_t)(base + c) * a.d + 4 * c4);
-                const float4 y = ldg4(a.partial + (uint64_t)(base + c + LONG_WARPS) * a.d + 4 * c4);
-                add4(s4, x);
-                add4(s5, y);
-            }
-            if (c < nch) add4(s4, ldg4(a.partial + (uint64_t)(base + c) * a.d + 4 * c4));
-            add4(s4, s5);
-            wsum[w * d4 + c4] = s4;
-        }
+        for (uint32_t c4 = hl; c4 < d4; c4 += 16)
+            wsum[stream * d4 + c4] = sum_rows_strided(a.partial + (uint64_t)base * a.d, stream, NS, nch, a.d, c4);
         __syncthreads();
-        if (w == 0) {
+        if (threadIdx.x < 32) {
             const SegTarget t = seg_target(a, u, nr, lane == 0);
             const bool app = seg_applies(a, t);
             for (uint32_t c4 = lane; c4 < d4; c4 += 32) {
@@ -609,7 +676,7 @@ __global__ void __launch_bounds__(32 * LONG_WARPS) k_long_final(SegArgs a) {
                     ac = reinterpret_cast<const float4*>(t.ac)[c4];
                 }
                 float4 g = wsum[c4];
-                for (uint32_t k = 1; k < LONG_WARPS; ++k) add4(g, wsum[k * d4 + c4]);
+                for (uint32_t k = 1; k < NS; ++k) add4(g, wsum[k * d4 + c4]);
                 seg_finish(a, t, c4, g, th, ac);
             }
         }
@@ -719,7 +786,7 @@ void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, cons
     const uint32_t warps = 8;
     k_chain_rule<<<(nb + warps - 1) / warps, warps * 32, 0, E.stream>>>(
         edges, nb, E.n_neg, pi, pj, E.rel_theta, E.m.kind, E.dim, E.s.dA, E.tc_engine() ? (uint32_t)E.b_cap : 0u,
-        E.s.g0, E.s.rank, E.s.grows);
+        E.s.g0, E.s.rank, E.s.grows, E.s.keys_sorted, E.slots(nb), E.direct_hi ? 1 : 0, E.m.lr, E.m.eps);
     EMBER_LAUNCHED(E);
 }
 
@@ -748,6 +815,8 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
     a.rel_theta = E.rel_theta;
     a.rel_acc = E.rel_acc;
     a.rel_dense = rel_dense ? (E.rel_ext ? E.rel_ext : E.s.rel_dense) : nullptr;
+    a.vals_sorted = E.s.vals_sorted;
+    a.direct_hi = apply ? E.direct_hi : 0u;
     a.d = E.dim;
     a.lr = E.m.lr;
     a.eps = E.m.eps;
@@ -760,7 +829,7 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
     EMBER_LAUNCHED(E);
     k_long_partial<<<2 * E.sm_count, 256, 0, E.stream>>>(a);
     EMBER_LAUNCHED(E);
-    k_long_final<<<E.sm_count, 32 * LONG_WARPS, LONG_WARPS * E.dim * sizeof(float), E.stream>>>(a);
+    k_long_final<<<E.sm_count, 32 * LONG_WARPS, 2 * LONG_WARPS * E.dim * sizeof(float), E.stream>>>(a);
     EMBER_LAUNCHED(E);
 }
 

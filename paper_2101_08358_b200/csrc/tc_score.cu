@@ -615,7 +615,8 @@ __global__ void k_dn_reduce(const float4* __restrict__ part, int chunks, int nt,
         const float4 x = __ldg(p + (size_t)c * cstride);
         acc.x += x.x, acc.y += x.y, acc.z += x.z, acc.w += x.w;
     }
-    reinterpret_cast<float4*>(out + (size_t)rank[slot0 + side * nt + n] * d)[c4] = acc;
+    const uint32_t pos = rank[slot0 + side * nt + n];
+    reinterpret_cast<float4*>(out + (size_t)pos * d)[c4] = acc;
 }
 
 // ---- tensor maps (driver entry point fetched through the runtime: no libcuda link) ---------
@@ -781,9 +782,8 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
     if (tr) dump(".negs.bin");
     const int64_t r = (int64_t)2 * nt * (d / 4);
     E.join_sorted();
-    k_dn_reduce<<<(unsigned)((r + 255) / 256), 256, 0, E.stream>>>(reinterpret_cast<const float4*>(t.dN_part),
-                                                                    a.chunks2, nt, t.n_pad, d, s.rank, 2 * nb,
-                                                                    s.grows);
+    k_dn_reduce<<<(unsigned)((r + 255) / 256), 256, 0, E.stream>>>(
+        reinterpret_cast<const float4*>(t.dN_part), a.chunks2, nt, t.n_pad, d, s.rank, 2 * nb, s.grows);
     EMBER_LAUNCHED(E);
 }
 

@@ -189,3 +189,23 @@ def test_tc_engine_headline_shapes(graph, monkeypatch, kind, dim, nt, nb, zmax, 
     assert row_rel_err(got["node_rows"], exp["node_rows"]) <= TOL
     if kind != "dot":
         assert row_rel_err(got["rel_rows"], exp["rel_rows"]) <= TOL
+
+
+@pytest.mark.parametrize("kind,engine", [("complex", "tc"), ("distmult", "tc"), ("dot", "simt")])
+def test_direct_unique_row_updates_bit_identical(graph, monkeypatch, kind, engine):
+    """Node rows whose key occurs once in a batch are updated by their producer (chain rule / dN
+    reduce) instead of the segmented reduction: parameters are bit-identical either way."""
+    edges, off, _ = graph
+    tabs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("EMBER_NO_DIRECT", flag)
+        tr = make_trainer(kind, dim=32, b=256, nt=64, p=2, engine=engine)
+        for step, (i, j) in enumerate([(0, 1), (1, 1), (1, 0)]):
+            b = i * 2 + j
+            bucket = _dev(edges[off[b]:off[b + 1]])
+            for k in range(3):
+                tr.train_batch(bucket, k * 256, 256, i, j, epoch=0, bucket_step=step, batch_in_bucket=k)
+        tabs.append(host_tables(tr))
+        tr.close()
+    for a, b_ in zip(tabs[0], tabs[1]):
+        assert a.tobytes() == b_.tobytes()
