@@ -54,6 +54,18 @@ def peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "_fallback": True}
 
 
+def executed_tc_flops(cfg, nb):
+    """Tensor-pipe FLOPs the bf16x3 engine executes per step (csrc/tc_score.cu): every 96-wide
+    streamed tile of either kernel runs S (128 x 96 x KP) and P.T (128 x KP x 96), 3 MMAs each
+    (hi.hi + hi.lo + lo.hi); rows kernel: 2 sides x ceil(nb/128) items x ceil(nt/96) tiles; negs
+    kernel (recomputes S): 2 sides x ceil(nt/128) x ceil(nb/96) tiles; KP = d rounded up to 16."""
+    d, nt = cfg["dim"], cfg["nt"]
+    kp = (d + 15) // 16 * 16
+    c = lambda a, b: -(-a // b)  # noqa: E731
+    tiles = 2 * c(nb, 128) * c(nt, 96) + 2 * c(nt, 128) * c(nb, 96)
+    return tiles * 2 * (2 * 128 * 96 * kp) * 3
+
+
 def algorithmic(cfg):
     """Per-edge algorithmic work (SURVEY §8(d)): FLOPs = 3 contractions x 2 sides x 2*n_t*d;
     HBM bytes = 12 + 32d + 32d*n_t/b (nominal: unique rows touched read+write theta and acc)."""
@@ -401,6 +413,8 @@ def bench_ours(args, rank, world, local_rank):
     contract_ms = prof["ms"]["contraction"] / max(1, args.steps)
     step_edges = edges / max(1, args.steps) / world
     achieved = flops_e * step_edges / (contract_ms / 1e3) / 1e12 if contract_ms > 0 else None
+    exe = (executed_tc_flops(cfg, cfg["b"]) / (contract_ms / 1e3) / 1e12
+           if contract_ms > 0 and args.engine == "tc" else None)
     peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
     traffic = None
     prof_file = os.path.join(ROOT, "profiles", f"ncu_summary_{args.engine}.json")
@@ -439,7 +453,13 @@ def bench_ours(args, rank, world, local_rank):
                      "achieved": round(achieved, 2) if achieved else None, "peak": peak, "unit": "TFLOP/s",
                      "frac": round(achieved / peak, 4) if achieved else None, "traffic": traffic,
                      "flops_per_edge": flops_e, "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"
-                     + (" (fallback)" if pk.get("_fallback") else "")},
+                     + (" (fallback)" if pk.get("_fallback") else ""),
+                     # the fp32-accurate bf16x3 scheme executes ~4.7x the algorithmic FLOPs (3 MMAs per
+                     # product, S recomputed by the dN kernel, K and N padding): tensor-pipe utilisation
+                     "executed_tflops": round(exe, 2) if exe else None,
+                     "executed_frac": round(exe / peak, 4) if exe else None,
+                     "executed_per_algorithmic": round(executed_tc_flops(cfg, cfg["b"]) / (flops_e * cfg["b"]), 3)
+                     if args.engine == "tc" else None},
         "hbm_roofline_edges_per_s": round(pk["hbm_gbs"] * 1e9 / bytes_e, 1),
         "clocks": clk,
     }

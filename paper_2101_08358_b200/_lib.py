@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libember_b200.so")
+# EMBER_LIB: load another build of the same library (A/B timing of two builds in one process tree)
+LIB_PATH = os.environ.get("EMBER_LIB") or os.path.join(HERE, "libember_b200.so")
 
 EMBER_OK, EMBER_EUSER, EMBER_EINTERNAL = 0, 1, 2
 KIND = {"dot": 0, "distmult": 1, "complex": 2}

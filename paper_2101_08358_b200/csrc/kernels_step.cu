@@ -103,55 +103,53 @@ __device__ __forceinline__ void adjust_quad(int kind, const Quad& S, const Quad&
     }
 }
 
-// One warp per edge (rows up to rows_pad: the packed layout is zero-padded to whole tiles).
-// Lanes load their quads of the source, relation and destination rows into registers and form
-// the adjusted quads. PACKED: the adjusted rows are staged in shared memory (2 x KP floats per
-// warp), then lane l < 2CB packs 8 consecutive coordinates into their bf16 hi|lo 16-byte
-// core-matrix rows; else fp32 rows A[0][e] = ad, A[1][e] = as. fpos[e] = ad . t.
-template <bool PACKED>
-__global__ void k_gather_adjust(const uint32_t* __restrict__ edges, uint32_t nb, uint32_t rows_pad, PartView pi,
-                                PartView pj, const float* __restrict__ rel, int kind, uint32_t d, uint32_t CB,
-                                uint32_t cap, float* __restrict__ A, uint16_t* __restrict__ Apk,
-                                float* __restrict__ fpos) {
-    extern __shared__ float sm[];
+// Edges per CTA of the packed gather: one 512-byte run per column block (the TMA box row group).
+constexpr uint32_t GP_ROWS = 32, GP_WARPS = 8;
+
+// Packed gather (tensor-core engine): a CTA builds the operand rows of GP_ROWS consecutive edges
+// (rows up to rows_pad: the packed layout is zero-padded to whole tiles). Each warp takes
+// GP_ROWS / GP_WARPS edges: lanes load their quads of the source, relation and destination rows
+// into registers, form the adjusted quads and stage them (2 x KP floats per warp); lanes < 2CB
+// split 8 consecutive coordinates into bf16 hi|lo 16-byte core-matrix rows of a shared tile
+// [2 sides][2CB blocks][GP_ROWS][16 B], which leaves in 512-byte coalesced runs, one per column
+// block (per-lane 16-byte stores would scatter over 56 blocks). fpos[e] = ad . t.
+// (Staging the rows with one TMA bulk copy per 400-byte row measured slower than register loads.)
+__global__ void __launch_bounds__(32 * GP_WARPS) k_gather_pack(const uint32_t* __restrict__ edges, uint32_t nb,
+                                                               PartView pi, PartView pj, const float* __restrict__ rel,
+                                                               int kind, uint32_t d, uint32_t CB, uint32_t cap,
+                                                               uint16_t* __restrict__ Apk, float* __restrict__ fpos) {
+    extern __shared__ uint4 gsm[];
+    uint4* tile = gsm;  // [2][2CB][GP_ROWS]
+    const uint32_t kp = 8 * CB, nblk = 4 * CB;
+    float* stage = reinterpret_cast<float*>(tile + (size_t)nblk * GP_ROWS);
     const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t e = blockIdx.x * (blockDim.x >> 5) + wib;
-    if (e >= (PACKED ? rows_pad : nb)) return;
-    uint4* P = reinterpret_cast<uint4*>(Apk);
-    const uint32_t kp = 8 * CB;  // padded dim (packed)
-    if (PACKED && e >= nb) {     // zero padding rows of the last tiles
-        const uint4 z = make_uint4(0, 0, 0, 0);
-        for (uint32_t c = lane; c < 4 * CB; c += 32) {
-            const uint32_t side = c / (2 * CB), cb = c % (2 * CB);
-            P[((uint64_t)side * 2 * CB + cb) * cap + e] = z;
-        }
-        return;
-    }
-    const uint32_t s = edges[3 * e], r = edges[3 * e + 1], t = edges[3 * e + 2];
-    const float* ss = node_row(pi, s, d);
-    const float* st = node_row(pj, t, d);
-    const float* sr = kind != EMBER_DOT ? rel + (uint64_t)r * d : nullptr;
-    const uint32_t h = d / 2, nq = d / 4;
-    float* xd = sm + wib * 2 * kp;
+    float* xd = stage + wib * 2 * kp;
     float* xs = xd + kp;
-    float part = 0.f;
-    for (uint32_t q = lane; q < nq; q += 32) {
-        const Quad S = load_quad(ss, kind, h, q), T = load_quad(st, kind, h, q);
-        const Quad R = sr ? load_quad(sr, kind, h, q) : S;
-        Quad ad, as;
-        adjust_quad(kind, S, R, T, ad, as);
+    const uint32_t e0 = blockIdx.x * GP_ROWS;
+    const uint32_t h = d / 2, nq = d / 4;
+    for (uint32_t k = d + lane; k < kp; k += 32) xd[k] = xs[k] = 0.f;  // K padding (never rewritten)
+    for (uint32_t rr = wib; rr < GP_ROWS; rr += GP_WARPS) {
+        const uint32_t e = e0 + rr;
+        if (e >= nb) {  // padding rows of the last tiles
+            for (uint32_t c = lane; c < nblk; c += 32) tile[c * GP_ROWS + rr] = make_uint4(0, 0, 0, 0);
+            continue;
+        }
+        const uint32_t s = edges[3 * e], r = edges[3 * e + 1], t = edges[3 * e + 2];
+        const float* ss = node_row(pi, s, d);
+        const float* st = node_row(pj, t, d);
+        const float* sr = kind != EMBER_DOT ? rel + (uint64_t)r * d : nullptr;
+        float part = 0.f;
+        __syncwarp();  // the previous edge's staged rows have been packed
+        for (uint32_t q = lane; q < nq; q += 32) {
+            const Quad S = load_quad(ss, kind, h, q), T = load_quad(st, kind, h, q);
+            const Quad R = sr ? load_quad(sr, kind, h, q) : S;
+            Quad ad, as;
+            adjust_quad(kind, S, R, T, ad, as);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) part += ad.v[i] * T.v[i];
-        if (PACKED) {
+            for (int i = 0; i < 4; ++i) part += ad.v[i] * T.v[i];
             store_quad(xd, kind, h, q, ad);
             store_quad(xs, kind, h, q, as);
-        } else {
-            store_quad(A + (uint64_t)e * d, kind, h, q, ad);
-            store_quad(A + ((uint64_t)nb + e) * d, kind, h, q, as);
         }
-    }
-    if (PACKED) {
-        for (uint32_t k = d + lane; k < kp; k += 32) xd[k] = xs[k] = 0.f;  // K padding
         __syncwarp();
         if (lane < 2 * CB) {
             const uint32_t cb = lane % CB, side = lane / CB;
@@ -160,9 +158,42 @@ __global__ void k_gather_adjust(const uint32_t* __restrict__ edges, uint32_t nb,
             float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
             uint4 hq, lq;
             tc::split8(v, hq, lq);
-            P[((uint64_t)side * 2 * CB + cb) * cap + e] = hq;
-            P[((uint64_t)side * 2 * CB + CB + cb) * cap + e] = lq;
+            tile[((side * 2 * CB) + cb) * GP_ROWS + rr] = hq;
+            tile[((side * 2 * CB) + CB + cb) * GP_ROWS + rr] = lq;
         }
+        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (lane == 0) fpos[e] = part;
+    }
+    __syncthreads();
+    uint4* P = reinterpret_cast<uint4*>(Apk);
+    for (uint32_t i = threadIdx.x; i < nblk * GP_ROWS; i += blockDim.x) {
+        const uint32_t blk = i / GP_ROWS, rr = i % GP_ROWS;  // blk = side * 2CB + column block
+        P[(uint64_t)blk * cap + e0 + rr] = tile[i];
+    }
+}
+
+// fp32 gather (SIMT engine): one warp per edge, A[0][e] = ad, A[1][e] = as, fpos[e] = ad . t.
+__global__ void k_gather_adjust(const uint32_t* __restrict__ edges, uint32_t nb, PartView pi, PartView pj,
+                                const float* __restrict__ rel, int kind, uint32_t d, float* __restrict__ A,
+                                float* __restrict__ fpos) {
+    const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t e = blockIdx.x * (blockDim.x >> 5) + wib;
+    if (e >= nb) return;
+    const uint32_t s = edges[3 * e], r = edges[3 * e + 1], t = edges[3 * e + 2];
+    const float* ss = node_row(pi, s, d);
+    const float* st = node_row(pj, t, d);
+    const float* sr = kind != EMBER_DOT ? rel + (uint64_t)r * d : nullptr;
+    const uint32_t h = d / 2, nq = d / 4;
+    float part = 0.f;
+    for (uint32_t q = lane; q < nq; q += 32) {
+        const Quad S = load_quad(ss, kind, h, q), T = load_quad(st, kind, h, q);
+        const Quad R = sr ? load_quad(sr, kind, h, q) : S;
+        Quad ad, as;
+        adjust_quad(kind, S, R, T, ad, as);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) part += ad.v[i] * T.v[i];
+        store_quad(A + (uint64_t)e * d, kind, h, q, ad);
+        store_quad(A + ((uint64_t)nb + e) * d, kind, h, q, as);
     }
     for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
     if (lane == 0) fpos[e] = part;
@@ -731,6 +762,8 @@ __global__ void k_init_rows(float* theta, float* acc, uint64_t first, uint64_t r
     }
 }
 
+constexpr size_t sm_cap() { return 227 * 1024; }
+
 }  // namespace
 
 void launch_sample(const Engine& E, uint32_t* out, uint64_t base, const uint32_t* bucket, uint64_t bucket_n,
@@ -745,15 +778,20 @@ void launch_sample(const Engine& E, uint32_t* out, uint64_t base, const uint32_t
 
 void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj,
                           bool packed) {
-    const uint32_t warps = 8;
     if (packed) {
-        const uint32_t rows_pad = (uint32_t)Engine::pad_rows(nb);
-        const size_t smp = (size_t)warps * 2 * E.KP * sizeof(float);
-        k_gather_adjust<true><<<(rows_pad + warps - 1) / warps, warps * 32, smp, E.stream>>>(
-            edges, nb, rows_pad, pi, pj, E.rel_theta, E.m.kind, E.dim, E.CB, E.b_cap, nullptr, E.s.Apk, E.s.fpos);
+        const uint32_t rows_pad = (uint32_t)Engine::pad_rows(nb);  // a multiple of GP_ROWS
+        const size_t sm = (size_t)4 * E.CB * GP_ROWS * 16 + (size_t)GP_WARPS * 2 * E.KP * sizeof(float);
+        static bool attr = false;
+        if (!attr) {
+            EMBER_CUDA(cudaFuncSetAttribute(k_gather_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_cap()));
+            attr = true;
+        }
+        k_gather_pack<<<rows_pad / GP_ROWS, 32 * GP_WARPS, sm, E.stream>>>(edges, nb, pi, pj, E.rel_theta, E.m.kind,
+                                                                           E.dim, E.CB, E.b_cap, E.s.Apk, E.s.fpos);
     } else {
-        k_gather_adjust<false><<<(nb + warps - 1) / warps, warps * 32, 0, E.stream>>>(
-            edges, nb, nb, pi, pj, E.rel_theta, E.m.kind, E.dim, 0, 0, E.s.A, nullptr, E.s.fpos);
+        const uint32_t warps = 8;
+        k_gather_adjust<<<(nb + warps - 1) / warps, warps * 32, 0, E.stream>>>(edges, nb, pi, pj, E.rel_theta,
+                                                                                E.m.kind, E.dim, E.s.A, E.s.fpos);
     }
     EMBER_LAUNCHED(E);
 }
