@@ -599,7 +599,8 @@ def main():
             os.environ.setdefault("RANK", str(rank))
             os.environ.setdefault("WORLD_SIZE", str(world))
             torch.cuda.set_device(local_rank)
-            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+            backend = os.environ.get("EMBER_DIST_BACKEND", "nccl")  # gloo: multi-rank checks on one GPU
+            dist.init_process_group(backend, device_id=torch.device(f"cuda:{local_rank}") if backend == "nccl" else None)
         if dist_path:
             out = bench_distributed(args, rank, world, local_rank)
         elif args.capacity:

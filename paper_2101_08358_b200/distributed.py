@@ -149,31 +149,48 @@ class DistributedTrainer:
         return n
 
     def handoff(self, r: int):
-        """Partitions leaving this rank after round r go to their round-(r+1) holder (P2P)."""
+        """Partitions leaving this rank after round r go to their round-(r+1) holder (P2P: NCCL
+        over NVLink for device tensors; a gloo group moves device tables through host copies)."""
         moves = self.plan.transfers(r)
         if not moves:
             return
         ops, incoming = [], []
         P2P = self.dist.P2POp
+        stage = self._host_staged()
         with self.be.collective_stream():
             for x, src, dst in moves:
                 if src == self.rank:
                     th, ac = self.be.tables(x)
+                    if stage:
+                        th, ac = th.cpu(), ac.cpu()
                     ops += [P2P(self.dist.isend, th, dst, self.group), P2P(self.dist.isend, ac, dst, self.group)]
                     self.handoff_bytes += th.numel() * th.element_size() * 2
                 elif dst == self.rank:
                     th, ac = self.be.empty_tables(x)
-                    ops += [P2P(self.dist.irecv, th, src, self.group), P2P(self.dist.irecv, ac, src, self.group)]
-                    incoming.append((x, th, ac))
+                    bufs = (th.cpu(), ac.cpu()) if stage else (th, ac)
+                    ops += [P2P(self.dist.irecv, bufs[0], src, self.group),
+                            P2P(self.dist.irecv, bufs[1], src, self.group)]
+                    incoming.append((x, th, ac, bufs))
             if ops:
                 for w in self.dist.batch_isend_irecv(ops):
                     w.wait()
+            if stage:
+                for x, th, ac, bufs in incoming:
+                    th.copy_(bufs[0])
+                    ac.copy_(bufs[1])
         self.be.after_handoff()
         for x, src, dst in moves:
             if src == self.rank:
                 self.be.drop(x)
-        for x, th, ac in incoming:
+        for x, th, ac, _ in incoming:
             self.be.adopt(x, th, ac)
+
+    def _host_staged(self) -> bool:
+        try:
+            backend = self.dist.get_backend(self.group)
+        except Exception:
+            return False
+        return backend == "gloo" and getattr(self.be, "device_tables", False)
 
     def local_tables(self):
         """This rank's partitions between epochs (the round-0 holders), as {x: (theta, acc)}."""
@@ -184,6 +201,8 @@ class GpuBackend:
     """The rank's GPU: a Trainer (C-ABI context) whose partition tables are bound as they arrive,
     relation gradients reduced externally (ember_relations_external) by the trainer's all-reduce on
     the context stream."""
+
+    device_tables = True
 
     def __init__(self, trainer, edges_dev):
         import torch

@@ -200,3 +200,86 @@ def test_gpu_backend_single_rank_matches_direct_training(kind):
             assert tr.rel_acc.cpu().numpy().tobytes() == ref.rel_acc.cpu().numpy().tobytes()
     finally:
         dist.destroy_process_group()
+
+
+GCFG = dict(kind="complex", dim=32, V=3000, R=12, p=4, b=300, nt=64, seed=11, epochs=2)
+
+
+def _gpu_graph():
+    edges, split = eb.generate_graph(GCFG["V"], GCFG["R"], 20000, seed=5, train_frac=0.9, valid_frac=0.05)
+    return eb.bucket_edges(edges[split == 0], GCFG["V"], GCFG["p"])
+
+
+def _gpu_hyper():
+    return eb.Hyper(kind=GCFG["kind"], dim=GCFG["dim"], batch_size=GCFG["b"], num_negatives=GCFG["nt"], neg_seed=3,
+                    engine="tc")
+
+
+def _gpu_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    bucketed, off = _gpu_graph()
+    dev = torch.from_numpy(bucketed.view(np.int32)).cuda()
+    tr = eb.Trainer(_gpu_hyper(), GCFG["V"], GCFG["R"], GCFG["p"], device=0, allocate=False)
+    D = ed.DistributedTrainer(ed.GpuBackend(tr, dev), GCFG["p"], off, GCFG["b"], rank, world, relations=True,
+                              dist=dist)
+    D.init_embeddings(GCFG["seed"])
+    for ep in range(GCFG["epochs"]):
+        D.train_epoch(ep)
+    torch.cuda.synchronize()
+    tabs = {x: (t[0].cpu().numpy(), t[1].cpu().numpy()) for x, t in D.local_tables().items()}
+    np.savez(os.path.join(out_dir, f"g{rank}.npz"), held=np.array(sorted(tabs)),
+             **{f"th{x}": v[0] for x, v in tabs.items()}, **{f"ac{x}": v[1] for x, v in tabs.items()},
+             rel_theta=tr.rel_theta.cpu().numpy(), rel_acc=tr.rel_acc.cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gpu_two_rank_epochs_bit_identical_to_serial_replay(tmp_path):
+    """Two processes on one GPU run the product backend (C-ABI steps, external relation gradients,
+    partition handoffs) over gloo; every parameter equals a serial replay of the same lockstep
+    schedule on one context (both ranks' batches of a step, relation gradients summed g0 + g1 before
+    one dense relation Adagrad)."""
+    import torch.multiprocessing as mp
+    import paper_2101_08358_b200._lib as L
+    world, port = 2, _free_port()
+    mp.start_processes(_gpu_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True, start_method="spawn")
+    # serial replay on one context
+    bucketed, off = _gpu_graph()
+    dev = torch.from_numpy(bucketed.view(np.int32)).cuda()
+    tr = eb.Trainer(_gpu_hyper(), GCFG["V"], GCFG["R"], GCFG["p"], device=0)
+    tr.init_embeddings(GCFG["seed"])
+    g = [torch.zeros((GCFG["R"], GCFG["dim"]), device="cuda") for _ in range(world)]
+    plan = ed.make_rounds(GCFG["p"], world)
+    base = dev.data_ptr()
+    for ep in range(GCFG["epochs"]):
+        for r in range(plan.rounds):
+            lists = [ed.round_batches(plan, off, GCFG["b"], r, k) for k in range(world)]
+            for s_ in range(max(len(x) for x in lists)):
+                for k in range(world):
+                    L.check(L.lib().ember_relations_external(tr.ctx, g[k].data_ptr()))
+                    if s_ < len(lists[k]):
+                        pos, i, j, kk, lo, hi, begin, nb = lists[k][s_]
+                        L.check(L.lib().ember_train_batch(tr.ctx, base + 12 * lo, hi - lo, begin, nb, i, j, ep, pos, kk,
+                                                          None))
+                    else:
+                        with torch.cuda.stream(tr.torch_stream()):
+                            g[k].zero_()
+                with torch.cuda.stream(tr.torch_stream()):
+                    total = g[0] + g[1]
+                L.check(L.lib().ember_relations_apply_dense(tr.ctx, total.data_ptr()))
+                tr.torch_stream().synchronize()
+    L.check(L.lib().ember_relations_external(tr.ctx, None))
+    th, ac = tr.node_table()
+    rt, ra = tr.rel_theta.cpu().numpy(), tr.rel_acc.cpu().numpy()
+    seen = set()
+    for k in range(world):
+        z = np.load(tmp_path / f"g{k}.npz")
+        assert z["rel_theta"].tobytes() == rt.tobytes() and z["rel_acc"].tobytes() == ra.tobytes()
+        for x in z["held"]:
+            o, n = eb.partition_offset(GCFG["V"], GCFG["p"], int(x)), eb.partition_size(GCFG["V"], GCFG["p"], int(x))
+            assert z[f"th{x}"].tobytes() == th[o:o + n].tobytes(), f"partition {x}"
+            assert z[f"ac{x}"].tobytes() == ac[o:o + n].tobytes()
+            seen.add(int(x))
+    assert seen == set(range(GCFG["p"]))
