@@ -206,6 +206,7 @@ def bench_distributed(args, rank, world, local_rank):
     stream = tr.torch_stream()
     start = D.steps_per_round[0]
     K = min(args.steps, D.total_steps() - start - args.warmup)
+    D.seek(start)  # round-1 layout (round 0 holds the self-buckets)
     D.run_steps(start, args.warmup, 0)
     torch.cuda.synchronize()
     tr.profile(True)
@@ -594,6 +595,7 @@ def main():
         if dist_path:
             import torch
             import torch.distributed as dist
+            local_rank %= max(1, torch.cuda.device_count())  # (more ranks than GPUs: gloo checks only)
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29533")
             os.environ.setdefault("RANK", str(rank))

@@ -45,10 +45,10 @@ class RoundPlan:
     def partitions(self, r: int, g: int) -> list[int]:
         return [int(x) for x in np.nonzero(self.holder[r] == g)[0]]
 
-    def transfers(self, r: int) -> list[tuple[int, int, int]]:
-        """(partition, src, dst) moving between round r and the next one (the last round hands
-        over to round 0 of the next epoch), ascending partition."""
-        a, b = self.holder[r], self.holder[(r + 1) % self.rounds]
+    def transfers(self, r: int, to: int | None = None) -> list[tuple[int, int, int]]:
+        """(partition, src, dst) moving between round r and round `to` (default: the next one; the
+        last round hands over to round 0 of the next epoch), ascending partition."""
+        a, b = self.holder[r], self.holder[(r + 1) % self.rounds if to is None else to]
         return [(int(x), int(a[x]), int(b[x])) for x in range(self.p) if a[x] != b[x]]
 
 
@@ -148,10 +148,18 @@ class DistributedTrainer:
             self.be.apply_relations()
         return n
 
-    def handoff(self, r: int):
-        """Partitions leaving this rank after round r go to their round-(r+1) holder (P2P: NCCL
-        over NVLink for device tensors; a gloo group moves device tables through host copies)."""
-        moves = self.plan.transfers(r)
+    def seek(self, step: int):
+        """Positions the partitions for lockstep step `step` of an epoch (from the round-0 layout):
+        the partitions move straight to their holders of that step's round."""
+        r, _ = self.locate(step)
+        if r:
+            self.handoff(0, to=r)
+
+    def handoff(self, r: int, to: int | None = None):
+        """Partitions leaving this rank after round r go to their round-(r+1) (or round-`to`) holder
+        (P2P: NCCL over NVLink for device tensors; a gloo group moves device tables through host
+        copies)."""
+        moves = self.plan.transfers(r, to)
         if not moves:
             return
         ops, incoming = [], []

@@ -283,3 +283,13 @@ def test_gpu_two_rank_epochs_bit_identical_to_serial_replay(tmp_path):
             assert z[f"ac{x}"].tobytes() == ac[o:o + n].tobytes()
             seen.add(int(x))
     assert seen == set(range(GCFG["p"]))
+
+
+def test_seek_transfers_reach_the_round_layout():
+    plan = ed.make_rounds(16, 8)
+    for r in range(plan.rounds):
+        held = plan.holder[0].copy()
+        for x, src, dst in plan.transfers(0, r):
+            assert held[x] == src
+            held[x] = dst
+        assert (held == plan.holder[r]).all()
