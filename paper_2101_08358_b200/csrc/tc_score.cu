@@ -475,6 +475,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (MODE == MODE_ROWS) {
                 const uint32_t zs = it & 3;
                 tc::mbar_wait(&bars[B_Z_READY + zs], (it >> 2) & 1);
+                if (qd == 2) TC_TRACE(32, it);
                 Z = 1.0f + z + sm.zbuf[zs * 128 + r];  // + exp(f_pos - f_pos) = 1: the positive
                 tc::mbar_arrive(&bars[B_ZB_FREE + zs]);
                 lse = fp + __logf(Z);
@@ -493,6 +494,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 for (int i = 0; i < 4; ++i)
                     if (4 * half + i < nchunks) tc::tmem_ld16(t_row + T_ACC + 16 * (4 * half + i), accv[i]);
                 tc::tmem_ld_wait();
+                if (qd == 2) TC_TRACE(30 + half, it);
                 if (half == 1 || nchunks <= 4) {
                     tc::fence_before();
                     if (half == 1 || nchunks <= 4) tc::mbar_arrive(&bars[B_ACC_EMPTY]);

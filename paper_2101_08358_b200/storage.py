@@ -44,6 +44,7 @@ def read_meta(root: str) -> dict:
 
 
 def write_edges(root: str, split: str, edges: np.ndarray, bucket_offsets: np.ndarray | None = None) -> None:
+    os.makedirs(root, exist_ok=True)
     _pod_write(os.path.join(root, f"edges_{split}.bin"), np.asarray(edges, np.uint32).reshape(-1, 3))
     if bucket_offsets is not None:
         _pod_write(os.path.join(root, "bucket_offsets.bin"), np.asarray(bucket_offsets, np.uint64))
@@ -62,6 +63,7 @@ def read_bucket_offsets(root: str, p: int) -> np.ndarray:
 
 
 def write_node_part(root: str, k: int, theta: np.ndarray, acc: np.ndarray) -> None:
+    os.makedirs(root, exist_ok=True)
     with open(os.path.join(root, f"node_part_{k}.bin"), "wb") as f:
         np.ascontiguousarray(theta, np.float32).tofile(f)
         np.ascontiguousarray(acc, np.float32).tofile(f)
@@ -80,6 +82,7 @@ def read_node_part(root: str, k: int, rows: int, dim: int, out_theta=None, out_a
 
 
 def write_relations(root: str, theta: np.ndarray, acc: np.ndarray) -> None:
+    os.makedirs(root, exist_ok=True)
     with open(os.path.join(root, "relations.bin"), "wb") as f:
         np.ascontiguousarray(theta, np.float32).tofile(f)
         np.ascontiguousarray(acc, np.float32).tofile(f)

@@ -9,7 +9,7 @@ import numpy as np
 NAMES = {1: "P.res_load", 2: "P.ring_slot", 10: "M.R_ready", 11: "M.ring_full", 12: "M.S_issued", 13: "M.P_full",
          14: "M.PN_issued", 15: "M.acc_empty", 16: "M.ring_wait", 17: "M.P_wait", 20: "E0.S_full", 21: "E1.S_full", 22: "E0.P_done", 23: "E1.P_done",
          24: "E0.stage_start", 25: "E0.stage_end", 26: "E0.acc_full", 27: "E1.acc_full", 28: "E0.tail_end",
-         29: "E1.tail_end"}
+         29: "E1.tail_end", 30: "E1.acc_ld0", 31: "E1.acc_ld1", 32: "E1.z_ready"}
 
 
 def main(path, show=120):
@@ -44,6 +44,10 @@ def main(path, show=120):
     iss = np.array(sorted(first[12].values()))
     if len(iss) > 2:
         print(f"{'S issue period':44s} median {np.median(np.diff(iss)):8.0f}  mean {np.mean(np.diff(iss)):8.0f}")
+    lat(27, 32, "tail: acc_full -> z ready")
+    lat(32, 30, "tail: z ready -> acc batch 0 loaded")
+    lat(30, 31, "tail: batch 0 stores + batch 1 loaded")
+    lat(31, 29, "tail: batch 1 stores -> tail end")
     rf = first[11]
     prev = {q: first[12].get(q - 1) for q in rf}
     d = [rf[q] - prev[q] for q in rf if prev[q] is not None]
