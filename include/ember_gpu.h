@@ -171,6 +171,21 @@ int ember_graph_generate(int device, uint64_t num_nodes, uint32_t num_relations,
 int ember_graph_bucket(int device, uint64_t num_nodes, uint32_t p, const uint32_t* edges_in, uint64_t n,
                        uint32_t* edges_out, uint64_t* offsets_out);
 
+/* Graph-store preprocessing on the device (ingest + partition_nodes + bucket_edges).
+ * raw_dev: n edges of (src, rel, dst) tokens (arbitrary u32 values, device). Node / relation
+ * tokens are mapped to dense ids (rank among the sorted unique tokens); the nodes are then
+ * relabeled by a seeded random permutation, so each partition (contiguous row range) is a random
+ * node subset; the edges are shuffled (seeded) and split: first floor(train_frac*n) train, next
+ * floor(valid_frac*n) valid, rest test. Train is bucketed (stable) into train_out_dev with
+ * offsets_host (p*p+1); valid/test (nullable) keep the shuffled order. counts_host[3]: split sizes.
+ * node_tokens_dev (nullable, capacity 2n): token of each relabeled node id; rel_tokens_dev
+ * (nullable, capacity n): token of each relation id. Exactly restated by the CPU oracle. */
+int ember_graph_preprocess(int device, const uint32_t* raw_dev, uint64_t n, uint32_t p, uint64_t seed,
+                           float train_frac, float valid_frac, uint32_t* train_out_dev, uint64_t* offsets_host,
+                           uint32_t* valid_out_dev, uint32_t* test_out_dev, uint64_t* counts_host,
+                           uint32_t* node_tokens_dev, uint32_t* rel_tokens_dev, uint64_t* num_nodes_host,
+                           uint32_t* num_relations_host);
+
 /* ---- measurement ----------------------------------------------------------------------------
  * enable != 0: record CUDA events on the context stream at step phase boundaries.
  * ms_out[6]: summed ms per phase {sample, gather, contraction, chain+loss, reduce+adagrad, -}

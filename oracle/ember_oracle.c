@@ -548,3 +548,115 @@ void orc_aggregate(const uint32_t* ranks, uint64_t n, const uint32_t* ks, uint32
     out[0] = n ? mrr / (double)n : 0.0;
     for (uint32_t j = 0; j < nk; ++j) out[1 + j] = n ? out[1 + j] / (double)n : 0.0;
 }
+
+/* ---------------------------------------------------------------- preprocessing */
+
+static int u32_cmp(const void* a, const void* b) {
+    const uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+    return x < y ? -1 : x > y;
+}
+
+typedef struct {
+    uint64_t key;
+    uint32_t idx;
+} orc_ki;
+
+static int ki_cmp(const void* a, const void* b) {
+    const orc_ki* x = (const orc_ki*)a;
+    const orc_ki* y = (const orc_ki*)b;
+    if (x->key != y->key) return x->key < y->key ? -1 : 1;
+    return x->idx < y->idx ? -1 : x->idx > y->idx;
+}
+
+static uint32_t sorted_unique(uint32_t* a, uint64_t n) {
+    qsort(a, n, sizeof(uint32_t), u32_cmp);
+    uint64_t m = 0;
+    for (uint64_t i = 0; i < n; ++i)
+        if (i == 0 || a[i] != a[i - 1]) a[m++] = a[i];
+    return (uint32_t)m;
+}
+
+static uint32_t lower_bound32(const uint32_t* a, uint32_t n, uint32_t x) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        uint32_t mid = (lo + hi) / 2;
+        if (a[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+/* order[i] = index of the i-th smallest (mix_seed(seed, index), index) */
+static void seeded_order(uint64_t seed, uint64_t n, uint32_t* order) {
+    orc_ki* v = (orc_ki*)malloc(n * sizeof(orc_ki));
+    for (uint64_t i = 0; i < n; ++i) {
+        v[i].key = orc_mix_seed(seed, i);
+        v[i].idx = (uint32_t)i;
+    }
+    qsort(v, n, sizeof(orc_ki), ki_cmp);
+    for (uint64_t i = 0; i < n; ++i) order[i] = v[i].idx;
+    free(v);
+}
+
+static uint32_t part_of(uint64_t id, uint64_t V, uint32_t p) {
+    const uint64_t q = V / p, r = V % p, big = r * (q + 1);
+    return id < big ? (uint32_t)(id / (q + 1)) : (uint32_t)(r + (id - big) / q);
+}
+
+void orc_preprocess(const uint32_t* raw, uint64_t n, uint32_t p, uint64_t seed, float train_frac, float valid_frac,
+                    uint32_t* train_out, uint64_t* offsets, uint32_t* valid_out, uint32_t* test_out, uint64_t* counts,
+                    uint32_t* node_tokens, uint32_t* rel_tokens, uint64_t* num_nodes, uint32_t* num_rel) {
+    uint32_t* U = (uint32_t*)malloc(2 * n * sizeof(uint32_t));
+    uint32_t* RU = (uint32_t*)malloc(n * sizeof(uint32_t));
+    for (uint64_t e = 0; e < n; ++e) {
+        U[e] = raw[3 * e];
+        U[n + e] = raw[3 * e + 2];
+        RU[e] = raw[3 * e + 1];
+    }
+    const uint32_t V = sorted_unique(U, 2 * n), R = sorted_unique(RU, n);
+    uint32_t* vorder = (uint32_t*)malloc((size_t)V * sizeof(uint32_t));
+    uint32_t* new_id = (uint32_t*)malloc((size_t)V * sizeof(uint32_t));
+    seeded_order(orc_mix_seed(seed, 0x9e47ULL), V, vorder);
+    for (uint32_t i = 0; i < V; ++i) new_id[vorder[i]] = i;
+    uint32_t* eorder = (uint32_t*)malloc(n * sizeof(uint32_t));
+    seeded_order(orc_mix_seed(seed, 0x5917ULL), n, eorder);
+    uint32_t* sh = (uint32_t*)malloc(3 * n * sizeof(uint32_t));
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t e = eorder[i];
+        sh[3 * i] = new_id[lower_bound32(U, V, raw[3 * e])];
+        sh[3 * i + 1] = lower_bound32(RU, R, raw[3 * e + 1]);
+        sh[3 * i + 2] = new_id[lower_bound32(U, V, raw[3 * e + 2])];
+    }
+    const uint64_t n_train = (uint64_t)((double)train_frac * (double)n);
+    uint64_t n_valid = (uint64_t)((double)valid_frac * (double)n);
+    if (n_valid > n - n_train) n_valid = n - n_train;
+    const uint64_t n_test = n - n_train - n_valid;
+    /* stable counting sort of the train split by bucket */
+    const uint32_t nb = p * p;
+    memset(offsets, 0, (nb + 1) * sizeof(uint64_t));
+    for (uint64_t i = 0; i < n_train; ++i) ++offsets[part_of(sh[3 * i], V, p) * p + part_of(sh[3 * i + 2], V, p) + 1];
+    for (uint32_t b = 0; b < nb; ++b) offsets[b + 1] += offsets[b];
+    uint64_t* at = (uint64_t*)malloc((nb + 1) * sizeof(uint64_t));
+    memcpy(at, offsets, (nb + 1) * sizeof(uint64_t));
+    for (uint64_t i = 0; i < n_train; ++i) {
+        const uint64_t k = at[part_of(sh[3 * i], V, p) * p + part_of(sh[3 * i + 2], V, p)]++;
+        memcpy(train_out + 3 * k, sh + 3 * i, 12);
+    }
+    if (valid_out) memcpy(valid_out, sh + 3 * n_train, n_valid * 12);
+    if (test_out) memcpy(test_out, sh + 3 * (n_train + n_valid), n_test * 12);
+    if (node_tokens)
+        for (uint32_t i = 0; i < V; ++i) node_tokens[i] = U[vorder[i]];
+    if (rel_tokens) memcpy(rel_tokens, RU, (size_t)R * 4);
+    counts[0] = n_train;
+    counts[1] = n_valid;
+    counts[2] = n_test;
+    *num_nodes = V;
+    *num_rel = R;
+    free(U);
+    free(RU);
+    free(vorder);
+    free(new_id);
+    free(eorder);
+    free(sh);
+    free(at);
+}

@@ -96,6 +96,15 @@ void orc_eval_ranks(int32_t kind, uint32_t dim, const float* node_theta, const f
 /* aggregate: out[0] = MRR, out[1..nk] = Hits@k. */
 void orc_aggregate(const uint32_t* ranks, uint64_t n, const uint32_t* ks, uint32_t nk, double* out);
 
+/* graph-store preprocessing, the semantics ember_graph_preprocess pins:
+ * dense ids = rank among sorted unique tokens; node relabel = position in the order of dense
+ * ids by (mix_seed(mix_seed(seed, 0x9e47), v), v); edge shuffle = order of edge indices by
+ * (mix_seed(mix_seed(seed, 0x5917), e), e); split floor(train*n) / floor(valid*n) / rest;
+ * train bucketed by (part(src), part(dst)), stable. Outputs as in the C-ABI (host arrays). */
+void orc_preprocess(const uint32_t* raw, uint64_t n, uint32_t p, uint64_t seed, float train_frac, float valid_frac,
+                    uint32_t* train_out, uint64_t* offsets, uint32_t* valid_out, uint32_t* test_out, uint64_t* counts,
+                    uint32_t* node_tokens, uint32_t* rel_tokens, uint64_t* num_nodes, uint32_t* num_rel);
+
 int orc_num_threads(void);
 
 #ifdef __cplusplus

@@ -80,6 +80,8 @@ def lib():
                                      u64p, C.c_uint64, u32p, C.c_uint64, C.c_uint32, C.c_float, C.c_uint32,
                                      C.c_uint64, u32p]
         L.orc_aggregate.argtypes = [u32p, C.c_uint64, u32p, C.c_uint32, f64p]
+        L.orc_preprocess.argtypes = [u32p, C.c_uint64, C.c_uint32, C.c_uint64, C.c_float, C.c_float, u32p, u64p, u32p,
+                                     u32p, u64p, u32p, u32p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32)]
         L.orc_num_threads.restype = C.c_int
         _ORACLE = L
     return _ORACLE
@@ -228,3 +230,23 @@ def aggregate(ranks, ks=(1, 10)):
     out = np.zeros(1 + len(ks), np.float64)
     lib().orc_aggregate(np.ascontiguousarray(ranks, np.uint32), len(ranks), ks_a, len(ks), out)
     return {"mrr": out[0], **{f"hits@{k}": out[1 + i] for i, k in enumerate(ks)}}
+
+
+def preprocess(raw, p, seed, train_frac=0.9, valid_frac=0.05):
+    """orc_preprocess (graph-store preprocessing restated on the CPU): same outputs as
+    paper_2101_08358_b200.preprocess_graph, as numpy arrays."""
+    raw = np.ascontiguousarray(raw, np.uint32).reshape(-1, 3)
+    n = raw.shape[0]
+    train = np.zeros((n, 3), np.uint32)
+    valid = np.zeros((n, 3), np.uint32)
+    test = np.zeros((n, 3), np.uint32)
+    off = np.zeros(p * p + 1, np.uint64)
+    counts = np.zeros(3, np.uint64)
+    ntok = np.zeros(2 * n, np.uint32)
+    rtok = np.zeros(n, np.uint32)
+    V, R = C.c_uint64(0), C.c_uint32(0)
+    lib().orc_preprocess(raw, n, p, seed, C.c_float(train_frac), C.c_float(valid_frac), train, off, valid, test,
+                         counts, ntok, rtok, C.byref(V), C.byref(R))
+    a, b, c = (int(x) for x in counts)
+    return {"train": train[:a], "valid": valid[:b], "test": test[:c], "offsets": off, "num_nodes": V.value,
+            "num_relations": R.value, "node_tokens": ntok[:V.value], "rel_tokens": rtok[:R.value]}

@@ -15,7 +15,7 @@ import numpy as np
 from ._lib import (ENGINE, KIND, ORDERING, BufferReport, ConfigError, EmberError, GraphDesc, ModelDesc,  # noqa: F401
                    StepStats, check, lib)
 
-__all__ = ["ConfigError", "EmberError", "Hyper", "Trainer", "PartitionBuffer", "make_plan", "lower_bound_swaps",
+__all__ = ["ConfigError", "EmberError", "Hyper", "Trainer", "PartitionBuffer", "preprocess_graph", "make_plan", "lower_bound_swaps",
            "elimination_swap_formula", "generate_graph", "bucket_edges", "partition_offset", "partition_size", "lib"]
 
 
@@ -103,6 +103,34 @@ def bucket_edges(edges, num_nodes: int, p: int, device: int | None = None):
     out = torch.empty_like(edges)
     check(lib().ember_graph_bucket(device, num_nodes, p, _ptr(edges), n, _ptr(out), _ptr(offsets)))
     return out, offsets
+
+
+def preprocess_graph(raw_edges, p: int, seed: int, train_frac: float = 0.9, valid_frac: float = 0.05,
+                     device: int = 0) -> dict:
+    """Graph-store preprocessing on the device: dense ids, seeded node permutation,
+    seeded shuffle + split, stable bucketing of train. raw_edges: (n, 3) u32 tokens (numpy or a
+    device tensor). Returns device tensors train/valid/test, offsets (numpy), num_nodes,
+    num_relations and the token of every relabeled node / relation id."""
+    import torch
+    dev = torch.device(f"cuda:{device}")
+    raw = raw_edges if hasattr(raw_edges, "data_ptr") else torch.from_numpy(
+        np.ascontiguousarray(raw_edges, np.uint32).view(np.int32))
+    raw = raw.to(dev).contiguous()
+    n = int(raw.shape[0])
+    train = torch.empty((n, 3), dtype=torch.int32, device=dev)
+    valid = torch.empty((n, 3), dtype=torch.int32, device=dev)
+    test = torch.empty((n, 3), dtype=torch.int32, device=dev)
+    ntok = torch.empty(2 * n, dtype=torch.int32, device=dev)
+    rtok = torch.empty(n, dtype=torch.int32, device=dev)
+    offsets = np.zeros(p * p + 1, np.uint64)
+    counts = np.zeros(3, np.uint64)
+    V, R = C.c_uint64(0), C.c_uint32(0)
+    check(lib().ember_graph_preprocess(device, _ptr(raw), n, p, seed, train_frac, valid_frac, _ptr(train),
+                                       _ptr(offsets), _ptr(valid), _ptr(test), _ptr(counts), _ptr(ntok), _ptr(rtok),
+                                       C.byref(V), C.byref(R)))
+    a, b, c = (int(x) for x in counts)
+    return {"train": train[:a], "valid": valid[:b], "test": test[:c], "offsets": offsets, "num_nodes": V.value,
+            "num_relations": R.value, "node_tokens": ntok[:V.value], "rel_tokens": rtok[:R.value]}
 
 
 # ---------------------------------------------------------------------------------- trainer

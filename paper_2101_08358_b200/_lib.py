@@ -78,6 +78,8 @@ def _declare(L):
         "ember_elimination_swap_formula": (u64, [u32, u32]),
         "ember_graph_generate": (C.c_int, [i32, u64, u32, u64, u64, f32, f32, vp, vp]),
         "ember_graph_bucket": (C.c_int, [i32, u64, u32, vp, u64, vp, vp]),
+        "ember_graph_preprocess": (C.c_int, [i32, vp, u64, u32, u64, f32, f32, vp, vp, vp, vp, vp, vp, vp,
+                                             C.POINTER(u64), C.POINTER(u32)]),
         "ember_tc_selftest": (C.c_int, [i32, i32, i32, i32, u64, C.POINTER(C.c_double)]),
         "ember_tc_mmabench": (C.c_int, [i32, i32, i32, i32, C.POINTER(C.c_double)]),
         "ember_profile_enable": (C.c_int, [vp, i32]),

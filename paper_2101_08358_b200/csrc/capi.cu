@@ -18,6 +18,10 @@ void graph_generate(int device, uint64_t V, uint32_t R, uint64_t n, uint64_t see
                     uint32_t* edges, uint8_t* split);
 void graph_bucket(int device, uint64_t V, uint32_t p, const uint32_t* in, uint64_t n, uint32_t* out,
                   uint64_t* offsets);
+void graph_preprocess(int device, const uint32_t* raw, uint64_t n, uint32_t p, uint64_t seed, float train_frac,
+                      float valid_frac, uint32_t* train_out, uint64_t* offsets, uint32_t* valid_out, uint32_t* test_out,
+                      uint64_t* counts, uint32_t* node_tokens, uint32_t* rel_tokens, uint64_t* num_nodes,
+                      uint32_t* num_rel);
 double tc_selftest(int device, int mode, int K, int N, uint64_t seed);
 double tc_mmabench(int device, int mode, int N, int iters, int nacc);
 void launch_eval_filtered(const Engine& E, const uint32_t* test, uint32_t n_test, const uint64_t* keys, uint64_t n_keys,
@@ -356,6 +360,22 @@ int ember_graph_bucket(int device, uint64_t V, uint32_t p, const uint32_t* in, u
         need(out, "edges_out");
         need(offsets, "offsets_out");
         graph_bucket(device, V, p, in, n, out, offsets);
+    });
+}
+
+int ember_graph_preprocess(int device, const uint32_t* raw, uint64_t n, uint32_t p, uint64_t seed, float train_frac,
+                           float valid_frac, uint32_t* train_out, uint64_t* offsets, uint32_t* valid_out,
+                           uint32_t* test_out, uint64_t* counts, uint32_t* node_tokens, uint32_t* rel_tokens,
+                           uint64_t* num_nodes, uint32_t* num_rel) {
+    return guarded([&] {
+        need(raw, "raw_dev");
+        need(train_out, "train_out_dev");
+        need(offsets, "offsets_host");
+        need(counts, "counts_host");
+        need(num_nodes, "num_nodes_host");
+        need(num_rel, "num_relations_host");
+        graph_preprocess(device, raw, n, p, seed, train_frac, valid_frac, train_out, offsets, valid_out, test_out,
+                         counts, node_tokens, rel_tokens, num_nodes, num_rel);
     });
 }
 

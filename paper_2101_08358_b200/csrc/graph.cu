@@ -217,4 +217,166 @@ void graph_bucket(int device, uint64_t V, uint32_t p, const uint32_t* in, uint64
     cudaFree(doff);
 }
 
+// ---- graph-store preprocessing on the device (ingest, partition_nodes,
+// bucket_edges) ----------------------------------------------------------------------------
+// Pinned semantics (SPEC leaves orders open): dense node ids = rank of the token among the sorted
+// unique src/dst tokens, dense relation ids likewise; the node permutation sorts dense ids by
+// (mix_seed(mix_seed(seed, 0x9e47), v), v) and relabels v -> its position, so partition k (a
+// contiguous row range) is a seeded random node subset; the edge shuffle sorts edge indices by
+// (mix_seed(mix_seed(seed, 0x5917), e), e); the first floor(train*n) shuffled edges are train,
+// the next floor(valid*n) valid, the rest test; train is bucketed stably (bucket_edges above).
+// Restated on the CPU in oracle/ember_oracle.c (orc_preprocess) and compared bit for bit.
+namespace {
+
+__global__ void k_prep_tokens(const uint32_t* raw, uint64_t n, uint32_t* nodes, uint32_t* rels) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    nodes[e] = raw[3 * e];
+    nodes[n + e] = raw[3 * e + 2];
+    rels[e] = raw[3 * e + 1];
+}
+
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t n, uint32_t x) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_prep_keys(uint64_t seed, uint64_t n, uint64_t* keys, uint32_t* vals) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    keys[i] = mix_seed(seed, i);
+    vals[i] = (uint32_t)i;
+}
+
+__global__ void k_prep_gather(const uint32_t* src, const uint32_t* idx, uint64_t n, uint32_t* out) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = src[idx[i]];
+}
+
+__global__ void k_prep_invert(const uint32_t* order, uint64_t n, uint32_t* new_id) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) new_id[order[i]] = (uint32_t)i;
+}
+
+// shuffled edge i = raw edge order[i], relabeled.
+__global__ void k_prep_relabel(const uint32_t* raw, const uint32_t* order, uint64_t n, const uint32_t* U, uint32_t V,
+                               const uint32_t* RU, uint32_t R, const uint32_t* new_id, uint32_t* out) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t e = order[i];
+    out[3 * i] = new_id[lower_bound_u32(U, V, raw[3 * e])];
+    out[3 * i + 1] = lower_bound_u32(RU, R, raw[3 * e + 1]);
+    out[3 * i + 2] = new_id[lower_bound_u32(U, V, raw[3 * e + 2])];
+}
+
+template <typename T>
+T* dnew(size_t n) {
+    T* p = nullptr;
+    EMBER_CUDA(cudaMalloc(&p, (n ? n : 1) * sizeof(T)));
+    return p;
+}
+
+// sorted unique values of in[0, n) -> out (capacity n), returns the count
+uint32_t sort_unique(const uint32_t* in, uint64_t n, uint32_t* out) {
+    uint32_t* sorted = dnew<uint32_t>(n);
+    uint32_t* cnt = dnew<uint32_t>(1);
+    size_t b1 = 0, b2 = 0;
+    EMBER_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, b1, in, sorted, (int)n));
+    EMBER_CUDA(cub::DeviceSelect::Unique(nullptr, b2, sorted, out, cnt, (int)n));
+    void* tmp = dnew<char>(std::max(b1, b2));
+    size_t b = std::max(b1, b2);
+    EMBER_CUDA(cub::DeviceRadixSort::SortKeys(tmp, b, in, sorted, (int)n));
+    b = std::max(b1, b2);
+    EMBER_CUDA(cub::DeviceSelect::Unique(tmp, b, sorted, out, cnt, (int)n));
+    uint32_t h = 0;
+    EMBER_CUDA(cudaMemcpy(&h, cnt, 4, cudaMemcpyDeviceToHost));
+    cudaFree(sorted);
+    cudaFree(cnt);
+    cudaFree(tmp);
+    return h;
+}
+
+// order[i] = index of the i-th smallest (mix_seed(seed, index), index)
+void seeded_order(uint64_t seed, uint64_t n, uint32_t* order) {
+    uint64_t *k1 = dnew<uint64_t>(n), *k2 = dnew<uint64_t>(n);
+    uint32_t* v1 = dnew<uint32_t>(n);
+    const unsigned blocks = (unsigned)((n + 255) / 256);
+    k_prep_keys<<<blocks, 256>>>(seed, n, k1, v1);
+    EMBER_CUDA(cudaGetLastError());
+    size_t b = 0;
+    EMBER_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, k1, k2, v1, order, (int)n));  // stable: ties by index
+    void* tmp = dnew<char>(b);
+    EMBER_CUDA(cub::DeviceRadixSort::SortPairs(tmp, b, k1, k2, v1, order, (int)n));
+    cudaFree(k1);
+    cudaFree(k2);
+    cudaFree(v1);
+    cudaFree(tmp);
+}
+
+}  // namespace
+
+void graph_preprocess(int device, const uint32_t* raw, uint64_t n, uint32_t p, uint64_t seed, float train_frac,
+                      float valid_frac, uint32_t* train_out, uint64_t* offsets, uint32_t* valid_out, uint32_t* test_out,
+                      uint64_t* counts, uint32_t* node_tokens, uint32_t* rel_tokens, uint64_t* num_nodes,
+                      uint32_t* num_rel) {
+    if (device < 0) throw ConfigError("graph preprocessing runs on a device (the CPU restatement is the oracle)");
+    if (n == 0) throw ConfigError("empty edge list");
+    if (n >= (1ULL << 31)) throw ConfigError("preprocessing supports < 2^31 edges per call");
+    if (!(train_frac >= 0.f && valid_frac >= 0.f && train_frac + valid_frac <= 1.f))
+        throw ConfigError("split fractions must be >= 0 and sum to <= 1");
+    EMBER_CUDA(cudaSetDevice(device));
+    const unsigned blocks = (unsigned)((n + 255) / 256);
+    uint32_t* toks = dnew<uint32_t>(2 * n);
+    uint32_t* rtoks = dnew<uint32_t>(n);
+    k_prep_tokens<<<blocks, 256>>>(raw, n, toks, rtoks);
+    EMBER_CUDA(cudaGetLastError());
+    uint32_t* U = dnew<uint32_t>(2 * n);
+    uint32_t* RU = dnew<uint32_t>(n);
+    const uint32_t V = sort_unique(toks, 2 * n, U);
+    const uint32_t R = sort_unique(rtoks, n, RU);
+    if (p == 0 || p > V) throw ConfigError("need 1 <= p <= number of nodes");
+    // partition_nodes: seeded permutation of the dense ids
+    uint32_t* vorder = dnew<uint32_t>(V);
+    uint32_t* new_id = dnew<uint32_t>(V);
+    seeded_order(mix_seed(seed, 0x9e47ULL), V, vorder);
+    k_prep_invert<<<(V + 255) / 256, 256>>>(vorder, V, new_id);
+    EMBER_CUDA(cudaGetLastError());
+    // ingest: seeded shuffle of the edges, relabeled
+    uint32_t* eorder = dnew<uint32_t>(n);
+    seeded_order(mix_seed(seed, 0x5917ULL), n, eorder);
+    uint32_t* shuffled = dnew<uint32_t>(3 * n);
+    k_prep_relabel<<<blocks, 256>>>(raw, eorder, n, U, V, RU, R, new_id, shuffled);
+    EMBER_CUDA(cudaGetLastError());
+    const uint64_t n_train = (uint64_t)((double)train_frac * (double)n);
+    const uint64_t n_valid = std::min<uint64_t>(n - n_train, (uint64_t)((double)valid_frac * (double)n));
+    const uint64_t n_test = n - n_train - n_valid;
+    // bucket_edges of the train split (stable)
+    if (n_train) graph_bucket(device, V, p, shuffled, n_train, train_out, offsets);
+    else
+        for (uint64_t b = 0; b <= (uint64_t)p * p; ++b) offsets[b] = 0;
+    if (valid_out && n_valid)
+        EMBER_CUDA(cudaMemcpy(valid_out, shuffled + 3 * n_train, n_valid * 12, cudaMemcpyDeviceToDevice));
+    if (test_out && n_test)
+        EMBER_CUDA(cudaMemcpy(test_out, shuffled + 3 * (n_train + n_valid), n_test * 12, cudaMemcpyDeviceToDevice));
+    if (node_tokens) {  // token of relabeled node i: U[vorder[i]]
+        k_prep_gather<<<(V + 255) / 256, 256>>>(U, vorder, V, node_tokens);
+        EMBER_CUDA(cudaGetLastError());
+    }
+    if (rel_tokens) EMBER_CUDA(cudaMemcpy(rel_tokens, RU, (size_t)R * 4, cudaMemcpyDeviceToDevice));
+    EMBER_CUDA(cudaDeviceSynchronize());
+    counts[0] = n_train;
+    counts[1] = n_valid;
+    counts[2] = n_test;
+    *num_nodes = V;
+    *num_rel = R;
+    for (void* q : {(void*)toks, (void*)rtoks, (void*)U, (void*)RU, (void*)vorder, (void*)new_id, (void*)eorder,
+                    (void*)shuffled})
+        cudaFree(q);
+}
+
 }  // namespace ember
