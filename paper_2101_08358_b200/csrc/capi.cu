@@ -219,10 +219,7 @@ int ember_train_batch_host(ember_ctx* ctx, const uint32_t* bucket, uint64_t buck
         Engine& E = eng(ctx);
         need(bucket, "bucket_edges_dev");
         need(host_batch, "host_batch");
-        if (nb == 0 || nb > E.cap_b) throw ConfigError("batch size must be in [1, batch_size]");
-        EMBER_CUDA(cudaMemcpyAsync(E.s.batch, host_batch, (size_t)nb * 12, cudaMemcpyHostToDevice, E.stream));
-        E.step(E.s.batch, nb, bucket, bucket_n, i, j, epoch, bucket_step, batch_in_bucket, E.s.loss);
-        if (loss_host) EMBER_CUDA(cudaMemcpyAsync(loss_host, E.s.loss, sizeof(float), cudaMemcpyDeviceToHost, E.stream));
+        E.train_batch_host(bucket, bucket_n, host_batch, nb, i, j, epoch, bucket_step, batch_in_bucket, loss_host);
     });
 }
 

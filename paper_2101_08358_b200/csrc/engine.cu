@@ -120,6 +120,11 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
         side = stream;
     else
         EMBER_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    EMBER_CUDA(cudaStreamCreateWithFlags(&io, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+        EMBER_CUDA(cudaEventCreateWithFlags(&ev_staged[k], cudaEventDisableTiming));
+        EMBER_CUDA(cudaEventCreateWithFlags(&ev_consumed[k], cudaEventDisableTiming));
+    }
     EMBER_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     EMBER_CUDA(cudaEventCreateWithFlags(&ev_sorted, cudaEventDisableTiming));
     parts.assign(g.num_partitions, PartView{nullptr, nullptr, 0, 0});
@@ -132,7 +137,7 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
 
     const uint64_t b = cap_b, d = dim;
     s.negs = dalloc<uint32_t>(n_neg);
-    s.batch = dalloc<uint32_t>(3 * b);
+    s.batch = dalloc<uint32_t>(2 * 3 * (uint64_t)b);
     s.A = dalloc<float>(2 * b * d);
     s.N = dalloc<float>((uint64_t)n_neg * d);
     s.fpos = dalloc<float>(b);
@@ -203,6 +208,12 @@ Engine::~Engine() {
         } catch (...) {
         }
     }
+    if (io) cudaStreamSynchronize(io);
+    for (int k = 0; k < 2; ++k) {
+        if (ev_staged[k]) cudaEventDestroy(ev_staged[k]);
+        if (ev_consumed[k]) cudaEventDestroy(ev_consumed[k]);
+    }
+    if (io) cudaStreamDestroy(io);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_sorted) cudaEventDestroy(ev_sorted);
     if (side && side != stream) cudaStreamDestroy(side);
@@ -311,6 +322,23 @@ void Engine::mark(int phase) {
     EMBER_CUDA(cudaEventCreate(&ev));
     EMBER_CUDA(cudaEventRecord(ev, stream));
     prof_events.emplace_back(phase, ev);
+}
+
+void Engine::train_batch_host(const uint32_t* bucket, uint64_t bucket_n, const uint32_t* host_batch, uint32_t nb,
+                              uint32_t i, uint32_t j, uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket,
+                              float* loss_host) {
+    if (nb == 0 || nb > cap_b) throw ConfigError("batch size must be in [1, batch_size]");
+    const int k = (int)(host_steps++ & 1);
+    uint32_t* slot = s.batch + (uint64_t)k * 3 * cap_b;
+    // the copy waits only for the step two calls back (the last reader of this slot), so it
+    // overlaps the previous step; the step waits for its copy
+    if (host_steps > 2) EMBER_CUDA(cudaStreamWaitEvent(io, ev_consumed[k], 0));
+    EMBER_CUDA(cudaMemcpyAsync(slot, host_batch, (size_t)nb * 12, cudaMemcpyHostToDevice, io));
+    EMBER_CUDA(cudaEventRecord(ev_staged[k], io));
+    EMBER_CUDA(cudaStreamWaitEvent(stream, ev_staged[k], 0));
+    step(slot, nb, bucket, bucket_n, i, j, epoch, bucket_step, batch_in_bucket, s.loss);
+    EMBER_CUDA(cudaEventRecord(ev_consumed[k], stream));
+    if (loss_host) EMBER_CUDA(cudaMemcpyAsync(loss_host, s.loss, sizeof(float), cudaMemcpyDeviceToHost, stream));
 }
 
 void Engine::train_batch(const uint32_t* bucket, uint64_t bucket_n, uint64_t batch_begin, uint32_t nb, uint32_t i,

@@ -71,7 +71,7 @@ struct KeySpace {
 //   grows  [3b + n_neg][dim]           gradient rows in sorted (key, slot) order
 struct Scratch {
     uint32_t* negs = nullptr;
-    uint32_t* batch = nullptr;  // staging for host batches [b][3]
+    uint32_t* batch = nullptr;  // staging for host batches: 2 x [b][3] (double-buffered)
     float* A = nullptr;
     float* N = nullptr;
     uint16_t* Apk = nullptr;
@@ -111,6 +111,11 @@ struct Engine {
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;  // key sort runs here, overlapped with gather + contraction
     cudaEvent_t ev_fork = nullptr, ev_sorted = nullptr;
+    // host-batch path: positives copied on `io` into one of two staging slots, overlapping the
+    // previous step; ev_staged[k]: copy into slot k done; ev_consumed[k]: the step reading slot k done
+    cudaStream_t io = nullptr;
+    cudaEvent_t ev_staged[2] = {nullptr, nullptr}, ev_consumed[2] = {nullptr, nullptr};
+    uint64_t host_steps = 0;
     bool own_stream = false;
     bool sorted_pending = false;
     ember_model_desc m{};
@@ -173,6 +178,10 @@ struct Engine {
                           float* node_rows_out, uint32_t* rel_ids_out, float* rel_rows_out);
     void train_batch(const uint32_t* bucket, uint64_t bucket_n, uint64_t batch_begin, uint32_t nb, uint32_t i,
                      uint32_t j, uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket, float* loss_out);
+    // The same step with the positives in host memory (double-buffered asynchronous copy).
+    void train_batch_host(const uint32_t* bucket, uint64_t bucket_n, const uint32_t* host_batch, uint32_t nb,
+                          uint32_t i, uint32_t j, uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket,
+                          float* loss_host);
     // One Algorithm-1 step on nb positives at `edges` (device) of bucket (i, j).
     void step(const uint32_t* edges, uint32_t nb, const uint32_t* bucket, uint64_t bucket_n, uint32_t i, uint32_t j,
               uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket, float* loss_out);

@@ -209,3 +209,30 @@ def test_direct_unique_row_updates_bit_identical(graph, monkeypatch, kind, engin
         tr.close()
     for a, b_ in zip(tabs[0], tabs[1]):
         assert a.tobytes() == b_.tobytes()
+
+
+def test_host_batch_path_bit_identical(graph):
+    """ember_train_batch_host (positives from pinned host memory, double-buffered asynchronous
+    copies overlapping the previous step) trains exactly like ember_train_batch."""
+    edges, off, _ = graph
+    tabs = []
+    keep = []  # pinned host batches must outlive their asynchronous copies
+    for host in (False, True):
+        tr = make_trainer("complex", dim=32, b=256, nt=64, p=2, engine="tc")
+        for step, (i, j) in enumerate([(0, 1), (1, 1), (1, 0), (0, 0)]):
+            b = i * 2 + j
+            bucket_np = edges[off[b]:off[b + 1]]
+            bucket = _dev(bucket_np)
+            for k in range(3):
+                if host:
+                    hb = torch.from_numpy(np.ascontiguousarray(bucket_np[k * 256:(k + 1) * 256]).view(np.int32))
+                    keep.append(hb.pin_memory())
+                    loss = tr.train_batch_host(bucket, keep[-1], i, j, 0, step, k, want_loss=(k == 2))
+                    if k == 2:
+                        assert np.isfinite(loss)
+                else:
+                    tr.train_batch(bucket, k * 256, 256, i, j, 0, step, k)
+        tabs.append(host_tables(tr))
+        tr.close()
+    for a, b_ in zip(tabs[0], tabs[1]):
+        assert a.tobytes() == b_.tobytes()
