@@ -154,6 +154,7 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     s.vals = dalloc<uint32_t>(cap_rows);
     s.vals_sorted = dalloc<uint32_t>(cap_rows);
     s.rank = dalloc<uint32_t>(cap_rows);
+    s.uniq = dalloc<uint8_t>(cap_rows);
     s.ukeys = dalloc<uint32_t>(cap_rows);
     s.counts = dalloc<uint32_t>(cap_rows);
     s.offsets = dalloc<uint32_t>(cap_rows);
@@ -198,7 +199,7 @@ Engine::~Engine() {
     tc_release(*this);
     void* ptrs[] = {s.negs,  s.batch,       s.A,    s.N,          s.Apk,       s.Npk,   s.fpos,   s.lse,
                     s.g0,    s.S,           s.dA,   s.dN_part,    s.grows,     s.loss,  s.loss_part,
-                    s.loss_done, s.keys,    s.keys_sorted, s.vals, s.vals_sorted, s.rank, s.ukeys,  s.counts,
+                    s.loss_done, s.keys,    s.keys_sorted, s.vals, s.vals_sorted, s.rank, s.uniq, s.ukeys,  s.counts,
                     s.offsets, s.nruns,     s.nunique, s.longs,   s.long_owner, s.long_partial, s.cub_tmp, s.rel_dense};
     for (void* p : ptrs)
         if (p) cudaFree(p);

@@ -91,6 +91,7 @@ struct Scratch {
     uint32_t* vals = nullptr;
     uint32_t* vals_sorted = nullptr;
     uint32_t* rank = nullptr;
+    uint8_t* uniq = nullptr;      // slot -> its key occurs once among the batch's slots
     uint32_t* ukeys = nullptr;
     uint32_t* counts = nullptr;
     uint32_t* offsets = nullptr;

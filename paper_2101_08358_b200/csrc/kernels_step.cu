@@ -255,9 +255,14 @@ __global__ void k_keys(const uint32_t* __restrict__ edges, uint32_t nb, const ui
     vals[i] = i;
 }
 
-__global__ void k_rank(const uint32_t* __restrict__ vals_sorted, uint32_t n, uint32_t* __restrict__ rank) {
+// rank[slot] = sorted position; uniq[slot] = the slot's key occurs once among the n slots.
+__global__ void k_rank(const uint32_t* __restrict__ vals_sorted, const uint32_t* __restrict__ keys_sorted, uint32_t n,
+                       uint32_t* __restrict__ rank, uint8_t* __restrict__ uniq) {
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p < n) rank[vals_sorted[p]] = p;
+    if (p >= n) return;
+    const uint32_t slot = vals_sorted[p], k = keys_sorted[p];
+    rank[slot] = p;
+    uniq[slot] = (p == 0 || keys_sorted[p - 1] != k) && (p + 1 == n || keys_sorted[p + 1] != k);
 }
 
 // The sorted position p holds a key that occurs exactly once among the batch's gradient slots.
@@ -378,6 +383,159 @@ __global__ void __launch_bounds__(256, 4) k_chain_rule(const uint32_t* __restric
         else store_quad(gT, kind, h, q, oT);
         if (gR) store_quad(gR, kind, h, q, oR);
     }
+}
+
+// ---- software-pipelined chain rule (tensor-core engine, d <= 128: one quad per lane) ---------
+// Persistent warps walk the edges e = gw, gw + nw, ...; while a warp computes edge e, the seven
+// row quads of its next edge (theta_s, theta_t, theta_r, acc_s, acc_t, dA_dst, dA_src) are already
+// in flight as cp.async copies into the lane's own shared-memory stage (double-buffered), so
+// every warp keeps two edges' random rows outstanding without holding them in registers. The
+// edge's indices, ranks, uniqueness flags and g0 are loaded with its copies (one latency).
+constexpr int CP_ROLES = 7;  // S, T, R, acc_S, acc_T, U (dA dst), W (dA src)
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(tc::smem_addr(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tc::smem_addr(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// quad q of a row (kind layout, see load_quad) -> one float4 slot in shared memory
+__device__ __forceinline__ void cp_quad(float4* dst, const float* row, int kind, uint32_t h, uint32_t q) {
+    if (kind == EMBER_COMPLEX) {
+        cp_async8(dst, row + 2 * q);
+        cp_async8(reinterpret_cast<float*>(dst) + 2, row + h + 2 * q);
+    } else {
+        cp_async16(dst, row + 4 * q);
+    }
+}
+
+// dA quad q of (side, row e), column-blocked [2][d/4][dcap][4]
+__device__ __forceinline__ void cp_dA_quad(float4* dst, const float* dA, uint32_t dcap, uint32_t side, uint32_t e,
+                                           int kind, uint32_t d, uint32_t q) {
+    const float* base = dA + (uint64_t)side * (d / 4) * dcap * 4;
+    auto at = [&](uint32_t c) { return base + ((uint64_t)(c / 4) * dcap + e) * 4 + c % 4; };
+    if (kind == EMBER_COMPLEX) {
+        cp_async8(dst, at(2 * q));
+        cp_async8(reinterpret_cast<float*>(dst) + 2, at(d / 2 + 2 * q));
+    } else {
+        cp_async16(dst, at(4 * q));
+    }
+}
+
+__device__ __forceinline__ Quad quad_of(const float4& v) {
+    Quad x;
+    x.v[0] = v.x, x.v[1] = v.y, x.v[2] = v.z, x.v[3] = v.w;
+    return x;
+}
+
+struct EdgeMeta {
+    uint32_t s, t, ps, pt, pr;
+    uint32_t uq;  // bit 0: source row unique, bit 1: destination row unique
+    float gd, gs;
+};
+
+__global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restrict__ edges, uint32_t nb, uint32_t n_neg,
+                                                      PartView pi, PartView pj, const float* __restrict__ rel,
+                                                      int kind, uint32_t d, const float* __restrict__ dA,
+                                                      uint32_t dcap, const float* __restrict__ g0,
+                                                      const uint32_t* __restrict__ rank,
+                                                      const uint8_t* __restrict__ uniq, float* __restrict__ grows,
+                                                      int direct, float lr, float eps) {
+    extern __shared__ float4 cpbuf[];  // [warps][2 stages][CP_ROLES][32 lanes]
+    const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + wib, nw = gridDim.x * (blockDim.x >> 5);
+    float4* my = cpbuf + (size_t)wib * 2 * CP_ROLES * 32 + lane;
+    const uint32_t h = d / 2, nq = d / 4;
+    const bool ql = lane < nq;
+    auto issue = [&](uint32_t e, int st, EdgeMeta& m) {
+        m.s = edges[3 * e];
+        const uint32_t r = edges[3 * e + 1];
+        m.t = edges[3 * e + 2];
+        m.ps = rank[e];
+        m.pt = rank[nb + e];
+        m.pr = kind != EMBER_DOT ? rank[2 * nb + n_neg + e] : 0u;
+        m.uq = direct ? (uint32_t)uniq[e] | ((uint32_t)uniq[nb + e] << 1) : 0u;
+        m.gd = g0[e];
+        m.gs = g0[(uint64_t)nb + e];
+        if (ql) {
+            float4* b = my + (size_t)st * CP_ROLES * 32;
+            cp_quad(b + 0 * 32, node_row(pi, m.s, d), kind, h, lane);
+            cp_quad(b + 1 * 32, node_row(pj, m.t, d), kind, h, lane);
+            if (kind != EMBER_DOT) cp_quad(b + 2 * 32, rel + (uint64_t)r * d, kind, h, lane);
+            if (m.uq & 1u) cp_quad(b + 3 * 32, pi.acc + (uint64_t)(m.s - pi.first) * d, kind, h, lane);
+            if (m.uq & 2u) cp_quad(b + 4 * 32, pj.acc + (uint64_t)(m.t - pj.first) * d, kind, h, lane);
+            cp_dA_quad(b + 5 * 32, dA, dcap, 0, e, kind, d, lane);
+            cp_dA_quad(b + 6 * 32, dA, dcap, 1, e, kind, d, lane);
+        }
+        cp_commit();
+    };
+    EdgeMeta cur{}, nxt{};
+    if (gw < nb) issue(gw, 0, cur);
+    else cp_commit();
+    uint32_t it = 0;
+    for (uint32_t e = gw; e < nb; e += nw, ++it) {
+        const int st = it & 1;
+        const uint32_t en = e + nw;
+        if (en < nb) issue(en, st ^ 1, nxt);
+        else cp_commit();
+        cp_wait<1>();  // this edge's copies (this lane's own) have landed
+        if (ql) {
+            const float4* b = my + (size_t)st * CP_ROLES * 32;
+            const Quad S = quad_of(b[0]), T = quad_of(b[32]);
+            const Quad R = kind != EMBER_DOT ? quad_of(b[2 * 32]) : S;
+            const Quad U = quad_of(b[5 * 32]), W = quad_of(b[6 * 32]);
+            const float gd = cur.gd, gs = cur.gs;
+            Quad ad, as, oS, oR, oT;
+            adjust_quad(kind, S, R, T, ad, as);
+            if (kind == EMBER_COMPLEX) {
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const float a = S.v[i], bb = S.v[2 + i], c = R.v[i], ee = R.v[2 + i], x = T.v[i], y = T.v[2 + i];
+                    const float u0 = U.v[i] + gd * x, u1 = U.v[2 + i] + gd * y;
+                    const float w0 = W.v[i] + gs * a, w1 = W.v[2 + i] + gs * bb;
+                    oS.v[i] = gs * as.v[i] + (u0 * c + u1 * ee);
+                    oS.v[2 + i] = gs * as.v[2 + i] + (u1 * c - u0 * ee);
+                    oR.v[i] = (u0 * a + u1 * bb) + (w0 * x + w1 * y);
+                    oR.v[2 + i] = (u1 * a - u0 * bb) + (w0 * y - w1 * x);
+                    oT.v[i] = gd * ad.v[i] + (w0 * c - w1 * ee);
+                    oT.v[2 + i] = gd * ad.v[2 + i] + (w0 * ee + w1 * c);
+                }
+            } else if (kind == EMBER_DISTMULT) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float uk = U.v[i] + gd * T.v[i], wk = W.v[i] + gs * S.v[i];
+                    oS.v[i] = gs * as.v[i] + uk * R.v[i];
+                    oR.v[i] = uk * S.v[i] + wk * T.v[i];
+                    oT.v[i] = gd * ad.v[i] + wk * R.v[i];
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    oS.v[i] = gs * T.v[i] + (U.v[i] + gd * T.v[i]);
+                    oT.v[i] = gd * S.v[i] + (W.v[i] + gs * S.v[i]);
+                }
+            }
+            float* thS = pi.theta + (uint64_t)(cur.s - pi.first) * d;
+            float* thT = pj.theta + (uint64_t)(cur.t - pj.first) * d;
+            if (cur.uq & 1u)
+                adagrad_quad(thS, pi.acc + (uint64_t)(cur.s - pi.first) * d, kind, h, lane, S, quad_of(b[3 * 32]), oS,
+                             lr, eps);
+            else
+                store_quad(grows + (uint64_t)cur.ps * d, kind, h, lane, oS);
+            if (cur.uq & 2u)
+                adagrad_quad(thT, pj.acc + (uint64_t)(cur.t - pj.first) * d, kind, h, lane, T, quad_of(b[4 * 32]), oT,
+                             lr, eps);
+            else
+                store_quad(grows + (uint64_t)cur.pt * d, kind, h, lane, oT);
+            if (kind != EMBER_DOT) store_quad(grows + (uint64_t)cur.pr * d, kind, h, lane, oR);
+        }
+        cur = nxt;
+    }
+    cp_wait<0>();
 }
 
 // loss = (1/nb) sum_e (lse_dst - f) + (lse_src - f): each block sums a contiguous range in a fixed
@@ -816,15 +974,29 @@ void launch_keys(const Engine& E, const uint32_t* edges, uint32_t nb, const uint
 }
 
 void launch_rank(const Engine& E, uint32_t n) {
-    k_rank<<<(n + 255) / 256, 256, 0, E.side>>>(E.s.vals_sorted, n, E.s.rank);
+    k_rank<<<(n + 255) / 256, 256, 0, E.side>>>(E.s.vals_sorted, E.s.keys_sorted, n, E.s.rank, E.s.uniq);
     EMBER_LAUNCHED(E);
 }
 
 void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj) {
     const uint32_t warps = 8;
-    k_chain_rule<<<(nb + warps - 1) / warps, warps * 32, 0, E.stream>>>(
-        edges, nb, E.n_neg, pi, pj, E.rel_theta, E.m.kind, E.dim, E.s.dA, E.tc_engine() ? (uint32_t)E.b_cap : 0u,
-        E.s.g0, E.s.rank, E.s.grows, E.s.keys_sorted, E.slots(nb), E.direct_hi ? 1 : 0, E.m.lr, E.m.eps);
+    if (E.tc_engine() && E.dim <= 128 && !getenv("EMBER_CHAIN_PLAIN")) {
+        // persistent pipelined warps: 3 CTAs of 8 warps per SM (shared stages: 8 x 2 x 7 x 512 B)
+        const size_t sm = (size_t)warps * 2 * CP_ROLES * 32 * sizeof(float4);
+        const uint32_t blocks = std::min<uint32_t>((nb + warps - 1) / warps, (uint32_t)E.sm_count * 3);
+        static bool attr = false;
+        if (!attr) {
+            EMBER_CUDA(cudaFuncSetAttribute(k_chain_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            attr = true;
+        }
+        k_chain_pipe<<<blocks, warps * 32, sm, E.stream>>>(edges, nb, E.n_neg, pi, pj, E.rel_theta, E.m.kind, E.dim,
+                                                          E.s.dA, (uint32_t)E.b_cap, E.s.g0, E.s.rank, E.s.uniq,
+                                                          E.s.grows, E.direct_hi ? 1 : 0, E.m.lr, E.m.eps);
+    } else {
+        k_chain_rule<<<(nb + warps - 1) / warps, warps * 32, 0, E.stream>>>(
+            edges, nb, E.n_neg, pi, pj, E.rel_theta, E.m.kind, E.dim, E.s.dA, E.tc_engine() ? (uint32_t)E.b_cap : 0u,
+            E.s.g0, E.s.rank, E.s.grows, E.s.keys_sorted, E.slots(nb), E.direct_hi ? 1 : 0, E.m.lr, E.m.eps);
+    }
     EMBER_LAUNCHED(E);
 }
 
