@@ -791,6 +791,90 @@ __global__ void __launch_bounds__(256, 4) k_segments(SegArgs a) {
     }
 }
 
+// Persistent version for d <= 128: each 16-lane half-warp walks the unique keys u = gh, gh + nh, ...
+// and, while it sums the current key's rows, the next key's theta / acc quads are already in
+// flight (cp.async into the lane's own stage), so the random parameter reads of two keys overlap.
+// Same arithmetic and order as k_segments (bit-identical results).
+struct SegKey {
+    uint32_t u, off, cnt;
+    bool active;
+    SegTarget t;
+};
+
+__global__ void __launch_bounds__(256, 4) k_segments_pipe(SegArgs a) {
+    extern __shared__ float4 sst[];  // [warps][2 halves][2 stages][2 roles][2 column blocks][16 lanes]
+    const uint32_t lane = threadIdx.x & 31, hl = lane & (SEG_LANES - 1), half = lane >> 4, wib = threadIdx.x >> 5;
+    const uint32_t gh = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 2 + half;
+    const uint32_t nh = ((gridDim.x * blockDim.x) >> 5) * 2;
+    const uint32_t hmask = half == 0 ? 0x0000ffffu : 0xffff0000u;
+    const uint32_t nr = *a.nruns, d4 = a.d / 4;
+    float4* my = sst + (size_t)(wib * 2 + half) * 2 * 2 * 2 * SEG_LANES + hl;
+    auto slot = [&](int st, int role, int cb) { return my + (size_t)((st * 2 + role) * 2 + cb) * SEG_LANES; };
+    auto issue = [&](uint32_t u, int st, SegKey& k) {
+        k.u = u;
+        k.active = false;
+        if (u < nr) {
+            const uint32_t key = a.ukeys[u];
+            if (hl == 0 && key < a.ks.node_range && (u + 1 == nr || a.ukeys[u + 1] >= a.ks.node_range)) {
+                a.nunique[0] = u + 1;
+                a.nunique[1] = nr - (u + 1);
+            }
+            k.off = a.offsets[u];
+            k.cnt = a.counts[u];
+            const bool done = k.cnt == 1 && key < a.ks.node_range && a.vals_sorted[k.off] < a.direct_hi;
+            if (!done && k.cnt > LONG_SEG) {  // reserve chunk slots for the long path
+                const uint32_t nch = (k.cnt + LONG_CHUNK - 1) / LONG_CHUNK;
+                uint32_t li = 0, base = 0;
+                if (hl == 0) {
+                    li = atomicAdd(&a.longs[0], 1u);
+                    base = atomicAdd(&a.longs[1], nch);
+                    uint32_t* rec = a.longs + 2 + 3 * li;
+                    rec[0] = u;
+                    rec[1] = base;
+                    rec[2] = nch;
+                }
+                li = __shfl_sync(hmask, li, 0, SEG_LANES);
+                base = __shfl_sync(hmask, base, 0, SEG_LANES);
+                for (uint32_t c = hl; c < nch; c += SEG_LANES) a.owner[base + c] = li;
+            } else if (!done) {
+                k.active = true;
+                k.t = seg_target(a, u, nr, hl == 0);
+                if (seg_applies(a, k.t))
+                    for (int cb = 0; cb < 2; ++cb) {
+                        const uint32_t c4 = hl + cb * SEG_LANES;
+                        if (c4 < d4) {
+                            cp_async16(slot(st, 0, cb), k.t.th + 4 * c4);
+                            cp_async16(slot(st, 1, cb), k.t.ac + 4 * c4);
+                        }
+                    }
+            }
+        }
+        cp_commit();
+    };
+    SegKey cur, nxt;
+    issue(gh, 0, cur);
+    for (uint32_t u = gh, it = 0; u < nr; u += nh, ++it) {
+        const int st = it & 1;
+        issue(u + nh, st ^ 1, nxt);
+        cp_wait<1>();
+        if (cur.active) {
+            const bool app = seg_applies(a, cur.t);
+            const float* base = a.rows + (uint64_t)cur.off * a.d;
+            const uint32_t c4 = hl, c4b = hl + SEG_LANES;
+            const bool hasa = c4 < d4, hasb = c4b < d4;
+            if (hasa) {
+                float4 ga, gb;
+                sum_rows2(base, cur.cnt, a.d, c4, c4b, hasb, ga, gb);
+                const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+                seg_finish(a, cur.t, c4, ga, app ? *slot(st, 0, 0) : z, app ? *slot(st, 1, 0) : z);
+                if (hasb) seg_finish(a, cur.t, c4b, gb, app ? *slot(st, 0, 1) : z, app ? *slot(st, 1, 1) : z);
+            }
+        }
+        cur = nxt;
+    }
+    cp_wait<0>();
+}
+
 // Sum of rows r = r0, r0 + step, ... < cnt at column block c4, 4 loads in flight, in row order.
 __device__ __forceinline__ float4 sum_rows_strided(const float* base, uint32_t r0, uint32_t step, uint32_t cnt,
                                                    uint32_t d, uint32_t c4) {
@@ -1035,7 +1119,18 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
     a.node_rows_out = node_rows_out;
     a.rel_ids_out = rel_ids_out;
     a.rel_rows_out = rel_rows_out;
-    k_segments<<<(n_slots * 16 + 255) / 256, 256, 0, E.stream>>>(a);  // 2 keys per warp
+    if (E.dim <= 128 && !getenv("EMBER_SEG_PLAIN")) {  // persistent, pipelined (A/B: EMBER_SEG_PLAIN=1)
+        const size_t sm = (size_t)8 * 2 * 2 * 2 * 2 * SEG_LANES * sizeof(float4);
+        static bool attr = false;
+        if (!attr) {
+            EMBER_CUDA(cudaFuncSetAttribute(k_segments_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            attr = true;
+        }
+        const uint32_t blocks = std::min<uint32_t>((n_slots + 15) / 16, (uint32_t)E.sm_count * 4);
+        k_segments_pipe<<<blocks, 256, sm, E.stream>>>(a);
+    } else {
+        k_segments<<<(n_slots * 16 + 255) / 256, 256, 0, E.stream>>>(a);  // 2 keys per warp
+    }
     EMBER_LAUNCHED(E);
     k_long_partial<<<2 * E.sm_count, 256, 0, E.stream>>>(a);
     EMBER_LAUNCHED(E);
