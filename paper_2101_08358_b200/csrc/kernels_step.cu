@@ -928,14 +928,18 @@ __global__ void k_long_partial(SegArgs a) {
 // One block per long segment: 2 * LONG_WARPS half-warp streams each add the chunk partials
 // c = stream, stream + 2 LONG_WARPS, ... (in order); warp 0 then adds the stream sums in stream
 // order (a fixed two-level order: deterministic) and applies Adagrad / export.
+constexpr uint32_t LONG_BIG = 8;  // long segments with more chunk partials than this get a whole block
+
 __global__ void __launch_bounds__(32 * LONG_WARPS) k_long_final(SegArgs a) {
     extern __shared__ float4 wsum[];  // [2 * LONG_WARPS][d/4]
     const uint32_t lane = threadIdx.x & 31, hl = lane & 15, stream = threadIdx.x >> 4, d4 = a.d / 4;
     const uint32_t NS = 2 * LONG_WARPS;
     const uint32_t n_long = *(volatile uint32_t*)&a.longs[0], nr = *a.nruns;
+    // big segments (hot relations): a block each, 2 LONG_WARPS half-warp streams
     for (uint32_t li = blockIdx.x; li < n_long; li += gridDim.x) {
         const uint32_t* rec = a.longs + 2 + 3 * li;
         const uint32_t u = rec[0], base = rec[1], nch = rec[2];
+        if (nch <= LONG_BIG) continue;  // block-uniform
         for (uint32_t c4 = hl; c4 < d4; c4 += 16)
             wsum[stream * d4 + c4] = sum_rows_strided(a.partial + (uint64_t)base * a.d, stream, NS, nch, a.d, c4);
         __syncthreads();
@@ -954,6 +958,29 @@ __global__ void __launch_bounds__(32 * LONG_WARPS) k_long_final(SegArgs a) {
             }
         }
         __syncthreads();
+    }
+    // the many small ones: a warp each (even / odd chunk streams, then their sum)
+    const uint32_t half = lane >> 4, nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < n_long; li += nw) {
+        const uint32_t* rec = a.longs + 2 + 3 * li;
+        const uint32_t u = rec[0], base = rec[1], nch = rec[2];
+        if (nch > LONG_BIG) continue;  // warp-uniform
+        const SegTarget t = seg_target(a, u, nr, lane == 0);
+        const bool app = seg_applies(a, t);
+        for (uint32_t c0 = 0; c0 < d4; c0 += 16) {  // warp-uniform trip count (shuffles below)
+            const uint32_t c4 = c0 + hl;
+            float4 th = make_float4(0.f, 0.f, 0.f, 0.f), ac = th;
+            if (app && half == 0 && c4 < d4) {
+                th = reinterpret_cast<const float4*>(t.th)[c4];
+                ac = reinterpret_cast<const float4*>(t.ac)[c4];
+            }
+            float4 g = c4 < d4 ? sum_rows_strided(a.partial + (uint64_t)base * a.d, half, 2, nch, a.d, c4) : th;
+            const float4 o = shfl_xor4(g, 16);
+            if (half == 0 && c4 < d4) {
+                add4(g, o);
+                seg_finish(a, t, c4, g, th, ac);
+            }
+        }
     }
 }
 
