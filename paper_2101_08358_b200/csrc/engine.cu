@@ -65,6 +65,7 @@ NcclApi& nccl() {
 }
 
 __global__ void k_adagrad_dense(float* th, float* ac, const float* g, uint64_t n, float lr, float eps) {
+    griddep_wait();
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const float gi = g[i];
@@ -81,6 +82,14 @@ bool getenv_direct() {
 }
 
 }  // namespace
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* v = getenv("EMBER_PDL");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
 
 Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, cudaStream_t st)
     : device(dev), m(md), g(gd) {
@@ -313,7 +322,8 @@ void Engine::apply_relations_dense(const float* grad) {
     if (m.kind == EMBER_DOT) return;
     if (!rel_theta || !rel_acc) throw ConfigError("relation table not bound");
     const uint64_t rn = (uint64_t)g.num_relations * dim;
-    k_adagrad_dense<<<(unsigned)((rn + 255) / 256), 256, 0, stream>>>(rel_theta, rel_acc, grad, rn, m.lr, m.eps);
+    launch_pdl(k_adagrad_dense, dim3((unsigned)((rn + 255) / 256)), dim3(256), 0, stream, rel_theta, rel_acc, grad, rn,
+               m.lr, m.eps);
     EMBER_LAUNCHED(*this);
 }
 

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "ember/common.h"
@@ -193,6 +194,31 @@ struct Engine {
 };
 
 enum Phase { PHASE_SAMPLE = 0, PHASE_GATHER = 1, PHASE_CONTRACT = 2, PHASE_CHAIN = 3, PHASE_REDUCE = 4, PHASE_END = 5 };
+
+// Programmatic dependent launch (PDL) on the step stream: a kernel's CTAs may be scheduled while
+// the previous kernel drains; every kernel launched this way starts (after its own set-up) with
+// griddep_wait(), which returns once the previous grid has completed and its writes are visible.
+// EMBER_PDL=0 launches them as ordinary stream-ordered kernels (A/B).
+__device__ __forceinline__ void griddep_wait() {
+#if defined(__CUDA_ARCH__)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    EMBER_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 // kernel launchers (kernels_step.cu, gemm_simt.cu, tc_score.cu, graph.cu)
 void launch_sample(const Engine& E, uint32_t* out, uint64_t base_seed, const uint32_t* bucket, uint64_t bucket_n,

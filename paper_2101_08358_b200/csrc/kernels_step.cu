@@ -29,6 +29,7 @@ __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpre
 __global__ void k_sample(uint32_t* out, uint32_t nt, uint32_t n_deg, uint32_t total, uint64_t base,
                          const uint32_t* __restrict__ bucket, uint64_t bucket_n, uint64_t src_first, uint64_t src_rows,
                          uint64_t dst_first, uint64_t dst_rows) {
+    griddep_wait();
     const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
     if (slot >= total) return;
     const uint32_t k = slot % nt;
@@ -118,6 +119,7 @@ __global__ void __launch_bounds__(32 * GP_WARPS) k_gather_pack(const uint32_t* _
                                                                PartView pi, PartView pj, const float* __restrict__ rel,
                                                                int kind, uint32_t d, uint32_t CB, uint32_t cap,
                                                                uint16_t* __restrict__ Apk, float* __restrict__ fpos) {
+    griddep_wait();
     extern __shared__ uint4 gsm[];
     uint4* tile = gsm;  // [2][2CB][GP_ROWS]
     const uint32_t kp = 8 * CB, nblk = 4 * CB;
@@ -204,6 +206,7 @@ __global__ void k_gather_adjust(const uint32_t* __restrict__ edges, uint32_t nb,
 template <bool PACKED>
 __global__ void k_gather_negs(const uint32_t* __restrict__ negs, uint32_t n, uint32_t nt, uint32_t n_pad, PartView pi,
                               PartView pj, uint32_t d, uint32_t CB, float* __restrict__ N, uint16_t* __restrict__ Npk) {
+    griddep_wait();
     const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (!PACKED) {
         if (w >= n) return;
@@ -445,6 +448,7 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
                                                       const uint32_t* __restrict__ rank,
                                                       const uint8_t* __restrict__ uniq, float* __restrict__ grows,
                                                       int direct, float lr, float eps) {
+    griddep_wait();
     extern __shared__ float4 cpbuf[];  // [warps][2 stages][CP_ROLES][32 lanes]
     const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + wib, nw = gridDim.x * (blockDim.x >> 5);
@@ -543,6 +547,7 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
 constexpr uint32_t LOSS_THREADS = 512;
 __global__ void k_loss(const float* __restrict__ lse, const float* __restrict__ fpos, uint32_t nb, uint32_t per_block,
                        double* __restrict__ part, uint32_t* __restrict__ done, float* __restrict__ out) {
+    griddep_wait();
     __shared__ double red[LOSS_THREADS];
     __shared__ bool last;
     const uint32_t b0 = blockIdx.x * per_block, b1 = min(nb, b0 + per_block);
@@ -802,6 +807,7 @@ struct SegKey {
 };
 
 __global__ void __launch_bounds__(256, 4) k_segments_pipe(SegArgs a) {
+    griddep_wait();
     extern __shared__ float4 sst[];  // [warps][2 halves][2 stages][2 roles][2 column blocks][16 lanes]
     const uint32_t lane = threadIdx.x & 31, hl = lane & (SEG_LANES - 1), half = lane >> 4, wib = threadIdx.x >> 5;
     const uint32_t gh = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 2 + half;
@@ -905,6 +911,7 @@ __device__ __forceinline__ float4 shfl_xor4(float4 v, int m) {
 // One warp per chunk slot of the long segments: partial[slot] = sum of its <= LONG_CHUNK rows;
 // the two half-warps take the even and the odd rows, then even + odd (fixed order).
 __global__ void k_long_partial(SegArgs a) {
+    griddep_wait();
     const uint32_t lane = threadIdx.x & 31, hl = lane & 15, half = lane >> 4;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5, d4 = a.d / 4;
     const uint32_t n_slots = *(volatile uint32_t*)&a.longs[1];
@@ -931,6 +938,7 @@ __global__ void k_long_partial(SegArgs a) {
 constexpr uint32_t LONG_BIG = 8;  // long segments with more chunk partials than this get a whole block
 
 __global__ void __launch_bounds__(32 * LONG_WARPS) k_long_final(SegArgs a) {
+    griddep_wait();
     extern __shared__ float4 wsum[];  // [2 * LONG_WARPS][d/4]
     const uint32_t lane = threadIdx.x & 31, hl = lane & 15, stream = threadIdx.x >> 4, d4 = a.d / 4;
     const uint32_t NS = 2 * LONG_WARPS;
@@ -1040,8 +1048,8 @@ void launch_sample(const Engine& E, uint32_t* out, uint64_t base, const uint32_t
     const uint32_t n_deg = (uint32_t)ceil((double)E.m.alpha * (double)E.nt);
     const uint32_t total = E.n_neg;
     if (!total) return;
-    k_sample<<<(total + 255) / 256, 256, 0, E.stream>>>(out, E.nt, n_deg, total, base, bucket, bucket_n, src.first,
-                                                         src.rows, dst.first, dst.rows);
+    launch_pdl(k_sample, dim3((total + 255) / 256), dim3(256), 0, E.stream, out, E.nt, n_deg, total, base, bucket,
+               bucket_n, src.first, src.rows, dst.first, dst.rows);
     EMBER_LAUNCHED(E);
 }
 
@@ -1055,8 +1063,8 @@ void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, c
             EMBER_CUDA(cudaFuncSetAttribute(k_gather_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_cap()));
             attr = true;
         }
-        k_gather_pack<<<rows_pad / GP_ROWS, 32 * GP_WARPS, sm, E.stream>>>(edges, nb, pi, pj, E.rel_theta, E.m.kind,
-                                                                           E.dim, E.CB, E.b_cap, E.s.Apk, E.s.fpos);
+        launch_pdl(k_gather_pack, dim3(rows_pad / GP_ROWS), dim3(32 * GP_WARPS), sm, E.stream, edges, nb, pi, pj,
+                   E.rel_theta, E.m.kind, E.dim, E.CB, (uint32_t)E.b_cap, E.s.Apk, E.s.fpos);
     } else {
         const uint32_t warps = 8;
         k_gather_adjust<<<(nb + warps - 1) / warps, warps * 32, 0, E.stream>>>(edges, nb, pi, pj, E.rel_theta,
@@ -1070,8 +1078,8 @@ void launch_gather_negatives(const Engine& E, const uint32_t* negs, const PartVi
     if (!E.n_neg) return;
     const uint32_t warps = packed ? 2 * E.n_pad : E.n_neg;
     if (packed)
-        k_gather_negs<true><<<(warps * 32 + 255) / 256, 256, 0, E.stream>>>(negs, E.n_neg, E.nt, E.n_pad, pi, pj, E.dim,
-                                                                            E.CB, nullptr, E.s.Npk);
+        launch_pdl(k_gather_negs<true>, dim3((warps * 32 + 255) / 256), dim3(256), 0, E.stream, negs, E.n_neg, E.nt,
+                   (uint32_t)E.n_pad, pi, pj, E.dim, E.CB, (float*)nullptr, E.s.Npk);
     else
         k_gather_negs<false><<<(warps * 32 + 255) / 256, 256, 0, E.stream>>>(negs, E.n_neg, E.nt, 0, pi, pj, E.dim, 0,
                                                                              E.s.N, nullptr);
@@ -1100,9 +1108,10 @@ void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, cons
             EMBER_CUDA(cudaFuncSetAttribute(k_chain_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             attr = true;
         }
-        k_chain_pipe<<<blocks, warps * 32, sm, E.stream>>>(edges, nb, E.n_neg, pi, pj, E.rel_theta, E.m.kind, E.dim,
-                                                          E.s.dA, (uint32_t)E.b_cap, E.s.g0, E.s.rank, E.s.uniq,
-                                                          E.s.grows, E.direct_hi ? 1 : 0, E.m.lr, E.m.eps);
+        launch_pdl(k_chain_pipe, dim3(blocks), dim3(warps * 32), sm, E.stream, edges, nb, E.n_neg, pi, pj,
+                   (const float*)E.rel_theta, E.m.kind, E.dim, (const float*)E.s.dA, (uint32_t)E.b_cap,
+                   (const float*)E.s.g0, (const uint32_t*)E.s.rank, (const uint8_t*)E.s.uniq, E.s.grows,
+                   E.direct_hi ? 1 : 0, E.m.lr, E.m.eps);
     } else {
         k_chain_rule<<<(nb + warps - 1) / warps, warps * 32, 0, E.stream>>>(
             edges, nb, E.n_neg, pi, pj, E.rel_theta, E.m.kind, E.dim, E.s.dA, E.tc_engine() ? (uint32_t)E.b_cap : 0u,
@@ -1114,8 +1123,8 @@ void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, cons
 void launch_loss(const Engine& E, uint32_t nb, float* loss_out) {
     const uint32_t per = LOSS_THREADS;  // ~100 blocks at b = 5e4: latency, not bandwidth
     const uint32_t blocks = (nb + per - 1) / per;
-    k_loss<<<blocks, LOSS_THREADS, 0, E.stream>>>(E.s.lse, E.s.fpos, nb, per, reinterpret_cast<double*>(E.s.loss_part),
-                                                 E.s.loss_done, loss_out);
+    launch_pdl(k_loss, dim3(blocks), dim3(LOSS_THREADS), 0, E.stream, (const float*)E.s.lse, (const float*)E.s.fpos, nb,
+               per, reinterpret_cast<double*>(E.s.loss_part), E.s.loss_done, loss_out);
     EMBER_LAUNCHED(E);
 }
 
@@ -1154,14 +1163,15 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
             attr = true;
         }
         const uint32_t blocks = std::min<uint32_t>((n_slots + 15) / 16, (uint32_t)E.sm_count * 4);
-        k_segments_pipe<<<blocks, 256, sm, E.stream>>>(a);
+        launch_pdl(k_segments_pipe, dim3(blocks), dim3(256), sm, E.stream, a);
     } else {
         k_segments<<<(n_slots * 16 + 255) / 256, 256, 0, E.stream>>>(a);  // 2 keys per warp
     }
     EMBER_LAUNCHED(E);
-    k_long_partial<<<2 * E.sm_count, 256, 0, E.stream>>>(a);
+    launch_pdl(k_long_partial, dim3(2 * E.sm_count), dim3(256), 0, E.stream, a);
     EMBER_LAUNCHED(E);
-    k_long_final<<<E.sm_count, 32 * LONG_WARPS, 2 * LONG_WARPS * E.dim * sizeof(float), E.stream>>>(a);
+    launch_pdl(k_long_final, dim3(E.sm_count), dim3(32 * LONG_WARPS), 2 * LONG_WARPS * E.dim * sizeof(float), E.stream,
+               a);
     EMBER_LAUNCHED(E);
 }
 

@@ -311,6 +311,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // column 0: the MMA issuer uses compile-time TMEM addresses.
     const uint32_t tbase = *tslot;
     if (tbase != 0) __trap();
+    griddep_wait();  // set-up above overlaps the previous kernel's tail (PDL)
 
     if (warp == 0) {
         if (lane == 0) {  // ------------------------------------------------------ TMA producer
@@ -541,6 +542,7 @@ __device__ __forceinline__ float packed_at(const uint16_t* pk, int cap, int CB, 
 }
 
 __global__ void k_tc_fixup(TcArgs g, const uint16_t* __restrict__ Apk, const uint16_t* __restrict__ Npk) {
+    griddep_wait();
     const uint32_t n = *(volatile uint32_t*)g.flags;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (uint32_t f = warp; f < n; f += nw) {
@@ -596,6 +598,7 @@ __global__ void k_tc_fixup(TcArgs g, const uint16_t* __restrict__ Apk, const uin
 // column-blocked partials [chunk][side][d/4][n_pad] float4 are read coalesced along n.
 __global__ void k_dn_reduce(const float4* __restrict__ part, int chunks, int nt, int n_pad, int d,
                             const uint32_t* __restrict__ rank, uint32_t slot0, float* __restrict__ out) {
+    griddep_wait();
     const int d4 = d / 4;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= (int64_t)2 * d4 * nt) return;
@@ -768,6 +771,8 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
         EMBER_CUDA(cudaMemsetAsync(t.trace, 0, (size_t)2 * 5 * TRACE_ROLE * 8, E.stream));
         a.trace = t.trace;
     }
+    // the persistent contraction kernels are launched stream-ordered (not PDL): early-resident CTAs
+    // waiting on the previous kernel would keep the helper stream's sort off those SMs
     k_tc<MODE_ROWS><<<std::min(items1, gmax), NTHREADS, smem_total(t.KP, t.nstage, MODE_ROWS), E.stream>>>(
         t.mA128, t.mN96, a);
     EMBER_LAUNCHED(E);
@@ -775,7 +780,7 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
         dump(".rows.bin");
         EMBER_CUDA(cudaMemsetAsync(t.trace, 0, (size_t)2 * 5 * TRACE_ROLE * 8, E.stream));
     }
-    k_tc_fixup<<<1, 1024, 0, E.stream>>>(a, s.Apk, s.Npk);
+    launch_pdl(k_tc_fixup, dim3(1), dim3(1024), 0, E.stream, a, (const uint16_t*)s.Apk, (const uint16_t*)s.Npk);
     EMBER_LAUNCHED(E);
     const int items2 = 2 * ((nt + RES - 1) / RES) * a.chunks2;
     k_tc<MODE_NEGS><<<std::min(items2, gmax), NTHREADS, smem_total(t.KP, t.nstage, MODE_NEGS), E.stream>>>(
@@ -784,8 +789,9 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
     if (tr) dump(".negs.bin");
     const int64_t r = (int64_t)2 * nt * (d / 4);
     E.join_sorted();
-    k_dn_reduce<<<(unsigned)((r + 255) / 256), 256, 0, E.stream>>>(
-        reinterpret_cast<const float4*>(t.dN_part), a.chunks2, nt, t.n_pad, d, s.rank, 2 * nb, s.grows);
+    launch_pdl(k_dn_reduce, dim3((unsigned)((r + 255) / 256)), dim3(256), 0, E.stream,
+               reinterpret_cast<const float4*>(t.dN_part), a.chunks2, nt, t.n_pad, d, (const uint32_t*)s.rank, 2 * nb,
+               s.grows);
     EMBER_LAUNCHED(E);
 }
 
