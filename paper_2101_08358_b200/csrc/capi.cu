@@ -241,6 +241,7 @@ int ember_loss_and_grad(ember_ctx* ctx, const uint32_t* edges, uint32_t nb, uint
         need(negs, "negs_dev");
         if (nb == 0 || nb > E.cap_b) throw ConfigError("batch size must be in [1, batch_size]");
         E.check_bucket(i, j);
+        E.loss_target = E.s.loss;
         E.forward_backward(edges, nb, i, j, negs);
         launch_loss(E, nb, E.s.loss);
         if (fpos) EMBER_CUDA(cudaMemcpyAsync(fpos, E.s.fpos, nb * sizeof(float), cudaMemcpyDeviceToDevice, E.stream));

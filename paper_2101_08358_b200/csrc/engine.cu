@@ -155,7 +155,8 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     s.dA = dalloc<float>(2 * (uint64_t)std::max<uint64_t>(b, (uint64_t)pad_rows(cap_b)) * d);
     s.grows = dalloc<float>((uint64_t)cap_rows * d);
     s.loss = dalloc<float>(1);
-    s.loss_part = reinterpret_cast<float*>(dalloc<double>(b / 512 + 2));  // one per k_loss block
+    // one per k_loss block, or one per warp of the fused chain rule (<= 3 x 8 warps per SM)
+    s.loss_part = reinterpret_cast<float*>(dalloc<double>(std::max<uint64_t>(b / 512 + 2, 24ull * sm_count + 32)));
     s.loss_done = dalloc<uint32_t>(1);
     EMBER_CUDA(cudaMemset(s.loss_done, 0, sizeof(uint32_t)));
     s.keys = dalloc<uint32_t>(cap_rows);
@@ -289,7 +290,7 @@ void Engine::forward_backward(const uint32_t* edges, uint32_t nb, uint32_t i, ui
     const PartView pi = view(i), pj = view(j);
     sort_keys(edges, nb, i, j, negs);  // helper stream, overlapped with the gathers and the contraction
     mark(PHASE_GATHER);
-    launch_gather_adjust(*this, edges, nb, pi, pj, tc_engine());
+    launch_gather_adjust(*this, edges, nb, pi, pj, tc_engine(), negs);
     launch_gather_negatives(*this, negs, pi, pj, tc_engine());
     mark(PHASE_CONTRACT);
     if (tc_engine())
@@ -365,6 +366,7 @@ void Engine::step(const uint32_t* edges, uint32_t nb, const uint32_t* bucket, ui
     mark(PHASE_SAMPLE);
     sample(bucket, bucket_n, i, j, epoch, bucket_step, batch_in_bucket, s.negs);
     direct_hi = getenv_direct() ? 2 * nb : 0;
+    loss_target = loss_out ? loss_out : s.loss;
     forward_backward(edges, nb, i, j, s.negs);
     launch_loss(*this, nb, loss_out ? loss_out : s.loss);
     mark(PHASE_REDUCE);

@@ -145,6 +145,9 @@ struct Engine {
     // right in the chain rule (slots < direct_hi = 2nb); 0: every row goes through the segmented
     // reduction.
     uint32_t direct_hi = 0;
+    // where the step's loss goes; the tensor-core chain rule reduces it there itself (loss_fused)
+    float* loss_target = nullptr;
+    mutable bool loss_fused = false;
     // profiling: CUDA events at phase boundaries on the step stream + our own kernel launches
     bool prof_on = false;
     std::vector<std::pair<int, cudaEvent_t>> prof_events;
@@ -225,7 +228,7 @@ void launch_sample(const Engine& E, uint32_t* out, uint64_t base_seed, const uin
                    const PartView& src, const PartView& dst);
 // packed: write the tensor-core engine's bf16 hi|lo operands (Apk/Npk), else fp32 A / N.
 void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj,
-                          bool packed);
+                          bool packed, const uint32_t* negs);
 void launch_gather_negatives(const Engine& E, const uint32_t* negs, const PartView& pi, const PartView& pj, bool packed);
 void launch_keys(const Engine& E, const uint32_t* edges, uint32_t nb, const uint32_t* negs, const KeySpace& ks);
 void launch_rank(const Engine& E, uint32_t n);

@@ -104,6 +104,29 @@ __device__ __forceinline__ void adjust_quad(int kind, const Quad& S, const Quad&
     }
 }
 
+// Packed negative row w of [2 sides][n_pad] (side 0 rows from partition j, side 1 from i; zero past
+// n_t): lane < CB splits 8 coordinates into bf16 hi|lo core-matrix rows of Npk.
+__device__ __forceinline__ void negs_pack_warp(uint32_t w, uint32_t lane, const uint32_t* __restrict__ negs,
+                                               uint32_t nt, uint32_t n_pad, const PartView& pi, const PartView& pj,
+                                               uint32_t d, uint32_t CB, uint16_t* __restrict__ Npk) {
+    if (w >= 2 * n_pad || lane >= CB) return;
+    const uint32_t side = w / n_pad, slot = w % n_pad;
+    float x[8];
+    if (slot < nt) {
+        const float* src = node_row(side == 0 ? pj : pi, negs[side * nt + slot], d);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = 8 * lane + i < d ? __ldg(src + 8 * lane + i) : 0.f;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = 0.f;
+    }
+    uint4 h, l;
+    tc::split8(x, h, l);
+    uint4* P = reinterpret_cast<uint4*>(Npk);
+    P[((uint64_t)side * 2 * CB + lane) * n_pad + slot] = h;
+    P[((uint64_t)side * 2 * CB + CB + lane) * n_pad + slot] = l;
+}
+
 // Edges per CTA of the packed gather: one 512-byte run per column block (the TMA box row group).
 constexpr uint32_t GP_ROWS = 32, GP_WARPS = 8;
 
@@ -118,8 +141,15 @@ constexpr uint32_t GP_ROWS = 32, GP_WARPS = 8;
 __global__ void __launch_bounds__(32 * GP_WARPS) k_gather_pack(const uint32_t* __restrict__ edges, uint32_t nb,
                                                                PartView pi, PartView pj, const float* __restrict__ rel,
                                                                int kind, uint32_t d, uint32_t CB, uint32_t cap,
-                                                               uint16_t* __restrict__ Apk, float* __restrict__ fpos) {
+                                                               uint16_t* __restrict__ Apk, float* __restrict__ fpos,
+                                                               uint32_t row_ctas, const uint32_t* __restrict__ negs,
+                                                               uint32_t nt, uint32_t n_pad, uint16_t* __restrict__ Npk) {
     griddep_wait();
+    if (blockIdx.x >= row_ctas) {  // the trailing CTAs pack the shared negatives (one warp per row)
+        const uint32_t w = (blockIdx.x - row_ctas) * GP_WARPS + (threadIdx.x >> 5);
+        negs_pack_warp(w, threadIdx.x & 31, negs, nt, n_pad, pi, pj, d, CB, Npk);
+        return;
+    }
     extern __shared__ uint4 gsm[];
     uint4* tile = gsm;  // [2][2CB][GP_ROWS]
     const uint32_t kp = 8 * CB, nblk = 4 * CB;
@@ -216,22 +246,7 @@ __global__ void k_gather_negs(const uint32_t* __restrict__ negs, uint32_t n, uin
         for (uint32_t v = lane; v < d / 4; v += 32) dst[v] = ldg4(src + 4 * v);
         return;
     }
-    if (w >= 2 * n_pad || lane >= CB) return;
-    const uint32_t side = w / n_pad, slot = w % n_pad;
-    float x[8];
-    if (slot < nt) {
-        const float* src = node_row(side == 0 ? pj : pi, negs[side * nt + slot], d);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) x[i] = 8 * lane + i < d ? __ldg(src + 8 * lane + i) : 0.f;
-    } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) x[i] = 0.f;
-    }
-    uint4 h, l;
-    tc::split8(x, h, l);
-    uint4* P = reinterpret_cast<uint4*>(Npk);
-    P[((uint64_t)side * 2 * CB + lane) * n_pad + slot] = h;
-    P[((uint64_t)side * 2 * CB + CB + lane) * n_pad + slot] = l;
+    negs_pack_warp(w, lane, negs, nt, n_pad, pi, pj, d, CB, Npk);
 }
 
 __device__ __forceinline__ uint32_t node_key(const KeySpace& ks, uint32_t id) {
@@ -439,6 +454,7 @@ struct EdgeMeta {
     uint32_t s, t, ps, pt, pr;
     uint32_t uq;  // bit 0: source row unique, bit 1: destination row unique
     float gd, gs;
+    float lterm;  // the edge's loss term (lse_dst - f) + (lse_src - f)
 };
 
 __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restrict__ edges, uint32_t nb, uint32_t n_neg,
@@ -447,7 +463,10 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
                                                       uint32_t dcap, const float* __restrict__ g0,
                                                       const uint32_t* __restrict__ rank,
                                                       const uint8_t* __restrict__ uniq, float* __restrict__ grows,
-                                                      int direct, float lr, float eps) {
+                                                      int direct, float lr, float eps,
+                                                      const float* __restrict__ lse, const float* __restrict__ fpos,
+                                                      double* __restrict__ loss_part, uint32_t* __restrict__ loss_done,
+                                                      float* __restrict__ loss_out) {
     griddep_wait();
     extern __shared__ float4 cpbuf[];  // [warps][2 stages][CP_ROLES][32 lanes]
     const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -465,6 +484,11 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
         m.uq = direct ? (uint32_t)uniq[e] | ((uint32_t)uniq[nb + e] << 1) : 0u;
         m.gd = g0[e];
         m.gs = g0[(uint64_t)nb + e];
+        {
+            const float f = fpos[e];
+            m.lterm = 0.f;
+            if (lane == 0) m.lterm = (lse[e] - f) + (lse[(uint64_t)nb + e] - f);  // same terms as k_loss
+        }
         if (ql) {
             float4* b = my + (size_t)st * CP_ROLES * 32;
             cp_quad(b + 0 * 32, node_row(pi, m.s, d), kind, h, lane);
@@ -481,7 +505,9 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
     if (gw < nb) issue(gw, 0, cur);
     else cp_commit();
     uint32_t it = 0;
+    double lacc = 0.0;  // lane 0: this warp's loss terms, in its (fixed) edge order
     for (uint32_t e = gw; e < nb; e += nw, ++it) {
+        lacc += (double)cur.lterm;
         const int st = it & 1;
         const uint32_t en = e + nw;
         if (en < nb) issue(en, st ^ 1, nxt);
@@ -540,6 +566,24 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
         cur = nxt;
     }
     cp_wait<0>();
+    // the loss (replaces k_loss): per-warp partials in warp order, summed by the last warp to finish
+    // in a fixed lane / tree order (deterministic)
+    __shared__ bool last_warp[8];
+    if (lane == 0) {
+        loss_part[gw] = lacc;
+        __threadfence();
+        last_warp[wib] = atomicAdd(loss_done, 1u) == nw - 1;
+    }
+    __syncwarp();
+    if (!last_warp[wib]) return;
+    __threadfence();
+    double v = 0.0;
+    for (uint32_t k = lane; k < nw; k += 32) v += ((volatile double*)loss_part)[k];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) {
+        loss_out[0] = (float)(v / (double)nb);
+        *loss_done = 0u;
+    }
 }
 
 // loss = (1/nb) sum_e (lse_dst - f) + (lse_src - f): each block sums a contiguous range in a fixed
@@ -1054,7 +1098,7 @@ void launch_sample(const Engine& E, uint32_t* out, uint64_t base, const uint32_t
 }
 
 void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj,
-                          bool packed) {
+                          bool packed, const uint32_t* negs) {
     if (packed) {
         const uint32_t rows_pad = (uint32_t)Engine::pad_rows(nb);  // a multiple of GP_ROWS
         const size_t sm = (size_t)4 * E.CB * GP_ROWS * 16 + (size_t)GP_WARPS * 2 * E.KP * sizeof(float);
@@ -1063,8 +1107,10 @@ void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, c
             EMBER_CUDA(cudaFuncSetAttribute(k_gather_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_cap()));
             attr = true;
         }
-        launch_pdl(k_gather_pack, dim3(rows_pad / GP_ROWS), dim3(32 * GP_WARPS), sm, E.stream, edges, nb, pi, pj,
-                   E.rel_theta, E.m.kind, E.dim, E.CB, (uint32_t)E.b_cap, E.s.Apk, E.s.fpos);
+        const uint32_t row_ctas = rows_pad / GP_ROWS, neg_ctas = (2 * E.n_pad + GP_WARPS - 1) / GP_WARPS;
+        launch_pdl(k_gather_pack, dim3(row_ctas + neg_ctas), dim3(32 * GP_WARPS), sm, E.stream, edges, nb, pi, pj,
+                   E.rel_theta, E.m.kind, E.dim, E.CB, (uint32_t)E.b_cap, E.s.Apk, E.s.fpos, row_ctas,
+                   negs, E.nt, (uint32_t)E.n_pad, E.s.Npk);
     } else {
         const uint32_t warps = 8;
         k_gather_adjust<<<(nb + warps - 1) / warps, warps * 32, 0, E.stream>>>(edges, nb, pi, pj, E.rel_theta,
@@ -1076,6 +1122,7 @@ void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, c
 void launch_gather_negatives(const Engine& E, const uint32_t* negs, const PartView& pi, const PartView& pj,
                              bool packed) {
     if (!E.n_neg) return;
+    if (packed) return;  // packed by k_gather_pack's trailing CTAs
     const uint32_t warps = packed ? 2 * E.n_pad : E.n_neg;
     if (packed)
         launch_pdl(k_gather_negs<true>, dim3((warps * 32 + 255) / 256), dim3(256), 0, E.stream, negs, E.n_neg, E.nt,
@@ -1111,7 +1158,9 @@ void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, cons
         launch_pdl(k_chain_pipe, dim3(blocks), dim3(warps * 32), sm, E.stream, edges, nb, E.n_neg, pi, pj,
                    (const float*)E.rel_theta, E.m.kind, E.dim, (const float*)E.s.dA, (uint32_t)E.b_cap,
                    (const float*)E.s.g0, (const uint32_t*)E.s.rank, (const uint8_t*)E.s.uniq, E.s.grows,
-                   E.direct_hi ? 1 : 0, E.m.lr, E.m.eps);
+                   E.direct_hi ? 1 : 0, E.m.lr, E.m.eps, (const float*)E.s.lse, (const float*)E.s.fpos,
+                   reinterpret_cast<double*>(E.s.loss_part), E.s.loss_done, E.loss_target);
+        E.loss_fused = true;
     } else {
         k_chain_rule<<<(nb + warps - 1) / warps, warps * 32, 0, E.stream>>>(
             edges, nb, E.n_neg, pi, pj, E.rel_theta, E.m.kind, E.dim, E.s.dA, E.tc_engine() ? (uint32_t)E.b_cap : 0u,
@@ -1121,6 +1170,12 @@ void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, cons
 }
 
 void launch_loss(const Engine& E, uint32_t nb, float* loss_out) {
+    if (E.loss_fused) {  // the chain rule already reduced the loss into E.loss_target
+        if (loss_out != E.loss_target)
+            EMBER_CUDA(cudaMemcpyAsync(loss_out, E.loss_target, sizeof(float), cudaMemcpyDeviceToDevice, E.stream));
+        E.loss_fused = false;
+        return;
+    }
     const uint32_t per = LOSS_THREADS;  // ~100 blocks at b = 5e4: latency, not bandwidth
     const uint32_t blocks = (nb + per - 1) / per;
     launch_pdl(k_loss, dim3(blocks), dim3(LOSS_THREADS), 0, E.stream, (const float*)E.s.lse, (const float*)E.s.fpos, nb,
@@ -1193,7 +1248,7 @@ void launch_init_rows(cudaStream_t st, float* theta, float* acc, uint64_t first,
 
 void launch_debug_scores(const Engine& E, const uint32_t* edges, uint32_t nb, const uint32_t* negs, int side,
                          uint32_t rows, float* out, const PartView& pi, const PartView& pj) {
-    launch_gather_adjust(E, edges, nb, pi, pj, false);
+    launch_gather_adjust(E, edges, nb, pi, pj, false, negs);
     launch_gather_negatives(E, negs, pi, pj, false);
     const float* A = E.s.A + (uint64_t)side * nb * E.dim;
     const float* N = E.s.N + (uint64_t)side * E.nt * E.dim;
