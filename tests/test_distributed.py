@@ -88,12 +88,14 @@ def _backend(edges):
                          CFG["neg_seed"], edges)
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, cfg=None):
     import torch.distributed as dist
+    if cfg:
+        CFG.update(cfg)
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     edges, off = _graph()
     be = _backend(edges)
-    tr = ed.DistributedTrainer(be, CFG["p"], off, CFG["b"], rank, world, relations=True, dist=dist)
+    tr = ed.DistributedTrainer(be, CFG["p"], off, CFG["b"], rank, world, relations=CFG["kind"] != "dot", dist=dist)
     tr.init_embeddings(CFG["seed"])
     n = 0
     for ep in range(CFG["epochs"]):
@@ -106,6 +108,10 @@ def _worker(rank, world, port, out_dir):
 
 
 def _serial_replay(world):
+    return _serial_replay_cfg(world)
+
+
+def _serial_replay_cfg(world):
     """The same lockstep schedule in one process: all ranks' batches of a step, node updates in
     place, relation gradients summed in rank order before one relation Adagrad."""
     edges, off = _graph()
@@ -293,3 +299,30 @@ def test_seek_transfers_reach_the_round_layout():
             assert held[x] == src
             held[x] = dst
         assert (held == plan.holder[r]).all()
+
+
+def test_four_rank_dot_epochs_bit_identical_to_serial_replay(tmp_path):
+    """Dot model (no relations, no per-step collective) over 4 ranks, p=8: the handoffs alone must
+    reproduce the serial replay bit for bit."""
+    import torch.multiprocessing as mp
+    world, port = 4, _free_port()
+    cfg = dict(kind="dot", p=8, V=1600, epochs=2)
+    saved = dict(CFG)
+    try:
+        CFG.update(cfg)
+        mp.start_processes(_worker, args=(world, port, str(tmp_path), cfg), nprocs=world, join=True,
+                           start_method="spawn")
+        ref, n_ref, off = _serial_replay(world)
+        got = np.full_like(ref.theta, np.nan)
+        total = 0
+        for g in range(world):
+            z = np.load(tmp_path / f"rank{g}.npz")
+            total += int(z["edges"][0])
+            for x in z["held"]:
+                o, sz = eb.partition_offset(CFG["V"], CFG["p"], int(x)), eb.partition_size(CFG["V"], CFG["p"], int(x))
+                got[o:o + sz] = z["theta"][o:o + sz]
+        assert total == n_ref
+        assert got.tobytes() == ref.theta.tobytes()
+    finally:
+        CFG.clear()
+        CFG.update(saved)
