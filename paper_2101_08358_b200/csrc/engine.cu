@@ -198,6 +198,17 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     EMBER_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t3, s.counts, s.offsets, (int)cap_rows, side));
     s.cub_bytes = std::max(t1, std::max(t2, t3));
     s.cub_tmp = dalloc<uint8_t>(s.cub_bytes);
+    sets[0] = SortSet{s.negs, s.keys, s.keys_sorted, s.vals, s.vals_sorted, s.rank, s.ukeys, s.counts,
+                      s.offsets, s.nruns, s.longs, s.long_owner, s.uniq, s.cub_tmp};
+    sets[1] = SortSet{dalloc<uint32_t>(n_neg), dalloc<uint32_t>(cap_rows), dalloc<uint32_t>(cap_rows),
+                      dalloc<uint32_t>(cap_rows), dalloc<uint32_t>(cap_rows), dalloc<uint32_t>(cap_rows),
+                      dalloc<uint32_t>(cap_rows), dalloc<uint32_t>(cap_rows), dalloc<uint32_t>(cap_rows),
+                      dalloc<uint32_t>(1), dalloc<uint32_t>(2 + 3 * max_long), dalloc<uint32_t>(max_chunks),
+                      dalloc<uint8_t>(cap_rows), dalloc<uint8_t>(s.cub_bytes)};
+    EMBER_CUDA(cudaMemset(sets[1].longs, 0, 2 * sizeof(uint32_t)));
+    EMBER_CUDA(cudaEventCreateWithFlags(&ev_after_tc, cudaEventDisableTiming));
+    EMBER_CUDA(cudaEventCreateWithFlags(&ev_sampled, cudaEventDisableTiming));
+    for (int k = 0; k < 2; ++k) EMBER_CUDA(cudaEventCreateWithFlags(&ev_set_free[k], cudaEventDisableTiming));
     if (tc_engine()) tc_setup(*this);
     EMBER_CUDA(cudaStreamSynchronize(stream));
 }
@@ -207,12 +218,21 @@ Engine::~Engine() {
     if (stream) cudaStreamSynchronize(stream);
     if (side && side != stream) cudaStreamSynchronize(side);
     tc_release(*this);
-    void* ptrs[] = {s.negs,  s.batch,       s.A,    s.N,          s.Apk,       s.Npk,   s.fpos,   s.lse,
-                    s.g0,    s.S,           s.dA,   s.dN_part,    s.grows,     s.loss,  s.loss_part,
-                    s.loss_done, s.keys,    s.keys_sorted, s.vals, s.vals_sorted, s.rank, s.uniq, s.ukeys,  s.counts,
-                    s.offsets, s.nruns,     s.nunique, s.longs,   s.long_owner, s.long_partial, s.cub_tmp, s.rel_dense};
+    // (the sort scratch is owned by sets[0..1]; s.* only points at the current one)
+    void* ptrs[] = {s.batch, s.A,         s.N,      s.Apk,       s.Npk,     s.fpos,       s.lse,    s.g0,
+                    s.S,     s.dA,        s.dN_part, s.grows,    s.loss,    s.loss_part,  s.loss_done,
+                    s.nunique, s.long_partial, s.rel_dense};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    for (const SortSet& t : sets) {
+        void* p1[] = {t.negs,  t.keys,  t.keys_sorted, t.vals,  t.vals_sorted, t.rank,      t.ukeys,
+                      t.counts, t.offsets, t.nruns,    t.longs, t.long_owner,  (void*)t.uniq, t.cub_tmp};
+        for (void* p : p1)
+            if (p) cudaFree(p);
+    }
+    cudaGetLastError();
+    for (cudaEvent_t e : {ev_after_tc, ev_sampled, ev_set_free[0], ev_set_free[1]})
+        if (e) cudaEventDestroy(e);
     if (nccl_comm) {
         try {
             nccl().destroy(static_cast<ncclComm_t>(nccl_comm));
@@ -263,8 +283,6 @@ void Engine::sample(const uint32_t* bucket, uint64_t bucket_n, uint32_t i, uint3
 void Engine::sort_keys(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs) {
     const KeySpace ks = keyspace(i, j);
     const uint32_t n = slots(nb);
-    EMBER_CUDA(cudaEventRecord(ev_fork, stream));
-    EMBER_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
     launch_keys(*this, edges, nb, negs, ks);
     size_t bytes = s.cub_bytes;
     EMBER_CUDA(cub::DeviceRadixSort::SortPairs(s.cub_tmp, bytes, s.keys, s.keys_sorted, s.vals, s.vals_sorted, (int)n,
@@ -286,9 +304,32 @@ void Engine::join_sorted() {
     sorted_pending = false;
 }
 
-void Engine::forward_backward(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs) {
+void Engine::use_set(int k) {
+    const SortSet& t = sets[k];
+    s.negs = t.negs;
+    s.keys = t.keys;
+    s.keys_sorted = t.keys_sorted;
+    s.vals = t.vals;
+    s.vals_sorted = t.vals_sorted;
+    s.rank = t.rank;
+    s.ukeys = t.ukeys;
+    s.counts = t.counts;
+    s.offsets = t.offsets;
+    s.nruns = t.nruns;
+    s.longs = t.longs;
+    s.long_owner = t.long_owner;
+    s.uniq = t.uniq;
+    s.cub_tmp = t.cub_tmp;
+}
+
+void Engine::forward_backward(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs,
+                              bool presorted) {
     const PartView pi = view(i), pj = view(j);
-    sort_keys(edges, nb, i, j, negs);  // helper stream, overlapped with the gathers and the contraction
+    if (!presorted) {  // helper stream, overlapped with the gathers and the contraction
+        EMBER_CUDA(cudaEventRecord(ev_fork, stream));
+        EMBER_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+        sort_keys(edges, nb, i, j, negs);
+    }
     mark(PHASE_GATHER);
     launch_gather_adjust(*this, edges, nb, pi, pj, tc_engine(), negs);
     launch_gather_negatives(*this, negs, pi, pj, tc_engine());
@@ -297,6 +338,9 @@ void Engine::forward_backward(const uint32_t* edges, uint32_t nb, uint32_t i, ui
         launch_contract_tc(*this, nb);  // joins the sort before scattering dN rows
     else
         launch_contract_simt(*this, nb);
+    // the next step's sampling + sort may start now: they overlap this step's memory-bound phase
+    EMBER_CUDA(cudaEventRecord(ev_after_tc, stream));
+    have_after_tc = true;
     mark(PHASE_CHAIN);
     join_sorted();
     launch_chain_rule(*this, edges, nb, pi, pj);
@@ -348,7 +392,7 @@ void Engine::train_batch_host(const uint32_t* bucket, uint64_t bucket_n, const u
     EMBER_CUDA(cudaMemcpyAsync(slot, host_batch, (size_t)nb * 12, cudaMemcpyHostToDevice, io));
     EMBER_CUDA(cudaEventRecord(ev_staged[k], io));
     EMBER_CUDA(cudaStreamWaitEvent(stream, ev_staged[k], 0));
-    step(slot, nb, bucket, bucket_n, i, j, epoch, bucket_step, batch_in_bucket, s.loss);
+    step(slot, nb, bucket, bucket_n, i, j, epoch, bucket_step, batch_in_bucket, s.loss, ev_staged[k]);
     EMBER_CUDA(cudaEventRecord(ev_consumed[k], stream));
     if (loss_host) EMBER_CUDA(cudaMemcpyAsync(loss_host, s.loss, sizeof(float), cudaMemcpyDeviceToHost, stream));
 }
@@ -360,18 +404,37 @@ void Engine::train_batch(const uint32_t* bucket, uint64_t bucket_n, uint64_t bat
 }
 
 void Engine::step(const uint32_t* edges, uint32_t nb, const uint32_t* bucket, uint64_t bucket_n, uint32_t i,
-                  uint32_t j, uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket, float* loss_out) {
+                  uint32_t j, uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket, float* loss_out,
+                  cudaEvent_t edges_ready) {
     if (nb == 0 || nb > cap_b) throw ConfigError("batch size must be in [1, batch_size]");
     check_bucket(i, j);
+    // Sampling and the (key, slot) sort of this step run on the helper stream with this step's
+    // parity of the sort scratch. They wait for the previous step's contraction (so they overlap
+    // that step's chain rule and reduction rather than competing with the persistent tensor-core
+    // kernels) and for the step that last used this scratch; the results do not depend on when
+    // they run (counter-based sampler, fixed inputs).
+    const int k = (int)(nsteps++ & 1);
+    use_set(k);
+    if (have_after_tc) EMBER_CUDA(cudaStreamWaitEvent(side, ev_after_tc, 0));
+    if (set_used[k]) EMBER_CUDA(cudaStreamWaitEvent(side, ev_set_free[k], 0));
+    if (edges_ready) EMBER_CUDA(cudaStreamWaitEvent(side, edges_ready, 0));
     mark(PHASE_SAMPLE);
-    sample(bucket, bucket_n, i, j, epoch, bucket_step, batch_in_bucket, s.negs);
+    {
+        const uint64_t base = mix_seed(mix_seed(m.neg_seed, epoch, bucket_step), batch_in_bucket);
+        launch_sample_on(*this, side, s.negs, base, bucket, bucket_n, view(i), view(j));
+    }
+    EMBER_CUDA(cudaEventRecord(ev_sampled, side));
+    sort_keys(edges, nb, i, j, s.negs);
+    EMBER_CUDA(cudaStreamWaitEvent(stream, ev_sampled, 0));
     direct_hi = getenv_direct() ? 2 * nb : 0;
     loss_target = loss_out ? loss_out : s.loss;
-    forward_backward(edges, nb, i, j, s.negs);
+    forward_backward(edges, nb, i, j, s.negs, true);
     launch_loss(*this, nb, loss_out ? loss_out : s.loss);
     mark(PHASE_REDUCE);
     reduce_and_apply(nb, i, j, true, nullptr, nullptr, nullptr, nullptr);
     direct_hi = 0;
+    EMBER_CUDA(cudaEventRecord(ev_set_free[k], stream));
+    set_used[k] = true;
     mark(PHASE_END);
 }
 

@@ -106,6 +106,16 @@ struct Scratch {
     float* rel_dense = nullptr;  // [R][dim] relation gradient summed over ranks (world > 1)
 };
 
+// The per-step sort scratch, double-buffered by step parity: step n+1's sampling and key sort run
+// on the helper stream while step n is still in its memory-bound phase (see Engine::step).
+struct SortSet {
+    uint32_t *negs = nullptr, *keys = nullptr, *keys_sorted = nullptr, *vals = nullptr, *vals_sorted = nullptr,
+             *rank = nullptr, *ukeys = nullptr, *counts = nullptr, *offsets = nullptr, *nruns = nullptr,
+             *longs = nullptr, *long_owner = nullptr;
+    uint8_t* uniq = nullptr;
+    void* cub_tmp = nullptr;
+};
+
 struct TcState;  // tensor-core engine state (tc_score.cu)
 
 struct Engine {
@@ -113,6 +123,13 @@ struct Engine {
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;  // key sort runs here, overlapped with gather + contraction
     cudaEvent_t ev_fork = nullptr, ev_sorted = nullptr;
+    // cross-step pipelining of sampling + sort (Engine::step)
+    SortSet sets[2];
+    bool set_used[2] = {false, false};
+    uint64_t nsteps = 0;
+    bool have_after_tc = false;
+    cudaEvent_t ev_after_tc = nullptr, ev_sampled = nullptr, ev_set_free[2] = {nullptr, nullptr};
+    void use_set(int k);
     // host-batch path: positives copied on `io` into one of two staging slots, overlapping the
     // previous step; ev_staged[k]: copy into slot k done; ev_consumed[k]: the step reading slot k done
     cudaStream_t io = nullptr;
@@ -177,7 +194,8 @@ struct Engine {
     void sort_keys(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs);
     void join_sorted();  // the step stream waits for sort_keys' results
     // Computes loss and gradient rows for one batch into grows (sorted order).
-    void forward_backward(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs);
+    void forward_backward(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs,
+                          bool presorted = false);
     // Segmented sum of the sorted gradient rows, then Adagrad (or export of the deltas).
     void reduce_and_apply(uint32_t nb, uint32_t i, uint32_t j, bool apply, uint32_t* node_ids_out,
                           float* node_rows_out, uint32_t* rel_ids_out, float* rel_rows_out);
@@ -188,8 +206,10 @@ struct Engine {
                           uint32_t i, uint32_t j, uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket,
                           float* loss_host);
     // One Algorithm-1 step on nb positives at `edges` (device) of bucket (i, j).
+    // edges_ready (nullable): an event the helper stream must wait for before reading `edges`.
     void step(const uint32_t* edges, uint32_t nb, const uint32_t* bucket, uint64_t bucket_n, uint32_t i, uint32_t j,
-              uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket, float* loss_out);
+              uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket, float* loss_out,
+              cudaEvent_t edges_ready = nullptr);
     void allreduce_relations();
     void apply_relations_dense(const float* grad);  // dense relation Adagrad (zero rows are no-ops)
     void comm_init(const void* nccl_unique_id, int rank, int world);
@@ -226,6 +246,8 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
 // kernel launchers (kernels_step.cu, gemm_simt.cu, tc_score.cu, graph.cu)
 void launch_sample(const Engine& E, uint32_t* out, uint64_t base_seed, const uint32_t* bucket, uint64_t bucket_n,
                    const PartView& src, const PartView& dst);
+void launch_sample_on(const Engine& E, cudaStream_t st, uint32_t* out, uint64_t base_seed, const uint32_t* bucket,
+                      uint64_t bucket_n, const PartView& src, const PartView& dst);
 // packed: write the tensor-core engine's bf16 hi|lo operands (Apk/Npk), else fp32 A / N.
 void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj,
                           bool packed, const uint32_t* negs);

@@ -1097,6 +1097,16 @@ void launch_sample(const Engine& E, uint32_t* out, uint64_t base, const uint32_t
     EMBER_LAUNCHED(E);
 }
 
+void launch_sample_on(const Engine& E, cudaStream_t st, uint32_t* out, uint64_t base, const uint32_t* bucket,
+                      uint64_t bucket_n, const PartView& src, const PartView& dst) {
+    const uint32_t n_deg = (uint32_t)ceil((double)E.m.alpha * (double)E.nt);
+    const uint32_t total = E.n_neg;
+    if (!total) return;
+    k_sample<<<(total + 255) / 256, 256, 0, st>>>(out, E.nt, n_deg, total, base, bucket, bucket_n, src.first, src.rows,
+                                                   dst.first, dst.rows);
+    EMBER_LAUNCHED(E);
+}
+
 void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj,
                           bool packed, const uint32_t* negs) {
     if (packed) {
