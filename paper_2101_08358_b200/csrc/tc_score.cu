@@ -771,10 +771,9 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
         EMBER_CUDA(cudaMemsetAsync(t.trace, 0, (size_t)2 * 5 * TRACE_ROLE * 8, E.stream));
         a.trace = t.trace;
     }
-    // the persistent contraction kernels are launched stream-ordered (not PDL): early-resident CTAs
-    // waiting on the previous kernel would keep the helper stream's sort off those SMs
-    k_tc<MODE_ROWS><<<std::min(items1, gmax), NTHREADS, smem_total(t.KP, t.nstage, MODE_ROWS), E.stream>>>(
-        t.mA128, t.mN96, a);
+    // programmatic launch: the CTAs set up barriers and TMEM while the gathers drain
+    launch_pdl(k_tc<MODE_ROWS>, dim3(std::min(items1, gmax)), dim3(NTHREADS), smem_total(t.KP, t.nstage, MODE_ROWS),
+               E.stream, t.mA128, t.mN96, a);
     EMBER_LAUNCHED(E);
     if (tr) {
         dump(".rows.bin");
@@ -783,8 +782,8 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
     launch_pdl(k_tc_fixup, dim3(1), dim3(1024), 0, E.stream, a, (const uint16_t*)s.Apk, (const uint16_t*)s.Npk);
     EMBER_LAUNCHED(E);
     const int items2 = 2 * ((nt + RES - 1) / RES) * a.chunks2;
-    k_tc<MODE_NEGS><<<std::min(items2, gmax), NTHREADS, smem_total(t.KP, t.nstage, MODE_NEGS), E.stream>>>(
-        t.mN128, t.mA96, a);
+    launch_pdl(k_tc<MODE_NEGS>, dim3(std::min(items2, gmax)), dim3(NTHREADS), smem_total(t.KP, t.nstage, MODE_NEGS),
+               E.stream, t.mN128, t.mA96, a);
     EMBER_LAUNCHED(E);
     if (tr) dump(".negs.bin");
     const int64_t r = (int64_t)2 * nt * (d / 4);
