@@ -86,6 +86,8 @@ int ember_ctx_create(int device, const ember_model_desc* model, const ember_grap
                      ember_ctx** out);
 int ember_ctx_destroy(ember_ctx* ctx);
 void* ember_ctx_stream(ember_ctx* ctx);
+/* Waits for all work of the context (its stream and its internal copy / helper streams). */
+int ember_ctx_synchronize(ember_ctx* ctx);
 const char* ember_last_error(void);
 int ember_version(void);
 
@@ -113,10 +115,11 @@ int ember_train_batch(ember_ctx* ctx, const uint32_t* bucket_edges_dev, uint64_t
  * stats (host, nullable) is filled after a stream sync when non-NULL. */
 int ember_train_bucket(ember_ctx* ctx, const uint32_t* bucket_edges_dev, uint64_t bucket_n, uint32_t i, uint32_t j,
                        uint64_t epoch, uint32_t bucket_step, ember_step_stats* stats);
-/* Same step with the nb positives in HOST memory (pinned recommended), copied in on the
- * context stream. The degree-based sampler still reads the bucket (bucket_edges_dev), which
- * stays device-resident. loss_host (nullable; pinned for an asynchronous copy) receives the
- * loss on the context stream: synchronise the stream before reading it. */
+/* Same step with the nb positives in HOST memory (pinned recommended), copied in asynchronously on
+ * an internal copy stream (double-buffered: the copy overlaps the previous step). The degree-based
+ * sampler still reads the bucket (bucket_edges_dev), which stays device-resident. loss_host
+ * (nullable; pinned for an asynchronous copy) receives the loss asynchronously: it is valid after
+ * ember_ctx_synchronize. The caller keeps host_batch alive until then as well. */
 int ember_train_batch_host(ember_ctx* ctx, const uint32_t* bucket_edges_dev, uint64_t bucket_n,
                            const uint32_t* host_batch, uint32_t nb, uint32_t i, uint32_t j, uint64_t epoch,
                            uint32_t bucket_step, uint32_t batch_in_bucket, float* loss_host);

@@ -207,6 +207,7 @@ class Trainer:
         return self.torch.cuda.ExternalStream(self.stream_ptr, device=self.dev)
 
     def synchronize(self):
+        check(lib().ember_ctx_synchronize(self.ctx))
         self.torch.cuda.synchronize(self.dev)
 
     # -- tables ---------------------------------------------------------------------------
@@ -245,8 +246,7 @@ class Trainer:
                                            int(host_batch.shape[0]), i, j, epoch, bucket_step, batch_in_bucket,
                                            C.byref(loss) if want_loss else None))
         if want_loss:
-            self.torch.cuda.current_stream(self.dev)  # ensure CUDA initialised
-            self.torch_stream().synchronize()
+            check(lib().ember_ctx_synchronize(self.ctx))
         return float(loss.value) if want_loss else None
 
     def train_bucket(self, bucket_edges, i=0, j=0, epoch=0, bucket_step=0) -> StepStats:

@@ -59,6 +59,7 @@ def _declare(L):
         "ember_ctx_create": (C.c_int, [i32, C.POINTER(ModelDesc), C.POINTER(GraphDesc), vp, C.POINTER(vp)]),
         "ember_ctx_destroy": (C.c_int, [vp]),
         "ember_ctx_stream": (vp, [vp]),
+        "ember_ctx_synchronize": (C.c_int, [vp]),
         "ember_tables_bind": (C.c_int, [vp, u32, vp, vp]),
         "ember_relations_bind": (C.c_int, [vp, vp, vp]),
         "ember_init_partition": (C.c_int, [vp, u32, u64]),

@@ -125,6 +125,14 @@ int ember_ctx_destroy(ember_ctx* ctx) {
 
 void* ember_ctx_stream(ember_ctx* ctx) { return ctx && ctx->e ? static_cast<void*>(ctx->e->stream) : nullptr; }
 
+int ember_ctx_synchronize(ember_ctx* ctx) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        for (cudaStream_t st : {E.stream, E.side, E.io, E.io_out})
+            if (st) EMBER_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
 int ember_tables_bind(ember_ctx* ctx, uint32_t part, float* theta, float* acc) {
     return guarded([&] {
         Engine& E = eng(ctx);

@@ -130,9 +130,11 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     else
         EMBER_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
     EMBER_CUDA(cudaStreamCreateWithFlags(&io, cudaStreamNonBlocking));
+    EMBER_CUDA(cudaStreamCreateWithFlags(&io_out, cudaStreamNonBlocking));
     for (int k = 0; k < 2; ++k) {
         EMBER_CUDA(cudaEventCreateWithFlags(&ev_staged[k], cudaEventDisableTiming));
         EMBER_CUDA(cudaEventCreateWithFlags(&ev_consumed[k], cudaEventDisableTiming));
+        EMBER_CUDA(cudaEventCreateWithFlags(&ev_loss_read[k], cudaEventDisableTiming));
     }
     EMBER_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     EMBER_CUDA(cudaEventCreateWithFlags(&ev_sorted, cudaEventDisableTiming));
@@ -154,7 +156,7 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     s.g0 = dalloc<float>(2 * b);
     s.dA = dalloc<float>(2 * (uint64_t)std::max<uint64_t>(b, (uint64_t)pad_rows(cap_b)) * d);
     s.grows = dalloc<float>((uint64_t)cap_rows * d);
-    s.loss = dalloc<float>(1);
+    s.loss = dalloc<float>(4);  // [0]: steps; [1 + k]: host-batch steps of staging slot k
     // one per k_loss block, or one per warp of the fused chain rule (<= 3 x 8 warps per SM)
     s.loss_part = reinterpret_cast<float*>(dalloc<double>(std::max<uint64_t>(b / 512 + 2, 24ull * sm_count + 32)));
     s.loss_done = dalloc<uint32_t>(1);
@@ -240,11 +242,14 @@ Engine::~Engine() {
         }
     }
     if (io) cudaStreamSynchronize(io);
+    if (io_out) cudaStreamSynchronize(io_out);
     for (int k = 0; k < 2; ++k) {
         if (ev_staged[k]) cudaEventDestroy(ev_staged[k]);
         if (ev_consumed[k]) cudaEventDestroy(ev_consumed[k]);
+        if (ev_loss_read[k]) cudaEventDestroy(ev_loss_read[k]);
     }
     if (io) cudaStreamDestroy(io);
+    if (io_out) cudaStreamDestroy(io_out);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_sorted) cudaEventDestroy(ev_sorted);
     if (side && side != stream) cudaStreamDestroy(side);
@@ -392,9 +397,16 @@ void Engine::train_batch_host(const uint32_t* bucket, uint64_t bucket_n, const u
     EMBER_CUDA(cudaMemcpyAsync(slot, host_batch, (size_t)nb * 12, cudaMemcpyHostToDevice, io));
     EMBER_CUDA(cudaEventRecord(ev_staged[k], io));
     EMBER_CUDA(cudaStreamWaitEvent(stream, ev_staged[k], 0));
-    step(slot, nb, bucket, bucket_n, i, j, epoch, bucket_step, batch_in_bucket, s.loss, ev_staged[k]);
+    // the loss lands in slot k's own word and is read back on io_out, off the step stream (whose
+    // kernels then chain with programmatic launches); the word is rewritten two steps later, after
+    // that read (ev_loss_read)
+    float* loss_dev = s.loss + 1 + k;
+    if (host_steps > 2) EMBER_CUDA(cudaStreamWaitEvent(stream, ev_loss_read[k], 0));
+    step(slot, nb, bucket, bucket_n, i, j, epoch, bucket_step, batch_in_bucket, loss_dev, ev_staged[k]);
     EMBER_CUDA(cudaEventRecord(ev_consumed[k], stream));
-    if (loss_host) EMBER_CUDA(cudaMemcpyAsync(loss_host, s.loss, sizeof(float), cudaMemcpyDeviceToHost, stream));
+    EMBER_CUDA(cudaStreamWaitEvent(io_out, ev_consumed[k], 0));
+    if (loss_host) EMBER_CUDA(cudaMemcpyAsync(loss_host, loss_dev, sizeof(float), cudaMemcpyDeviceToHost, io_out));
+    EMBER_CUDA(cudaEventRecord(ev_loss_read[k], io_out));
 }
 
 void Engine::train_batch(const uint32_t* bucket, uint64_t bucket_n, uint64_t batch_begin, uint32_t nb, uint32_t i,

@@ -132,8 +132,9 @@ struct Engine {
     void use_set(int k);
     // host-batch path: positives copied on `io` into one of two staging slots, overlapping the
     // previous step; ev_staged[k]: copy into slot k done; ev_consumed[k]: the step reading slot k done
-    cudaStream_t io = nullptr;
+    cudaStream_t io = nullptr, io_out = nullptr;  // host->device batches / device->host losses
     cudaEvent_t ev_staged[2] = {nullptr, nullptr}, ev_consumed[2] = {nullptr, nullptr};
+    cudaEvent_t ev_loss_read[2] = {nullptr, nullptr};  // the loss of the step using slot k has been read back
     uint64_t host_steps = 0;
     bool own_stream = false;
     bool sorted_pending = false;
