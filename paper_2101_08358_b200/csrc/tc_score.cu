@@ -75,6 +75,7 @@ struct TcArgs {
     float* dA;        // column-blocked [2][d/4][b_cap] float4
     float* dN_part;   // column-blocked [chunks][2][d/4][n_pad] float4
     uint32_t* flags;  // [0] = count, [1..] = side * b_cap + row
+    int early;        // tiles 0 .. early-1 of an item go to epilogue group 0 (tile_group)
     unsigned long long* trace;  // debug timeline of CTA 0 (EMBER_TC_TRACE), nullptr normally
 };
 
@@ -262,6 +263,12 @@ __device__ __forceinline__ void epi_chunk(uint32_t tS, int c0, int k, const TcAr
     }
 }
 
+// Epilogue group of an item's streamed tile k. Group 1 also drains every item's accumulator
+// (the tail), which delays its next tile; so the first tiles of each item (0, 1, 2) go to group 0
+// and the rest alternate (odd -> group 1): group 1's first tile of the next item comes ~3 tiles
+// after the boundary, by when its tail is done. (EMBER_TC_EARLY=1: plain alternation, A/B.)
+__device__ __forceinline__ int tile_group(int k, int early) { return k < early ? 0 : (k & 1); }
+
 template <int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_tc(const __grid_constant__ CUtensorMap mapR, const __grid_constant__ CUtensorMap mapT, TcArgs g) {
@@ -382,7 +389,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         tc::mma_ts_elect(tS, rh, th, id_s, 1u);
                     }
                 }
-                tc::mma_commit_elect(&bars[B_S_FULL + (k & 1) * NSP_MAX + b]);  // tile k of an item -> group k & 1
+                tc::mma_commit_elect(&bars[B_S_FULL + tile_group(k, g.early) * NSP_MAX + b]);  // tile k -> its group
                 TC_TRACE(12, q);
             }
             gt += I.T;
@@ -423,12 +430,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             gt += I.T;
         }
     } else {  // -------------------------------------------------------------------- epilogue
-        const int G = (warp - 3) >> 2;          // ping-pong group: takes tiles k of an item with k % 2 == G
+        const int G = (warp - 3) >> 2;          // ping-pong group: takes the tiles k with tile_group(k) == G
         const int qd = warp & 3;                // TMEM lane quadrant
         const int r = 32 * qd + lane;           // resident row (MODE_ROWS: batch row; NEGS: negative)
         const uint32_t t_row = tbase + ((uint32_t)(32 * qd) << 16);
-        // Tile k of every item goes to group k & 1 (group 0 always starts an item); group 1 also
-        // does every item tail, so group 0 moves straight on to the next item's first tile.
+        // Tile k of every item goes to group tile_group(k) (group 0 always starts an item); group 1
+        // also does every item tail, so group 0 moves straight on to the next item's first tiles.
         uint32_t it = 0, gt = 0;
         uint32_t sphase = 0;  // bit b: parity of this group's next wait on S_FULL[G][b]
         for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
@@ -437,7 +444,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             float fp = 0.f, z = 0.f;
             if (MODE == MODE_ROWS) fp = row < g.nb ? g.fpos[row] : 0.f;
             const float cshift = -fp * L2E;
-            for (int k = G; k < I.T; k += 2) {
+            for (int k = 0; k < I.T; ++k) {
+                if (tile_group(k, g.early) != G) continue;
                 const uint32_t q = gt + k;
                 const uint32_t b = q % NSP;
                 const uint32_t tS = t_row + b * TILE;
@@ -747,6 +755,8 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
     a.dA = s.dA;
     a.dN_part = t.dN_part;
     a.flags = t.flags;
+    a.early = 3;
+    if (const char* e = getenv("EMBER_TC_EARLY")) a.early = std::max(1, atoi(e));  // A/B (1: plain alternation)
     a.trace = nullptr;
     const int nsub = (int)((nb + TILE - 1) / TILE);
     a.chunks2 = std::min(t.chunks2, nsub);
