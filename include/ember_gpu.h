@@ -115,6 +115,12 @@ int ember_train_batch(ember_ctx* ctx, const uint32_t* bucket_edges_dev, uint64_t
  * stats (host, nullable) is filled after a stream sync when non-NULL. */
 int ember_train_bucket(ember_ctx* ctx, const uint32_t* bucket_edges_dev, uint64_t bucket_n, uint32_t i, uint32_t j,
                        uint64_t epoch, uint32_t bucket_step, ember_step_stats* stats);
+/* train_epoch_partitioned with every partition bound (HBM-resident): all buckets
+ * of seq (2*p*p u32: the plan's bucket sequence) in order, each bucket's batches in order,
+ * bucket_step = position in seq. edges_dev: bucketed edges, offsets_host: p*p+1 u64. stats
+ * (nullable) is filled after one synchronisation at the end of the epoch. */
+int ember_train_epoch(ember_ctx* ctx, const uint32_t* edges_dev, const uint64_t* offsets_host, const uint32_t* seq,
+                      uint64_t epoch, ember_step_stats* stats);
 /* Same step with the nb positives in HOST memory (pinned recommended), copied in asynchronously on
  * an internal copy stream (double-buffered: the copy overlaps the previous step). The degree-based
  * sampler still reads the bucket (bucket_edges_dev), which stays device-resident. loss_host
@@ -196,6 +202,10 @@ int ember_graph_preprocess(int device, const uint32_t* raw_dev, uint64_t n, uint
  * CUB device-wide calls (library kernels) since creation. Synchronises the stream. */
 int ember_profile_enable(ember_ctx* ctx, int enable);
 int ember_profile_read(ember_ctx* ctx, double* ms_out, uint64_t* launches_out, uint64_t* lib_calls_out);
+/* Rows (batch row x side) whose log-sum-exp left the tensor-core engine's safe range and were
+ * recomputed exactly (fp32, CUDA cores), summed since context creation (0 for the SIMT engine).
+ * Synchronises the context stream. */
+int ember_overflow_rows(ember_ctx* ctx, uint64_t* total);
 /* Self-test of the tcgen05 building blocks on `device` (one 128 x N x K bf16 product vs a double
  * host product); max_rel_err_out = max|err| / max|ref|. mode: see csrc/tc_selftest.cu. */
 int ember_tc_selftest(int device, int mode, int K, int N, uint64_t seed, double* max_rel_err_out);

@@ -256,16 +256,13 @@ class Trainer:
         return st
 
     def train_epoch(self, edges_dev, offsets, plan_seq, epoch: int) -> dict:
-        """train_epoch_partitioned (Algorithm 2): buckets in plan order."""
-        total = StepStats()
-        for step, (i, j) in enumerate(np.asarray(plan_seq).reshape(-1, 2)):
-            b = int(i) * self.p + int(j)
-            lo, hi = int(offsets[b]), int(offsets[b + 1])
-            if hi == lo:
-                continue
-            check(lib().ember_train_bucket(self.ctx, _ptr(edges_dev[lo:hi]), hi - lo, int(i), int(j), epoch, step,
-                                           C.byref(total)))
-        return {"loss": total.loss_sum / max(1, total.batches), "batches": total.batches, "edges": total.edges}
+        """train_epoch_partitioned (Algorithm 2): buckets in plan order, one C-ABI call
+        (no host synchronisation inside the epoch)."""
+        st = StepStats()
+        seq = np.ascontiguousarray(np.asarray(plan_seq, dtype=np.uint32).reshape(-1))
+        off = np.ascontiguousarray(np.asarray(offsets, dtype=np.uint64))
+        check(lib().ember_train_epoch(self.ctx, _ptr(edges_dev), _ptr(off), _ptr(seq), epoch, C.byref(st)))
+        return {"loss": st.loss_sum / max(1, st.batches), "batches": st.batches, "edges": st.edges}
 
     # -- per-op entry points (parity tests) ----------------------------------------------
     def sample_negatives(self, bucket_edges, i=0, j=0, epoch=0, bucket_step=0, batch_in_bucket=0):
@@ -326,6 +323,12 @@ class Trainer:
                                               int(filter_keys.numel()), _ptr(ranks)))
         self.synchronize()
         return ranks.cpu().numpy().view(np.uint32)
+
+    def overflow_rows(self) -> int:
+        """Rows recomputed exactly because their log-sum-exp left the tensor-core engine's range."""
+        v = C.c_uint64(0)
+        check(lib().ember_overflow_rows(self.ctx, C.byref(v)))
+        return v.value
 
     def profile(self, enable: bool = True):
         check(lib().ember_profile_enable(self.ctx, 1 if enable else 0))

@@ -66,6 +66,7 @@ def _declare(L):
         "ember_init_relations": (C.c_int, [vp, u64]),
         "ember_train_batch": (C.c_int, [vp, vp, u64, u64, u32, u32, u32, u64, u32, u32, vp]),
         "ember_train_bucket": (C.c_int, [vp, vp, u64, u32, u32, u64, u32, C.POINTER(StepStats)]),
+        "ember_train_epoch": (C.c_int, [vp, vp, vp, vp, u64, C.POINTER(StepStats)]),
         "ember_train_batch_host": (C.c_int, [vp, vp, u64, vp, u32, u32, u32, u64, u32, u32, vp]),
         "ember_sample_negatives": (C.c_int, [vp, vp, u64, u32, u32, u64, u32, u32, vp]),
         "ember_loss_and_grad": (C.c_int, [vp, vp, u32, u32, u32, vp, vp, vp, vp, vp, C.POINTER(u32), vp, vp,
@@ -96,6 +97,7 @@ def _declare(L):
         "ember_make_rounds": (C.c_int, [u32, u32, vp, vp, vp, vp, C.POINTER(u32)]),
         "ember_relations_external": (C.c_int, [vp, vp]),
         "ember_relations_apply_dense": (C.c_int, [vp, vp]),
+        "ember_overflow_rows": (C.c_int, [vp, C.POINTER(u64)]),
         "ember_comm_init": (C.c_int, [vp, vp, i32, i32]),
         "ember_comm_barrier": (C.c_int, [vp]),
         "ember_partition_copy": (C.c_int, [vp, vp, vp, i32, vp, vp, i32, u64]),

@@ -92,6 +92,49 @@ void need(const void* p, const char* what) {
 }
 }  // namespace
 
+namespace {
+// train_epoch_partitioned (Algorithm 2): the buckets of `seq` in order, every batch
+// of each; acquire/release (nullable) bracket each bucket (the partition buffer). The per-batch
+// losses go to one device array read once at the end: no host synchronisation inside the epoch.
+template <typename Acquire, typename Release>
+void train_epoch_impl(Engine& E, const uint32_t* edges, const uint64_t* offsets, const uint32_t* seq,
+                      uint64_t epoch, ember_step_stats* stats, Acquire&& acquire, Release&& release) {
+    const uint32_t p = E.g.num_partitions;
+    uint64_t nbatch = 0;
+    for (uint64_t k = 0; k < (uint64_t)p * p; ++k) {
+        if (offsets[k + 1] < offsets[k]) throw ConfigError("offsets must be non-decreasing");
+        nbatch += (offsets[k + 1] - offsets[k] + E.cap_b - 1) / E.cap_b;
+    }
+    const uint64_t n_edges = offsets[(size_t)p * p] - offsets[0];
+    float* losses = nullptr;
+    if (stats && nbatch) EMBER_CUDA(cudaMallocAsync(&losses, nbatch * sizeof(float), E.stream));
+    uint64_t slot = 0;
+    for (uint32_t t = 0; t < p * p; ++t) {
+        uint32_t i = seq ? seq[2 * t] : 0, j = seq ? seq[2 * t + 1] : 0;
+        acquire(t, &i, &j);
+        if (i >= p || j >= p) throw ConfigError("bucket out of range");
+        const uint64_t lo = offsets[(size_t)i * p + j], hi = offsets[(size_t)i * p + j + 1];
+        for (uint64_t b0 = 0, k = 0; lo + b0 < hi; b0 += E.cap_b, ++k) {
+            const uint32_t nb = (uint32_t)std::min<uint64_t>(E.cap_b, hi - lo - b0);
+            E.train_batch(edges + 3 * lo, hi - lo, b0, nb, i, j, epoch, t, (uint32_t)k, losses ? losses + slot : nullptr);
+            ++slot;
+        }
+        release(t);
+    }
+    if (stats) {
+        std::vector<float> h(nbatch);
+        if (nbatch) {
+            EMBER_CUDA(cudaMemcpyAsync(h.data(), losses, nbatch * sizeof(float), cudaMemcpyDeviceToHost, E.stream));
+            EMBER_CUDA(cudaFreeAsync(losses, E.stream));
+        }
+        EMBER_CUDA(cudaStreamSynchronize(E.stream));
+        for (float x : h) stats->loss_sum += x;
+        stats->batches += nbatch;
+        stats->edges += n_edges;
+    }
+}
+}  // namespace
+
 extern "C" {
 
 const char* ember_last_error(void) { return g_err.c_str(); }
@@ -463,6 +506,7 @@ int ember_buffer_decisions(ember_buffer* b, uint32_t* out, uint32_t* n) {
     });
 }
 
+
 int ember_train_epoch_buffered(ember_ctx* ctx, ember_buffer* b, const uint32_t* edges, const uint64_t* offsets,
                                uint64_t epoch, ember_step_stats* stats) {
     return guarded([&] {
@@ -471,39 +515,22 @@ int ember_train_epoch_buffered(ember_ctx* ctx, ember_buffer* b, const uint32_t* 
         if (&buffer_engine(&B) != &E) throw ConfigError("buffer belongs to another context");
         need(edges, "edges_dev");
         need(offsets, "offsets_host");
-        const uint32_t p = E.g.num_partitions;
-        uint64_t nbatch = 0, n_edges = 0;
-        for (uint64_t k = 0; k < (uint64_t)p * p; ++k) {
-            if (offsets[k + 1] < offsets[k]) throw ConfigError("offsets must be non-decreasing");
-            nbatch += (offsets[k + 1] - offsets[k] + E.cap_b - 1) / E.cap_b;
-        }
-        n_edges = offsets[(size_t)p * p] - offsets[0];
-        float* losses = nullptr;  // one slot per batch, read once at the end (no per-bucket sync)
-        if (stats && nbatch) EMBER_CUDA(cudaMallocAsync(&losses, nbatch * sizeof(float), E.stream));
-        uint64_t slot = 0;
-        for (uint32_t t = 0; t < p * p; ++t) {
-            uint32_t i = 0, j = 0;
-            buffer_acquire(&B, t, &i, &j);
-            const uint64_t lo = offsets[(size_t)i * p + j], hi = offsets[(size_t)i * p + j + 1];
-            for (uint64_t b0 = 0, k = 0; lo + b0 < hi; b0 += E.cap_b, ++k) {
-                const uint32_t nb = (uint32_t)std::min<uint64_t>(E.cap_b, hi - lo - b0);
-                E.train_batch(edges + 3 * lo, hi - lo, b0, nb, i, j, epoch, t, (uint32_t)k,
-                              losses ? losses + slot : nullptr);
-                ++slot;
-            }
-            buffer_release(&B, t);
-        }
-        if (stats) {
-            std::vector<float> h(nbatch);
-            if (nbatch) {
-                EMBER_CUDA(cudaMemcpyAsync(h.data(), losses, nbatch * sizeof(float), cudaMemcpyDeviceToHost, E.stream));
-                EMBER_CUDA(cudaFreeAsync(losses, E.stream));
-            }
-            EMBER_CUDA(cudaStreamSynchronize(E.stream));
-            for (float x : h) stats->loss_sum += x;
-            stats->batches += nbatch;
-            stats->edges += n_edges;
-        }
+        train_epoch_impl(
+            E, edges, offsets, nullptr, epoch, stats, [&](uint32_t t, uint32_t* i, uint32_t* j) { buffer_acquire(&B, t, i, j); },
+            [&](uint32_t t) { buffer_release(&B, t); });
+    });
+}
+
+int ember_train_epoch(ember_ctx* ctx, const uint32_t* edges, const uint64_t* offsets, const uint32_t* seq,
+                      uint64_t epoch, ember_step_stats* stats) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        need(edges, "edges_dev");
+        need(offsets, "offsets_host");
+        need(seq, "seq");
+        for (uint32_t k = 0; k < E.g.num_partitions; ++k) E.view(k);  // every partition bound
+        train_epoch_impl(E, edges, offsets, seq, epoch, stats, [](uint32_t, uint32_t*, uint32_t*) {},
+                         [](uint32_t) {});
     });
 }
 
@@ -532,6 +559,13 @@ int ember_relations_apply_dense(ember_ctx* ctx, const float* grad) {
         Engine& E = eng(ctx);
         need(grad, "grad_dev");
         E.apply_relations_dense(grad);
+    });
+}
+
+int ember_overflow_rows(ember_ctx* ctx, uint64_t* total) {
+    return guarded([&] {
+        need(total, "total");
+        *total = tc_overflow_rows(eng(ctx));
     });
 }
 

@@ -272,5 +272,6 @@ void launch_eval_ranks(const Engine& E, const uint32_t* test, uint32_t n_test, c
 bool tc_engine_supported(const Engine& E);
 void tc_setup(Engine& E);
 void tc_release(Engine& E);
+uint64_t tc_overflow_rows(Engine& E);
 
 }  // namespace ember

@@ -552,8 +552,9 @@ __device__ __forceinline__ float packed_at(const uint16_t* pk, int cap, int CB, 
 __global__ void k_tc_fixup(TcArgs g, const uint16_t* __restrict__ Apk, const uint16_t* __restrict__ Npk) {
     griddep_wait();
     const uint32_t n = *(volatile uint32_t*)g.flags;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (uint32_t f = warp; f < n; f += nw) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t f = gw; f < n; f += nw) {  // a warp per flagged row, all blocks
         const uint32_t code = g.flags[1 + f];
         const int side = (int)(code / g.b_cap), row = (int)(code % g.b_cap);
         // operands as the tensor cores saw them (hi + lo), rows of at most 128 floats: 4 per lane
@@ -589,12 +590,12 @@ __global__ void k_tc_fixup(TcArgs g, const uint16_t* __restrict__ Apk, const uin
         }
     }
     // streamed 96-row tiles may reach past the last 128-row item: those rows never score
-    for (int i = threadIdx.x; i < 2 * (g.rows_pad - g.rows128); i += blockDim.x) {
-        const int side = i / (g.rows_pad - g.rows128), row = g.rows128 + i % (g.rows_pad - g.rows128);
-        g.lse_pad[(size_t)side * g.b_cap + row] = -INFINITY;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && n) *g.flags = 0u;
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i < 2 * (g.rows_pad - g.rows128); i += blockDim.x) {
+            const int side = i / (g.rows_pad - g.rows128), row = g.rows128 + i % (g.rows_pad - g.rows128);
+            g.lse_pad[(size_t)side * g.b_cap + row] = -INFINITY;
+        }
+    // (the flag count is reset by k_dn_reduce, after every reader)
 }
 
 // =========================================================================================
@@ -605,8 +606,13 @@ __global__ void k_tc_fixup(TcArgs g, const uint16_t* __restrict__ Apk, const uin
 // goes to its sorted position grows[rank[slot]]. Thread per (side, column block, negative): the
 // column-blocked partials [chunk][side][d/4][n_pad] float4 are read coalesced along n.
 __global__ void k_dn_reduce(const float4* __restrict__ part, int chunks, int nt, int n_pad, int d,
-                            const uint32_t* __restrict__ rank, uint32_t slot0, float* __restrict__ out) {
+                            const uint32_t* __restrict__ rank, uint32_t slot0, float* __restrict__ out,
+                            uint32_t* flags, unsigned long long* flags_total) {
     griddep_wait();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // overflow list consumed (k_tc_fixup): count, reset
+        flags_total[0] += flags[0];
+        *flags = 0u;
+    }
     const int d4 = d / 4;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= (int64_t)2 * d4 * nt) return;
@@ -675,8 +681,9 @@ struct TcState {
     float* dN_part = nullptr;
     float* lse_pad = nullptr;
     uint32_t* flags = nullptr;
+    unsigned long long* flags_total = nullptr;  // overflowed rows recomputed exactly, since creation
     CUtensorMap mA128, mA96, mN128, mN96;  // resident (RES rows) and streamed (TILE rows) boxes
-    float zmax = 1e24f;
+    float zmax = 1e30f;  // sum exp(S - f_pos) above this: exact recompute (fp32 and the P.N sums stay finite)
     int max_grid = 0;  // test hook (EMBER_TC_MAXGRID): several items per CTA at small sizes
     unsigned long long* trace = nullptr;  // EMBER_TC_TRACE=<file prefix>: CTA-0 timeline dump
     std::string trace_path;
@@ -711,6 +718,8 @@ void tc_setup(Engine& E) {
     EMBER_CUDA(cudaMalloc(&t->lse_pad, (size_t)2 * t->b_cap * sizeof(float)));
     EMBER_CUDA(cudaMalloc(&t->flags, (size_t)(1 + 2 * t->b_cap) * sizeof(uint32_t)));
     EMBER_CUDA(cudaMemset(t->flags, 0, sizeof(uint32_t)));
+    EMBER_CUDA(cudaMalloc(&t->flags_total, sizeof(unsigned long long)));
+    EMBER_CUDA(cudaMemset(t->flags_total, 0, sizeof(unsigned long long)));
     t->mA128 = make_map(E.s.Apk, t->b_cap, t->CB, RES);
     t->mA96 = make_map(E.s.Apk, t->b_cap, t->CB, TILE);
     t->mN128 = make_map(E.s.Npk, t->n_pad, t->CB, RES);
@@ -722,11 +731,20 @@ void tc_setup(Engine& E) {
     E.tc = t;
 }
 
+uint64_t tc_overflow_rows(Engine& E) {
+    if (!E.tc) return 0;
+    unsigned long long v = 0;
+    EMBER_CUDA(cudaStreamSynchronize(E.stream));
+    EMBER_CUDA(cudaMemcpy(&v, E.tc->flags_total, sizeof(v), cudaMemcpyDeviceToHost));
+    return v;
+}
+
 void tc_release(Engine& E) {
     if (!E.tc) return;
     cudaFree(E.tc->dN_part);
     cudaFree(E.tc->lse_pad);
     cudaFree(E.tc->flags);
+    cudaFree(E.tc->flags_total);
     if (E.tc->trace) cudaFree(E.tc->trace);
     delete E.tc;
     E.tc = nullptr;
@@ -789,7 +807,10 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
         dump(".rows.bin");
         EMBER_CUDA(cudaMemsetAsync(t.trace, 0, (size_t)2 * 5 * TRACE_ROLE * 8, E.stream));
     }
-    launch_pdl(k_tc_fixup, dim3(1), dim3(1024), 0, E.stream, a, (const uint16_t*)s.Apk, (const uint16_t*)s.Npk);
+    // normally no row is flagged and every block exits at once; when training drives scores far
+    // apart the flagged rows are spread over the whole GPU (a warp each)
+    launch_pdl(k_tc_fixup, dim3(E.sm_count * 2), dim3(256), 0, E.stream, a, (const uint16_t*)s.Apk,
+               (const uint16_t*)s.Npk);
     EMBER_LAUNCHED(E);
     const int items2 = 2 * ((nt + RES - 1) / RES) * a.chunks2;
     launch_pdl(k_tc<MODE_NEGS>, dim3(std::min(items2, gmax)), dim3(NTHREADS), smem_total(t.KP, t.nstage, MODE_NEGS),
@@ -800,7 +821,7 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
     E.join_sorted();
     launch_pdl(k_dn_reduce, dim3((unsigned)((r + 255) / 256)), dim3(256), 0, E.stream,
                reinterpret_cast<const float4*>(t.dN_part), a.chunks2, nt, t.n_pad, d, (const uint32_t*)s.rank, 2 * nb,
-               s.grows);
+               s.grows, t.flags, t.flags_total);
     EMBER_LAUNCHED(E);
 }
 
