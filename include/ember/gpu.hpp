@@ -63,6 +63,14 @@ public:
         return st;
     }
 
+    // train_epoch_partitioned: the plan's bucket sequence (2 u32 per bucket) in one call.
+    ember_step_stats train_epoch(const uint32_t* edges_dev, const std::vector<uint64_t>& bucket_offsets,
+                                 const std::vector<uint32_t>& seq, uint64_t epoch) {
+        ember_step_stats st{};
+        check(ember_train_epoch(ctx_, edges_dev, bucket_offsets.data(), seq.data(), epoch, &st));
+        return st;
+    }
+
 private:
     void reset() {
         if (ctx_) ember_ctx_destroy(ctx_);
