@@ -484,6 +484,9 @@ def _oracle_sample(W_or_graph, cfg, rows_per_step, max_steps, budget_s, threads=
     m = po.model(cfg["kind"], dim=cfg["dim"], lr=0.1, eps=1e-10, n_t=cfg["nt"], alpha=cfg["alpha"], chunks=1,
                  seed=NEG_SEED)
     L = po.lib()
+    all_threads = L.orc_num_threads()
+    if threads:
+        L.orc_set_num_threads(threads)
     done_edges, t_total, n = 0, 0.0, 0
     V, p, d = cfg["V"], cfg["p"], cfg["dim"]
     for (lo, hi, begin, nb, i, j, step, k) in batches:
@@ -513,7 +516,10 @@ def _oracle_sample(W_or_graph, cfg, rows_per_step, max_steps, budget_s, threads=
         t_total += time.perf_counter() - t0
         done_edges += nbat
         n += 1
-    return done_edges, t_total, n, L.orc_num_threads()
+    used = L.orc_num_threads()
+    if threads:
+        L.orc_set_num_threads(all_threads)
+    return done_edges, t_total, n, used
 
 
 def _init_many(po, ids, d):
@@ -531,10 +537,13 @@ def cpu_baseline(W, args, budget_s=20.0):
     start = len(W.batches) // 3
     rows = min(cfg["b"], args.cpu_rows)
     done, t, n, thr = _oracle_sample((edges_fn, W.offsets, W.batches[start:]), cfg, rows, 1000, budget_s)
+    # the 1-thread rate beside the all-core one (a shorter window of the same stream)
+    d1, t1, n1, _ = _oracle_sample((edges_fn, W.offsets, W.batches[start:]), cfg, rows, 1000, budget_s / 4, threads=1)
     return {"value": round(done / t, 1), "unit": "edges/s", "cores": thr, "kind": "port",
+            "single_thread_value": round(d1 / t1, 1),
             "sample": f"{n} batch samples x {rows} positives (of b={cfg['b']}) with the batch's full "
                       f"{cfg['nt']}-per-side shared negatives; CPU oracle (oracle/ember_oracle.c, OpenMP), "
-                      f"{t:.1f} s of CPU work"}
+                      f"{t:.1f} s of CPU work on {thr} threads (+ {n1} samples, {t1:.1f} s on 1 thread)"}
 
 
 def bench_reference(args, rank, world):

@@ -106,6 +106,7 @@ void orc_preprocess(const uint32_t* raw, uint64_t n, uint32_t p, uint64_t seed, 
                     uint32_t* node_tokens, uint32_t* rel_tokens, uint64_t* num_nodes, uint32_t* num_rel);
 
 int orc_num_threads(void);
+void orc_set_num_threads(int n);  /* OpenMP team size of later calls (bench: 1-thread leg) */
 
 #ifdef __cplusplus
 }

@@ -83,6 +83,7 @@ def lib():
         L.orc_preprocess.argtypes = [u32p, C.c_uint64, C.c_uint32, C.c_uint64, C.c_float, C.c_float, u32p, u64p, u32p,
                                      u32p, u64p, u32p, u32p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32)]
         L.orc_num_threads.restype = C.c_int
+        L.orc_set_num_threads.argtypes = [C.c_int]
         _ORACLE = L
     return _ORACLE
 
