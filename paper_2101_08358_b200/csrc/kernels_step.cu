@@ -944,6 +944,35 @@ __device__ __forceinline__ float4 sum_rows_strided(const float* base, uint32_t r
     return s;
 }
 
+// The same for two column blocks at once (c4a, and c4b when hasb): 8 loads in flight, and per
+// column the same row order (bit-identical to two sum_rows_strided passes).
+__device__ __forceinline__ void sum_rows_strided2(const float* base, uint32_t r0, uint32_t step, uint32_t cnt,
+                                                  uint32_t d, uint32_t c4a, uint32_t c4b, bool hasb, float4& sa,
+                                                  float4& sb) {
+    sa = make_float4(0.f, 0.f, 0.f, 0.f);
+    sb = sa;
+    uint32_t r = r0;
+    for (; r + 3 * step < cnt; r += 4 * step) {
+        float4 x[4], y[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) x[i] = ldg4(base + (uint64_t)(r + i * step) * d + 4 * c4a);
+        if (hasb) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) y[i] = ldg4(base + (uint64_t)(r + i * step) * d + 4 * c4b);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) add4(sa, x[i]);
+        if (hasb) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) add4(sb, y[i]);
+        }
+    }
+    for (; r < cnt; r += step) {
+        add4(sa, ldg4(base + (uint64_t)r * d + 4 * c4a));
+        if (hasb) add4(sb, ldg4(base + (uint64_t)r * d + 4 * c4b));
+    }
+}
+
 __device__ __forceinline__ float4 shfl_xor4(float4 v, int m) {
     v.x = __shfl_xor_sync(0xffffffffu, v.x, m);
     v.y = __shfl_xor_sync(0xffffffffu, v.y, m);
@@ -964,13 +993,22 @@ __global__ void k_long_partial(SegArgs a) {
         const uint32_t u = rec[0], c = sl - rec[1];
         const uint32_t r0 = c * LONG_CHUNK, cnt = min(LONG_CHUNK, a.counts[u] - r0);
         const float* base = a.rows + ((uint64_t)a.offsets[u] + r0) * a.d;
-        for (uint32_t c0 = 0; c0 < d4; c0 += 16) {  // warp-uniform trip count (shuffles below)
-            const uint32_t c4 = c0 + hl;
-            float4 v = c4 < d4 ? sum_rows_strided(base, half, 2, cnt, a.d, c4) : make_float4(0.f, 0.f, 0.f, 0.f);
-            const float4 o = shfl_xor4(v, 16);
-            if (half == 0 && c4 < d4) {
-                add4(v, o);  // even rows + odd rows
-                reinterpret_cast<float4*>(a.partial + (uint64_t)sl * a.d)[c4] = v;
+        for (uint32_t c0 = 0; c0 < d4; c0 += 32) {  // warp-uniform trip count (shuffles below)
+            const uint32_t c4 = c0 + hl, c4b = c4 + 16;
+            const bool hasa = c4 < d4, hasb = c4b < d4;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f), vb = v;
+            if (hasa) sum_rows_strided2(base, half, 2, cnt, a.d, c4, c4b, hasb, v, vb);
+            const float4 o = shfl_xor4(v, 16), ob = shfl_xor4(vb, 16);
+            if (half == 0) {  // even rows + odd rows
+                float4* out = reinterpret_cast<float4*>(a.partial + (uint64_t)sl * a.d);
+                if (hasa) {
+                    add4(v, o);
+                    out[c4] = v;
+                }
+                if (hasb) {
+                    add4(vb, ob);
+                    out[c4b] = vb;
+                }
             }
         }
     }
@@ -992,8 +1030,12 @@ __global__ void __launch_bounds__(32 * LONG_WARPS) k_long_final(SegArgs a) {
         const uint32_t* rec = a.longs + 2 + 3 * li;
         const uint32_t u = rec[0], base = rec[1], nch = rec[2];
         if (nch <= LONG_BIG) continue;  // block-uniform
-        for (uint32_t c4 = hl; c4 < d4; c4 += 16)
-            wsum[stream * d4 + c4] = sum_rows_strided(a.partial + (uint64_t)base * a.d, stream, NS, nch, a.d, c4);
+        for (uint32_t c4 = hl; c4 < d4; c4 += 32) {
+            float4 va, vb;
+            sum_rows_strided2(a.partial + (uint64_t)base * a.d, stream, NS, nch, a.d, c4, c4 + 16, c4 + 16 < d4, va, vb);
+            wsum[stream * d4 + c4] = va;
+            if (c4 + 16 < d4) wsum[stream * d4 + c4 + 16] = vb;
+        }
         __syncthreads();
         if (threadIdx.x < 32) {
             const SegTarget t = seg_target(a, u, nr, lane == 0);
@@ -1019,18 +1061,33 @@ __global__ void __launch_bounds__(32 * LONG_WARPS) k_long_final(SegArgs a) {
         if (nch > LONG_BIG) continue;  // warp-uniform
         const SegTarget t = seg_target(a, u, nr, lane == 0);
         const bool app = seg_applies(a, t);
-        for (uint32_t c0 = 0; c0 < d4; c0 += 16) {  // warp-uniform trip count (shuffles below)
-            const uint32_t c4 = c0 + hl;
-            float4 th = make_float4(0.f, 0.f, 0.f, 0.f), ac = th;
-            if (app && half == 0 && c4 < d4) {
-                th = reinterpret_cast<const float4*>(t.th)[c4];
-                ac = reinterpret_cast<const float4*>(t.ac)[c4];
+        for (uint32_t c0 = 0; c0 < d4; c0 += 32) {  // warp-uniform trip count (shuffles below)
+            const uint32_t c4 = c0 + hl, c4b = c4 + 16;
+            const bool hasa = c4 < d4, hasb = c4b < d4;
+            const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+            float4 th = z, ac = z, thb = z, acb = z;
+            if (app && half == 0) {
+                if (hasa) {
+                    th = reinterpret_cast<const float4*>(t.th)[c4];
+                    ac = reinterpret_cast<const float4*>(t.ac)[c4];
+                }
+                if (hasb) {
+                    thb = reinterpret_cast<const float4*>(t.th)[c4b];
+                    acb = reinterpret_cast<const float4*>(t.ac)[c4b];
+                }
             }
-            float4 g = c4 < d4 ? sum_rows_strided(a.partial + (uint64_t)base * a.d, half, 2, nch, a.d, c4) : th;
-            const float4 o = shfl_xor4(g, 16);
-            if (half == 0 && c4 < d4) {
-                add4(g, o);
-                seg_finish(a, t, c4, g, th, ac);
+            float4 g = z, gb = z;
+            if (hasa) sum_rows_strided2(a.partial + (uint64_t)base * a.d, half, 2, nch, a.d, c4, c4b, hasb, g, gb);
+            const float4 o = shfl_xor4(g, 16), ob = shfl_xor4(gb, 16);
+            if (half == 0) {
+                if (hasa) {
+                    add4(g, o);
+                    seg_finish(a, t, c4, g, th, ac);
+                }
+                if (hasb) {
+                    add4(gb, ob);
+                    seg_finish(a, t, c4b, gb, thb, acb);
+                }
             }
         }
     }
