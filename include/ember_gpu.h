@@ -141,8 +141,15 @@ int ember_loss_and_grad(ember_ctx* ctx, const uint32_t* edges_dev, uint32_t nb, 
                         const uint32_t* negs_dev, float* fpos_dev, float* lse_dev, uint32_t* node_ids_dev,
                         float* node_rows_dev, uint32_t* n_node_host, uint32_t* rel_ids_dev, float* rel_rows_dev,
                         uint32_t* n_rel_host, double* loss_host);
+/* ParameterSlice gather (getGpuParameters): exactly one row per id,
+ * in id order. Node ids (global) must lie in partition i or j; relations != 0: relation ids.
+ * theta_out_dev: n x dim f32; acc_out_dev (nullable) likewise. Synchronises the stream (status 1
+ * and nothing written for the offending rows when an id is out of range). */
+int ember_gather(ember_ctx* ctx, const uint32_t* ids_dev, uint32_t n, uint32_t i, uint32_t j, int relations,
+                 float* theta_out_dev, float* acc_out_dev);
 /* adagrad_step on n rows of bucket (i, j)'s node tables (relations != 0: the
- * relation table). ids/rows device. */
+ * relation table). ids/rows device. Synchronises the stream; ids outside partitions i and j (or
+ * outside [0, R)) are not written and make the call return status 1. */
 int ember_adagrad_apply(ember_ctx* ctx, const uint32_t* ids_dev, const float* rows_dev, uint32_t n, uint32_t i,
                         uint32_t j, int relations);
 /* Scores S[r][k] = f(edge r, negative k) for the first `rows` edges of a batch against chunk 0's

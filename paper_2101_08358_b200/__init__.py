@@ -295,6 +295,17 @@ class Trainer:
     def adagrad_apply(self, ids, rows, i=0, j=0, relations=False):
         check(lib().ember_adagrad_apply(self.ctx, _ptr(ids), _ptr(rows), int(ids.numel()), i, j, 1 if relations else 0))
 
+    def gather(self, ids, i=0, j=0, relations=False, with_acc=True):
+        """ParameterSlice gather: (theta, acc) rows of `ids` (device u32), one per
+        id in order; node ids must lie in partition i or j (ConfigError otherwise)."""
+        t = self.torch
+        n = int(ids.numel())
+        th = t.empty((n, self.h.dim), dtype=t.float32, device=self.dev)
+        ac = t.empty_like(th) if with_acc else None
+        check(lib().ember_gather(self.ctx, _ptr(ids), n, i, j, 1 if relations else 0, _ptr(th),
+                                 _ptr(ac) if ac is not None else None))
+        return th, ac
+
     def debug_scores(self, edges, negs, side=0, rows=None, i=0, j=0):
         t = self.torch
         rows = int(edges.shape[0]) if rows is None else rows

@@ -72,6 +72,7 @@ def _declare(L):
         "ember_loss_and_grad": (C.c_int, [vp, vp, u32, u32, u32, vp, vp, vp, vp, vp, C.POINTER(u32), vp, vp,
                                           C.POINTER(u32), C.POINTER(C.c_double)]),
         "ember_adagrad_apply": (C.c_int, [vp, vp, vp, u32, u32, u32, i32]),
+        "ember_gather": (C.c_int, [vp, vp, u32, u32, u32, i32, vp, vp]),
         "ember_debug_scores": (C.c_int, [vp, vp, u32, u32, u32, vp, i32, u32, vp]),
         "ember_eval_ranks": (C.c_int, [vp, vp, u32, vp, u64, u32, f32, u32, u64, vp]),
         "ember_eval_ranks_filtered": (C.c_int, [vp, vp, u32, vp, u64, vp]),

@@ -316,12 +316,50 @@ int ember_adagrad_apply(ember_ctx* ctx, const uint32_t* ids, const float* rows, 
         if (!n) return;
         need(ids, "ids_dev");
         need(rows, "rows_dev");
+        uint32_t* bad = nullptr;
+        EMBER_CUDA(cudaMallocAsync(&bad, sizeof(uint32_t), E.stream));
+        EMBER_CUDA(cudaMemsetAsync(bad, 0, sizeof(uint32_t), E.stream));
         if (relations) {
             if (!E.rel_theta) throw ConfigError("relation table not bound");
-            launch_adagrad_rows(E, ids, rows, n, E.parts[0], E.parts[0], true);
+            launch_adagrad_rows(E, ids, rows, n, E.parts[0], E.parts[0], true, bad);
         } else {
-            launch_adagrad_rows(E, ids, rows, n, E.view(i), E.view(j), false);
+            E.check_bucket(i, j);
+            launch_adagrad_rows(E, ids, rows, n, E.view(i), E.view(j), false, bad);
         }
+        uint32_t nbad = 0;
+        EMBER_CUDA(cudaMemcpyAsync(&nbad, bad, sizeof(uint32_t), cudaMemcpyDeviceToHost, E.stream));
+        EMBER_CUDA(cudaFreeAsync(bad, E.stream));
+        EMBER_CUDA(cudaStreamSynchronize(E.stream));
+        if (nbad)
+            throw ConfigError(std::to_string(nbad) + (relations ? " relation ids out of range (rows not updated)"
+                                                              : " node ids outside partitions i and j (rows not updated)"));
+    });
+}
+
+int ember_gather(ember_ctx* ctx, const uint32_t* ids, uint32_t n, uint32_t i, uint32_t j, int relations,
+                 float* theta_out, float* acc_out) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        if (!n) return;
+        need(ids, "ids_dev");
+        need(theta_out, "theta_out_dev");
+        uint32_t* bad = nullptr;
+        EMBER_CUDA(cudaMallocAsync(&bad, sizeof(uint32_t), E.stream));
+        EMBER_CUDA(cudaMemsetAsync(bad, 0, sizeof(uint32_t), E.stream));
+        if (relations) {
+            if (!E.rel_theta) throw ConfigError("relation table not bound");
+            launch_gather_rows(E, ids, n, E.parts[0], E.parts[0], true, theta_out, acc_out, bad);
+        } else {
+            E.check_bucket(i, j);
+            launch_gather_rows(E, ids, n, E.view(i), E.view(j), false, theta_out, acc_out, bad);
+        }
+        uint32_t nbad = 0;
+        EMBER_CUDA(cudaMemcpyAsync(&nbad, bad, sizeof(uint32_t), cudaMemcpyDeviceToHost, E.stream));
+        EMBER_CUDA(cudaFreeAsync(bad, E.stream));
+        EMBER_CUDA(cudaStreamSynchronize(E.stream));
+        if (nbad)
+            throw ConfigError(std::to_string(nbad) + (relations ? " relation ids out of range"
+                                                              : " node ids outside partitions i and j"));
     });
 }
 

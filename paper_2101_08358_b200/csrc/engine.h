@@ -262,7 +262,10 @@ void launch_loss(const Engine& E, uint32_t nb, float* loss_out);
 void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool apply, bool rel_dense,
                      uint32_t* node_ids_out, float* node_rows_out, uint32_t* rel_ids_out, float* rel_rows_out);
 void launch_adagrad_rows(const Engine& E, const uint32_t* ids, const float* rows, uint32_t n, const PartView& pi,
-                         const PartView& pj, bool relations);
+                         const PartView& pj, bool relations,
+                         uint32_t* bad);
+void launch_gather_rows(const Engine& E, const uint32_t* ids, uint32_t n, const PartView& pi, const PartView& pj,
+                        bool relations, float* th_out, float* ac_out, uint32_t* bad);
 void launch_init_rows(cudaStream_t st, float* theta, float* acc, uint64_t first_row, uint64_t rows, uint32_t dim,
                       uint64_t seed);
 void launch_debug_scores(const Engine& E, const uint32_t* edges, uint32_t nb, const uint32_t* negs, int side,

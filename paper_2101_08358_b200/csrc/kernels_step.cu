@@ -1095,16 +1095,24 @@ __global__ void __launch_bounds__(32 * LONG_WARPS) k_long_final(SegArgs a) {
 
 __global__ void k_adagrad_rows(const uint32_t* __restrict__ ids, const float* __restrict__ rows, uint32_t n,
                                uint32_t d, PartView pi, PartView pj, int relations, float* rel_theta, float* rel_acc,
-                               float lr, float eps) {
+                               uint32_t n_rel, float lr, float eps, uint32_t* bad) {
     const uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (u >= n) return;
     const uint32_t key = ids[u];
     float* th;
     float* ac;
     if (relations) {
+        if (key >= n_rel) {  // out of range: counted, never written
+            if (lane == 0) atomicAdd(bad, 1u);
+            return;
+        }
         th = rel_theta + (uint64_t)key * d;
         ac = rel_acc + (uint64_t)key * d;
     } else {
+        if (key - pi.first >= pi.rows && key - pj.first >= pj.rows) {
+            if (lane == 0) atomicAdd(bad, 1u);
+            return;
+        }
         const PartView& v = (key - pi.first < pi.rows) ? pi : pj;
         th = v.theta + (uint64_t)(key - v.first) * d;
         ac = v.acc + (uint64_t)(key - v.first) * d;
@@ -1298,10 +1306,53 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
 }
 
 void launch_adagrad_rows(const Engine& E, const uint32_t* ids, const float* rows, uint32_t n, const PartView& pi,
-                         const PartView& pj, bool relations) {
+                         const PartView& pj, bool relations, uint32_t* bad) {
     if (!n) return;
     k_adagrad_rows<<<(n * 32 + 255) / 256, 256, 0, E.stream>>>(ids, rows, n, E.dim, pi, pj, relations ? 1 : 0,
-                                                                E.rel_theta, E.rel_acc, E.m.lr, E.m.eps);
+                                                                E.rel_theta, E.rel_acc, E.g.num_relations, E.m.lr,
+                                                                E.m.eps, bad);
+    EMBER_LAUNCHED(E);
+}
+
+// ParameterSlice gather (getGpuParameters): warp per id, the theta
+// (and acc) row of a node of partition i or j, or of a relation, copied out in id order. Ids
+// outside both partitions (outside [0, R) for relations) are counted in *bad, their rows untouched.
+__global__ void k_gather_rows(const uint32_t* __restrict__ ids, uint32_t n, uint32_t d, PartView pi, PartView pj,
+                              int relations, const float* rel_theta, const float* rel_acc, uint32_t n_rel,
+                              float* th_out, float* ac_out, uint32_t* bad) {
+    const uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (u >= n) return;
+    const uint32_t key = ids[u];
+    const float* th;
+    const float* ac;
+    if (relations) {
+        if (key >= n_rel) {
+            if (lane == 0) atomicAdd(bad, 1u);
+            return;
+        }
+        th = rel_theta + (uint64_t)key * d;
+        ac = rel_acc + (uint64_t)key * d;
+    } else {
+        const bool in_i = key - pi.first < pi.rows, in_j = key - pj.first < pj.rows;
+        if (!in_i && !in_j) {
+            if (lane == 0) atomicAdd(bad, 1u);
+            return;
+        }
+        const PartView& v = in_i ? pi : pj;
+        th = v.theta + (uint64_t)(key - v.first) * d;
+        ac = v.acc + (uint64_t)(key - v.first) * d;
+    }
+    for (uint32_t k = lane; k < d; k += 32) {
+        th_out[(uint64_t)u * d + k] = th[k];
+        if (ac_out) ac_out[(uint64_t)u * d + k] = ac[k];
+    }
+}
+
+void launch_gather_rows(const Engine& E, const uint32_t* ids, uint32_t n, const PartView& pi, const PartView& pj,
+                        bool relations, float* th_out, float* ac_out, uint32_t* bad) {
+    if (!n) return;
+    k_gather_rows<<<(n * 32 + 255) / 256, 256, 0, E.stream>>>(ids, n, E.dim, pi, pj, relations ? 1 : 0, E.rel_theta,
+                                                               E.rel_acc, E.g.num_relations, th_out, ac_out, bad);
     EMBER_LAUNCHED(E);
 }
 

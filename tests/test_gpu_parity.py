@@ -116,6 +116,36 @@ def test_adagrad_bit_exact():
     assert rt.tobytes() == rt0.tobytes() and ra.tobytes() == ra0.tobytes()
 
 
+def test_gather_parameter_slice():
+    """ParameterSlice gather: one row per id, in id order, from partition i or j
+    (or the relation table), bit-exact copies; an id outside both partitions is a ConfigError."""
+    tr = make_trainer("complex", dim=40, V=3000, p=3)
+    for k in range(3):  # non-zero acc rows
+        lo, n = eb.partition_offset(3000, 3, k), eb.partition_size(3000, 3, k)
+        ids_k = np.arange(lo, lo + n, 7, dtype=np.uint32)
+        tr.adagrad_apply(_dev(ids_k), torch.ones((len(ids_k), 40), device="cuda"), k, k)
+    with pytest.raises(eb.ConfigError):  # an id outside partitions i and j is rejected, not written
+        tr.adagrad_apply(_dev(np.array([0], np.uint32)), torch.ones((1, 40), device="cuda"), 1, 2)
+    th, ac, rt, ra = host_tables(tr)
+    lo1, n1 = eb.partition_offset(3000, 3, 1), eb.partition_size(3000, 3, 1)
+    lo2, n2 = eb.partition_offset(3000, 3, 2), eb.partition_size(3000, 3, 2)
+    rng = np.random.default_rng(3)
+    ids = np.concatenate([rng.integers(lo1, lo1 + n1, 200), rng.integers(lo2, lo2 + n2, 100), [lo1, lo2 + n2 - 1]])
+    ids = ids.astype(np.uint32)
+    gth, gac = tr.gather(_dev(ids), 1, 2)
+    assert gth.cpu().numpy().tobytes() == th[ids].tobytes()
+    assert gac.cpu().numpy().tobytes() == ac[ids].tobytes()
+    gth, gac = tr.gather(_dev(ids[::-1].copy()), 2, 1, with_acc=False)
+    assert gac is None and gth.cpu().numpy().tobytes() == th[ids[::-1]].tobytes()
+    rid = np.array([19, 0, 7, 7], np.uint32)
+    rth, rac = tr.gather(_dev(rid), relations=True)
+    assert rth.cpu().numpy().tobytes() == rt[rid].tobytes() and rac.cpu().numpy().tobytes() == ra[rid].tobytes()
+    with pytest.raises(eb.ConfigError):
+        tr.gather(_dev(np.array([lo1, 0], np.uint32)), 1, 2)  # id 0 lives in partition 0
+    with pytest.raises(eb.ConfigError):
+        tr.gather(_dev(np.array([20], np.uint32)), relations=True)
+
+
 @pytest.mark.parametrize("engine", ENGINES)
 def test_training_trajectory_matches_oracle(graph, engine):
     """A few full steps (sample -> grads -> Adagrad) over two buckets; losses within 1e-4, tables
