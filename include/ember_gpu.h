@@ -8,6 +8,10 @@
  * device pointers are `T*` into memory on the context's device, host pointers are marked.
  * Every call returns EMBER_OK (0), EMBER_EUSER (1: bad config/arguments, the reference's
  * ConfigError) or EMBER_EINTERNAL (2: CUDA/IO failure, non-finite score);
+ * a non-finite batch loss is recorded on the device without a host sync and
+ * reported by the next synchronising call (ember_ctx_synchronize, ember_train_bucket/epoch with
+ * stats, ember_loss_and_grad) as status 2 with "non-finite loss in batch (epoch e, bucket step
+ * s, batch k)";
  * ember_last_error() returns the thread-local message (SPEC.md:552 exit codes).
  * No exceptions cross this boundary. One context per GPU, not thread-safe, all work is
  * enqueued on the context's stream ("the model computation stage only uses a

@@ -128,6 +128,7 @@ void train_epoch_impl(Engine& E, const uint32_t* edges, const uint64_t* offsets,
             EMBER_CUDA(cudaFreeAsync(losses, E.stream));
         }
         EMBER_CUDA(cudaStreamSynchronize(E.stream));
+        E.check_finite();
         for (float x : h) stats->loss_sum += x;
         stats->batches += nbatch;
         stats->edges += n_edges;
@@ -173,6 +174,7 @@ int ember_ctx_synchronize(ember_ctx* ctx) {
         Engine& E = eng(ctx);
         for (cudaStream_t st : {E.stream, E.side, E.io, E.io_out})
             if (st) EMBER_CUDA(cudaStreamSynchronize(st));
+        E.check_finite();  // a non-finite loss since the last check is an error naming its batch
     });
 }
 
@@ -246,6 +248,7 @@ void train_bucket(Engine& E, const uint32_t* bucket, uint64_t n, uint32_t i, uin
                 EMBER_CUDA(cudaFreeAsync(losses, E.stream));
             }
             EMBER_CUDA(cudaStreamSynchronize(E.stream));
+            E.check_finite();
             for (float x : h) loss_sum += x;
             stats->loss_sum += loss_sum;
             stats->batches += batches;
@@ -293,6 +296,7 @@ int ember_loss_and_grad(ember_ctx* ctx, const uint32_t* edges, uint32_t nb, uint
         if (nb == 0 || nb > E.cap_b) throw ConfigError("batch size must be in [1, batch_size]");
         E.check_bucket(i, j);
         E.loss_target = E.s.loss;
+        E.batch_tag = 1ull << 63;  // batch id 0 (a standalone batch)
         E.forward_backward(edges, nb, i, j, negs);
         launch_loss(E, nb, E.s.loss);
         if (fpos) EMBER_CUDA(cudaMemcpyAsync(fpos, E.s.fpos, nb * sizeof(float), cudaMemcpyDeviceToDevice, E.stream));
@@ -303,6 +307,7 @@ int ember_loss_and_grad(ember_ctx* ctx, const uint32_t* edges, uint32_t nb, uint
         EMBER_CUDA(cudaMemcpyAsync(counts, E.s.nunique, sizeof(counts), cudaMemcpyDeviceToHost, E.stream));
         EMBER_CUDA(cudaMemcpyAsync(&l, E.s.loss, sizeof(float), cudaMemcpyDeviceToHost, E.stream));
         EMBER_CUDA(cudaStreamSynchronize(E.stream));
+        E.check_finite();
         if (n_node) *n_node = counts[0];
         if (n_rel) *n_rel = E.m.kind == EMBER_DOT ? 0 : counts[1];
         if (loss) *loss = l;

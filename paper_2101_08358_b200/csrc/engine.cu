@@ -161,6 +161,8 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     s.loss_part = reinterpret_cast<float*>(dalloc<double>(std::max<uint64_t>(b / 512 + 2, 24ull * sm_count + 32)));
     s.loss_done = dalloc<uint32_t>(1);
     EMBER_CUDA(cudaMemset(s.loss_done, 0, sizeof(uint32_t)));
+    s.bad_batch = dalloc<unsigned long long>(1);
+    EMBER_CUDA(cudaMemset(s.bad_batch, 0, sizeof(unsigned long long)));
     s.keys = dalloc<uint32_t>(cap_rows);
     s.keys_sorted = dalloc<uint32_t>(cap_rows);
     s.vals = dalloc<uint32_t>(cap_rows);
@@ -222,7 +224,7 @@ Engine::~Engine() {
     tc_release(*this);
     // (the sort scratch is owned by sets[0..1]; s.* only points at the current one)
     void* ptrs[] = {s.batch, s.A,         s.N,      s.Apk,       s.Npk,     s.fpos,       s.lse,    s.g0,
-                    s.S,     s.dA,        s.dN_part, s.grows,    s.loss,    s.loss_part,  s.loss_done,
+                    s.S,     s.dA,        s.dN_part, s.grows,    s.loss,    s.loss_part,  s.loss_done,  s.bad_batch,
                     s.nunique, s.long_partial, s.rel_dense};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -415,6 +417,16 @@ void Engine::train_batch(const uint32_t* bucket, uint64_t bucket_n, uint64_t bat
     step(bucket + 3 * batch_begin, nb, bucket, bucket_n, i, j, epoch, bucket_step, batch_in_bucket, loss_out);
 }
 
+void Engine::check_finite() {
+    unsigned long long tag = 0;
+    EMBER_CUDA(cudaStreamSynchronize(stream));
+    EMBER_CUDA(cudaMemcpy(&tag, s.bad_batch, sizeof(tag), cudaMemcpyDeviceToHost));
+    if (!tag) return;
+    EMBER_CUDA(cudaMemset(s.bad_batch, 0, sizeof(tag)));
+    throw EmberError("non-finite loss in batch (epoch " + std::to_string((tag >> 40) & 0xFFFFF) + ", bucket step " +
+                     std::to_string((tag >> 20) & 0xFFFFF) + ", batch " + std::to_string(tag & 0xFFFFF) + ")");
+}
+
 void Engine::step(const uint32_t* edges, uint32_t nb, const uint32_t* bucket, uint64_t bucket_n, uint32_t i,
                   uint32_t j, uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket, float* loss_out,
                   cudaEvent_t edges_ready) {
@@ -440,6 +452,8 @@ void Engine::step(const uint32_t* edges, uint32_t nb, const uint32_t* bucket, ui
     EMBER_CUDA(cudaStreamWaitEvent(stream, ev_sampled, 0));
     direct_hi = getenv_direct() ? 2 * nb : 0;
     loss_target = loss_out ? loss_out : s.loss;
+    batch_tag = (1ull << 63) | ((epoch & 0xFFFFFull) << 40) | ((uint64_t)(bucket_step & 0xFFFFFu) << 20) |
+                (batch_in_bucket & 0xFFFFFu);
     forward_backward(edges, nb, i, j, s.negs, true);
     launch_loss(*this, nb, loss_out ? loss_out : s.loss);
     mark(PHASE_REDUCE);

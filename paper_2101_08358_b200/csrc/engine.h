@@ -87,6 +87,7 @@ struct Scratch {
     float* loss = nullptr;       // [1]
     float* loss_part = nullptr;  // per-block partial sums of the loss reduction
     uint32_t* loss_done = nullptr;
+    unsigned long long* bad_batch = nullptr;  // first batch whose loss was non-finite (sticky, 0 = none)
     uint32_t* keys = nullptr;
     uint32_t* keys_sorted = nullptr;
     uint32_t* vals = nullptr;
@@ -165,6 +166,9 @@ struct Engine {
     uint32_t direct_hi = 0;
     // where the step's loss goes; the tensor-core chain rule reduces it there itself (loss_fused)
     float* loss_target = nullptr;
+    // batch id of the step being enqueued ("non-finite score -> error carrying batch id")
+    unsigned long long batch_tag = 0;
+    void check_finite();  // throws EmberError (status 2) naming the first non-finite batch since the last check
     mutable bool loss_fused = false;
     // profiling: CUDA events at phase boundaries on the step stream + our own kernel launches
     bool prof_on = false;

@@ -466,7 +466,8 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
                                                       int direct, float lr, float eps,
                                                       const float* __restrict__ lse, const float* __restrict__ fpos,
                                                       double* __restrict__ loss_part, uint32_t* __restrict__ loss_done,
-                                                      float* __restrict__ loss_out) {
+                                                      float* __restrict__ loss_out, unsigned long long* bad,
+                                                      unsigned long long tag) {
     griddep_wait();
     extern __shared__ float4 cpbuf[];  // [warps][2 stages][CP_ROLES][32 lanes]
     const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -583,6 +584,7 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
     if (lane == 0) {
         loss_out[0] = (float)(v / (double)nb);
         *loss_done = 0u;
+        if (!isfinite(v)) atomicCAS(bad, 0ull, tag);  // SPEC.md:161, reported at the next sync
     }
 }
 
@@ -590,7 +592,8 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
 // order, the last block to finish adds the block partials in index order (deterministic).
 constexpr uint32_t LOSS_THREADS = 512;
 __global__ void k_loss(const float* __restrict__ lse, const float* __restrict__ fpos, uint32_t nb, uint32_t per_block,
-                       double* __restrict__ part, uint32_t* __restrict__ done, float* __restrict__ out) {
+                       double* __restrict__ part, uint32_t* __restrict__ done, float* __restrict__ out,
+                       unsigned long long* bad, unsigned long long tag) {
     griddep_wait();
     __shared__ double red[LOSS_THREADS];
     __shared__ bool last;
@@ -624,6 +627,7 @@ __global__ void k_loss(const float* __restrict__ lse, const float* __restrict__ 
     if (threadIdx.x == 0) {
         out[0] = (float)(red[0] / (double)nb);
         *done = 0u;
+        if (!isfinite(red[0])) atomicCAS(bad, 0ull, tag);  // SPEC.md:161, reported at the next sync
     }
 }
 
@@ -1234,7 +1238,8 @@ void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, cons
                    (const float*)E.rel_theta, E.m.kind, E.dim, (const float*)E.s.dA, (uint32_t)E.b_cap,
                    (const float*)E.s.g0, (const uint32_t*)E.s.rank, (const uint8_t*)E.s.uniq, E.s.grows,
                    E.direct_hi ? 1 : 0, E.m.lr, E.m.eps, (const float*)E.s.lse, (const float*)E.s.fpos,
-                   reinterpret_cast<double*>(E.s.loss_part), E.s.loss_done, E.loss_target);
+                   reinterpret_cast<double*>(E.s.loss_part), E.s.loss_done, E.loss_target, E.s.bad_batch,
+                   E.batch_tag);
         E.loss_fused = true;
     } else {
         k_chain_rule<<<(nb + warps - 1) / warps, warps * 32, 0, E.stream>>>(
@@ -1254,7 +1259,7 @@ void launch_loss(const Engine& E, uint32_t nb, float* loss_out) {
     const uint32_t per = LOSS_THREADS;  // ~100 blocks at b = 5e4: latency, not bandwidth
     const uint32_t blocks = (nb + per - 1) / per;
     launch_pdl(k_loss, dim3(blocks), dim3(LOSS_THREADS), 0, E.stream, (const float*)E.s.lse, (const float*)E.s.fpos, nb,
-               per, reinterpret_cast<double*>(E.s.loss_part), E.s.loss_done, loss_out);
+               per, reinterpret_cast<double*>(E.s.loss_part), E.s.loss_done, loss_out, E.s.bad_batch, E.batch_tag);
     EMBER_LAUNCHED(E);
 }
 

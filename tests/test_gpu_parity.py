@@ -147,6 +147,22 @@ def test_gather_parameter_slice():
 
 
 @pytest.mark.parametrize("engine", ENGINES)
+def test_non_finite_loss_is_an_error_naming_the_batch(graph, engine):
+    """a non-finite score is an error carrying the batch id. The step records it on the
+    device (no host sync in the step) and the next synchronising call returns status 2."""
+    edges, off, _ = graph
+    bucket = edges[off[1]:off[2]]
+    tr = make_trainer("complex", dim=32, b=256, nt=64, p=2, engine=engine)
+    tr.train_bucket(_dev(bucket), 0, 1, epoch=3, bucket_step=2)  # healthy: no error
+    tr.synchronize()
+    s = int(bucket[300, 0])  # source of an edge in batch 1 of the bucket (b = 256; batch 0 may draw it as a negative)
+    tr.theta[0][s - eb.partition_offset(3000, 2, 0), 0] = float("nan")
+    with pytest.raises(eb.EmberError, match=r"non-finite loss in batch \(epoch 4, bucket step 5, batch [01]\)"):
+        tr.train_bucket(_dev(bucket), 0, 1, epoch=4, bucket_step=5)
+    tr.synchronize()  # reported once
+
+
+@pytest.mark.parametrize("engine", ENGINES)
 def test_training_trajectory_matches_oracle(graph, engine):
     """A few full steps (sample -> grads -> Adagrad) over two buckets; losses within 1e-4, tables
     close (Adagrad's first step is ~ -lr*sign(g), so elements whose gradient is at rounding level can
