@@ -42,6 +42,11 @@ CONFIGS = {
                     train=0.9, valid=0.05, desc="Twitter-shaped graph, Dot d=100, 16 partitions"),
     "fb86m_d800": dict(V=86_054_151, R=14_824, E=338_586_276, kind="complex", dim=800, b=50_000, nt=1000, alpha=0.5,
                        p=16, train=0.9, valid=0.05, desc="Freebase86m-shaped KG, ComplEx d=800, 16 partitions"),
+    # C5's step (d = 800, b, n_t, |R| as C3) on 1/8 of the nodes and edges, so the 68.8 GB of tables
+    # fit one GPU; run with --engine simt (the tensor-core TMEM layout stops at d = 128)
+    "fb86m_d800_step": dict(V=10_756_769, R=14_824, E=42_323_284, kind="complex", dim=800, b=50_000, nt=1000,
+                            alpha=0.5, p=16, train=0.9, valid=0.05,
+                            desc="C5 step shape (ComplEx d=800, b=5e4, n_t=1e3) on 1/8 of Freebase86m's nodes/edges"),
 }
 METRIC = "train edges/sec (Freebase86m-shape ComplEx d=100, 16 partitions, BETA ordering)"
 GRAPH_SEED, INIT_SEED, NEG_SEED, ORDER_SEED = 210108358, 11, 1, 0
@@ -589,7 +594,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="fb86m", choices=sorted(CONFIGS))
-    ap.add_argument("--engine", default=os.environ.get("EMBER_ENGINE", "tc"), choices=["simt", "tc"])
+    ap.add_argument("--engine", default=os.environ.get("EMBER_ENGINE", "tc"), choices=["simt", "tc", "blas"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--cpu-rows", type=int, default=5000)
     ap.add_argument("--no-cpu", action="store_true")

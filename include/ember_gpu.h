@@ -42,6 +42,9 @@ extern "C" {
  * SIMT_FP32: CUDA-core fp32 tiles (correctness baseline). */
 #define EMBER_ENGINE_SIMT_FP32 0
 #define EMBER_ENGINE_TC_BF16X3 1
+/* the same bf16x3 arithmetic through cuBLAS bf16 GEMMs on materialised scores (any d; for d > 128,
+ * beyond the hand-written kernels' TMEM layout, e.g. config C5 d = 800); num_chunks must be 1 */
+#define EMBER_ENGINE_TC_BLAS 2
 
 /* OrderingKind (reference ordering.h:14) */
 #define EMBER_ORDER_ELIMINATION 0

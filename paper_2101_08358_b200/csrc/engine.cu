@@ -95,13 +95,16 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     : device(dev), m(md), g(gd) {
     if (m.kind < EMBER_DOT || m.kind > EMBER_COMPLEX) throw ConfigError("model kind must be 0 (Dot), 1 (DistMult), 2 (ComplEx)");
     if (m.dim == 0 || m.dim % 4 != 0) throw ConfigError("dim must be a positive multiple of 4");
+    if (m.dim > 1792) throw ConfigError("dim must be <= 1792 (long-segment reduction stages 32 rows in shared memory)");
     if (m.batch_size == 0) throw ConfigError("batch_size must be >= 1");
     if (!(m.alpha >= 0.f && m.alpha <= 1.f)) throw ConfigError("alpha must be in [0, 1]");
     if (!(m.eps > 0.f)) throw ConfigError("eps must be > 0 (SPEC.md:170)");
     if (g.num_partitions == 0 || g.num_nodes < g.num_partitions) throw ConfigError("need 1 <= p <= |V|");
     if (g.num_nodes > 0xffffffffULL) throw ConfigError("node ids are u32");
     if (m.kind != EMBER_DOT && g.num_relations == 0) throw ConfigError("DistMult/ComplEx need relations");
-    if (m.engine != EMBER_ENGINE_SIMT_FP32 && m.engine != EMBER_ENGINE_TC_BF16X3) throw ConfigError("unknown engine");
+    if (m.engine != EMBER_ENGINE_SIMT_FP32 && m.engine != EMBER_ENGINE_TC_BF16X3 && m.engine != EMBER_ENGINE_TC_BLAS)
+        throw ConfigError("unknown engine");
+    if (m.engine == EMBER_ENGINE_TC_BLAS && m.num_chunks > 1) throw ConfigError("blas engine: num_chunks must be 1");
     dim = m.dim;
     nt = m.num_negatives;
     chunks = m.num_chunks ? m.num_chunks : 1;
@@ -186,6 +189,13 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
         s.S = dalloc<float>(2 * b * (uint64_t)(nt ? nt : 1));
         s.dN_part = dalloc<float>((uint64_t)dsplit * n_neg * d);
     }
+    if (blas_engine()) {
+        s.S = dalloc<float>(2 * b * (uint64_t)(nt ? nt : 1));
+        s.dN_part = dalloc<float>((uint64_t)n_neg * d);
+        s.Ahl = dalloc<uint16_t>((uint64_t)2 * 2 * b * d);
+        s.Nhl = dalloc<uint16_t>((uint64_t)2 * 2 * (nt ? nt : 1) * d);
+        s.Phl = dalloc<uint16_t>((uint64_t)2 * 2 * b * (nt ? nt : 1));
+    }
     if (tc_engine()) {  // packed operand geometry: dim padded to 16, rows to 128- and 96-row tiles
         KP = (int)((dim + 15) / 16 * 16);
         CB = KP / 8;
@@ -214,6 +224,7 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     EMBER_CUDA(cudaEventCreateWithFlags(&ev_sampled, cudaEventDisableTiming));
     for (int k = 0; k < 2; ++k) EMBER_CUDA(cudaEventCreateWithFlags(&ev_set_free[k], cudaEventDisableTiming));
     if (tc_engine()) tc_setup(*this);
+    if (blas_engine()) blas_setup(*this);
     EMBER_CUDA(cudaStreamSynchronize(stream));
 }
 
@@ -222,9 +233,10 @@ Engine::~Engine() {
     if (stream) cudaStreamSynchronize(stream);
     if (side && side != stream) cudaStreamSynchronize(side);
     tc_release(*this);
+    blas_release(*this);
     // (the sort scratch is owned by sets[0..1]; s.* only points at the current one)
     void* ptrs[] = {s.batch, s.A,         s.N,      s.Apk,       s.Npk,     s.fpos,       s.lse,    s.g0,
-                    s.S,     s.dA,        s.dN_part, s.grows,    s.loss,    s.loss_part,  s.loss_done,  s.bad_batch,
+                    s.S,     s.dA,        s.dN_part, s.grows,    s.loss,    s.loss_part,  s.loss_done,  s.bad_batch, s.Ahl, s.Nhl, s.Phl,
                     s.nunique, s.long_partial, s.rel_dense};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -343,6 +355,8 @@ void Engine::forward_backward(const uint32_t* edges, uint32_t nb, uint32_t i, ui
     mark(PHASE_CONTRACT);
     if (tc_engine())
         launch_contract_tc(*this, nb);  // joins the sort before scattering dN rows
+    else if (blas_engine())
+        launch_contract_blas(*this, nb);
     else
         launch_contract_simt(*this, nb);
     // the next step's sampling + sort may start now: they overlap this step's memory-bound phase

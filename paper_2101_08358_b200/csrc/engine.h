@@ -81,6 +81,9 @@ struct Scratch {
     float* lse = nullptr;
     float* g0 = nullptr;
     float* S = nullptr;       // SIMT engine: [2][b][nt] scores -> P/b
+    void* Ahl = nullptr;      // blas engine: bf16 hi|lo splits of A [2][2][b][d], N [2][2][nt][d], P [2][2][b][nt]
+    void* Nhl = nullptr;
+    void* Phl = nullptr;
     float* dA = nullptr;
     float* dN_part = nullptr; // SIMT engine split-K partials
     float* grows = nullptr;
@@ -153,6 +156,8 @@ struct Engine {
     float* rel_acc = nullptr;
     Scratch s;
     TcState* tc = nullptr;
+    void* blas = nullptr;  // cublasHandle_t of the blas engine
+    bool blas_engine() const { return m.engine == EMBER_ENGINE_TC_BLAS; }
     // packed-operand geometry (tensor-core engine)
     int KP = 0, CB = 0, b_cap = 0, n_pad = 0;
     int sm_count = 148;
@@ -260,6 +265,9 @@ void launch_gather_negatives(const Engine& E, const uint32_t* negs, const PartVi
 void launch_keys(const Engine& E, const uint32_t* edges, uint32_t nb, const uint32_t* negs, const KeySpace& ks);
 void launch_rank(const Engine& E, uint32_t n);
 void launch_contract_simt(Engine& E, uint32_t nb);
+void launch_contract_blas(Engine& E, uint32_t nb);
+void blas_setup(Engine& E);
+void blas_release(Engine& E);
 void launch_contract_tc(Engine& E, uint32_t nb);
 void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj);
 void launch_loss(const Engine& E, uint32_t nb, float* loss_out);

@@ -7,7 +7,10 @@
 //   P  = softmax rows   (log-sum-exp with the positive as an extra column)
 //   dA = P N            (gradient wrt the adjusted vectors, before the positive term)
 //   dN = P^T A          (gradient of the shared negatives; split over rows, reduced in order)
+#include <cublas_v2.h>  // types and enums only: the library is bound at run time (dlopen)
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include "engine.h"
 
@@ -196,6 +199,135 @@ void launch_contract_simt(Engine& E, uint32_t nb) {
     E.join_sorted();
     k_sum_parts<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(s.dN_part, ks, total, total, (uint32_t)d, s.rank,
                                                                   2 * nb, s.grows);
+    EMBER_LAUNCHED(E);
+}
+
+// ---- EMBER_ENGINE_TC_BLAS: the same materialised-score contraction on tensor cores through
+// cuBLAS bf16 GEMMs with the bf16x3 split (hi.lo + lo.hi + hi.hi, fp32 accumulation: the
+// tensor-core engine's arithmetic), for d > 128 where the hand-written kernels' TMEM layout ends
+// (config C5, d = 800). cuBLAS is bound at run time from the process (torch's copy when loaded)
+// or the CUDA toolkit, so the library has no link-time dependency on it.
+namespace {
+
+struct BlasApi {
+    void* h = nullptr;
+    decltype(&cublasCreate_v2) create = nullptr;
+    decltype(&cublasDestroy_v2) destroy = nullptr;
+    decltype(&cublasSetStream_v2) set_stream = nullptr;
+    using GemmFn = cublasStatus_t (*)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int, int, const void*,
+                                      const void*, cudaDataType, int, long long, const void*, cudaDataType, int,
+                                      long long, const void*, void*, cudaDataType, int, long long, int,
+                                      cublasComputeType_t, cublasGemmAlgo_t);
+    GemmFn gemm = nullptr;
+};
+
+const BlasApi& blas_api() {
+    static BlasApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        for (const char* n : {"libcublas.so.12", "/usr/local/cuda/lib64/libcublas.so.12"})
+            if ((api.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+        if (api.h) {
+            api.create = reinterpret_cast<decltype(api.create)>(dlsym(api.h, "cublasCreate_v2"));
+            api.destroy = reinterpret_cast<decltype(api.destroy)>(dlsym(api.h, "cublasDestroy_v2"));
+            api.set_stream = reinterpret_cast<decltype(api.set_stream)>(dlsym(api.h, "cublasSetStream_v2"));
+            api.gemm = reinterpret_cast<decltype(api.gemm)>(dlsym(api.h, "cublasGemmStridedBatchedEx"));
+        }
+    }
+    if (!api.create || !api.destroy || !api.set_stream || !api.gemm)
+        throw EmberError("cuBLAS (libcublas.so.12) not loadable: the blas engine needs it");
+    return api;
+}
+
+void blas_check(cublasStatus_t st, const char* what) {
+    if (st != CUBLAS_STATUS_SUCCESS) throw EmberError(std::string("cuBLAS ") + what + " failed: status " + std::to_string((int)st));
+}
+
+// hi = bf16(x), lo = bf16(x - hi), elementwise (n multiple of 4 not required)
+__global__ void k_split_bf16(const float* __restrict__ x, uint64_t n, __nv_bfloat16* __restrict__ hi,
+                             __nv_bfloat16* __restrict__ lo) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const float v = x[i];
+        const __nv_bfloat16 h = __float2bfloat16_rn(v);
+        hi[i] = h;
+        lo[i] = __float2bfloat16_rn(v - __bfloat162float(h));
+    }
+}
+
+void split(const Engine& E, const float* x, uint64_t n, __nv_bfloat16* hi, __nv_bfloat16* lo) {
+    const unsigned blocks = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)E.sm_count * 16);
+    k_split_bf16<<<blocks, 256, 0, E.stream>>>(x, n, hi, lo);
+    EMBER_LAUNCHED(E);
+}
+
+// Column-major C[m x n] (+)= op(A) op(B) over 2 batches (the corruption sides), bf16x3.
+struct Split {
+    const __nv_bfloat16 *hi, *lo;
+    int ld;
+    long long stride;
+};
+void gemm3(const Engine& E, cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k, const Split& a,
+           const Split& b, float* c, int ldc, long long sc) {
+    const BlasApi& api = blas_api();
+    cublasHandle_t h = static_cast<cublasHandle_t>(E.blas);
+    const float one = 1.f, zero = 0.f;
+    const __nv_bfloat16* as[3] = {a.hi, a.lo, a.hi};
+    const __nv_bfloat16* bs[3] = {b.lo, b.hi, b.hi};  // small terms first, then hi.hi
+    for (int t = 0; t < 3; ++t)
+        blas_check(api.gemm(h, ta, tb, m, n, k, &one, as[t], CUDA_R_16BF, a.ld, a.stride, bs[t], CUDA_R_16BF, b.ld,
+                            b.stride, t ? &one : &zero, c, CUDA_R_32F, ldc, sc, 2, CUBLAS_COMPUTE_32F,
+                            CUBLAS_GEMM_DEFAULT),
+                   "gemm");
+    EMBER_LAUNCHED(E);
+}
+
+}  // namespace
+
+void blas_setup(Engine& E) {
+    const BlasApi& api = blas_api();
+    cublasHandle_t h = nullptr;
+    blas_check(api.create(&h), "create");
+    blas_check(api.set_stream(h, E.stream), "set stream");
+    E.blas = h;
+}
+
+void blas_release(Engine& E) {
+    if (E.blas) blas_api().destroy(static_cast<cublasHandle_t>(E.blas));
+    E.blas = nullptr;
+}
+
+void launch_contract_blas(Engine& E, uint32_t nb) {
+    const int d = (int)E.dim, nt = (int)E.nt, b = (int)nb;
+    Scratch& s = E.s;
+    using bf = __nv_bfloat16;
+    bf* Ahi = reinterpret_cast<bf*>(s.Ahl);
+    bf* Alo = Ahi + (size_t)2 * E.cap_b * d;
+    bf* Nhi = reinterpret_cast<bf*>(s.Nhl);
+    bf* Nlo = Nhi + (size_t)2 * nt * d;
+    bf* Phi = reinterpret_cast<bf*>(s.Phl);
+    bf* Plo = Phi + (size_t)2 * E.cap_b * nt;
+    // s.A: [2][nb][d] (side stride nb*d), s.N: [2][nt][d], s.S: [2][nb][nt] -- all row-major
+    split(E, s.A, (uint64_t)2 * b * d, Ahi, Alo);
+    split(E, s.N, (uint64_t)2 * nt * d, Nhi, Nlo);
+    const Split A{Ahi, Alo, d, (long long)b * d}, N{Nhi, Nlo, d, (long long)nt * d};
+    // 1) S = A N^T  (row-major [nb x nt]) == column-major S^T = N A^T
+    gemm3(E, CUBLAS_OP_T, CUBLAS_OP_N, nt, b, d, N, A, s.S, nt, (long long)b * nt);
+    // 2) softmax with the positive column: P = exp(S - lse) / nb in place
+    const uint32_t warps = 2 * nb;
+    k_softmax_rows<<<(warps * 32 + 255) / 256, 256, 0, E.stream>>>(s.S, s.fpos, s.lse, s.g0, nb, E.nt,
+                                                                   1.0f / (float)nb);
+    EMBER_LAUNCHED(E);
+    split(E, s.S, (uint64_t)2 * b * nt, Phi, Plo);
+    const Split P{Phi, Plo, nt, (long long)b * nt};
+    // 3) dA = P N  (row-major [nb x d]) == column-major dA^T = N^T P^T
+    gemm3(E, CUBLAS_OP_N, CUBLAS_OP_N, d, b, nt, N, P, s.dA, d, (long long)b * d);
+    // 4) dN = P^T A  (row-major [nt x d]) == column-major dN^T = A^T P
+    gemm3(E, CUBLAS_OP_N, CUBLAS_OP_T, d, nt, b, A, P, s.dN_part, d, (long long)nt * d);
+    const uint64_t total = (uint64_t)E.n_neg * d;
+    E.join_sorted();
+    k_sum_parts<<<(unsigned)((total + 255) / 256), 256, 0, E.stream>>>(s.dN_part, 1, total, total, (uint32_t)d, s.rank,
+                                                                        2 * nb, s.grows);
     EMBER_LAUNCHED(E);
 }
 

@@ -1305,7 +1305,13 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
     EMBER_LAUNCHED(E);
     launch_pdl(k_long_partial, dim3(2 * E.sm_count), dim3(256), 0, E.stream, a);
     EMBER_LAUNCHED(E);
-    launch_pdl(k_long_final, dim3(E.sm_count), dim3(32 * LONG_WARPS), 2 * LONG_WARPS * E.dim * sizeof(float), E.stream,
+    const size_t lf_smem = 2 * LONG_WARPS * E.dim * sizeof(float);  // > 48 KB from d = 376 on (C5: d = 800)
+    static size_t lf_attr = 48 * 1024;
+    if (lf_smem > lf_attr) {
+        EMBER_CUDA(cudaFuncSetAttribute(k_long_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lf_smem));
+        lf_attr = lf_smem;
+    }
+    launch_pdl(k_long_final, dim3(E.sm_count), dim3(32 * LONG_WARPS), lf_smem, E.stream,
                a);
     EMBER_LAUNCHED(E);
 }

@@ -77,6 +77,31 @@ def test_loss_and_grad_match_oracle(graph, engine, kind, chunks, nb):
         assert row_rel_err(got["rel_rows"], exp["rel_rows"]) <= TOL
 
 
+@pytest.mark.parametrize("engine", ["simt", "blas"])
+@pytest.mark.parametrize("kind,dim", [("complex", 800), ("distmult", 256), ("dot", 132), ("complex", 100)])
+def test_loss_and_grad_large_dim(graph, engine, kind, dim):
+    """SURVEY config C5's d = 800 (and other d > 128, beyond the hand-written tensor-core kernels'
+    TMEM layout) on the SIMT engine and on the blas engine (cuBLAS bf16 GEMMs with the bf16x3
+    split): scores, losses and gradients within 1e-4 of the oracle."""
+    edges, off, _ = graph
+    tr = make_trainer(kind, dim=dim, b=256, nt=100, p=2, engine=engine)
+    th, _, rt, _ = host_tables(tr)
+    bucket = edges[off[1]:off[2]]
+    negs = tr.sample_negatives(_dev(bucket), 0, 1, 0, 0, 0)
+    batch = bucket[:200]
+    got = tr.loss_and_grad(_dev(batch), negs, 0, 1)
+    exp = po.loss_and_grad(oracle_model(tr), batch, negs.cpu().numpy().view(np.uint32), th, rt)
+    assert abs(got["loss"] - exp["loss"]) <= TOL * abs(exp["loss"])
+    assert rel_err(got["lse"], exp["lse"]) <= TOL
+    assert (got["node_ids"] == exp["node_ids"]).all()
+    assert row_rel_err(got["node_rows"], exp["node_rows"]) <= TOL
+    if kind != "dot":
+        assert row_rel_err(got["rel_rows"], exp["rel_rows"]) <= TOL
+    if dim > 128:
+        with pytest.raises(eb.ConfigError):  # the hand-written tensor-core kernels stop at d = 128
+            make_trainer(kind, dim=dim, b=256, nt=100, p=2, engine="tc")
+
+
 def test_scores_match_oracle(graph):
     edges, off, _ = graph
     tr = make_trainer("complex", dim=32, nt=64, p=2)
@@ -162,7 +187,7 @@ def test_non_finite_loss_is_an_error_naming_the_batch(graph, engine):
     tr.synchronize()  # reported once
 
 
-@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("engine", ENGINES + ["blas"])
 def test_training_trajectory_matches_oracle(graph, engine):
     """A few full steps (sample -> grads -> Adagrad) over two buckets; losses within 1e-4, tables
     close (Adagrad's first step is ~ -lr*sign(g), so elements whose gradient is at rounding level can
