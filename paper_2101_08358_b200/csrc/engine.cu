@@ -191,10 +191,10 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     }
     if (blas_engine()) {
         s.S = dalloc<float>(2 * b * (uint64_t)(nt ? nt : 1));
-        s.dN_part = dalloc<float>((uint64_t)n_neg * d);
-        s.Ahl = dalloc<uint16_t>((uint64_t)2 * 2 * b * d);
-        s.Nhl = dalloc<uint16_t>((uint64_t)2 * 2 * (nt ? nt : 1) * d);
-        s.Phl = dalloc<uint16_t>((uint64_t)2 * 2 * b * (nt ? nt : 1));
+        s.dN_part = dalloc<float>((uint64_t)16 * n_neg * d);  // up to 16 K-chunk partials of dN
+        s.Ahl = dalloc<uint16_t>((uint64_t)2 * 2 * 3 * b * d);  // K-concatenated + K-stacked bf16x3 operands
+        s.Nhl = dalloc<uint16_t>((uint64_t)2 * 2 * 3 * (nt ? nt : 1) * d);
+        s.Phl = dalloc<uint16_t>((uint64_t)2 * 2 * 3 * b * (nt ? nt : 1));
     }
     if (tc_engine()) {  // packed operand geometry: dim padded to 16, rows to 128- and 96-row tiles
         KP = (int)((dim + 15) / 16 * 16);

@@ -81,7 +81,7 @@ struct Scratch {
     float* lse = nullptr;
     float* g0 = nullptr;
     float* S = nullptr;       // SIMT engine: [2][b][nt] scores -> P/b
-    void* Ahl = nullptr;      // blas engine: bf16 hi|lo splits of A [2][2][b][d], N [2][2][nt][d], P [2][2][b][nt]
+    void* Ahl = nullptr;      // blas engine: bf16x3 operands of A, N, P: K-concatenated then K-stacked (gemm_simt.cu)
     void* Nhl = nullptr;
     void* Phl = nullptr;
     float* dA = nullptr;

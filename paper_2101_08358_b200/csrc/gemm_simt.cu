@@ -244,41 +244,102 @@ void blas_check(cublasStatus_t st, const char* what) {
     if (st != CUBLAS_STATUS_SUCCESS) throw EmberError(std::string("cuBLAS ") + what + " failed: status " + std::to_string((int)st));
 }
 
-// hi = bf16(x), lo = bf16(x - hi), elementwise (n multiple of 4 not required)
-__global__ void k_split_bf16(const float* __restrict__ x, uint64_t n, __nv_bfloat16* __restrict__ hi,
-                             __nv_bfloat16* __restrict__ lo) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+// The bf16x3 product hi.lo + hi.hi + lo.hi as ONE GEMM over a 3x longer K: the K-concatenated
+// operands carry [hi | hi | lo] and [lo | hi | hi] blocks (so the output is written once, no beta
+// accumulation). Each operand is needed with K along its columns ("kd": [side][rows][3 cols]) or
+// along its rows ("stack": [side][3 rows][cols]); lo_first selects [lo, hi, hi] over [hi, hi, lo].
+__device__ __forceinline__ void put3(__nv_bfloat16* base, uint64_t blk, __nv_bfloat16 h, __nv_bfloat16 l, bool lo_first) {
+    base[0] = lo_first ? l : h;
+    base[blk] = h;
+    base[2 * blk] = lo_first ? h : l;
+}
+
+__global__ void k_split3(const float* __restrict__ x, uint32_t rows, uint32_t cols, __nv_bfloat16* __restrict__ kd,
+                         bool kd_lo_first, __nv_bfloat16* __restrict__ st, bool st_lo_first) {
+    const uint32_t per = rows * cols, n = 2 * per;  // < 2^32 (checked by the caller)
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t side = i >= per, rc = i - side * per, r = rc / cols, c = rc - r * cols;
         const float v = x[i];
-        const __nv_bfloat16 h = __float2bfloat16_rn(v);
-        hi[i] = h;
-        lo[i] = __float2bfloat16_rn(v - __bfloat162float(h));
+        const __nv_bfloat16 h = __float2bfloat16_rn(v), l = __float2bfloat16_rn(v - __bfloat162float(h));
+        put3(kd + (uint64_t)side * 3 * per + (uint64_t)r * 3 * cols + c, cols, h, l, kd_lo_first);
+        put3(st + (uint64_t)side * 3 * per + rc, per, h, l, st_lo_first);
     }
 }
 
-void split(const Engine& E, const float* x, uint64_t n, __nv_bfloat16* hi, __nv_bfloat16* lo) {
-    const unsigned blocks = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)E.sm_count * 16);
-    k_split_bf16<<<blocks, 256, 0, E.stream>>>(x, n, hi, lo);
-    EMBER_LAUNCHED(E);
+// Softmax rows with the positive column (as k_softmax_rows) writing P = exp(S - lse) / nb straight
+// into its two split layouts: kd [hi | hi | lo] (dA = P N) and stack [lo; hi; hi] (dN = P^T A).
+__global__ void k_softmax_split(const float* __restrict__ S, const float* __restrict__ fpos, float* lse, float* g0,
+                                uint32_t nb, uint32_t nt, float inv_b, __nv_bfloat16* __restrict__ pkd,
+                                __nv_bfloat16* __restrict__ pst) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    if (warp >= 2 * nb) return;
+    const uint32_t side = warp / nb, e = warp % nb;
+    const float* row = S + (uint64_t)side * nb * nt + (uint64_t)e * nt;
+    const float f = fpos[e];
+    float mx = f;
+    for (uint32_t k = lane; k < nt; k += 32) mx = fmaxf(mx, row[k]);
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float z = 0.f;
+    for (uint32_t k = lane; k < nt; k += 32) z += expf(row[k] - mx);
+    for (int o = 16; o; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+    z += expf(f - mx);
+    const float l = mx + logf(z);
+    const uint64_t per = (uint64_t)nb * nt;
+    __nv_bfloat16* kd = pkd + side * 3 * per + (uint64_t)e * 3 * nt;
+    __nv_bfloat16* st = pst + side * 3 * per + (uint64_t)e * nt;
+    if ((nt & 1) == 0) {  // pairs of columns per lane: 4-byte stores
+        for (uint32_t k = 2 * lane; k < nt; k += 64) {
+            const float2 x = *reinterpret_cast<const float2*>(row + k);
+            const float v0 = expf(x.x - l) * inv_b, v1 = expf(x.y - l) * inv_b;
+            const __nv_bfloat162 h = __floats2bfloat162_rn(v0, v1);
+            const float2 hf = __bfloat1622float2(h);
+            const __nv_bfloat162 lo = __floats2bfloat162_rn(v0 - hf.x, v1 - hf.y);
+            __nv_bfloat162* k2 = reinterpret_cast<__nv_bfloat162*>(kd + k);
+            __nv_bfloat162* s2 = reinterpret_cast<__nv_bfloat162*>(st + k);
+            k2[0] = h;
+            k2[nt / 2] = h;
+            k2[nt] = lo;
+            s2[0] = lo;
+            s2[per / 2] = h;
+            s2[per] = h;
+        }
+    } else {
+        for (uint32_t k = lane; k < nt; k += 32) {
+            const float v = expf(row[k] - l) * inv_b;
+            const __nv_bfloat16 h = __float2bfloat16_rn(v), lo = __float2bfloat16_rn(v - __bfloat162float(h));
+            put3(kd + k, nt, h, lo, false);
+            put3(st + k, per, h, lo, true);
+        }
+    }
+    if (lane == 0) {
+        lse[(uint64_t)side * nb + e] = l;
+        g0[(uint64_t)side * nb + e] = (expf(f - l) - 1.0f) * inv_b;
+    }
 }
 
-// Column-major C[m x n] (+)= op(A) op(B) over 2 batches (the corruption sides), bf16x3.
-struct Split {
-    const __nv_bfloat16 *hi, *lo;
-    int ld;
-    long long stride;
-};
-void gemm3(const Engine& E, cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k, const Split& a,
-           const Split& b, float* c, int ldc, long long sc) {
+// dN partials [side][kc][nt][d] -> sum over the kc chunks in order -> sorted gradient rows.
+__global__ void k_sum_chunks(const float* __restrict__ parts, uint32_t kc, uint64_t per, uint64_t n, uint32_t d,
+                             const uint32_t* __restrict__ rank, uint32_t slot0, float* out) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t side = i / per, rest = i % per;
+    const float* p = parts + side * kc * per + rest;
+    float acc = 0.f;
+    for (uint32_t k = 0; k < kc; ++k) acc += p[k * per];
+    out[(uint64_t)rank[slot0 + i / d] * d + i % d] = acc;
+}
+
+// Column-major C[m x n] = op(A) op(B) over the 2 corruption sides, bf16 in, fp32 out.
+void gemm(const Engine& E, cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k, const __nv_bfloat16* a,
+          int lda, long long sa, const __nv_bfloat16* b, int ldb, long long sb, float* c, int ldc, long long sc,
+          int batches = 2) {
     const BlasApi& api = blas_api();
-    cublasHandle_t h = static_cast<cublasHandle_t>(E.blas);
     const float one = 1.f, zero = 0.f;
-    const __nv_bfloat16* as[3] = {a.hi, a.lo, a.hi};
-    const __nv_bfloat16* bs[3] = {b.lo, b.hi, b.hi};  // small terms first, then hi.hi
-    for (int t = 0; t < 3; ++t)
-        blas_check(api.gemm(h, ta, tb, m, n, k, &one, as[t], CUDA_R_16BF, a.ld, a.stride, bs[t], CUDA_R_16BF, b.ld,
-                            b.stride, t ? &one : &zero, c, CUDA_R_32F, ldc, sc, 2, CUBLAS_COMPUTE_32F,
-                            CUBLAS_GEMM_DEFAULT),
-                   "gemm");
+    blas_check(api.gemm(static_cast<cublasHandle_t>(E.blas), ta, tb, m, n, k, &one, a, CUDA_R_16BF, lda, sa, b,
+                        CUDA_R_16BF, ldb, sb, &zero, c, CUDA_R_32F, ldc, sc, batches, CUBLAS_COMPUTE_32F,
+                        CUBLAS_GEMM_DEFAULT),
+               "gemm");
     EMBER_LAUNCHED(E);
 }
 
@@ -301,33 +362,50 @@ void launch_contract_blas(Engine& E, uint32_t nb) {
     const int d = (int)E.dim, nt = (int)E.nt, b = (int)nb;
     Scratch& s = E.s;
     using bf = __nv_bfloat16;
-    bf* Ahi = reinterpret_cast<bf*>(s.Ahl);
-    bf* Alo = Ahi + (size_t)2 * E.cap_b * d;
-    bf* Nhi = reinterpret_cast<bf*>(s.Nhl);
-    bf* Nlo = Nhi + (size_t)2 * nt * d;
-    bf* Phi = reinterpret_cast<bf*>(s.Phl);
-    bf* Plo = Phi + (size_t)2 * E.cap_b * nt;
-    // s.A: [2][nb][d] (side stride nb*d), s.N: [2][nt][d], s.S: [2][nb][nt] -- all row-major
-    split(E, s.A, (uint64_t)2 * b * d, Ahi, Alo);
-    split(E, s.N, (uint64_t)2 * nt * d, Nhi, Nlo);
-    const Split A{Ahi, Alo, d, (long long)b * d}, N{Nhi, Nlo, d, (long long)nt * d};
-    // 1) S = A N^T  (row-major [nb x nt]) == column-major S^T = N A^T
-    gemm3(E, CUBLAS_OP_T, CUBLAS_OP_N, nt, b, d, N, A, s.S, nt, (long long)b * nt);
-    // 2) softmax with the positive column: P = exp(S - lse) / nb in place
-    const uint32_t warps = 2 * nb;
-    k_softmax_rows<<<(warps * 32 + 255) / 256, 256, 0, E.stream>>>(s.S, s.fpos, s.lse, s.g0, nb, E.nt,
-                                                                   1.0f / (float)nb);
+    const size_t ab = (size_t)2 * 3 * E.cap_b * d, nbf = (size_t)2 * 3 * nt * d;
+    bf* Akd = reinterpret_cast<bf*>(s.Ahl);
+    bf* Ast = Akd + ab;
+    bf* Nkd = reinterpret_cast<bf*>(s.Nhl);
+    bf* Nst = Nkd + nbf;
+    bf* Pkd = reinterpret_cast<bf*>(s.Phl);
+    bf* Pst = Pkd + (size_t)2 * 3 * E.cap_b * nt;
+    const unsigned sb = (unsigned)E.sm_count * 16;
+    if ((uint64_t)2 * b * d >= (1ull << 32) || (uint64_t)2 * nt * d >= (1ull << 32))
+        throw ConfigError("blas engine: 2 * batch_size * dim must be < 2^32");
+    // s.A: [2][nb][d], s.N: [2][nt][d], s.S: [2][nb][nt] -- row-major fp32
+    k_split3<<<sb, 256, 0, E.stream>>>(s.A, nb, (uint32_t)d, Akd, false, Ast, false);  // [hi hi lo] both ways
     EMBER_LAUNCHED(E);
-    split(E, s.S, (uint64_t)2 * b * nt, Phi, Plo);
-    const Split P{Phi, Plo, nt, (long long)b * nt};
-    // 3) dA = P N  (row-major [nb x d]) == column-major dA^T = N^T P^T
-    gemm3(E, CUBLAS_OP_N, CUBLAS_OP_N, d, b, nt, N, P, s.dA, d, (long long)b * d);
-    // 4) dN = P^T A  (row-major [nt x d]) == column-major dN^T = A^T P
-    gemm3(E, CUBLAS_OP_N, CUBLAS_OP_T, d, nt, b, A, P, s.dN_part, d, (long long)nt * d);
+    k_split3<<<sb, 256, 0, E.stream>>>(s.N, (uint32_t)nt, (uint32_t)d, Nkd, true, Nst, true);  // [lo hi hi]
+    EMBER_LAUNCHED(E);
+    const int d3 = 3 * d, nt3 = 3 * nt, b3 = 3 * b;
+    // 1) S = A N^T (row-major [nb x nt]) == column-major S^T = N A^T, K = 3d
+    gemm(E, CUBLAS_OP_T, CUBLAS_OP_N, nt, b, d3, Nkd, d3, (long long)nt * d3, Akd, d3, (long long)b * d3, s.S, nt,
+         (long long)b * nt);
+    // 2) softmax with the positive column, P split into both layouts
+    const uint32_t warps = 2 * nb;
+    k_softmax_split<<<(warps * 32 + 255) / 256, 256, 0, E.stream>>>(s.S, s.fpos, s.lse, s.g0, nb, E.nt,
+                                                                    1.0f / (float)nb, Pkd, Pst);
+    EMBER_LAUNCHED(E);
+    // 3) dA = P N (row-major [nb x d]) == column-major dA^T = N^T P^T, K = 3 nt (stacked N, kd P)
+    gemm(E, CUBLAS_OP_N, CUBLAS_OP_N, d, b, nt3, Nst, d, (long long)nt3 * d, Pkd, nt3, (long long)b * nt3, s.dA, d,
+         (long long)b * d);
+    // 4) dN = P^T A (row-major [nt x d]) == column-major dN^T = A^T P, K = 3 nb (stacked A, stacked P).
+    // The output is small (d x nt) and K long, so K is cut into kc chunks that run as extra GEMM
+    // batches (batch = side * kc + chunk: uniform strides because a side's K is kc chunks long);
+    // the partials are added in chunk order (deterministic) while scattering the rows.
+    int kc = 1;
+    for (int c : {16, 12, 8, 6, 4, 3, 2})
+        if (b3 % c == 0) {
+            kc = c;
+            break;
+        }
+    const int kch = b3 / kc;
+    gemm(E, CUBLAS_OP_N, CUBLAS_OP_T, d, nt, kch, Ast, d, (long long)kch * d, Pst, nt, (long long)kch * nt, s.dN_part, d,
+         (long long)nt * d, 2 * kc);
     const uint64_t total = (uint64_t)E.n_neg * d;
     E.join_sorted();
-    k_sum_parts<<<(unsigned)((total + 255) / 256), 256, 0, E.stream>>>(s.dN_part, 1, total, total, (uint32_t)d, s.rank,
-                                                                        2 * nb, s.grows);
+    k_sum_chunks<<<(unsigned)((total + 255) / 256), 256, 0, E.stream>>>(s.dN_part, (uint32_t)kc, (uint64_t)nt * d,
+                                                                         total, (uint32_t)d, s.rank, 2 * nb, s.grows);
     EMBER_LAUNCHED(E);
 }
 
