@@ -8,8 +8,9 @@ ranking metrics agree. Both parameter sets are ranked by the same evaluator (the
 filtered protocol: every node is a candidate, known true edges are filtered,
 pessimistic ties), so the comparison isolates training.
 
-Cases: a small DistMult graph, a 2-partition ComplEx graph, and the FB15k-237-shaped config C1
-at full shape (14,541 nodes, 237 relations, d=100, b=10^4, n_t=10^3).
+Cases: a small DistMult graph, a 2-partition ComplEx graph, the FB15k-237-shaped config C1
+at full shape (14,541 nodes, 237 relations, d=100, b=10^4, n_t=10^3), and a d=160
+ComplEx graph on the blas engine (d > 128).
 """
 import numpy as np
 import pytest
@@ -29,6 +30,9 @@ CASES = {
                        seed=22),
     "fb15k237-shape": dict(kind="distmult", V=14541, R=237, E=340144, d=100, p=1, b=10000, nt=1000, epochs=3,
                            n_test=5000, seed=210108358),
+    # d > 128 (beyond the hand-written kernels' TMEM layout): the blas engine (cuBLAS bf16x3 GEMMs)
+    "complex-p2-d160-blas": dict(kind="complex", V=4000, R=20, E=80000, d=160, p=2, b=1500, nt=200, epochs=3,
+                                 n_test=2000, seed=23, engine="blas"),
 }
 
 
@@ -43,7 +47,8 @@ def test_trained_mrr_matches_cpu_reference(case):
     plan = eb.make_plan("elimination", p, p, 0)
 
     # GPU (the product path, tensor-core engine)
-    h = eb.Hyper(kind=c["kind"], dim=d, batch_size=B, num_negatives=c["nt"], alpha=0.5, neg_seed=1, engine="tc")
+    h = eb.Hyper(kind=c["kind"], dim=d, batch_size=B, num_negatives=c["nt"], alpha=0.5, neg_seed=1,
+                 engine=c.get("engine", "tc"))
     tr = eb.Trainer(h, V, R, p, device=0)
     tr.init_embeddings(11)
     dev = torch.from_numpy(bucketed.view(np.int32)).cuda()
