@@ -14,6 +14,9 @@
 // Rows are dim floats (dim % 4 == 0) and are moved warp-per-row with 128-bit accesses.
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
+
 #include "engine.h"
 #include "tc_common.cuh"
 
@@ -1152,9 +1155,21 @@ __global__ void k_init_rows(float* theta, float* acc, uint64_t first, uint64_t r
     }
 }
 
-constexpr size_t sm_cap() { return 227 * 1024; }
 
 }  // namespace
+
+// Dynamic shared memory above 48 KB needs a per-kernel opt-in, and the attribute is per device:
+// remember the largest size set per (kernel, device) (several contexts / GPUs in one process).
+void opt_in_smem(const void* fn, size_t bytes, int device) {
+    if (bytes <= 48 * 1024) return;
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& have = done[{fn, device}];
+    if (bytes <= have) return;
+    EMBER_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    have = bytes;
+}
 
 void launch_sample(const Engine& E, uint32_t* out, uint64_t base, const uint32_t* bucket, uint64_t bucket_n,
                    const PartView& src, const PartView& dst) {
@@ -1181,11 +1196,7 @@ void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, c
     if (packed) {
         const uint32_t rows_pad = (uint32_t)Engine::pad_rows(nb);  // a multiple of GP_ROWS
         const size_t sm = (size_t)4 * E.CB * GP_ROWS * 16 + (size_t)GP_WARPS * 2 * E.KP * sizeof(float);
-        static bool attr = false;
-        if (!attr) {
-            EMBER_CUDA(cudaFuncSetAttribute(k_gather_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_cap()));
-            attr = true;
-        }
+        opt_in_smem((const void*)k_gather_pack, sm, E.device);
         const uint32_t row_ctas = rows_pad / GP_ROWS, neg_ctas = (2 * E.n_pad + GP_WARPS - 1) / GP_WARPS;
         launch_pdl(k_gather_pack, dim3(row_ctas + neg_ctas), dim3(32 * GP_WARPS), sm, E.stream, edges, nb, pi, pj,
                    E.rel_theta, E.m.kind, E.dim, E.CB, (uint32_t)E.b_cap, E.s.Apk, E.s.fpos, row_ctas,
@@ -1229,11 +1240,7 @@ void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, cons
         // persistent pipelined warps: 3 CTAs of 8 warps per SM (shared stages: 8 x 2 x 7 x 512 B)
         const size_t sm = (size_t)warps * 2 * CP_ROLES * 32 * sizeof(float4);
         const uint32_t blocks = std::min<uint32_t>((nb + warps - 1) / warps, (uint32_t)E.sm_count * 3);
-        static bool attr = false;
-        if (!attr) {
-            EMBER_CUDA(cudaFuncSetAttribute(k_chain_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            attr = true;
-        }
+        opt_in_smem((const void*)k_chain_pipe, sm, E.device);
         launch_pdl(k_chain_pipe, dim3(blocks), dim3(warps * 32), sm, E.stream, edges, nb, E.n_neg, pi, pj,
                    (const float*)E.rel_theta, E.m.kind, E.dim, (const float*)E.s.dA, (uint32_t)E.b_cap,
                    (const float*)E.s.g0, (const uint32_t*)E.s.rank, (const uint8_t*)E.s.uniq, E.s.grows,
@@ -1292,11 +1299,7 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
     a.rel_rows_out = rel_rows_out;
     if (E.dim <= 128 && !getenv("EMBER_SEG_PLAIN")) {  // persistent, pipelined (A/B: EMBER_SEG_PLAIN=1)
         const size_t sm = (size_t)8 * 2 * 2 * 2 * 2 * SEG_LANES * sizeof(float4);
-        static bool attr = false;
-        if (!attr) {
-            EMBER_CUDA(cudaFuncSetAttribute(k_segments_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            attr = true;
-        }
+        opt_in_smem((const void*)k_segments_pipe, sm, E.device);
         const uint32_t blocks = std::min<uint32_t>((n_slots + 15) / 16, (uint32_t)E.sm_count * 4);
         launch_pdl(k_segments_pipe, dim3(blocks), dim3(256), sm, E.stream, a);
     } else {
@@ -1306,11 +1309,7 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
     launch_pdl(k_long_partial, dim3(2 * E.sm_count), dim3(256), 0, E.stream, a);
     EMBER_LAUNCHED(E);
     const size_t lf_smem = 2 * LONG_WARPS * E.dim * sizeof(float);  // > 48 KB from d = 376 on (C5: d = 800)
-    static size_t lf_attr = 48 * 1024;
-    if (lf_smem > lf_attr) {
-        EMBER_CUDA(cudaFuncSetAttribute(k_long_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lf_smem));
-        lf_attr = lf_smem;
-    }
+    opt_in_smem((const void*)k_long_final, lf_smem, E.device);
     launch_pdl(k_long_final, dim3(E.sm_count), dim3(32 * LONG_WARPS), lf_smem, E.stream,
                a);
     EMBER_LAUNCHED(E);
