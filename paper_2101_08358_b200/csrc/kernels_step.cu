@@ -138,8 +138,9 @@ constexpr uint32_t GP_ROWS = 32, GP_WARPS = 8;
 // GP_ROWS / GP_WARPS edges: lanes load their quads of the source, relation and destination rows
 // into registers, form the adjusted quads and stage them (2 x KP floats per warp); lanes < 2CB
 // split 8 consecutive coordinates into bf16 hi|lo 16-byte core-matrix rows of a shared tile
-// [2 sides][2CB blocks][GP_ROWS][16 B], which leaves in 512-byte coalesced runs, one per column
-// block (per-lane 16-byte stores would scatter over 56 blocks). fpos[e] = ad . t.
+// [2 sides][2CB blocks][GP_ROWS][16 B] (row slot XOR-swizzled by the block, so the lanes' 16-byte
+// stores are bank-conflict free), which leaves in 512-byte coalesced runs, one per column block
+// (per-lane 16-byte stores would scatter over 56 blocks). fpos[e] = ad . t.
 // (Staging the rows with one TMA bulk copy per 400-byte row measured slower than register loads.)
 __global__ void __launch_bounds__(32 * GP_WARPS) k_gather_pack(const uint32_t* __restrict__ edges, uint32_t nb,
                                                                PartView pi, PartView pj, const float* __restrict__ rel,
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(32 * GP_WARPS) k_gather_pack(const uint32_t* _
     for (uint32_t rr = wib; rr < GP_ROWS; rr += GP_WARPS) {
         const uint32_t e = e0 + rr;
         if (e >= nb) {  // padding rows of the last tiles
-            for (uint32_t c = lane; c < nblk; c += 32) tile[c * GP_ROWS + rr] = make_uint4(0, 0, 0, 0);
+            for (uint32_t c = lane; c < nblk; c += 32) tile[c * GP_ROWS + (rr ^ (c % GP_ROWS))] = make_uint4(0, 0, 0, 0);
             continue;
         }
         const uint32_t s = edges[3 * e], r = edges[3 * e + 1], t = edges[3 * e + 2];
@@ -193,8 +194,10 @@ __global__ void __launch_bounds__(32 * GP_WARPS) k_gather_pack(const uint32_t* _
             float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
             uint4 hq, lq;
             tc::split8(v, hq, lq);
-            tile[((side * 2 * CB) + cb) * GP_ROWS + rr] = hq;
-            tile[((side * 2 * CB) + CB + cb) * GP_ROWS + rr] = lq;
+            // row slot rr ^ block: the lanes (one block each) hit distinct 16-byte bank groups
+            const uint32_t bh = side * 2 * CB + cb, bl = bh + CB;
+            tile[bh * GP_ROWS + (rr ^ (bh % GP_ROWS))] = hq;
+            tile[bl * GP_ROWS + (rr ^ (bl % GP_ROWS))] = lq;
         }
         for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
         if (lane == 0) fpos[e] = part;
@@ -203,7 +206,7 @@ __global__ void __launch_bounds__(32 * GP_WARPS) k_gather_pack(const uint32_t* _
     uint4* P = reinterpret_cast<uint4*>(Apk);
     for (uint32_t i = threadIdx.x; i < nblk * GP_ROWS; i += blockDim.x) {
         const uint32_t blk = i / GP_ROWS, rr = i % GP_ROWS;  // blk = side * 2CB + column block
-        P[(uint64_t)blk * cap + e0 + rr] = tile[i];
+        P[(uint64_t)blk * cap + e0 + rr] = tile[blk * GP_ROWS + (rr ^ (blk % GP_ROWS))];
     }
 }
 
