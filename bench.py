@@ -618,6 +618,23 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # stdout carries exactly one JSON line: native libraries' banners (e.g. NCCL's version line at
+    # communicator creation) go to stderr until the result is printed
+    sys.stdout.flush()
+    saved_stdout = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        out = _run(args, rank, world, local_rank)
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved_stdout, 1)
+        os.close(saved_stdout)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+def _run(args, rank, world, local_rank):
+    out = None
     if args.impl == "reference":
         out = bench_reference(args, rank, world)
     else:
@@ -642,8 +659,7 @@ def main():
         if dist_path:
             import torch.distributed as dist
             dist.destroy_process_group()
-    if out is not None:
-        print(json.dumps(out), flush=True)
+    return out
 
 
 if __name__ == "__main__":
