@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "engine.h"
 
@@ -50,6 +51,8 @@ struct NcclApi {
 
 NcclApi& nccl() {
     static NcclApi api;
+    static std::mutex mu;  // contexts may be created from several host threads
+    std::lock_guard<std::mutex> lock(mu);
     if (!api.h) {
         const char* names[] = {"libnccl.so.2", "libnccl.so"};
         for (const char* n : names)

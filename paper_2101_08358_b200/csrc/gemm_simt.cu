@@ -10,6 +10,7 @@
 #include <cublas_v2.h>  // types and enums only: the library is bound at run time (dlopen)
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <mutex>
 #include <dlfcn.h>
 
 #include "engine.h"
@@ -224,6 +225,8 @@ struct BlasApi {
 const BlasApi& blas_api() {
     static BlasApi api;
     static bool tried = false;
+    static std::mutex mu;  // contexts may be created from several host threads
+    std::lock_guard<std::mutex> lock(mu);
     if (!tried) {
         tried = true;
         for (const char* n : {"libcublas.so.12", "/usr/local/cuda/lib64/libcublas.so.12"})
