@@ -353,7 +353,7 @@ void Engine::forward_backward(const uint32_t* edges, uint32_t nb, uint32_t i, ui
         sort_keys(edges, nb, i, j, negs);
     }
     mark(PHASE_GATHER);
-    launch_gather_adjust(*this, edges, nb, pi, pj, tc_engine(), negs);
+    launch_gather_adjust(*this, edges, nb, pi, pj, tc_engine(), negs, blas_engine());
     launch_gather_negatives(*this, negs, pi, pj, tc_engine());
     mark(PHASE_CONTRACT);
     if (tc_engine())

@@ -260,7 +260,7 @@ void launch_sample_on(const Engine& E, cudaStream_t st, uint32_t* out, uint64_t 
                       uint64_t bucket_n, const PartView& src, const PartView& dst);
 // packed: write the tensor-core engine's bf16 hi|lo operands (Apk/Npk), else fp32 A / N.
 void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj,
-                          bool packed, const uint32_t* negs);
+                          bool packed, const uint32_t* negs, bool split_bf16 = false);
 void launch_gather_negatives(const Engine& E, const uint32_t* negs, const PartView& pi, const PartView& pj, bool packed);
 void launch_keys(const Engine& E, const uint32_t* edges, uint32_t nb, const uint32_t* negs, const KeySpace& ks);
 void launch_rank(const Engine& E, uint32_t n);

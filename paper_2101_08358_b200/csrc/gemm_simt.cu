@@ -376,8 +376,7 @@ void launch_contract_blas(Engine& E, uint32_t nb) {
     if ((uint64_t)2 * b * d >= (1ull << 32) || (uint64_t)2 * nt * d >= (1ull << 32))
         throw ConfigError("blas engine: 2 * batch_size * dim must be < 2^32");
     // s.A: [2][nb][d], s.N: [2][nt][d], s.S: [2][nb][nt] -- row-major fp32
-    k_split3<<<sb, 256, 0, E.stream>>>(s.A, nb, (uint32_t)d, Akd, false, Ast, false);  // [hi hi lo] both ways
-    EMBER_LAUNCHED(E);
+    // (A's splits, [hi hi lo] both ways, were written by the gather: k_gather_adjust<true>)
     k_split3<<<sb, 256, 0, E.stream>>>(s.N, (uint32_t)nt, (uint32_t)d, Nkd, true, Nst, true);  // [lo hi hi]
     EMBER_LAUNCHED(E);
     const int d3 = 3 * d, nt3 = 3 * nt, b3 = 3 * b;
