@@ -76,6 +76,7 @@ struct TcArgs {
     float* dN_part;   // column-blocked [chunks][2][d/4][n_pad] float4
     uint32_t* flags;  // [0] = count, [1..] = side * b_cap + row
     int early;        // tiles 0 .. early-1 of an item go to epilogue group 0 (tile_group)
+    int diag;         // EMBER_TC_DIAG=1 (measurement only, wrong results): the epilogue skips its TMEM work
     unsigned long long* trace;  // debug timeline of CTA 0 (EMBER_TC_TRACE), nullptr normally
 };
 
@@ -456,8 +457,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 if (qd == 2) TC_TRACE(20 + G, q);
                 tc::fence_after();
                 // 64 columns per TMEM round trip, then the 32-column remainder (TILE = 96)
-                epi_chunk<MODE, 2>(tS, 0, k, g, sm, st, KP, cshift, z);
-                epi_chunk<MODE, 1>(tS, 64, k, g, sm, st, KP, cshift, z);
+                if (!g.diag) {
+                    epi_chunk<MODE, 2>(tS, 0, k, g, sm, st, KP, cshift, z);
+                    epi_chunk<MODE, 1>(tS, 64, k, g, sm, st, KP, cshift, z);
+                }
                 tc::tmem_st_wait();
                 tc::fence_before();
                 tc::mbar_arrive(&bars[B_P_FULL + b]);
@@ -775,6 +778,7 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
     a.flags = t.flags;
     a.early = 3;
     if (const char* e = getenv("EMBER_TC_EARLY")) a.early = std::max(1, atoi(e));  // A/B (1: plain alternation)
+    a.diag = getenv("EMBER_TC_DIAG") ? 1 : 0;
     a.trace = nullptr;
     const int nsub = (int)((nb + TILE - 1) / TILE);
     a.chunks2 = std::min(t.chunks2, nsub);
