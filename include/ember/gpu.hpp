@@ -71,6 +71,27 @@ public:
         return st;
     }
 
+    // Waits for all of the context's streams; a non-finite batch loss since the last check
+    // surfaces here as EmberError naming the batch.
+    void synchronize() { check(ember_ctx_synchronize(ctx_)); }
+
+    // Per-op entry points (SPEC model ops), device pointers:
+    // sample_negatives: 2*n_t ids [side][slot]
+    void sample_negatives(const uint32_t* bucket_edges_dev, uint64_t n, uint32_t i, uint32_t j, uint64_t epoch,
+                          uint32_t bucket_step, uint32_t batch_in_bucket, uint32_t* negs_dev) {
+        check(ember_sample_negatives(ctx_, bucket_edges_dev, n, i, j, epoch, bucket_step, batch_in_bucket, negs_dev));
+    }
+    // ParameterSlice gather: one theta (and acc) row per id, in order
+    void gather(const uint32_t* ids_dev, uint32_t n, uint32_t i, uint32_t j, bool relations, float* theta_out_dev,
+                float* acc_out_dev = nullptr) {
+        check(ember_gather(ctx_, ids_dev, n, i, j, relations ? 1 : 0, theta_out_dev, acc_out_dev));
+    }
+    // adagrad_step on rows of bucket (i, j)'s partitions (or the relation table)
+    void adagrad_apply(const uint32_t* ids_dev, const float* rows_dev, uint32_t n, uint32_t i, uint32_t j,
+                       bool relations) {
+        check(ember_adagrad_apply(ctx_, ids_dev, rows_dev, n, i, j, relations ? 1 : 0));
+    }
+
 private:
     void reset() {
         if (ctx_) ember_ctx_destroy(ctx_);
