@@ -55,10 +55,13 @@ def main():
     epochs = []
     for ep in range(args.epochs):
         torch.cuda.synchronize()
+        clocks = bench.ClockSampler(0)
+        clocks.start()
         e0 = time.perf_counter()
         out = tr.train_epoch(bucketed, offsets, plan["seq"], ep)
         torch.cuda.synchronize()
         dt = time.perf_counter() - e0
+        clk = clocks.stop()
         ovf = tr.overflow_rows()
         # phase breakdown of a few batches at the end of the epoch (instrumented, not timed above)
         tr.profile(True)
@@ -74,7 +77,7 @@ def main():
                        "edges_per_s": round(out["edges"] / dt, 1),
                        "mrr": round(float(m["mrr"]), 4), "hits@1": round(float(m["hits@1"]), 4),
                        "hits@10": round(float(m["hits@10"]), 4), "phase_ms_per_step_after": ph,
-                       "overflow_rows_total": int(ovf)})
+                       "overflow_rows_total": int(ovf), "clocks": clk})
     print(json.dumps({"workload": cfg["desc"], "train_edges": int(offsets[-1]), "setup_s": round(setup_s, 1),
                       "eval": f"unfiltered, {args.test} test edges x 2 sides, 1000 sampled negatives per block of 1000",
                       "mrr_before": round(float(before["mrr"]), 4), "epochs": epochs}), flush=True)
