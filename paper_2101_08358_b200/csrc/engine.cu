@@ -456,7 +456,10 @@ void Engine::step(const uint32_t* edges, uint32_t nb, const uint32_t* bucket, ui
     // they run (counter-based sampler, fixed inputs).
     const int k = (int)(nsteps++ & 1);
     use_set(k);
-    if (have_after_tc) EMBER_CUDA(cudaStreamWaitEvent(side, ev_after_tc, 0));
+    // (A/B: EMBER_SORT_AFTER_TC=1 holds them until the previous step's contraction is done; by
+    // default they start at once and run on the SMs the contraction kernels leave free)
+    static const bool after_tc = getenv("EMBER_SORT_AFTER_TC") != nullptr;
+    if (have_after_tc && after_tc) EMBER_CUDA(cudaStreamWaitEvent(side, ev_after_tc, 0));
     if (set_used[k]) EMBER_CUDA(cudaStreamWaitEvent(side, ev_set_free[k], 0));
     if (edges_ready) EMBER_CUDA(cudaStreamWaitEvent(side, edges_ready, 0));
     mark(PHASE_SAMPLE);

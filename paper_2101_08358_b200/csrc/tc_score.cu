@@ -787,6 +787,7 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
     a.rows128 = rows_pad;
     a.rows_pad = E.pad_rows(nb);
     const int items1 = 2 * (rows_pad / RES);
+    const int items2 = 2 * ((nt + RES - 1) / RES) * a.chunks2;
     const int gmax = t.max_grid > 0 ? std::min(t.max_grid, E.sm_count) : E.sm_count;
     const bool tr = t.trace && t.trace_calls++ == 4;  // one warmed-up call per process
     auto dump = [&](const char* tag) {
@@ -804,7 +805,11 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
         a.trace = t.trace;
     }
     // programmatic launch: the CTAs set up barriers and TMEM while the gathers drain
-    launch_pdl(k_tc<MODE_ROWS>, dim3(std::min(items1, gmax)), dim3(NTHREADS), smem_total(t.KP, t.nstage, MODE_ROWS),
+    // The dN kernel's grid (items2, e.g. 144 of 148 SMs) also bounds the rows kernel's: same number
+    // of waves, and the SMs left free run the helper stream's sampling + sort for the next step.
+    const int g2 = std::min(items2, gmax);
+    const int grid1 = std::min(items1, g2 >= gmax - 8 ? g2 : gmax);
+    launch_pdl(k_tc<MODE_ROWS>, dim3(grid1), dim3(NTHREADS), smem_total(t.KP, t.nstage, MODE_ROWS),
                E.stream, t.mA128, t.mN96, a);
     EMBER_LAUNCHED(E);
     if (tr) {
@@ -816,7 +821,6 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
     launch_pdl(k_tc_fixup, dim3(E.sm_count * 2), dim3(256), 0, E.stream, a, (const uint16_t*)s.Apk,
                (const uint16_t*)s.Npk);
     EMBER_LAUNCHED(E);
-    const int items2 = 2 * ((nt + RES - 1) / RES) * a.chunks2;
     launch_pdl(k_tc<MODE_NEGS>, dim3(std::min(items2, gmax)), dim3(NTHREADS), smem_total(t.KP, t.nstage, MODE_NEGS),
                E.stream, t.mN128, t.mA96, a);
     EMBER_LAUNCHED(E);
