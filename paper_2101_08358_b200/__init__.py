@@ -172,8 +172,13 @@ class Trainer:
         md = hyper.desc()
         gd = GraphDesc(num_nodes, num_relations, num_partitions)
         ctx = C.c_void_p()
-        check(lib().ember_ctx_create(device, C.byref(md), C.byref(gd), _ptr(stream) if stream is not None else None,
-                                     C.byref(ctx)))
+        if stream is None:
+            # a torch-owned stream (torch never destroys its streams): tensors recorded on it with
+            # record_stream stay valid after the context is gone; highest priority, like the
+            # engine's own stream
+            stream = torch.cuda.Stream(device=self.dev, priority=-100)
+        self._ts = stream
+        check(lib().ember_ctx_create(device, C.byref(md), C.byref(gd), stream.cuda_stream, C.byref(ctx)))
         self.ctx = ctx
         self.theta: dict[int, object] = {}
         self.acc: dict[int, object] = {}
@@ -204,7 +209,29 @@ class Trainer:
         return lib().ember_ctx_stream(self.ctx)
 
     def torch_stream(self):
-        return self.torch.cuda.ExternalStream(self.stream_ptr, device=self.dev)
+        return self._ts
+
+    def _enter(self, *tensors):
+        """Orders a C-ABI call after the caller's work: the context stream waits for torch's current
+        stream (which produced the inputs), and every borrowed device tensor is recorded on the
+        context stream, so torch's caching allocator cannot hand its memory out again before the
+        engine's (asynchronous) kernels are done with it."""
+        t = self.torch
+        ts = self.torch_stream()
+        cur = t.cuda.current_stream(self.dev)
+        if cur.cuda_stream != ts.cuda_stream:
+            ts.wait_stream(cur)
+        for x in tensors:
+            if x is not None and isinstance(x, t.Tensor) and x.is_cuda:
+                x.record_stream(ts)
+
+    def _leave(self):
+        """Outputs handed back without a host synchronisation: torch's current stream waits for them."""
+        t = self.torch
+        ts = self.torch_stream()
+        cur = t.cuda.current_stream(self.dev)
+        if cur.cuda_stream != ts.cuda_stream:
+            cur.wait_stream(ts)
 
     def synchronize(self):
         check(lib().ember_ctx_synchronize(self.ctx))
@@ -213,18 +240,22 @@ class Trainer:
     # -- tables ---------------------------------------------------------------------------
     def bind_partition(self, k, theta, acc):
         self.theta[k], self.acc[k] = theta, acc
+        self._enter(theta, acc)
         check(lib().ember_tables_bind(self.ctx, k, _ptr(theta), _ptr(acc)))
 
     def bind_relations(self, theta, acc):
         self.rel_theta, self.rel_acc = theta, acc
+        self._enter(theta, acc)
         check(lib().ember_relations_bind(self.ctx, _ptr(theta), _ptr(acc)))
 
     def init_embeddings(self, seed: int):
         """init_embeddings: every bound partition + relations, on the device."""
+        self._enter()
         for k in self.theta:
             check(lib().ember_init_partition(self.ctx, k, seed))
         if self.rel_theta is not None:
             check(lib().ember_init_relations(self.ctx, seed))
+        self._leave()
 
     def node_table(self):
         """Concatenated theta/acc of all partitions (host copies for parity checks)."""
@@ -236,12 +267,15 @@ class Trainer:
     # -- the step -------------------------------------------------------------------------
     def train_batch(self, bucket_edges, batch_begin: int, nb: int, i: int = 0, j: int = 0, epoch: int = 0,
                     bucket_step: int = 0, batch_in_bucket: int = 0, loss_out=None):
+        self._enter(bucket_edges, loss_out)
         check(lib().ember_train_batch(self.ctx, _ptr(bucket_edges), int(bucket_edges.shape[0]), batch_begin, nb, i, j,
                                       epoch, bucket_step, batch_in_bucket, _ptr(loss_out)))
+        self._leave()
 
     def train_batch_host(self, bucket_edges, host_batch, i=0, j=0, epoch=0, bucket_step=0, batch_in_bucket=0,
                          want_loss=True) -> float | None:
         loss = C.c_float(0.0)
+        self._enter(bucket_edges)
         check(lib().ember_train_batch_host(self.ctx, _ptr(bucket_edges), int(bucket_edges.shape[0]), _ptr(host_batch),
                                            int(host_batch.shape[0]), i, j, epoch, bucket_step, batch_in_bucket,
                                            C.byref(loss) if want_loss else None))
@@ -251,6 +285,7 @@ class Trainer:
 
     def train_bucket(self, bucket_edges, i=0, j=0, epoch=0, bucket_step=0) -> StepStats:
         st = StepStats()
+        self._enter(bucket_edges)
         check(lib().ember_train_bucket(self.ctx, _ptr(bucket_edges), int(bucket_edges.shape[0]), i, j, epoch,
                                        bucket_step, C.byref(st)))
         return st
@@ -261,6 +296,7 @@ class Trainer:
         st = StepStats()
         seq = np.ascontiguousarray(np.asarray(plan_seq, dtype=np.uint32).reshape(-1))
         off = np.ascontiguousarray(np.asarray(offsets, dtype=np.uint64))
+        self._enter(edges_dev)
         check(lib().ember_train_epoch(self.ctx, _ptr(edges_dev), _ptr(off), _ptr(seq), epoch, C.byref(st)))
         return {"loss": st.loss_sum / max(1, st.batches), "batches": st.batches, "edges": st.edges}
 
@@ -268,8 +304,10 @@ class Trainer:
     def sample_negatives(self, bucket_edges, i=0, j=0, epoch=0, bucket_step=0, batch_in_bucket=0):
         t = self.torch
         out = t.empty(max(1, self.h.num_chunks) * 2 * self.h.num_negatives, dtype=t.int32, device=self.dev)
+        self._enter(bucket_edges, out)
         check(lib().ember_sample_negatives(self.ctx, _ptr(bucket_edges), int(bucket_edges.shape[0]), i, j, epoch,
                                            bucket_step, batch_in_bucket, _ptr(out)))
+        self._leave()
         return out
 
     def loss_and_grad(self, edges, negs, i=0, j=0) -> dict:
@@ -284,6 +322,7 @@ class Trainer:
         rids = t.empty(max(nb, 1), dtype=t.int32, device=self.dev)
         rrows = t.empty((max(nb, 1), d), dtype=t.float32, device=self.dev)
         nu, nr, loss = C.c_uint32(0), C.c_uint32(0), C.c_double(0)
+        self._enter(edges, negs, fpos, lse, ids, rows, rids, rrows)
         check(lib().ember_loss_and_grad(self.ctx, _ptr(edges), nb, i, j, _ptr(negs), _ptr(fpos), _ptr(lse), _ptr(ids),
                                         _ptr(rows), C.byref(nu), _ptr(rids), _ptr(rrows), C.byref(nr), C.byref(loss)))
         self.synchronize()
@@ -293,7 +332,9 @@ class Trainer:
                 "rel_ids": rids[:r].cpu().numpy().view(np.uint32), "rel_rows": rrows[:r].cpu().numpy()}
 
     def adagrad_apply(self, ids, rows, i=0, j=0, relations=False):
+        self._enter(ids, rows)
         check(lib().ember_adagrad_apply(self.ctx, _ptr(ids), _ptr(rows), int(ids.numel()), i, j, 1 if relations else 0))
+        self._leave()
 
     def gather(self, ids, i=0, j=0, relations=False, with_acc=True):
         """ParameterSlice gather: (theta, acc) rows of `ids` (device u32), one per
@@ -302,14 +343,17 @@ class Trainer:
         n = int(ids.numel())
         th = t.empty((n, self.h.dim), dtype=t.float32, device=self.dev)
         ac = t.empty_like(th) if with_acc else None
+        self._enter(ids, th, ac)
         check(lib().ember_gather(self.ctx, _ptr(ids), n, i, j, 1 if relations else 0, _ptr(th),
                                  _ptr(ac) if ac is not None else None))
+        self._leave()
         return th, ac
 
     def debug_scores(self, edges, negs, side=0, rows=None, i=0, j=0):
         t = self.torch
         rows = int(edges.shape[0]) if rows is None else rows
         out = t.empty((rows, self.h.num_negatives), dtype=t.float32, device=self.dev)
+        self._enter(edges, negs, out)
         check(lib().ember_debug_scores(self.ctx, _ptr(edges), int(edges.shape[0]), i, j, _ptr(negs), side, rows,
                                        _ptr(out)))
         self.synchronize()
@@ -319,6 +363,7 @@ class Trainer:
         t = self.torch
         n = int(test_edges.shape[0])
         ranks = t.empty(2 * n, dtype=t.int32, device=self.dev)
+        self._enter(test_edges, train_edges, ranks)
         check(lib().ember_eval_ranks(self.ctx, _ptr(test_edges), n, _ptr(train_edges), int(train_edges.shape[0]),
                                      n_eval, alpha_eval, block, eval_seed, _ptr(ranks)))
         self.synchronize()
@@ -330,6 +375,7 @@ class Trainer:
         t = self.torch
         n = int(test_edges.shape[0])
         ranks = t.empty(2 * n, dtype=t.int32, device=self.dev)
+        self._enter(test_edges, filter_keys, ranks)
         check(lib().ember_eval_ranks_filtered(self.ctx, _ptr(test_edges), n, _ptr(filter_keys),
                                               int(filter_keys.numel()), _ptr(ranks)))
         self.synchronize()

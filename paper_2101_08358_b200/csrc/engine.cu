@@ -2,9 +2,9 @@
 //
 // Engine: the device-resident training step (Algorithm 1, PAPER.md:84-99 / SPEC.md:376-384
 // train_epoch_sync semantics, bound = 1). Per batch:
-//   step stream:   sample -+-> gather+adjust -> contraction (scores, LSE, dA, dN) -> chain rule
-//                          |                                  (join) ^           -> loss
-//   helper stream:         +-> gradient-slot keys -> radix sort -> runs -> rank -+
+//   step stream:   sample + slot keys -+-> gather+adjust -> contraction (scores, LSE, dA, dN) -> chain rule
+//                                      |                              (join) ^           -> loss
+//   helper stream:                     +-> radix sort -> runs -> rank -------+
 //   then one segmented sum over the sorted gradient rows -> Adagrad (relations and nodes;
 //   relations synchronously, after an NCCL all-reduce when world > 1).
 // The helper stream only overlaps work that the step stream would otherwise serialise; the
@@ -215,17 +215,6 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     EMBER_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t3, s.counts, s.offsets, (int)cap_rows, side));
     s.cub_bytes = std::max(t1, std::max(t2, t3));
     s.cub_tmp = dalloc<uint8_t>(s.cub_bytes);
-    sets[0] = SortSet{s.negs, s.keys, s.keys_sorted, s.vals, s.vals_sorted, s.rank, s.ukeys, s.counts,
-                      s.offsets, s.nruns, s.longs, s.long_owner, s.uniq, s.cub_tmp};
-    sets[1] = SortSet{dalloc<uint32_t>(n_neg), dalloc<uint32_t>(cap_rows), dalloc<uint32_t>(cap_rows),
-                      dalloc<uint32_t>(cap_rows), dalloc<uint32_t>(cap_rows), dalloc<uint32_t>(cap_rows),
-                      dalloc<uint32_t>(cap_rows), dalloc<uint32_t>(cap_rows), dalloc<uint32_t>(cap_rows),
-                      dalloc<uint32_t>(1), dalloc<uint32_t>(2 + 3 * max_long), dalloc<uint32_t>(max_chunks),
-                      dalloc<uint8_t>(cap_rows), dalloc<uint8_t>(s.cub_bytes)};
-    EMBER_CUDA(cudaMemset(sets[1].longs, 0, 2 * sizeof(uint32_t)));
-    EMBER_CUDA(cudaEventCreateWithFlags(&ev_after_tc, cudaEventDisableTiming));
-    EMBER_CUDA(cudaEventCreateWithFlags(&ev_sampled, cudaEventDisableTiming));
-    for (int k = 0; k < 2; ++k) EMBER_CUDA(cudaEventCreateWithFlags(&ev_set_free[k], cudaEventDisableTiming));
     if (tc_engine()) tc_setup(*this);
     if (blas_engine()) blas_setup(*this);
     EMBER_CUDA(cudaStreamSynchronize(stream));
@@ -237,21 +226,13 @@ Engine::~Engine() {
     if (side && side != stream) cudaStreamSynchronize(side);
     tc_release(*this);
     blas_release(*this);
-    // (the sort scratch is owned by sets[0..1]; s.* only points at the current one)
     void* ptrs[] = {s.batch, s.A,         s.N,      s.Apk,       s.Npk,     s.fpos,       s.lse,    s.g0,
                     s.S,     s.dA,        s.dN_part, s.grows,    s.loss,    s.loss_part,  s.loss_done,  s.bad_batch, s.Ahl, s.Nhl, s.Phl,
-                    s.nunique, s.long_partial, s.rel_dense};
+                    s.nunique, s.long_partial, s.rel_dense, s.negs, s.keys, s.keys_sorted, s.vals, s.vals_sorted,
+                    s.rank, s.ukeys, s.counts, s.offsets, s.nruns, s.longs, s.long_owner, s.uniq, s.cub_tmp};
     for (void* p : ptrs)
         if (p) cudaFree(p);
-    for (const SortSet& t : sets) {
-        void* p1[] = {t.negs,  t.keys,  t.keys_sorted, t.vals,  t.vals_sorted, t.rank,      t.ukeys,
-                      t.counts, t.offsets, t.nruns,    t.longs, t.long_owner,  (void*)t.uniq, t.cub_tmp};
-        for (void* p : p1)
-            if (p) cudaFree(p);
-    }
     cudaGetLastError();
-    for (cudaEvent_t e : {ev_after_tc, ev_sampled, ev_set_free[0], ev_set_free[1]})
-        if (e) cudaEventDestroy(e);
     if (nccl_comm) {
         try {
             nccl().destroy(static_cast<ncclComm_t>(nccl_comm));
@@ -304,8 +285,12 @@ void Engine::sample(const uint32_t* bucket, uint64_t bucket_n, uint32_t i, uint3
 
 void Engine::sort_keys(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs) {
     const KeySpace ks = keyspace(i, j);
-    const uint32_t n = slots(nb);
     launch_keys(*this, edges, nb, negs, ks);
+    sort_slots(nb, ks);
+}
+
+void Engine::sort_slots(uint32_t nb, const KeySpace& ks) {
+    const uint32_t n = slots(nb);
     size_t bytes = s.cub_bytes;
     EMBER_CUDA(cub::DeviceRadixSort::SortPairs(s.cub_tmp, bytes, s.keys, s.keys_sorted, s.vals, s.vals_sorted, (int)n,
                                                0, (int)ks.bits, side));
@@ -326,24 +311,6 @@ void Engine::join_sorted() {
     sorted_pending = false;
 }
 
-void Engine::use_set(int k) {
-    const SortSet& t = sets[k];
-    s.negs = t.negs;
-    s.keys = t.keys;
-    s.keys_sorted = t.keys_sorted;
-    s.vals = t.vals;
-    s.vals_sorted = t.vals_sorted;
-    s.rank = t.rank;
-    s.ukeys = t.ukeys;
-    s.counts = t.counts;
-    s.offsets = t.offsets;
-    s.nruns = t.nruns;
-    s.longs = t.longs;
-    s.long_owner = t.long_owner;
-    s.uniq = t.uniq;
-    s.cub_tmp = t.cub_tmp;
-}
-
 void Engine::forward_backward(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs,
                               bool presorted) {
     const PartView pi = view(i), pj = view(j);
@@ -362,9 +329,6 @@ void Engine::forward_backward(const uint32_t* edges, uint32_t nb, uint32_t i, ui
         launch_contract_blas(*this, nb);
     else
         launch_contract_simt(*this, nb);
-    // the next step's sampling + sort may start now: they overlap this step's memory-bound phase
-    EMBER_CUDA(cudaEventRecord(ev_after_tc, stream));
-    have_after_tc = true;
     mark(PHASE_CHAIN);
     join_sorted();
     launch_chain_rule(*this, edges, nb, pi, pj);
@@ -449,27 +413,18 @@ void Engine::step(const uint32_t* edges, uint32_t nb, const uint32_t* bucket, ui
                   cudaEvent_t edges_ready) {
     if (nb == 0 || nb > cap_b) throw ConfigError("batch size must be in [1, batch_size]");
     check_bucket(i, j);
-    // Sampling and the (key, slot) sort of this step run on the helper stream with this step's
-    // parity of the sort scratch. They wait for the previous step's contraction (so they overlap
-    // that step's chain rule and reduction rather than competing with the persistent tensor-core
-    // kernels) and for the step that last used this scratch; the results do not depend on when
-    // they run (counter-based sampler, fixed inputs).
-    const int k = (int)(nsteps++ & 1);
-    use_set(k);
-    // (A/B: EMBER_SORT_AFTER_TC=1 holds them until the previous step's contraction is done; by
-    // default they start at once and run on the SMs the contraction kernels leave free)
-    static const bool after_tc = getenv("EMBER_SORT_AFTER_TC") != nullptr;
-    if (have_after_tc && after_tc) EMBER_CUDA(cudaStreamWaitEvent(side, ev_after_tc, 0));
-    if (set_used[k]) EMBER_CUDA(cudaStreamWaitEvent(side, ev_set_free[k], 0));
-    if (edges_ready) EMBER_CUDA(cudaStreamWaitEvent(side, edges_ready, 0));
+    // Sampling and the gradient-slot keys: one kernel on the step stream (ordered after the caller's
+    // work that produced the batch and the bucket). Only the (key, slot) sort forks onto the helper
+    // stream, where it overlaps the gathers and the contraction; the step stream joins it before the
+    // first gradient scatter. edges_ready: the batch is staged by another stream (host batches).
+    if (edges_ready) EMBER_CUDA(cudaStreamWaitEvent(stream, edges_ready, 0));
+    const KeySpace ks = keyspace(i, j);
     mark(PHASE_SAMPLE);
-    {
-        const uint64_t base = mix_seed(mix_seed(m.neg_seed, epoch, bucket_step), batch_in_bucket);
-        launch_sample_on(*this, side, s.negs, base, bucket, bucket_n, view(i), view(j));
-    }
-    EMBER_CUDA(cudaEventRecord(ev_sampled, side));
-    sort_keys(edges, nb, i, j, s.negs);
-    EMBER_CUDA(cudaStreamWaitEvent(stream, ev_sampled, 0));
+    const uint64_t base = mix_seed(mix_seed(m.neg_seed, epoch, bucket_step), batch_in_bucket);
+    launch_sample_keys(*this, edges, nb, base, bucket, bucket_n, view(i), view(j), ks);
+    EMBER_CUDA(cudaEventRecord(ev_fork, stream));
+    EMBER_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+    sort_slots(nb, ks);
     direct_hi = getenv_direct() ? 2 * nb : 0;
     loss_target = loss_out ? loss_out : s.loss;
     batch_tag = (1ull << 63) | ((epoch & 0xFFFFFull) << 40) | ((uint64_t)(bucket_step & 0xFFFFFu) << 20) |
@@ -479,8 +434,6 @@ void Engine::step(const uint32_t* edges, uint32_t nb, const uint32_t* bucket, ui
     mark(PHASE_REDUCE);
     reduce_and_apply(nb, i, j, true, nullptr, nullptr, nullptr, nullptr);
     direct_hi = 0;
-    EMBER_CUDA(cudaEventRecord(ev_set_free[k], stream));
-    set_used[k] = true;
     mark(PHASE_END);
 }
 

@@ -110,16 +110,6 @@ struct Scratch {
     float* rel_dense = nullptr;  // [R][dim] relation gradient summed over ranks (world > 1)
 };
 
-// The per-step sort scratch, double-buffered by step parity: step n+1's sampling and key sort run
-// on the helper stream while step n is still in its memory-bound phase (see Engine::step).
-struct SortSet {
-    uint32_t *negs = nullptr, *keys = nullptr, *keys_sorted = nullptr, *vals = nullptr, *vals_sorted = nullptr,
-             *rank = nullptr, *ukeys = nullptr, *counts = nullptr, *offsets = nullptr, *nruns = nullptr,
-             *longs = nullptr, *long_owner = nullptr;
-    uint8_t* uniq = nullptr;
-    void* cub_tmp = nullptr;
-};
-
 struct TcState;  // tensor-core engine state (tc_score.cu)
 
 struct Engine {
@@ -127,13 +117,6 @@ struct Engine {
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;  // key sort runs here, overlapped with gather + contraction
     cudaEvent_t ev_fork = nullptr, ev_sorted = nullptr;
-    // cross-step pipelining of sampling + sort (Engine::step)
-    SortSet sets[2];
-    bool set_used[2] = {false, false};
-    uint64_t nsteps = 0;
-    bool have_after_tc = false;
-    cudaEvent_t ev_after_tc = nullptr, ev_sampled = nullptr, ev_set_free[2] = {nullptr, nullptr};
-    void use_set(int k);
     // host-batch path: positives copied on `io` into one of two staging slots, overlapping the
     // previous step; ev_staged[k]: copy into slot k done; ev_consumed[k]: the step reading slot k done
     cudaStream_t io = nullptr, io_out = nullptr;  // host->device batches / device->host losses
@@ -200,8 +183,9 @@ struct Engine {
     // pipeline stages
     void sample(const uint32_t* bucket, uint64_t bucket_n, uint32_t i, uint32_t j, uint64_t epoch,
                 uint32_t bucket_step, uint32_t batch_in_bucket, uint32_t* negs_out);
-    // Keys of the batch's gradient slots, sorted on the helper stream (forked here).
+    // Keys of the batch's gradient slots, sorted on the helper stream (forked by the caller).
     void sort_keys(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs);
+    void sort_slots(uint32_t nb, const KeySpace& ks);  // sort of s.keys / s.vals on the helper stream
     void join_sorted();  // the step stream waits for sort_keys' results
     // Computes loss and gradient rows for one batch into grows (sorted order).
     void forward_backward(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs,
@@ -263,6 +247,9 @@ void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, c
                           bool packed, const uint32_t* negs, bool split_bf16 = false);
 void launch_gather_negatives(const Engine& E, const uint32_t* negs, const PartView& pi, const PartView& pj, bool packed);
 void launch_keys(const Engine& E, const uint32_t* edges, uint32_t nb, const uint32_t* negs, const KeySpace& ks);
+// the training step's sample_negatives + gradient-slot keys, one kernel on the step stream
+void launch_sample_keys(const Engine& E, const uint32_t* edges, uint32_t nb, uint64_t base, const uint32_t* bucket,
+                        uint64_t bucket_n, const PartView& src, const PartView& dst, const KeySpace& ks);
 void launch_rank(const Engine& E, uint32_t n);
 void launch_contract_simt(Engine& E, uint32_t nb);
 void launch_contract_blas(Engine& E, uint32_t nb);

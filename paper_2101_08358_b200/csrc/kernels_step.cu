@@ -29,25 +29,29 @@ __device__ __forceinline__ const float* node_row(const PartView& v, uint32_t id,
 
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 
+// Negative `slot` ([chunk][side][k] layout) of the batch whose stream seed is `base`.
+__device__ __forceinline__ uint32_t sample_one(uint32_t slot, uint32_t nt, uint32_t n_deg, uint64_t base,
+                                               const uint32_t* __restrict__ bucket, uint64_t bucket_n,
+                                               uint64_t src_first, uint64_t src_rows, uint64_t dst_first,
+                                               uint64_t dst_rows) {
+    const uint32_t k = slot % nt;
+    const uint32_t side = (slot / nt) & 1u;
+    Rng g(mix_seed(base, (uint64_t)slot));
+    if (k < n_deg && bucket_n > 0) {
+        const uint64_t e = g.uniform_below(bucket_n);
+        return bucket[3 * e + (side == 0 ? 2 : 0)];  // endpoint of a uniform bucket edge
+    }
+    if (side == 0) return (uint32_t)(dst_first + g.uniform_below(dst_rows));
+    return (uint32_t)(src_first + g.uniform_below(src_rows));
+}
+
 __global__ void k_sample(uint32_t* out, uint32_t nt, uint32_t n_deg, uint32_t total, uint64_t base,
                          const uint32_t* __restrict__ bucket, uint64_t bucket_n, uint64_t src_first, uint64_t src_rows,
                          uint64_t dst_first, uint64_t dst_rows) {
     griddep_wait();
     const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
     if (slot >= total) return;
-    const uint32_t k = slot % nt;
-    const uint32_t side = (slot / nt) & 1u;
-    Rng g(mix_seed(base, (uint64_t)slot));
-    uint32_t id;
-    if (k < n_deg && bucket_n > 0) {
-        const uint64_t e = g.uniform_below(bucket_n);
-        id = bucket[3 * e + (side == 0 ? 2 : 0)];  // endpoint of a uniform bucket edge
-    } else if (side == 0) {
-        id = (uint32_t)(dst_first + g.uniform_below(dst_rows));
-    } else {
-        id = (uint32_t)(src_first + g.uniform_below(src_rows));
-    }
-    out[slot] = id;
+    out[slot] = sample_one(slot, nt, n_deg, base, bucket, bucket_n, src_first, src_rows, dst_first, dst_rows);
 }
 
 // Coordinates are handled in quads: quad q of a row is {4q .. 4q+3} for Dot/DistMult and, for
@@ -313,6 +317,38 @@ __global__ void k_keys(const uint32_t* __restrict__ edges, uint32_t nb, const ui
     else if (i < 2 * nb) k = node_key(ks, edges[3 * (i - nb) + 2]);
     else if (i < 2 * nb + n_neg) k = node_key(ks, negs[i - 2 * nb]);
     else k = (uint32_t)ks.node_range + edges[3 * (i - 2 * nb - n_neg) + 1];
+    keys[i] = k;
+    vals[i] = i;
+}
+
+// The training step's first kernel: sample_negatives fused with the gradient-slot keys (the
+// negative slots sample their id and key it at once). It runs on the step stream, so every read
+// of the caller's batch / bucket is ordered after the caller's earlier work on that stream; only
+// the key sort forks onto the helper stream.
+__global__ void k_sample_keys(const uint32_t* __restrict__ edges, uint32_t nb, uint32_t* __restrict__ negs,
+                              uint32_t n_neg, uint32_t nt, uint32_t n_deg, uint64_t base,
+                              const uint32_t* __restrict__ bucket, uint64_t bucket_n, PartView src, PartView dst,
+                              uint32_t n_slots, KeySpace ks, uint32_t* keys, uint32_t* vals, uint32_t* longs) {
+    griddep_wait();
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) {  // long-segment list of this step's reduction
+        longs[0] = 0u;
+        longs[1] = 0u;
+    }
+    if (i >= n_slots) return;
+    uint32_t k;
+    if (i < nb) {
+        k = node_key(ks, edges[3 * i]);
+    } else if (i < 2 * nb) {
+        k = node_key(ks, edges[3 * (i - nb) + 2]);
+    } else if (i < 2 * nb + n_neg) {
+        const uint32_t id =
+            sample_one(i - 2 * nb, nt, n_deg, base, bucket, bucket_n, src.first, src.rows, dst.first, dst.rows);
+        negs[i - 2 * nb] = id;
+        k = node_key(ks, id);
+    } else {
+        k = (uint32_t)ks.node_range + edges[3 * (i - 2 * nb - n_neg) + 1];
+    }
     keys[i] = k;
     vals[i] = i;
 }
@@ -1274,6 +1310,15 @@ void launch_gather_negatives(const Engine& E, const uint32_t* negs, const PartVi
 void launch_keys(const Engine& E, const uint32_t* edges, uint32_t nb, const uint32_t* negs, const KeySpace& ks) {
     const uint32_t n = E.slots(nb);
     k_keys<<<(n + 255) / 256, 256, 0, E.side>>>(edges, nb, negs, E.n_neg, n, ks, E.s.keys, E.s.vals, E.s.longs);
+    EMBER_LAUNCHED(E);
+}
+
+void launch_sample_keys(const Engine& E, const uint32_t* edges, uint32_t nb, uint64_t base, const uint32_t* bucket,
+                        uint64_t bucket_n, const PartView& src, const PartView& dst, const KeySpace& ks) {
+    const uint32_t n = E.slots(nb);
+    const uint32_t n_deg = (uint32_t)ceil((double)E.m.alpha * (double)E.nt);
+    launch_pdl(k_sample_keys, dim3((n + 255) / 256), dim3(256), 0, E.stream, edges, nb, E.s.negs, E.n_neg, E.nt, n_deg,
+               base, bucket, bucket_n, src, dst, n, ks, E.s.keys, E.s.vals, E.s.longs);
     EMBER_LAUNCHED(E);
 }
 

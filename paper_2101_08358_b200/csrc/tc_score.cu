@@ -805,10 +805,12 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
         a.trace = t.trace;
     }
     // programmatic launch: the CTAs set up barriers and TMEM while the gathers drain
-    // The dN kernel's grid (items2, e.g. 144 of 148 SMs) also bounds the rows kernel's: same number
-    // of waves, and the SMs left free run the helper stream's sampling + sort for the next step.
+    // Performance only: when the dN kernel's grid (items2, e.g. 144 of 148 SMs) leaves at most
+    // kSpareSms SMs idle, the rows kernel takes the same grid (the same number of waves), and the
+    // free SMs run the helper stream's key sort. Test caps (EMBER_TC_MAXGRID) are used as given.
+    constexpr int kSpareSms = 8;
     const int g2 = std::min(items2, gmax);
-    const int grid1 = std::min(items1, g2 >= gmax - 8 ? g2 : gmax);
+    const int grid1 = std::min(items1, t.max_grid == 0 && E.sm_count - g2 <= kSpareSms ? g2 : gmax);
     launch_pdl(k_tc<MODE_ROWS>, dim3(grid1), dim3(NTHREADS), smem_total(t.KP, t.nstage, MODE_ROWS),
                E.stream, t.mA128, t.mN96, a);
     EMBER_LAUNCHED(E);
