@@ -9,8 +9,10 @@ BETA bucket order from a synthetic graph of the named shape, parameters resident
   value : edges/s with inputs already in HBM, CUDA events on the step stream, max over ranks.
   e2e   : the same steps through the host-buffer C-ABI call (ember_train_batch_host): every step
           copies its positives from pinned host memory and reads its loss back.
-  --impl reference: the CPU oracle (oracle/, the reference has no runnable trainer) on the host
-          cores, bounded sample per step, same metric/unit.
+  --impl reference: the reference's CPU training step (its SPEC restated in oracle/; the reference
+          ships no runnable trainer) on the host cores: same graph, plan and full batches as the GPU
+          arm's timed window, sampling + dedupe + gather + loss_and_grad + Adagrad per step; never
+          loads the product library.
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config fb86m] [--engine tc|simt]
 """
 from __future__ import annotations
@@ -158,12 +160,7 @@ class Workload:
         self.tr = eb.Trainer(h, cfg["V"], cfg["R"], p, device=device)
         self.tr.init_embeddings(INIT_SEED)
         self.plan = eb.make_plan("elimination", p, p, ORDER_SEED)  # all partitions resident: c = p
-        self.batches = []
-        for step, (i, j) in enumerate(self.plan["seq"]):
-            bk = int(i) * p + int(j)
-            lo, hi = int(self.offsets[bk]), int(self.offsets[bk + 1])
-            for k, b0 in enumerate(range(lo, hi, cfg["b"])):
-                self.batches.append((lo, hi, b0 - lo, min(cfg["b"], hi - b0), int(i), int(j), step, k))
+        self.batches = batch_list(self.plan["seq"], self.offsets, p, cfg["b"])
         self.base = self.edges.data_ptr()
         torch.cuda.synchronize()
 
@@ -266,7 +263,7 @@ def bench_distributed(args, rank, world, local_rank):
         return None
     flops_e, bytes_e = algorithmic(cfg)
     pk = peaks()
-    peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    peak = pk.get("bf16_tflops")
     contract_ms = prof["ms"]["contraction"] / n_prof if n_prof else 0.0  # per step
     achieved = flops_e * (n_edges / world / K) / (contract_ms / 1e3) / 1e12 if contract_ms > 0 else None
     return {
@@ -437,15 +434,28 @@ def bench_ours(args, rank, world, local_rank):
     achieved = flops_e * step_edges / (contract_ms / 1e3) / 1e12 if contract_ms > 0 else None
     exe = (executed_tc_flops(cfg, cfg["b"]) / (contract_ms / 1e3) / 1e12
            if contract_ms > 0 and args.engine == "tc" else None)
-    peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
-    traffic = None
+    # the contraction runs inside a 0.35 ms step at the maximum SM clock (clocks below): the burst
+    # peak is its denominator; the power-capped sustained figure is reported beside it
+    peak = pk.get("bf16_tflops")
+    peak_s = pk.get("bf16_tflops_sustained", peak)
+    traffic, ncu = None, {}
     prof_file = os.path.join(ROOT, "profiles", f"ncu_summary_{args.engine}.json")
     if os.path.exists(prof_file):
         try:
-            traffic = json.load(open(prof_file)).get("dram_bytes_per_launch")
+            ncu = json.load(open(prof_file))
+            traffic = ncu.get("dram_bytes_per_launch")
         except Exception:
-            traffic = None
+            ncu = {}
     value = edges / (ms / 1e3)
+    # memory-bound phases: this run's phase times against the DRAM bytes ncu measured for the same
+    # kernels (profiles/ncu_summary_<engine>.json, one cold-cache launch each)
+    hbm_phases = {}
+    for ph, mb in (ncu.get("phase_dram_mb") or {}).items():
+        t_ms = prof["ms"].get(ph, 0.0) / max(1, args.steps)
+        if t_ms > 0:
+            gbs = mb * 1e6 / (t_ms / 1e3) / 1e9
+            hbm_phases[ph] = {"ms": round(t_ms, 4), "dram_mb": mb, "gbs": round(gbs, 1),
+                              "frac": round(gbs / pk["hbm_gbs"], 4), "kernels": ncu.get("phase_kernels", {}).get(ph)}
     out = {
         "metric": METRIC if args.config == "fb86m" else f"train edges/sec ({cfg['desc']})",
         "value": round(value, 1),
@@ -474,12 +484,16 @@ def bench_ours(args, rank, world, local_rank):
         "roofline": {"bound": "tensor", "kernel": "contraction (scores + LSE + dA + dN)",
                      "achieved": round(achieved, 2) if achieved else None, "peak": peak, "unit": "TFLOP/s",
                      "frac": round(achieved / peak, 4) if achieved else None, "traffic": traffic,
-                     "flops_per_edge": flops_e, "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"
+                     "frac_sustained": round(achieved / peak_s, 4) if achieved else None,
+                     "flops_per_edge": flops_e, "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst: the step "
+                     "runs at the maximum SM clock); frac_sustained uses bf16_tflops_sustained"
                      + (" (fallback)" if pk.get("_fallback") else ""),
+                     "traffic_source": ncu.get("source"),
                      # the fp32-accurate bf16x3 scheme executes ~4.7x the algorithmic FLOPs (3 MMAs per
                      # product, S recomputed by the dN kernel, K and N padding): tensor-pipe utilisation
                      "executed_tflops": round(exe, 2) if exe else None,
                      "executed_frac": round(exe / peak, 4) if exe else None,
+                     "memory_phases": hbm_phases or None,
                      "executed_per_algorithmic": round(executed_tc_flops(cfg, cfg["b"]) / (flops_e * cfg["b"]), 3)
                      if args.engine == "tc" else None},
         "hbm_roofline_edges_per_s": round(pk["hbm_gbs"] * 1e9 / bytes_e, 1),
@@ -490,112 +504,149 @@ def bench_ours(args, rank, world, local_rank):
     return out
 
 
-# ------------------------------------------------------------------------------ CPU oracle
+# ------------------------------------------------------------------------------ CPU reference path
 
-def _oracle_sample(W_or_graph, cfg, rows_per_step, max_steps, budget_s, threads=None):
-    """Runs the CPU oracle (oracle/liboracle.so) on bounded samples of the same batch stream.
-    Each sample = `rows_per_step` positives of one batch with that batch's full negative sets."""
-    from oracle import pyoracle as po
-    edges, offsets, batches = W_or_graph
-    m = po.model(cfg["kind"], dim=cfg["dim"], lr=0.1, eps=1e-10, n_t=cfg["nt"], alpha=cfg["alpha"], chunks=1,
-                 seed=NEG_SEED)
-    L = po.lib()
-    all_threads = L.orc_num_threads()
-    if threads:
-        L.orc_set_num_threads(threads)
-    done_edges, t_total, n = 0, 0.0, 0
-    V, p, d = cfg["V"], cfg["p"], cfg["dim"]
-    for (lo, hi, begin, nb, i, j, step, k) in batches:
-        if n >= max_steps or (t_total >= budget_s and n > 0):
-            break
-        bucket = edges(lo, hi)
-        negs = po.sample_negatives(m, 0, step, k, bucket, po.part_offset(V, p, i), po.part_size(V, p, i),
-                                   po.part_offset(V, p, j), po.part_size(V, p, j))
-        batch = bucket[begin:begin + min(nb, rows_per_step)]
-        ids, inv = np.unique(np.concatenate([batch[:, 0], batch[:, 2], negs]), return_inverse=True)
-        nbat = len(batch)
-        cb = np.stack([inv[:nbat], batch[:, 1], inv[nbat:2 * nbat]], 1).astype(np.uint32)
-        cn = inv[2 * nbat:].astype(np.uint32)
-        theta = np.concatenate([po.init_rows(INIT_SEED, d, int(g), 1) for g in ids]) if len(ids) < 2000 else \
-            _init_many(po, ids, d)
-        acc = np.zeros_like(theta)
-        rels, rinv = np.unique(batch[:, 1], return_inverse=True)
-        cb[:, 1] = rinv
-        rt = np.concatenate([po.init_rows(INIT_SEED ^ 0x52454C, d, int(r), 1) for r in rels]) \
-            if cfg["kind"] != "dot" else np.zeros((1, d), np.float32)
-        ra = np.zeros_like(rt)
-        t0 = time.perf_counter()
-        out = po.loss_and_grad(m, cb, cn, theta, rt)                    # loss_and_grad (SPEC.md:157)
-        if len(out["rel_ids"]):
-            po.adagrad_apply(d, 0.1, 1e-10, out["rel_ids"], out["rel_rows"], rt, ra)
-        po.adagrad_apply(d, 0.1, 1e-10, out["node_ids"], out["node_rows"], theta, acc)
-        t_total += time.perf_counter() - t0
-        done_edges += nbat
-        n += 1
-    used = L.orc_num_threads()
-    if threads:
-        L.orc_set_num_threads(all_threads)
-    return done_edges, t_total, n, used
-
-
-def _init_many(po, ids, d):
-    # contiguous runs are initialised in one call each (rows are independent streams)
-    out = np.empty((len(ids), d), np.float32)
-    runs = np.split(np.arange(len(ids)), np.where(np.diff(ids) != 1)[0] + 1)
-    for r in runs:
-        out[r] = po.init_rows(INIT_SEED, d, int(ids[r[0]]), len(r))
+def batch_list(plan_seq, offsets, p, b):
+    """The epoch's batches in plan order: (lo, hi, begin, nb, i, j, bucket_step, batch_in_bucket)."""
+    out = []
+    for step, (i, j) in enumerate(plan_seq):
+        bk = int(i) * p + int(j)
+        lo, hi = int(offsets[bk]), int(offsets[bk + 1])
+        for k, b0 in enumerate(range(lo, hi, b)):
+            out.append((lo, hi, b0 - lo, min(b, hi - b0), int(i), int(j), step, k))
     return out
 
 
+class CpuTrainer:
+    """The reference's CPU training step (oracle/ember_oracle.c orc_train_batch_parts, OpenMP on the host
+    cores): per batch sample_negatives -> dedupe of the batch's node ids -> gather of the parameter slice
+    -> loss_and_grad -> Adagrad of relations and touched node rows, with partitions i and j held in host
+    memory (initialised like the device tables on first use, outside any timed region)."""
+
+    def __init__(self, cfg, edges_fn):
+        from oracle import pyoracle as po
+        self.po, self.cfg, self.edges_fn = po, cfg, edges_fn
+        d = cfg["dim"]
+        self.m = po.model(cfg["kind"], dim=d, lr=0.1, eps=1e-10, n_t=cfg["nt"], alpha=cfg["alpha"], chunks=1,
+                          seed=NEG_SEED)
+        R = cfg["R"] if cfg["kind"] != "dot" else 1
+        self.rel_theta = po.init_rows(INIT_SEED ^ 0x52454C, d, 0, R).reshape(R, d)
+        self.rel_acc = np.zeros_like(self.rel_theta)
+        self.parts = {}
+
+    def part(self, k):
+        if k not in self.parts:
+            V, p, d = self.cfg["V"], self.cfg["p"], self.cfg["dim"]
+            first, rows = self.po.part_offset(V, p, k), self.po.part_size(V, p, k)
+            th = self.po.init_rows(INIT_SEED, d, first, rows).reshape(rows, d)
+            self.parts[k] = (first, th, np.zeros_like(th))
+        return self.parts[k]
+
+    def step(self, batch, epoch=0):
+        lo, hi, begin, nb, i, j, step, k = batch
+        bucket = self.edges_fn(lo, hi)
+        pi, pj = self.part(i), self.part(j)
+        return self.po.train_batch_parts(self.m, epoch, step, k, bucket, begin, nb, pi, pj, self.rel_theta,
+                                         self.rel_acc)
+
+    def run(self, batches, budget_s, max_steps, threads=None):
+        """Timed steps (host wall clock around each C call) until max_steps or budget_s of CPU work."""
+        L = self.po.lib()
+        all_threads = L.orc_num_threads()
+        if threads:
+            L.orc_set_num_threads(threads)
+        done, t_total, n = 0, 0.0, 0
+        try:
+            for bt in batches:
+                if n >= max_steps or (t_total >= budget_s and n > 0):
+                    break
+                self.part(bt[4]), self.part(bt[5])  # (table initialisation stays outside the timing)
+                t0 = time.perf_counter()
+                loss, _ = self.step(bt)
+                t_total += time.perf_counter() - t0
+                if not np.isfinite(loss):
+                    raise RuntimeError("CPU reference: non-finite loss")
+                done += bt[3]
+                n += 1
+            used = L.orc_num_threads()
+        finally:
+            if threads:
+                L.orc_set_num_threads(all_threads)
+        return done, t_total, n, used
+
+
 def cpu_baseline(W, args, budget_s=20.0):
+    """The reference CPU path timed on this host beside the GPU run (rank 0, N=1): the same batches as
+    the timed GPU steps, full b positives each (sampling and dedupe inside the timing)."""
     cfg = W.cfg
     edges_fn = lambda lo, hi: W.edges[lo:hi].cpu().numpy().view(np.uint32)  # noqa: E731
-    start = len(W.batches) // 3
-    rows = min(cfg["b"], args.cpu_rows)
-    done, t, n, thr = _oracle_sample((edges_fn, W.offsets, W.batches[start:]), cfg, rows, 1000, budget_s)
-    # SURVEY.md §8(d): the 1-thread rate beside the all-core one (a shorter window of the same stream)
-    d1, t1, n1, _ = _oracle_sample((edges_fn, W.offsets, W.batches[start:]), cfg, rows, 1000, budget_s / 4, threads=1)
+    start = len(W.batches) // 3 + args.warmup
+    cpu = CpuTrainer(cfg, edges_fn)
+    done, t, n, thr = cpu.run(W.batches[start:], budget_s, 1000)
+    # SURVEY.md §8(d): the 1-thread rate beside the all-core one (one batch of the same stream)
+    d1, t1, n1, _ = cpu.run(W.batches[start + n:], budget_s / 4, 1, threads=1)
     return {"value": round(done / t, 1), "unit": "edges/s", "cores": thr, "kind": "port",
             "single_thread_value": round(d1 / t1, 1),
-            "sample": f"{n} batch samples x {rows} positives (of b={cfg['b']}) with the batch's full "
-                      f"{cfg['nt']}-per-side shared negatives; CPU oracle (oracle/ember_oracle.c, OpenMP), "
-                      f"{t:.1f} s of CPU work on {thr} threads (+ {n1} samples, {t1:.1f} s on 1 thread)"}
+            "sample": f"{n} full batches (b={cfg['b']} positives, {cfg['nt']}-per-side shared negatives) of the timed "
+                      f"GPU steps' batch stream, sampling + dedupe + gather + loss_and_grad + Adagrad "
+                      f"(oracle/ember_oracle.c orc_train_batch_parts, OpenMP): {t:.1f} s on {thr} threads "
+                      f"(+ {n1} batch, {t1:.1f} s on 1 thread)"}
 
 
 def bench_reference(args, rank, world):
-    """--impl reference: the CPU path of the reference on this host's cores. The reference ships no
-    trainer (proj/src/model.cpp, pipeline.cpp absent), so this is our C restatement (oracle/)."""
+    """--impl reference: the reference's CPU training step on this host's cores. The reference ships no
+    trainer (proj/src/model.cpp, pipeline.cpp absent), so its algorithm runs as our C restatement
+    (oracle/ember_oracle.c); the graph comes from the oracle's restatement of the benchmark generator and
+    the bucket order from the reference's own make_plan (ordering.cpp built in place, oracle/_ref). Same
+    graph, plan, batches (the GPU arm's timed window) and full batch size as our arm; nothing here loads
+    the product library."""
     if rank != 0:
         return None
-    import paper_2101_08358_b200 as eb
+    from oracle import pyoracle as po
     cfg = CONFIGS[args.config]
-    # host-side graph (no GPU needed): only the buckets the sample touches
-    n_gen = min(cfg["E"], 4_000_000)
-    edges, split = eb.generate_graph(cfg["V"], cfg["R"], n_gen, GRAPH_SEED, cfg["train"], cfg["valid"])
-    train = edges[split == 0]
-    bucketed, offsets = eb.bucket_edges(train, cfg["V"], cfg["p"])
-    plan = eb.make_plan("elimination", cfg["p"], cfg["p"], ORDER_SEED)
-    batches = []
-    for step, (i, j) in enumerate(plan["seq"]):
-        bk = int(i) * cfg["p"] + int(j)
-        lo, hi = int(offsets[bk]), int(offsets[bk + 1])
-        for k, b0 in enumerate(range(lo, hi, cfg["b"])):
-            batches.append((lo, hi, b0 - lo, min(cfg["b"], hi - b0), int(i), int(j), step, k))
-    rows = min(cfg["b"], args.cpu_rows)
-    fn = lambda lo, hi: bucketed[lo:hi]  # noqa: E731
-    _oracle_sample((fn, offsets, batches), cfg, rows, args.warmup, 1e9)
-    done, t, n, thr = _oracle_sample((fn, offsets, batches[args.warmup:]), cfg, rows, args.steps, 1e9)
+    t0 = time.perf_counter()
+    edges, split = po.graph_generate(cfg["V"], cfg["R"], cfg["E"], GRAPH_SEED, cfg["train"], cfg["valid"])
+    bucketed, offsets = po.graph_bucket(cfg["V"], cfg["p"], edges, split, 0)
+    del edges, split
+    plan = po.ref_plan(0, cfg["p"], cfg["p"], ORDER_SEED)  # OrderingKind::Elimination (ordering.h:14), c = p
+    batches = batch_list(plan["seq"], offsets, cfg["p"], cfg["b"])
+    setup_s = time.perf_counter() - t0
+    cpu = CpuTrainer(cfg, lambda lo, hi: bucketed[lo:hi])
+    first = len(batches) // 3 + args.warmup  # the first batch the GPU arm times
+    warm = min(args.warmup, 3)  # (untimed, on the batches just before it)
+    cpu.run(batches[first - warm:first], 1e9, warm)
+    done, t, n, thr = cpu.run(batches[first:], args.cpu_budget, args.steps)
     v = done / t
     return {"metric": METRIC if args.config == "fb86m" else f"train edges/sec ({cfg['desc']})", "impl": "reference",
-            "value": round(v, 1), "unit": "edges/s", "n_gpus": world, "steps": n, "warmup": args.warmup,
+            "value": round(v, 1), "unit": "edges/s", "n_gpus": world, "steps": n, "warmup": warm,
             "ms_per_step": round(1e3 * t / max(1, n), 3), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic (same generator and batch stream)",
-            "config": {"workload": cfg["desc"], "sample_rows_per_step": rows, "negatives_per_side": cfg["nt"]},
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (same generator, graph, plan and batch stream)",
+            "config": {"workload": cfg["desc"], "nodes": cfg["V"], "relations": cfg["R"], "edges_total": cfg["E"],
+                       "train_edges": int(offsets[-1]), "model": cfg["kind"], "dim": cfg["dim"], "batch": cfg["b"],
+                       "negatives_per_side": cfg["nt"], "alpha": cfg["alpha"], "partitions": cfg["p"],
+                       "ordering": "elimination (BETA), reference make_plan", "first_batch": first,
+                       "setup_s": round(setup_s, 1)},
             "cpu_baseline": {"value": round(v, 1), "unit": "edges/s", "cores": thr, "kind": "port",
-                             "sample": f"{n} steps x {rows} positives with full shared negatives; the reference has "
-                                       "no runnable trainer (proj/src/model.cpp absent), oracle/ember_oracle.c is "
-                                       "its SPEC restatement"},
-            "e2e": {"value": round(v, 1), "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                             "sample": f"{n} full batches of b={cfg['b']} from the GPU arm's timed window (batch "
+                                       f"{first} on), sampling + dedupe + gather + loss_and_grad + Adagrad per "
+                                       f"step; the reference has no runnable trainer (proj/src/model.cpp absent), "
+                                       f"oracle/ember_oracle.c is its SPEC restatement"
+                                       + (f"; stopped at the {args.cpu_budget:.0f} s budget" if n < args.steps else "")},
+            "e2e": {"value": round(v, 1), "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "native_libraries": loaded_native_libraries()}
+
+
+def loaded_native_libraries():
+    """The repo's own shared objects mapped into this process (the reference arm must map only oracle/)."""
+    libs = set()
+    try:
+        for line in open("/proc/self/maps"):
+            path = line.split()[-1] if len(line.split()) >= 6 else ""
+            if path.startswith(ROOT) and path.endswith(".so"):
+                libs.add(os.path.relpath(path, ROOT))
+    except OSError:
+        pass
+    return sorted(libs)
 
 
 def main():
@@ -607,7 +658,8 @@ def main():
     ap.add_argument("--config", default="fb86m", choices=sorted(CONFIGS))
     ap.add_argument("--engine", default=os.environ.get("EMBER_ENGINE", "tc"), choices=["simt", "tc", "blas"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--cpu-rows", type=int, default=5000)
+    ap.add_argument("--cpu-budget", type=float, default=150.0,
+                    help="--impl reference: stop timing after this many seconds of CPU work")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--capacity", type=int, default=0,
                     help="partition-buffer capacity c < p: train through the device buffer (one timed epoch)")

@@ -269,6 +269,12 @@ double orc_loss_and_grad(const orc_model* m, const uint32_t* edges, uint32_t nb,
     int bad = 0;
 
     for (uint64_t i = 0; i < nneg; ++i) memcpy(N + i * d, node_theta + (uint64_t)negs[i] * d, d * sizeof(float));
+    /* N^T per (chunk, side): [j][k], so the scores of one edge against all n_t negatives run as
+     * independent sums across k, each accumulated over j in the order dotf uses (same result bits) */
+    float* NT = (float*)malloc((nneg ? nneg : 1) * d * sizeof(float));
+    for (uint64_t cs = 0; cs < (uint64_t)chunks * 2; ++cs)
+        for (uint32_t k = 0; k < nt; ++k)
+            for (uint32_t j = 0; j < d; ++j) NT[(cs * d + j) * nt + k] = N[(cs * nt + k) * d + j];
 
     /* gather + adjust + positive score (Alg.1 formBatch) */
 #pragma omp parallel for schedule(static)
@@ -290,11 +296,17 @@ double orc_loss_and_grad(const orc_model* m, const uint32_t* edges, uint32_t nb,
         for (uint32_t side = 0; side < 2; ++side) {
             const float* a = A + ((uint64_t)side * nb + e) * d;
             const float* Ns = N + ((uint64_t)q * 2 + side) * nt * d;
+            const float* NTs = NT + ((uint64_t)q * 2 + side) * nt * d;
             float* p = P + ((uint64_t)side * nb + e) * nt;
             const float f = fpos[e];
             float mx = f;
+            for (uint32_t k = 0; k < nt; ++k) p[k] = 0.f;
+            for (uint32_t j = 0; j < d; ++j) {  /* p[k] = dotf(a, N_k) for every k */
+                const float aj = a[j];
+                const float* col = NTs + (uint64_t)j * nt;
+                for (uint32_t k = 0; k < nt; ++k) p[k] += aj * col[k];
+            }
             for (uint32_t k = 0; k < nt; ++k) {
-                p[k] = dotf(a, Ns + (uint64_t)k * d, d);
                 if (!(p[k] == p[k]) || isinf(p[k])) bad = 1;
                 if (p[k] > mx) mx = p[k];
             }
@@ -320,19 +332,25 @@ double orc_loss_and_grad(const orc_model* m, const uint32_t* edges, uint32_t nb,
         loss_e[e] = le;
     }
 
-    /* dN = P^T A per chunk and side, fixed edge order */
-#pragma omp parallel for schedule(static)
-    for (int64_t i = 0; i < (int64_t)nneg; ++i) {
-        const uint32_t q = (uint32_t)(i / (2 * nt));
-        const uint32_t side = (uint32_t)((i / nt) % 2);
-        const uint32_t k = (uint32_t)(i % nt);
+    /* dN = P^T A per chunk and side, fixed edge order; blocks of 16 negatives walk the
+     * edges once (row-contiguous reads of P and A), every element still summed in edge order */
+    const uint64_t nblk = (nt + 15) / 16;
+#pragma omp parallel for schedule(dynamic)
+    for (int64_t bi = 0; bi < (int64_t)((uint64_t)chunks * 2 * nblk); ++bi) {
+        const uint32_t cs = (uint32_t)(bi / nblk);
+        const uint32_t q = cs / 2, side = cs % 2;
+        const uint32_t k0 = (uint32_t)(bi % nblk) * 16;
+        const uint32_t k1 = k0 + 16 < nt ? k0 + 16 : nt;
         const uint32_t e0 = q * chunk_rows;
         const uint32_t e1 = e0 + chunk_rows < nb ? e0 + chunk_rows : nb;
-        float* out = dN + (uint64_t)i * d;
         for (uint32_t e = e0; e < e1; ++e) {
-            const float pk = P[((uint64_t)side * nb + e) * nt + k];
+            const float* prow = P + ((uint64_t)side * nb + e) * nt;
             const float* a = A + ((uint64_t)side * nb + e) * d;
-            for (uint32_t j = 0; j < d; ++j) out[j] += pk * a[j];
+            for (uint32_t k = k0; k < k1; ++k) {
+                const float pk = prow[k];
+                float* out = dN + ((uint64_t)cs * nt + k) * d;
+                for (uint32_t j = 0; j < d; ++j) out[j] += pk * a[j];
+            }
         }
     }
 
@@ -423,6 +441,7 @@ double orc_loss_and_grad(const orc_model* m, const uint32_t* edges, uint32_t nb,
     free(dA);
     free(P);
     free(N);
+    free(NT);
     free(dN);
     free(fpos);
     free(g0);
@@ -667,4 +686,197 @@ void orc_preprocess(const uint32_t* raw, uint64_t n, uint32_t p, uint64_t seed, 
     free(eorder);
     free(sh);
     free(at);
+}
+
+/* ---------------------------------------------------------------- synthetic graphs
+ * The benchmark graph generator, restated for the CPU arm so that it never loads the product library.
+ * Edge e is a pure function of (seed, e) — the definition ember_graph_generate implements
+ * (paper_2101_08358_b200/csrc/graph.cu:1-9): power-law source ranks w(r) ∝ (r+1)^-0.9 by inverse CDF,
+ * Zipf(1) relations, with probability 0.9 a power-law destination inside community pi_r(comm(src))
+ * (comm = rank mod K, pi_r affine on Z_K), else global; ranks become ids through a keyed 4-round
+ * Feistel permutation with cycle walking. */
+typedef struct {
+    uint64_t V, seed;
+    uint32_t R, K, half;
+    double train, valid;
+} orc_gen;
+
+static double g_u01(uint64_t h) { return (double)(h >> 11) * 0x1.0p-53; }
+
+static uint64_t g_powerlaw(double u, uint64_t n) {
+    const double a = pow((double)n + 1.0, 0.1) - 1.0;
+    const double x = pow(1.0 + u * a, 10.0);
+    const uint64_t r = x < 1.0 ? 0 : (uint64_t)x - 1;
+    return r >= n ? n - 1 : r;
+}
+
+static uint32_t g_zipf(double u, uint32_t R) {
+    const double x = exp(u * log((double)R + 1.0));
+    const uint32_t r = x < 1.0 ? 0 : (uint32_t)x - 1;
+    return r >= R ? R - 1 : r;
+}
+
+static uint64_t g_feistel(uint64_t x, const orc_gen* g) {
+    const uint64_t mask = (1ULL << g->half) - 1;
+    do {
+        uint64_t l = x >> g->half, r = x & mask;
+        for (uint32_t round = 0; round < 4; ++round) {
+            const uint64_t f = orc_splitmix64(r ^ orc_mix_seed(g->seed, 0xfe15ULL + round)) & mask;
+            const uint64_t nl = r;
+            r = l ^ f;
+            l = nl;
+        }
+        x = (l << g->half) | r;
+    } while (x >= g->V);
+    return x;
+}
+
+static void g_edge(const orc_gen* g, uint64_t e, uint32_t* out3, uint8_t* split) {
+    const uint64_t h = orc_mix_seed(g->seed, e);
+    const uint64_t src = g_powerlaw(g_u01(orc_splitmix64(h + 1)), g->V);
+    const uint32_t rel = g->R <= 1 ? 0u : g_zipf(g_u01(orc_splitmix64(h + 2)), g->R);
+    uint64_t dst;
+    if (g_u01(orc_splitmix64(h + 3)) < 0.9) {
+        const uint64_t c = src & (g->K - 1);
+        uint64_t c2 = c;
+        if (g->R > 1) {
+            const uint64_t hr = orc_mix_seed(g->seed ^ 0x7e1aULL, rel);
+            const uint64_t a = 2 * (hr % (g->K / 2 > 0 ? g->K / 2 : 1)) + 1;
+            c2 = (a * c + (orc_splitmix64(hr) & (g->K - 1))) & (g->K - 1);
+        }
+        const uint64_t members = (g->V - c2 + g->K - 1) / g->K;
+        dst = c2 + g->K * g_powerlaw(g_u01(orc_splitmix64(h + 4)), members);
+    } else {
+        dst = g_powerlaw(g_u01(orc_splitmix64(h + 4)), g->V);
+    }
+    out3[0] = (uint32_t)g_feistel(src, g);
+    out3[1] = rel;
+    out3[2] = (uint32_t)g_feistel(dst, g);
+    if (split) {
+        const double us = g_u01(orc_splitmix64(h + 5));
+        *split = us < g->train ? 0 : (us < g->train + g->valid ? 1 : 2);
+    }
+}
+
+void orc_graph_generate(uint64_t V, uint32_t R, uint64_t first, uint64_t n, uint64_t seed, float train_frac,
+                        float valid_frac, uint32_t* edges, uint8_t* split) {
+    orc_gen g;
+    g.V = V;
+    g.R = R;
+    g.K = 1;
+    while (g.K < 1024 && (uint64_t)g.K * 8 <= V) g.K <<= 1;
+    g.seed = seed;
+    uint32_t bits = 1;
+    while ((1ULL << bits) < V) ++bits;
+    g.half = (bits + 1) / 2;
+    g.train = train_frac; /* float -> double, as the device generator widens them */
+    g.valid = valid_frac;
+#pragma omp parallel for schedule(static, 65536)
+    for (int64_t e = 0; e < (int64_t)n; ++e) g_edge(&g, first + (uint64_t)e, edges + 3 * e, split ? split + e : NULL);
+}
+
+/* bucket_edges of the edges whose split byte is `which` (split NULL: all edges):
+ * stable counting sort by (part(src), part(dst)); out: the selected edges bucketed, offsets[p*p+1]. */
+uint64_t orc_graph_bucket(uint64_t V, uint32_t p, const uint32_t* edges, const uint8_t* split, uint8_t which,
+                          uint64_t n, uint32_t* out, uint64_t* offsets) {
+    const uint32_t nb = p * p;
+    memset(offsets, 0, ((size_t)nb + 1) * sizeof(uint64_t));
+    for (uint64_t e = 0; e < n; ++e)
+        if (!split || split[e] == which) ++offsets[part_of(edges[3 * e], V, p) * p + part_of(edges[3 * e + 2], V, p) + 1];
+    for (uint32_t b = 0; b < nb; ++b) offsets[b + 1] += offsets[b];
+    uint64_t* at = (uint64_t*)malloc(((size_t)nb + 1) * sizeof(uint64_t));
+    memcpy(at, offsets, ((size_t)nb + 1) * sizeof(uint64_t));
+    for (uint64_t e = 0; e < n; ++e) {
+        if (split && split[e] != which) continue;
+        const uint64_t k = at[part_of(edges[3 * e], V, p) * p + part_of(edges[3 * e + 2], V, p)]++;
+        memcpy(out + 3 * k, edges + 3 * e, 12);
+    }
+    free(at);
+    return offsets[nb];
+}
+
+/* ---------------------------------------------------------------- the CPU trainer's step on partitions
+ * Marius's CPU path for one batch of bucket (i, j) with partitions i and j resident in host memory
+ * (Algorithm 1; getCpuParameters / updateCpuParameters):
+ * sample_negatives -> unique node ids of the batch (dedupe) -> gather their rows into a compact
+ * parameter slice -> loss_and_grad -> Adagrad of the relations and of the touched node rows in place. */
+static int u32_cmp_q(const void* a, const void* b) {
+    const uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+    return x < y ? -1 : x > y;
+}
+
+double orc_train_batch_parts(const orc_model* m, uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket,
+                             const uint32_t* bucket_edges, uint64_t bucket_n, uint64_t batch_begin, uint32_t nb,
+                             uint64_t first_i, uint64_t rows_i, float* theta_i, float* acc_i, uint64_t first_j,
+                             uint64_t rows_j, float* theta_j, float* acc_j, float* rel_theta, float* rel_acc,
+                             uint32_t* n_unique_out) {
+    const uint32_t d = m->dim;
+    const uint32_t chunks = m->num_chunks ? m->num_chunks : 1;
+    const uint64_t nneg = (uint64_t)chunks * 2 * m->num_negatives;
+    const uint32_t* batch = bucket_edges + 3 * batch_begin;
+    uint32_t* negs = (uint32_t*)malloc((nneg ? nneg : 1) * sizeof(uint32_t));
+    /* negatives: destination side from partition j, source side from partition i */
+    orc_sample_negatives(m, epoch, bucket_step, batch_in_bucket, bucket_edges, bucket_n, first_i, rows_i, first_j,
+                         rows_j, negs);
+    const uint64_t cap = 2 * (uint64_t)nb + nneg;
+    uint32_t* uniq = (uint32_t*)malloc(cap * sizeof(uint32_t));
+    for (uint32_t e = 0; e < nb; ++e) {
+        uniq[e] = batch[3 * e];
+        uniq[nb + e] = batch[3 * e + 2];
+    }
+    memcpy(uniq + 2 * (uint64_t)nb, negs, nneg * sizeof(uint32_t));
+    qsort(uniq, cap, sizeof(uint32_t), u32_cmp_q);
+    uint32_t nu = 0;
+    for (uint64_t k = 0; k < cap; ++k)
+        if (k == 0 || uniq[k] != uniq[k - 1]) uniq[nu++] = uniq[k];
+    /* compact ids and the gathered parameter slice */
+    uint32_t* cb = (uint32_t*)malloc((size_t)nb * 3 * sizeof(uint32_t));
+    uint32_t* cn = (uint32_t*)malloc((nneg ? nneg : 1) * sizeof(uint32_t));
+    float* slice = (float*)malloc((size_t)nu * d * sizeof(float));
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < (int64_t)nb; ++e) {
+        cb[3 * e] = lower_bound32(uniq, nu, batch[3 * e]);
+        cb[3 * e + 1] = batch[3 * e + 1];
+        cb[3 * e + 2] = lower_bound32(uniq, nu, batch[3 * e + 2]);
+    }
+    for (uint64_t k = 0; k < nneg; ++k) cn[k] = lower_bound32(uniq, nu, negs[k]);
+#pragma omp parallel for schedule(static)
+    for (int64_t u = 0; u < (int64_t)nu; ++u) {
+        const uint64_t id = uniq[u];
+        const float* src = id - first_i < rows_i ? theta_i + (id - first_i) * d : theta_j + (id - first_j) * d;
+        memcpy(slice + (uint64_t)u * d, src, d * sizeof(float));
+    }
+    uint32_t* ids = (uint32_t*)malloc(cap * sizeof(uint32_t));
+    float* rows = (float*)malloc(cap * d * sizeof(float));
+    uint32_t* rids = (uint32_t*)malloc((size_t)(nb ? nb : 1) * sizeof(uint32_t));
+    float* rrows = (float*)malloc((size_t)(nb ? nb : 1) * d * sizeof(float));
+    uint32_t ng = 0, nr = 0;
+    const double loss =
+        orc_loss_and_grad(m, cb, nb, cn, slice, rel_theta, NULL, NULL, ids, rows, &ng, rids, rrows, &nr);
+    if (nr) orc_adagrad_apply(d, m->lr, m->eps, rids, rrows, nr, rel_theta, rel_acc);
+    /* node Adagrad straight into the partition tables (compact id -> global id -> partition row) */
+#pragma omp parallel for schedule(static)
+    for (int64_t u = 0; u < (int64_t)ng; ++u) {
+        const uint64_t id = uniq[ids[u]];
+        const int in_i = id - first_i < rows_i;
+        float* th = in_i ? theta_i + (id - first_i) * d : theta_j + (id - first_j) * d;
+        float* ac = in_i ? acc_i + (id - first_i) * d : acc_j + (id - first_j) * d;
+        const float* g = rows + (uint64_t)u * d;
+        for (uint32_t k = 0; k < d; ++k) {
+            const float a = ac[k] + g[k] * g[k];
+            ac[k] = a;
+            th[k] -= m->lr * g[k] / (sqrtf(a) + m->eps);
+        }
+    }
+    if (n_unique_out) *n_unique_out = nu;
+    free(negs);
+    free(uniq);
+    free(cb);
+    free(cn);
+    free(slice);
+    free(ids);
+    free(rows);
+    free(rids);
+    free(rrows);
+    return loss;
 }

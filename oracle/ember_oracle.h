@@ -105,6 +105,24 @@ void orc_preprocess(const uint32_t* raw, uint64_t n, uint32_t p, uint64_t seed, 
                     uint32_t* train_out, uint64_t* offsets, uint32_t* valid_out, uint32_t* test_out, uint64_t* counts,
                     uint32_t* node_tokens, uint32_t* rel_tokens, uint64_t* num_nodes, uint32_t* num_rel);
 
+/* The benchmark graph generator (the definition ember_graph_generate implements):
+ * edges first .. first+n-1 of the graph (V, R, seed) into edges (n x 3), split bytes (nullable). */
+void orc_graph_generate(uint64_t V, uint32_t R, uint64_t first, uint64_t n, uint64_t seed, float train_frac,
+                        float valid_frac, uint32_t* edges, uint8_t* split);
+/* bucket_edges: the edges with split byte `which` (split NULL: all), stably sorted by
+ * (part(src), part(dst)); offsets: p*p+1. Returns the number of selected edges. */
+uint64_t orc_graph_bucket(uint64_t V, uint32_t p, const uint32_t* edges, const uint8_t* split, uint8_t which,
+                          uint64_t n, uint32_t* out, uint64_t* offsets);
+/* The CPU trainer's step on a batch of bucket (i, j) with partitions i and j in host memory
+ * ([rows x dim] theta/acc each, global rows first_i.. / first_j..; i == j: pass the same partition
+ * twice): sample -> dedupe -> gather the parameter slice -> loss_and_grad -> Adagrad in place.
+ * Returns the batch loss; *n_unique_out (nullable) = unique node rows of the batch. */
+double orc_train_batch_parts(const orc_model* m, uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket,
+                             const uint32_t* bucket_edges, uint64_t bucket_n, uint64_t batch_begin, uint32_t nb,
+                             uint64_t first_i, uint64_t rows_i, float* theta_i, float* acc_i, uint64_t first_j,
+                             uint64_t rows_j, float* theta_j, float* acc_j, float* rel_theta, float* rel_acc,
+                             uint32_t* n_unique_out);
+
 int orc_num_threads(void);
 void orc_set_num_threads(int n);  /* OpenMP team size of later calls (bench: 1-thread leg) */
 

@@ -82,6 +82,16 @@ def lib():
         L.orc_aggregate.argtypes = [u32p, C.c_uint64, u32p, C.c_uint32, f64p]
         L.orc_preprocess.argtypes = [u32p, C.c_uint64, C.c_uint32, C.c_uint64, C.c_float, C.c_float, u32p, u64p, u32p,
                                      u32p, u64p, u32p, u32p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32)]
+        u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+        L.orc_graph_generate.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_float,
+                                         C.c_float, u32p, u8p]
+        L.orc_graph_bucket.restype = C.c_uint64
+        L.orc_graph_bucket.argtypes = [C.c_uint64, C.c_uint32, u32p, C.c_void_p, C.c_uint8, C.c_uint64, u32p, u64p]
+        L.orc_train_batch_parts.restype = C.c_double
+        L.orc_train_batch_parts.argtypes = [C.POINTER(OrcModel), C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p,
+                                            C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, C.c_void_p,
+                                            C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                            C.c_void_p, C.POINTER(C.c_uint32)]
         L.orc_num_threads.restype = C.c_int
         L.orc_set_num_threads.argtypes = [C.c_int]
         _ORACLE = L
@@ -251,3 +261,44 @@ def preprocess(raw, p, seed, train_frac=0.9, valid_frac=0.05):
     a, b, c = (int(x) for x in counts)
     return {"train": train[:a], "valid": valid[:b], "test": test[:c], "offsets": off, "num_nodes": V.value,
             "num_relations": R.value, "node_tokens": ntok[:V.value], "rel_tokens": rtok[:R.value]}
+
+
+def graph_generate(V, R, n, seed, train_frac=0.9, valid_frac=0.05, first=0):
+    """The benchmark graph generator restated on the CPU (orc_graph_generate): (edges (n,3) u32, split (n,) u8)."""
+    edges = np.zeros((n, 3), np.uint32)
+    split = np.zeros(n, np.uint8)
+    lib().orc_graph_generate(V, R, first, n, seed, C.c_float(train_frac), C.c_float(valid_frac),
+                             edges.reshape(-1), split)
+    return edges, split
+
+
+def graph_bucket(V, p, edges, split=None, which=0):
+    """bucket_edges of the edges whose split byte == which (split None: all):
+    (bucketed (m,3) u32, offsets (p*p+1,) u64)."""
+    edges = np.ascontiguousarray(edges, np.uint32).reshape(-1, 3)
+    n = edges.shape[0]
+    if split is not None:
+        split = np.ascontiguousarray(split, np.uint8)
+        m = int(np.count_nonzero(split == which))
+    else:
+        m = n
+    out = np.zeros((max(m, 1), 3), np.uint32)
+    off = np.zeros(p * p + 1, np.uint64)
+    lib().orc_graph_bucket(V, p, edges.reshape(-1), split.ctypes.data if split is not None else None, which, n,
+                           out.reshape(-1), off)
+    return out[:m], off
+
+
+def train_batch_parts(m: OrcModel, epoch, bucket_step, batch_in_bucket, bucket_edges, batch_begin, nb, part_i, part_j,
+                      rel_theta, rel_acc):
+    """The CPU trainer's step on partitions (orc_train_batch_parts): part_* = (first_row, theta, acc) with
+    theta/acc (rows, dim) f32 arrays updated in place. Returns (loss, unique node rows)."""
+    be = np.ascontiguousarray(bucket_edges, np.uint32)
+    fi, ti, ai = part_i
+    fj, tj, aj = part_j
+    nu = C.c_uint32(0)
+    loss = lib().orc_train_batch_parts(C.byref(m), epoch, bucket_step, batch_in_bucket, be.ctypes.data, be.size // 3,
+                                       batch_begin, nb, fi, ti.shape[0], ti.ctypes.data, ai.ctypes.data, fj,
+                                       tj.shape[0], tj.ctypes.data, aj.ctypes.data, rel_theta.ctypes.data,
+                                       rel_acc.ctypes.data, C.byref(nu))
+    return loss, nu.value

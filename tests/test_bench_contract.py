@@ -20,3 +20,8 @@ def test_reference_arm_prints_one_json_line():
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "port"
+    # the reference arm runs the CPU restatement only: no product library in the process
+    assert d["native_libraries"] and all(x.startswith("oracle/") for x in d["native_libraries"]), d["native_libraries"]
+    assert "paper_2101_08358_b200" not in r.stderr
+    # same batch stream as the GPU arm: full batches from its timed window
+    assert d["config"]["batch"] == 10_000 and d["config"]["first_batch"] == 27 // 3 + 3

@@ -314,3 +314,19 @@ def test_eval_monotone_in_negatives():
     r2 = po.eval_ranks("dot", 4, theta, np.zeros((1, 4), np.float32), 50, test, train_edges=test, n_eval_neg=40,
                        alpha_eval=0.0, block=20)
     assert (r2 >= 1).all() and r2.mean() >= r1.mean()
+
+
+def test_graph_generator_restatement_matches_product_generator():
+    """bench.py's CPU arm builds its graph with the oracle's restatement of the benchmark generator
+    (orc_graph_generate / orc_graph_bucket); it must give the product generator's graph exactly."""
+    import paper_2101_08358_b200 as eb
+    V, R = 86_054_151, 14_824
+    e1, s1 = po.graph_generate(V, R, 300_000, 210108358, 0.9, 0.05, first=12_345)
+    e2, s2 = eb.generate_graph(V, R, 312_345, 210108358, 0.9, 0.05)
+    assert np.array_equal(e1, e2[12_345:]) and np.array_equal(s1, s2[12_345:])
+    b1, o1 = po.graph_bucket(V, 16, e1, s1, 0)
+    b2, o2 = eb.bucket_edges(e2[12_345:][s2[12_345:] == 0], V, 16)
+    assert np.array_equal(b1, b2) and np.array_equal(o1, o2)
+    e3, _ = po.graph_generate(4_847_571, 1, 50_000, 7)
+    e4, _ = eb.generate_graph(4_847_571, 1, 50_000, 7)
+    assert np.array_equal(e3, e4)
