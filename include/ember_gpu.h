@@ -98,11 +98,28 @@ int ember_ctx_synchronize(ember_ctx* ctx);
 const char* ember_last_error(void);
 int ember_version(void);
 
+/* ---- device memory through the context (for C/C++ callers without a CUDA runtime of their own)
+ * ember_device_alloc: `bytes` of device memory on the context's device, owned by the context (freed
+ * by ember_device_free or ember_ctx_destroy). The copies are ordered on the context stream and
+ * return when done (host memory may be pageable). Pinned host memory (for the partition buffer's
+ * backing store and asynchronous host batches): ember_host_alloc_pinned / ember_host_free_pinned. */
+int ember_device_alloc(ember_ctx* ctx, size_t bytes, void** out);
+int ember_device_free(ember_ctx* ctx, void* dev_ptr);
+int ember_copy_to_device(ember_ctx* ctx, void* dst_dev, const void* src_host, size_t bytes);
+int ember_copy_to_host(ember_ctx* ctx, void* dst_host, const void* src_dev, size_t bytes);
+int ember_host_alloc_pinned(size_t bytes, void** out);
+int ember_host_free_pinned(void* host_ptr);
+
 /* ---- parameter storage (PartitionBlock; ParameterSlice SPEC.md:125) ------------
  * Caller-owned device memory, borrowed: theta and acc are [rows x dim] f32 row-major for the
  * partition's rows (the on-disk node_part_<k>.bin layout). */
 int ember_tables_bind(ember_ctx* ctx, uint32_t part, float* theta_dev, float* acc_dev);
 int ember_relations_bind(ember_ctx* ctx, float* theta_dev, float* acc_dev);
+/* Context-owned tables: allocates theta and acc of partition `part` (EMBER_RELATIONS: the relation
+ * table) on the device and binds them; ember_tables_get returns the bound pointers and row count. */
+#define EMBER_RELATIONS 0xffffffffu
+int ember_tables_allocate(ember_ctx* ctx, uint32_t part);
+int ember_tables_get(ember_ctx* ctx, uint32_t part, float** theta_dev, float** acc_dev, uint64_t* rows);
 /* init_embeddings for one bound partition / the relation table:
  * global row g <- Rng(mix_seed(seed, g)).uniform(-1/sqrt(d), 1/sqrt(d)) x d; acc <- 0.
  * Relations use seed ^ 0x52454c (row = relation id). */

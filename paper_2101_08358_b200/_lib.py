@@ -99,6 +99,14 @@ def _declare(L):
         "ember_relations_external": (C.c_int, [vp, vp]),
         "ember_relations_apply_dense": (C.c_int, [vp, vp]),
         "ember_overflow_rows": (C.c_int, [vp, C.POINTER(u64)]),
+        "ember_device_alloc": (C.c_int, [vp, C.c_size_t, C.POINTER(vp)]),
+        "ember_device_free": (C.c_int, [vp, vp]),
+        "ember_copy_to_device": (C.c_int, [vp, vp, vp, C.c_size_t]),
+        "ember_copy_to_host": (C.c_int, [vp, vp, vp, C.c_size_t]),
+        "ember_host_alloc_pinned": (C.c_int, [C.c_size_t, C.POINTER(vp)]),
+        "ember_host_free_pinned": (C.c_int, [vp]),
+        "ember_tables_allocate": (C.c_int, [vp, u32]),
+        "ember_tables_get": (C.c_int, [vp, u32, C.POINTER(vp), C.POINTER(vp), C.POINTER(u64)]),
         "ember_comm_init": (C.c_int, [vp, vp, i32, i32]),
         "ember_comm_barrier": (C.c_int, [vp]),
         "ember_partition_copy": (C.c_int, [vp, vp, vp, i32, vp, vp, i32, u64]),

@@ -4,6 +4,7 @@
 // (ConfigError -> EMBER_EUSER, anything else -> EMBER_EINTERNAL) with a thread-local message.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <new>
@@ -198,6 +199,97 @@ int ember_relations_bind(ember_ctx* ctx, float* theta, float* acc) {
         need(acc, "acc");
         E.rel_theta = theta;
         E.rel_acc = acc;
+    });
+}
+
+int ember_device_alloc(ember_ctx* ctx, size_t bytes, void** out) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        need(out, "out");
+        *out = nullptr;
+        void* p = nullptr;
+        EMBER_CUDA(cudaMalloc(&p, bytes ? bytes : 16));
+        E.owned.push_back(p);
+        *out = p;
+    });
+}
+
+int ember_device_free(ember_ctx* ctx, void* p) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        if (!p) return;
+        auto it = std::find(E.owned.begin(), E.owned.end(), p);
+        if (it == E.owned.end()) throw ConfigError("pointer was not allocated by this context");
+        EMBER_CUDA(cudaStreamSynchronize(E.stream));  // (work on the context stream may still read it)
+        EMBER_CUDA(cudaFree(p));
+        E.owned.erase(it);
+    });
+}
+
+int ember_copy_to_device(ember_ctx* ctx, void* dst_dev, const void* src_host, size_t bytes) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        if (!bytes) return;
+        need(dst_dev, "dst_dev");
+        need(src_host, "src_host");
+        EMBER_CUDA(cudaMemcpyAsync(dst_dev, src_host, bytes, cudaMemcpyHostToDevice, E.stream));
+        EMBER_CUDA(cudaStreamSynchronize(E.stream));
+    });
+}
+
+int ember_copy_to_host(ember_ctx* ctx, void* dst_host, const void* src_dev, size_t bytes) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        if (!bytes) return;
+        need(dst_host, "dst_host");
+        need(src_dev, "src_dev");
+        EMBER_CUDA(cudaMemcpyAsync(dst_host, src_dev, bytes, cudaMemcpyDeviceToHost, E.stream));
+        EMBER_CUDA(cudaStreamSynchronize(E.stream));
+    });
+}
+
+int ember_host_alloc_pinned(size_t bytes, void** out) {
+    return guarded([&] {
+        need(out, "out");
+        *out = nullptr;
+        EMBER_CUDA(cudaHostAlloc(out, bytes ? bytes : 16, cudaHostAllocPortable));
+    });
+}
+
+int ember_host_free_pinned(void* p) {
+    return guarded([&] {
+        if (p) EMBER_CUDA(cudaFreeHost(p));
+    });
+}
+
+int ember_tables_allocate(ember_ctx* ctx, uint32_t part) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        const bool rel = part == EMBER_RELATIONS;
+        if (!rel && part >= E.parts.size()) throw ConfigError("partition id out of range");
+        if (rel && E.m.kind == EMBER_DOT) throw ConfigError("Dot models have no relation table");
+        const uint64_t rows = rel ? E.g.num_relations : E.parts[part].rows;
+        float* p = nullptr;
+        EMBER_CUDA(cudaMalloc(&p, 2 * rows * E.dim * sizeof(float)));
+        E.owned.push_back(p);
+        if (rel) {
+            E.rel_theta = p;
+            E.rel_acc = p + rows * E.dim;
+        } else {
+            E.parts[part].theta = p;
+            E.parts[part].acc = p + rows * E.dim;
+        }
+    });
+}
+
+int ember_tables_get(ember_ctx* ctx, uint32_t part, float** theta_dev, float** acc_dev, uint64_t* rows) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        const bool rel = part == EMBER_RELATIONS;
+        if (!rel && part >= E.parts.size()) throw ConfigError("partition id out of range");
+        if (theta_dev) *theta_dev = rel ? E.rel_theta : E.parts[part].theta;
+        if (acc_dev) *acc_dev = rel ? E.rel_acc : E.parts[part].acc;
+        if (rows) *rows = rel ? E.g.num_relations : E.parts[part].rows;
     });
 }
 

@@ -232,6 +232,7 @@ Engine::~Engine() {
                     s.rank, s.ukeys, s.counts, s.offsets, s.nruns, s.longs, s.long_owner, s.uniq, s.cub_tmp};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    for (void* p : owned) cudaFree(p);
     cudaGetLastError();
     if (nccl_comm) {
         try {

@@ -135,6 +135,7 @@ struct Engine {
     uint32_t cap_rows = 0;  // 3 * cap_b + n_neg gradient slots
     uint32_t dsplit = 16;   // split-K factor for dN in the SIMT engine
     std::vector<PartView> parts;
+    std::vector<void*> owned;  // device memory allocated through the context (ember_device_alloc, tables)
     float* rel_theta = nullptr;
     float* rel_acc = nullptr;
     Scratch s;

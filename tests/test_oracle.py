@@ -330,3 +330,25 @@ def test_graph_generator_restatement_matches_product_generator():
     e3, _ = po.graph_generate(4_847_571, 1, 50_000, 7)
     e4, _ = eb.generate_graph(4_847_571, 1, 50_000, 7)
     assert np.array_equal(e3, e4)
+
+
+@pytest.mark.parametrize("kind,chunks", [("dot", 1), ("distmult", 2), ("complex", 1), ("complex", 3)])
+def test_float64_yardstick_matches_oracle(kind, chunks):
+    """oracle/f64.py (the float64 restatement the full-size GPU parity test measures element-wise
+    errors against) agrees with the C oracle on the same inputs."""
+    from oracle import f64
+    rng = np.random.default_rng(1)
+    V, R, d, nb, nt = 400, 7, 24, 90, 16
+    th = (rng.standard_normal((V, d)) * 0.4).astype(np.float32)
+    rt = (rng.standard_normal((R, d)) * 0.4).astype(np.float32)
+    e = np.stack([rng.integers(0, V, nb), rng.integers(0, R, nb), rng.integers(0, V, nb)], 1).astype(np.uint32)
+    negs = rng.integers(0, V, chunks * 2 * nt).astype(np.uint32)
+    a = po.loss_and_grad(po.model(kind, dim=d, n_t=nt, chunks=chunks), e, negs, th, rt)
+    b = f64.loss_and_grad(kind, e, negs, th, rt, chunks=chunks)
+    assert abs(a["loss"] - b["loss"]) <= 1e-6 * abs(b["loss"])
+    assert np.abs(a["lse"].reshape(2, -1) - b["lse"]).max() <= 1e-5
+    assert (a["node_ids"] == b["node_ids"]).all() and (a["rel_ids"] == b["rel_ids"]).all()
+    st = f64.elementwise(a["node_rows"], b["node_rows"], b["node_mag"])
+    assert st["max_err_over_mag"] <= 1e-6, st
+    if kind != "dot":
+        assert f64.elementwise(a["rel_rows"], b["rel_rows"], b["rel_mag"])["max_err_over_mag"] <= 1e-6
