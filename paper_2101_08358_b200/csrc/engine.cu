@@ -296,6 +296,8 @@ void Engine::sort_slots(uint32_t nb, const KeySpace& ks) {
     EMBER_CUDA(cub::DeviceRadixSort::SortPairs(s.cub_tmp, bytes, s.keys, s.keys_sorted, s.vals, s.vals_sorted, (int)n,
                                                0, (int)ks.bits, side));
     bytes = s.cub_bytes;
+    // (the scan below runs over n entries; the runs past nruns must read as zero, not stale memory)
+    EMBER_CUDA(cudaMemsetAsync(s.counts, 0, (size_t)n * sizeof(uint32_t), side));
     EMBER_CUDA(cub::DeviceRunLengthEncode::Encode(s.cub_tmp, bytes, s.keys_sorted, s.ukeys, s.counts, s.nruns, (int)n,
                                                   side));
     bytes = s.cub_bytes;
