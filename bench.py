@@ -656,7 +656,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="fb86m", choices=sorted(CONFIGS))
-    ap.add_argument("--engine", default=os.environ.get("EMBER_ENGINE", "tc"), choices=["simt", "tc", "blas"])
+    ap.add_argument("--engine", default=os.environ.get("EMBER_ENGINE", "tc"), choices=["simt", "tc"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--cpu-budget", type=float, default=150.0,
                     help="--impl reference: stop timing after this many seconds of CPU work")
@@ -667,6 +667,8 @@ def main():
                     help="use the multi-GPU round-schedule path even at N=1 (a 1-rank NCCL group; for checks)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.engine == "simt":  # the fp32 reference engine (baseline measurements only)
+        os.environ["EMBER_TEST_ENGINES"] = "1"
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

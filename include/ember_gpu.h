@@ -38,13 +38,13 @@ extern "C" {
 
 /* Contraction engine for the shared-negative scores.
  * TC_BF16X3: tcgen05 tensor cores, operands split hi+lo in bf16 (3 products, fp32 accumulate),
- *            ~2^-17 relative per product — inside the 1e-4 parity tolerance.
- * SIMT_FP32: CUDA-core fp32 tiles (correctness baseline). */
+ *            ~2^-16 relative per product — inside the 1e-4 parity tolerance. Any d (d <= 128 with
+ *            one negative set per batch: the fused kernels of tc_score.cu; d > 128 or chunked
+ *            negatives: the three-pass kernels of tc_wide.cu). The product engine.
+ * SIMT_FP32: CUDA-core fp32 tiles, the tests' reference engine: rejected unless the environment
+ *            sets EMBER_TEST_ENGINES=1. */
 #define EMBER_ENGINE_SIMT_FP32 0
 #define EMBER_ENGINE_TC_BF16X3 1
-/* the same bf16x3 arithmetic through cuBLAS bf16 GEMMs on materialised scores (any d; for d > 128,
- * beyond the hand-written kernels' TMEM layout, e.g. config C5 d = 800); num_chunks must be 1 */
-#define EMBER_ENGINE_TC_BLAS 2
 
 /* OrderingKind (reference ordering.h:14) */
 #define EMBER_ORDER_ELIMINATION 0

@@ -147,7 +147,7 @@ class Hyper:
     alpha: float = 0.5
     num_chunks: int = 1
     neg_seed: int = 1
-    engine: str = "simt"
+    engine: str = "tc"  # "simt": the tests' fp32 reference engine (needs EMBER_TEST_ENGINES=1)
 
     def desc(self) -> ModelDesc:
         return ModelDesc(KIND[self.kind], self.dim, self.lr, self.eps, self.batch_size, self.num_negatives,

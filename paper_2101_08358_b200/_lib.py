@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("EMBER_LIB") or os.path.join(HERE, "libember_b200.so")
 
 EMBER_OK, EMBER_EUSER, EMBER_EINTERNAL = 0, 1, 2
 KIND = {"dot": 0, "distmult": 1, "complex": 2}
-ENGINE = {"simt": 0, "tc": 1, "blas": 2}
+ENGINE = {"simt": 0, "tc": 1}
 ORDERING = {"elimination": 0, "beta": 0, "hilbert": 1, "hilbert_symmetric": 2, "random": 3}
 
 

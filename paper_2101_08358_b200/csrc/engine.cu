@@ -78,6 +78,11 @@ __global__ void k_adagrad_dense(float* th, float* ac, const float* g, uint64_t n
     th[i] = __fsub_rn(th[i], __fdiv_rn(__fmul_rn(lr, gi), __fadd_rn(__fsqrt_rn(a), eps)));
 }
 
+bool getenv_flag(const char* name) {
+    const char* v = getenv(name);
+    return v && v[0] == '1';
+}
+
 // A/B switch: EMBER_NO_DIRECT=1 sends every gradient row through the segmented reduction.
 bool getenv_direct() {
     const char* v = getenv("EMBER_NO_DIRECT");
@@ -105,9 +110,9 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     if (g.num_partitions == 0 || g.num_nodes < g.num_partitions) throw ConfigError("need 1 <= p <= |V|");
     if (g.num_nodes > 0xffffffffULL) throw ConfigError("node ids are u32");
     if (m.kind != EMBER_DOT && g.num_relations == 0) throw ConfigError("DistMult/ComplEx need relations");
-    if (m.engine != EMBER_ENGINE_SIMT_FP32 && m.engine != EMBER_ENGINE_TC_BF16X3 && m.engine != EMBER_ENGINE_TC_BLAS)
-        throw ConfigError("unknown engine");
-    if (m.engine == EMBER_ENGINE_TC_BLAS && m.num_chunks > 1) throw ConfigError("blas engine: num_chunks must be 1");
+    if (m.engine != EMBER_ENGINE_TC_BF16X3 && m.engine != EMBER_ENGINE_SIMT_FP32) throw ConfigError("unknown engine");
+    if (m.engine == EMBER_ENGINE_SIMT_FP32 && !getenv_flag("EMBER_TEST_ENGINES"))
+        throw ConfigError("the SIMT fp32 engine is the tests' reference engine (set EMBER_TEST_ENGINES=1)");
     dim = m.dim;
     nt = m.num_negatives;
     chunks = m.num_chunks ? m.num_chunks : 1;
@@ -150,7 +155,8 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
         parts[k].rows = partition_size(g.num_nodes, g.num_partitions, k);
     }
     if (tc_engine() && !tc_engine_supported(*this))
-        throw ConfigError("tensor-core engine needs a CC 10.0 device (B200), dim <= 128 and num_chunks == 1");
+        throw ConfigError("tensor-core engine needs a CC 10.0 device (B200) and num_chunks == 1");
+    const bool wide_path = tc_engine() && (dim > 128 || chunks > 1);
 
     const uint64_t b = cap_b, d = dim;
     s.negs = dalloc<uint32_t>(n_neg);
@@ -192,14 +198,7 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
         s.S = dalloc<float>(2 * b * (uint64_t)(nt ? nt : 1));
         s.dN_part = dalloc<float>((uint64_t)dsplit * n_neg * d);
     }
-    if (blas_engine()) {
-        s.S = dalloc<float>(2 * b * (uint64_t)(nt ? nt : 1));
-        s.dN_part = dalloc<float>((uint64_t)16 * n_neg * d);  // up to 16 K-chunk partials of dN
-        s.Ahl = dalloc<uint16_t>((uint64_t)2 * 2 * 3 * b * d);  // K-concatenated + K-stacked bf16x3 operands
-        s.Nhl = dalloc<uint16_t>((uint64_t)2 * 2 * 3 * (nt ? nt : 1) * d);
-        s.Phl = dalloc<uint16_t>((uint64_t)2 * 2 * 3 * b * (nt ? nt : 1));
-    }
-    if (tc_engine()) {  // packed operand geometry: dim padded to 16, rows to 128- and 96-row tiles
+    if (tc_engine() && !wide_path) {  // packed operand geometry: dim padded to 16, rows to 128- and 96-row tiles
         KP = (int)((dim + 15) / 16 * 16);
         CB = KP / 8;
         b_cap = pad_rows(cap_b);
@@ -215,8 +214,10 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     EMBER_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t3, s.counts, s.offsets, (int)cap_rows, side));
     s.cub_bytes = std::max(t1, std::max(t2, t3));
     s.cub_tmp = dalloc<uint8_t>(s.cub_bytes);
-    if (tc_engine()) tc_setup(*this);
-    if (blas_engine()) blas_setup(*this);
+    if (tc_engine()) {
+        if (wide_path) wide_setup(*this);
+        else tc_setup(*this);
+    }
     EMBER_CUDA(cudaStreamSynchronize(stream));
 }
 
@@ -225,9 +226,9 @@ Engine::~Engine() {
     if (stream) cudaStreamSynchronize(stream);
     if (side && side != stream) cudaStreamSynchronize(side);
     tc_release(*this);
-    blas_release(*this);
+    wide_release(*this);
     void* ptrs[] = {s.batch, s.A,         s.N,      s.Apk,       s.Npk,     s.fpos,       s.lse,    s.g0,
-                    s.S,     s.dA,        s.dN_part, s.grows,    s.loss,    s.loss_part,  s.loss_done,  s.bad_batch, s.Ahl, s.Nhl, s.Phl,
+                    s.S,     s.dA,        s.dN_part, s.grows,    s.loss,    s.loss_part,  s.loss_done,  s.bad_batch,
                     s.nunique, s.long_partial, s.rel_dense, s.negs, s.keys, s.keys_sorted, s.vals, s.vals_sorted,
                     s.rank, s.ukeys, s.counts, s.offsets, s.nruns, s.longs, s.long_owner, s.uniq, s.cub_tmp};
     for (void* p : ptrs)
@@ -323,13 +324,14 @@ void Engine::forward_backward(const uint32_t* edges, uint32_t nb, uint32_t i, ui
         sort_keys(edges, nb, i, j, negs);
     }
     mark(PHASE_GATHER);
-    launch_gather_adjust(*this, edges, nb, pi, pj, tc_engine(), negs, blas_engine());
-    launch_gather_negatives(*this, negs, pi, pj, tc_engine());
+    const bool fused = tc_engine() && !wide;  // d <= 128: the gather packs the bf16 operands itself
+    launch_gather_adjust(*this, edges, nb, pi, pj, fused, negs);
+    launch_gather_negatives(*this, negs, pi, pj, fused);
     mark(PHASE_CONTRACT);
-    if (tc_engine())
+    if (wide)
+        launch_contract_wide(*this, nb);  // joins the sort before scattering dN rows
+    else if (tc_engine())
         launch_contract_tc(*this, nb);  // joins the sort before scattering dN rows
-    else if (blas_engine())
-        launch_contract_blas(*this, nb);
     else
         launch_contract_simt(*this, nb);
     mark(PHASE_CHAIN);

@@ -81,9 +81,6 @@ struct Scratch {
     float* lse = nullptr;
     float* g0 = nullptr;
     float* S = nullptr;       // SIMT engine: [2][b][nt] scores -> P/b
-    void* Ahl = nullptr;      // blas engine: bf16x3 operands of A, N, P: K-concatenated then K-stacked (gemm_simt.cu)
-    void* Nhl = nullptr;
-    void* Phl = nullptr;
     float* dA = nullptr;
     float* dN_part = nullptr; // SIMT engine split-K partials
     float* grows = nullptr;
@@ -110,7 +107,8 @@ struct Scratch {
     float* rel_dense = nullptr;  // [R][dim] relation gradient summed over ranks (world > 1)
 };
 
-struct TcState;  // tensor-core engine state (tc_score.cu)
+struct TcState;    // tensor-core engine state (tc_score.cu, d <= 128)
+struct WideState;  // tensor-core engine state for d > 128 (tc_wide.cu)
 
 struct Engine {
     int device = 0;
@@ -140,8 +138,7 @@ struct Engine {
     float* rel_acc = nullptr;
     Scratch s;
     TcState* tc = nullptr;
-    void* blas = nullptr;  // cublasHandle_t of the blas engine
-    bool blas_engine() const { return m.engine == EMBER_ENGINE_TC_BLAS; }
+    WideState* wide = nullptr;  // d > 128: the three-pass tcgen05 GEMM path (tc_wide.cu)
     // packed-operand geometry (tensor-core engine)
     int KP = 0, CB = 0, b_cap = 0, n_pad = 0;
     int sm_count = 148;
@@ -245,7 +242,7 @@ void launch_sample_on(const Engine& E, cudaStream_t st, uint32_t* out, uint64_t 
                       uint64_t bucket_n, const PartView& src, const PartView& dst);
 // packed: write the tensor-core engine's bf16 hi|lo operands (Apk/Npk), else fp32 A / N.
 void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj,
-                          bool packed, const uint32_t* negs, bool split_bf16 = false);
+                          bool packed, const uint32_t* negs);
 void launch_gather_negatives(const Engine& E, const uint32_t* negs, const PartView& pi, const PartView& pj, bool packed);
 void launch_keys(const Engine& E, const uint32_t* edges, uint32_t nb, const uint32_t* negs, const KeySpace& ks);
 // the training step's sample_negatives + gradient-slot keys, one kernel on the step stream
@@ -253,9 +250,6 @@ void launch_sample_keys(const Engine& E, const uint32_t* edges, uint32_t nb, uin
                         uint64_t bucket_n, const PartView& src, const PartView& dst, const KeySpace& ks);
 void launch_rank(const Engine& E, uint32_t n);
 void launch_contract_simt(Engine& E, uint32_t nb);
-void launch_contract_blas(Engine& E, uint32_t nb);
-void blas_setup(Engine& E);
-void blas_release(Engine& E);
 void launch_contract_tc(Engine& E, uint32_t nb);
 void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj);
 void launch_loss(const Engine& E, uint32_t nb, float* loss_out);
@@ -276,5 +270,10 @@ bool tc_engine_supported(const Engine& E);
 void tc_setup(Engine& E);
 void tc_release(Engine& E);
 uint64_t tc_overflow_rows(Engine& E);
+bool wide_supported(const Engine& E);
+void wide_setup(Engine& E);
+void wide_release(Engine& E);
+uint64_t wide_overflow_rows(Engine& E);
+void launch_contract_wide(Engine& E, uint32_t nb);
 
 }  // namespace ember

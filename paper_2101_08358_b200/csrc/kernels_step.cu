@@ -214,43 +214,11 @@ __global__ void __launch_bounds__(32 * GP_WARPS) k_gather_pack(const uint32_t* _
     }
 }
 
-// Two coordinates (c, c+1) of adjusted row e of side `side` -> the blas engine's bf16x3 operand
-// layouts of A: K-concatenated [side][nb][hi | hi | lo] and K-stacked [side][hi; hi; lo][nb] rows.
-__device__ __forceinline__ void put_split_pair(__nv_bfloat16* kd, __nv_bfloat16* st, uint32_t nb, uint32_t d,
-                                               uint32_t side, uint32_t e, uint32_t c, float x0, float x1) {
-    const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
-    const float2 hf = __bfloat1622float2(h);
-    const __nv_bfloat162 l = __floats2bfloat162_rn(x0 - hf.x, x1 - hf.y);
-    const uint64_t per = (uint64_t)nb * d;
-    __nv_bfloat16* k = kd + side * 3 * per + (uint64_t)e * 3 * d + c;
-    __nv_bfloat16* s = st + side * 3 * per + (uint64_t)e * d + c;
-    *reinterpret_cast<__nv_bfloat162*>(k) = h;
-    *reinterpret_cast<__nv_bfloat162*>(k + d) = h;
-    *reinterpret_cast<__nv_bfloat162*>(k + 2 * d) = l;
-    *reinterpret_cast<__nv_bfloat162*>(s) = h;
-    *reinterpret_cast<__nv_bfloat162*>(s + per) = h;
-    *reinterpret_cast<__nv_bfloat162*>(s + 2 * per) = l;
-}
-
-__device__ __forceinline__ void put_split_quad(__nv_bfloat16* kd, __nv_bfloat16* st, uint32_t nb, uint32_t d,
-                                               uint32_t side, uint32_t e, int kind, uint32_t h, uint32_t q,
-                                               const Quad& x) {
-    if (kind == EMBER_COMPLEX) {
-        put_split_pair(kd, st, nb, d, side, e, 2 * q, x.v[0], x.v[1]);
-        put_split_pair(kd, st, nb, d, side, e, h + 2 * q, x.v[2], x.v[3]);
-    } else {
-        put_split_pair(kd, st, nb, d, side, e, 4 * q, x.v[0], x.v[1]);
-        put_split_pair(kd, st, nb, d, side, e, 4 * q + 2, x.v[2], x.v[3]);
-    }
-}
-
-// fp32 gather (SIMT engine): one warp per edge, A[0][e] = ad, A[1][e] = as, fpos[e] = ad . t.
-// SPLIT (blas engine): the adjusted rows go straight into the bf16x3 operand layouts instead.
-template <bool SPLIT>
+// fp32 gather (SIMT engine, and the wide tensor-core path that packs it afterwards, tc_wide.cu):
+// one warp per edge, A[0][e] = ad, A[1][e] = as, fpos[e] = ad . t.
 __global__ void k_gather_adjust(const uint32_t* __restrict__ edges, uint32_t nb, PartView pi, PartView pj,
                                 const float* __restrict__ rel, int kind, uint32_t d, float* __restrict__ A,
-                                float* __restrict__ fpos, __nv_bfloat16* __restrict__ akd,
-                                __nv_bfloat16* __restrict__ ast) {
+                                float* __restrict__ fpos) {
     const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t e = blockIdx.x * (blockDim.x >> 5) + wib;
     if (e >= nb) return;
@@ -267,13 +235,8 @@ __global__ void k_gather_adjust(const uint32_t* __restrict__ edges, uint32_t nb,
         adjust_quad(kind, S, R, T, ad, as);
 #pragma unroll
         for (int i = 0; i < 4; ++i) part += ad.v[i] * T.v[i];
-        if (SPLIT) {
-            put_split_quad(akd, ast, nb, d, 0, e, kind, h, q, ad);
-            put_split_quad(akd, ast, nb, d, 1, e, kind, h, q, as);
-        } else {
-            store_quad(A + (uint64_t)e * d, kind, h, q, ad);
-            store_quad(A + ((uint64_t)nb + e) * d, kind, h, q, as);
-        }
+        store_quad(A + (uint64_t)e * d, kind, h, q, ad);
+        store_quad(A + ((uint64_t)nb + e) * d, kind, h, q, as);
     }
     for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
     if (lane == 0) fpos[e] = part;
@@ -1269,7 +1232,7 @@ void launch_sample_on(const Engine& E, cudaStream_t st, uint32_t* out, uint64_t 
 }
 
 void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj,
-                          bool packed, const uint32_t* negs, bool split_bf16) {
+                          bool packed, const uint32_t* negs) {
     if (packed) {
         const uint32_t rows_pad = (uint32_t)Engine::pad_rows(nb);  // a multiple of GP_ROWS
         const size_t sm = (size_t)4 * E.CB * GP_ROWS * 16 + (size_t)GP_WARPS * 2 * E.KP * sizeof(float);
@@ -1280,15 +1243,8 @@ void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, c
                    negs, E.nt, (uint32_t)E.n_pad, E.s.Npk);
     } else {
         const uint32_t warps = 8;
-        if (split_bf16) {  // blas engine: A's K-concatenated then K-stacked bf16x3 layouts (gemm_simt.cu)
-            __nv_bfloat16* akd = reinterpret_cast<__nv_bfloat16*>(E.s.Ahl);
-            __nv_bfloat16* ast = akd + (size_t)2 * 3 * E.cap_b * E.dim;
-            k_gather_adjust<true><<<(nb + warps - 1) / warps, warps * 32, 0, E.stream>>>(
-                edges, nb, pi, pj, E.rel_theta, E.m.kind, E.dim, E.s.A, E.s.fpos, akd, ast);
-        } else {
-            k_gather_adjust<false><<<(nb + warps - 1) / warps, warps * 32, 0, E.stream>>>(
-                edges, nb, pi, pj, E.rel_theta, E.m.kind, E.dim, E.s.A, E.s.fpos, nullptr, nullptr);
-        }
+        k_gather_adjust<<<(nb + warps - 1) / warps, warps * 32, 0, E.stream>>>(edges, nb, pi, pj, E.rel_theta,
+                                                                                E.m.kind, E.dim, E.s.A, E.s.fpos);
     }
     EMBER_LAUNCHED(E);
 }

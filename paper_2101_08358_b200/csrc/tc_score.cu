@@ -608,9 +608,10 @@ __global__ void k_tc_fixup(TcArgs g, const uint16_t* __restrict__ Apk, const uin
 // dN rows summed over chunks in fixed order; row (side, n) is gradient slot 2nb + side*nt + n and
 // goes to its sorted position grows[rank[slot]]. Thread per (side, column block, negative): the
 // column-blocked partials [chunk][side][d/4][n_pad] float4 are read coalesced along n.
+// nsides: 2 (one shared negative set per side), or 2 x num_chunks ([chunk][side] sets, tc_wide.cu).
 __global__ void k_dn_reduce(const float4* __restrict__ part, int chunks, int nt, int n_pad, int d,
                             const uint32_t* __restrict__ rank, uint32_t slot0, float* __restrict__ out,
-                            uint32_t* flags, unsigned long long* flags_total) {
+                            uint32_t* flags, unsigned long long* flags_total, int nsides) {
     griddep_wait();
     if (blockIdx.x == 0 && threadIdx.x == 0) {  // overflow list consumed (k_tc_fixup): count, reset
         flags_total[0] += flags[0];
@@ -618,12 +619,12 @@ __global__ void k_dn_reduce(const float4* __restrict__ part, int chunks, int nt,
     }
     const int d4 = d / 4;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= (int64_t)2 * d4 * nt) return;
+    if (t >= (int64_t)nsides * d4 * nt) return;
     const int n = (int)(t % nt);
     const int c4 = (int)((t / nt) % d4);
     const int side = (int)(t / ((int64_t)nt * d4));
     const float4* p = part + ((size_t)side * d4 + c4) * n_pad + n;
-    const size_t cstride = (size_t)2 * d4 * n_pad;
+    const size_t cstride = (size_t)nsides * d4 * n_pad;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     int c = 0;
     for (; c + 4 <= chunks; c += 4) {  // 4 loads in flight, added in chunk order
@@ -678,6 +679,32 @@ CUtensorMap make_map(uint16_t* base, int cap, int CB, int box_rows) {
 
 }  // namespace
 
+// 4-D view of any packed operand [2 sides][nblocks2][cap rows][8 bf16] with a box of box_rows rows
+// (a multiple of 32) x box_blocks column blocks: lands in smem as [box_blocks][box_rows][16 B], the
+// canonical K-major tile (columns along K) or MN-major tile (rows along K). Used by tc_wide.cu.
+CUtensorMap make_packed_map(uint16_t* base, int cap, int nblocks2, int box_rows, int box_blocks) {
+    CUtensorMap m;
+    const cuuint64_t dims[4] = {256, (cuuint64_t)(cap / 32), (cuuint64_t)nblocks2, 2};
+    const cuuint64_t strides[3] = {512, (cuuint64_t)cap * 16, (cuuint64_t)cap * 16 * nblocks2};
+    const cuuint32_t box[4] = {256, (cuuint32_t)(box_rows / 32), (cuuint32_t)box_blocks, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, estr,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw EmberError("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return m;
+}
+
+// The fixed-order dN reduction of k_dn_reduce for the wide engine's partials (tc_wide.cu).
+void dn_reduce_launch(Engine& E, const float* part, int chunks, int nt, int n_pad, int d, uint32_t slot0,
+                      uint32_t* flags, unsigned long long* flags_total, int nsides) {
+    const int64_t r = (int64_t)nsides * nt * (d / 4);
+    launch_pdl(k_dn_reduce, dim3((unsigned)((r + 255) / 256)), dim3(256), 0, E.stream,
+               reinterpret_cast<const float4*>(part), chunks, nt, n_pad, d, (const uint32_t*)E.s.rank, slot0, E.s.grows,
+               flags, flags_total, nsides);
+    EMBER_LAUNCHED(E);
+}
+
 // Engine-side state of the tensor-core engine (allocated once per context).
 struct TcState {
     int KP = 0, CB = 0, b_cap = 0, n_pad = 0, chunks2 = 1, nstage = 4, nsp = 2;
@@ -697,7 +724,7 @@ bool tc_engine_supported(const Engine& E) {
     int major = 0, minor = 0;
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, E.device);
     cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, E.device);
-    return major == 10 && minor == 0 && E.dim <= (uint32_t)KPMAX && E.chunks == 1 && E.nt >= 1;
+    return major == 10 && minor == 0 && E.nt >= 1 && ((E.dim <= (uint32_t)KPMAX && E.chunks == 1) || wide_supported(E));
 }
 
 void tc_setup(Engine& E) {
@@ -735,6 +762,7 @@ void tc_setup(Engine& E) {
 }
 
 uint64_t tc_overflow_rows(Engine& E) {
+    if (E.wide) return wide_overflow_rows(E);
     if (!E.tc) return 0;
     unsigned long long v = 0;
     EMBER_CUDA(cudaStreamSynchronize(E.stream));
@@ -831,7 +859,7 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
     E.join_sorted();
     launch_pdl(k_dn_reduce, dim3((unsigned)((r + 255) / 256)), dim3(256), 0, E.stream,
                reinterpret_cast<const float4*>(t.dN_part), a.chunks2, nt, t.n_pad, d, (const uint32_t*)s.rank, 2 * nb,
-               s.grows, t.flags, t.flags_total);
+               s.grows, t.flags, t.flags_total, 2);
     EMBER_LAUNCHED(E);
 }
 

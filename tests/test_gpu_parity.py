@@ -55,8 +55,6 @@ def test_negative_ids_bit_exact(graph, chunks, alpha):
 @pytest.mark.parametrize("kind,chunks,nb", [("dot", 1, 512), ("distmult", 1, 512), ("complex", 1, 512),
                                             ("complex", 4, 509), ("distmult", 2, 77)])
 def test_loss_and_grad_match_oracle(graph, engine, kind, chunks, nb):
-    if engine == "tc" and chunks > 1:
-        pytest.skip("tensor-core engine shares one negative set per batch (num_chunks == 1)")
     edges, off, _ = graph
     tr = make_trainer(kind, dim=32, nt=64, chunks=chunks, p=2, engine=engine)
     th, _, rt, _ = host_tables(tr)
@@ -77,14 +75,21 @@ def test_loss_and_grad_match_oracle(graph, engine, kind, chunks, nb):
         assert row_rel_err(got["rel_rows"], exp["rel_rows"]) <= TOL
 
 
-@pytest.mark.parametrize("engine", ["simt", "blas"])
-@pytest.mark.parametrize("kind,dim", [("complex", 800), ("distmult", 256), ("dot", 132), ("complex", 100)])
-def test_loss_and_grad_large_dim(graph, engine, kind, dim):
-    """SURVEY config C5's d = 800 (and other d > 128, beyond the hand-written tensor-core kernels'
-    TMEM layout) on the SIMT engine and on the blas engine (cuBLAS bf16 GEMMs with the bf16x3
-    split): scores, losses and gradients within 1e-4 of the oracle."""
+@pytest.mark.parametrize("engine", ["simt", "tc"])
+@pytest.mark.parametrize("kind,dim,chunks,grid,zmax", [("complex", 800, 1, None, None), ("distmult", 256, 1, None, None),
+                                                       ("dot", 132, 1, None, None), ("complex", 800, 3, "4", None),
+                                                       ("complex", 160, 1, "3", "0"), ("distmult", 100, 2, None, None)])
+def test_loss_and_grad_large_dim_and_chunks(graph, monkeypatch, engine, kind, dim, chunks, grid, zmax):
+    """SURVEY config C5's d = 800 (and other d > 128) and chunked negative sets on the
+    tensor-core engine's three-pass kernels (tc_wide.cu) and on the SIMT reference: scores, losses and
+    gradients within 1e-4 of the oracle, including a capped grid (several items per CTA) and every row
+    forced through the exact overflow recompute (EMBER_TC_ZMAX=0)."""
+    if grid is not None:
+        monkeypatch.setenv("EMBER_TC_MAXGRID", grid)
+    if zmax is not None:
+        monkeypatch.setenv("EMBER_TC_ZMAX", zmax)
     edges, off, _ = graph
-    tr = make_trainer(kind, dim=dim, b=256, nt=100, p=2, engine=engine)
+    tr = make_trainer(kind, dim=dim, b=256, nt=100, chunks=chunks, p=2, engine=engine)
     th, _, rt, _ = host_tables(tr)
     bucket = edges[off[1]:off[2]]
     negs = tr.sample_negatives(_dev(bucket), 0, 1, 0, 0, 0)
@@ -97,9 +102,8 @@ def test_loss_and_grad_large_dim(graph, engine, kind, dim):
     assert row_rel_err(got["node_rows"], exp["node_rows"]) <= TOL
     if kind != "dot":
         assert row_rel_err(got["rel_rows"], exp["rel_rows"]) <= TOL
-    if dim > 128:
-        with pytest.raises(eb.ConfigError):  # the hand-written tensor-core kernels stop at d = 128
-            make_trainer(kind, dim=dim, b=256, nt=100, p=2, engine="tc")
+    if zmax == "0" and engine == "tc":
+        assert tr.overflow_rows() == 2 * 200  # every (row, side) took the exact path
 
 
 def test_scores_match_oracle(graph):
@@ -187,13 +191,13 @@ def test_non_finite_loss_is_an_error_naming_the_batch(graph, engine):
     tr.synchronize()  # reported once
 
 
-@pytest.mark.parametrize("engine", ENGINES + ["blas"])
-def test_training_trajectory_matches_oracle(graph, engine):
+@pytest.mark.parametrize("engine,dim,chunks", [("simt", 32, 1), ("tc", 32, 1), ("tc", 160, 1), ("tc", 32, 2)])
+def test_training_trajectory_matches_oracle(graph, engine, dim, chunks):
     """A few full steps (sample -> grads -> Adagrad) over two buckets; losses within 1e-4, tables
     close (Adagrad's first step is ~ -lr*sign(g), so elements whose gradient is at rounding level can
     legitimately flip: allow < 0.01% of elements)."""
     edges, off, _ = graph
-    tr = make_trainer("complex", dim=32, b=256, nt=64, p=2, engine=engine)
+    tr = make_trainer("complex", dim=dim, b=256, nt=64, chunks=chunks, p=2, engine=engine)
     th, ac, rt, ra = host_tables(tr)
     m = oracle_model(tr)
     V, p = 3000, 2
@@ -214,7 +218,7 @@ def test_training_trajectory_matches_oracle(graph, engine):
     gth, gac, grt, gra = host_tables(tr)
     for a, b_ in ((gth, th), (grt, rt)):
         bad = np.abs(a - b_) > 1e-3
-        assert bad.mean() < 1e-4, bad.sum()
+        assert bad.sum() <= max(1, 1e-4 * bad.size), bad.sum()  # (the small relation table: one flip at most)
     assert rel_err(gac, ac) <= 1e-3 and rel_err(gra, ra) <= 1e-3
 
 
