@@ -107,11 +107,13 @@ void train_epoch_impl(Engine& E, const uint32_t* edges, const uint64_t* offsets,
         nbatch += (offsets[k + 1] - offsets[k] + E.cap_b - 1) / E.cap_b;
     }
     const uint64_t n_edges = offsets[(size_t)p * p] - offsets[0];
+    NvtxRange nvtx("ember::train_epoch");
     float* losses = nullptr;
     if (stats && nbatch) EMBER_CUDA(cudaMallocAsync(&losses, nbatch * sizeof(float), E.stream));
     uint64_t slot = 0;
     for (uint32_t t = 0; t < p * p; ++t) {
         uint32_t i = seq ? seq[2 * t] : 0, j = seq ? seq[2 * t + 1] : 0;
+        NvtxRange nvtx_bucket("ember::bucket");
         acquire(t, &i, &j);
         if (i >= p || j >= p) throw ConfigError("bucket out of range");
         const uint64_t lo = offsets[(size_t)i * p + j], hi = offsets[(size_t)i * p + j + 1];

@@ -418,6 +418,7 @@ void Engine::step(const uint32_t* edges, uint32_t nb, const uint32_t* bucket, ui
                   cudaEvent_t edges_ready) {
     if (nb == 0 || nb > cap_b) throw ConfigError("batch size must be in [1, batch_size]");
     check_bucket(i, j);
+    NvtxRange nvtx("ember::step");
     // Sampling and the gradient-slot keys: one kernel on the step stream (ordered after the caller's
     // work that produced the batch and the bucket). Only the (key, slot) sort forks onto the helper
     // stream, where it overlaps the gathers and the contraction; the step stream joins it before the

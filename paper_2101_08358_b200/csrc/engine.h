@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdint>
@@ -209,6 +210,15 @@ struct Engine {
 };
 
 enum Phase { PHASE_SAMPLE = 0, PHASE_GATHER = 1, PHASE_CONTRACT = 2, PHASE_CHAIN = 3, PHASE_REDUCE = 4, PHASE_END = 5 };
+
+// NVTX range for the scope (host-side enqueue of a step / bucket / epoch; visible in Nsight timelines,
+// near-free without a tool attached).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Programmatic dependent launch (PDL) on the step stream: a kernel's CTAs may be scheduled while
 // the previous kernel drains; every kernel launched this way starts (after its own set-up) with
