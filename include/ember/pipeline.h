@@ -122,7 +122,8 @@ public:
         }
     }
 
-    // theta (and acc) of partition k, or of the relation table (k = EMBER_RELATIONS), on the host.
+    // theta (and acc) of partition k, or of the relation table (k = EMBER_RELATIONS), on the host,
+    // in on-disk coordinate order (the tables and the backing store hold the HBM row layout).
     std::vector<float> download(std::uint32_t k, bool acc = false) {
         const std::uint64_t n = rows(k) * cfg_.dim;
         std::vector<float> out(n);
@@ -130,11 +131,12 @@ public:
             buffer_->flush();
             const float* src = acc ? host_acc_[k] : host_theta_[k];
             std::copy(src, src + n, out.begin());
-            return out;
+        } else {
+            float *t = nullptr, *a = nullptr;
+            gpu::check(ember_tables_get(ctx_->get(), k, &t, &a, nullptr));
+            gpu::check(ember_copy_to_host(ctx_->get(), out.data(), acc ? a : t, n * sizeof(float)));
         }
-        float *t = nullptr, *a = nullptr;
-        gpu::check(ember_tables_get(ctx_->get(), k, &t, &a, nullptr));
-        gpu::check(ember_copy_to_host(ctx_->get(), out.data(), acc ? a : t, n * sizeof(float)));
+        gpu::check(ember_rows_layout_host(static_cast<int>(cfg_.model), cfg_.dim, out.data(), rows(k), 0));
         return out;
     }
 

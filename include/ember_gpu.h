@@ -112,7 +112,15 @@ int ember_host_free_pinned(void* host_ptr);
 
 /* ---- parameter storage (PartitionBlock; ParameterSlice SPEC.md:125) ------------
  * Caller-owned device memory, borrowed: theta and acc are [rows x dim] f32 row-major for the
- * partition's rows (the on-disk node_part_<k>.bin layout). */
+ * partition's rows in the HBM row layout. For Dot/DistMult that is the on-disk node_part_<k>.bin
+ * layout. A ComplEx row ([re | im] halves of h = dim/2 on disk) holds
+ * its halves interleaved by pairs: re k at 4(k/2) + k%2, im k at 4(k/2) + 2 + k%2, so each
+ * aligned 16 bytes are {re 2q, re 2q+1, im 2q, im 2q+1}. ember_rows_layout converts rows in place
+ * (to_hbm = 1: on-disk -> HBM; 0: back) on the context stream, ember_rows_layout_host on the host;
+ * both are no-ops unless the model is ComplEx. The per-op entry points that take or return rows
+ * (ember_gather, ember_adagrad_apply, ember_loss_and_grad) use the on-disk coordinate order. */
+int ember_rows_layout(ember_ctx* ctx, float* rows_dev, uint64_t rows, int to_hbm);
+int ember_rows_layout_host(int kind, uint32_t dim, float* rows, uint64_t n, int to_hbm);
 int ember_tables_bind(ember_ctx* ctx, uint32_t part, float* theta_dev, float* acc_dev);
 int ember_relations_bind(ember_ctx* ctx, float* theta_dev, float* acc_dev);
 /* Context-owned tables: allocates theta and acc of partition `part` (EMBER_RELATIONS: the relation
@@ -297,6 +305,13 @@ int ember_train_epoch_buffered(ember_ctx* ctx, ember_buffer* buf, const uint32_t
  * The global position of a bucket is its bucket_step for the sampler seeds. */
 int ember_make_rounds(uint32_t p, uint32_t world, uint32_t* order, uint32_t* round, uint32_t* rank, uint32_t* holder,
                       uint32_t* n_rounds);
+/* Overlapped round schedule (csrc/host/rounds.cpp make_rounds_overlap): p a power of two >= 4 and
+ * world | p/4. Rounds use the matchings {x, x ^ v_r} over GF(2)^k; every GPU holds whole cosets
+ * x + span{v_{r-1}, v_r}, trains the pair that leaves it after the round first (early = 1) and the
+ * pair that stays second, so the departing partitions' handoff overlaps the staying pair's
+ * buckets. Same outputs as ember_make_rounds plus early: p*p u8. */
+int ember_make_rounds_overlap(uint32_t p, uint32_t world, uint32_t* order, uint32_t* round, uint32_t* rank,
+                              uint8_t* early, uint32_t* holder, uint32_t* n_rounds);
 /* External relation reduction: with grad_dev != NULL every training step zeroes grad_dev
  * ([R x dim] f32, device) and writes the batch's summed relation gradients into it instead of
  * updating the relation table; the caller reduces it across ranks (e.g. an NCCL all-reduce on the

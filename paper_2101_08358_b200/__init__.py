@@ -16,7 +16,8 @@ from ._lib import (ENGINE, KIND, ORDERING, BufferReport, ConfigError, EmberError
                    StepStats, check, lib)
 
 __all__ = ["ConfigError", "EmberError", "Hyper", "Trainer", "PartitionBuffer", "preprocess_graph", "make_plan", "lower_bound_swaps",
-           "elimination_swap_formula", "generate_graph", "bucket_edges", "partition_offset", "partition_size", "lib"]
+           "elimination_swap_formula", "generate_graph", "bucket_edges", "partition_offset", "partition_size", "lib",
+           "rows_to_disk", "rows_to_hbm"]
 
 
 def partition_offset(V: int, p: int, k: int) -> int:
@@ -27,6 +28,25 @@ def partition_offset(V: int, p: int, k: int) -> int:
 def partition_size(V: int, p: int, k: int) -> int:
     q, r = divmod(V, p)
     return q + (1 if k < r else 0)
+
+
+def rows_to_disk(x: np.ndarray, kind) -> np.ndarray:
+    """Rows in the HBM row layout -> on-disk coordinate order. Only ComplEx rows
+    differ: HBM holds their [re | im] halves interleaved by pairs (include/ember_gpu.h)."""
+    x = np.asarray(x)
+    if KIND.get(kind, kind) != KIND["complex"]:
+        return x
+    n, d = x.shape
+    return np.ascontiguousarray(x.reshape(n, d // 4, 2, 2).transpose(0, 2, 1, 3).reshape(n, d))
+
+
+def rows_to_hbm(x: np.ndarray, kind) -> np.ndarray:
+    """On-disk coordinate order -> the HBM row layout (inverse of rows_to_disk)."""
+    x = np.asarray(x)
+    if KIND.get(kind, kind) != KIND["complex"]:
+        return x
+    n, d = x.shape
+    return np.ascontiguousarray(x.reshape(n, 2, d // 4, 2).transpose(0, 2, 1, 3).reshape(n, d))
 
 
 def _ptr(x) -> int | None:
@@ -258,11 +278,18 @@ class Trainer:
         self._leave()
 
     def node_table(self):
-        """Concatenated theta/acc of all partitions (host copies for parity checks)."""
+        """Concatenated theta/acc of all partitions: host copies in on-disk coordinate order (the
+        device tables hold the HBM row layout, rows_to_disk)."""
         self.synchronize()
         th = self.torch.cat([self.theta[k] for k in range(self.p)]).cpu().numpy()
         ac = self.torch.cat([self.acc[k] for k in range(self.p)]).cpu().numpy()
-        return th, ac
+        return rows_to_disk(th, self.h.kind), rows_to_disk(ac, self.h.kind)
+
+    def relation_table(self):
+        """theta/acc of the relation table, host copies in on-disk coordinate order."""
+        self.synchronize()
+        return (rows_to_disk(self.rel_theta.cpu().numpy(), self.h.kind),
+                rows_to_disk(self.rel_acc.cpu().numpy(), self.h.kind))
 
     # -- the step -------------------------------------------------------------------------
     def train_batch(self, bucket_edges, batch_begin: int, nb: int, i: int = 0, j: int = 0, epoch: int = 0,
@@ -474,10 +501,11 @@ class PartitionBuffer:
         return out[:3 * n.value].reshape(-1, 3)
 
     def node_table(self):
-        """Concatenated host backing store (after flush)."""
+        """Concatenated host backing store (after flush), in on-disk coordinate order."""
         self.flush()
-        return (np.concatenate([x.numpy() for x in self.host_theta]),
-                np.concatenate([x.numpy() for x in self.host_acc]))
+        k = self.tr.h.kind
+        return (rows_to_disk(np.concatenate([x.numpy() for x in self.host_theta]), k),
+                rows_to_disk(np.concatenate([x.numpy() for x in self.host_acc]), k))
 
     def close(self):
         if getattr(self, "buf", None):

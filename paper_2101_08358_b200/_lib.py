@@ -96,6 +96,7 @@ def _declare(L):
         "ember_buffer_decisions": (C.c_int, [vp, vp, C.POINTER(u32)]),
         "ember_train_epoch_buffered": (C.c_int, [vp, vp, vp, vp, u64, C.POINTER(StepStats)]),
         "ember_make_rounds": (C.c_int, [u32, u32, vp, vp, vp, vp, C.POINTER(u32)]),
+        "ember_make_rounds_overlap": (C.c_int, [u32, u32, vp, vp, vp, vp, vp, C.POINTER(u32)]),
         "ember_relations_external": (C.c_int, [vp, vp]),
         "ember_relations_apply_dense": (C.c_int, [vp, vp]),
         "ember_overflow_rows": (C.c_int, [vp, C.POINTER(u64)]),
@@ -107,6 +108,8 @@ def _declare(L):
         "ember_host_free_pinned": (C.c_int, [vp]),
         "ember_tables_allocate": (C.c_int, [vp, u32]),
         "ember_tables_get": (C.c_int, [vp, u32, C.POINTER(vp), C.POINTER(vp), C.POINTER(u64)]),
+        "ember_rows_layout": (C.c_int, [vp, vp, u64, C.c_int]),
+        "ember_rows_layout_host": (C.c_int, [C.c_int, u32, vp, u64, C.c_int]),
         "ember_comm_init": (C.c_int, [vp, vp, i32, i32]),
         "ember_comm_barrier": (C.c_int, [vp]),
         "ember_partition_copy": (C.c_int, [vp, vp, vp, i32, vp, vp, i32, u64]),

@@ -295,11 +295,38 @@ int ember_tables_get(ember_ctx* ctx, uint32_t part, float** theta_dev, float** a
     });
 }
 
+int ember_rows_layout(ember_ctx* ctx, float* rows_dev, uint64_t rows, int to_hbm) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        if (rows && !rows_dev) throw ConfigError("rows_dev is null");
+        launch_rows_layout(E.stream, rows_dev, rows, nullptr, E.dim, E.m.kind, to_hbm != 0);
+    });
+}
+
+int ember_rows_layout_host(int kind, uint32_t dim, float* rows, uint64_t n, int to_hbm) {
+    return guarded([&] {
+        if (kind < EMBER_DOT || kind > EMBER_COMPLEX) throw ConfigError("model kind must be 0, 1 or 2");
+        if (dim == 0 || dim % 4) throw ConfigError("dim must be a positive multiple of 4");
+        if (kind != EMBER_COMPLEX || !n) return;
+        if (!rows) throw ConfigError("rows is null");
+        std::vector<float> t(dim);
+        for (uint64_t r = 0; r < n; ++r) {
+            float* row = rows + r * dim;
+            std::copy(row, row + dim, t.begin());
+            for (uint32_t c = 0; c < dim; ++c) {
+                const uint32_t p = hbm_pos(kind, dim, c);
+                if (to_hbm) row[p] = t[c];
+                else row[c] = t[p];
+            }
+        }
+    });
+}
+
 int ember_init_partition(ember_ctx* ctx, uint32_t part, uint64_t seed) {
     return guarded([&] {
         Engine& E = eng(ctx);
         const PartView v = E.view(part);
-        launch_init_rows(E.stream, v.theta, v.acc, v.first, v.rows, E.dim, seed);
+        launch_init_rows(E.stream, v.theta, v.acc, v.first, v.rows, E.dim, E.m.kind, seed);
     });
 }
 
@@ -307,7 +334,7 @@ int ember_init_relations(ember_ctx* ctx, uint64_t seed) {
     return guarded([&] {
         Engine& E = eng(ctx);
         if (!E.rel_theta) throw ConfigError("relation table not bound");
-        launch_init_rows(E.stream, E.rel_theta, E.rel_acc, 0, E.g.num_relations, E.dim, seed ^ 0x52454cULL);
+        launch_init_rows(E.stream, E.rel_theta, E.rel_acc, 0, E.g.num_relations, E.dim, E.m.kind, seed ^ 0x52454cULL);
     });
 }
 
@@ -396,6 +423,9 @@ int ember_loss_and_grad(ember_ctx* ctx, const uint32_t* edges, uint32_t nb, uint
         if (fpos) EMBER_CUDA(cudaMemcpyAsync(fpos, E.s.fpos, nb * sizeof(float), cudaMemcpyDeviceToDevice, E.stream));
         if (lse) EMBER_CUDA(cudaMemcpyAsync(lse, E.s.lse, 2ull * nb * sizeof(float), cudaMemcpyDeviceToDevice, E.stream));
         E.reduce_and_apply(nb, i, j, false, node_ids, node_rows, rel_ids, rel_rows);
+        // GradientDelta rows leave in on-disk coordinate order (counts known on the device)
+        launch_rows_layout(E.stream, node_rows, E.slots(nb), E.s.nunique, E.dim, E.m.kind, false);
+        launch_rows_layout(E.stream, rel_rows, E.slots(nb), E.s.nunique + 1, E.dim, E.m.kind, false);
         uint32_t counts[2] = {0, 0};
         float l = 0.f;
         EMBER_CUDA(cudaMemcpyAsync(counts, E.s.nunique, sizeof(counts), cudaMemcpyDeviceToHost, E.stream));
@@ -678,6 +708,19 @@ int ember_make_rounds(uint32_t p, uint32_t world, uint32_t* order, uint32_t* rou
         if (order) std::memcpy(order, S.order.data(), S.order.size() * sizeof(uint32_t));
         if (round) std::memcpy(round, S.round.data(), S.round.size() * sizeof(uint32_t));
         if (rank) std::memcpy(rank, S.rank.data(), S.rank.size() * sizeof(uint32_t));
+        if (holder) std::memcpy(holder, S.holder.data(), S.holder.size() * sizeof(uint32_t));
+        if (n_rounds) *n_rounds = S.rounds;
+    });
+}
+
+int ember_make_rounds_overlap(uint32_t p, uint32_t world, uint32_t* order, uint32_t* round, uint32_t* rank,
+                              uint8_t* early, uint32_t* holder, uint32_t* n_rounds) {
+    return guarded([&] {
+        const RoundSchedule S = make_rounds_overlap(p, world);
+        if (order) std::memcpy(order, S.order.data(), S.order.size() * sizeof(uint32_t));
+        if (round) std::memcpy(round, S.round.data(), S.round.size() * sizeof(uint32_t));
+        if (rank) std::memcpy(rank, S.rank.data(), S.rank.size() * sizeof(uint32_t));
+        if (early) std::memcpy(early, S.early.data(), S.early.size());
         if (holder) std::memcpy(holder, S.holder.data(), S.holder.size() * sizeof(uint32_t));
         if (n_rounds) *n_rounds = S.rounds;
     });

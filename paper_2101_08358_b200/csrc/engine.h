@@ -40,6 +40,19 @@ namespace ember {
         ++(E).launches;                        \
     } while (0)
 
+// HBM row layout. Dot/DistMult rows are stored in coordinate order. A ComplEx row, [re | im]
+// halves of h = d/2 on disk, is stored with its halves interleaved by pairs:
+// on-disk coordinate re k sits at 4(k/2) + k%2 and im k at 4(k/2) + 2 + k%2, so the 16 bytes at
+// float offset 4q hold the complex coordinates {re 2q, re 2q+1, im 2q, im 2q+1} (one aligned
+// 128-bit access per lane, d % 4 == 0). Every product of the step is a dot product over a row's
+// coordinates, so kernels work on HBM order throughout; only init, the ParameterSlice /
+// GradientDelta entry points and the storage boundary map coordinates (ember_rows_layout).
+__host__ __device__ inline uint32_t hbm_pos(int kind, uint32_t d, uint32_t c) {
+    if (kind != EMBER_COMPLEX) return c;
+    const uint32_t h = d / 2, im = c >= h ? 1u : 0u, k = c - im * h;
+    return 4 * (k >> 1) + 2 * im + (k & 1);
+}
+
 // A node id -> row pointer view of one partition: row(id) = base + (id - first) * dim.
 struct PartView {
     float* theta;
@@ -271,7 +284,11 @@ void launch_adagrad_rows(const Engine& E, const uint32_t* ids, const float* rows
 void launch_gather_rows(const Engine& E, const uint32_t* ids, uint32_t n, const PartView& pi, const PartView& pj,
                         bool relations, float* th_out, float* ac_out, uint32_t* bad);
 void launch_init_rows(cudaStream_t st, float* theta, float* acc, uint64_t first_row, uint64_t rows, uint32_t dim,
-                      uint64_t seed);
+                      int kind, uint64_t seed);
+// rows between on-disk coordinate order and the HBM layout, in place (no-op unless ComplEx);
+// n_dev (nullable): row count read on the device, n its upper bound
+void launch_rows_layout(cudaStream_t st, float* rows, uint64_t n, const uint32_t* n_dev, uint32_t dim, int kind,
+                        bool to_hbm);
 void launch_debug_scores(const Engine& E, const uint32_t* edges, uint32_t nb, const uint32_t* negs, int side,
                          uint32_t rows, float* out, const PartView& pi, const PartView& pj);
 void launch_eval_ranks(const Engine& E, const uint32_t* test, uint32_t n_test, const uint32_t* negs, uint32_t n_eval,

@@ -64,13 +64,14 @@ __global__ void k_eval_rank(Tables T, const float* __restrict__ rel, int kind, u
         } else if (kind == EMBER_DISTMULT) {
             a[k] = side == 0 ? ts[k] * tr[k] : tr[k] * tt[k];
         } else {
-            const float c = tr[k], ee = tr[h + k];
+            const uint32_t re = hbm_pos(kind, d, k), im = re + 2;  // complex coordinate k (HBM layout)
+            const float c = tr[re], ee = tr[im];
             if (side == 0) {
-                a[k] = ts[k] * c - ts[h + k] * ee;
-                a[h + k] = ts[k] * ee + ts[h + k] * c;
+                a[re] = ts[re] * c - ts[im] * ee;
+                a[im] = ts[re] * ee + ts[im] * c;
             } else {
-                a[k] = c * tt[k] + ee * tt[h + k];
-                a[h + k] = c * tt[h + k] - ee * tt[k];
+                a[re] = c * tt[re] + ee * tt[im];
+                a[im] = c * tt[im] - ee * tt[re];
             }
         }
     }
@@ -139,13 +140,14 @@ __global__ void __launch_bounds__(FT) k_eval_filtered(Tables T, const float* __r
             } else if (kind == EMBER_DISTMULT) {
                 a[k] = side == 0 ? ts[k] * tr[k] : tr[k] * tt[k];
             } else {
-                const float c = tr[k], ee = tr[h + k];
+                const uint32_t re = hbm_pos(kind, d, k), im = re + 2;  // complex coordinate k (HBM layout)
+                const float c = tr[re], ee = tr[im];
                 if (side == 0) {
-                    a[k] = ts[k] * c - ts[h + k] * ee;
-                    a[h + k] = ts[k] * ee + ts[h + k] * c;
+                    a[re] = ts[re] * c - ts[im] * ee;
+                    a[im] = ts[re] * ee + ts[im] * c;
                 } else {
-                    a[k] = c * tt[k] + ee * tt[h + k];
-                    a[h + k] = c * tt[h + k] - ee * tt[k];
+                    a[re] = c * tt[re] + ee * tt[im];
+                    a[im] = c * tt[im] - ee * tt[re];
                 }
             }
         }

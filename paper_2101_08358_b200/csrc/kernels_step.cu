@@ -54,39 +54,29 @@ __global__ void k_sample(uint32_t* out, uint32_t nt, uint32_t n_deg, uint32_t to
     out[slot] = sample_one(slot, nt, n_deg, base, bucket, bucket_n, src_first, src_rows, dst_first, dst_rows);
 }
 
-// Coordinates are handled in quads: quad q of a row is {4q .. 4q+3} for Dot/DistMult and, for
-// ComplEx ([re | im] halves of h = d/2), the two complex pairs {2q, 2q+1} (re) and
-// {h+2q, h+2q+1} (im), so that every lane loads its rows' quads straight into registers with
-// 16- or 8-byte loads (d % 4 == 0 keeps both aligned) and computes ComplEx products locally.
+// Coordinates are handled in quads: quad q of a row is its 16 bytes at float offset 4q. For
+// Dot/DistMult that is coordinates {4q .. 4q+3}; a ComplEx row ([re | im] halves of h = d/2 in the
+// on-disk layout) is held in HBM with its halves interleaved by pairs (hbm_pos,
+// engine.h), so quad q is the two complex coordinates {re 2q, re 2q+1, im 2q, im 2q+1} and every
+// lane moves its rows' quads with one aligned 128-bit access and computes ComplEx products locally.
 struct Quad {
     float v[4];
 };
 
-__device__ __forceinline__ Quad load_quad(const float* row, int kind, uint32_t h, uint32_t q) {
+__device__ __forceinline__ Quad load_quad(const float* row, uint32_t q) {
+    const float4 a = ldg4(row + 4 * q);
     Quad x;
-    if (kind == EMBER_COMPLEX) {
-        const float2 a = __ldg(reinterpret_cast<const float2*>(row + 2 * q));
-        const float2 b = __ldg(reinterpret_cast<const float2*>(row + h + 2 * q));
-        x.v[0] = a.x, x.v[1] = a.y, x.v[2] = b.x, x.v[3] = b.y;
-    } else {
-        const float4 a = ldg4(row + 4 * q);
-        x.v[0] = a.x, x.v[1] = a.y, x.v[2] = a.z, x.v[3] = a.w;
-    }
+    x.v[0] = a.x, x.v[1] = a.y, x.v[2] = a.z, x.v[3] = a.w;
     return x;
 }
 
-__device__ __forceinline__ void store_quad(float* row, int kind, uint32_t h, uint32_t q, const Quad& x) {
-    if (kind == EMBER_COMPLEX) {
-        *reinterpret_cast<float2*>(row + 2 * q) = make_float2(x.v[0], x.v[1]);
-        *reinterpret_cast<float2*>(row + h + 2 * q) = make_float2(x.v[2], x.v[3]);
-    } else {
-        *reinterpret_cast<float4*>(row + 4 * q) = make_float4(x.v[0], x.v[1], x.v[2], x.v[3]);
-    }
+__device__ __forceinline__ void store_quad(float* row, uint32_t q, const Quad& x) {
+    *reinterpret_cast<float4*>(row + 4 * q) = make_float4(x.v[0], x.v[1], x.v[2], x.v[3]);
 }
 
 // Adjusted quads: ad = the row the destination is scored against (s o r; ComplEx s * r), as = the
 // row the source is scored against (r o t; ComplEx r * conj(t)), so that f(s, r, t) = ad . t = s . as
-// (ComplEx halves [re | im]). Products are rounded individually (no
+// (ComplEx quads {re, re, im, im}, see above). Products are rounded individually (no
 // FMA contraction), like the oracle.
 __device__ __forceinline__ void adjust_quad(int kind, const Quad& S, const Quad& R, const Quad& T, Quad& ad,
                                             Quad& as) {
@@ -121,8 +111,9 @@ __device__ __forceinline__ void negs_pack_warp(uint32_t w, uint32_t lane, const 
     float x[8];
     if (slot < nt) {
         const float* src = node_row(side == 0 ? pj : pi, negs[side * nt + slot], d);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) x[i] = 8 * lane + i < d ? __ldg(src + 8 * lane + i) : 0.f;
+        const float4 a = ldg4(src + 8 * lane);  // d % 4 == 0: the second quad is all in or all out
+        const float4 b = 8 * lane + 4 < d ? ldg4(src + 8 * lane + 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        x[0] = a.x, x[1] = a.y, x[2] = a.z, x[3] = a.w, x[4] = b.x, x[5] = b.y, x[6] = b.z, x[7] = b.w;
     } else {
 #pragma unroll
         for (int i = 0; i < 8; ++i) x[i] = 0.f;
@@ -166,7 +157,7 @@ __global__ void __launch_bounds__(32 * GP_WARPS) k_gather_pack(const uint32_t* _
     float* xd = stage + wib * 2 * kp;
     float* xs = xd + kp;
     const uint32_t e0 = blockIdx.x * GP_ROWS;
-    const uint32_t h = d / 2, nq = d / 4;
+    const uint32_t nq = d / 4;
     for (uint32_t k = d + lane; k < kp; k += 32) xd[k] = xs[k] = 0.f;  // K padding (never rewritten)
     for (uint32_t rr = wib; rr < GP_ROWS; rr += GP_WARPS) {
         const uint32_t e = e0 + rr;
@@ -181,14 +172,14 @@ __global__ void __launch_bounds__(32 * GP_WARPS) k_gather_pack(const uint32_t* _
         float part = 0.f;
         __syncwarp();  // the previous edge's staged rows have been packed
         for (uint32_t q = lane; q < nq; q += 32) {
-            const Quad S = load_quad(ss, kind, h, q), T = load_quad(st, kind, h, q);
-            const Quad R = sr ? load_quad(sr, kind, h, q) : S;
+            const Quad S = load_quad(ss, q), T = load_quad(st, q);
+            const Quad R = sr ? load_quad(sr, q) : S;
             Quad ad, as;
             adjust_quad(kind, S, R, T, ad, as);
 #pragma unroll
             for (int i = 0; i < 4; ++i) part += ad.v[i] * T.v[i];
-            store_quad(xd, kind, h, q, ad);
-            store_quad(xs, kind, h, q, as);
+            store_quad(xd, q, ad);
+            store_quad(xs, q, as);
         }
         __syncwarp();
         if (lane < 2 * CB) {
@@ -226,17 +217,17 @@ __global__ void k_gather_adjust(const uint32_t* __restrict__ edges, uint32_t nb,
     const float* ss = node_row(pi, s, d);
     const float* st = node_row(pj, t, d);
     const float* sr = kind != EMBER_DOT ? rel + (uint64_t)r * d : nullptr;
-    const uint32_t h = d / 2, nq = d / 4;
+    const uint32_t nq = d / 4;
     float part = 0.f;
     for (uint32_t q = lane; q < nq; q += 32) {
-        const Quad S = load_quad(ss, kind, h, q), T = load_quad(st, kind, h, q);
-        const Quad R = sr ? load_quad(sr, kind, h, q) : S;
+        const Quad S = load_quad(ss, q), T = load_quad(st, q);
+        const Quad R = sr ? load_quad(sr, q) : S;
         Quad ad, as;
         adjust_quad(kind, S, R, T, ad, as);
 #pragma unroll
         for (int i = 0; i < 4; ++i) part += ad.v[i] * T.v[i];
-        store_quad(A + (uint64_t)e * d, kind, h, q, ad);
-        store_quad(A + ((uint64_t)nb + e) * d, kind, h, q, as);
+        store_quad(A + (uint64_t)e * d, q, ad);
+        store_quad(A + ((uint64_t)nb + e) * d, q, as);
     }
     for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
     if (lane == 0) fpos[e] = part;
@@ -339,32 +330,20 @@ __device__ __forceinline__ void adagrad_one(float& th, float& ac, float g, float
 }
 
 // Adagrad of one quad of a row whose parameters Th were already loaded.
-__device__ __forceinline__ void adagrad_quad(float* th_row, float* ac_row, int kind, uint32_t h, uint32_t q,
-                                             Quad Th, Quad Ac, const Quad& G, float lr, float eps) {
+__device__ __forceinline__ void adagrad_quad(float* th_row, float* ac_row, uint32_t q, Quad Th, Quad Ac, const Quad& G,
+                                             float lr, float eps) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) adagrad_one(Th.v[i], Ac.v[i], G.v[i], lr, eps);
-    store_quad(th_row, kind, h, q, Th);
-    store_quad(ac_row, kind, h, q, Ac);
+    store_quad(th_row, q, Th);
+    store_quad(ac_row, q, Ac);
 }
 
 // dA quad q of (side, edge e): column-blocked [2][d/4][dcap][4] (tensor-core engine) or
-// row-major [2][nb][d] (SIMT engine, dcap == 0).
+// row-major [2][nb][d] (SIMT engine, dcap == 0); its columns are the rows' HBM coordinates.
 __device__ __forceinline__ Quad load_dA_quad(const float* __restrict__ dA, uint32_t dcap, uint32_t nb, uint32_t side,
-                                             uint32_t e, int kind, uint32_t d, uint32_t q) {
-    const uint32_t h = d / 2;
-    if (!dcap) return load_quad(dA + ((uint64_t)side * nb + e) * d, kind, h, q);
-    const float* base = dA + (uint64_t)side * (d / 4) * dcap * 4;
-    auto at = [&](uint32_t c) { return base + ((uint64_t)(c / 4) * dcap + e) * 4 + c % 4; };
-    Quad x;
-    if (kind == EMBER_COMPLEX) {
-        const float2 a = __ldg(reinterpret_cast<const float2*>(at(2 * q)));
-        const float2 b = __ldg(reinterpret_cast<const float2*>(at(h + 2 * q)));
-        x.v[0] = a.x, x.v[1] = a.y, x.v[2] = b.x, x.v[3] = b.y;
-    } else {
-        const float4 a = ldg4(at(4 * q));
-        x.v[0] = a.x, x.v[1] = a.y, x.v[2] = a.z, x.v[3] = a.w;
-    }
-    return x;
+                                             uint32_t e, uint32_t d, uint32_t q) {
+    if (!dcap) return load_quad(dA + ((uint64_t)side * nb + e) * d, q);
+    return load_quad(dA + ((uint64_t)side * (d / 4) + q) * dcap * 4 + (uint64_t)e * 4, 0);
 }
 
 // Chain rule (one warp per edge, lanes on quads in registers), adjusted vectors recomputed from
@@ -397,16 +376,16 @@ __global__ void __launch_bounds__(256, 4) k_chain_rule(const uint32_t* __restric
     float* gR = kind != EMBER_DOT ? grows + (uint64_t)rank[2 * nb + n_neg + e] * d : nullptr;
     float* aS = pi.acc + (uint64_t)(s - pi.first) * d;
     float* aT = pj.acc + (uint64_t)(t - pj.first) * d;
-    const uint32_t h = d / 2, nq = d / 4;
+    const uint32_t nq = d / 4;
     for (uint32_t q = lane; q < nq; q += 32) {
-        const Quad S = load_quad(ss, kind, h, q), T = load_quad(st, kind, h, q);
-        const Quad R = sr ? load_quad(sr, kind, h, q) : S;
-        const Quad U = load_dA_quad(dA, dcap, nb, 0, e, kind, d, q);  // destination side
-        const Quad W = load_dA_quad(dA, dcap, nb, 1, e, kind, d, q);  // source side
+        const Quad S = load_quad(ss, q), T = load_quad(st, q);
+        const Quad R = sr ? load_quad(sr, q) : S;
+        const Quad U = load_dA_quad(dA, dcap, nb, 0, e, d, q);  // destination side
+        const Quad W = load_dA_quad(dA, dcap, nb, 1, e, d, q);  // source side
         Quad AS, AT;  // accumulators, loaded with the rows (speculatively: used when the key is unique)
         if (direct) {
-            AS = load_quad(aS, kind, h, q);
-            AT = load_quad(aT, kind, h, q);
+            AS = load_quad(aS, q);
+            AT = load_quad(aT, q);
         }
         Quad ad, as, oS, oR, oT;
         adjust_quad(kind, S, R, T, ad, as);
@@ -438,11 +417,11 @@ __global__ void __launch_bounds__(256, 4) k_chain_rule(const uint32_t* __restric
                 oT.v[i] = gd * S.v[i] + (W.v[i] + gs * S.v[i]);
             }
         }
-        if (us) adagrad_quad(const_cast<float*>(ss), aS, kind, h, q, S, AS, oS, lr, eps);
-        else store_quad(gS, kind, h, q, oS);
-        if (ut) adagrad_quad(const_cast<float*>(st), aT, kind, h, q, T, AT, oT, lr, eps);
-        else store_quad(gT, kind, h, q, oT);
-        if (gR) store_quad(gR, kind, h, q, oR);
+        if (us) adagrad_quad(const_cast<float*>(ss), aS, q, S, AS, oS, lr, eps);
+        else store_quad(gS, q, oS);
+        if (ut) adagrad_quad(const_cast<float*>(st), aT, q, T, AT, oT, lr, eps);
+        else store_quad(gT, q, oT);
+        if (gR) store_quad(gR, q, oR);
     }
 }
 
@@ -464,27 +443,13 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// quad q of a row (kind layout, see load_quad) -> one float4 slot in shared memory
-__device__ __forceinline__ void cp_quad(float4* dst, const float* row, int kind, uint32_t h, uint32_t q) {
-    if (kind == EMBER_COMPLEX) {
-        cp_async8(dst, row + 2 * q);
-        cp_async8(reinterpret_cast<float*>(dst) + 2, row + h + 2 * q);
-    } else {
-        cp_async16(dst, row + 4 * q);
-    }
-}
+// quad q of a row -> one float4 slot in shared memory
+__device__ __forceinline__ void cp_quad(float4* dst, const float* row, uint32_t q) { cp_async16(dst, row + 4 * q); }
 
 // dA quad q of (side, row e), column-blocked [2][d/4][dcap][4]
 __device__ __forceinline__ void cp_dA_quad(float4* dst, const float* dA, uint32_t dcap, uint32_t side, uint32_t e,
-                                           int kind, uint32_t d, uint32_t q) {
-    const float* base = dA + (uint64_t)side * (d / 4) * dcap * 4;
-    auto at = [&](uint32_t c) { return base + ((uint64_t)(c / 4) * dcap + e) * 4 + c % 4; };
-    if (kind == EMBER_COMPLEX) {
-        cp_async8(dst, at(2 * q));
-        cp_async8(reinterpret_cast<float*>(dst) + 2, at(d / 2 + 2 * q));
-    } else {
-        cp_async16(dst, at(4 * q));
-    }
+                                           uint32_t d, uint32_t q) {
+    cp_async16(dst, dA + ((uint64_t)side * (d / 4) + q) * dcap * 4 + (uint64_t)e * 4);
 }
 
 __device__ __forceinline__ Quad quad_of(const float4& v) {
@@ -516,7 +481,7 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
     const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + wib, nw = gridDim.x * (blockDim.x >> 5);
     float4* my = cpbuf + (size_t)wib * 2 * CP_ROLES * 32 + lane;
-    const uint32_t h = d / 2, nq = d / 4;
+    const uint32_t nq = d / 4;
     const bool ql = lane < nq;
     auto issue = [&](uint32_t e, int st, EdgeMeta& m) {
         m.s = edges[3 * e];
@@ -535,13 +500,13 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
         }
         if (ql) {
             float4* b = my + (size_t)st * CP_ROLES * 32;
-            cp_quad(b + 0 * 32, node_row(pi, m.s, d), kind, h, lane);
-            cp_quad(b + 1 * 32, node_row(pj, m.t, d), kind, h, lane);
-            if (kind != EMBER_DOT) cp_quad(b + 2 * 32, rel + (uint64_t)r * d, kind, h, lane);
-            if (m.uq & 1u) cp_quad(b + 3 * 32, pi.acc + (uint64_t)(m.s - pi.first) * d, kind, h, lane);
-            if (m.uq & 2u) cp_quad(b + 4 * 32, pj.acc + (uint64_t)(m.t - pj.first) * d, kind, h, lane);
-            cp_dA_quad(b + 5 * 32, dA, dcap, 0, e, kind, d, lane);
-            cp_dA_quad(b + 6 * 32, dA, dcap, 1, e, kind, d, lane);
+            cp_quad(b + 0 * 32, node_row(pi, m.s, d), lane);
+            cp_quad(b + 1 * 32, node_row(pj, m.t, d), lane);
+            if (kind != EMBER_DOT) cp_quad(b + 2 * 32, rel + (uint64_t)r * d, lane);
+            if (m.uq & 1u) cp_quad(b + 3 * 32, pi.acc + (uint64_t)(m.s - pi.first) * d, lane);
+            if (m.uq & 2u) cp_quad(b + 4 * 32, pj.acc + (uint64_t)(m.t - pj.first) * d, lane);
+            cp_dA_quad(b + 5 * 32, dA, dcap, 0, e, d, lane);
+            cp_dA_quad(b + 6 * 32, dA, dcap, 1, e, d, lane);
         }
         cp_commit();
     };
@@ -596,16 +561,16 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
             float* thS = pi.theta + (uint64_t)(cur.s - pi.first) * d;
             float* thT = pj.theta + (uint64_t)(cur.t - pj.first) * d;
             if (cur.uq & 1u)
-                adagrad_quad(thS, pi.acc + (uint64_t)(cur.s - pi.first) * d, kind, h, lane, S, quad_of(b[3 * 32]), oS,
+                adagrad_quad(thS, pi.acc + (uint64_t)(cur.s - pi.first) * d, lane, S, quad_of(b[3 * 32]), oS,
                              lr, eps);
             else
-                store_quad(grows + (uint64_t)cur.ps * d, kind, h, lane, oS);
+                store_quad(grows + (uint64_t)cur.ps * d, lane, oS);
             if (cur.uq & 2u)
-                adagrad_quad(thT, pj.acc + (uint64_t)(cur.t - pj.first) * d, kind, h, lane, T, quad_of(b[4 * 32]), oT,
+                adagrad_quad(thT, pj.acc + (uint64_t)(cur.t - pj.first) * d, lane, T, quad_of(b[4 * 32]), oT,
                              lr, eps);
             else
-                store_quad(grows + (uint64_t)cur.pt * d, kind, h, lane, oT);
-            if (kind != EMBER_DOT) store_quad(grows + (uint64_t)cur.pr * d, kind, h, lane, oR);
+                store_quad(grows + (uint64_t)cur.pt * d, lane, oT);
+            if (kind != EMBER_DOT) store_quad(grows + (uint64_t)cur.pr * d, lane, oR);
         }
         cur = nxt;
     }
@@ -1141,7 +1106,7 @@ __global__ void __launch_bounds__(32 * LONG_WARPS) k_long_final(SegArgs a) {
 }
 
 __global__ void k_adagrad_rows(const uint32_t* __restrict__ ids, const float* __restrict__ rows, uint32_t n,
-                               uint32_t d, PartView pi, PartView pj, int relations, float* rel_theta, float* rel_acc,
+                               uint32_t d, int kind, PartView pi, PartView pj, int relations, float* rel_theta, float* rel_acc,
                                uint32_t n_rel, float lr, float eps, uint32_t* bad) {
     const uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (u >= n) return;
@@ -1164,7 +1129,10 @@ __global__ void k_adagrad_rows(const uint32_t* __restrict__ ids, const float* __
         th = v.theta + (uint64_t)(key - v.first) * d;
         ac = v.acc + (uint64_t)(key - v.first) * d;
     }
-    for (uint32_t k = lane; k < d; k += 32) adagrad_elem(th[k], ac[k], rows[(uint64_t)u * d + k], lr, eps);
+    for (uint32_t c = lane; c < d; c += 32) {  // c: on-disk coordinate of the caller's row
+        const uint32_t k = hbm_pos(kind, d, c);
+        adagrad_elem(th[k], ac[k], rows[(uint64_t)u * d + c], lr, eps);
+    }
 }
 
 // Warp per (row, negative): debug scores for parity tests.
@@ -1178,20 +1146,47 @@ __global__ void k_debug_scores(const float* A, const float* N, uint32_t rows, ui
     if (lane == 0) out[w] = acc;
 }
 
-__global__ void k_init_rows(float* theta, float* acc, uint64_t first, uint64_t rows, uint32_t d, uint64_t seed,
-                            float a) {
+// Row r's draws are its coordinates in on-disk order; each lands at its HBM
+// position (hbm_pos: ComplEx pair interleave).
+__global__ void k_init_rows(float* theta, float* acc, uint64_t first, uint64_t rows, uint32_t d, int kind,
+                            uint64_t seed, float a) {
     const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= rows) return;
     Rng g(mix_seed(seed, first + r));
     float* out = theta + r * d;
-    for (uint32_t k = 0; k < d; k += 4) {
-        float4 v;
-        v.x = g.uniform(-a, a);
-        v.y = g.uniform(-a, a);
-        v.z = g.uniform(-a, a);
-        v.w = g.uniform(-a, a);
-        reinterpret_cast<float4*>(out)[k / 4] = v;
-        if (acc) reinterpret_cast<float4*>(acc + r * d)[k / 4] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (kind == EMBER_COMPLEX) {
+        for (uint32_t c = 0; c < d; ++c) out[hbm_pos(kind, d, c)] = g.uniform(-a, a);
+    } else {
+        for (uint32_t k = 0; k < d; k += 4) {
+            float4 v;
+            v.x = g.uniform(-a, a);
+            v.y = g.uniform(-a, a);
+            v.z = g.uniform(-a, a);
+            v.w = g.uniform(-a, a);
+            reinterpret_cast<float4*>(out)[k / 4] = v;
+        }
+    }
+    if (acc)
+        for (uint32_t k = 0; k < d; k += 4) reinterpret_cast<float4*>(acc + r * d)[k / 4] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// Rows between the on-disk coordinate order and the HBM layout (in place, a warp per row; no-op
+// unless ComplEx). n_dev (nullable): the row count is read on the device (export buffers whose
+// length the step produced).
+__global__ void k_rows_layout(float* rows, uint64_t n, const uint32_t* n_dev, uint32_t d, int to_hbm) {
+    extern __shared__ float rl_tmp[];  // [warps][d]
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint64_t r = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+    const uint64_t cnt = n_dev ? (uint64_t)*n_dev : n;
+    if (r >= cnt) return;
+    float* row = rows + r * d;
+    float* t = rl_tmp + (size_t)wib * d;
+    for (uint32_t c = lane; c < d; c += 32) t[c] = row[c];
+    __syncwarp();
+    for (uint32_t c = lane; c < d; c += 32) {
+        const uint32_t p = hbm_pos(EMBER_COMPLEX, d, c);
+        if (to_hbm) row[p] = t[c];
+        else row[c] = t[p];
     }
 }
 
@@ -1367,7 +1362,7 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
 void launch_adagrad_rows(const Engine& E, const uint32_t* ids, const float* rows, uint32_t n, const PartView& pi,
                          const PartView& pj, bool relations, uint32_t* bad) {
     if (!n) return;
-    k_adagrad_rows<<<(n * 32 + 255) / 256, 256, 0, E.stream>>>(ids, rows, n, E.dim, pi, pj, relations ? 1 : 0,
+    k_adagrad_rows<<<(n * 32 + 255) / 256, 256, 0, E.stream>>>(ids, rows, n, E.dim, E.m.kind, pi, pj, relations ? 1 : 0,
                                                                 E.rel_theta, E.rel_acc, E.g.num_relations, E.m.lr,
                                                                 E.m.eps, bad);
     EMBER_LAUNCHED(E);
@@ -1376,7 +1371,7 @@ void launch_adagrad_rows(const Engine& E, const uint32_t* ids, const float* rows
 // ParameterSlice gather (getGpuParameters): warp per id, the theta
 // (and acc) row of a node of partition i or j, or of a relation, copied out in id order. Ids
 // outside both partitions (outside [0, R) for relations) are counted in *bad, their rows untouched.
-__global__ void k_gather_rows(const uint32_t* __restrict__ ids, uint32_t n, uint32_t d, PartView pi, PartView pj,
+__global__ void k_gather_rows(const uint32_t* __restrict__ ids, uint32_t n, uint32_t d, int kind, PartView pi, PartView pj,
                               int relations, const float* rel_theta, const float* rel_acc, uint32_t n_rel,
                               float* th_out, float* ac_out, uint32_t* bad) {
     const uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -1401,25 +1396,35 @@ __global__ void k_gather_rows(const uint32_t* __restrict__ ids, uint32_t n, uint
         th = v.theta + (uint64_t)(key - v.first) * d;
         ac = v.acc + (uint64_t)(key - v.first) * d;
     }
-    for (uint32_t k = lane; k < d; k += 32) {
-        th_out[(uint64_t)u * d + k] = th[k];
-        if (ac_out) ac_out[(uint64_t)u * d + k] = ac[k];
+    for (uint32_t c = lane; c < d; c += 32) {  // out in on-disk coordinate order
+        const uint32_t k = hbm_pos(kind, d, c);
+        th_out[(uint64_t)u * d + c] = th[k];
+        if (ac_out) ac_out[(uint64_t)u * d + c] = ac[k];
     }
 }
 
 void launch_gather_rows(const Engine& E, const uint32_t* ids, uint32_t n, const PartView& pi, const PartView& pj,
                         bool relations, float* th_out, float* ac_out, uint32_t* bad) {
     if (!n) return;
-    k_gather_rows<<<(n * 32 + 255) / 256, 256, 0, E.stream>>>(ids, n, E.dim, pi, pj, relations ? 1 : 0, E.rel_theta,
+    k_gather_rows<<<(n * 32 + 255) / 256, 256, 0, E.stream>>>(ids, n, E.dim, E.m.kind, pi, pj, relations ? 1 : 0, E.rel_theta,
                                                                E.rel_acc, E.g.num_relations, th_out, ac_out, bad);
     EMBER_LAUNCHED(E);
 }
 
 void launch_init_rows(cudaStream_t st, float* theta, float* acc, uint64_t first, uint64_t rows, uint32_t dim,
-                      uint64_t seed) {
+                      int kind, uint64_t seed) {
     if (!rows) return;
     const float a = (float)(1.0 / sqrt((double)dim));
-    k_init_rows<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(theta, acc, first, rows, dim, seed, a);
+    k_init_rows<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(theta, acc, first, rows, dim, kind, seed, a);
+    EMBER_CUDA(cudaGetLastError());
+}
+
+void launch_rows_layout(cudaStream_t st, float* rows, uint64_t n, const uint32_t* n_dev, uint32_t dim, int kind,
+                        bool to_hbm) {
+    if (kind != EMBER_COMPLEX || !rows || (!n && !n_dev)) return;
+    const uint32_t warps = 8;
+    k_rows_layout<<<(unsigned)((n + warps - 1) / warps), warps * 32, warps * dim * sizeof(float), st>>>(
+        rows, n, n_dev, dim, to_hbm ? 1 : 0);
     EMBER_CUDA(cudaGetLastError());
 }
 

@@ -36,6 +36,7 @@ class RoundPlan:
     round: np.ndarray   # [p*p] round of each position
     rank: np.ndarray    # [p*p] GPU of each position
     holder: np.ndarray  # [rounds, p] GPU holding partition x during round r
+    early: np.ndarray | None = None  # [p*p] overlapped schedule: bucket's partitions leave after the round
 
     def buckets(self, r: int, g: int) -> list[tuple[int, int, int]]:
         """(bucket_step, i, j) of GPU g in round r, in training order."""
@@ -52,15 +53,24 @@ class RoundPlan:
         return [(int(x), int(a[x]), int(b[x])) for x in range(self.p) if a[x] != b[x]]
 
 
-def make_rounds(p: int, world: int) -> RoundPlan:
+def make_rounds(p: int, world: int, overlap: bool = False) -> RoundPlan:
+    """Circle-method rounds (ember_make_rounds), or with overlap=True the coset schedule
+    (ember_make_rounds_overlap: p a power of two, world | p/4) whose departing partitions are used
+    only by each round's first (early) buckets."""
     n = p * p
     order, rnd, rank = (np.zeros(n, np.uint32) for _ in range(3))
     holder = np.zeros(max(1, p - 1) * p, np.uint32)
     nr = C.c_uint32(0)
-    check(lib().ember_make_rounds(p, world, order.ctypes.data, rnd.ctypes.data, rank.ctypes.data,
-                                  holder.ctypes.data, C.byref(nr)))
+    early = None
+    if overlap:
+        early = np.zeros(n, np.uint8)
+        check(lib().ember_make_rounds_overlap(p, world, order.ctypes.data, rnd.ctypes.data, rank.ctypes.data,
+                                              early.ctypes.data, holder.ctypes.data, C.byref(nr)))
+    else:
+        check(lib().ember_make_rounds(p, world, order.ctypes.data, rnd.ctypes.data, rank.ctypes.data,
+                                      holder.ctypes.data, C.byref(nr)))
     R = int(nr.value)
-    return RoundPlan(p, world, R, order, rnd, rank, holder[:R * p].reshape(R, p))
+    return RoundPlan(p, world, R, order, rnd, rank, holder[:R * p].reshape(R, p), early)
 
 
 def round_batches(plan: RoundPlan, offsets, batch_size: int, r: int, g: int) -> list[tuple]:

@@ -15,7 +15,7 @@ import os
 
 import numpy as np
 
-from . import partition_size
+from . import partition_size, rows_to_disk, rows_to_hbm
 
 
 def _pod_write(path: str, arr: np.ndarray) -> None:
@@ -98,10 +98,12 @@ def save_trainer(root: str, trainer) -> None:
     """Checkpoint of a Trainer with HBM-resident tables (every partition + relations)."""
     trainer.synchronize()
     write_meta(root, trainer.V, trainer.R, trainer.p, trainer.h.dim, model=trainer.h.kind)
+    kind = trainer.h.kind  # the files hold on-disk coordinate order, the tables the HBM layout
     for k in range(trainer.p):
-        write_node_part(root, k, trainer.theta[k].cpu().numpy(), trainer.acc[k].cpu().numpy())
+        write_node_part(root, k, rows_to_disk(trainer.theta[k].cpu().numpy(), kind),
+                        rows_to_disk(trainer.acc[k].cpu().numpy(), kind))
     if trainer.rel_theta is not None:
-        write_relations(root, trainer.rel_theta.cpu().numpy(), trainer.rel_acc.cpu().numpy())
+        write_relations(root, *trainer.relation_table())
 
 
 def load_trainer(root: str, trainer) -> None:
@@ -110,28 +112,31 @@ def load_trainer(root: str, trainer) -> None:
     if (meta["num_nodes"], meta["num_relations"], meta["num_partitions"], meta["dim"]) != \
             (trainer.V, trainer.R, trainer.p, trainer.h.dim):
         raise ValueError("checkpoint geometry does not match the trainer")  # ConfigError
-    t = trainer.torch
+    t, kind = trainer.torch, trainer.h.kind
     for k in range(trainer.p):
         th, ac = read_node_part(root, k, partition_size(trainer.V, trainer.p, k), trainer.h.dim)
-        trainer.theta[k].copy_(t.from_numpy(th))
-        trainer.acc[k].copy_(t.from_numpy(ac))
+        trainer.theta[k].copy_(t.from_numpy(rows_to_hbm(th, kind)))
+        trainer.acc[k].copy_(t.from_numpy(rows_to_hbm(ac, kind)))
     if trainer.rel_theta is not None:
         th, ac = read_relations(root, trainer.R, trainer.h.dim)
-        trainer.rel_theta.copy_(t.from_numpy(th))
-        trainer.rel_acc.copy_(t.from_numpy(ac))
+        trainer.rel_theta.copy_(t.from_numpy(rows_to_hbm(th, kind)))
+        trainer.rel_acc.copy_(t.from_numpy(rows_to_hbm(ac, kind)))
     trainer.synchronize()
 
 
 def load_buffer_backing(root: str, buf) -> None:
     """Fills a PartitionBuffer's pinned host backing store from node_part_<k>.bin files."""
-    tr = buf.tr
+    tr = buf.tr  # the backing store holds the HBM row layout
     for k in range(tr.p):
-        read_node_part(root, k, buf.host_theta[k].shape[0], tr.h.dim, buf.host_theta[k].numpy(),
-                       buf.host_acc[k].numpy())
+        th, ac = read_node_part(root, k, buf.host_theta[k].shape[0], tr.h.dim)
+        buf.host_theta[k].numpy()[:] = rows_to_hbm(th, tr.h.kind)
+        buf.host_acc[k].numpy()[:] = rows_to_hbm(ac, tr.h.kind)
 
 
 def save_buffer_backing(root: str, buf) -> None:
     """Writes the backing store (after an epoch, i.e. after the buffer's flush) as node_part files."""
     buf.flush()
+    kind = buf.tr.h.kind
     for k in range(buf.tr.p):
-        write_node_part(root, k, buf.host_theta[k].numpy(), buf.host_acc[k].numpy())
+        write_node_part(root, k, rows_to_disk(buf.host_theta[k].numpy(), kind),
+                        rows_to_disk(buf.host_acc[k].numpy(), kind))

@@ -26,8 +26,7 @@ def make_trainer(kind="distmult", dim=32, b=512, nt=64, alpha=0.5, chunks=1, V=3
 def host_tables(tr):
     th, ac = tr.node_table()
     if tr.rel_theta is not None:
-        rt = tr.rel_theta.cpu().numpy().copy()
-        ra = tr.rel_acc.cpu().numpy().copy()
+        rt, ra = tr.relation_table()
     else:
         rt = np.zeros((1, tr.h.dim), np.float32)
         ra = np.zeros((1, tr.h.dim), np.float32)

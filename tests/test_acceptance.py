@@ -113,7 +113,7 @@ def test_in_memory_10_epochs_mrr_matches_cpu_reference(case):
         rec["epochs"].append({"epoch": ep, "loss_gpu": g_loss, "loss_oracle": c_loss,
                               "loss_rel_diff": abs(g_loss - c_loss) / abs(c_loss)})
     g_th, _ = tr.node_table()
-    g_rt = tr.rel_theta.cpu().numpy()
+    g_rt = tr.relation_table()[0]
     gm = _filtered(c["kind"], d, g_th, g_rt, V, test, keys)
     cm = _filtered(c["kind"], d, cpu.th, cpu.rt, V, test, keys)
     rec.update(filtered_gpu=gm, filtered_oracle=cm, train_seconds_gpu=round(t_gpu, 2),

@@ -70,7 +70,7 @@ def test_fb86m_steps_match_oracle(workload):
         batch = bucket[begin:begin + nb]
         ids = np.unique(np.concatenate([batch[:, 0], batch[:, 2], negs_np]))
         th_c, ac_c = (x.cpu().numpy() for x in tr.gather(_dev(ids), i, j))
-        rt, ra = tr.rel_theta.cpu().numpy(), tr.rel_acc.cpu().numpy()
+        rt, ra = tr.relation_table()
         cb = np.stack([np.searchsorted(ids, batch[:, 0]), batch[:, 1], np.searchsorted(ids, batch[:, 2])], 1)
         cb = cb.astype(np.uint32)
         cn = np.searchsorted(ids, negs_np).astype(np.uint32)
@@ -104,7 +104,7 @@ def test_fb86m_steps_match_oracle(workload):
         # the training step through ember_train_batch: post-Adagrad rows bit-exact
         tr.train_batch(bucket_dev, begin, nb, i, j, 0, step, k)
         th_n, ac_n = (x.cpu().numpy() for x in tr.gather(_dev(ids), i, j))
-        rt_n, ra_n = tr.rel_theta.cpu().numpy(), tr.rel_acc.cpu().numpy()
+        rt_n, ra_n = tr.relation_table()
         th_e, ac_e = th_c.copy(), ac_c.copy()
         po.adagrad_apply(d, 0.1, 1e-10, np.searchsorted(ids, got["node_ids"]).astype(np.uint32), got["node_rows"],
                          th_e, ac_e)

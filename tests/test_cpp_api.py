@@ -91,7 +91,7 @@ def test_cpp_api_trains_like_the_oracle(tmp_path):
     py = tr.train_epoch(torch.from_numpy(edges.view(np.int32)).cuda(), off, plan["seq"], 0)
     th_py, _ = tr.node_table()
     assert np.concatenate([ld("theta2_p0"), ld("theta2_p1")]).tobytes() == th_py.tobytes()
-    assert ld("rel2").tobytes() == tr.rel_theta.cpu().numpy().tobytes()
+    assert ld("rel2").tobytes() == tr.relation_table()[0].tobytes()
     assert float(ld("epoch_loss_p2", np.float64)[0]) == pytest.approx(py["loss"], rel=1e-12)
     tr.close()
     ls = []

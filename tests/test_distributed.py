@@ -48,6 +48,33 @@ def test_round_schedule_is_conflict_free_cover(p, world):
     assert (np.diff(plan.round.astype(np.int64)) >= 0).all()
 
 
+@pytest.mark.parametrize("p,world", [(4, 1), (8, 1), (8, 2), (16, 1), (16, 2), (16, 4), (32, 4), (32, 8), (64, 16)])
+def test_overlapped_schedule_departing_pairs_first(p, world):
+    """Coset schedule: a conflict-free cover like the circle method, and every partition that leaves
+    its GPU after a round is used only by that GPU's early buckets, which come first in its round;
+    each GPU receives exactly the pairs it sends (2 partitions per coset per round)."""
+    plan = ed.make_rounds(p, world, overlap=True)
+    assert plan.rounds == p - 1
+    assert sorted(plan.order.tolist()) == list(range(p * p))
+    for r in range(plan.rounds):
+        for g in range(world):
+            held = set(plan.partitions(r, g))
+            assert len(held) == p // world
+            sel = np.nonzero((plan.round == r) & (plan.rank == g))[0]
+            flags = plan.early[sel]
+            assert flags.tolist() == sorted(flags.tolist(), reverse=True), "early buckets first"
+            for s_ in sel:
+                i, j = divmod(int(plan.order[s_]), p)
+                assert i in held and j in held
+        if r + 1 < plan.rounds:
+            for x, src, dst in plan.transfers(r):
+                uses = [s_ for s_ in range(p * p) if plan.round[s_] == r and x in divmod(int(plan.order[s_]), p)]
+                assert uses and all(plan.early[s_] for s_ in uses), "a departing partition trains early only"
+            into = np.bincount([dst for _, _, dst in plan.transfers(r)], minlength=world)
+            out = np.bincount([src for _, src, _ in plan.transfers(r)], minlength=world)
+            assert (into == out).all() and into.max() <= 2 * (p // 4) // world
+
+
 def test_round_schedule_handoff_volume():
     """p=16 over 8 GPUs: every round moves at most 2 partitions into each GPU (and the greedy
     assignment keeps at least one partition in place for most GPUs)."""
@@ -197,8 +224,8 @@ def test_gpu_backend_single_rank_matches_direct_training(kind):
             ref.train_epoch(dev_edges, off, seq, ep)
         th_ref, ac_ref = ref.node_table()
         tabs = D.local_tables()
-        th = np.concatenate([tabs[x][0].cpu().numpy() for x in range(p)])
-        ac = np.concatenate([tabs[x][1].cpu().numpy() for x in range(p)])
+        th = eb.rows_to_disk(np.concatenate([tabs[x][0].cpu().numpy() for x in range(p)]), kind)
+        ac = eb.rows_to_disk(np.concatenate([tabs[x][1].cpu().numpy() for x in range(p)]), kind)
         assert th.tobytes() == th_ref.tobytes()
         assert ac.tobytes() == ac_ref.tobytes()
         if kind != "dot":
@@ -233,10 +260,12 @@ def _gpu_worker(rank, world, port, out_dir):
     for ep in range(GCFG["epochs"]):
         D.train_epoch(ep)
     torch.cuda.synchronize()
-    tabs = {x: (t[0].cpu().numpy(), t[1].cpu().numpy()) for x, t in D.local_tables().items()}
+    k = GCFG["kind"]
+    tabs = {x: (eb.rows_to_disk(t[0].cpu().numpy(), k), eb.rows_to_disk(t[1].cpu().numpy(), k))
+            for x, t in D.local_tables().items()}
     np.savez(os.path.join(out_dir, f"g{rank}.npz"), held=np.array(sorted(tabs)),
              **{f"th{x}": v[0] for x, v in tabs.items()}, **{f"ac{x}": v[1] for x, v in tabs.items()},
-             rel_theta=tr.rel_theta.cpu().numpy(), rel_acc=tr.rel_acc.cpu().numpy())
+             rel_theta=tr.relation_table()[0], rel_acc=tr.relation_table()[1])
     dist.barrier()
     dist.destroy_process_group()
 
@@ -278,7 +307,7 @@ def test_gpu_two_rank_epochs_bit_identical_to_serial_replay(tmp_path):
                 tr.torch_stream().synchronize()
     L.check(L.lib().ember_relations_external(tr.ctx, None))
     th, ac = tr.node_table()
-    rt, ra = tr.rel_theta.cpu().numpy(), tr.rel_acc.cpu().numpy()
+    rt, ra = tr.relation_table()
     seen = set()
     for k in range(world):
         z = np.load(tmp_path / f"g{k}.npz")

@@ -54,7 +54,7 @@ def test_trained_mrr_matches_cpu_reference(case):
     dev = torch.from_numpy(bucketed.view(np.int32)).cuda()
     g_loss = [tr.train_epoch(dev, off, plan["seq"], ep)["loss"] for ep in range(c["epochs"])]
     g_th, _ = tr.node_table()
-    g_rt = tr.rel_theta.cpu().numpy() if tr.rel_theta is not None else np.zeros((1, d), np.float32)
+    g_rt = tr.relation_table()[0] if tr.rel_theta is not None else np.zeros((1, d), np.float32)
 
     # CPU reference path (oracle), same batches in the same order
     m = po.model(c["kind"], dim=d, lr=0.1, eps=1e-10, n_t=c["nt"], alpha=0.5, chunks=1, seed=1)

@@ -47,7 +47,7 @@ def main():
         for ep in range(a.epochs):
             loss = tr.train_epoch(dev, off, plan["seq"], ep)["loss"]
             th, _ = tr.node_table()
-            rt = tr.rel_theta.cpu().numpy() if tr.rel_theta is not None else np.zeros((1, a.dim), np.float32)
+            rt = tr.relation_table()[0] if tr.rel_theta is not None else np.zeros((1, a.dim), np.float32)
             ev = lambda x: po.aggregate(po.eval_ranks(a.kind, a.dim, th, rt, a.V, x, train_edges=train,  # noqa: E731
                                                       n_eval_neg=1000, alpha_eval=0.5, block=1000, eval_seed=7))
             rows.append({"epoch": ep, "loss": round(loss, 4), "test_mrr": round(float(ev(test)["mrr"]), 5),
