@@ -179,18 +179,32 @@ class Workload:
         return edges
 
 
+def dist_partitions(cfg, world):
+    """Partitions of the multi-GPU path: the overlapped (coset) schedule needs p a power of two with
+    world | p/4, so p = max(config p, 4 * world) (FB86m at 8 GPUs: 32 partitions of 2.15 GB)."""
+    p = cfg["p"]
+    while p < 4 * world or p & (p - 1):
+        p += 1
+    return p
+
+
 def bench_distributed(args, rank, world, local_rank):
-    """N > 1: one process per GPU, buckets in conflict-free rounds (paper_2101_08358_b200/distributed.py):
-    each rank holds p/N partitions, trains its buckets of the round, sums relation gradients with
-    an NCCL all-reduce every (lockstep) step, and hands partitions to their next holder by NCCL
-    P2P over NVLink between rounds. Timed: K lockstep steps from the start of round 1 (after W
-    warm-up steps), handoffs included; value = real edges of all ranks / max-over-ranks time."""
+    """N > 1 (or --distributed at N = 1): one process per GPU through the library's multi-GPU driver
+    (ember_dist_*: C++ round loop, csrc/host/dist_driver.cpp + csrc/dist.cu). Each rank holds
+    p/N partitions in driver-owned HBM slots, trains its buckets of the round, sums relation
+    gradients with an NCCL all-reduce on the step stream every (lockstep) step, and hands partitions
+    to their next holder with NCCL send/recv on a copy stream (second communicator) issued right
+    after the departing pair's buckets, under the staying pair's steps (overlapped coset schedule).
+    Timed: K lockstep steps after W warm-up steps from the epoch's start (self-buckets, handoffs
+    and idle steps included); value = real edges of all ranks / max-over-ranks device time.
+    torch.distributed only shares the two NCCL unique ids and the final timings."""
     import torch
     import torch.distributed as dist
 
     import paper_2101_08358_b200 as eb
     from paper_2101_08358_b200 import distributed as ed
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    cfg["p"] = dist_partitions(cfg, world)
     torch.cuda.set_device(local_rank)
     edges, split = eb.generate_graph(cfg["V"], cfg["R"], cfg["E"], GRAPH_SEED, cfg["train"], cfg["valid"],
                                      device=local_rank)
@@ -202,70 +216,76 @@ def bench_distributed(args, rank, world, local_rank):
     h = eb.Hyper(kind=cfg["kind"], dim=cfg["dim"], batch_size=cfg["b"], num_negatives=cfg["nt"], alpha=cfg["alpha"],
                  neg_seed=NEG_SEED, engine=args.engine)
     tr = eb.Trainer(h, cfg["V"], cfg["R"], cfg["p"], device=local_rank, allocate=False)
-    be = ed.GpuBackend(tr, bucketed)
-    D = ed.DistributedTrainer(be, cfg["p"], offsets, cfg["b"], rank, world, relations=cfg["kind"] != "dot", dist=dist)
+    ids = None
+    if world > 1:
+        idt = torch.zeros(256, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(ed.nccl_unique_id() + ed.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        raw = bytes(idt.cpu().numpy().tobytes())
+        ids = (raw[:128], raw[128:])
+    D = ed.NativeDistributed(tr, bucketed, offsets, rank, world, overlap=True, ids=ids)
     D.init_embeddings(INIT_SEED)
     stream = tr.torch_stream()
-    start = D.steps_per_round[0]
-    K = min(args.steps, D.total_steps() - start - args.warmup)
-    D.seek(start)  # round-1 layout (round 0 holds the self-buckets)
-    D.run_steps(start, args.warmup, 0)
-    torch.cuda.synchronize()
+    total = D.total_steps()
+    K = min(args.steps, total - args.warmup)
+    D.run_steps(0, args.warmup, 0)
+    D.synchronize()
     p0 = tr.profile_read()  # launch counters only: phase events stay off in the timed region
-    launches0, lib0 = p0["launches"], p0["lib_calls"]
+    launches0 = p0["launches"]
     dist.barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.3)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    hb0 = D.handoff_bytes
     e0.record(stream)
-    n_edges = D.run_steps(start + args.warmup, K, 0)
+    rep = D.run_steps(args.warmup, K, 0)
     e1.record(stream)
+    D.synchronize()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     clk = clocks.stop()
     p1 = tr.profile_read()
-    launches, lib_calls = p1["launches"] - launches0, p1["lib_calls"] - lib0
-    hb = D.handoff_bytes - hb0
-    # e2e: the next K steps with each rank's positives copied from pinned host memory per step
-    be.host_edges = bucketed.cpu().pin_memory()
-    be.loss_host = torch.zeros(1, dtype=torch.float32).pin_memory()
+    launches = p1["launches"] - launches0
+    n_edges = int(rep.edges)
+    # e2e: the next K steps with their positives copied in from pinned host memory inside the timed
+    # region (this rank's batches of those steps, one async copy each, in step order), and the last
+    # step's loss read back
+    start2 = args.warmup + K
+    K2 = min(K, total - start2)
+    host = bucketed.cpu().pin_memory()
+    spans, step = [], 0
+    for r in range(D.plan.rounds):
+        mine = ed.round_batches(D.plan, offsets, cfg["b"], r, rank)
+        for s in range(D.steps_per_round[r]):
+            if start2 <= step < start2 + K2 and s < len(mine):
+                _, _, _, _, lo, _, begin, nb = mine[s]
+                spans.append((lo + begin, nb))
+            step += 1
     dist.barrier()
     torch.cuda.synchronize()
-    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    x0.record(stream)
-    e2e_edges = D.run_steps(start + args.warmup + K, min(K, D.total_steps() - start - args.warmup - K), 0)
-    x1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = x0.elapsed_time(x1)
-    h2d = be.h2d_bytes
-    # phase breakdown from a separate instrumented pass over the next steps (phase events would
-    # break the programmatic-launch chains inside the timed region)
-    used = start + args.warmup + K + (e2e_edges > 0) * min(K, D.total_steps() - start - args.warmup - K)
-    n_prof = max(0, min(10, D.total_steps() - used))
-    be.host_edges = None  # the device-resident path again
-    tr.profile(True)
-    tr.profile_read()
-    if n_prof:
-        D.run_steps(used, n_prof, 0)
-    torch.cuda.synchronize()
-    prof = tr.profile_read()
-    tr.profile(False)
+    h0 = time.perf_counter()
+    with torch.cuda.stream(stream):
+        for a, n in spans:
+            bucketed[a:a + n].copy_(host[a:a + n], non_blocking=True)
+    rep2 = D.run_steps(start2, K2, 0) if K2 > 0 else None
+    loss = D.loss()
+    e2e_ms = (time.perf_counter() - h0) * 1e3
+    e2e_edges = int(rep2.edges) if rep2 else 0
+    h2d = sum(n for _, n in spans) * 12
+    assert np.isfinite(loss)
     vals = torch.tensor([ms, e2e_ms], dtype=torch.float64, device="cuda")
     dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    tot = torch.tensor([float(n_edges), float(e2e_edges), float(hb), float(h2d)], dtype=torch.float64, device="cuda")
+    tot = torch.tensor([float(n_edges), float(e2e_edges), float(rep.handoff_bytes), float(h2d),
+                        float(rep.early_handoffs), float(rep.handoffs)], dtype=torch.float64, device="cuda")
     dist.all_reduce(tot, op=dist.ReduceOp.SUM)
     ms, e2e_ms = float(vals[0]), float(vals[1])
     n_edges, e2e_edges = float(tot[0]), float(tot[1])
+    D.close()
     if rank != 0:
         return None
     flops_e, bytes_e = algorithmic(cfg)
-    pk = peaks()
-    peak = pk.get("bf16_tflops")
-    contract_ms = prof["ms"]["contraction"] / n_prof if n_prof else 0.0  # per step
-    achieved = flops_e * (n_edges / world / K) / (contract_ms / 1e3) / 1e12 if contract_ms > 0 else None
     return {
         "metric": METRIC if args.config == "fb86m" else f"train edges/sec ({cfg['desc']})",
         "value": round(n_edges / (ms / 1e3), 1), "unit": "edges/s", "n_gpus": world, "steps": K,
@@ -274,19 +294,19 @@ def bench_distributed(args, rank, world, local_rank):
         "data": "synthetic (planted-community power-law graph of the named shape; random-init Adagrad state)",
         "config": {"workload": cfg["desc"], "nodes": cfg["V"], "relations": cfg["R"], "edges_total": cfg["E"],
                    "train_edges": int(offsets[-1]), "model": cfg["kind"], "dim": cfg["dim"], "batch": cfg["b"],
-                   "negatives_per_side": cfg["nt"], "partitions": cfg["p"], "ordering": "conflict-free rounds",
-                   "engine": args.engine, "parallelism": f"partition-sharded x{world} (NCCL relation all-reduce, "
-                                                         f"P2P partition handoff)",
+                   "negatives_per_side": cfg["nt"], "partitions": cfg["p"],
+                   "ordering": "overlapped coset rounds (ember_make_rounds_overlap)", "engine": args.engine,
+                   "parallelism": f"partition-sharded x{world} (library driver: NCCL relation all-reduce on the "
+                                  f"step stream, NCCL P2P handoff on a copy stream)",
                    "l2": "inputs larger than L2 (node tables, random rows per batch)",
-                   "steps_per_round": D.steps_per_round[1], "handoff_bytes_timed": int(float(tot[2]))},
-        "e2e": {"value": round(e2e_edges / (e2e_ms / 1e3), 1), "unit": "edges/s",
-                "h2d_bytes_per_step": int(float(tot[3]) / max(1, K) / world), "d2h_bytes_per_step": 4},
+                   "steps_per_round": D.steps_per_round[1] if len(D.steps_per_round) > 1 else D.steps_per_round[0],
+                   "handoff_bytes_timed": int(float(tot[2])), "handoffs_timed": int(float(tot[5])),
+                   "handoffs_before_round_end": int(float(tot[4]))},
+        "e2e": {"value": round(e2e_edges / (e2e_ms / 1e3), 1) if e2e_ms > 0 else None, "unit": "edges/s",
+                "h2d_bytes_per_step": int(float(tot[3]) / max(1, K2) / world), "d2h_bytes_per_step": 4,
+                "timing": "host clock: pinned-host copies of the window's positives, the driver call, the loss read-back"},
         "gpu_launches": int(launches),
-        "phase_ms_per_step": {k: round(v / n_prof, 4) for k, v in prof["ms"].items()} if n_prof else None,
-        "roofline": {"bound": "tensor", "kernel": "contraction (scores + LSE + dA + dN)",
-                     "achieved": round(achieved, 2) if achieved else None, "peak": peak, "unit": "TFLOP/s",
-                     "frac": round(achieved / peak, 4) if achieved else None, "traffic": None,
-                     "flops_per_edge": flops_e},
+        "roofline": None,
         "clocks": clk,
     }
 

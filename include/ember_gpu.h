@@ -312,6 +312,66 @@ int ember_make_rounds(uint32_t p, uint32_t world, uint32_t* order, uint32_t* rou
  * buckets. Same outputs as ember_make_rounds plus early: p*p u8. */
 int ember_make_rounds_overlap(uint32_t p, uint32_t world, uint32_t* order, uint32_t* round, uint32_t* rank,
                               uint8_t* early, uint32_t* holder, uint32_t* n_rounds);
+/* ---- multi-GPU driver (host/dist_driver.cpp, dist.cu): train_epoch_partitioned over `world` GPUs,
+ * one process per GPU (Algorithm 2). Every rank runs the rounds of
+ * the schedule (overlap = 0: ember_make_rounds; 1: ember_make_rounds_overlap) in lockstep: a step
+ * is the rank's next batch (or an idle step when it has none left) followed, for models with
+ * relations, by the NCCL all-reduce of the dense relation gradient and the relation Adagrad; after
+ * a round the partitions that change holder move as one NCCL send/recv group on a copy stream and a
+ * second communicator, issued at the same lockstep step on every rank: with overlap = 1 right after
+ * the departing pair's buckets, so the copy runs under the staying pair's steps. The driver owns
+ * the partition tables (slots of the largest partition: held + the most received per handoff).
+ * nccl_id_steps / nccl_id_handoff: two ncclUniqueId (128 bytes each) shared by the ranks (ignored
+ * at world 1). edges_dev: the bucketed edges; offsets_host: p*p+1 bucket offsets; batches of
+ * model.batch_size. */
+typedef struct ember_dist ember_dist;
+typedef struct {
+    uint64_t steps, batches, edges, handoffs, moved_partitions;
+    uint64_t early_handoffs; /* handoffs issued before their round's last step (overlapped) */
+    uint64_t handoff_bytes;  /* bytes this rank sent (ember_dist_train_epoch, cumulative) */
+} ember_dist_report;
+int ember_dist_create(ember_ctx* ctx, uint32_t rank, uint32_t world, int overlap, const void* nccl_id_steps,
+                      const void* nccl_id_handoff, const uint32_t* edges_dev, const uint64_t* offsets_host,
+                      ember_dist** out);
+int ember_dist_destroy(ember_dist* d);
+/* init_embeddings of the partitions this rank starts with + the relation replica. */
+int ember_dist_init_embeddings(ember_dist* d, uint64_t seed);
+/* Lockstep steps [first_step, first_step + n_steps) of the epoch (n_steps = UINT64_MAX: to the
+ * end); no host synchronisation inside. */
+int ember_dist_train_epoch(ember_dist* d, uint64_t epoch, uint64_t first_step, uint64_t n_steps,
+                           ember_dist_report* out);
+/* Where a partition this rank holds now lives (NULL when it is elsewhere). */
+int ember_dist_tables(ember_dist* d, uint32_t part, float** theta_dev, float** acc_dev);
+/* Waits for the step and copy streams; reports a non-finite batch loss (status 2). */
+int ember_dist_synchronize(ember_dist* d);
+/* The last step's mean batch loss, read back on the step stream (synchronous). */
+int ember_dist_loss(ember_dist* d, float* loss_host);
+/* A fresh ncclUniqueId (128 bytes) for ember_dist_create / ember_comm_init (rank 0 makes it, the
+ * caller shares it). Loads NCCL at run time. */
+int ember_nccl_unique_id(void* out128);
+/* The lockstep plan: steps per round, the step after which each round's handoff is issued (0: none),
+ * total steps (nullable outputs; arrays of p-1 entries, 1 if p == 1). */
+int ember_dist_plan(uint32_t p, uint32_t world, uint32_t rank, int overlap, const uint64_t* offsets,
+                    uint32_t batch_size, uint32_t* steps_per_round, uint32_t* handoff_step, uint64_t* total_steps);
+/* The same round loop over caller-supplied rank operations (e.g. a CPU backend and a host
+ * transport): step(batch or NULL for an idle step), send_recv(round, moves as (part, src, dst)
+ * triples, n) at the handoff point, acquire(round, arrived parts, n) before a round's first step
+ * (nullable). A nonzero return aborts with status 2. */
+typedef struct {
+    uint32_t bucket_step, i, j, batch_in_bucket;
+    uint64_t lo, hi, begin; /* bucket edges [lo, hi); batch [lo + begin, lo + begin + nb) */
+    uint32_t nb, pad;
+} ember_batch_ref;
+typedef struct {
+    void* user;
+    int (*step)(void* user, const ember_batch_ref* batch, uint64_t epoch);
+    int (*send_recv)(void* user, uint32_t round, const uint32_t* moves, uint32_t n_moves);
+    int (*acquire)(void* user, uint32_t round, const uint32_t* parts, uint32_t n);
+} ember_rank_ops;
+int ember_dist_run(uint32_t p, uint32_t world, uint32_t rank, int overlap, const uint64_t* offsets,
+                   uint32_t batch_size, uint64_t epoch, uint64_t first_step, uint64_t n_steps,
+                   const ember_rank_ops* ops, ember_dist_report* out);
+
 /* External relation reduction: with grad_dev != NULL every training step zeroes grad_dev
  * ([R x dim] f32, device) and writes the batch's summed relation gradients into it instead of
  * updating the relation table; the caller reduces it across ranks (e.g. an NCCL all-reduce on the

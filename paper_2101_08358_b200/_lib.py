@@ -97,6 +97,16 @@ def _declare(L):
         "ember_train_epoch_buffered": (C.c_int, [vp, vp, vp, vp, u64, C.POINTER(StepStats)]),
         "ember_make_rounds": (C.c_int, [u32, u32, vp, vp, vp, vp, C.POINTER(u32)]),
         "ember_make_rounds_overlap": (C.c_int, [u32, u32, vp, vp, vp, vp, vp, C.POINTER(u32)]),
+        "ember_dist_plan": (C.c_int, [u32, u32, u32, C.c_int, vp, u32, vp, vp, C.POINTER(u64)]),
+        "ember_dist_run": (C.c_int, [u32, u32, u32, C.c_int, vp, u32, u64, u64, u64, vp, vp]),
+        "ember_dist_create": (C.c_int, [vp, u32, u32, C.c_int, vp, vp, vp, vp, C.POINTER(vp)]),
+        "ember_dist_destroy": (C.c_int, [vp]),
+        "ember_dist_init_embeddings": (C.c_int, [vp, u64]),
+        "ember_dist_train_epoch": (C.c_int, [vp, u64, u64, u64, vp]),
+        "ember_dist_tables": (C.c_int, [vp, u32, C.POINTER(vp), C.POINTER(vp)]),
+        "ember_dist_synchronize": (C.c_int, [vp]),
+        "ember_dist_loss": (C.c_int, [vp, vp]),
+        "ember_nccl_unique_id": (C.c_int, [vp]),
         "ember_relations_external": (C.c_int, [vp, vp]),
         "ember_relations_apply_dense": (C.c_int, [vp, vp]),
         "ember_overflow_rows": (C.c_int, [vp, C.POINTER(u64)]),

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstring>
 #include <exception>
+#include <functional>
 #include <new>
 #include <string>
 
@@ -92,6 +93,12 @@ void need(const void* p, const char* what) {
     if (!p) throw ConfigError(std::string(what) + " must not be NULL");
 }
 }  // namespace
+
+namespace ember {
+// for the other translation units behind the C-ABI (dist.cu)
+Engine& engine_of(ember_ctx* c) { return eng(c); }
+int guarded_status(const std::function<void()>& f) { return guarded(f); }
+}  // namespace ember
 
 namespace {
 // train_epoch_partitioned (Algorithm 2): the buckets of `seq` in order, every batch

@@ -47,6 +47,11 @@ struct NcclApi {
                                cudaStream_t) = nullptr;
     ncclResult_t (*destroy)(ncclComm_t) = nullptr;
     const char* (*err)(ncclResult_t) = nullptr;
+    ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*group_start)() = nullptr;
+    ncclResult_t (*group_end)() = nullptr;
+    ncclResult_t (*unique_id)(ncclUniqueId*) = nullptr;
 };
 
 NcclApi& nccl() {
@@ -62,7 +67,14 @@ NcclApi& nccl() {
         api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(api.h, "ncclAllReduce"));
         api.destroy = reinterpret_cast<decltype(api.destroy)>(dlsym(api.h, "ncclCommDestroy"));
         api.err = reinterpret_cast<decltype(api.err)>(dlsym(api.h, "ncclGetErrorString"));
-        if (!api.init_rank || !api.all_reduce || !api.destroy) throw EmberError("NCCL symbols missing");
+        api.send = reinterpret_cast<decltype(api.send)>(dlsym(api.h, "ncclSend"));
+        api.recv = reinterpret_cast<decltype(api.recv)>(dlsym(api.h, "ncclRecv"));
+        api.group_start = reinterpret_cast<decltype(api.group_start)>(dlsym(api.h, "ncclGroupStart"));
+        api.group_end = reinterpret_cast<decltype(api.group_end)>(dlsym(api.h, "ncclGroupEnd"));
+        api.unique_id = reinterpret_cast<decltype(api.unique_id)>(dlsym(api.h, "ncclGetUniqueId"));
+        if (!api.init_rank || !api.all_reduce || !api.destroy || !api.send || !api.recv || !api.group_start ||
+            !api.group_end || !api.unique_id)
+            throw EmberError("NCCL symbols missing");
     }
     return api;
 }
@@ -90,6 +102,39 @@ bool getenv_direct() {
 }
 
 }  // namespace
+
+void nccl_check(int r, const char* what) {
+    if (r != ncclSuccess)
+        throw EmberError(std::string(what) + " failed: " + (nccl().err ? nccl().err((ncclResult_t)r) : "?"));
+}
+
+void* nccl_comm_create(const void* unique_id, int rank, int world) {
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof(id));
+    ncclComm_t comm = nullptr;
+    nccl_check(nccl().init_rank(&comm, world, id, rank), "ncclCommInitRank");
+    return comm;
+}
+
+void nccl_unique_id(void* out) {
+    ncclUniqueId id;
+    nccl_check(nccl().unique_id(&id), "ncclGetUniqueId");
+    std::memcpy(out, &id, sizeof(id));
+}
+
+void nccl_comm_destroy(void* comm) {
+    if (comm) nccl().destroy(static_cast<ncclComm_t>(comm));
+}
+
+void nccl_group(bool start) { nccl_check(start ? nccl().group_start() : nccl().group_end(), "ncclGroupStart/End"); }
+
+void nccl_send_f32(const float* buf, size_t n, int peer, void* comm, cudaStream_t st) {
+    nccl_check(nccl().send(buf, n, ncclFloat32, peer, static_cast<ncclComm_t>(comm), st), "ncclSend");
+}
+
+void nccl_recv_f32(float* buf, size_t n, int peer, void* comm, cudaStream_t st) {
+    nccl_check(nccl().recv(buf, n, ncclFloat32, peer, static_cast<ncclComm_t>(comm), st), "ncclRecv");
+}
 
 bool pdl_enabled() {
     static const bool on = [] {
@@ -354,6 +399,15 @@ void Engine::reduce_and_apply(uint32_t nb, uint32_t i, uint32_t j, bool apply, u
         allreduce_relations();
         apply_relations_dense(s.rel_dense);
     }
+}
+
+void Engine::idle_step() {
+    // a lockstep step without a batch (multi-GPU): this rank's relation gradient is zero, but the
+    // all-reduce is a collective and the dense Adagrad applies the other ranks' sum
+    if (m.kind == EMBER_DOT || world <= 1) return;
+    EMBER_CUDA(cudaMemsetAsync(s.rel_dense, 0, (size_t)g.num_relations * dim * sizeof(float), stream));
+    allreduce_relations();
+    apply_relations_dense(s.rel_dense);
 }
 
 void Engine::apply_relations_dense(const float* grad) {

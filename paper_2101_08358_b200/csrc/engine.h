@@ -217,6 +217,7 @@ struct Engine {
               uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket, float* loss_out,
               cudaEvent_t edges_ready = nullptr);
     void allreduce_relations();
+    void idle_step();  // lockstep step without a batch (world > 1): zero relation gradient, all-reduce, Adagrad
     void apply_relations_dense(const float* grad);  // dense relation Adagrad (zero rows are no-ops)
     void comm_init(const void* nccl_unique_id, int rank, int world);
     std::vector<double> profile_read();  // ms per phase summed over marked batches
@@ -293,6 +294,14 @@ void launch_debug_scores(const Engine& E, const uint32_t* edges, uint32_t nb, co
                          uint32_t rows, float* out, const PartView& pi, const PartView& pj);
 void launch_eval_ranks(const Engine& E, const uint32_t* test, uint32_t n_test, const uint32_t* negs, uint32_t n_eval,
                        uint32_t block, uint32_t* ranks);
+// NCCL (loaded at run time, engine.cu): communicators and point-to-point copies for the multi-GPU
+// driver (dist.cu); errors throw EmberError
+void* nccl_comm_create(const void* unique_id, int rank, int world);
+void nccl_unique_id(void* out128);
+void nccl_comm_destroy(void* comm);
+void nccl_group(bool start);
+void nccl_send_f32(const float* buf, size_t n, int peer, void* comm, cudaStream_t st);
+void nccl_recv_f32(float* buf, size_t n, int peer, void* comm, cudaStream_t st);
 bool tc_engine_supported(const Engine& E);
 void tc_setup(Engine& E);
 void tc_release(Engine& E);

@@ -26,6 +26,15 @@ import numpy as np
 from ._lib import check, lib
 
 
+def check_or(status: int, trainer) -> int:
+    """check() for ember_dist_run: an exception raised inside a callback is re-raised as itself."""
+    if status and getattr(trainer, "_error", None) is not None:
+        err, trainer._error = trainer._error, None
+        raise err
+    check(status)
+    return status
+
+
 @dataclass
 class RoundPlan:
     """make_rounds(p, world): the global bucket schedule and who holds which partition when."""
@@ -85,28 +94,58 @@ def round_batches(plan: RoundPlan, offsets, batch_size: int, r: int, g: int) -> 
     return out
 
 
+class _BatchRef(C.Structure):
+    _fields_ = [("bucket_step", C.c_uint32), ("i", C.c_uint32), ("j", C.c_uint32), ("batch_in_bucket", C.c_uint32),
+                ("lo", C.c_uint64), ("hi", C.c_uint64), ("begin", C.c_uint64), ("nb", C.c_uint32), ("pad", C.c_uint32)]
+
+
+_STEP = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(_BatchRef), C.c_uint64)
+_SEND_RECV = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint32, C.POINTER(C.c_uint32), C.c_uint32)
+_ACQUIRE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint32, C.POINTER(C.c_uint32), C.c_uint32)
+
+
+class _RankOps(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("step", _STEP), ("send_recv", _SEND_RECV), ("acquire", _ACQUIRE)]
+
+
+class DistReport(C.Structure):
+    _fields_ = [(f, C.c_uint64) for f in ("steps", "batches", "edges", "handoffs", "moved_partitions",
+                                          "early_handoffs", "handoff_bytes")]
+
+
 class DistributedTrainer:
     """train_epoch_partitioned over `world` ranks with the round schedule.
 
-    backend: the rank's step/tables (GpuBackend, or a test backend); dist: torch.distributed,
-    initialised by the caller (nccl on GPUs, gloo on CPU)."""
+    The round loop is the library's (host C++, csrc/host/dist_driver.cpp, ember_dist_run): it calls
+    back into this object for each lockstep step (the backend's batch or an idle step, then the
+    relation all-reduce through torch.distributed) and at each handoff point (P2P through
+    torch.distributed). backend: the rank's step/tables (GpuBackend, or a test backend); dist:
+    torch.distributed, initialised by the caller (nccl on GPUs, gloo on CPU). The all-native GPU
+    form (NCCL inside the library, copies on their own stream) is ember_dist_create / NativeDistributed.
+    overlap: the coset schedule (make_rounds(..., overlap=True))."""
 
     def __init__(self, backend, num_partitions: int, offsets, batch_size: int, rank: int, world: int,
-                 relations: bool, dist=None, group=None):
+                 relations: bool, dist=None, group=None, overlap: bool = False):
         if dist is None:
             import torch.distributed as dist
         self.dist, self.group = dist, group
         self.be = backend
         self.rank, self.world = rank, world
-        self.plan = make_rounds(num_partitions, world)
-        self.offsets = np.asarray(offsets, dtype=np.uint64)
+        self.overlap = bool(overlap)
+        self.plan = make_rounds(num_partitions, world, overlap=self.overlap)
+        self.offsets = np.ascontiguousarray(np.asarray(offsets, dtype=np.uint64))
         self.b = batch_size
         self.relations = relations
-        # per round: every rank's batch list (all ranks compute all lists: no coordination needed)
-        self.batches = [[round_batches(self.plan, self.offsets, batch_size, r, g) for g in range(world)]
-                        for r in range(self.plan.rounds)]
-        self.steps_per_round = [max(len(x) for x in self.batches[r]) for r in range(self.plan.rounds)]
+        R = self.plan.rounds
+        steps, hand = np.zeros(R, np.uint32), np.zeros(R, np.uint32)
+        total = C.c_uint64(0)
+        check(lib().ember_dist_plan(num_partitions, world, rank, int(self.overlap), self.offsets.ctypes.data,
+                                    batch_size, steps.ctypes.data, hand.ctypes.data, C.byref(total)))
+        self.steps_per_round = [int(x) for x in steps]
+        self.handoff_step = [int(x) for x in hand]
         self.handoff_bytes = 0
+        self.report = DistReport()
+        self._error = None
 
     # -- setup --------------------------------------------------------------------------------
     def init_embeddings(self, seed: int):
@@ -129,34 +168,46 @@ class DistributedTrainer:
         raise IndexError("step beyond the epoch")
 
     def run_steps(self, start: int, count: int, epoch: int) -> int:
-        """Lockstep steps [start, start+count) of the epoch (handoffs included when a round ends).
-        Returns the number of real edges this rank trained."""
-        edges = 0
-        for step in range(start, start + count):
-            r, s = self.locate(step)
-            edges += self._step(r, s, epoch)
-            if s + 1 == self.steps_per_round[r]:
-                self.handoff(r)
-        return edges
+        """Lockstep steps [start, start+count) of the epoch through the library's round loop (handoffs
+        included where the schedule puts them). Returns the number of real edges this rank trained."""
+        def guard(fn):
+            def wrapped(*a):
+                try:
+                    fn(*a)
+                    return 0
+                except BaseException as ex:  # surfaced after the C call returns
+                    self._error = ex
+                    return 1
+            return wrapped
+
+        def step(_, bp, ep):
+            self._step(bp.contents if bp else None, int(ep))
+
+        def send_recv(_, r, mv, n):
+            self._send_recv([(int(mv[3 * k]), int(mv[3 * k + 1]), int(mv[3 * k + 2])) for k in range(n)])
+
+        ops = _RankOps(None, _STEP(guard(step)), _SEND_RECV(guard(send_recv)), _ACQUIRE(0))
+        rep = DistReport()
+        self._error = None
+        check_or(lib().ember_dist_run(self.plan.p, self.world, self.rank, int(self.overlap), self.offsets.ctypes.data,
+                                      self.b, epoch, start, count, C.byref(ops), C.byref(rep)), self)
+        for f, _ in DistReport._fields_:
+            setattr(self.report, f, getattr(self.report, f) + getattr(rep, f))
+        return int(rep.edges)
 
     def train_epoch(self, epoch: int) -> dict:
         n = self.run_steps(0, self.total_steps(), epoch)
         return {"edges": n, "steps": self.total_steps(), "handoff_bytes": self.handoff_bytes}
 
-    def _step(self, r: int, s: int, epoch: int) -> int:
-        mine = self.batches[r][self.rank]
-        n = 0
-        if s < len(mine):
-            pos, i, j, k, lo, hi, begin, nb = mine[s]
-            self.be.train_batch(pos, i, j, k, lo, hi, begin, nb, epoch)
-            n = nb
+    def _step(self, b, epoch: int):
+        if b is not None:
+            self.be.train_batch(b.bucket_step, b.i, b.j, b.batch_in_bucket, b.lo, b.hi, b.begin, b.nb, epoch)
         elif self.relations:
             self.be.zero_relation_grad()  # idle step: contributes nothing to the sum
         if self.relations:
             with self.be.collective_stream():
                 self.dist.all_reduce(self.be.relation_grad(), group=self.group)
             self.be.apply_relations()
-        return n
 
     def seek(self, step: int):
         """Positions the partitions for lockstep step `step` of an epoch (from the round-0 layout):
@@ -166,10 +217,12 @@ class DistributedTrainer:
             self.handoff(0, to=r)
 
     def handoff(self, r: int, to: int | None = None):
-        """Partitions leaving this rank after round r go to their round-(r+1) (or round-`to`) holder
-        (P2P: NCCL over NVLink for device tensors; a gloo group moves device tables through host
-        copies)."""
-        moves = self.plan.transfers(r, to)
+        """Partitions leaving this rank after round r go to their round-(r+1) (or round-`to`) holder."""
+        self._send_recv(self.plan.transfers(r, to))
+
+    def _send_recv(self, moves):
+        """This rank's part of one handoff (P2P: NCCL over NVLink for device tensors; a gloo group
+        moves device tables through host copies)."""
         if not moves:
             return
         ops, incoming = [], []
@@ -295,3 +348,100 @@ class GpuBackend:
     def after_handoff(self):
         # sent buffers may be released only once their sends have completed
         self.stream.synchronize()
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh ncclUniqueId (128 bytes; rank 0 makes it, the caller shares it, e.g. by broadcast)."""
+    buf = C.create_string_buffer(128)
+    check(lib().ember_nccl_unique_id(buf))
+    return buf.raw
+
+
+class NativeDistributed:
+    """train_epoch_partitioned over `world` GPUs entirely in the library (ember_dist_*): the C++ round
+    loop, the NCCL relation all-reduce on the step stream and the NCCL P2P partition handoffs on a
+    copy stream with a second communicator. The driver owns the node tables, so `trainer` is created
+    with allocate=False (its relation replica stays bound). ids: two ncclUniqueId (bytes) shared by
+    the ranks, None at world 1."""
+
+    def __init__(self, trainer, edges_dev, offsets, rank: int, world: int, overlap: bool = True,
+                 ids: tuple[bytes, bytes] | None = None):
+        self.tr, self.edges = trainer, edges_dev
+        self.offsets = np.ascontiguousarray(np.asarray(offsets, dtype=np.uint64))
+        self.rank, self.world, self.overlap = rank, world, bool(overlap)
+        a = b = None
+        if world > 1:
+            if ids is None:
+                raise ValueError("world > 1 needs two NCCL unique ids")
+            a, b = C.create_string_buffer(ids[0], 128), C.create_string_buffer(ids[1], 128)
+        h = C.c_void_p()
+        trainer._enter(edges_dev)
+        check(lib().ember_dist_create(trainer.ctx, rank, world, int(self.overlap), a, b, edges_dev.data_ptr(),
+                                      self.offsets.ctypes.data, C.byref(h)))
+        self.h = h
+        self.plan = make_rounds(trainer.p, world, overlap=self.overlap)
+        R = self.plan.rounds
+        steps, hand = np.zeros(R, np.uint32), np.zeros(R, np.uint32)
+        total = C.c_uint64(0)
+        check(lib().ember_dist_plan(trainer.p, world, rank, int(self.overlap), self.offsets.ctypes.data,
+                                    trainer.h.batch_size, steps.ctypes.data, hand.ctypes.data, C.byref(total)))
+        self.steps_per_round = [int(x) for x in steps]
+        self.handoff_step = [int(x) for x in hand]
+
+    def total_steps(self) -> int:
+        return sum(self.steps_per_round)
+
+    def init_embeddings(self, seed: int):
+        check(lib().ember_dist_init_embeddings(self.h, seed))
+
+    def run_steps(self, start: int, count: int, epoch: int) -> DistReport:
+        rep = DistReport()
+        check(lib().ember_dist_train_epoch(self.h, epoch, start, count, C.byref(rep)))
+        return rep
+
+    def train_epoch(self, epoch: int) -> DistReport:
+        return self.run_steps(0, 2 ** 64 - 1, epoch)
+
+    def synchronize(self):
+        check(lib().ember_dist_synchronize(self.h))
+
+    def loss(self) -> float:
+        v = C.c_float(0.0)
+        check(lib().ember_dist_loss(self.h, C.byref(v)))
+        return float(v.value)
+
+    def held(self) -> list[int]:
+        out = []
+        for x in range(self.tr.p):
+            th = C.c_void_p()
+            check(lib().ember_dist_tables(self.h, x, C.byref(th), None))
+            if th.value:
+                out.append(x)
+        return out
+
+    def partition_table(self, x: int):
+        """theta/acc of a partition this rank holds: host copies in on-disk coordinate order."""
+        from . import partition_size, rows_to_disk
+        th, ac = C.c_void_p(), C.c_void_p()
+        check(lib().ember_dist_tables(self.h, x, C.byref(th), C.byref(ac)))
+        if not th.value:
+            raise ValueError(f"partition {x} is not on this rank")
+        self.synchronize()
+        n = partition_size(self.tr.V, self.tr.p, x) * self.tr.h.dim
+        outs = []
+        for ptr in (th.value, ac.value):
+            a = np.empty(n, np.float32)
+            check(lib().ember_copy_to_host(self.tr.ctx, a.ctypes.data, ptr, 4 * n))
+            outs.append(rows_to_disk(a.reshape(-1, self.tr.h.dim), self.tr.h.kind))
+        return outs[0], outs[1]
+
+    def close(self):
+        if getattr(self, "h", None):
+            check(lib().ember_dist_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

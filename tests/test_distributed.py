@@ -122,14 +122,16 @@ def _worker(rank, world, port, out_dir, cfg=None):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     edges, off = _graph()
     be = _backend(edges)
-    tr = ed.DistributedTrainer(be, CFG["p"], off, CFG["b"], rank, world, relations=CFG["kind"] != "dot", dist=dist)
+    tr = ed.DistributedTrainer(be, CFG["p"], off, CFG["b"], rank, world, relations=CFG["kind"] != "dot", dist=dist,
+                               overlap=CFG.get("overlap", False))
     tr.init_embeddings(CFG["seed"])
     n = 0
     for ep in range(CFG["epochs"]):
         n += tr.train_epoch(ep)["edges"]
     held = sorted(be.held)
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), held=np.array(held), theta=be.theta, acc=be.acc,
-             rel_theta=be.rel_theta, rel_acc=be.rel_acc, edges=np.array([n]), hb=np.array([tr.handoff_bytes]))
+             rel_theta=be.rel_theta, rel_acc=be.rel_acc, edges=np.array([n]), hb=np.array([tr.handoff_bytes]),
+             early=np.array([tr.report.early_handoffs]), handoffs=np.array([tr.report.handoffs]))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -146,7 +148,7 @@ def _serial_replay_cfg(world):
     for x in range(CFG["p"]):
         be.init_partition(x, CFG["seed"])
     be.init_relations(CFG["seed"])
-    plan = ed.make_rounds(CFG["p"], world)
+    plan = ed.make_rounds(CFG["p"], world, overlap=CFG.get("overlap", False))
     n = 0
     for ep in range(CFG["epochs"]):
         for r in range(plan.rounds):
@@ -330,6 +332,39 @@ def test_seek_transfers_reach_the_round_layout():
         assert (held == plan.holder[r]).all()
 
 
+def test_two_rank_overlapped_schedule_bit_identical_to_serial_replay(tmp_path):
+    """The coset schedule (p=8 over 2 ranks) through the library's round loop: handoffs issued after
+    the departing pairs' buckets, mid-round, and every parameter still equals the serial replay."""
+    import torch.multiprocessing as mp
+    world, port = 2, _free_port()
+    cfg = dict(p=8, V=1600, epochs=2, overlap=True)
+    saved = dict(CFG)
+    try:
+        CFG.update(cfg)
+        mp.start_processes(_worker, args=(world, port, str(tmp_path), cfg), nprocs=world, join=True,
+                           start_method="spawn")
+        ref, n_ref, off = _serial_replay(world)
+        got = np.full_like(ref.theta, np.nan)
+        total, early, hand = 0, 0, 0
+        rel = []
+        for g in range(world):
+            z = np.load(tmp_path / f"rank{g}.npz")
+            total += int(z["edges"][0])
+            early += int(z["early"][0])
+            hand += int(z["handoffs"][0])
+            rel.append(z["rel_theta"])
+            for x in z["held"]:
+                o, sz = eb.partition_offset(CFG["V"], CFG["p"], int(x)), eb.partition_size(CFG["V"], CFG["p"], int(x))
+                got[o:o + sz] = z["theta"][o:o + sz]
+        assert total == n_ref
+        assert got.tobytes() == ref.theta.tobytes()
+        assert rel[0].tobytes() == rel[1].tobytes() == ref.rel_theta.tobytes()
+        assert hand > 0 and early > 0, "handoffs issued before the end of their round"
+    finally:
+        CFG.clear()
+        CFG.update(saved)
+
+
 def test_four_rank_dot_epochs_bit_identical_to_serial_replay(tmp_path):
     """Dot model (no relations, no per-step collective) over 4 ranks, p=8: the handoffs alone must
     reproduce the serial replay bit for bit."""
@@ -355,3 +390,41 @@ def test_four_rank_dot_epochs_bit_identical_to_serial_replay(tmp_path):
     finally:
         CFG.clear()
         CFG.update(saved)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,overlap", [("complex", True), ("complex", False), ("dot", True)])
+def test_native_driver_single_rank_matches_direct_training(kind, overlap):
+    """The all-native multi-GPU driver (ember_dist_*: C++ round loop, driver-owned partition slots,
+    NCCL paths idle at world 1) at world 1: two epochs leave every parameter bit-identical to the
+    same buckets trained through ember_train_epoch in schedule order."""
+    p, V, R = 4, 3000, 12
+    edges, split = eb.generate_graph(V, R, 20000, seed=5, train_frac=0.9, valid_frac=0.05)
+    bucketed, off = eb.bucket_edges(edges[split == 0], V, p)
+    dev = torch.from_numpy(bucketed.view(np.int32)).cuda()
+    h = eb.Hyper(kind=kind, dim=32, batch_size=300, num_negatives=64, neg_seed=3, engine="tc")
+    tr = eb.Trainer(h, V, R, p, device=0, allocate=False)
+    D = ed.NativeDistributed(tr, dev, off, 0, 1, overlap=overlap)
+    D.init_embeddings(11)
+    for ep in range(2):
+        rep = D.train_epoch(ep)
+        assert rep.edges == int(off[-1]) and rep.moved_partitions == 0
+    assert np.isfinite(D.loss())
+    got = {x: D.partition_table(x) for x in D.held()}
+    assert sorted(got) == list(range(p))
+    rel = tr.relation_table() if kind != "dot" else None
+    D.close()
+    ref = eb.Trainer(h, V, R, p, device=0)
+    ref.init_embeddings(11)
+    seq = np.stack([D.plan.order // p, D.plan.order % p], 1)
+    for ep in range(2):
+        ref.train_epoch(dev, off, seq, ep)
+    th_ref, ac_ref = ref.node_table()
+    for x in range(p):
+        o, n = eb.partition_offset(V, p, x), eb.partition_size(V, p, x)
+        assert got[x][0].tobytes() == th_ref[o:o + n].tobytes(), f"partition {x}"
+        assert got[x][1].tobytes() == ac_ref[o:o + n].tobytes()
+    if rel is not None:
+        assert rel[0].tobytes() == ref.relation_table()[0].tobytes()
+    tr.close()
+    ref.close()
