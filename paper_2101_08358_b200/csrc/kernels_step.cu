@@ -459,7 +459,7 @@ __device__ __forceinline__ Quad quad_of(const float4& v) {
 }
 
 struct EdgeMeta {
-    uint32_t s, t, ps, pt, pr;
+    uint32_t s, r, t, ps, pt, pr;
     uint32_t uq;  // bit 0: source row unique, bit 1: destination row unique
     float gd, gs;
     float lterm;  // the edge's loss term (lse_dst - f) + (lse_src - f)
@@ -483,9 +483,11 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
     float4* my = cpbuf + (size_t)wib * 2 * CP_ROLES * 32 + lane;
     const uint32_t nq = d / 4;
     const bool ql = lane < nq;
-    auto issue = [&](uint32_t e, int st, EdgeMeta& m) {
+    // An edge's indices, ranks, flags and scalars are loaded one edge ahead of its row copies, so
+    // the copies of edge e + nw are issued without waiting on those dependent loads.
+    auto load_meta = [&](uint32_t e, EdgeMeta& m) {
         m.s = edges[3 * e];
-        const uint32_t r = edges[3 * e + 1];
+        m.r = edges[3 * e + 1];
         m.t = edges[3 * e + 2];
         m.ps = rank[e];
         m.pt = rank[nb + e];
@@ -498,11 +500,13 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
             m.lterm = 0.f;
             if (lane == 0) m.lterm = (lse[e] - f) + (lse[(uint64_t)nb + e] - f);  // same terms as k_loss
         }
+    };
+    auto issue = [&](uint32_t e, int st, const EdgeMeta& m) {
         if (ql) {
             float4* b = my + (size_t)st * CP_ROLES * 32;
             cp_quad(b + 0 * 32, node_row(pi, m.s, d), lane);
             cp_quad(b + 1 * 32, node_row(pj, m.t, d), lane);
-            if (kind != EMBER_DOT) cp_quad(b + 2 * 32, rel + (uint64_t)r * d, lane);
+            if (kind != EMBER_DOT) cp_quad(b + 2 * 32, rel + (uint64_t)m.r * d, lane);
             if (m.uq & 1u) cp_quad(b + 3 * 32, pi.acc + (uint64_t)(m.s - pi.first) * d, lane);
             if (m.uq & 2u) cp_quad(b + 4 * 32, pj.acc + (uint64_t)(m.t - pj.first) * d, lane);
             cp_dA_quad(b + 5 * 32, dA, dcap, 0, e, d, lane);
@@ -510,9 +514,14 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
         }
         cp_commit();
     };
-    EdgeMeta cur{}, nxt{};
-    if (gw < nb) issue(gw, 0, cur);
-    else cp_commit();
+    EdgeMeta cur{}, nxt{}, nn{};
+    if (gw < nb) {
+        load_meta(gw, cur);
+        issue(gw, 0, cur);
+    } else {
+        cp_commit();
+    }
+    if (gw + nw < nb) load_meta(gw + nw, nxt);
     uint32_t it = 0;
     double lacc = 0.0;  // lane 0: this warp's loss terms, in its (fixed) edge order
     for (uint32_t e = gw; e < nb; e += nw, ++it) {
@@ -521,6 +530,7 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
         const uint32_t en = e + nw;
         if (en < nb) issue(en, st ^ 1, nxt);
         else cp_commit();
+        if (en + nw < nb) load_meta(en + nw, nn);  // consumed next iteration
         cp_wait<1>();  // this edge's copies (this lane's own) have landed
         if (ql) {
             const float4* b = my + (size_t)st * CP_ROLES * 32;
@@ -573,6 +583,7 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
             if (kind != EMBER_DOT) store_quad(grows + (uint64_t)cur.pr * d, lane, oR);
         }
         cur = nxt;
+        nxt = nn;
     }
     cp_wait<0>();
     // the loss (replaces k_loss): per-warp partials in warp order, summed by the last warp to finish
@@ -1230,9 +1241,9 @@ void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, c
                           bool packed, const uint32_t* negs) {
     if (packed) {
         const uint32_t rows_pad = (uint32_t)Engine::pad_rows(nb);  // a multiple of GP_ROWS
+        const uint32_t row_ctas = rows_pad / GP_ROWS, neg_ctas = (2 * E.n_pad + GP_WARPS - 1) / GP_WARPS;
         const size_t sm = (size_t)4 * E.CB * GP_ROWS * 16 + (size_t)GP_WARPS * 2 * E.KP * sizeof(float);
         opt_in_smem((const void*)k_gather_pack, sm, E.device);
-        const uint32_t row_ctas = rows_pad / GP_ROWS, neg_ctas = (2 * E.n_pad + GP_WARPS - 1) / GP_WARPS;
         launch_pdl(k_gather_pack, dim3(row_ctas + neg_ctas), dim3(32 * GP_WARPS), sm, E.stream, edges, nb, pi, pj,
                    E.rel_theta, E.m.kind, E.dim, E.CB, (uint32_t)E.b_cap, E.s.Apk, E.s.fpos, row_ctas,
                    negs, E.nt, (uint32_t)E.n_pad, E.s.Npk);
