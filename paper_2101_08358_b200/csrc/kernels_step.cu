@@ -307,16 +307,6 @@ __global__ void k_sample_keys(const uint32_t* __restrict__ edges, uint32_t nb, u
     vals[i] = i;
 }
 
-// rank[slot] = sorted position; uniq[slot] = the slot's key occurs once among the n slots.
-__global__ void k_rank(const uint32_t* __restrict__ vals_sorted, const uint32_t* __restrict__ keys_sorted, uint32_t n,
-                       uint32_t* __restrict__ rank, uint8_t* __restrict__ uniq) {
-    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    const uint32_t slot = vals_sorted[p], k = keys_sorted[p];
-    rank[slot] = p;
-    uniq[slot] = (p == 0 || keys_sorted[p - 1] != k) && (p + 1 == n || keys_sorted[p + 1] != k);
-}
-
 // The sorted position p holds a key that occurs exactly once among the batch's gradient slots.
 __device__ __forceinline__ bool slot_unique(const uint32_t* __restrict__ ks, uint32_t n, uint32_t p) {
     const uint32_t k = ks[p];
@@ -658,7 +648,6 @@ __device__ __forceinline__ float adagrad_elem(float& th, float& ac, float g, flo
 struct SegArgs {
     const uint32_t* ukeys;
     const uint32_t* offsets;
-    const uint32_t* counts;
     const uint32_t* nruns;
     uint32_t* nunique;   // [2] written: node uniques, relation uniques
     uint32_t* longs;     // [0] long segments, [1] chunk slots; then u, base, nch per long (3 x cap)
@@ -822,7 +811,7 @@ __global__ void __launch_bounds__(256, 4) k_segments(SegArgs a) {
         a.nunique[0] = u + 1;
         a.nunique[1] = nr - (u + 1);
     }
-    const uint32_t off = a.offsets[u], cnt = a.counts[u];
+    const uint32_t off = a.offsets[u], cnt = a.offsets[u + 1] - off;
     if (cnt == 1 && key < a.ks.node_range && a.vals_sorted[off] < a.direct_hi) return;  // applied already
     if (cnt > LONG_SEG) {  // reserve chunk slots for the long path
         const uint32_t nch = (cnt + LONG_CHUNK - 1) / LONG_CHUNK;
@@ -873,6 +862,10 @@ struct SegKey {
     SegTarget t;
 };
 
+struct SegMeta {
+    uint32_t key, off, cnt, next_key;
+};
+
 __global__ void __launch_bounds__(256, 4) k_segments_pipe(SegArgs a) {
     griddep_wait();
     extern __shared__ float4 sst[];  // [warps][2 halves][2 stages][2 roles][2 column blocks][16 lanes]
@@ -883,17 +876,25 @@ __global__ void __launch_bounds__(256, 4) k_segments_pipe(SegArgs a) {
     const uint32_t nr = *a.nruns, d4 = a.d / 4;
     float4* my = sst + (size_t)(wib * 2 + half) * 2 * 2 * 2 * SEG_LANES + hl;
     auto slot = [&](int st, int role, int cb) { return my + (size_t)((st * 2 + role) * 2 + cb) * SEG_LANES; };
-    auto issue = [&](uint32_t u, int st, SegKey& k) {
+    // A key's (key, offset, count) are loaded one key ahead of its parameter copies, so the copies
+    // of key u + nh are issued without waiting on those loads.
+    auto load_meta = [&](uint32_t u, SegMeta& m) {
+        m.key = a.ukeys[u];
+        m.off = a.offsets[u];
+        m.cnt = a.offsets[u + 1] - m.off;
+        m.next_key = u + 1 < nr ? a.ukeys[u + 1] : 0xffffffffu;
+    };
+    auto issue = [&](uint32_t u, int st, const SegMeta& m, SegKey& k) {
         k.u = u;
         k.active = false;
         if (u < nr) {
-            const uint32_t key = a.ukeys[u];
-            if (hl == 0 && key < a.ks.node_range && (u + 1 == nr || a.ukeys[u + 1] >= a.ks.node_range)) {
+            const uint32_t key = m.key;
+            if (hl == 0 && key < a.ks.node_range && (u + 1 == nr || m.next_key >= a.ks.node_range)) {
                 a.nunique[0] = u + 1;
                 a.nunique[1] = nr - (u + 1);
             }
-            k.off = a.offsets[u];
-            k.cnt = a.counts[u];
+            k.off = m.off;
+            k.cnt = m.cnt;
             const bool done = k.cnt == 1 && key < a.ks.node_range && a.vals_sorted[k.off] < a.direct_hi;
             if (!done && k.cnt > LONG_SEG) {  // reserve chunk slots for the long path
                 const uint32_t nch = (k.cnt + LONG_CHUNK - 1) / LONG_CHUNK;
@@ -925,10 +926,14 @@ __global__ void __launch_bounds__(256, 4) k_segments_pipe(SegArgs a) {
         cp_commit();
     };
     SegKey cur, nxt;
-    issue(gh, 0, cur);
+    SegMeta mn{}, mnn{};
+    if (gh < nr) load_meta(gh, mn);
+    issue(gh, 0, mn, cur);
+    if (gh + nh < nr) load_meta(gh + nh, mn);
     for (uint32_t u = gh, it = 0; u < nr; u += nh, ++it) {
         const int st = it & 1;
-        issue(u + nh, st ^ 1, nxt);
+        issue(u + nh, st ^ 1, mn, nxt);
+        if (u + 2 * nh < nr) load_meta(u + 2 * nh, mnn);  // consumed next iteration
         cp_wait<1>();
         if (cur.active) {
             const bool app = seg_applies(a, cur.t);
@@ -944,6 +949,7 @@ __global__ void __launch_bounds__(256, 4) k_segments_pipe(SegArgs a) {
             }
         }
         cur = nxt;
+        mn = mnn;
     }
     cp_wait<0>();
 }
@@ -1014,7 +1020,7 @@ __global__ void k_long_partial(SegArgs a) {
     for (uint32_t sl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < n_slots; sl += nw) {
         const uint32_t* rec = a.longs + 2 + 3 * a.owner[sl];
         const uint32_t u = rec[0], c = sl - rec[1];
-        const uint32_t r0 = c * LONG_CHUNK, cnt = min(LONG_CHUNK, a.counts[u] - r0);
+        const uint32_t r0 = c * LONG_CHUNK, cnt = min(LONG_CHUNK, a.offsets[u + 1] - a.offsets[u] - r0);
         const float* base = a.rows + ((uint64_t)a.offsets[u] + r0) * a.d;
         for (uint32_t c0 = 0; c0 < d4; c0 += 32) {  // warp-uniform trip count (shuffles below)
             const uint32_t c4 = c0 + hl, c4b = c4 + 16;
@@ -1284,10 +1290,6 @@ void launch_sample_keys(const Engine& E, const uint32_t* edges, uint32_t nb, uin
     EMBER_LAUNCHED(E);
 }
 
-void launch_rank(const Engine& E, uint32_t n) {
-    k_rank<<<(n + 255) / 256, 256, 0, E.side>>>(E.s.vals_sorted, E.s.keys_sorted, n, E.s.rank, E.s.uniq);
-    EMBER_LAUNCHED(E);
-}
 
 void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj) {
     const uint32_t warps = 8;
@@ -1331,7 +1333,6 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
     SegArgs a{};
     a.ukeys = E.s.ukeys;
     a.offsets = E.s.offsets;
-    a.counts = E.s.counts;
     a.nruns = E.s.nruns;
     a.nunique = E.s.nunique;
     a.longs = E.s.longs;
