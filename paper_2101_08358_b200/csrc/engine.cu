@@ -227,8 +227,8 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     s.rank = dalloc<uint32_t>(cap_rows);
     s.uniq = dalloc<uint8_t>(cap_rows);
     s.ukeys = dalloc<uint32_t>(cap_rows);
-    s.counts = dalloc<uint32_t>(cap_rows);
-    s.offsets = dalloc<uint32_t>(cap_rows);
+    s.counts = dalloc<uint32_t>(cap_rows + 1);
+    s.offsets = dalloc<uint32_t>(cap_rows + 1);  // offsets[nruns] = n closes the last run
     s.nruns = dalloc<uint32_t>(1);
     s.nunique = dalloc<uint32_t>(2);
     // at most cap_rows / LONG_SEG long segments, each with <= len / LONG_CHUNK + 1 chunks
@@ -256,7 +256,7 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
                                                (int)cap_rows, 0, 32, side));
     EMBER_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, t2, s.keys_sorted, s.ukeys, s.counts, s.nruns,
                                                   (int)cap_rows, side));
-    EMBER_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t3, s.counts, s.offsets, (int)cap_rows, side));
+    EMBER_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t3, s.counts, s.offsets, (int)cap_rows + 1, side));
     s.cub_bytes = std::max(t1, std::max(t2, t3));
     s.cub_tmp = dalloc<uint8_t>(s.cub_bytes);
     if (tc_engine()) {
@@ -343,11 +343,11 @@ void Engine::sort_slots(uint32_t nb, const KeySpace& ks) {
                                                0, (int)ks.bits, side));
     bytes = s.cub_bytes;
     // (the scan below runs over n entries; the runs past nruns must read as zero, not stale memory)
-    EMBER_CUDA(cudaMemsetAsync(s.counts, 0, (size_t)n * sizeof(uint32_t), side));
+    EMBER_CUDA(cudaMemsetAsync(s.counts, 0, (size_t)(n + 1) * sizeof(uint32_t), side));
     EMBER_CUDA(cub::DeviceRunLengthEncode::Encode(s.cub_tmp, bytes, s.keys_sorted, s.ukeys, s.counts, s.nruns, (int)n,
                                                   side));
     bytes = s.cub_bytes;
-    EMBER_CUDA(cub::DeviceScan::ExclusiveSum(s.cub_tmp, bytes, s.counts, s.offsets, (int)n, side));
+    EMBER_CUDA(cub::DeviceScan::ExclusiveSum(s.cub_tmp, bytes, s.counts, s.offsets, (int)n + 1, side));
     lib_calls += 3;
     launch_rank(*this, n);
     EMBER_CUDA(cudaEventRecord(ev_sorted, side));
