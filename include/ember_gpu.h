@@ -188,6 +188,13 @@ int ember_adagrad_apply(ember_ctx* ctx, const uint32_t* ids_dev, const float* ro
  * side-`side` negatives (debug/parity; out_dev: rows x n_t). */
 int ember_debug_scores(ember_ctx* ctx, const uint32_t* edges_dev, uint32_t nb, uint32_t i, uint32_t j,
                        const uint32_t* negs_dev, int side, uint32_t rows, float* out_dev);
+/* The step's (key, slot) sort on n <= 3 batch_size + n_neg keys of `bits` bits (debug/parity):
+ * keys_sorted / vals_sorted (n), rank (n: slot -> sorted position), uniq (n bytes: the slot's key
+ * occurs once), ukeys (n), offsets (n + 1: run u = [offsets[u], offsets[u + 1])), nruns (1); all
+ * device buffers, written on the context stream. */
+int ember_debug_sort_slots(ember_ctx* ctx, const uint32_t* keys_dev, uint32_t n, uint32_t bits, uint32_t* keys_sorted_dev,
+                           uint32_t* vals_sorted_dev, uint32_t* rank_dev, uint8_t* uniq_dev, uint32_t* ukeys_dev,
+                           uint32_t* offsets_dev, uint32_t* nruns_dev);
 
 /* ---- link-prediction eval, unfiltered sampled negatives ------------------ */
 int ember_eval_ranks(ember_ctx* ctx, const uint32_t* test_edges_dev, uint32_t n_test, const uint32_t* train_edges_dev,

@@ -386,6 +386,24 @@ class Trainer:
         self.synchronize()
         return out.cpu().numpy()
 
+    def debug_sort_slots(self, keys, bits):
+        """The step's (key, slot) sort + runs on device keys (uint32 as int32): dict of numpy arrays."""
+        t = self.torch
+        n = int(keys.numel())
+        i32 = dict(dtype=t.int32, device=self.dev)
+        out = {k: t.empty(n, **i32) for k in ("keys_sorted", "vals_sorted", "rank", "ukeys")}
+        out["uniq"] = t.empty(n, dtype=t.uint8, device=self.dev)
+        out["offsets"] = t.empty(n + 1, **i32)
+        out["nruns"] = t.empty(1, **i32)
+        self._enter(keys, *out.values())
+        check(lib().ember_debug_sort_slots(self.ctx, _ptr(keys), n, int(bits), *(_ptr(out[k]) for k in (
+            "keys_sorted", "vals_sorted", "rank", "uniq", "ukeys", "offsets", "nruns"))))
+        self.synchronize()
+        res = {k: v.cpu().numpy() for k, v in out.items()}
+        for k in ("keys_sorted", "vals_sorted", "rank", "ukeys", "offsets", "nruns"):
+            res[k] = res[k].view(np.uint32)
+        return res
+
     def eval_ranks(self, test_edges, train_edges, n_eval=1000, alpha_eval=0.5, block=1000, eval_seed=7):
         t = self.torch
         n = int(test_edges.shape[0])

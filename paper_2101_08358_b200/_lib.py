@@ -74,6 +74,7 @@ def _declare(L):
         "ember_adagrad_apply": (C.c_int, [vp, vp, vp, u32, u32, u32, i32]),
         "ember_gather": (C.c_int, [vp, vp, u32, u32, u32, i32, vp, vp]),
         "ember_debug_scores": (C.c_int, [vp, vp, u32, u32, u32, vp, i32, u32, vp]),
+        "ember_debug_sort_slots": (C.c_int, [vp, vp, u32, u32, vp, vp, vp, vp, vp, vp, vp]),
         "ember_eval_ranks": (C.c_int, [vp, vp, u32, vp, u64, u32, f32, u32, u64, vp]),
         "ember_eval_ranks_filtered": (C.c_int, [vp, vp, u32, vp, u64, vp]),
         "ember_make_plan": (C.c_int, [i32, u32, u32, u64, vp, C.POINTER(u64), vp, C.POINTER(u32), vp, vp]),

@@ -510,6 +510,34 @@ int ember_debug_scores(ember_ctx* ctx, const uint32_t* edges, uint32_t nb, uint3
     });
 }
 
+int ember_debug_sort_slots(ember_ctx* ctx, const uint32_t* keys, uint32_t n, uint32_t bits, uint32_t* keys_sorted,
+                           uint32_t* vals_sorted, uint32_t* rank, uint8_t* uniq, uint32_t* ukeys, uint32_t* offsets,
+                           uint32_t* nruns) {
+    return guarded([&] {
+        Engine& E = eng(ctx);
+        if (n > E.cap_rows) throw ConfigError("n exceeds the context's gradient slots (3 batch_size + n_neg)");
+        if (bits < 1 || bits > 32) throw ConfigError("bits must be in [1, 32]");
+        if (n) need(keys, "keys_dev");
+        const size_t b4 = (size_t)n * sizeof(uint32_t);
+        EMBER_CUDA(cudaMemcpyAsync(E.s.keys, keys, b4, cudaMemcpyDeviceToDevice, E.stream));
+        EMBER_CUDA(cudaEventRecord(E.ev_fork, E.stream));
+        EMBER_CUDA(cudaStreamWaitEvent(E.side, E.ev_fork, 0));
+        launch_slot_sort(E, n, bits);
+        EMBER_CUDA(cudaEventRecord(E.ev_sorted, E.side));
+        EMBER_CUDA(cudaStreamWaitEvent(E.stream, E.ev_sorted, 0));
+        auto out = [&](void* dst, const void* src, size_t bytes) {
+            if (dst && bytes) EMBER_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, E.stream));
+        };
+        out(keys_sorted, E.s.keys_sorted, b4);
+        out(vals_sorted, E.s.vals_sorted, b4);
+        out(rank, E.s.rank, b4);
+        out(uniq, E.s.uniq, n);
+        out(ukeys, E.s.ukeys, b4);
+        out(offsets, E.s.offsets, b4 + sizeof(uint32_t));
+        out(nruns, E.s.nruns, sizeof(uint32_t));
+    });
+}
+
 int ember_eval_ranks(ember_ctx* ctx, const uint32_t* test, uint32_t n_test, const uint32_t* train, uint64_t n_train,
                      uint32_t n_eval, float alpha_eval, uint32_t block, uint64_t eval_seed, uint32_t* ranks) {
     return guarded([&] {

@@ -4,13 +4,12 @@
 // train_epoch_sync semantics, bound = 1). Per batch:
 //   step stream:   sample + slot keys -+-> gather+adjust -> contraction (scores, LSE, dA, dN) -> chain rule
 //                                      |                              (join) ^           -> loss
-//   helper stream:                     +-> radix sort -> runs -> rank -------+
+//   helper stream:                     +-> (key, slot) sort -> runs -------+
 //   then one segmented sum over the sorted gradient rows -> Adagrad (relations and nodes;
 //   relations synchronously, after an NCCL all-reduce when world > 1).
 // The helper stream only overlaps work that the step stream would otherwise serialise; the
 // result is identical to a single-stream order. Stage 2/4 transfers of the paper's pipeline
 // vanish: parameters stay in HBM.
-#include <cub/cub.cuh>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -227,8 +226,14 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     s.rank = dalloc<uint32_t>(cap_rows);
     s.uniq = dalloc<uint8_t>(cap_rows);
     s.ukeys = dalloc<uint32_t>(cap_rows);
-    s.counts = dalloc<uint32_t>(cap_rows + 1);
     s.offsets = dalloc<uint32_t>(cap_rows + 1);  // offsets[nruns] = n closes the last run
+    for (int k = 0; k < 2; ++k) {
+        s.sort_keys[k] = dalloc<uint32_t>(cap_rows);
+        s.sort_vals[k] = dalloc<uint32_t>(cap_rows);
+    }
+    s.sort_hist = dalloc<uint32_t>(slot_sort_scratch_words(cap_rows));
+    s.sort_status = dalloc<unsigned long long>(slot_sort_tiles(cap_rows));
+    s.sort_ctr = dalloc<uint32_t>(1);
     s.nruns = dalloc<uint32_t>(1);
     s.nunique = dalloc<uint32_t>(2);
     // at most cap_rows / LONG_SEG long segments, each with <= len / LONG_CHUNK + 1 chunks
@@ -251,14 +256,6 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
         s.Apk = dalloc<uint16_t>((size_t)2 * 2 * CB * b_cap * 8);
         s.Npk = dalloc<uint16_t>((size_t)2 * 2 * CB * n_pad * 8);
     }
-    size_t t1 = 0, t2 = 0, t3 = 0;
-    EMBER_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t1, s.keys, s.keys_sorted, s.vals, s.vals_sorted,
-                                               (int)cap_rows, 0, 32, side));
-    EMBER_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, t2, s.keys_sorted, s.ukeys, s.counts, s.nruns,
-                                                  (int)cap_rows, side));
-    EMBER_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t3, s.counts, s.offsets, (int)cap_rows + 1, side));
-    s.cub_bytes = std::max(t1, std::max(t2, t3));
-    s.cub_tmp = dalloc<uint8_t>(s.cub_bytes);
     if (tc_engine()) {
         if (wide_path) wide_setup(*this);
         else tc_setup(*this);
@@ -275,7 +272,8 @@ Engine::~Engine() {
     void* ptrs[] = {s.batch, s.A,         s.N,      s.Apk,       s.Npk,     s.fpos,       s.lse,    s.g0,
                     s.S,     s.dA,        s.dN_part, s.grows,    s.loss,    s.loss_part,  s.loss_done,  s.bad_batch,
                     s.nunique, s.long_partial, s.rel_dense, s.negs, s.keys, s.keys_sorted, s.vals, s.vals_sorted,
-                    s.rank, s.ukeys, s.counts, s.offsets, s.nruns, s.longs, s.long_owner, s.uniq, s.cub_tmp};
+                    s.rank, s.ukeys, s.offsets, s.nruns, s.longs, s.long_owner, s.uniq, s.sort_keys[0],
+                    s.sort_keys[1], s.sort_vals[0], s.sort_vals[1], s.sort_hist, s.sort_status, s.sort_ctr};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (void* p : owned) cudaFree(p);
@@ -338,18 +336,7 @@ void Engine::sort_keys(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t 
 
 void Engine::sort_slots(uint32_t nb, const KeySpace& ks) {
     const uint32_t n = slots(nb);
-    size_t bytes = s.cub_bytes;
-    EMBER_CUDA(cub::DeviceRadixSort::SortPairs(s.cub_tmp, bytes, s.keys, s.keys_sorted, s.vals, s.vals_sorted, (int)n,
-                                               0, (int)ks.bits, side));
-    bytes = s.cub_bytes;
-    // (the scan below runs over n entries; the runs past nruns must read as zero, not stale memory)
-    EMBER_CUDA(cudaMemsetAsync(s.counts, 0, (size_t)(n + 1) * sizeof(uint32_t), side));
-    EMBER_CUDA(cub::DeviceRunLengthEncode::Encode(s.cub_tmp, bytes, s.keys_sorted, s.ukeys, s.counts, s.nruns, (int)n,
-                                                  side));
-    bytes = s.cub_bytes;
-    EMBER_CUDA(cub::DeviceScan::ExclusiveSum(s.cub_tmp, bytes, s.counts, s.offsets, (int)n + 1, side));
-    lib_calls += 3;
-    launch_rank(*this, n);
+    launch_slot_sort(*this, slots(nb), ks.bits);
     EMBER_CUDA(cudaEventRecord(ev_sorted, side));
     sorted_pending = true;
 }

@@ -109,15 +109,18 @@ struct Scratch {
     uint32_t* rank = nullptr;
     uint8_t* uniq = nullptr;      // slot -> its key occurs once among the batch's slots
     uint32_t* ukeys = nullptr;
-    uint32_t* counts = nullptr;
-    uint32_t* offsets = nullptr;
+    uint32_t* offsets = nullptr;  // [runs + 1]: offsets[nruns] = n
     uint32_t* nruns = nullptr;    // [1] unique keys (RLE)
     uint32_t* nunique = nullptr;  // [2] unique node keys, unique relation keys
     uint32_t* longs = nullptr;        // [2 + 3 * cap]: long segments, chunk slots, then (u, base, nch)
     uint32_t* long_owner = nullptr;   // chunk slot -> long segment
     float* long_partial = nullptr;    // chunk slot -> partial row
-    void* cub_tmp = nullptr;
-    size_t cub_bytes = 0;
+    // slot sort (sort.cu): ping-pong key/value buffers, per-tile digit histograms, run-scan state
+    uint32_t* sort_keys[2] = {nullptr, nullptr};
+    uint32_t* sort_vals[2] = {nullptr, nullptr};
+    uint32_t* sort_hist = nullptr;
+    unsigned long long* sort_status = nullptr;
+    uint32_t* sort_ctr = nullptr;
     float* rel_dense = nullptr;  // [R][dim] relation gradient summed over ranks (world > 1)
 };
 
@@ -174,7 +177,7 @@ struct Engine {
     bool prof_on = false;
     std::vector<std::pair<int, cudaEvent_t>> prof_events;
     mutable uint64_t launches = 0;
-    mutable uint64_t lib_calls = 0;  // CUB device-wide calls (library kernels, counted separately)
+    mutable uint64_t lib_calls = 0;  // library kernel calls on the step (none since the hand-written slot sort)
     void mark(int phase);
 
     Engine(int device, const ember_model_desc& m, const ember_graph_desc& g, cudaStream_t stream);
@@ -272,7 +275,10 @@ void launch_keys(const Engine& E, const uint32_t* edges, uint32_t nb, const uint
 // the training step's sample_negatives + gradient-slot keys, one kernel on the step stream
 void launch_sample_keys(const Engine& E, const uint32_t* edges, uint32_t nb, uint64_t base, const uint32_t* bucket,
                         uint64_t bucket_n, const PartView& src, const PartView& dst, const KeySpace& ks);
-void launch_rank(const Engine& E, uint32_t n);
+// the (key, slot) sort of s.keys and its runs, on the helper stream (sort.cu)
+void launch_slot_sort(const Engine& E, uint32_t n, uint32_t bits);
+size_t slot_sort_scratch_words(uint32_t cap);
+uint32_t slot_sort_tiles(uint32_t cap);
 void launch_contract_simt(Engine& E, uint32_t nb);
 void launch_contract_tc(Engine& E, uint32_t nb);
 void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj);

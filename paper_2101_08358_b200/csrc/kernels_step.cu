@@ -6,7 +6,7 @@
 //                     written as fp32 (SIMT engine) or straight into the tensor-core engine's
 //                     bf16 hi|lo operand layout
 //   k_gather_negs     negative rows, fp32 or packed
-//   k_keys / k_rank   gradient-slot keys for the (key, slot) sort and its inverse permutation
+//   k_keys            gradient-slot keys for the (key, slot) sort (sort.cu)
 //   k_chain_rule      chain rule back through adjust, rows written in sorted order
 //   k_loss            deterministic loss reduction (fixed-order partials, last block finishes)
 //   k_segments, k_long_partial, k_long_final
@@ -305,16 +305,6 @@ __global__ void k_sample_keys(const uint32_t* __restrict__ edges, uint32_t nb, u
     }
     keys[i] = k;
     vals[i] = i;
-}
-
-// rank[slot] = sorted position; uniq[slot] = the slot's key occurs once among the n slots.
-__global__ void k_rank(const uint32_t* __restrict__ vals_sorted, const uint32_t* __restrict__ keys_sorted, uint32_t n,
-                       uint32_t* __restrict__ rank, uint8_t* __restrict__ uniq) {
-    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    const uint32_t slot = vals_sorted[p], k = keys_sorted[p];
-    rank[slot] = p;
-    uniq[slot] = (p == 0 || keys_sorted[p - 1] != k) && (p + 1 == n || keys_sorted[p + 1] != k);
 }
 
 // The sorted position p holds a key that occurs exactly once among the batch's gradient slots.
@@ -1300,11 +1290,6 @@ void launch_sample_keys(const Engine& E, const uint32_t* edges, uint32_t nb, uin
     EMBER_LAUNCHED(E);
 }
 
-
-void launch_rank(const Engine& E, uint32_t n) {
-    k_rank<<<(n + 255) / 256, 256, 0, E.side>>>(E.s.vals_sorted, E.s.keys_sorted, n, E.s.rank, E.s.uniq);
-    EMBER_LAUNCHED(E);
-}
 
 void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj) {
     const uint32_t warps = 8;
