@@ -180,10 +180,15 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
         EMBER_CUDA(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, pr && atoi(pr) == 0 ? least : greatest));
         own_stream = true;
     }
-    if (getenv("EMBER_SERIAL_SORT"))  // A/B switch: sort on the step stream (no overlap)
+    if (getenv("EMBER_SERIAL_SORT")) {  // A/B switch: sort on the step stream (no overlap)
         side = stream;
-    else
+    } else if (const char* sp = getenv("EMBER_SIDE_PRIORITY")) {  // A/B: 1 = the greatest priority
+        int least = 0, greatest = 0;
+        EMBER_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        EMBER_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, atoi(sp) ? greatest : least));
+    } else {
         EMBER_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    }
     EMBER_CUDA(cudaStreamCreateWithFlags(&io, cudaStreamNonBlocking));
     EMBER_CUDA(cudaStreamCreateWithFlags(&io_out, cudaStreamNonBlocking));
     for (int k = 0; k < 2; ++k) {

@@ -78,6 +78,17 @@ struct TcArgs {
     int early;        // tiles 0 .. early-1 of an item go to epilogue group 0 (tile_group)
     int diag;         // EMBER_TC_DIAG=1 (measurement only, wrong results): the epilogue skips its TMEM work
     unsigned long long* trace;  // debug timeline of CTA 0 (EMBER_TC_TRACE), nullptr normally
+    unsigned long long* cta_times;  // EMBER_TC_CTATIMES: per CTA (start, end) %globaltimer ns, nullptr normally
+    // Items go to CTAs in arrival order, not blockIdx order: a CTA that becomes resident late (its SM
+    // was still running a helper-stream kernel) takes the last of the grid-stride item sequences,
+    // which are the shorter ones when the items do not divide evenly. rank = atomicAdd - base.
+    uint32_t* arrive;
+    uint32_t arrive_base;
+    // dyn: after its first item a CTA claims the next from a counter (claim - claim_base + grid), so
+    // SMs that run faster take more items; the producer publishes each work's item to the other roles.
+    int dyn;
+    uint32_t* claim;
+    uint32_t claim_base;
 };
 
 // Debug timeline: (clock64, event << 32 | arg) records from CTA 0's producer, MMA issuer and one
@@ -102,7 +113,7 @@ __host__ __device__ constexpr size_t stage_bytes(int KP, int mode) {
 }
 __host__ __device__ constexpr size_t zbuf_bytes(int mode) { return mode == MODE_ROWS ? 4 * RES * 4 : 0; }
 __host__ __device__ constexpr size_t smem_total(int KP, int nstage, int mode) {
-    return 128 + res_bytes(KP) + nstage * stage_bytes(KP, mode) + zbuf_bytes(mode) + 256;
+    return 128 + res_bytes(KP) + nstage * stage_bytes(KP, mode) + zbuf_bytes(mode) + 512;  // bars: 53 x 8 B
 }
 constexpr size_t SMEM_LIMIT = 232448;
 inline int stages_for(int KP) {
@@ -124,8 +135,10 @@ enum {
     B_ACC_EMPTY = 3 + 2 * NSTAGE_MAX + 4 * NSP_MAX,  // consumer: P.T issuer
     B_Z_READY = 4 + 2 * NSTAGE_MAX + 4 * NSP_MAX,    // + 4: group 0's row sums of item i in zbuf[i % 4]
     B_ZB_FREE = 8 + 2 * NSTAGE_MAX + 4 * NSP_MAX,    // + 4: group 1 has read zbuf[i % 4]
-    B_TMEM_SLOT = 12 + 2 * NSTAGE_MAX + 4 * NSP_MAX,
+    B_TMEM_SLOT = 12 + 2 * NSTAGE_MAX + 4 * NSP_MAX,  // [0] TMEM base, [1] arrival rank
+    B_WORK = 13 + 2 * NSTAGE_MAX + 4 * NSP_MAX,       // + WORK_SLOTS: (work << 32 | item), by the producer
 };
+constexpr uint32_t WORK_SLOTS = 16;  // the producer runs at most ~3 works ahead of the slowest role
 
 struct Smem {
     uint8_t* res;   // the item's resident tile (TMA landing zone, copied to TMEM by tcgen05.cp)
@@ -264,6 +277,20 @@ __device__ __forceinline__ void epi_chunk(uint32_t tS, int c0, int k, const TcAr
     }
 }
 
+// The item of work `it` (published by the producer; items = no more work).
+__device__ __forceinline__ void work_publish(uint64_t* bars, uint32_t it, int item) {
+    volatile uint64_t* w = bars + B_WORK + (it % WORK_SLOTS);
+    *w = ((uint64_t)it << 32) | (uint32_t)item;
+}
+__device__ __forceinline__ int work_fetch(uint64_t* bars, uint32_t it) {
+    volatile uint64_t* w = bars + B_WORK + (it % WORK_SLOTS);
+    uint64_t v;
+    do {
+        v = *w;
+    } while ((uint32_t)(v >> 32) != it);
+    return (int)(uint32_t)v;
+}
+
 // Epilogue group of an item's streamed tile k. Group 1 also drains every item's accumulator
 // (the tail), which delays its next tile; so the first tiles of each item (0, 1, 2) go to group 0
 // and the rest alternate (odd -> group 1): group 1's first tile of the next item comes ~3 tiles
@@ -310,6 +337,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tc::fence_mbar_init();
         tc::tmap_prefetch(&mapR);
         tc::tmap_prefetch(&mapT);
+        tslot[1] = atomicAdd(g.arrive, 1u) - g.arrive_base;  // this CTA's rank in arrival order
+        for (uint32_t w = 0; w < WORK_SLOTS; ++w) bars[B_WORK + w] = ~0ull;  // no work published yet
     }
     if (warp == 1) tc::tmem_alloc(tslot, TCOLS);
     tc::fence_before();
@@ -319,14 +348,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // column 0: the MMA issuer uses compile-time TMEM addresses.
     const uint32_t tbase = *tslot;
     if (tbase != 0) __trap();
+    const int cta = (int)tslot[1];
     griddep_wait();  // set-up above overlaps the previous kernel's tail (PDL)
+    if (g.cta_times && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g.cta_times[2 * blockIdx.x] = t;
+    }
 
     if (warp == 0) {
         if (lane == 0) {  // ------------------------------------------------------ TMA producer
             const uint32_t bytesR = (uint32_t)res_bytes(KP);
             const uint32_t bytesT = (uint32_t)(TILE * KP * 4 + trailer_bytes(MODE));  // TMA'd bytes per tile
             uint32_t it = 0, gr = 0;  // gr: streamed-tile ring slots used
-            for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+            for (int item = cta;; ++it) {
+                if (it > 0)
+                    item = g.dyn ? (int)(atomicAdd(g.claim, 1u) - g.claim_base) + (int)gridDim.x
+                                 : item + (int)gridDim.x;
+                work_publish(bars, it, min(item, items));
+                if (item >= items) break;
                 const Item I = item_geo<MODE>(g, item);
                 // resident tile: its previous occupant has been copied into TMEM (RES_EMPTY)
                 tc::mbar_wait(&bars[B_RES_EMPTY], (it & 1) ^ 1);
@@ -353,7 +393,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // over two issuing warps lets each warp's barrier waits hide behind the other's issue.
         const uint32_t id_s = tc::idesc_bf16(128, TILE, false, false);
         uint32_t it = 0, gt = 0;  // gt: streamed tiles (S/P buffers and ring slots)
-        for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        for (;; ++it) {
+            const int item = work_fetch(bars, it);
+            if (item >= items) break;
             const Item I = item_geo<MODE>(g, item);
             {  // resident operand smem -> TMEM, in this warp's MMA stream after the previous item's last S
                 tc::mbar_wait_warp(&bars[B_RES_FULL], it & 1);
@@ -398,7 +440,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     } else if (warp == 2) {  // ----------------------------------------------------- P.T issuer
         const uint32_t id_a = tc::idesc_bf16(128, KP, false, true);
         uint32_t it = 0, gt = 0;
-        for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        for (;; ++it) {
+            const int item = work_fetch(bars, it);
+            if (item >= items) break;
             const Item I = item_geo<MODE>(g, item);
             for (int k = 0; k < I.T; ++k) {  // acc += P_k . T_k   (P from TMEM, T MN-major from smem)
                 const uint32_t q = gt + k;
@@ -439,7 +483,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // also does every item tail, so group 0 moves straight on to the next item's first tiles.
         uint32_t it = 0, gt = 0;
         uint32_t sphase = 0;  // bit b: parity of this group's next wait on S_FULL[G][b]
-        for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        for (;; ++it) {
+            const int item = work_fetch(bars, it);
+            if (item >= items) break;
             const Item I = item_geo<MODE>(g, item);
             const int row = I.r0 + r;
             float fp = 0.f, z = 0.f;
@@ -541,6 +587,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc::fence_before();
     __syncthreads();
     if (warp == 1) tc::tmem_dealloc(tbase, TCOLS);
+    if (g.cta_times && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g.cta_times[2 * blockIdx.x + 1] = t;
+    }
 }
 
 // Exact two-pass recomputation (fp32, CUDA cores) of the rows k_tc<MODE_ROWS> flagged because
@@ -716,6 +767,11 @@ struct TcState {
     float zmax = 1e30f;  // sum exp(S - f_pos) above this: exact recompute (fp32 and the P.N sums stay finite)
     int max_grid = 0;  // test hook (EMBER_TC_MAXGRID): several items per CTA at small sizes
     unsigned long long* trace = nullptr;  // EMBER_TC_TRACE=<file prefix>: CTA-0 timeline dump
+    unsigned long long* cta_times = nullptr;  // EMBER_TC_CTATIMES=<file>: per-CTA spans of one rows + one dN launch
+    uint32_t* arrive = nullptr;     // [3]: CTA arrival counters of the rows / dN kernels, rows-item claims (never reset)
+    uint32_t arrive_base[2] = {0, 0};
+    uint32_t claim_base = 0;
+    bool dyn = true;                // dynamic rows-item claims (EMBER_TC_DYNAMIC=0: static grid stride)
     std::string trace_path;
     int trace_calls = 0;
 };
@@ -738,8 +794,13 @@ void tc_setup(Engine& E) {
     if (t->nsp < 2) throw ConfigError("tensor-core engine: dim too large for the TMEM layout");
     t->chunks2 = std::max(1, E.sm_count / (2 * ntl));
     t->nstage = stages_for(t->KP);
+    if (const char* s = getenv("EMBER_TC_NSTAGE")) t->nstage = std::max(2, std::min(t->nstage, atoi(s)));  // A/B
     if (const char* s = getenv("EMBER_TC_ZMAX")) t->zmax = (float)atof(s);  // test hook: 0 flags every row
     if (const char* s = getenv("EMBER_TC_MAXGRID")) t->max_grid = atoi(s);
+    if (getenv("EMBER_TC_CTATIMES")) EMBER_CUDA(cudaMalloc(&t->cta_times, (size_t)2 * 2 * E.sm_count * 8));
+    EMBER_CUDA(cudaMalloc(&t->arrive, 3 * sizeof(uint32_t)));
+    EMBER_CUDA(cudaMemset(t->arrive, 0, 3 * sizeof(uint32_t)));
+    if (const char* s = getenv("EMBER_TC_DYNAMIC")) t->dyn = atoi(s) != 0;
     if (const char* s = getenv("EMBER_TC_TRACE")) {
         t->trace_path = s;
         EMBER_CUDA(cudaMalloc(&t->trace, (size_t)2 * 5 * TRACE_ROLE * 8));
@@ -777,6 +838,8 @@ void tc_release(Engine& E) {
     cudaFree(E.tc->flags);
     cudaFree(E.tc->flags_total);
     if (E.tc->trace) cudaFree(E.tc->trace);
+    if (E.tc->cta_times) cudaFree(E.tc->cta_times);
+    cudaFree(E.tc->arrive);
     delete E.tc;
     E.tc = nullptr;
 }
@@ -832,6 +895,8 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
         EMBER_CUDA(cudaMemsetAsync(t.trace, 0, (size_t)2 * 5 * TRACE_ROLE * 8, E.stream));
         a.trace = t.trace;
     }
+    const bool ct = t.cta_times && t.trace_calls++ == 6;  // one warmed-up call: rows CTAs then dN CTAs
+    a.cta_times = ct ? t.cta_times : nullptr;
     // programmatic launch: the CTAs set up barriers and TMEM while the gathers drain
     // Performance only: when the dN kernel's grid (items2, e.g. 144 of 148 SMs) leaves at most
     // kSpareSms SMs idle, the rows kernel takes the same grid (the same number of waves), and the
@@ -839,6 +904,14 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
     constexpr int kSpareSms = 8;
     const int g2 = std::min(items2, gmax);
     const int grid1 = std::min(items1, t.max_grid == 0 && E.sm_count - g2 <= kSpareSms ? g2 : gmax);
+    a.arrive = t.arrive;
+    a.arrive_base = t.arrive_base[0];
+    t.arrive_base[0] += (uint32_t)grid1;
+    // every CTA claims until a claim fails: items1 - grid1 successful + grid1 failed claims
+    a.dyn = t.dyn ? 1 : 0;
+    a.claim = t.arrive + 2;
+    a.claim_base = t.claim_base;
+    if (t.dyn) t.claim_base += (uint32_t)items1;
     launch_pdl(k_tc<MODE_ROWS>, dim3(grid1), dim3(NTHREADS), smem_total(t.KP, t.nstage, MODE_ROWS),
                E.stream, t.mA128, t.mN96, a);
     EMBER_LAUNCHED(E);
@@ -851,9 +924,23 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
     launch_pdl(k_tc_fixup, dim3(E.sm_count * 2), dim3(256), 0, E.stream, a, (const uint16_t*)s.Apk,
                (const uint16_t*)s.Npk);
     EMBER_LAUNCHED(E);
+    if (ct) a.cta_times = t.cta_times + 2 * E.sm_count;
+    a.arrive = t.arrive + 1;
+    a.arrive_base = t.arrive_base[1];
+    a.dyn = 0;  // one item per CTA
+    t.arrive_base[1] += (uint32_t)std::min(items2, gmax);
     launch_pdl(k_tc<MODE_NEGS>, dim3(std::min(items2, gmax)), dim3(NTHREADS), smem_total(t.KP, t.nstage, MODE_NEGS),
                E.stream, t.mN128, t.mA96, a);
     EMBER_LAUNCHED(E);
+    if (ct) {  // host copy of both launches' spans (measurement only: synchronises the stream)
+        EMBER_CUDA(cudaStreamSynchronize(E.stream));
+        std::vector<unsigned long long> buf((size_t)4 * E.sm_count);
+        EMBER_CUDA(cudaMemcpy(buf.data(), t.cta_times, buf.size() * 8, cudaMemcpyDeviceToHost));
+        if (FILE* f = fopen(getenv("EMBER_TC_CTATIMES"), "wb")) {
+            fwrite(buf.data(), 8, buf.size(), f);
+            fclose(f);
+        }
+    }
     if (tr) dump(".negs.bin");
     const int64_t r = (int64_t)2 * nt * (d / 4);
     E.join_sorted();
