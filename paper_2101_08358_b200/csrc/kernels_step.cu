@@ -131,8 +131,9 @@ constexpr uint32_t GP_ROWS = 32, GP_WARPS = 8;
 // Packed gather (tensor-core engine): a CTA builds the operand rows of GP_ROWS consecutive edges
 // (rows up to rows_pad: the packed layout is zero-padded to whole tiles). Each warp takes
 // GP_ROWS / GP_WARPS edges: lanes load their quads of the source, relation and destination rows
-// into registers, form the adjusted quads and stage them (2 x KP floats per warp); lanes < 2CB
-// split 8 consecutive coordinates into bf16 hi|lo 16-byte core-matrix rows of a shared tile
+// into registers and form the adjusted quads; lane pairs swap quads (shuffle) so that each lane
+// < 2CB holds the 8 consecutive coordinates of one column block of one side, split into bf16 hi|lo
+// 16-byte core-matrix rows of a shared tile
 // [2 sides][2CB blocks][GP_ROWS][16 B] (row slot XOR-swizzled by the block, so the lanes' 16-byte
 // stores are bank-conflict free), which leaves in 512-byte coalesced runs, one per column block
 // (per-lane 16-byte stores would scatter over 56 blocks). fpos[e] = ad . t.
@@ -151,14 +152,10 @@ __global__ void __launch_bounds__(32 * GP_WARPS) k_gather_pack(const uint32_t* _
     }
     extern __shared__ uint4 gsm[];
     uint4* tile = gsm;  // [2][2CB][GP_ROWS]
-    const uint32_t kp = 8 * CB, nblk = 4 * CB;
-    float* stage = reinterpret_cast<float*>(tile + (size_t)nblk * GP_ROWS);
+    const uint32_t nblk = 4 * CB;
     const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* xd = stage + wib * 2 * kp;
-    float* xs = xd + kp;
     const uint32_t e0 = blockIdx.x * GP_ROWS;
     const uint32_t nq = d / 4;
-    for (uint32_t k = d + lane; k < kp; k += 32) xd[k] = xs[k] = 0.f;  // K padding (never rewritten)
     for (uint32_t rr = wib; rr < GP_ROWS; rr += GP_WARPS) {
         const uint32_t e = e0 + rr;
         if (e >= nb) {  // padding rows of the last tiles
@@ -166,31 +163,31 @@ __global__ void __launch_bounds__(32 * GP_WARPS) k_gather_pack(const uint32_t* _
             continue;
         }
         const uint32_t s = edges[3 * e], r = edges[3 * e + 1], t = edges[3 * e + 2];
-        const float* ss = node_row(pi, s, d);
-        const float* st = node_row(pj, t, d);
-        const float* sr = kind != EMBER_DOT ? rel + (uint64_t)r * d : nullptr;
+        // d <= 128: lane q holds quad q of each row (zeros past d: the K padding)
+        Quad ad{}, as{};
         float part = 0.f;
-        __syncwarp();  // the previous edge's staged rows have been packed
-        for (uint32_t q = lane; q < nq; q += 32) {
-            const Quad S = load_quad(ss, q), T = load_quad(st, q);
-            const Quad R = sr ? load_quad(sr, q) : S;
-            Quad ad, as;
+        if (lane < nq) {
+            const Quad S = load_quad(node_row(pi, s, d), lane), T = load_quad(node_row(pj, t, d), lane);
+            const Quad R = kind != EMBER_DOT ? load_quad(rel + (uint64_t)r * d, lane) : S;
             adjust_quad(kind, S, R, T, ad, as);
 #pragma unroll
             for (int i = 0; i < 4; ++i) part += ad.v[i] * T.v[i];
-            store_quad(xd, q, ad);
-            store_quad(xs, q, as);
         }
-        __syncwarp();
+        // Column block cb (8 coordinates) = quads 2cb and 2cb + 1. Lane 2cb packs side 0's block and
+        // lane 2cb + 1 side 1's, each taking the other quad from its neighbour (registers only).
+        const bool odd = lane & 1;
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float got = __shfl_xor_sync(0xffffffffu, odd ? ad.v[i] : as.v[i], 1);
+            v[i] = odd ? got : ad.v[i];
+            v[4 + i] = odd ? as.v[i] : got;
+        }
         if (lane < 2 * CB) {
-            const uint32_t cb = lane % CB, side = lane / CB;
-            const float4* src = reinterpret_cast<const float4*>((side == 0 ? xd : xs) + 8 * cb);
-            const float4 v0 = src[0], v1 = src[1];
-            float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
             uint4 hq, lq;
             tc::split8(v, hq, lq);
             // row slot rr ^ block: the lanes (one block each) hit distinct 16-byte bank groups
-            const uint32_t bh = side * 2 * CB + cb, bl = bh + CB;
+            const uint32_t bh = (lane & 1) * 2 * CB + (lane >> 1), bl = bh + CB;
             tile[bh * GP_ROWS + (rr ^ (bh % GP_ROWS))] = hq;
             tile[bl * GP_ROWS + (rr ^ (bl % GP_ROWS))] = lq;
         }
@@ -1248,7 +1245,7 @@ void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, c
     if (packed) {
         const uint32_t rows_pad = (uint32_t)Engine::pad_rows(nb);  // a multiple of GP_ROWS
         const uint32_t row_ctas = rows_pad / GP_ROWS, neg_ctas = (2 * E.n_pad + GP_WARPS - 1) / GP_WARPS;
-        const size_t sm = (size_t)4 * E.CB * GP_ROWS * 16 + (size_t)GP_WARPS * 2 * E.KP * sizeof(float);
+        const size_t sm = (size_t)4 * E.CB * GP_ROWS * 16;
         opt_in_smem((const void*)k_gather_pack, sm, E.device);
         launch_pdl(k_gather_pack, dim3(row_ctas + neg_ctas), dim3(32 * GP_WARPS), sm, E.stream, edges, nb, pi, pj,
                    E.rel_theta, E.m.kind, E.dim, E.CB, (uint32_t)E.b_cap, E.s.Apk, E.s.fpos, row_ctas,
