@@ -362,11 +362,11 @@ void Engine::forward_backward(const uint32_t* edges, uint32_t nb, uint32_t i, ui
     }
     mark(PHASE_GATHER);
     const bool fused = tc_engine() && !wide;  // d <= 128: the gather packs the bf16 operands itself
-    launch_gather_adjust(*this, edges, nb, pi, pj, fused, negs);
+    if (!wide) launch_gather_adjust(*this, edges, nb, pi, pj, fused, negs);  // (wide: in launch_contract_wide)
     launch_gather_negatives(*this, negs, pi, pj, fused);
     mark(PHASE_CONTRACT);
     if (wide)
-        launch_contract_wide(*this, nb);  // joins the sort before scattering dN rows
+        launch_contract_wide(*this, nb, edges, pi, pj);  // joins the sort before scattering dN rows
     else if (tc_engine())
         launch_contract_tc(*this, nb);  // joins the sort before scattering dN rows
     else

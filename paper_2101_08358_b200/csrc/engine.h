@@ -271,6 +271,9 @@ void launch_sample_on(const Engine& E, cudaStream_t st, uint32_t* out, uint64_t 
 void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj,
                           bool packed, const uint32_t* negs);
 void launch_gather_negatives(const Engine& E, const uint32_t* negs, const PartView& pi, const PartView& pj, bool packed);
+// the wide tensor-core path's packed gather (tc_wide.cu layout: cap rows, chunk q at q CP, cr rows per chunk)
+void launch_gather_pack_wide(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj,
+                             uint16_t* Apk, uint32_t CBA, uint32_t cap, uint32_t CP, uint32_t cr);
 void launch_keys(const Engine& E, const uint32_t* edges, uint32_t nb, const uint32_t* negs, const KeySpace& ks);
 // the training step's sample_negatives + gradient-slot keys, one kernel on the step stream
 void launch_sample_keys(const Engine& E, const uint32_t* edges, uint32_t nb, uint64_t base, const uint32_t* bucket,
@@ -316,6 +319,6 @@ bool wide_supported(const Engine& E);
 void wide_setup(Engine& E);
 void wide_release(Engine& E);
 uint64_t wide_overflow_rows(Engine& E);
-void launch_contract_wide(Engine& E, uint32_t nb);
+void launch_contract_wide(Engine& E, uint32_t nb, const uint32_t* edges, const PartView& pi, const PartView& pj);
 
 }  // namespace ember

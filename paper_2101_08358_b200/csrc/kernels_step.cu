@@ -202,6 +202,72 @@ __global__ void __launch_bounds__(32 * GP_WARPS) k_gather_pack(const uint32_t* _
     }
 }
 
+// Packed gather of the wide tensor-core path (tc_wide.cu; d > 128 or chunked negatives): the same
+// job as k_gather_pack for rows of any width, into the wide layout [side][2 CBA blocks][cap][8 bf16]
+// with chunk q's rows at packed rows [q CP, q CP + cr). A CTA builds GW_ROWS consecutive packed rows
+// (a warp each; rows without an edge are zero) in a shared tile [2 sides x 2 CBA blocks][GW_ROWS]
+// of 16-byte core-matrix rows (slot XOR-swizzled by the block) that leaves in 128-byte runs. Lane
+// pairs swap quads (shuffle) so each lane packs one 8-column block of one side per 64 columns.
+constexpr uint32_t GW_ROWS = 8;
+__global__ void __launch_bounds__(32 * GW_ROWS) k_gather_pack_wide(const uint32_t* __restrict__ edges, uint32_t nb,
+                                                                  PartView pi, PartView pj,
+                                                                  const float* __restrict__ rel, int kind, uint32_t d,
+                                                                  uint32_t CBA, uint32_t cap, uint32_t CP, uint32_t cr,
+                                                                  uint16_t* __restrict__ Apk, float* __restrict__ fpos) {
+    griddep_wait();
+    extern __shared__ uint4 gws[];  // [4 CBA][GW_ROWS]
+    const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t pr = blockIdx.x * GW_ROWS + w, q = pr / CP, r = pr - q * CP, e = q * cr + r;
+    const bool valid = r < cr && e < nb;
+    const uint32_t nq = d / 4, nqp = CBA * 2;  // quads with data / quads of the padded width
+    uint32_t s = 0, rr = 0, t = 0;
+    if (valid) {
+        s = edges[3 * e];
+        rr = edges[3 * e + 1];
+        t = edges[3 * e + 2];
+    }
+    const float* ss = valid ? node_row(pi, s, d) : nullptr;
+    const float* st = valid ? node_row(pj, t, d) : nullptr;
+    const float* sr = valid && kind != EMBER_DOT ? rel + (uint64_t)rr * d : nullptr;
+    float part = 0.f;
+    const bool odd = lane & 1;
+    for (uint32_t q0 = 0; q0 < nqp; q0 += 32) {  // warp-uniform (shuffles)
+        const uint32_t q4 = q0 + lane;
+        Quad ad{}, as{};
+        if (valid && q4 < nq) {
+            const Quad S = load_quad(ss, q4), T = load_quad(st, q4);
+            const Quad R = sr ? load_quad(sr, q4) : S;
+            adjust_quad(kind, S, R, T, ad, as);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) part += ad.v[i] * T.v[i];
+        }
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float got = __shfl_xor_sync(0xffffffffu, odd ? ad.v[i] : as.v[i], 1);
+            v[i] = odd ? got : ad.v[i];
+            v[4 + i] = odd ? as.v[i] : got;
+        }
+        const uint32_t blk = q4 >> 1;  // column block of this lane pair
+        if (blk < CBA) {
+            uint4 hq, lq;
+            tc::split8(v, hq, lq);
+            const uint32_t bh = (lane & 1) * 2 * CBA + blk, bl = bh + CBA;
+            gws[bh * GW_ROWS + (w ^ (bh % GW_ROWS))] = hq;
+            gws[bl * GW_ROWS + (w ^ (bl % GW_ROWS))] = lq;
+        }
+    }
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (valid && lane == 0) fpos[e] = part;
+    __syncthreads();
+    uint4* P = reinterpret_cast<uint4*>(Apk);
+    const uint32_t row0 = blockIdx.x * GW_ROWS;
+    for (uint32_t i = threadIdx.x; i < 4 * CBA * GW_ROWS; i += blockDim.x) {
+        const uint32_t blk = i / GW_ROWS, row = i % GW_ROWS;  // blk = side * 2CBA + column block
+        P[(uint64_t)blk * cap + row0 + row] = gws[blk * GW_ROWS + (row ^ (blk % GW_ROWS))];
+    }
+}
+
 // fp32 gather (SIMT engine, and the wide tensor-core path that packs it afterwards, tc_wide.cu):
 // one warp per edge, A[0][e] = ad, A[1][e] = as, fpos[e] = ad . t.
 __global__ void k_gather_adjust(const uint32_t* __restrict__ edges, uint32_t nb, PartView pi, PartView pj,
@@ -1255,6 +1321,15 @@ void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, c
         k_gather_adjust<<<(nb + warps - 1) / warps, warps * 32, 0, E.stream>>>(edges, nb, pi, pj, E.rel_theta,
                                                                                 E.m.kind, E.dim, E.s.A, E.s.fpos);
     }
+    EMBER_LAUNCHED(E);
+}
+
+void launch_gather_pack_wide(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj,
+                             uint16_t* Apk, uint32_t CBA, uint32_t cap, uint32_t CP, uint32_t cr) {
+    const size_t sm = (size_t)4 * CBA * GW_ROWS * 16;
+    opt_in_smem((const void*)k_gather_pack_wide, sm, E.device);
+    launch_pdl(k_gather_pack_wide, dim3(cap / GW_ROWS), dim3(32 * GW_ROWS), sm, E.stream, edges, nb, pi, pj,
+               (const float*)E.rel_theta, E.m.kind, E.dim, CBA, cap, CP, cr, Apk, E.s.fpos);
     EMBER_LAUNCHED(E);
 }
 

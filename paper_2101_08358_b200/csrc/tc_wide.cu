@@ -356,6 +356,37 @@ __global__ void k_pack_rows(const float* __restrict__ x, int nb, int nt, int cr,
     o[(size_t)CBA * cap] = lo;
 }
 
+// A' = A / (Z b) in the packed layout, from the packed A itself (x = hi + lo, scaled, split again):
+// thread per (side, block, packed row), reads and writes coalesced along rows. Rows without an
+// edge have scale 0.
+__global__ void k_repack_scaled(const uint16_t* __restrict__ in, int CBA, int cap, const float* __restrict__ scale,
+                                uint16_t* __restrict__ out) {
+    griddep_wait();
+    const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t total = (size_t)2 * CBA * cap;
+    if (t >= total) return;
+    const int pr = (int)(t % cap);
+    const int blk = (int)((t / cap) % CBA);
+    const int side = (int)(t / ((size_t)cap * CBA));
+    const uint4* I = reinterpret_cast<const uint4*>(in) + ((size_t)side * 2 * CBA + blk) * cap + pr;
+    const uint4 h = I[0], l = I[(size_t)CBA * cap];
+    const float s = scale[(size_t)side * cap + pr];
+    const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hw[i]));
+        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&lw[i]));
+        v[2 * i] = (a.x + b.x) * s;
+        v[2 * i + 1] = (a.y + b.y) * s;
+    }
+    uint4 hi, lo;
+    tc::split8(v, hi, lo);
+    uint4* o = reinterpret_cast<uint4*>(out) + ((size_t)side * 2 * CBA + blk) * cap + pr;
+    o[0] = hi;
+    o[(size_t)CBA * cap] = lo;
+}
+
 // Row statistics after SCORES: Z = 1 + sum of the tiles' partial sums (fixed order), lse, g0, the
 // dA / A' row scale 1/(Z b); rows whose Z left the safe range are listed for k_wide_fixup.
 __global__ void k_wide_stats(const float* __restrict__ zpart, int ntiles, int nb, int cr, int CP, int b_cap, float inv_b,
@@ -526,8 +557,9 @@ uint64_t wide_overflow_rows(Engine& E) {
 void dn_reduce_launch(Engine& E, const float* part, int chunks, int nt, int n_pad, int d, uint32_t slot0,
                       uint32_t* flags, unsigned long long* flags_total, int nsides);  // tc_score.cu
 
-// s.A [2][nb][d] and s.N [chunks][2][nt][d] (fp32, written by the gathers) -> lse, g0, dA, sorted dN rows.
-void launch_contract_wide(Engine& E, uint32_t nb) {
+// The batch's rows gathered straight into the packed A (k_gather_pack_wide) and s.N [chunks][2][nt][d]
+// (fp32, written by the negatives' gather) -> lse, g0, dA, sorted dN rows.
+void launch_contract_wide(Engine& E, uint32_t nb, const uint32_t* edges, const PartView& pi, const PartView& pj) {
     WideState& w = *E.wide;
     Scratch& s = E.s;
     const int d = (int)E.dim, nt = (int)E.nt;
@@ -556,9 +588,8 @@ void launch_contract_wide(Engine& E, uint32_t nb) {
     const int sms = w.max_grid > 0 ? std::min(w.max_grid, E.sm_count) : E.sm_count;
     const size_t tA = (size_t)2 * w.CBA * w.b_cap, tN = (size_t)2 * w.CBA * w.n_cap;
     // operands packed into the tensor-core layout (chunk q's rows / negatives at packed row q CP / q n_pad)
-    launch_pdl(k_pack_rows, dim3((unsigned)((tA + 255) / 256)), dim3(256), 0, E.stream, (const float*)s.A, (int)nb, 0,
-               a.cr, w.CP, d, w.CBA, w.b_cap, w.chunks, (const float*)nullptr, w.Apk);
-    EMBER_LAUNCHED(E);
+    launch_gather_pack_wide(E, edges, nb, pi, pj, w.Apk, (uint32_t)w.CBA, (uint32_t)w.b_cap, (uint32_t)w.CP,
+                            (uint32_t)a.cr);
     launch_pdl(k_pack_rows, dim3((unsigned)((tN + 255) / 256)), dim3(256), 0, E.stream, (const float*)s.N, (int)nb, nt,
                a.cr, w.n_pad, d, w.CBA, w.n_cap, w.chunks, (const float*)nullptr, w.Npk);
     EMBER_LAUNCHED(E);
@@ -577,8 +608,8 @@ void launch_contract_wide(Engine& E, uint32_t nb) {
                (const uint16_t*)w.Npk, w.CBA, w.b_cap, w.n_pad, w.n_cap, w.NBP, (int)nb, nt, d, a.cr, w.CP, a.inv_b,
                (const float*)s.fpos, s.lse, s.g0, w.scale, w.Ppk);
     EMBER_LAUNCHED(E);
-    launch_pdl(k_pack_rows, dim3((unsigned)((tA + 255) / 256)), dim3(256), 0, E.stream, (const float*)s.A, (int)nb, 0,
-               a.cr, w.CP, d, w.CBA, w.b_cap, w.chunks, (const float*)w.scale, w.Ascaled);
+    launch_pdl(k_repack_scaled, dim3((unsigned)((tA + 255) / 256)), dim3(256), 0, E.stream, (const uint16_t*)w.Apk,
+               w.CBA, w.b_cap, (const float*)w.scale, w.Ascaled);
     EMBER_LAUNCHED(E);
     // 2) dA = P~ N / (Z b)
     a.kchunks = w.n_pad / WKC;
