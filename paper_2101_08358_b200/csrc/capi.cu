@@ -522,7 +522,7 @@ int ember_debug_sort_slots(ember_ctx* ctx, const uint32_t* keys, uint32_t n, uin
         EMBER_CUDA(cudaMemcpyAsync(E.s.keys, keys, b4, cudaMemcpyDeviceToDevice, E.stream));
         EMBER_CUDA(cudaEventRecord(E.ev_fork, E.stream));
         EMBER_CUDA(cudaStreamWaitEvent(E.side, E.ev_fork, 0));
-        launch_slot_sort(E, n, bits);
+        launch_slot_sort(E, n, bits, ~0u);
         EMBER_CUDA(cudaEventRecord(E.ev_sorted, E.side));
         EMBER_CUDA(cudaStreamWaitEvent(E.stream, E.ev_sorted, 0));
         auto out = [&](void* dst, const void* src, size_t bytes) {

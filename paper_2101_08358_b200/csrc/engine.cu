@@ -198,6 +198,10 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     }
     EMBER_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     EMBER_CUDA(cudaEventCreateWithFlags(&ev_sorted, cudaEventDisableTiming));
+    EMBER_CUDA(cudaStreamCreateWithFlags(&comm, cudaStreamNonBlocking));
+    EMBER_CUDA(cudaEventCreateWithFlags(&ev_rel_grad, cudaEventDisableTiming));
+    EMBER_CUDA(cudaEventCreateWithFlags(&ev_rel_done, cudaEventDisableTiming));
+    if (const char* e = getenv("EMBER_DENSE_RELATIONS")) force_dense = atoi(e) != 0;
     parts.assign(g.num_partitions, PartView{nullptr, nullptr, 0, 0});
     for (uint32_t k = 0; k < g.num_partitions; ++k) {
         parts[k].first = partition_offset(g.num_nodes, g.num_partitions, k);
@@ -239,6 +243,7 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     s.sort_hist = dalloc<uint32_t>(slot_sort_scratch_words(cap_rows));
     s.sort_status = dalloc<unsigned long long>(slot_sort_tiles(cap_rows));
     s.sort_ctr = dalloc<uint32_t>(1);
+    s.nsplit = dalloc<uint32_t>(1);
     s.nruns = dalloc<uint32_t>(1);
     s.nunique = dalloc<uint32_t>(2);
     // at most cap_rows / LONG_SEG long segments, each with <= len / LONG_CHUNK + 1 chunks
@@ -247,6 +252,12 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     s.longs = dalloc<uint32_t>(2 + 3 * max_long);
     s.long_owner = dalloc<uint32_t>(max_chunks);
     s.long_partial = dalloc<float>((uint64_t)max_chunks * d);
+    {  // relation keys: at most cap_b rows
+        const uint32_t rl = cap_b / EMBER_LONG_SEG + 1, rc = cap_b / EMBER_LONG_CHUNK + rl;
+        s.longs_rel = dalloc<uint32_t>(2 + 3 * rl);
+        s.long_owner_rel = dalloc<uint32_t>(rc);
+        s.long_partial_rel = dalloc<float>((uint64_t)rc * d);
+    }
     EMBER_CUDA(cudaMemset(s.nunique, 0, 2 * sizeof(uint32_t)));
     EMBER_CUDA(cudaMemset(s.longs, 0, 2 * sizeof(uint32_t)));
     if (m.engine == EMBER_ENGINE_SIMT_FP32) {
@@ -278,7 +289,8 @@ Engine::~Engine() {
                     s.S,     s.dA,        s.dN_part, s.grows,    s.loss,    s.loss_part,  s.loss_done,  s.bad_batch,
                     s.nunique, s.long_partial, s.rel_dense, s.negs, s.keys, s.keys_sorted, s.vals, s.vals_sorted,
                     s.rank, s.ukeys, s.offsets, s.nruns, s.longs, s.long_owner, s.uniq, s.sort_keys[0],
-                    s.sort_keys[1], s.sort_vals[0], s.sort_vals[1], s.sort_hist, s.sort_status, s.sort_ctr};
+                    s.sort_keys[1], s.sort_vals[0], s.sort_vals[1], s.sort_hist, s.sort_status, s.sort_ctr, s.nsplit,
+                    s.longs_rel, s.long_owner_rel, s.long_partial_rel};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (void* p : owned) cudaFree(p);
@@ -300,6 +312,12 @@ Engine::~Engine() {
     if (io_out) cudaStreamDestroy(io_out);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_sorted) cudaEventDestroy(ev_sorted);
+    if (ev_rel_grad) cudaEventDestroy(ev_rel_grad);
+    if (ev_rel_done) cudaEventDestroy(ev_rel_done);
+    if (comm) {
+        cudaStreamSynchronize(comm);
+        cudaStreamDestroy(comm);
+    }
     if (side && side != stream) cudaStreamDestroy(side);
     if (own_stream) cudaStreamDestroy(stream);
 }
@@ -341,7 +359,7 @@ void Engine::sort_keys(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t 
 
 void Engine::sort_slots(uint32_t nb, const KeySpace& ks) {
     const uint32_t n = slots(nb);
-    launch_slot_sort(*this, slots(nb), ks.bits);
+    launch_slot_sort(*this, slots(nb), ks.bits, (uint32_t)ks.node_range);
     EMBER_CUDA(cudaEventRecord(ev_sorted, side));
     sorted_pending = true;
 }
@@ -383,14 +401,26 @@ void Engine::reduce_and_apply(uint32_t nb, uint32_t i, uint32_t j, bool apply, u
     // (internal NCCL comm) or handed to the caller (rel_ext: external reduction, then
     // ember_relations_apply_dense) before the relation Adagrad.
     const bool ext = rel_ext != nullptr;
-    const bool dense = apply && m.kind != EMBER_DOT && (world > 1 || ext);
+    const bool dense = apply && m.kind != EMBER_DOT && (world > 1 || ext || force_dense);
     float* buf = ext ? rel_ext : s.rel_dense;
+    if (dense && !ext) {
+        // The relation keys are reduced, summed across ranks and applied (dense Adagrad) on `comm`
+        // while the node keys (most of the reduction) are reduced on the step stream; the step
+        // stream joins before anything reads relations again.
+        if (!s.rel_dense) s.rel_dense = dalloc<float>((uint64_t)g.num_relations * dim);
+        EMBER_CUDA(cudaEventRecord(ev_rel_grad, stream));
+        EMBER_CUDA(cudaStreamWaitEvent(comm, ev_rel_grad, 0));
+        EMBER_CUDA(cudaMemsetAsync(s.rel_dense, 0, (size_t)g.num_relations * dim * sizeof(float), comm));
+        launch_segments(*this, slots(nb), ks, apply, true, nullptr, nullptr, nullptr, nullptr, 1, comm);
+        allreduce_relations(comm);
+        apply_relations_dense(s.rel_dense, comm);
+        EMBER_CUDA(cudaEventRecord(ev_rel_done, comm));
+        launch_segments(*this, slots(nb), ks, apply, true, node_ids_out, node_rows_out, rel_ids_out, rel_rows_out, 2);
+        EMBER_CUDA(cudaStreamWaitEvent(stream, ev_rel_done, 0));
+        return;
+    }
     if (dense) EMBER_CUDA(cudaMemsetAsync(buf, 0, (size_t)g.num_relations * dim * sizeof(float), stream));
     launch_segments(*this, slots(nb), ks, apply, dense, node_ids_out, node_rows_out, rel_ids_out, rel_rows_out);
-    if (dense && !ext) {
-        allreduce_relations();
-        apply_relations_dense(s.rel_dense);
-    }
 }
 
 void Engine::idle_step() {
@@ -398,16 +428,16 @@ void Engine::idle_step() {
     // all-reduce is a collective and the dense Adagrad applies the other ranks' sum
     if (m.kind == EMBER_DOT || world <= 1) return;
     EMBER_CUDA(cudaMemsetAsync(s.rel_dense, 0, (size_t)g.num_relations * dim * sizeof(float), stream));
-    allreduce_relations();
+    allreduce_relations(stream);
     apply_relations_dense(s.rel_dense);
 }
 
-void Engine::apply_relations_dense(const float* grad) {
+void Engine::apply_relations_dense(const float* grad, cudaStream_t st) {
     if (m.kind == EMBER_DOT) return;
     if (!rel_theta || !rel_acc) throw ConfigError("relation table not bound");
     const uint64_t rn = (uint64_t)g.num_relations * dim;
-    launch_pdl(k_adagrad_dense, dim3((unsigned)((rn + 255) / 256)), dim3(256), 0, stream, rel_theta, rel_acc, grad, rn,
-               m.lr, m.eps);
+    launch_pdl(k_adagrad_dense, dim3((unsigned)((rn + 255) / 256)), dim3(256), 0, st ? st : stream, rel_theta, rel_acc,
+               grad, rn, m.lr, m.eps);
     EMBER_LAUNCHED(*this);
 }
 
@@ -518,10 +548,10 @@ void Engine::comm_init(const void* unique_id, int r, int w) {
     if (m.kind != EMBER_DOT && !s.rel_dense) s.rel_dense = dalloc<float>((uint64_t)g.num_relations * dim);
 }
 
-void Engine::allreduce_relations() {
+void Engine::allreduce_relations(cudaStream_t st) {
     if (!nccl_comm) return;
     const uint64_t rn = (uint64_t)g.num_relations * dim;
-    ncclResult_t r = nccl().all_reduce(s.rel_dense, s.rel_dense, rn, ncclFloat32, ncclSum, static_cast<ncclComm_t>(nccl_comm), stream);
+    ncclResult_t r = nccl().all_reduce(s.rel_dense, s.rel_dense, rn, ncclFloat32, ncclSum, static_cast<ncclComm_t>(nccl_comm), st);
     if (r != ncclSuccess) throw EmberError(std::string("ncclAllReduce failed: ") + (nccl().err ? nccl().err(r) : "?"));
 }
 

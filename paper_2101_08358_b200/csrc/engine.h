@@ -115,12 +115,17 @@ struct Scratch {
     uint32_t* longs = nullptr;        // [2 + 3 * cap]: long segments, chunk slots, then (u, base, nch)
     uint32_t* long_owner = nullptr;   // chunk slot -> long segment
     float* long_partial = nullptr;    // chunk slot -> partial row
+    // the relation part's own long-segment list (relation keys reduced on the comm stream, world > 1)
+    uint32_t* longs_rel = nullptr;
+    uint32_t* long_owner_rel = nullptr;
+    float* long_partial_rel = nullptr;
     // slot sort (sort.cu): ping-pong key/value buffers, per-tile digit histograms, run-scan state
     uint32_t* sort_keys[2] = {nullptr, nullptr};
     uint32_t* sort_vals[2] = {nullptr, nullptr};
     uint32_t* sort_hist = nullptr;
     unsigned long long* sort_status = nullptr;
     uint32_t* sort_ctr = nullptr;
+    uint32_t* nsplit = nullptr;  // [1] first run of a relation key (~0u: none), written by the sort
     float* rel_dense = nullptr;  // [R][dim] relation gradient summed over ranks (world > 1)
 };
 
@@ -132,6 +137,11 @@ struct Engine {
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;  // key sort runs here, overlapped with gather + contraction
     cudaEvent_t ev_fork = nullptr, ev_sorted = nullptr;
+    // relation gradients summed across ranks (world > 1): the relation keys are reduced first, their
+    // all-reduce + dense Adagrad run on `comm` while the node keys are reduced on the step stream
+    cudaStream_t comm = nullptr;
+    cudaEvent_t ev_rel_grad = nullptr, ev_rel_done = nullptr;
+    bool force_dense = false;  // EMBER_DENSE_RELATIONS=1: that path at world 1 (tests: bit-identical)
     // host-batch path: positives copied on `io` into one of two staging slots, overlapping the
     // previous step; ev_staged[k]: copy into slot k done; ev_consumed[k]: the step reading slot k done
     cudaStream_t io = nullptr, io_out = nullptr;  // host->device batches / device->host losses
@@ -219,9 +229,9 @@ struct Engine {
     void step(const uint32_t* edges, uint32_t nb, const uint32_t* bucket, uint64_t bucket_n, uint32_t i, uint32_t j,
               uint64_t epoch, uint32_t bucket_step, uint32_t batch_in_bucket, float* loss_out,
               cudaEvent_t edges_ready = nullptr);
-    void allreduce_relations();
+    void allreduce_relations(cudaStream_t st);
     void idle_step();  // lockstep step without a batch (world > 1): zero relation gradient, all-reduce, Adagrad
-    void apply_relations_dense(const float* grad);  // dense relation Adagrad (zero rows are no-ops)
+    void apply_relations_dense(const float* grad, cudaStream_t st = nullptr);  // dense relation Adagrad (zero rows are no-ops)
     void comm_init(const void* nccl_unique_id, int rank, int world);
     std::vector<double> profile_read();  // ms per phase summed over marked batches
 };
@@ -279,15 +289,17 @@ void launch_keys(const Engine& E, const uint32_t* edges, uint32_t nb, const uint
 void launch_sample_keys(const Engine& E, const uint32_t* edges, uint32_t nb, uint64_t base, const uint32_t* bucket,
                         uint64_t bucket_n, const PartView& src, const PartView& dst, const KeySpace& ks);
 // the (key, slot) sort of s.keys and its runs, on the helper stream (sort.cu)
-void launch_slot_sort(const Engine& E, uint32_t n, uint32_t bits);
+void launch_slot_sort(const Engine& E, uint32_t n, uint32_t bits, uint32_t split_key);
 size_t slot_sort_scratch_words(uint32_t cap);
 uint32_t slot_sort_tiles(uint32_t cap);
 void launch_contract_simt(Engine& E, uint32_t nb);
 void launch_contract_tc(Engine& E, uint32_t nb);
 void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj);
 void launch_loss(const Engine& E, uint32_t nb, float* loss_out);
+// part: 0 every key, 1 relation keys only, 2 node keys only (the split: s.nsplit)
 void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool apply, bool rel_dense,
-                     uint32_t* node_ids_out, float* node_rows_out, uint32_t* rel_ids_out, float* rel_rows_out);
+                     uint32_t* node_ids_out, float* node_rows_out, uint32_t* rel_ids_out, float* rel_rows_out,
+                     int part = 0, cudaStream_t st = nullptr);
 void launch_adagrad_rows(const Engine& E, const uint32_t* ids, const float* rows, uint32_t n, const PartView& pi,
                          const PartView& pj, bool relations,
                          uint32_t* bad);

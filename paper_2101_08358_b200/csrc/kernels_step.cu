@@ -731,7 +731,23 @@ struct SegArgs {
     float* node_rows_out;
     uint32_t* rel_ids_out;
     float* rel_rows_out;
+    int part;                 // 0 every key; 1 relation keys [nsplit, nr); 2 node keys [0, nsplit)
+    const uint32_t* nsplit;   // first relation run (~0u: none)
 };
+
+// The unique keys this launch reduces: [lo, hi) of the nr runs.
+__device__ __forceinline__ void seg_range(const SegArgs& a, uint32_t nr, uint32_t& lo, uint32_t& hi) {
+    const uint32_t split = min(*a.nsplit, nr);
+    lo = a.part == 1 ? split : 0u;
+    hi = a.part == 2 ? split : nr;
+}
+
+// A long segment's key belongs to this launch's part.
+__device__ __forceinline__ bool seg_in_part(const SegArgs& a, uint32_t u) {
+    if (a.part == 0) return true;
+    const bool rel = a.ukeys[u] >= a.ks.node_range;
+    return a.part == 1 ? rel : !rel;
+}
 
 // Segments longer than LONG_SEG rows (hot relations, hub nodes) are cut into LONG_CHUNK-row chunks
 // summed by separate warps; a block per long segment then adds the chunk partials in a fixed
@@ -868,7 +884,9 @@ __global__ void __launch_bounds__(256, 4) k_segments(SegArgs a) {
     const uint32_t u = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 2 + (lane >> 4);
     const uint32_t hmask = lane < SEG_LANES ? 0x0000ffffu : 0xffff0000u;
     const uint32_t nr = *a.nruns;
-    if (u >= nr) return;
+    uint32_t lo, hi;
+    seg_range(a, nr, lo, hi);
+    if (u < lo || u >= hi) return;
     const uint32_t key = a.ukeys[u];
     if (hl == 0 && key < a.ks.node_range && (u + 1 == nr || a.ukeys[u + 1] >= a.ks.node_range)) {
         a.nunique[0] = u + 1;
@@ -937,6 +955,8 @@ __global__ void __launch_bounds__(256, 4) k_segments_pipe(SegArgs a) {
     const uint32_t nh = ((gridDim.x * blockDim.x) >> 5) * 2;
     const uint32_t hmask = half == 0 ? 0x0000ffffu : 0xffff0000u;
     const uint32_t nr = *a.nruns, d4 = a.d / 4;
+    uint32_t u_lo, u_hi;
+    seg_range(a, nr, u_lo, u_hi);
     float4* my = sst + (size_t)(wib * 2 + half) * 2 * 2 * 2 * SEG_LANES + hl;
     auto slot = [&](int st, int role, int cb) { return my + (size_t)((st * 2 + role) * 2 + cb) * SEG_LANES; };
     // A key's (key, offset, count) are loaded one key ahead of its parameter copies, so the copies
@@ -950,7 +970,7 @@ __global__ void __launch_bounds__(256, 4) k_segments_pipe(SegArgs a) {
     auto issue = [&](uint32_t u, int st, const SegMeta& m, SegKey& k) {
         k.u = u;
         k.active = false;
-        if (u < nr) {
+        if (u < u_hi) {
             const uint32_t key = m.key;
             if (hl == 0 && key < a.ks.node_range && (u + 1 == nr || m.next_key >= a.ks.node_range)) {
                 a.nunique[0] = u + 1;
@@ -990,13 +1010,14 @@ __global__ void __launch_bounds__(256, 4) k_segments_pipe(SegArgs a) {
     };
     SegKey cur, nxt;
     SegMeta mn{}, mnn{};
-    if (gh < nr) load_meta(gh, mn);
-    issue(gh, 0, mn, cur);
-    if (gh + nh < nr) load_meta(gh + nh, mn);
-    for (uint32_t u = gh, it = 0; u < nr; u += nh, ++it) {
+    const uint32_t u0 = u_lo + gh;
+    if (u0 < u_hi) load_meta(u0, mn);
+    issue(u0, 0, mn, cur);
+    if (u0 + nh < u_hi) load_meta(u0 + nh, mn);
+    for (uint32_t u = u0, it = 0; u < u_hi; u += nh, ++it) {
         const int st = it & 1;
         issue(u + nh, st ^ 1, mn, nxt);
-        if (u + 2 * nh < nr) load_meta(u + 2 * nh, mnn);  // consumed next iteration
+        if (u + 2 * nh < u_hi) load_meta(u + 2 * nh, mnn);  // consumed next iteration
         cp_wait<1>();
         if (cur.active) {
             const bool app = seg_applies(a, cur.t);
@@ -1083,6 +1104,7 @@ __global__ void k_long_partial(SegArgs a) {
     for (uint32_t sl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < n_slots; sl += nw) {
         const uint32_t* rec = a.longs + 2 + 3 * a.owner[sl];
         const uint32_t u = rec[0], c = sl - rec[1];
+        if (!seg_in_part(a, u)) continue;  // warp-uniform: reduced by the other launch
         const uint32_t r0 = c * LONG_CHUNK, cnt = min(LONG_CHUNK, a.offsets[u + 1] - a.offsets[u] - r0);
         const float* base = a.rows + ((uint64_t)a.offsets[u] + r0) * a.d;
         for (uint32_t c0 = 0; c0 < d4; c0 += 32) {  // warp-uniform trip count (shuffles below)
@@ -1121,7 +1143,7 @@ __global__ void __launch_bounds__(32 * LONG_WARPS) k_long_final(SegArgs a) {
     for (uint32_t li = blockIdx.x; li < n_long; li += gridDim.x) {
         const uint32_t* rec = a.longs + 2 + 3 * li;
         const uint32_t u = rec[0], base = rec[1], nch = rec[2];
-        if (nch <= LONG_BIG) continue;  // block-uniform
+        if (nch <= LONG_BIG || !seg_in_part(a, u)) continue;  // block-uniform
         for (uint32_t c4 = hl; c4 < d4; c4 += 32) {
             float4 va, vb;
             sum_rows_strided2(a.partial + (uint64_t)base * a.d, stream, NS, nch, a.d, c4, c4 + 16, c4 + 16 < d4, va, vb);
@@ -1150,7 +1172,7 @@ __global__ void __launch_bounds__(32 * LONG_WARPS) k_long_final(SegArgs a) {
     for (uint32_t li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < n_long; li += nw) {
         const uint32_t* rec = a.longs + 2 + 3 * li;
         const uint32_t u = rec[0], base = rec[1], nch = rec[2];
-        if (nch > LONG_BIG) continue;  // warp-uniform
+        if (nch > LONG_BIG || !seg_in_part(a, u)) continue;  // warp-uniform
         const SegTarget t = seg_target(a, u, nr, lane == 0);
         const bool app = seg_applies(a, t);
         for (uint32_t c0 = 0; c0 < d4; c0 += 32) {  // warp-uniform trip count (shuffles below)
@@ -1400,16 +1422,23 @@ void launch_loss(const Engine& E, uint32_t nb, float* loss_out) {
 }
 
 void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool apply, bool rel_dense,
-                     uint32_t* node_ids_out, float* node_rows_out, uint32_t* rel_ids_out, float* rel_rows_out) {
+                     uint32_t* node_ids_out, float* node_rows_out, uint32_t* rel_ids_out, float* rel_rows_out,
+                     int part, cudaStream_t st) {
     if (!n_slots) return;
+    if (!st) st = E.stream;
+    // the relation part keeps its long segments in a list of its own (it runs beside the node part)
+    const bool own = part == 1;
+    if (own) EMBER_CUDA(cudaMemsetAsync(E.s.longs_rel, 0, 2 * sizeof(uint32_t), st));
     SegArgs a{};
+    a.part = part;
+    a.nsplit = E.s.nsplit;
     a.ukeys = E.s.ukeys;
     a.offsets = E.s.offsets;
     a.nruns = E.s.nruns;
     a.nunique = E.s.nunique;
-    a.longs = E.s.longs;
-    a.owner = E.s.long_owner;
-    a.partial = E.s.long_partial;
+    a.longs = own ? E.s.longs_rel : E.s.longs;
+    a.owner = own ? E.s.long_owner_rel : E.s.long_owner;
+    a.partial = own ? E.s.long_partial_rel : E.s.long_partial;
     a.rows = E.s.grows;
     a.ks = ks;
     a.rel_theta = E.rel_theta;
@@ -1429,16 +1458,16 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
         const size_t sm = (size_t)8 * 2 * 2 * 2 * 2 * SEG_LANES * sizeof(float4);
         opt_in_smem((const void*)k_segments_pipe, sm, E.device);
         const uint32_t blocks = std::min<uint32_t>((n_slots + 15) / 16, (uint32_t)E.sm_count * 4);
-        launch_pdl(k_segments_pipe, dim3(blocks), dim3(256), sm, E.stream, a);
+        launch_pdl(k_segments_pipe, dim3(blocks), dim3(256), sm, st, a);
     } else {
-        k_segments<<<(n_slots * 16 + 255) / 256, 256, 0, E.stream>>>(a);  // 2 keys per warp
+        k_segments<<<(n_slots * 16 + 255) / 256, 256, 0, st>>>(a);  // 2 keys per warp
     }
     EMBER_LAUNCHED(E);
-    launch_pdl(k_long_partial, dim3(2 * E.sm_count), dim3(256), 0, E.stream, a);
+    launch_pdl(k_long_partial, dim3(2 * E.sm_count), dim3(256), 0, st, a);
     EMBER_LAUNCHED(E);
     const size_t lf_smem = 2 * LONG_WARPS * E.dim * sizeof(float);  // > 48 KB from d = 376 on (C5: d = 800)
     opt_in_smem((const void*)k_long_final, lf_smem, E.device);
-    launch_pdl(k_long_final, dim3(E.sm_count), dim3(32 * LONG_WARPS), lf_smem, E.stream,
+    launch_pdl(k_long_final, dim3(E.sm_count), dim3(32 * LONG_WARPS), lf_smem, st,
                a);
     EMBER_LAUNCHED(E);
 }

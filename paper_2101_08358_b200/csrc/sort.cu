@@ -15,7 +15,8 @@
 //                     of a 32-slot chunk: hot keys would serialise per-slot atomics on one address),
 //                     and the last pass writes rank[] instead
 //   k_sort_runs       run heads, run numbers by a decoupled look-back scan over tiles, ukeys /
-//                     offsets / uniq / nruns
+//                     offsets / uniq / nruns, and the first run whose key >= split_key (nsplit:
+//                     the node / relation boundary of the step's keys; ~0u when there is none)
 // Everything here moves ~1.2 MB per pass (L2-resident): the kernels are bound by dependent global
 // round trips, so each issues its independent loads together (keys, values and the histogram
 // column at once) and keeps the serial per-warp work to 4 chunks.
@@ -68,7 +69,7 @@ __device__ __forceinline__ uint32_t scan256(uint32_t v, uint32_t* warp_sums) {
 __global__ void __launch_bounds__(SORT_THREADS) k_sort_hist(const uint32_t* __restrict__ keys, uint32_t n,
                                                             uint32_t* __restrict__ hist, uint32_t n_tiles,
                                                             uint32_t passes, unsigned long long* __restrict__ status,
-                                                            uint32_t* __restrict__ tile_ctr) {
+                                                            uint32_t* __restrict__ tile_ctr, uint32_t* __restrict__ nsplit) {
     __shared__ uint32_t h[SORT_BINS];
     griddep_wait();
     const uint32_t t = blockIdx.x, tid = threadIdx.x;
@@ -83,7 +84,10 @@ __global__ void __launch_bounds__(SORT_THREADS) k_sort_hist(const uint32_t* __re
         for (uint32_t p = 1; p < passes; ++p) hist[((uint64_t)p * n_tiles + t) * SORT_BINS + tid] = 0;
     }
     if (tid == 0) status[t] = 0ull;
-    if (t == 0 && tid == 0) *tile_ctr = 0u;
+    if (t == 0 && tid == 0) {
+        *tile_ctr = 0u;
+        *nsplit = ~0u;
+    }
     __syncthreads();
 #pragma unroll
     for (uint32_t c = 0; c < SORT_C; ++c)
@@ -196,7 +200,8 @@ __global__ void __launch_bounds__(SORT_THREADS) k_sort_runs(const uint32_t* __re
                                                             uint32_t* __restrict__ ukeys, uint32_t* __restrict__ offsets,
                                                             uint32_t* __restrict__ nruns, uint8_t* __restrict__ uniq,
                                                             unsigned long long* status, uint32_t* tile_ctr,
-                                                            uint32_t n_tiles) {
+                                                            uint32_t n_tiles, uint32_t split_key,
+                                                            uint32_t* __restrict__ nsplit) {
     constexpr unsigned long long AGG = 1ull << 32, INC = 1ull << 33;
     __shared__ uint32_t s_tile, s_prefix;
     __shared__ uint32_t warp_heads[SORT_WARPS];
@@ -214,21 +219,23 @@ __global__ void __launch_bounds__(SORT_THREADS) k_sort_runs(const uint32_t* __re
         const uint32_t j = lane == 0 ? i - 1 : i + 1;  // lane 0: the slot before, lane 31: the slot after
         edge[c] = (lane == 0 || lane == 31) && i < n && j < n ? ks[j] : 0u;
     }
-    uint32_t head_bits[SORT_C];
+    uint32_t head_bits[SORT_C], split_bits[SORT_C];
     uint32_t mine = 0;  // heads of this warp
 #pragma unroll
     for (uint32_t c = 0; c < SORT_C; ++c) {
         const uint32_t i = tile_index(t, w, c, lane);
         const uint32_t prev = __shfl_up_sync(0xffffffffu, key[c], 1);
         const uint32_t next = __shfl_down_sync(0xffffffffu, key[c], 1);
-        bool head = false;
+        bool head = false, split = false;
         if (i < n) {
             const bool prev_differs = i == 0 || (lane ? prev : edge[c]) != key[c];
+            split = key[c] >= split_key && (i == 0 || (lane ? prev : edge[c]) < split_key);
             const bool next_differs = i + 1 >= n || (lane != 31 ? next : edge[c]) != key[c];
             head = prev_differs;
             uniq[val[c]] = prev_differs && next_differs ? 1 : 0;
         }
         head_bits[c] = __ballot_sync(0xffffffffu, head);
+        split_bits[c] = __ballot_sync(0xffffffffu, split);
         mine += __popc(head_bits[c]);
     }
     if (lane == 0) warp_heads[w] = mine;
@@ -277,6 +284,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_sort_runs(const uint32_t* __re
         if (hb >> lane & 1u) {
             const uint32_t r = u + __popc(hb & lanemask_lt());
             ukeys[r] = key[c];
+            if (split_bits[c] >> lane & 1u) *nsplit = r;
             offsets[r] = tile_index(t, w, c, lane);
         }
         u += __popc(hb);
@@ -291,10 +299,11 @@ size_t slot_sort_scratch_words(uint32_t cap) {
     return (size_t)4 * slot_sort_tiles(cap) * SORT_BINS;  // up to 4 passes of per-tile histograms
 }
 
-void launch_slot_sort(const Engine& E, uint32_t n, uint32_t bits) {
+void launch_slot_sort(const Engine& E, uint32_t n, uint32_t bits, uint32_t split_key) {
     const Scratch& s = E.s;
     cudaStream_t st = E.side;
     if (n == 0) {
+        EMBER_CUDA(cudaMemsetAsync(s.nsplit, 0xff, sizeof(uint32_t), st));
         EMBER_CUDA(cudaMemsetAsync(s.nruns, 0, sizeof(uint32_t), st));
         EMBER_CUDA(cudaMemsetAsync(s.offsets, 0, sizeof(uint32_t), st));
         return;
@@ -302,7 +311,7 @@ void launch_slot_sort(const Engine& E, uint32_t n, uint32_t bits) {
     const uint32_t passes = std::max(1u, std::min(4u, (bits + 7) / 8));
     const uint32_t tiles = slot_sort_tiles(n);
     launch_pdl(k_sort_hist, dim3(tiles), dim3(SORT_THREADS), 0, st, (const uint32_t*)s.keys, n, s.sort_hist, tiles,
-               passes, s.sort_status, s.sort_ctr);
+               passes, s.sort_status, s.sort_ctr, s.nsplit);
     EMBER_LAUNCHED(E);
     // ping-pong: pass p reads src(p) and writes dst(p); the last pass writes keys_sorted / vals_sorted
     const uint32_t* kin = s.keys;
@@ -322,7 +331,7 @@ void launch_slot_sort(const Engine& E, uint32_t n, uint32_t bits) {
     }
     launch_pdl(k_sort_runs, dim3(tiles), dim3(SORT_THREADS), 0, st, (const uint32_t*)s.keys_sorted,
                (const uint32_t*)s.vals_sorted, n, s.ukeys, s.offsets, s.nruns, s.uniq, s.sort_status, s.sort_ctr,
-               tiles);
+               tiles, split_key, s.nsplit);
     EMBER_LAUNCHED(E);
 }
 

@@ -286,6 +286,30 @@ def test_direct_unique_row_updates_bit_identical(graph, monkeypatch, kind, engin
         assert a.tobytes() == b_.tobytes()
 
 
+@pytest.mark.parametrize("kind,b", [("complex", 256), ("distmult", 1500)])
+def test_relation_first_reduction_bit_identical(graph, monkeypatch, kind, b):
+    """The multi-GPU reduction order (relation keys reduced first into the dense buffer, their
+    all-reduce + dense Adagrad on the communication stream while the node keys are reduced;
+    EMBER_DENSE_RELATIONS=1 runs it at world 1) leaves every parameter bit-identical to the
+    in-place single-launch reduction — hot relations and hub nodes (long segments) included."""
+    edges, off, _ = graph
+    tabs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("EMBER_DENSE_RELATIONS", flag)
+        tr = make_trainer(kind, dim=32, b=b, nt=64, p=2, engine="tc")
+        for step, (i, j) in enumerate([(0, 1), (1, 1), (1, 0), (0, 0)]):
+            bk = i * 2 + j
+            bucket = _dev(edges[off[bk]:off[bk + 1]])
+            n = (off[bk + 1] - off[bk]) // b
+            for k in range(min(3, n)):
+                tr.train_batch(bucket, k * b, b, i, j, epoch=0, bucket_step=step, batch_in_bucket=k)
+        tr.synchronize()
+        tabs.append(host_tables(tr))
+        tr.close()
+    for a, b_ in zip(tabs[0], tabs[1]):
+        assert a.tobytes() == b_.tobytes()
+
+
 def test_host_batch_path_bit_identical(graph):
     """ember_train_batch_host (positives from pinned host memory, double-buffered asynchronous
     copies overlapping the previous step) trains exactly like ember_train_batch."""
