@@ -129,6 +129,43 @@ struct Scratch {
     float* rel_dense = nullptr;  // [R][dim] relation gradient summed over ranks (world > 1)
 };
 
+// The fixed-order sum of the dN partials over chunks, row (side, n) -> gradient slot slot0 + side nt + n
+// at its sorted position: k_dn_reduce, or the prologue of the pipelined chain rule (pending in
+// Engine::dn until then). nsides: 2, or 2 x num_chunks (tc_wide.cu).
+struct DnReduce {
+    const float4* part = nullptr;  // column-blocked [chunk][nsides][d/4][n_pad]
+    int chunks = 0, nt = 0, n_pad = 0, d = 0, nsides = 0;
+    uint32_t slot0 = 0;
+    uint32_t* flags = nullptr;  // the overflow list consumed by the fixup: counted and reset here
+    unsigned long long* flags_total = nullptr;
+};
+
+// One (side, column block, negative) item of a DnReduce; t < nsides * (d/4) * nt.
+__device__ __forceinline__ void dn_reduce_item(const DnReduce& r, int64_t t, const uint32_t* __restrict__ rank,
+                                               float* __restrict__ out) {
+    const int d4 = r.d / 4;
+    const int n = (int)(t % r.nt);
+    const int c4 = (int)((t / r.nt) % d4);
+    const int side = (int)(t / ((int64_t)r.nt * d4));
+    const float4* p = r.part + ((size_t)side * d4 + c4) * r.n_pad + n;
+    const size_t cstride = (size_t)r.nsides * d4 * r.n_pad;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int c = 0;
+    for (; c + 4 <= r.chunks; c += 4) {  // 4 loads in flight, added in chunk order
+        float4 x[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) x[i] = __ldg(p + (size_t)(c + i) * cstride);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc.x += x[i].x, acc.y += x[i].y, acc.z += x[i].z, acc.w += x[i].w;
+    }
+    for (; c < r.chunks; ++c) {
+        const float4 x = __ldg(p + (size_t)c * cstride);
+        acc.x += x.x, acc.y += x.y, acc.z += x.z, acc.w += x.w;
+    }
+    const uint32_t pos = rank[r.slot0 + side * r.nt + n];
+    reinterpret_cast<float4*>(out + (size_t)pos * r.d)[c4] = acc;
+}
+
 struct TcState;    // tensor-core engine state (tc_score.cu, d <= 128)
 struct WideState;  // tensor-core engine state for d > 128 (tc_wide.cu)
 
@@ -183,6 +220,9 @@ struct Engine {
     unsigned long long batch_tag = 0;
     void check_finite();  // throws EmberError (status 2) naming the first non-finite batch since the last check
     mutable bool loss_fused = false;
+    // the contraction's dN reduction, left to the chain rule's prologue (launch_chain_rule)
+    mutable DnReduce dn{};
+    mutable bool dn_pending = false;
     // profiling: CUDA events at phase boundaries on the step stream + our own kernel launches
     bool prof_on = false;
     std::vector<std::pair<int, cudaEvent_t>> prof_events;
@@ -235,6 +275,8 @@ struct Engine {
     void comm_init(const void* nccl_unique_id, int rank, int world);
     std::vector<double> profile_read();  // ms per phase summed over marked batches
 };
+
+void dn_reduce_run(const Engine& E, const DnReduce& r);  // k_dn_reduce on the step stream (tc_score.cu)
 
 enum Phase { PHASE_SAMPLE = 0, PHASE_GATHER = 1, PHASE_CONTRACT = 2, PHASE_CHAIN = 3, PHASE_REDUCE = 4, PHASE_END = 5 };
 

@@ -528,8 +528,17 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
                                                       const float* __restrict__ lse, const float* __restrict__ fpos,
                                                       double* __restrict__ loss_part, uint32_t* __restrict__ loss_done,
                                                       float* __restrict__ loss_out, unsigned long long* bad,
-                                                      unsigned long long tag) {
+                                                      unsigned long long tag, DnReduce dn, int dn_on) {
     griddep_wait();
+    if (dn_on) {  // the contraction's dN reduction first (independent of the edges below: other slots)
+        if (blockIdx.x == 0 && threadIdx.x == 0) {  // overflow list consumed (k_tc_fixup): count, reset
+            dn.flags_total[0] += dn.flags[0];
+            *dn.flags = 0u;
+        }
+        const int64_t total = (int64_t)dn.nsides * (dn.d / 4) * dn.nt, step = (int64_t)gridDim.x * blockDim.x;
+        for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += step)
+            dn_reduce_item(dn, t, rank, grows);
+    }
     extern __shared__ float4 cpbuf[];  // [warps][2 stages][CP_ROLES][32 lanes]
     const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + wib, nw = gridDim.x * (blockDim.x >> 5);
@@ -1397,9 +1406,14 @@ void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, cons
                    (const float*)E.s.g0, (const uint32_t*)E.s.rank, (const uint8_t*)E.s.uniq, E.s.grows,
                    E.direct_hi ? 1 : 0, E.m.lr, E.m.eps, (const float*)E.s.lse, (const float*)E.s.fpos,
                    reinterpret_cast<double*>(E.s.loss_part), E.s.loss_done, E.loss_target, E.s.bad_batch,
-                   E.batch_tag);
+                   E.batch_tag, E.dn, E.dn_pending ? 1 : 0);
+        E.dn_pending = false;
         E.loss_fused = true;
     } else {
+        if (E.dn_pending) {
+            dn_reduce_run(E, E.dn);
+            E.dn_pending = false;
+        }
         k_chain_rule<<<(nb + warps - 1) / warps, warps * 32, 0, E.stream>>>(
             edges, nb, E.n_neg, pi, pj, E.rel_theta, E.m.kind, E.dim, E.s.dA, E.tc_engine() ? (uint32_t)E.b_cap : 0u,
             E.s.g0, E.s.rank, E.s.grows, E.s.keys_sorted, E.slots(nb), E.direct_hi ? 1 : 0, E.m.lr, E.m.eps);

@@ -24,7 +24,7 @@
 //              k_tc_fixup before anything reads lse.
 //   MODE_NEGS  item = 128-negative tile of N (resident) x a chunk of 128-row tiles of A:
 //              S^T = N A^T, P^T = exp(S^T - lse)/b, dN += P^T A; per-chunk partials are summed
-//              in a fixed order by k_dn_reduce (deterministic).
+//              in a fixed order by the dN reduction (k_dn_reduce / the chain rule's prologue).
 // TMEM (512 columns): [0,128) and [128,256) two S buffers of 128 fp32 columns, each overwritten
 // in place by P as bf16 pairs (per 32-column chunk: 16 hi columns then 16 lo columns) — the A
 // operand of the second product (TS mode); [256,256+KP) the accumulator; [384,384+KP) the
@@ -649,7 +649,7 @@ __global__ void k_tc_fixup(TcArgs g, const uint16_t* __restrict__ Apk, const uin
             const int side = i / (g.rows_pad - g.rows128), row = g.rows128 + i % (g.rows_pad - g.rows128);
             g.lse_pad[(size_t)side * g.b_cap + row] = -INFINITY;
         }
-    // (the flag count is reset by k_dn_reduce, after every reader)
+    // (the flag count is reset by the dN reduction, after every reader)
 }
 
 // =========================================================================================
@@ -660,37 +660,15 @@ __global__ void k_tc_fixup(TcArgs g, const uint16_t* __restrict__ Apk, const uin
 // goes to its sorted position grows[rank[slot]]. Thread per (side, column block, negative): the
 // column-blocked partials [chunk][side][d/4][n_pad] float4 are read coalesced along n.
 // nsides: 2 (one shared negative set per side), or 2 x num_chunks ([chunk][side] sets, tc_wide.cu).
-__global__ void k_dn_reduce(const float4* __restrict__ part, int chunks, int nt, int n_pad, int d,
-                            const uint32_t* __restrict__ rank, uint32_t slot0, float* __restrict__ out,
-                            uint32_t* flags, unsigned long long* flags_total, int nsides) {
+__global__ void k_dn_reduce(DnReduce r, const uint32_t* __restrict__ rank, float* __restrict__ out) {
     griddep_wait();
     if (blockIdx.x == 0 && threadIdx.x == 0) {  // overflow list consumed (k_tc_fixup): count, reset
-        flags_total[0] += flags[0];
-        *flags = 0u;
+        r.flags_total[0] += r.flags[0];
+        *r.flags = 0u;
     }
-    const int d4 = d / 4;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= (int64_t)nsides * d4 * nt) return;
-    const int n = (int)(t % nt);
-    const int c4 = (int)((t / nt) % d4);
-    const int side = (int)(t / ((int64_t)nt * d4));
-    const float4* p = part + ((size_t)side * d4 + c4) * n_pad + n;
-    const size_t cstride = (size_t)nsides * d4 * n_pad;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    int c = 0;
-    for (; c + 4 <= chunks; c += 4) {  // 4 loads in flight, added in chunk order
-        float4 x[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) x[i] = __ldg(p + (size_t)(c + i) * cstride);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) acc.x += x[i].x, acc.y += x[i].y, acc.z += x[i].z, acc.w += x[i].w;
-    }
-    for (; c < chunks; ++c) {
-        const float4 x = __ldg(p + (size_t)c * cstride);
-        acc.x += x.x, acc.y += x.y, acc.z += x.z, acc.w += x.w;
-    }
-    const uint32_t pos = rank[slot0 + side * nt + n];
-    reinterpret_cast<float4*>(out + (size_t)pos * d)[c4] = acc;
+    if (t >= (int64_t)r.nsides * (r.d / 4) * r.nt) return;
+    dn_reduce_item(r, t, rank, out);
 }
 
 // ---- tensor maps (driver entry point fetched through the runtime: no libcuda link) ---------
@@ -749,10 +727,23 @@ CUtensorMap make_packed_map(uint16_t* base, int cap, int nblocks2, int box_rows,
 // The fixed-order dN reduction of k_dn_reduce for the wide engine's partials (tc_wide.cu).
 void dn_reduce_launch(Engine& E, const float* part, int chunks, int nt, int n_pad, int d, uint32_t slot0,
                       uint32_t* flags, unsigned long long* flags_total, int nsides) {
-    const int64_t r = (int64_t)nsides * nt * (d / 4);
-    launch_pdl(k_dn_reduce, dim3((unsigned)((r + 255) / 256)), dim3(256), 0, E.stream,
-               reinterpret_cast<const float4*>(part), chunks, nt, n_pad, d, (const uint32_t*)E.s.rank, slot0, E.s.grows,
-               flags, flags_total, nsides);
+    DnReduce r;
+    r.part = reinterpret_cast<const float4*>(part);
+    r.chunks = chunks;
+    r.nt = nt;
+    r.n_pad = n_pad;
+    r.d = d;
+    r.nsides = nsides;
+    r.slot0 = slot0;
+    r.flags = flags;
+    r.flags_total = flags_total;
+    dn_reduce_run(E, r);
+}
+
+void dn_reduce_run(const Engine& E, const DnReduce& r) {
+    const int64_t n = (int64_t)r.nsides * r.nt * (r.d / 4);
+    launch_pdl(k_dn_reduce, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, E.stream, r, (const uint32_t*)E.s.rank,
+               E.s.grows);
     EMBER_LAUNCHED(E);
 }
 
@@ -942,12 +933,19 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
         }
     }
     if (tr) dump(".negs.bin");
-    const int64_t r = (int64_t)2 * nt * (d / 4);
-    E.join_sorted();
-    launch_pdl(k_dn_reduce, dim3((unsigned)((r + 255) / 256)), dim3(256), 0, E.stream,
-               reinterpret_cast<const float4*>(t.dN_part), a.chunks2, nt, t.n_pad, d, (const uint32_t*)s.rank, 2 * nb,
-               s.grows, t.flags, t.flags_total, 2);
-    EMBER_LAUNCHED(E);
+    // the fixed-order dN reduction: the chain rule's prologue (launch_chain_rule) does it
+    DnReduce& r = E.dn;
+    r.part = reinterpret_cast<const float4*>(t.dN_part);
+    r.chunks = a.chunks2;
+    r.nt = nt;
+    r.n_pad = t.n_pad;
+    r.d = d;
+    r.nsides = 2;
+    r.slot0 = 2 * nb;
+    r.flags = t.flags;
+    r.flags_total = t.flags_total;
+    E.dn_pending = true;
+    (void)s;
 }
 
 }  // namespace ember
