@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
                                                       unsigned long long tag, DnReduce dn, int dn_on) {
     griddep_wait();
     if (dn_on) {  // the contraction's dN reduction first (independent of the edges below: other slots)
-        if (blockIdx.x == 0 && threadIdx.x == 0) {  // overflow list consumed (k_tc_fixup): count, reset
+        if (blockIdx.x == 0 && threadIdx.x == 0) {  // overflow list consumed (tc_fixup_rows): count, reset
             dn.flags_total[0] += dn.flags[0];
             *dn.flags = 0u;
         }

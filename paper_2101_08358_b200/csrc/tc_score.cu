@@ -21,7 +21,7 @@
 //              is part of every row's log-sum-exp, so no online rescaling is needed), dA += P N.
 //              Item end: lse = f_pos + log(1 + sum P), g0 = (exp(f_pos - lse) - 1)/b, dA/(Z b).
 //              Rows whose sum overflows the safe range are listed and recomputed exactly by
-//              k_tc_fixup before anything reads lse.
+//              by the dN kernel's CTAs (tc_fixup_rows) before anything reads lse.
 //   MODE_NEGS  item = 128-negative tile of N (resident) x a chunk of 128-row tiles of A:
 //              S^T = N A^T, P^T = exp(S^T - lse)/b, dN += P^T A; per-chunk partials are summed
 //              in a fixed order by the dN reduction (k_dn_reduce / the chain rule's prologue).
@@ -89,6 +89,12 @@ struct TcArgs {
     int dyn;
     uint32_t* claim;
     uint32_t claim_base;
+    // MODE_NEGS: rows flagged by the rows kernel are recomputed exactly by the dN kernel's CTAs
+    // before any reads their lse (all CTAs arrive on fix_bar; they wait only when a row is flagged)
+    const uint16_t* Apk;
+    const uint16_t* Npk;
+    uint32_t* fix_bar;
+    uint32_t fix_base;
 };
 
 // Debug timeline: (clock64, event << 32 | arg) records from CTA 0's producer, MMA issuer and one
@@ -297,9 +303,11 @@ __device__ __forceinline__ int work_fetch(uint64_t* bars, uint32_t it) {
 // after the boundary, by when its tail is done. (EMBER_TC_EARLY=1: plain alternation, A/B.)
 __device__ __forceinline__ int tile_group(int k, int early) { return k < early ? 0 : (k & 1); }
 
+__device__ __noinline__ void tc_fixup_rows(const TcArgs& g, uint32_t n);
+
 template <int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
-    k_tc(const __grid_constant__ CUtensorMap mapR, const __grid_constant__ CUtensorMap mapT, TcArgs g) {
+    k_tc(const __grid_constant__ CUtensorMap mapR, const __grid_constant__ CUtensorMap mapT, const __grid_constant__ TcArgs g) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     const Smem sm = carve<MODE>(smem_raw, g.KP, g.nstage);
     const int NSTAGE = g.nstage;
@@ -354,6 +362,31 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         g.cta_times[2 * blockIdx.x] = t;
+    }
+    if (MODE == MODE_ROWS && blockIdx.x == 0) {
+        // streamed 96-row tiles may reach past the last 128-row item: those rows never score
+        for (int i = threadIdx.x; i < 2 * (g.rows_pad - g.rows128); i += blockDim.x) {
+            const int side = i / (g.rows_pad - g.rows128), row = g.rows128 + i % (g.rows_pad - g.rows128);
+            g.lse_pad[(size_t)side * g.b_cap + row] = -INFINITY;
+        }
+    }
+    if (MODE == MODE_NEGS) {  // rows the rows kernel flagged: exact recompute before any lse is read
+        const uint32_t nflag = *(volatile uint32_t*)g.flags;
+        if (nflag) {
+            tc_fixup_rows(g, nflag);
+            __threadfence();
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // the producers read lse_pad by TMA
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            atomicAdd(g.fix_bar, 1u);
+            if (nflag) {  // every CTA's repairs visible before any producer loads an lse
+                while ((int)(*(volatile uint32_t*)g.fix_bar - (g.fix_base + gridDim.x)) < 0) __nanosleep(64);
+                __threadfence();
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
+        }
+        __syncthreads();
     }
 
     if (warp == 0) {
@@ -603,9 +636,9 @@ __device__ __forceinline__ float packed_at(const uint16_t* pk, int cap, int CB, 
     return __bfloat162float(__ushort_as_bfloat16(pk[hi])) + __bfloat162float(__ushort_as_bfloat16(pk[lo]));
 }
 
-__global__ void k_tc_fixup(TcArgs g, const uint16_t* __restrict__ Apk, const uint16_t* __restrict__ Npk) {
-    griddep_wait();
-    const uint32_t n = *(volatile uint32_t*)g.flags;
+__device__ __noinline__ void tc_fixup_rows(const TcArgs& g, uint32_t n) {
+    const uint16_t* __restrict__ Apk = g.Apk;
+    const uint16_t* __restrict__ Npk = g.Npk;
     const int lane = threadIdx.x & 31;
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t f = gw; f < n; f += nw) {  // a warp per flagged row, all blocks
@@ -643,12 +676,6 @@ __global__ void k_tc_fixup(TcArgs g, const uint16_t* __restrict__ Apk, const uin
             g.g0[(size_t)side * g.nb + row] = (expf(fp - lse) - 1.0f) * g.inv_b;
         }
     }
-    // streamed 96-row tiles may reach past the last 128-row item: those rows never score
-    if (blockIdx.x == 0)
-        for (int i = threadIdx.x; i < 2 * (g.rows_pad - g.rows128); i += blockDim.x) {
-            const int side = i / (g.rows_pad - g.rows128), row = g.rows128 + i % (g.rows_pad - g.rows128);
-            g.lse_pad[(size_t)side * g.b_cap + row] = -INFINITY;
-        }
     // (the flag count is reset by the dN reduction, after every reader)
 }
 
@@ -662,7 +689,7 @@ __global__ void k_tc_fixup(TcArgs g, const uint16_t* __restrict__ Apk, const uin
 // nsides: 2 (one shared negative set per side), or 2 x num_chunks ([chunk][side] sets, tc_wide.cu).
 __global__ void k_dn_reduce(DnReduce r, const uint32_t* __restrict__ rank, float* __restrict__ out) {
     griddep_wait();
-    if (blockIdx.x == 0 && threadIdx.x == 0) {  // overflow list consumed (k_tc_fixup): count, reset
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // overflow list consumed (tc_fixup_rows): count, reset
         r.flags_total[0] += r.flags[0];
         *r.flags = 0u;
     }
@@ -762,6 +789,8 @@ struct TcState {
     uint32_t* arrive = nullptr;     // [3]: CTA arrival counters of the rows / dN kernels, rows-item claims (never reset)
     uint32_t arrive_base[2] = {0, 0};
     uint32_t claim_base = 0;
+    uint32_t* fix_bar = nullptr;    // dN-kernel CTA arrivals (never reset) and their expected count
+    uint32_t fix_base = 0;
     bool dyn = true;                // dynamic rows-item claims (EMBER_TC_DYNAMIC=0: static grid stride)
     std::string trace_path;
     int trace_calls = 0;
@@ -791,6 +820,8 @@ void tc_setup(Engine& E) {
     if (getenv("EMBER_TC_CTATIMES")) EMBER_CUDA(cudaMalloc(&t->cta_times, (size_t)2 * 2 * E.sm_count * 8));
     EMBER_CUDA(cudaMalloc(&t->arrive, 3 * sizeof(uint32_t)));
     EMBER_CUDA(cudaMemset(t->arrive, 0, 3 * sizeof(uint32_t)));
+    EMBER_CUDA(cudaMalloc(&t->fix_bar, sizeof(uint32_t)));
+    EMBER_CUDA(cudaMemset(t->fix_bar, 0, sizeof(uint32_t)));
     if (const char* s = getenv("EMBER_TC_DYNAMIC")) t->dyn = atoi(s) != 0;
     if (const char* s = getenv("EMBER_TC_TRACE")) {
         t->trace_path = s;
@@ -831,6 +862,7 @@ void tc_release(Engine& E) {
     if (E.tc->trace) cudaFree(E.tc->trace);
     if (E.tc->cta_times) cudaFree(E.tc->cta_times);
     cudaFree(E.tc->arrive);
+    cudaFree(E.tc->fix_bar);
     delete E.tc;
     E.tc = nullptr;
 }
@@ -910,11 +942,13 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
         dump(".rows.bin");
         EMBER_CUDA(cudaMemsetAsync(t.trace, 0, (size_t)2 * 5 * TRACE_ROLE * 8, E.stream));
     }
-    // normally no row is flagged and every block exits at once; when training drives scores far
-    // apart the flagged rows are spread over the whole GPU (a warp each)
-    launch_pdl(k_tc_fixup, dim3(E.sm_count * 2), dim3(256), 0, E.stream, a, (const uint16_t*)s.Apk,
-               (const uint16_t*)s.Npk);
-    EMBER_LAUNCHED(E);
+    // rows flagged by the rows kernel (normally none) are recomputed by the dN kernel's CTAs, a warp
+    // each, before its producers load any lse (tc_fixup_rows)
+    a.Apk = s.Apk;
+    a.Npk = s.Npk;
+    a.fix_bar = t.fix_bar;
+    a.fix_base = t.fix_base;
+    t.fix_base += (uint32_t)std::min(items2, gmax);
     if (ct) a.cta_times = t.cta_times + 2 * E.sm_count;
     a.arrive = t.arrive + 1;
     a.arrive_base = t.arrive_base[1];
