@@ -252,12 +252,7 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     s.longs = dalloc<uint32_t>(2 + 3 * max_long);
     s.long_owner = dalloc<uint32_t>(max_chunks);
     s.long_partial = dalloc<float>((uint64_t)max_chunks * d);
-    {  // relation keys: at most cap_b rows
-        const uint32_t rl = cap_b / EMBER_LONG_SEG + 1, rc = cap_b / EMBER_LONG_CHUNK + rl;
-        s.longs_rel = dalloc<uint32_t>(2 + 3 * rl);
-        s.long_owner_rel = dalloc<uint32_t>(rc);
-        s.long_partial_rel = dalloc<float>((uint64_t)rc * d);
-    }
+
     EMBER_CUDA(cudaMemset(s.nunique, 0, 2 * sizeof(uint32_t)));
     EMBER_CUDA(cudaMemset(s.longs, 0, 2 * sizeof(uint32_t)));
     if (m.engine == EMBER_ENGINE_SIMT_FP32) {
@@ -289,8 +284,7 @@ Engine::~Engine() {
                     s.S,     s.dA,        s.dN_part, s.grows,    s.loss,    s.loss_part,  s.loss_done,  s.bad_batch,
                     s.nunique, s.long_partial, s.rel_dense, s.negs, s.keys, s.keys_sorted, s.vals, s.vals_sorted,
                     s.rank, s.ukeys, s.offsets, s.nruns, s.longs, s.long_owner, s.uniq, s.sort_keys[0],
-                    s.sort_keys[1], s.sort_vals[0], s.sort_vals[1], s.sort_hist, s.sort_status, s.sort_ctr, s.nsplit,
-                    s.longs_rel, s.long_owner_rel, s.long_partial_rel};
+                    s.sort_keys[1], s.sort_vals[0], s.sort_vals[1], s.sort_hist, s.sort_status, s.sort_ctr, s.nsplit};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (void* p : owned) cudaFree(p);
@@ -360,6 +354,7 @@ void Engine::sort_keys(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t 
 void Engine::sort_slots(uint32_t nb, const KeySpace& ks) {
     const uint32_t n = slots(nb);
     launch_slot_sort(*this, slots(nb), ks.bits, (uint32_t)ks.node_range);
+    launch_long_plan(*this, slots(nb));
     EMBER_CUDA(cudaEventRecord(ev_sorted, side));
     sorted_pending = true;
 }

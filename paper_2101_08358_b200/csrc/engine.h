@@ -115,10 +115,7 @@ struct Scratch {
     uint32_t* longs = nullptr;        // [2 + 3 * cap]: long segments, chunk slots, then (u, base, nch)
     uint32_t* long_owner = nullptr;   // chunk slot -> long segment
     float* long_partial = nullptr;    // chunk slot -> partial row
-    // the relation part's own long-segment list (relation keys reduced on the comm stream, world > 1)
-    uint32_t* longs_rel = nullptr;
-    uint32_t* long_owner_rel = nullptr;
-    float* long_partial_rel = nullptr;
+
     // slot sort (sort.cu): ping-pong key/value buffers, per-tile digit histograms, run-scan state
     uint32_t* sort_keys[2] = {nullptr, nullptr};
     uint32_t* sort_vals[2] = {nullptr, nullptr};
@@ -338,6 +335,8 @@ void launch_contract_simt(Engine& E, uint32_t nb);
 void launch_contract_tc(Engine& E, uint32_t nb);
 void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj);
 void launch_loss(const Engine& E, uint32_t nb, float* loss_out);
+// the long-segment chunk plan (keys with > EMBER_LONG_SEG rows) on the helper stream after the sort
+void launch_long_plan(const Engine& E, uint32_t n_slots);
 // part: 0 every key, 1 relation keys only, 2 node keys only (the split: s.nsplit)
 void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool apply, bool rel_dense,
                      uint32_t* node_ids_out, float* node_rows_out, uint32_t* rel_ids_out, float* rel_rows_out,

@@ -9,8 +9,10 @@
 //   k_keys            gradient-slot keys for the (key, slot) sort (sort.cu)
 //   k_chain_rule      chain rule back through adjust, rows written in sorted order
 //   k_loss            deterministic loss reduction (fixed-order partials, last block finishes)
-//   k_segments, k_long_partial, k_long_final
-//                     segmented sum of the sorted gradient rows + sparse Adagrad
+//   k_long_plan       (helper stream, after the sort) chunk plan of the keys with many rows
+//   k_segments(_pipe), k_long_final
+//                     segmented sum of the sorted gradient rows + sparse Adagrad;
+//                     long keys as chunk partials (the segment kernels' prologue) + k_long_final
 // Rows are dim floats (dim % 4 == 0) and are moved warp-per-row with 128-bit accesses.
 #include <cuda_runtime.h>
 
@@ -888,10 +890,14 @@ __device__ __forceinline__ void sum_rows2(const float* base, uint32_t cnt, uint3
 // half sums its key's contiguous rows (slot order) and applies Adagrad / export. A lane owns
 // column blocks c4 and c4 + 16 (d <= 128; larger d loops).
 constexpr uint32_t SEG_LANES = 16;
-__global__ void __launch_bounds__(256, 4) k_segments(SegArgs a) {
+__device__ __forceinline__ void long_partials(const SegArgs& a, uint32_t gw, uint32_t nw, uint32_t lane);
+
+__global__ void __launch_bounds__(256, 4) k_segments(const __grid_constant__ SegArgs a) {
+    griddep_wait();
     const uint32_t lane = threadIdx.x & 31, hl = lane & (SEG_LANES - 1);
-    const uint32_t u = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 2 + (lane >> 4);
-    const uint32_t hmask = lane < SEG_LANES ? 0x0000ffffu : 0xffff0000u;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t u = gw * 2 + (lane >> 4);
+    long_partials(a, gw, (gridDim.x * blockDim.x) >> 5, lane);  // the long segments' chunk partials first
     const uint32_t nr = *a.nruns;
     uint32_t lo, hi;
     seg_range(a, nr, lo, hi);
@@ -903,22 +909,7 @@ __global__ void __launch_bounds__(256, 4) k_segments(SegArgs a) {
     }
     const uint32_t off = a.offsets[u], cnt = a.offsets[u + 1] - off;
     if (cnt == 1 && key < a.ks.node_range && a.vals_sorted[off] < a.direct_hi) return;  // applied already
-    if (cnt > LONG_SEG) {  // reserve chunk slots for the long path
-        const uint32_t nch = (cnt + LONG_CHUNK - 1) / LONG_CHUNK;
-        uint32_t li = 0, base = 0;
-        if (hl == 0) {
-            li = atomicAdd(&a.longs[0], 1u);
-            base = atomicAdd(&a.longs[1], nch);
-            uint32_t* rec = a.longs + 2 + 3 * li;
-            rec[0] = u;
-            rec[1] = base;
-            rec[2] = nch;
-        }
-        li = __shfl_sync(hmask, li, 0, SEG_LANES);
-        base = __shfl_sync(hmask, base, 0, SEG_LANES);
-        for (uint32_t c = hl; c < nch; c += SEG_LANES) a.owner[base + c] = li;
-        return;
-    }
+    if (cnt > LONG_SEG) return;  // chunked (long_partials, k_long_final)
     const SegTarget t = seg_target(a, u, nr, hl == 0);
     const bool app = seg_applies(a, t);
     const float* base = a.rows + (uint64_t)off * a.d;
@@ -956,13 +947,14 @@ struct SegMeta {
     uint32_t key, off, cnt, next_key;
 };
 
-__global__ void __launch_bounds__(256, 4) k_segments_pipe(SegArgs a) {
+__global__ void __launch_bounds__(256, 4) k_segments_pipe(const __grid_constant__ SegArgs a) {
     griddep_wait();
+    long_partials(a, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, (gridDim.x * blockDim.x) >> 5,
+                  threadIdx.x & 31);  // the long segments' chunk partials first
     extern __shared__ float4 sst[];  // [warps][2 halves][2 stages][2 roles][2 column blocks][16 lanes]
     const uint32_t lane = threadIdx.x & 31, hl = lane & (SEG_LANES - 1), half = lane >> 4, wib = threadIdx.x >> 5;
     const uint32_t gh = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 2 + half;
     const uint32_t nh = ((gridDim.x * blockDim.x) >> 5) * 2;
-    const uint32_t hmask = half == 0 ? 0x0000ffffu : 0xffff0000u;
     const uint32_t nr = *a.nruns, d4 = a.d / 4;
     uint32_t u_lo, u_hi;
     seg_range(a, nr, u_lo, u_hi);
@@ -987,22 +979,9 @@ __global__ void __launch_bounds__(256, 4) k_segments_pipe(SegArgs a) {
             }
             k.off = m.off;
             k.cnt = m.cnt;
-            const bool done = k.cnt == 1 && key < a.ks.node_range && a.vals_sorted[k.off] < a.direct_hi;
-            if (!done && k.cnt > LONG_SEG) {  // reserve chunk slots for the long path
-                const uint32_t nch = (k.cnt + LONG_CHUNK - 1) / LONG_CHUNK;
-                uint32_t li = 0, base = 0;
-                if (hl == 0) {
-                    li = atomicAdd(&a.longs[0], 1u);
-                    base = atomicAdd(&a.longs[1], nch);
-                    uint32_t* rec = a.longs + 2 + 3 * li;
-                    rec[0] = u;
-                    rec[1] = base;
-                    rec[2] = nch;
-                }
-                li = __shfl_sync(hmask, li, 0, SEG_LANES);
-                base = __shfl_sync(hmask, base, 0, SEG_LANES);
-                for (uint32_t c = hl; c < nch; c += SEG_LANES) a.owner[base + c] = li;
-            } else if (!done) {
+            const bool done = (k.cnt == 1 && key < a.ks.node_range && a.vals_sorted[k.off] < a.direct_hi) ||
+                              k.cnt > LONG_SEG;  // applied by the chain rule / chunked (long_partials)
+            if (!done) {
                 k.active = true;
                 k.t = seg_target(a, u, nr, hl == 0);
                 if (seg_applies(a, k.t))
@@ -1105,12 +1084,13 @@ __device__ __forceinline__ float4 shfl_xor4(float4 v, int m) {
 
 // One warp per chunk slot of the long segments: partial[slot] = sum of its <= LONG_CHUNK rows;
 // the two half-warps take the even and the odd rows, then even + odd (fixed order).
-__global__ void k_long_partial(SegArgs a) {
-    griddep_wait();
-    const uint32_t lane = threadIdx.x & 31, hl = lane & 15, half = lane >> 4;
-    const uint32_t nw = (gridDim.x * blockDim.x) >> 5, d4 = a.d / 4;
-    const uint32_t n_slots = *(volatile uint32_t*)&a.longs[1];
-    for (uint32_t sl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < n_slots; sl += nw) {
+// Warp gw's share of the long segments' chunk partials (the segment kernels' prologue):
+// partial[slot] = sum of its <= LONG_CHUNK rows; the two half-warps take the even and the odd rows,
+// then even + odd (fixed order). The chunk plan comes from k_long_plan (helper stream, after the sort).
+__device__ __forceinline__ void long_partials(const SegArgs& a, uint32_t gw, uint32_t nw, uint32_t lane) {
+    const uint32_t hl = lane & 15, half = lane >> 4, d4 = a.d / 4;
+    const uint32_t n_slots = a.longs[1];
+    for (uint32_t sl = gw; sl < n_slots; sl += nw) {
         const uint32_t* rec = a.longs + 2 + 3 * a.owner[sl];
         const uint32_t u = rec[0], c = sl - rec[1];
         if (!seg_in_part(a, u)) continue;  // warp-uniform: reduced by the other launch
@@ -1135,6 +1115,25 @@ __global__ void k_long_partial(SegArgs a) {
             }
         }
     }
+}
+
+// The reduction's long-segment plan, on the helper stream after the sort (thread per run): keys with
+// more than LONG_SEG rows get LONG_CHUNK-row chunk slots (record (u, base, nch), owner per slot).
+__global__ void k_long_plan(const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ nruns, uint32_t n_max,
+                            uint32_t* __restrict__ longs, uint32_t* __restrict__ owner) {
+    griddep_wait();
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= *nruns || u >= n_max) return;
+    const uint32_t cnt = offsets[u + 1] - offsets[u];
+    if (cnt <= LONG_SEG) return;
+    const uint32_t nch = (cnt + LONG_CHUNK - 1) / LONG_CHUNK;
+    const uint32_t li = atomicAdd(&longs[0], 1u);
+    const uint32_t base = atomicAdd(&longs[1], nch);
+    uint32_t* rec = longs + 2 + 3 * li;
+    rec[0] = u;
+    rec[1] = base;
+    rec[2] = nch;
+    for (uint32_t c = 0; c < nch; ++c) owner[base + c] = li;
 }
 
 // One block per long segment: 2 * LONG_WARPS half-warp streams each add the chunk partials
@@ -1440,9 +1439,6 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
                      int part, cudaStream_t st) {
     if (!n_slots) return;
     if (!st) st = E.stream;
-    // the relation part keeps its long segments in a list of its own (it runs beside the node part)
-    const bool own = part == 1;
-    if (own) EMBER_CUDA(cudaMemsetAsync(E.s.longs_rel, 0, 2 * sizeof(uint32_t), st));
     SegArgs a{};
     a.part = part;
     a.nsplit = E.s.nsplit;
@@ -1450,9 +1446,9 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
     a.offsets = E.s.offsets;
     a.nruns = E.s.nruns;
     a.nunique = E.s.nunique;
-    a.longs = own ? E.s.longs_rel : E.s.longs;
-    a.owner = own ? E.s.long_owner_rel : E.s.long_owner;
-    a.partial = own ? E.s.long_partial_rel : E.s.long_partial;
+    a.longs = E.s.longs;
+    a.owner = E.s.long_owner;
+    a.partial = E.s.long_partial;
     a.rows = E.s.grows;
     a.ks = ks;
     a.rel_theta = E.rel_theta;
@@ -1477,12 +1473,17 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
         k_segments<<<(n_slots * 16 + 255) / 256, 256, 0, st>>>(a);  // 2 keys per warp
     }
     EMBER_LAUNCHED(E);
-    launch_pdl(k_long_partial, dim3(2 * E.sm_count), dim3(256), 0, st, a);
-    EMBER_LAUNCHED(E);
     const size_t lf_smem = 2 * LONG_WARPS * E.dim * sizeof(float);  // > 48 KB from d = 376 on (C5: d = 800)
     opt_in_smem((const void*)k_long_final, lf_smem, E.device);
     launch_pdl(k_long_final, dim3(E.sm_count), dim3(32 * LONG_WARPS), lf_smem, st,
                a);
+    EMBER_LAUNCHED(E);
+}
+
+void launch_long_plan(const Engine& E, uint32_t n_slots) {
+    if (!n_slots) return;
+    launch_pdl(k_long_plan, dim3((n_slots + 255) / 256), dim3(256), 0, E.side, (const uint32_t*)E.s.offsets,
+               (const uint32_t*)E.s.nruns, n_slots, E.s.longs, E.s.long_owner);
     EMBER_LAUNCHED(E);
 }
 
