@@ -236,6 +236,9 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     s.uniq = dalloc<uint8_t>(cap_rows);
     s.ukeys = dalloc<uint32_t>(cap_rows);
     s.offsets = dalloc<uint32_t>(cap_rows + 1);  // offsets[nruns] = n closes the last run
+    // (runs past nruns are never read by the step; zeroed once so whole-buffer copies are defined)
+    EMBER_CUDA(cudaMemset(s.ukeys, 0, (size_t)cap_rows * sizeof(uint32_t)));
+    EMBER_CUDA(cudaMemset(s.offsets, 0, (size_t)(cap_rows + 1) * sizeof(uint32_t)));
     for (int k = 0; k < 2; ++k) {
         s.sort_keys[k] = dalloc<uint32_t>(cap_rows);
         s.sort_vals[k] = dalloc<uint32_t>(cap_rows);

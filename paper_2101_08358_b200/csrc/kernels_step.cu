@@ -113,8 +113,10 @@ __device__ __forceinline__ void negs_pack_warp(uint32_t w, uint32_t lane, const 
     float x[8];
     if (slot < nt) {
         const float* src = node_row(side == 0 ? pj : pi, negs[side * nt + slot], d);
-        const float4 a = ldg4(src + 8 * lane);  // d % 4 == 0: the second quad is all in or all out
-        const float4 b = 8 * lane + 4 < d ? ldg4(src + 8 * lane + 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        // d % 4 == 0: each quad is all in or all out (lanes past d read nothing: the K padding is 0)
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 a = 8 * lane < d ? ldg4(src + 8 * lane) : z;
+        const float4 b = 8 * lane + 4 < d ? ldg4(src + 8 * lane + 4) : z;
         x[0] = a.x, x[1] = a.y, x[2] = a.z, x[3] = a.w, x[4] = b.x, x[5] = b.y, x[6] = b.z, x[7] = b.w;
     } else {
 #pragma unroll

@@ -284,9 +284,10 @@ __device__ __forceinline__ void epi_chunk(uint32_t tS, int c0, int k, const TcAr
 }
 
 // The item of work `it` (published by the producer; items = no more work).
+// (shared-memory atomics: the slot is written by the producer while the other roles poll it)
 __device__ __forceinline__ void work_publish(uint64_t* bars, uint32_t it, int item) {
-    volatile uint64_t* w = bars + B_WORK + (it % WORK_SLOTS);
-    *w = ((uint64_t)it << 32) | (uint32_t)item;
+    auto* w = reinterpret_cast<unsigned long long*>(bars + B_WORK + (it % WORK_SLOTS));
+    atomicExch(w, ((unsigned long long)it << 32) | (uint32_t)item);
 }
 __device__ __forceinline__ int work_fetch(uint64_t* bars, uint32_t it) {
     volatile uint64_t* w = bars + B_WORK + (it % WORK_SLOTS);
@@ -346,7 +347,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tc::tmap_prefetch(&mapR);
         tc::tmap_prefetch(&mapT);
         tslot[1] = atomicAdd(g.arrive, 1u) - g.arrive_base;  // this CTA's rank in arrival order
-        for (uint32_t w = 0; w < WORK_SLOTS; ++w) bars[B_WORK + w] = ~0ull;  // no work published yet
+        for (uint32_t w = 0; w < WORK_SLOTS; ++w)  // no work published yet
+            atomicExch(reinterpret_cast<unsigned long long*>(bars + B_WORK + w), ~0ull);
     }
     if (warp == 1) tc::tmem_alloc(tslot, TCOLS);
     tc::fence_before();

@@ -2,7 +2,8 @@
 """Small training workload for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
 the tensor-core engine's kernels (TMA + mbarrier + tcgen05 pipelines, k_tc<ROWS/NEGS>, the fixup),
 the cp.async-pipelined chain rule and segmented Adagrad, the gather/pack, sampling and key sort, eval,
-plus the partition buffer, at small sizes (several items per CTA through a capped grid)."""
+the wide tensor-core path, the forced overflow repair, the multi-GPU relation path at world 1, plus
+the partition buffer, at small sizes (several items per CTA through a capped grid)."""
 import os
 import sys
 
@@ -32,6 +33,28 @@ def main():
         tr.eval_ranks(dev[:200], dev, n_eval=100, block=100)
         tr.synchronize()
         tr.close()
+    # the wide tensor-core path (d > 128, chunked negatives), the overflow fixup forced on every row
+    # (repaired inside the dN kernel), the multi-GPU relation path at world 1 (communication stream)
+    for kind, dim, nt, b, chunks, env in (("complex", 160, 200, 256, 1, {}), ("distmult", 32, 64, 256, 2, {}),
+                                          ("complex", 32, 64, 256, 1, {"EMBER_TC_ZMAX": "0"}),
+                                          ("complex", 32, 64, 256, 1, {"EMBER_DENSE_RELATIONS": "1"})):
+        os.environ.update(env)
+        h = eb.Hyper(kind=kind, dim=dim, batch_size=b, num_negatives=nt, num_chunks=chunks, neg_seed=3, engine="tc")
+        tr = eb.Trainer(h, V, R, p, device=0)
+        tr.init_embeddings(11)
+        tr.train_epoch(dev, off, plan["seq"], 0)
+        tr.synchronize()
+        tr.close()
+        for k in env:
+            del os.environ[k]
+    # the (key, slot) sort on its own (bits 24 and 32)
+    h = eb.Hyper(kind="complex", dim=16, batch_size=2000, num_negatives=100, neg_seed=3, engine="tc")
+    tr = eb.Trainer(h, V, R, p, device=0)
+    rng = np.random.default_rng(1)
+    for bits in (24, 32):
+        keys = rng.integers(0, 1 << 20, size=6000, dtype=np.int64).astype(np.uint32)
+        tr.debug_sort_slots(torch.from_numpy(keys.view(np.int32)).cuda(), bits)
+    tr.close()
     # the partition buffer (p=4, c=2)
     bucketed4, off4 = eb.bucket_edges(edges[split == 0], V, 4)
     dev4 = torch.from_numpy(bucketed4.view(np.int32)).cuda()
