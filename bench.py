@@ -611,9 +611,10 @@ def cpu_baseline(W, args, budget_s=20.0):
     cpu = CpuTrainer(cfg, edges_fn)
     done, t, n, thr = cpu.run(W.batches[start:], budget_s, 1000)
     # the 1-thread rate beside the all-core one (one batch of the same stream)
-    d1, t1, n1, _ = cpu.run(W.batches[start + n:], budget_s / 4, 1, threads=1)
+    rest = W.batches[start + n:] or W.batches[start:]  # (small configs: the stream may be used up)
+    d1, t1, n1, _ = cpu.run(rest, budget_s / 4, 1, threads=1)
     return {"value": round(done / t, 1), "unit": "edges/s", "cores": thr, "kind": "port",
-            "single_thread_value": round(d1 / t1, 1),
+            "single_thread_value": round(d1 / t1, 1) if t1 > 0 else None,
             "sample": f"{n} full batches (b={cfg['b']} positives, {cfg['nt']}-per-side shared negatives) of the timed "
                       f"GPU steps' batch stream, sampling + dedupe + gather + loss_and_grad + Adagrad "
                       f"(oracle/ember_oracle.c orc_train_batch_parts, OpenMP): {t:.1f} s on {thr} threads "
