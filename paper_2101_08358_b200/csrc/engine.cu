@@ -371,6 +371,7 @@ void Engine::join_sorted() {
 void Engine::forward_backward(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs,
                               bool presorted) {
     const PartView pi = view(i), pj = view(j);
+    dn_pending = false;  // (set by this step's contraction, consumed by its chain rule)
     if (!presorted) {  // helper stream, overlapped with the gathers and the contraction
         EMBER_CUDA(cudaEventRecord(ev_fork, stream));
         EMBER_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
