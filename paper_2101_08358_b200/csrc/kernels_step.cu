@@ -160,13 +160,22 @@ __global__ void __launch_bounds__(32 * GP_WARPS) k_gather_pack(const uint32_t* _
     const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t e0 = blockIdx.x * GP_ROWS;
     const uint32_t nq = d / 4;
-    for (uint32_t rr = wib; rr < GP_ROWS; rr += GP_WARPS) {
+    // this warp's edges' (s, r, t) in one round of loads (lane 3k + i: word i of the k-th edge), so
+    // each edge's row loads wait for one memory latency, not two
+    constexpr uint32_t GP_PER_WARP = GP_ROWS / GP_WARPS;
+    uint32_t idx = 0;
+    {
+        const uint32_t k = lane / 3, e = e0 + wib + k * GP_WARPS;
+        if (lane < 3 * GP_PER_WARP && e < nb) idx = edges[3 * e + lane % 3];
+    }
+    for (uint32_t rr = wib, kk = 0; rr < GP_ROWS; rr += GP_WARPS, ++kk) {
         const uint32_t e = e0 + rr;
+        const uint32_t s = __shfl_sync(0xffffffffu, idx, 3 * kk), r = __shfl_sync(0xffffffffu, idx, 3 * kk + 1),
+                       t = __shfl_sync(0xffffffffu, idx, 3 * kk + 2);
         if (e >= nb) {  // padding rows of the last tiles
             for (uint32_t c = lane; c < nblk; c += 32) tile[c * GP_ROWS + (rr ^ (c % GP_ROWS))] = make_uint4(0, 0, 0, 0);
             continue;
         }
-        const uint32_t s = edges[3 * e], r = edges[3 * e + 1], t = edges[3 * e + 2];
         // d <= 128: lane q holds quad q of each row (zeros past d: the K padding)
         Quad ad{}, as{};
         float part = 0.f;
