@@ -539,8 +539,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 tc::fence_after();
                 // 64 columns per TMEM round trip, then the 32-column remainder (TILE = 96)
                 if (!g.diag) {
-                    epi_chunk<MODE, 2>(tS, 0, k, g, sm, st, KP, cshift, z);
-                    epi_chunk<MODE, 1>(tS, 64, k, g, sm, st, KP, cshift, z);
+                    if (MODE == MODE_ROWS) {  // 32 columns per TMEM round trip: no epilogue spills
+                        epi_chunk<MODE, 1>(tS, 0, k, g, sm, st, KP, cshift, z);
+                        epi_chunk<MODE, 1>(tS, 32, k, g, sm, st, KP, cshift, z);
+                        epi_chunk<MODE, 1>(tS, 64, k, g, sm, st, KP, cshift, z);
+                    } else {  // 64 columns, then the 32-column remainder (TILE = 96)
+                        epi_chunk<MODE, 2>(tS, 0, k, g, sm, st, KP, cshift, z);
+                        epi_chunk<MODE, 1>(tS, 64, k, g, sm, st, KP, cshift, z);
+                    }
                 }
                 tc::tmem_st_wait();
                 tc::fence_before();
