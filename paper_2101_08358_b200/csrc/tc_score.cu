@@ -57,7 +57,7 @@ namespace {
 enum { MODE_ROWS = 0, MODE_NEGS = 1 };
 constexpr int RES = 128;       // resident rows per item (MMA M)
 constexpr int TILE = 96;       // streamed rows per tile (first product's N, second product's K)
-constexpr int NSTAGE_MAX = 4;  // streamed-tile ring depth (as many as fit in shared memory)
+constexpr int NSTAGE_MAX = 5;  // streamed-tile ring depth (as many as fit in shared memory, + the resident buffer)
 constexpr int KPMAX = 128;     // largest padded dim
 constexpr int NTHREADS = 352;  // producer, S issuer, P.T issuer, 2 x 4 epilogue warps
 constexpr uint32_t TCOLS = 512;
@@ -66,6 +66,9 @@ constexpr float L2E = 1.4426950408889634f;
 
 struct TcArgs {
     int KP, CB, d, nb, nt, n_pad, b_cap, chunks2, nstage, nsp;
+    // res_stage: every CTA runs one item, so once its resident tile is in TMEM the resident buffer
+    // serves as one more ring stage (the dN kernel: its ring depth is what limits its tile period)
+    int res_stage;
     int rows128, rows_pad;  // batch rows covered by the 128-row items / by the packed padding
     float inv_b, log2_inv_b, zmax;
     const float* fpos;
@@ -152,7 +155,8 @@ struct Smem {
     float* zbuf;    // [4 items][128]: group 0's partial row sums (MODE_ROWS)
     uint64_t* bars;
     uint32_t sbytes;
-    __device__ uint8_t* stage(int st) const { return ring + (size_t)st * sbytes; }
+    int nring;  // stages in `ring`; stage nring (if used) is the resident buffer
+    __device__ uint8_t* stage(int st) const { return st < nring ? ring + (size_t)st * sbytes : res; }
 };
 
 template <int MODE>
@@ -162,6 +166,7 @@ __device__ __forceinline__ Smem carve(uint8_t* raw, int KP, int nstage) {
     s.sbytes = (uint32_t)stage_bytes(KP, MODE);
     s.res = base;
     s.ring = base + res_bytes(KP);
+    s.nring = nstage;
     s.zbuf = reinterpret_cast<float*>(s.ring + (size_t)nstage * s.sbytes);
     s.bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(s.zbuf) + zbuf_bytes(MODE));
     return s;
@@ -311,7 +316,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     k_tc(const __grid_constant__ CUtensorMap mapR, const __grid_constant__ CUtensorMap mapT, const __grid_constant__ TcArgs g) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     const Smem sm = carve<MODE>(smem_raw, g.KP, g.nstage);
-    const int NSTAGE = g.nstage;
+    const int NSTAGE = g.nstage + (g.res_stage ? 1 : 0);  // ring depth (the last stage may be the resident buffer)
     uint64_t* bars = sm.bars;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(&bars[B_TMEM_SLOT]);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -328,7 +333,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (threadIdx.x == 0) {
         tc::mbar_init(&bars[B_RES_FULL], 1);
         tc::mbar_init(&bars[B_RES_EMPTY], 1);
-        for (int i = 0; i < g.nstage; ++i) {
+        for (int i = 0; i < NSTAGE; ++i) {
             tc::mbar_init(&bars[B_RING_FULL + i], 1);
             tc::mbar_init(&bars[B_RING_EMPTY + i], 1);
         }
@@ -404,6 +409,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 if (item >= items) break;
                 const Item I = item_geo<MODE>(g, item);
                 // resident tile: its previous occupant has been copied into TMEM (RES_EMPTY)
+                if (g.res_stage && it > 0) __trap();  // (res_stage: one item per CTA, set by the host)
                 tc::mbar_wait(&bars[B_RES_EMPTY], (it & 1) ^ 1);
                 tc::mbar_expect_tx(&bars[B_RES_FULL], bytesR);
                 tc::tma_load_4d(sm.res, &mapR, 0, I.r0 / 32, 0, I.side, &bars[B_RES_FULL]);
@@ -411,6 +417,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 for (int k = 0; k < I.T; ++k, ++gr) {
                     const int st = gr % NSTAGE;
                     tc::mbar_wait(&bars[B_RING_EMPTY + st], ((gr / NSTAGE) & 1) ^ 1);
+                    // first use of the resident buffer as a ring stage: its tile is in TMEM by now
+                    if (st == g.nstage && gr < (uint32_t)NSTAGE) tc::mbar_wait(&bars[B_RES_EMPTY], 0);
                     TC_TRACE(2, gr);
                     tc::mbar_expect_tx(&bars[B_RING_FULL + st], bytesT);
                     uint8_t* dst = sm.stage(st);
@@ -785,6 +793,7 @@ void dn_reduce_run(const Engine& E, const DnReduce& r) {
 // Engine-side state of the tensor-core engine (allocated once per context).
 struct TcState {
     int KP = 0, CB = 0, b_cap = 0, n_pad = 0, chunks2 = 1, nstage = 4, nsp = 2;
+    bool res_stage = true;  // the dN kernel's resident buffer as an extra ring stage (EMBER_TC_RES_STAGE=0: off)
     float* dN_part = nullptr;
     float* lse_pad = nullptr;
     uint32_t* flags = nullptr;
@@ -823,6 +832,7 @@ void tc_setup(Engine& E) {
     t->chunks2 = std::max(1, E.sm_count / (2 * ntl));
     t->nstage = stages_for(t->KP);
     if (const char* s = getenv("EMBER_TC_NSTAGE")) t->nstage = std::max(2, std::min(t->nstage, atoi(s)));  // A/B
+    if (const char* s = getenv("EMBER_TC_RES_STAGE")) t->res_stage = atoi(s) != 0;
     if (const char* s = getenv("EMBER_TC_ZMAX")) t->zmax = (float)atof(s);  // test hook: 0 flags every row
     if (const char* s = getenv("EMBER_TC_MAXGRID")) t->max_grid = atoi(s);
     if (getenv("EMBER_TC_CTATIMES")) EMBER_CUDA(cudaMalloc(&t->cta_times, (size_t)2 * 2 * E.sm_count * 8));
@@ -960,6 +970,8 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
     if (ct) a.cta_times = t.cta_times + 2 * E.sm_count;
     a.arrive = t.arrive + 1;
     a.arrive_base = t.arrive_base[1];
+    // one item per CTA, and a barrier pair left for the extra stage
+    a.res_stage = (t.res_stage && std::min(items2, gmax) >= items2 && t.nstage < NSTAGE_MAX) ? 1 : 0;
     a.dyn = 0;  // one item per CTA
     t.arrive_base[1] += (uint32_t)std::min(items2, gmax);
     launch_pdl(k_tc<MODE_NEGS>, dim3(std::min(items2, gmax)), dim3(NTHREADS), smem_total(t.KP, t.nstage, MODE_NEGS),
