@@ -230,7 +230,6 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     EMBER_CUDA(cudaMemset(s.bad_batch, 0, sizeof(unsigned long long)));
     s.keys = dalloc<uint32_t>(cap_rows);
     s.keys_sorted = dalloc<uint32_t>(cap_rows);
-    s.vals = dalloc<uint32_t>(cap_rows);
     s.vals_sorted = dalloc<uint32_t>(cap_rows);
     s.rank = dalloc<uint32_t>(cap_rows);
     s.uniq = dalloc<uint8_t>(cap_rows);
@@ -285,7 +284,7 @@ Engine::~Engine() {
     wide_release(*this);
     void* ptrs[] = {s.batch, s.A,         s.N,      s.Apk,       s.Npk,     s.fpos,       s.lse,    s.g0,
                     s.S,     s.dA,        s.dN_part, s.grows,    s.loss,    s.loss_part,  s.loss_done,  s.bad_batch,
-                    s.nunique, s.long_partial, s.rel_dense, s.negs, s.keys, s.keys_sorted, s.vals, s.vals_sorted,
+                    s.nunique, s.long_partial, s.rel_dense, s.negs, s.keys, s.keys_sorted, s.vals_sorted,
                     s.rank, s.ukeys, s.offsets, s.nruns, s.longs, s.long_owner, s.uniq, s.sort_keys[0],
                     s.sort_keys[1], s.sort_vals[0], s.sort_vals[1], s.sort_hist, s.sort_status, s.sort_ctr, s.nsplit};
     for (void* p : ptrs)

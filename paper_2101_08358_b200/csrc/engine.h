@@ -104,7 +104,6 @@ struct Scratch {
     unsigned long long* bad_batch = nullptr;  // first batch whose loss was non-finite (sticky, 0 = none)
     uint32_t* keys = nullptr;
     uint32_t* keys_sorted = nullptr;
-    uint32_t* vals = nullptr;
     uint32_t* vals_sorted = nullptr;
     uint32_t* rank = nullptr;
     uint8_t* uniq = nullptr;      // slot -> its key occurs once among the batch's slots
@@ -247,7 +246,7 @@ struct Engine {
                 uint32_t bucket_step, uint32_t batch_in_bucket, uint32_t* negs_out);
     // Keys of the batch's gradient slots, sorted on the helper stream (forked by the caller).
     void sort_keys(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs);
-    void sort_slots(uint32_t nb, const KeySpace& ks);  // sort of s.keys / s.vals on the helper stream
+    void sort_slots(uint32_t nb, const KeySpace& ks);  // (key, slot) sort of s.keys on the helper stream
     void join_sorted();  // the step stream waits for sort_keys' results
     // Computes loss and gradient rows for one batch into grows (sorted order).
     void forward_backward(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs,

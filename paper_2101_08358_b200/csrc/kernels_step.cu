@@ -332,10 +332,9 @@ __device__ __forceinline__ uint32_t node_key(const KeySpace& ks, uint32_t id) {
     return o < ks.lo.rows ? (uint32_t)o : (uint32_t)(ks.lo.rows + ((uint64_t)id - ks.hi.first));
 }
 
-// keys[slot], vals[slot] = slot (slot layout: engine.h).
+// keys[slot] (slot layout: engine.h); the sort numbers the slots itself.
 __global__ void k_keys(const uint32_t* __restrict__ edges, uint32_t nb, const uint32_t* __restrict__ negs,
-                       uint32_t n_neg, uint32_t n_slots, KeySpace ks, uint32_t* keys, uint32_t* vals,
-                       uint32_t* longs) {
+                       uint32_t n_neg, uint32_t n_slots, KeySpace ks, uint32_t* keys, uint32_t* longs) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0) {  // long-segment list of this step's reduction
         longs[0] = 0u;
@@ -348,7 +347,6 @@ __global__ void k_keys(const uint32_t* __restrict__ edges, uint32_t nb, const ui
     else if (i < 2 * nb + n_neg) k = node_key(ks, negs[i - 2 * nb]);
     else k = (uint32_t)ks.node_range + edges[3 * (i - 2 * nb - n_neg) + 1];
     keys[i] = k;
-    vals[i] = i;
 }
 
 // The training step's first kernel: sample_negatives fused with the gradient-slot keys (the
@@ -358,7 +356,7 @@ __global__ void k_keys(const uint32_t* __restrict__ edges, uint32_t nb, const ui
 __global__ void k_sample_keys(const uint32_t* __restrict__ edges, uint32_t nb, uint32_t* __restrict__ negs,
                               uint32_t n_neg, uint32_t nt, uint32_t n_deg, uint64_t base,
                               const uint32_t* __restrict__ bucket, uint64_t bucket_n, PartView src, PartView dst,
-                              uint32_t n_slots, KeySpace ks, uint32_t* keys, uint32_t* vals, uint32_t* longs) {
+                              uint32_t n_slots, KeySpace ks, uint32_t* keys, uint32_t* longs) {
     griddep_wait();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0) {  // long-segment list of this step's reduction
@@ -380,7 +378,6 @@ __global__ void k_sample_keys(const uint32_t* __restrict__ edges, uint32_t nb, u
         k = (uint32_t)ks.node_range + edges[3 * (i - 2 * nb - n_neg) + 1];
     }
     keys[i] = k;
-    vals[i] = i;
 }
 
 // The sorted position p holds a key that occurs exactly once among the batch's gradient slots.
@@ -1390,7 +1387,7 @@ void launch_gather_negatives(const Engine& E, const uint32_t* negs, const PartVi
 
 void launch_keys(const Engine& E, const uint32_t* edges, uint32_t nb, const uint32_t* negs, const KeySpace& ks) {
     const uint32_t n = E.slots(nb);
-    k_keys<<<(n + 255) / 256, 256, 0, E.side>>>(edges, nb, negs, E.n_neg, n, ks, E.s.keys, E.s.vals, E.s.longs);
+    k_keys<<<(n + 255) / 256, 256, 0, E.side>>>(edges, nb, negs, E.n_neg, n, ks, E.s.keys, E.s.longs);
     EMBER_LAUNCHED(E);
 }
 
@@ -1399,7 +1396,7 @@ void launch_sample_keys(const Engine& E, const uint32_t* edges, uint32_t nb, uin
     const uint32_t n = E.slots(nb);
     const uint32_t n_deg = (uint32_t)ceil((double)E.m.alpha * (double)E.nt);
     launch_pdl(k_sample_keys, dim3((n + 255) / 256), dim3(256), 0, E.stream, edges, nb, E.s.negs, E.n_neg, E.nt, n_deg,
-               base, bucket, bucket_n, src, dst, n, ks, E.s.keys, E.s.vals, E.s.longs);
+               base, bucket, bucket_n, src, dst, n, ks, E.s.keys, E.s.longs);
     EMBER_LAUNCHED(E);
 }
 
