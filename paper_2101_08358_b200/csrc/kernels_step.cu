@@ -528,7 +528,8 @@ struct EdgeMeta {
     float lterm;  // the edge's loss term (lse_dst - f) + (lse_src - f)
 };
 
-__global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restrict__ edges, uint32_t nb, uint32_t n_neg,
+template <int NS, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_chain_pipe(const uint32_t* __restrict__ edges, uint32_t nb, uint32_t n_neg,
                                                       PartView pi, PartView pj, const float* __restrict__ rel,
                                                       int kind, uint32_t d, const float* __restrict__ dA,
                                                       uint32_t dcap, const float* __restrict__ g0,
@@ -549,10 +550,10 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
         for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += step)
             dn_reduce_item(dn, t, rank, grows);
     }
-    extern __shared__ float4 cpbuf[];  // [warps][2 stages][CP_ROLES][32 lanes]
+    extern __shared__ float4 cpbuf[];  // [warps][NS stages][CP_ROLES][32 lanes]
     const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + wib, nw = gridDim.x * (blockDim.x >> 5);
-    float4* my = cpbuf + (size_t)wib * 2 * CP_ROLES * 32 + lane;
+    float4* my = cpbuf + (size_t)wib * NS * CP_ROLES * 32 + lane;
     const uint32_t nq = d / 4;
     const bool ql = lane < nq;
     // An edge's indices, ranks, flags and scalars are loaded one edge ahead of its row copies, so
@@ -586,24 +587,32 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
         }
         cp_commit();
     };
-    EdgeMeta cur{}, nxt{}, nn{};
-    if (gw < nb) {
-        load_meta(gw, cur);
-        issue(gw, 0, cur);
-    } else {
-        cp_commit();
+    // q[k]: the metadata of edge gw + (it + k) nw, whose copies sit in stage (it + k) % NS; each
+    // iteration issues edge e + (NS - 1) nw into the stage the previous edge freed before waiting on
+    // edge e, so NS edges are in flight through the wait and NS - 1 through the compute.
+    // pre: the metadata one edge beyond the newest issued.
+    EdgeMeta q[NS]{}, pre{};
+#pragma unroll
+    for (int k = 0; k + 1 < NS; ++k) {
+        const uint32_t e = gw + k * nw;
+        if (e < nb) {
+            load_meta(e, q[k]);
+            issue(e, k, q[k]);
+        } else {
+            cp_commit();
+        }
     }
-    if (gw + nw < nb) load_meta(gw + nw, nxt);
-    uint32_t it = 0;
+    if (gw + (NS - 1) * nw < nb) load_meta(gw + (NS - 1) * nw, q[NS - 1]);
+    int st = 0;
     double lacc = 0.0;  // lane 0: this warp's loss terms, in its (fixed) edge order
-    for (uint32_t e = gw; e < nb; e += nw, ++it) {
+    for (uint32_t e = gw; e < nb; e += nw) {
+        const EdgeMeta& cur = q[0];
         lacc += (double)cur.lterm;
-        const int st = it & 1;
-        const uint32_t en = e + nw;
-        if (en < nb) issue(en, st ^ 1, nxt);
+        const uint32_t en = e + (NS - 1) * nw;
+        if (en < nb) issue(en, st == 0 ? NS - 1 : st - 1, q[NS - 1]);
         else cp_commit();
-        if (en + nw < nb) load_meta(en + nw, nn);  // consumed next iteration
-        cp_wait<1>();  // this edge's copies (this lane's own) have landed
+        if (en + nw < nb) load_meta(en + nw, pre);  // consumed next iteration
+        cp_wait<NS - 1>();  // this edge's copies (this lane's own) have landed
         if (ql) {
             const float4* b = my + (size_t)st * CP_ROLES * 32;
             const Quad S = quad_of(b[0]), T = quad_of(b[32]);
@@ -654,8 +663,10 @@ __global__ void __launch_bounds__(256, 3) k_chain_pipe(const uint32_t* __restric
                 store_quad(grows + (uint64_t)cur.pt * d, lane, oT);
             if (kind != EMBER_DOT) store_quad(grows + (uint64_t)cur.pr * d, lane, oR);
         }
-        cur = nxt;
-        nxt = nn;
+#pragma unroll
+        for (int k = 0; k + 1 < NS; ++k) q[k] = q[k + 1];
+        q[NS - 1] = pre;
+        st = st + 1 == NS ? 0 : st + 1;
     }
     cp_wait<0>();
     // the loss (replaces k_loss): per-warp partials in warp order, summed by the last warp to finish
@@ -1404,11 +1415,18 @@ void launch_sample_keys(const Engine& E, const uint32_t* edges, uint32_t nb, uin
 void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj) {
     const uint32_t warps = 8;
     if (E.tc_engine() && E.dim <= 128 && !getenv("EMBER_CHAIN_PLAIN")) {
-        // persistent pipelined warps: 3 CTAs of 8 warps per SM (shared stages: 8 x 2 x 7 x 512 B)
-        const size_t sm = (size_t)warps * 2 * CP_ROLES * 32 * sizeof(float4);
-        const uint32_t blocks = std::min<uint32_t>((nb + warps - 1) / warps, (uint32_t)E.sm_count * 3);
-        opt_in_smem((const void*)k_chain_pipe, sm, E.device);
-        launch_pdl(k_chain_pipe, dim3(blocks), dim3(warps * 32), sm, E.stream, edges, nb, E.n_neg, pi, pj,
+        // persistent pipelined warps: 8 warps per CTA, each with NS shared stages of 7 x 512 B;
+        // 2 stages -> 3 CTAs per SM (57 KB each), 3 stages -> 2 CTAs per SM (86 KB each)
+        static const int ns = [] {
+            const char* v = getenv("EMBER_CHAIN_STAGES");
+            return v && atoi(v) == 3 ? 3 : 2;
+        }();
+        const size_t sm = (size_t)warps * ns * CP_ROLES * 32 * sizeof(float4);
+        const uint32_t per_sm = ns == 3 ? 2 : 3;
+        const uint32_t blocks = std::min<uint32_t>((nb + warps - 1) / warps, (uint32_t)E.sm_count * per_sm);
+        auto kern = ns == 3 ? k_chain_pipe<3, 2> : k_chain_pipe<2, 3>;
+        opt_in_smem((const void*)kern, sm, E.device);
+        launch_pdl(kern, dim3(blocks), dim3(warps * 32), sm, E.stream, edges, nb, E.n_neg, pi, pj,
                    (const float*)E.rel_theta, E.m.kind, E.dim, (const float*)E.s.dA, (uint32_t)E.b_cap,
                    (const float*)E.s.g0, (const uint32_t*)E.s.rank, (const uint8_t*)E.s.uniq, E.s.grows,
                    E.direct_hi ? 1 : 0, E.m.lr, E.m.eps, (const float*)E.s.lse, (const float*)E.s.fpos,
