@@ -595,22 +595,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                     ((size_t)I.chunk * 2 + I.side) * (g.d / 4) * g.n_pad + row;
             const size_t cstride = MODE == MODE_ROWS ? (size_t)g.b_cap : (size_t)g.n_pad;
 #pragma unroll
+            // batches: chunks [0, nchunks - 4), then the last 4 (one batch when nchunks <= 4)
+            const int b0 = nchunks > 4 ? nchunks - 4 : nchunks;
             for (int half = 0; half < 2; ++half) {
+                const int c0 = half ? b0 : 0, cn = half ? nchunks : b0;
                 uint32_t accv[4][16];
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
-                    if (4 * half + i < nchunks) tc::tmem_ld16(t_row + T_ACC + 16 * (4 * half + i), accv[i]);
+                    if (c0 + i < cn) tc::tmem_ld16(t_row + T_ACC + 16 * (c0 + i), accv[i]);
                 tc::tmem_ld_wait();
                 if (qd == 2) TC_TRACE(30 + half, it);
-                if (half == 1 || nchunks <= 4) {
+                if (cn == nchunks) {
                     tc::fence_before();
-                    if (half == 1 || nchunks <= 4) tc::mbar_arrive(&bars[B_ACC_EMPTY]);
+                    tc::mbar_arrive(&bars[B_ACC_EMPTY]);
                 }
                 if (valid) {
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        const int c = 4 * half + i;
-                        if (c >= nchunks) continue;
+                        const int c = c0 + i;
+                        if (c >= cn) continue;
 #pragma unroll
                         for (int j = 0; j < 16; j += 4)
                             if (16 * c + j < g.d)
@@ -619,7 +622,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                     __uint_as_float(accv[i][j + 2]) * scale, __uint_as_float(accv[i][j + 3]) * scale);
                     }
                 }
-                if (nchunks <= 4) break;
+                if (cn == nchunks) break;
             }
             if (MODE == MODE_ROWS) {
                 if (valid) {
