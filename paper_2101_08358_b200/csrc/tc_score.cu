@@ -594,7 +594,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                               : reinterpret_cast<float4*>(g.dN_part) +
                                     ((size_t)I.chunk * 2 + I.side) * (g.d / 4) * g.n_pad + row;
             const size_t cstride = MODE == MODE_ROWS ? (size_t)g.b_cap : (size_t)g.n_pad;
-#pragma unroll
             // batches: chunks [0, nchunks - 4), then the last 4 (one batch when nchunks <= 4)
             const int b0 = nchunks > 4 ? nchunks - 4 : nchunks;
             for (int half = 0; half < 2; ++half) {
