@@ -294,6 +294,13 @@ __device__ __forceinline__ void griddep_wait() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
 }
+// The dependent grid (launched with PDL) may be scheduled once every CTA of this grid has executed
+// this (or exited); its griddep_wait() still waits for this grid's completion.
+__device__ __forceinline__ void griddep_launch() {
+#if defined(__CUDA_ARCH__)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
 bool pdl_enabled();
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {

@@ -747,6 +747,7 @@ struct SegArgs {
     uint32_t* owner;     // chunk slot -> long index
     float* partial;      // chunk slot -> partial sum row
     uint32_t long_cap;
+    int early_final;     // k_long_final scheduled once the segment kernel's CTAs have written the partials
     const float* rows;   // sorted gradient rows
     KeySpace ks;
     float* rel_theta;
@@ -970,6 +971,14 @@ __global__ void __launch_bounds__(256, 4) k_segments_pipe(const __grid_constant_
     griddep_wait();
     long_partials(a, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, (gridDim.x * blockDim.x) >> 5,
                   threadIdx.x & 31);  // the long segments' chunk partials first
+    // k_long_final only needs the partials: once every CTA is past this point it may be scheduled
+    // on the SMs this grid's tail leaves idle (it reads them through L2 and waits for this grid
+    // before it completes)
+    if (a.early_final) {  // every warp of the CTA past its partials (fenced) before the CTA triggers
+        __threadfence();
+        __syncthreads();
+        griddep_launch();
+    }
     extern __shared__ float4 sst[];  // [warps][2 halves][2 stages][2 roles][2 column blocks][16 lanes]
     const uint32_t lane = threadIdx.x & 31, hl = lane & (SEG_LANES - 1), half = lane >> 4, wib = threadIdx.x >> 5;
     const uint32_t gh = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 2 + half;
@@ -1066,6 +1075,12 @@ __device__ __forceinline__ float4 sum_rows_strided(const float* base, uint32_t r
 
 // The same for two column blocks at once (c4a, and c4b when hasb): 8 loads in flight, and per
 // column the same row order (bit-identical to two sum_rows_strided passes).
+// CG: loads through L2 only (rows written by a grid that may still be running: k_long_final)
+template <bool CG = false>
+__device__ __forceinline__ float4 ld4(const float* p) {
+    return CG ? __ldcg(reinterpret_cast<const float4*>(p)) : __ldg(reinterpret_cast<const float4*>(p));
+}
+template <bool CG = false>
 __device__ __forceinline__ void sum_rows_strided2(const float* base, uint32_t r0, uint32_t step, uint32_t cnt,
                                                   uint32_t d, uint32_t c4a, uint32_t c4b, bool hasb, float4& sa,
                                                   float4& sb) {
@@ -1075,10 +1090,10 @@ __device__ __forceinline__ void sum_rows_strided2(const float* base, uint32_t r0
     for (; r + 3 * step < cnt; r += 4 * step) {
         float4 x[4], y[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) x[i] = ldg4(base + (uint64_t)(r + i * step) * d + 4 * c4a);
+        for (int i = 0; i < 4; ++i) x[i] = ld4<CG>(base + (uint64_t)(r + i * step) * d + 4 * c4a);
         if (hasb) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) y[i] = ldg4(base + (uint64_t)(r + i * step) * d + 4 * c4b);
+            for (int i = 0; i < 4; ++i) y[i] = ld4<CG>(base + (uint64_t)(r + i * step) * d + 4 * c4b);
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) add4(sa, x[i]);
@@ -1088,8 +1103,8 @@ __device__ __forceinline__ void sum_rows_strided2(const float* base, uint32_t r0
         }
     }
     for (; r < cnt; r += step) {
-        add4(sa, ldg4(base + (uint64_t)r * d + 4 * c4a));
-        if (hasb) add4(sb, ldg4(base + (uint64_t)r * d + 4 * c4b));
+        add4(sa, ld4<CG>(base + (uint64_t)r * d + 4 * c4a));
+        if (hasb) add4(sb, ld4<CG>(base + (uint64_t)r * d + 4 * c4b));
     }
 }
 
@@ -1160,8 +1175,7 @@ __global__ void k_long_plan(const uint32_t* __restrict__ offsets, const uint32_t
 // order (a fixed two-level order: deterministic) and applies Adagrad / export.
 constexpr uint32_t LONG_BIG = 8;  // long segments with more chunk partials than this get a whole block
 
-__global__ void __launch_bounds__(32 * LONG_WARPS) k_long_final(SegArgs a) {
-    griddep_wait();
+__device__ __forceinline__ void long_final_body(const SegArgs& a) {
     extern __shared__ float4 wsum[];  // [2 * LONG_WARPS][d/4]
     const uint32_t lane = threadIdx.x & 31, hl = lane & 15, stream = threadIdx.x >> 4, d4 = a.d / 4;
     const uint32_t NS = 2 * LONG_WARPS;
@@ -1173,7 +1187,7 @@ __global__ void __launch_bounds__(32 * LONG_WARPS) k_long_final(SegArgs a) {
         if (nch <= LONG_BIG || !seg_in_part(a, u)) continue;  // block-uniform
         for (uint32_t c4 = hl; c4 < d4; c4 += 32) {
             float4 va, vb;
-            sum_rows_strided2(a.partial + (uint64_t)base * a.d, stream, NS, nch, a.d, c4, c4 + 16, c4 + 16 < d4, va, vb);
+            sum_rows_strided2<true>(a.partial + (uint64_t)base * a.d, stream, NS, nch, a.d, c4, c4 + 16, c4 + 16 < d4, va, vb);
             wsum[stream * d4 + c4] = va;
             if (c4 + 16 < d4) wsum[stream * d4 + c4 + 16] = vb;
         }
@@ -1218,7 +1232,7 @@ __global__ void __launch_bounds__(32 * LONG_WARPS) k_long_final(SegArgs a) {
                 }
             }
             float4 g = z, gb = z;
-            if (hasa) sum_rows_strided2(a.partial + (uint64_t)base * a.d, half, 2, nch, a.d, c4, c4b, hasb, g, gb);
+            if (hasa) sum_rows_strided2<true>(a.partial + (uint64_t)base * a.d, half, 2, nch, a.d, c4, c4b, hasb, g, gb);
             const float4 o = shfl_xor4(g, 16), ob = shfl_xor4(gb, 16);
             if (half == 0) {
                 if (hasa) {
@@ -1232,6 +1246,12 @@ __global__ void __launch_bounds__(32 * LONG_WARPS) k_long_final(SegArgs a) {
             }
         }
     }
+}
+
+__global__ void __launch_bounds__(32 * LONG_WARPS) k_long_final(SegArgs a) {
+    if (!a.early_final) griddep_wait();
+    long_final_body(a);
+    if (a.early_final) griddep_wait();  // not complete before the segment kernel: stream order for what follows
 }
 
 __global__ void k_adagrad_rows(const uint32_t* __restrict__ ids, const float* __restrict__ rows, uint32_t n,
@@ -1494,6 +1514,7 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
         const size_t sm = (size_t)8 * 2 * 2 * 2 * 2 * SEG_LANES * sizeof(float4);
         opt_in_smem((const void*)k_segments_pipe, sm, E.device);
         const uint32_t blocks = std::min<uint32_t>((n_slots + 15) / 16, (uint32_t)E.sm_count * 4);
+        a.early_final = pdl_enabled() && !getenv("EMBER_LONG_FINAL_LATE") ? 1 : 0;
         launch_pdl(k_segments_pipe, dim3(blocks), dim3(256), sm, st, a);
     } else {
         k_segments<<<(n_slots * 16 + 255) / 256, 256, 0, st>>>(a);  // 2 keys per warp
