@@ -251,12 +251,13 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     // at most cap_rows / LONG_SEG long segments, each with <= len / LONG_CHUNK + 1 chunks
     const uint32_t max_long = cap_rows / EMBER_LONG_SEG + 1;
     const uint32_t max_chunks = cap_rows / EMBER_LONG_CHUNK + max_long;
-    s.longs = dalloc<uint32_t>(2 + 3 * max_long);
+    s.longs = dalloc<uint32_t>(3 + 3 * max_long);
+    s.seg_act = dalloc<uint32_t>(cap_rows);
     s.long_owner = dalloc<uint32_t>(max_chunks);
     s.long_partial = dalloc<float>((uint64_t)max_chunks * d);
 
     EMBER_CUDA(cudaMemset(s.nunique, 0, 2 * sizeof(uint32_t)));
-    EMBER_CUDA(cudaMemset(s.longs, 0, 2 * sizeof(uint32_t)));
+    EMBER_CUDA(cudaMemset(s.longs, 0, 3 * sizeof(uint32_t)));
     if (m.engine == EMBER_ENGINE_SIMT_FP32) {
         s.S = dalloc<float>(2 * b * (uint64_t)(nt ? nt : 1));
         s.dN_part = dalloc<float>((uint64_t)dsplit * n_neg * d);
@@ -286,7 +287,8 @@ Engine::~Engine() {
                     s.S,     s.dA,        s.dN_part, s.grows,    s.loss,    s.loss_part,  s.loss_done,  s.bad_batch,
                     s.nunique, s.long_partial, s.rel_dense, s.negs, s.keys, s.keys_sorted, s.vals_sorted,
                     s.rank, s.ukeys, s.offsets, s.nruns, s.longs, s.long_owner, s.uniq, s.sort_keys[0],
-                    s.sort_keys[1], s.sort_vals[0], s.sort_vals[1], s.sort_hist, s.sort_status, s.sort_ctr, s.nsplit};
+                    s.sort_keys[1], s.sort_vals[0], s.sort_vals[1], s.sort_hist, s.sort_status, s.sort_ctr, s.nsplit,
+                    s.seg_act};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (void* p : owned) cudaFree(p);
@@ -353,10 +355,10 @@ void Engine::sort_keys(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t 
     sort_slots(nb, ks);
 }
 
-void Engine::sort_slots(uint32_t nb, const KeySpace& ks) {
+void Engine::sort_slots(uint32_t nb, const KeySpace& ks, uint32_t direct) {
     const uint32_t n = slots(nb);
     launch_slot_sort(*this, slots(nb), ks.bits, (uint32_t)ks.node_range);
-    launch_long_plan(*this, slots(nb));
+    launch_long_plan(*this, slots(nb), ks.node_range, direct);
     EMBER_CUDA(cudaEventRecord(ev_sorted, side));
     sorted_pending = true;
 }
@@ -504,8 +506,8 @@ void Engine::step(const uint32_t* edges, uint32_t nb, const uint32_t* bucket, ui
     launch_sample_keys(*this, edges, nb, base, bucket, bucket_n, view(i), view(j), ks);
     EMBER_CUDA(cudaEventRecord(ev_fork, stream));
     EMBER_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
-    sort_slots(nb, ks);
     direct_hi = getenv_direct() ? 2 * nb : 0;
+    sort_slots(nb, ks, direct_hi);
     loss_target = loss_out ? loss_out : s.loss;
     batch_tag = (1ull << 63) | ((epoch & 0xFFFFFull) << 40) | ((uint64_t)(bucket_step & 0xFFFFFu) << 20) |
                 (batch_in_bucket & 0xFFFFFu);

@@ -113,6 +113,7 @@ struct Scratch {
     uint32_t* nunique = nullptr;  // [2] unique node keys, unique relation keys
     uint32_t* longs = nullptr;        // [2 + 3 * cap]: long segments, chunk slots, then (u, base, nch)
     uint32_t* long_owner = nullptr;   // chunk slot -> long segment
+    uint32_t* seg_act = nullptr;      // runs with segment-kernel work (k_long_plan; count in longs[2])
     float* long_partial = nullptr;    // chunk slot -> partial row
 
     // slot sort (sort.cu): ping-pong key/value buffers, per-tile digit histograms, run-scan state
@@ -210,6 +211,7 @@ struct Engine {
     // right in the chain rule (slots < direct_hi = 2nb); 0: every row goes through the segmented
     // reduction.
     uint32_t direct_hi = 0;
+    mutable uint32_t plan_direct = 0;  // direct threshold the last k_long_plan's run list was built for
     // where the step's loss goes; the tensor-core chain rule reduces it there itself (loss_fused)
     float* loss_target = nullptr;
     // batch id of the step being enqueued ("non-finite score -> error carrying batch id")
@@ -246,7 +248,9 @@ struct Engine {
                 uint32_t bucket_step, uint32_t batch_in_bucket, uint32_t* negs_out);
     // Keys of the batch's gradient slots, sorted on the helper stream (forked by the caller).
     void sort_keys(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs);
-    void sort_slots(uint32_t nb, const KeySpace& ks);  // (key, slot) sort of s.keys on the helper stream
+    // direct: the chain rule applies node keys occurring once with slot < direct (k_long_plan leaves
+    // them out of the segment kernel's run list)
+    void sort_slots(uint32_t nb, const KeySpace& ks, uint32_t direct = 0);  // (key, slot) sort of s.keys on the helper stream
     void join_sorted();  // the step stream waits for sort_keys' results
     // Computes loss and gradient rows for one batch into grows (sorted order).
     void forward_backward(const uint32_t* edges, uint32_t nb, uint32_t i, uint32_t j, const uint32_t* negs,
@@ -342,7 +346,7 @@ void launch_contract_tc(Engine& E, uint32_t nb);
 void launch_chain_rule(const Engine& E, const uint32_t* edges, uint32_t nb, const PartView& pi, const PartView& pj);
 void launch_loss(const Engine& E, uint32_t nb, float* loss_out);
 // the long-segment chunk plan (keys with > EMBER_LONG_SEG rows) on the helper stream after the sort
-void launch_long_plan(const Engine& E, uint32_t n_slots);
+void launch_long_plan(const Engine& E, uint32_t n_slots, uint64_t node_range, uint32_t direct);
 // part: 0 every key, 1 relation keys only, 2 node keys only (the split: s.nsplit)
 void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool apply, bool rel_dense,
                      uint32_t* node_ids_out, float* node_rows_out, uint32_t* rel_ids_out, float* rel_rows_out,

@@ -339,6 +339,7 @@ __global__ void k_keys(const uint32_t* __restrict__ edges, uint32_t nb, const ui
     if (i == 0) {  // long-segment list of this step's reduction
         longs[0] = 0u;
         longs[1] = 0u;
+        longs[2] = 0u;
     }
     if (i >= n_slots) return;
     uint32_t k;
@@ -362,6 +363,7 @@ __global__ void k_sample_keys(const uint32_t* __restrict__ edges, uint32_t nb, u
     if (i == 0) {  // long-segment list of this step's reduction
         longs[0] = 0u;
         longs[1] = 0u;
+        longs[2] = 0u;
     }
     if (i >= n_slots) return;
     uint32_t k;
@@ -743,7 +745,8 @@ struct SegArgs {
     const uint32_t* offsets;
     const uint32_t* nruns;
     uint32_t* nunique;   // [2] written: node uniques, relation uniques
-    uint32_t* longs;     // [0] long segments, [1] chunk slots; then u, base, nch per long (3 x cap)
+    uint32_t* longs;     // [0] long segments, [1] chunk slots, [2] active runs; then u, base, nch per long
+    const uint32_t* act; // runs the segment kernel visits (k_long_plan), longs[2] of them; null: every run
     uint32_t* owner;     // chunk slot -> long index
     float* partial;      // chunk slot -> partial sum row
     uint32_t long_cap;
@@ -787,6 +790,7 @@ __device__ __forceinline__ bool seg_in_part(const SegArgs& a, uint32_t u) {
 constexpr uint32_t LONG_SEG = EMBER_LONG_SEG;
 constexpr uint32_t LONG_CHUNK = EMBER_LONG_CHUNK;
 constexpr uint32_t LONG_WARPS = 16;
+constexpr uint32_t LONG_HDR = 3;  // longs[]: header words before the long-segment records
 
 // Where unique key u's summed row goes: Adagrad target (th, ac) or export/dense destination.
 struct SegTarget {
@@ -923,10 +927,6 @@ __global__ void __launch_bounds__(256, 4) k_segments(const __grid_constant__ Seg
     seg_range(a, nr, lo, hi);
     if (u < lo || u >= hi) return;
     const uint32_t key = a.ukeys[u];
-    if (hl == 0 && key < a.ks.node_range && (u + 1 == nr || a.ukeys[u + 1] >= a.ks.node_range)) {
-        a.nunique[0] = u + 1;
-        a.nunique[1] = nr - (u + 1);
-    }
     const uint32_t off = a.offsets[u], cnt = a.offsets[u + 1] - off;
     if (cnt == 1 && key < a.ks.node_range && a.vals_sorted[off] < a.direct_hi) return;  // applied already
     if (cnt > LONG_SEG) return;  // chunked (long_partials, k_long_final)
@@ -964,7 +964,7 @@ struct SegKey {
 };
 
 struct SegMeta {
-    uint32_t key, off, cnt, next_key;
+    uint32_t u, key, off, cnt;
 };
 
 __global__ void __launch_bounds__(256, 4) k_segments_pipe(const __grid_constant__ SegArgs a) {
@@ -988,30 +988,30 @@ __global__ void __launch_bounds__(256, 4) k_segments_pipe(const __grid_constant_
     seg_range(a, nr, u_lo, u_hi);
     float4* my = sst + (size_t)(wib * 2 + half) * 2 * 2 * 2 * SEG_LANES + hl;
     auto slot = [&](int st, int role, int cb) { return my + (size_t)((st * 2 + role) * 2 + cb) * SEG_LANES; };
-    // A key's (key, offset, count) are loaded one key ahead of its parameter copies, so the copies
-    // of key u + nh are issued without waiting on those loads.
-    auto load_meta = [&](uint32_t u, SegMeta& m) {
-        m.key = a.ukeys[u];
-        m.off = a.offsets[u];
-        m.cnt = a.offsets[u + 1] - m.off;
-        m.next_key = u + 1 < nr ? a.ukeys[u + 1] : 0xffffffffu;
+    // The runs this half-warp visits: the plan's list of runs with work (k_long_plan), else every
+    // run of the part. A run's (key, offset, count) are loaded one run ahead of its parameter copies,
+    // so the copies of run i + nh are issued without waiting on those loads.
+    const bool list = a.act != nullptr;
+    const uint32_t n_items = list ? *(volatile uint32_t*)&a.longs[2] : u_hi - u_lo;
+    auto load_meta = [&](uint32_t i, SegMeta& m) {
+        m.u = list ? a.act[i] : u_lo + i;
+        m.key = a.ukeys[m.u];
+        m.off = a.offsets[m.u];
+        m.cnt = a.offsets[m.u + 1] - m.off;
     };
-    auto issue = [&](uint32_t u, int st, const SegMeta& m, SegKey& k) {
-        k.u = u;
+    auto issue = [&](uint32_t i, int st, const SegMeta& m, SegKey& k) {
+        k.u = m.u;
         k.active = false;
-        if (u < u_hi) {
+        if (i < n_items && m.u >= u_lo && m.u < u_hi) {
             const uint32_t key = m.key;
-            if (hl == 0 && key < a.ks.node_range && (u + 1 == nr || m.next_key >= a.ks.node_range)) {
-                a.nunique[0] = u + 1;
-                a.nunique[1] = nr - (u + 1);
-            }
             k.off = m.off;
             k.cnt = m.cnt;
-            const bool done = (k.cnt == 1 && key < a.ks.node_range && a.vals_sorted[k.off] < a.direct_hi) ||
-                              k.cnt > LONG_SEG;  // applied by the chain rule / chunked (long_partials)
+            const bool done = k.cnt > LONG_SEG ||  // chunked (long_partials)
+                              (!list && k.cnt == 1 && key < a.ks.node_range &&
+                               a.vals_sorted[k.off] < a.direct_hi);  // applied by the chain rule
             if (!done) {
                 k.active = true;
-                k.t = seg_target(a, u, nr, hl == 0);
+                k.t = seg_target(a, m.u, nr, hl == 0);
                 if (seg_applies(a, k.t))
                     for (int cb = 0; cb < 2; ++cb) {
                         const uint32_t c4 = hl + cb * SEG_LANES;
@@ -1026,14 +1026,13 @@ __global__ void __launch_bounds__(256, 4) k_segments_pipe(const __grid_constant_
     };
     SegKey cur, nxt;
     SegMeta mn{}, mnn{};
-    const uint32_t u0 = u_lo + gh;
-    if (u0 < u_hi) load_meta(u0, mn);
-    issue(u0, 0, mn, cur);
-    if (u0 + nh < u_hi) load_meta(u0 + nh, mn);
-    for (uint32_t u = u0, it = 0; u < u_hi; u += nh, ++it) {
+    if (gh < n_items) load_meta(gh, mn);
+    issue(gh, 0, mn, cur);
+    if (gh + nh < n_items) load_meta(gh + nh, mn);
+    for (uint32_t i = gh, it = 0; i < n_items; i += nh, ++it) {
         const int st = it & 1;
-        issue(u + nh, st ^ 1, mn, nxt);
-        if (u + 2 * nh < u_hi) load_meta(u + 2 * nh, mnn);  // consumed next iteration
+        issue(i + nh, st ^ 1, mn, nxt);
+        if (i + 2 * nh < n_items) load_meta(i + 2 * nh, mnn);  // consumed next iteration
         cp_wait<1>();
         if (cur.active) {
             const bool app = seg_applies(a, cur.t);
@@ -1125,7 +1124,7 @@ __device__ __forceinline__ void long_partials(const SegArgs& a, uint32_t gw, uin
     const uint32_t hl = lane & 15, half = lane >> 4, d4 = a.d / 4;
     const uint32_t n_slots = a.longs[1];
     for (uint32_t sl = gw; sl < n_slots; sl += nw) {
-        const uint32_t* rec = a.longs + 2 + 3 * a.owner[sl];
+        const uint32_t* rec = a.longs + LONG_HDR + 3 * a.owner[sl];
         const uint32_t u = rec[0], c = sl - rec[1];
         if (!seg_in_part(a, u)) continue;  // warp-uniform: reduced by the other launch
         const uint32_t r0 = c * LONG_CHUNK, cnt = min(LONG_CHUNK, a.offsets[u + 1] - a.offsets[u] - r0);
@@ -1151,19 +1150,35 @@ __device__ __forceinline__ void long_partials(const SegArgs& a, uint32_t gw, uin
     }
 }
 
-// The reduction's long-segment plan, on the helper stream after the sort (thread per run): keys with
-// more than LONG_SEG rows get LONG_CHUNK-row chunk slots (record (u, base, nch), owner per slot).
+// The reduction's plan, on the helper stream after the sort (thread per run): keys with more than
+// LONG_SEG rows get LONG_CHUNK-row chunk slots (record (u, base, nch), owner per slot); the other
+// runs the segment kernel has work for (repeated keys, relations, node keys whose single row was not
+// applied by the chain rule: slot >= direct) are listed in act (any order: each run is reduced
+// alone, in its fixed row order), so its warps skip the runs the chain rule already applied.
 __global__ void k_long_plan(const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ nruns, uint32_t n_max,
-                            uint32_t* __restrict__ longs, uint32_t* __restrict__ owner) {
+                            const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ vals_sorted,
+                            uint64_t node_range, uint32_t direct, const uint32_t* __restrict__ nsplit,
+                            uint32_t* __restrict__ nunique, uint32_t* __restrict__ longs,
+                            uint32_t* __restrict__ owner, uint32_t* __restrict__ act) {
     griddep_wait();
     const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= *nruns || u >= n_max) return;
-    const uint32_t cnt = offsets[u + 1] - offsets[u];
-    if (cnt <= LONG_SEG) return;
+    const uint32_t nr = *nruns;
+    if (u == 0) {  // runs of node keys / of relation keys (the sort's first run with key >= node_range)
+        const uint32_t split = min(*nsplit, nr);
+        nunique[0] = split;
+        nunique[1] = nr - split;
+    }
+    if (u >= nr || u >= n_max) return;
+    const uint32_t off = offsets[u], cnt = offsets[u + 1] - off;
+    if (cnt <= LONG_SEG) {
+        if (cnt == 1 && ukeys[u] < node_range && vals_sorted[off] < direct) return;  // applied by the chain rule
+        act[atomicAdd(&longs[2], 1u)] = u;
+        return;
+    }
     const uint32_t nch = (cnt + LONG_CHUNK - 1) / LONG_CHUNK;
     const uint32_t li = atomicAdd(&longs[0], 1u);
     const uint32_t base = atomicAdd(&longs[1], nch);
-    uint32_t* rec = longs + 2 + 3 * li;
+    uint32_t* rec = longs + LONG_HDR + 3 * li;
     rec[0] = u;
     rec[1] = base;
     rec[2] = nch;
@@ -1182,7 +1197,7 @@ __device__ __forceinline__ void long_final_body(const SegArgs& a) {
     const uint32_t n_long = *(volatile uint32_t*)&a.longs[0], nr = *a.nruns;
     // big segments (hot relations): a block each, 2 LONG_WARPS half-warp streams
     for (uint32_t li = blockIdx.x; li < n_long; li += gridDim.x) {
-        const uint32_t* rec = a.longs + 2 + 3 * li;
+        const uint32_t* rec = a.longs + LONG_HDR + 3 * li;
         const uint32_t u = rec[0], base = rec[1], nch = rec[2];
         if (nch <= LONG_BIG || !seg_in_part(a, u)) continue;  // block-uniform
         for (uint32_t c4 = hl; c4 < d4; c4 += 32) {
@@ -1211,7 +1226,7 @@ __device__ __forceinline__ void long_final_body(const SegArgs& a) {
     // the many small ones: a warp each (even / odd chunk streams, then their sum)
     const uint32_t half = lane >> 4, nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < n_long; li += nw) {
-        const uint32_t* rec = a.longs + 2 + 3 * li;
+        const uint32_t* rec = a.longs + LONG_HDR + 3 * li;
         const uint32_t u = rec[0], base = rec[1], nch = rec[2];
         if (nch > LONG_BIG || !seg_in_part(a, u)) continue;  // warp-uniform
         const SegTarget t = seg_target(a, u, nr, lane == 0);
@@ -1502,6 +1517,9 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
     a.rel_dense = rel_dense ? (E.rel_ext ? E.rel_ext : E.s.rel_dense) : nullptr;
     a.vals_sorted = E.s.vals_sorted;
     a.direct_hi = apply ? E.direct_hi : 0u;
+    // the plan's run list is valid when it was built for the same direct-apply threshold
+    static const bool walk = getenv("EMBER_SEG_WALK") != nullptr;  // A/B: every run visited
+    a.act = (!walk && a.direct_hi == E.plan_direct) ? E.s.seg_act : nullptr;
     a.d = E.dim;
     a.lr = E.m.lr;
     a.eps = E.m.eps;
@@ -1527,10 +1545,13 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
     EMBER_LAUNCHED(E);
 }
 
-void launch_long_plan(const Engine& E, uint32_t n_slots) {
+void launch_long_plan(const Engine& E, uint32_t n_slots, uint64_t node_range, uint32_t direct) {
     if (!n_slots) return;
     launch_pdl(k_long_plan, dim3((n_slots + 255) / 256), dim3(256), 0, E.side, (const uint32_t*)E.s.offsets,
-               (const uint32_t*)E.s.nruns, n_slots, E.s.longs, E.s.long_owner);
+               (const uint32_t*)E.s.nruns, n_slots, (const uint32_t*)E.s.ukeys, (const uint32_t*)E.s.vals_sorted,
+               node_range, direct, (const uint32_t*)E.s.nsplit, E.s.nunique, E.s.longs, E.s.long_owner,
+               E.s.seg_act);
+    E.plan_direct = direct;
     EMBER_LAUNCHED(E);
 }
 
