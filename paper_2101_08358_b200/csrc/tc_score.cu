@@ -79,6 +79,8 @@ struct TcArgs {
     float* dN_part;   // column-blocked [chunks][2][d/4][n_pad] float4
     uint32_t* flags;  // [0] = count, [1..] = side * b_cap + row
     int early;        // tiles 0 .. early-1 of an item go to epilogue group 0 (tile_group)
+    int l2_keep;      // dA stored with an L2 evict_last policy: the chain rule reads it back after the
+                      // dN kernel has streamed the packed operands through L2 (EMBER_DA_L2=0: plain stores)
     int diag;         // EMBER_TC_DIAG=1 (measurement only, wrong results): the epilogue skips its TMEM work
     unsigned long long* trace;  // debug timeline of CTA 0 (EMBER_TC_TRACE), nullptr normally
     unsigned long long* cta_times;  // EMBER_TC_CTATIMES: per CTA (start, end) %globaltimer ns, nullptr normally
@@ -594,6 +596,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                               : reinterpret_cast<float4*>(g.dN_part) +
                                     ((size_t)I.chunk * 2 + I.side) * (g.d / 4) * g.n_pad + row;
             const size_t cstride = MODE == MODE_ROWS ? (size_t)g.b_cap : (size_t)g.n_pad;
+            uint64_t l2pol = 0;
+            if (MODE == MODE_ROWS && g.l2_keep)
+                asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(l2pol));
             // batches: chunks [0, nchunks - 4), then the last 4 (one batch when nchunks <= 4)
             const int b0 = nchunks > 4 ? nchunks - 4 : nchunks;
             for (int half = 0; half < 2; ++half) {
@@ -615,10 +620,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         if (c >= cn) continue;
 #pragma unroll
                         for (int j = 0; j < 16; j += 4)
-                            if (16 * c + j < g.d)
-                                out[(size_t)((16 * c + j) / 4) * cstride] = make_float4(
-                                    __uint_as_float(accv[i][j]) * scale, __uint_as_float(accv[i][j + 1]) * scale,
-                                    __uint_as_float(accv[i][j + 2]) * scale, __uint_as_float(accv[i][j + 3]) * scale);
+                            if (16 * c + j < g.d) {
+                                float4* o = out + (size_t)((16 * c + j) / 4) * cstride;
+                                const float x0 = __uint_as_float(accv[i][j]) * scale,
+                                            x1 = __uint_as_float(accv[i][j + 1]) * scale,
+                                            x2 = __uint_as_float(accv[i][j + 2]) * scale,
+                                            x3 = __uint_as_float(accv[i][j + 3]) * scale;
+                                if (MODE == MODE_ROWS && g.l2_keep)  // dA: read back by the chain rule
+                                    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(o),
+                                                 "f"(x0), "f"(x1), "f"(x2), "f"(x3), "l"(l2pol)
+                                                 : "memory");
+                                else
+                                    *o = make_float4(x0, x1, x2, x3);
+                            }
                     }
                 }
                 if (cn == nchunks) break;
@@ -913,6 +927,7 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
     a.early = 3;
     if (const char* e = getenv("EMBER_TC_EARLY")) a.early = std::max(1, atoi(e));  // A/B (1: plain alternation)
     a.diag = getenv("EMBER_TC_DIAG") ? 1 : 0;
+    a.l2_keep = getenv("EMBER_DA_L2") && atoi(getenv("EMBER_DA_L2")) == 0 ? 0 : 1;
     a.trace = nullptr;
     const int nsub = (int)((nb + TILE - 1) / TILE);
     a.chunks2 = std::min(t.chunks2, nsub);
