@@ -503,15 +503,30 @@ void Engine::step(const uint32_t* edges, uint32_t nb, const uint32_t* bucket, ui
     const KeySpace ks = keyspace(i, j);
     mark(PHASE_SAMPLE);
     const uint64_t base = mix_seed(mix_seed(m.neg_seed, epoch, bucket_step), batch_in_bucket);
-    launch_sample_keys(*this, edges, nb, base, bucket, bucket_n, view(i), view(j), ks);
-    EMBER_CUDA(cudaEventRecord(ev_fork, stream));
-    EMBER_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
     direct_hi = getenv_direct() ? 2 * nb : 0;
+    static const bool sample_on_step = getenv("EMBER_SAMPLE_ON_STEP") != nullptr;  // A/B
+    if (tc_engine() && !wide && !sample_on_step) {
+        // The packed gather draws the shared negatives itself (same counter-based stream), so the
+        // sampling + keys kernel runs on the helper stream beside it, forked here: after the caller's
+        // work on the step stream and the previous step's updates.
+        EMBER_CUDA(cudaEventRecord(ev_fork, stream));
+        EMBER_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+        launch_sample_keys(*this, edges, nb, base, bucket, bucket_n, view(i), view(j), ks, side);
+        neg_inline.on = 1;
+        neg_inline.base = base;
+        neg_inline.bucket = bucket;
+        neg_inline.bucket_n = bucket_n;
+    } else {
+        launch_sample_keys(*this, edges, nb, base, bucket, bucket_n, view(i), view(j), ks);
+        EMBER_CUDA(cudaEventRecord(ev_fork, stream));
+        EMBER_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+    }
     sort_slots(nb, ks, direct_hi);
     loss_target = loss_out ? loss_out : s.loss;
     batch_tag = (1ull << 63) | ((epoch & 0xFFFFFull) << 40) | ((uint64_t)(bucket_step & 0xFFFFFu) << 20) |
                 (batch_in_bucket & 0xFFFFFu);
     forward_backward(edges, nb, i, j, s.negs, true);
+    neg_inline.on = 0;
     launch_loss(*this, nb, loss_out ? loss_out : s.loss);
     mark(PHASE_REDUCE);
     reduce_and_apply(nb, i, j, true, nullptr, nullptr, nullptr, nullptr);

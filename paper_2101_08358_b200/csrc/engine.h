@@ -211,7 +211,13 @@ struct Engine {
     // right in the chain rule (slots < direct_hi = 2nb); 0: every row goes through the segmented
     // reduction.
     uint32_t direct_hi = 0;
-    mutable uint32_t plan_direct = 0;  // direct threshold the last k_long_plan's run list was built for
+    mutable uint32_t plan_direct = 0;
+    // this step's negatives drawn by the packed gather itself (sampling + keys on the helper stream)
+    struct {
+        int on = 0;
+        uint64_t base = 0, bucket_n = 0;
+        const uint32_t* bucket = nullptr;
+    } neg_inline;  // direct threshold the last k_long_plan's run list was built for
     // where the step's loss goes; the tensor-core chain rule reduces it there itself (loss_fused)
     float* loss_target = nullptr;
     // batch id of the step being enqueued ("non-finite score -> error carrying batch id")
@@ -336,7 +342,7 @@ void launch_gather_pack_wide(const Engine& E, const uint32_t* edges, uint32_t nb
 void launch_keys(const Engine& E, const uint32_t* edges, uint32_t nb, const uint32_t* negs, const KeySpace& ks);
 // the training step's sample_negatives + gradient-slot keys, one kernel on the step stream
 void launch_sample_keys(const Engine& E, const uint32_t* edges, uint32_t nb, uint64_t base, const uint32_t* bucket,
-                        uint64_t bucket_n, const PartView& src, const PartView& dst, const KeySpace& ks);
+                        uint64_t bucket_n, const PartView& src, const PartView& dst, const KeySpace& ks, cudaStream_t st = nullptr);
 // the (key, slot) sort of s.keys and its runs, on the helper stream (sort.cu)
 void launch_slot_sort(const Engine& E, uint32_t n, uint32_t bits, uint32_t split_key);
 size_t slot_sort_scratch_words(uint32_t cap);

@@ -105,14 +105,27 @@ __device__ __forceinline__ void adjust_quad(int kind, const Quad& S, const Quad&
 
 // Packed negative row w of [2 sides][n_pad] (side 0 rows from partition j, side 1 from i; zero past
 // n_t): lane < CB splits 8 coordinates into bf16 hi|lo core-matrix rows of Npk.
+// Without negs (ns.bucket set instead) the warp draws the negative id itself with the same
+// counter-based stream as k_sample_keys (sample_one: slot side * nt + k), so the gather does not wait
+// for the sampling kernel, which then runs on the helper stream beside it.
+struct NegSampling {
+    uint64_t base = 0, bucket_n = 0;
+    const uint32_t* bucket = nullptr;
+    uint32_t n_deg = 0;
+    int on = 0;
+};
 __device__ __forceinline__ void negs_pack_warp(uint32_t w, uint32_t lane, const uint32_t* __restrict__ negs,
-                                               uint32_t nt, uint32_t n_pad, const PartView& pi, const PartView& pj,
-                                               uint32_t d, uint32_t CB, uint16_t* __restrict__ Npk) {
+                                               const NegSampling& ns, uint32_t nt, uint32_t n_pad, const PartView& pi,
+                                               const PartView& pj, uint32_t d, uint32_t CB,
+                                               uint16_t* __restrict__ Npk) {
     if (w >= 2 * n_pad || lane >= CB) return;
     const uint32_t side = w / n_pad, slot = w % n_pad;
     float x[8];
     if (slot < nt) {
-        const float* src = node_row(side == 0 ? pj : pi, negs[side * nt + slot], d);
+        const uint32_t id = ns.on ? sample_one(side * nt + slot, nt, ns.n_deg, ns.base, ns.bucket, ns.bucket_n, pi.first,
+                                               pi.rows, pj.first, pj.rows)
+                                  : negs[side * nt + slot];
+        const float* src = node_row(side == 0 ? pj : pi, id, d);
         // d % 4 == 0: each quad is all in or all out (lanes past d read nothing: the K padding is 0)
         const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
         const float4 a = 8 * lane < d ? ldg4(src + 8 * lane) : z;
@@ -147,11 +160,12 @@ __global__ void __launch_bounds__(32 * GP_WARPS) k_gather_pack(const uint32_t* _
                                                                int kind, uint32_t d, uint32_t CB, uint32_t cap,
                                                                uint16_t* __restrict__ Apk, float* __restrict__ fpos,
                                                                uint32_t row_ctas, const uint32_t* __restrict__ negs,
-                                                               uint32_t nt, uint32_t n_pad, uint16_t* __restrict__ Npk) {
+                                                               NegSampling ns, uint32_t nt, uint32_t n_pad,
+                                                               uint16_t* __restrict__ Npk) {
     griddep_wait();
     if (blockIdx.x >= row_ctas) {  // the trailing CTAs pack the shared negatives (one warp per row)
         const uint32_t w = (blockIdx.x - row_ctas) * GP_WARPS + (threadIdx.x >> 5);
-        negs_pack_warp(w, threadIdx.x & 31, negs, nt, n_pad, pi, pj, d, CB, Npk);
+        negs_pack_warp(w, threadIdx.x & 31, negs, ns, nt, n_pad, pi, pj, d, CB, Npk);
         return;
     }
     extern __shared__ uint4 gsm[];
@@ -324,7 +338,7 @@ __global__ void k_gather_negs(const uint32_t* __restrict__ negs, uint32_t n, uin
         for (uint32_t v = lane; v < d / 4; v += 32) dst[v] = ldg4(src + 4 * v);
         return;
     }
-    negs_pack_warp(w, lane, negs, nt, n_pad, pi, pj, d, CB, Npk);
+    negs_pack_warp(w, lane, negs, NegSampling{}, nt, n_pad, pi, pj, d, CB, Npk);
 }
 
 __device__ __forceinline__ uint32_t node_key(const KeySpace& ks, uint32_t id) {
@@ -1397,9 +1411,17 @@ void launch_gather_adjust(const Engine& E, const uint32_t* edges, uint32_t nb, c
         const uint32_t row_ctas = rows_pad / GP_ROWS, neg_ctas = (2 * E.n_pad + GP_WARPS - 1) / GP_WARPS;
         const size_t sm = (size_t)4 * E.CB * GP_ROWS * 16;
         opt_in_smem((const void*)k_gather_pack, sm, E.device);
+        NegSampling ns;
+        if (E.neg_inline.on) {  // the step's negatives drawn here (k_sample_keys runs on the helper stream)
+            ns.on = 1;
+            ns.base = E.neg_inline.base;
+            ns.bucket = E.neg_inline.bucket;
+            ns.bucket_n = E.neg_inline.bucket_n;
+            ns.n_deg = (uint32_t)ceil((double)E.m.alpha * (double)E.nt);
+        }
         launch_pdl(k_gather_pack, dim3(row_ctas + neg_ctas), dim3(32 * GP_WARPS), sm, E.stream, edges, nb, pi, pj,
                    E.rel_theta, E.m.kind, E.dim, E.CB, (uint32_t)E.b_cap, E.s.Apk, E.s.fpos, row_ctas,
-                   negs, E.nt, (uint32_t)E.n_pad, E.s.Npk);
+                   negs, ns, E.nt, (uint32_t)E.n_pad, E.s.Npk);
     } else {
         const uint32_t warps = 8;
         k_gather_adjust<<<(nb + warps - 1) / warps, warps * 32, 0, E.stream>>>(edges, nb, pi, pj, E.rel_theta,
@@ -1438,10 +1460,12 @@ void launch_keys(const Engine& E, const uint32_t* edges, uint32_t nb, const uint
 }
 
 void launch_sample_keys(const Engine& E, const uint32_t* edges, uint32_t nb, uint64_t base, const uint32_t* bucket,
-                        uint64_t bucket_n, const PartView& src, const PartView& dst, const KeySpace& ks) {
+                        uint64_t bucket_n, const PartView& src, const PartView& dst, const KeySpace& ks,
+                        cudaStream_t st) {
     const uint32_t n = E.slots(nb);
     const uint32_t n_deg = (uint32_t)ceil((double)E.m.alpha * (double)E.nt);
-    launch_pdl(k_sample_keys, dim3((n + 255) / 256), dim3(256), 0, E.stream, edges, nb, E.s.negs, E.n_neg, E.nt, n_deg,
+    launch_pdl(k_sample_keys, dim3((n + 255) / 256), dim3(256), 0, st ? st : E.stream, edges, nb, E.s.negs, E.n_neg,
+               E.nt, n_deg,
                base, bucket, bucket_n, src, dst, n, ks, E.s.keys, E.s.longs);
     EMBER_LAUNCHED(E);
 }
