@@ -7,10 +7,11 @@ import numpy as np
 import torch
 
 sys.path.insert(0, ".")
-sys.path.insert(0, "tests")
-from gpu_helpers import make_trainer  # noqa: E402
+import paper_2101_08358_b200 as eb  # noqa: E402
 
-tr = make_trainer("complex", dim=16, b=50000, nt=1000, V=3000, engine="tc")
+tr = eb.Trainer(eb.Hyper(kind="complex", dim=16, batch_size=50000, num_negatives=1000, engine="tc"), 3000, 20, 1,
+                device=0)
+tr.init_embeddings(11)
 rng = np.random.default_rng(1)
 nb, n_neg, node_range = 50000, 2000, 10_757_000
 z = rng.zipf(1.2, size=2 * nb + n_neg).astype(np.uint64) - 1
@@ -19,7 +20,6 @@ zr = rng.zipf(1.5, size=nb).astype(np.uint64) - 1
 rels = (node_range + (zr * 2654435761) % 14824).astype(np.uint32)
 keys = np.concatenate([nodes, rels])
 dk = torch.from_numpy(keys.view(np.int32)).cuda()
-import paper_2101_08358_b200 as eb  # noqa: E402
 from paper_2101_08358_b200 import _lib  # noqa: E402
 
 lib = eb.lib()
