@@ -202,6 +202,8 @@ Engine::Engine(int dev, const ember_model_desc& md, const ember_graph_desc& gd, 
     EMBER_CUDA(cudaEventCreateWithFlags(&ev_rel_grad, cudaEventDisableTiming));
     EMBER_CUDA(cudaEventCreateWithFlags(&ev_rel_done, cudaEventDisableTiming));
     if (const char* e = getenv("EMBER_DENSE_RELATIONS")) force_dense = atoi(e) != 0;
+    sample_on_step = getenv("EMBER_SAMPLE_ON_STEP") && atoi(getenv("EMBER_SAMPLE_ON_STEP")) != 0;
+    seg_walk = getenv("EMBER_SEG_WALK") && atoi(getenv("EMBER_SEG_WALK")) != 0;
     parts.assign(g.num_partitions, PartView{nullptr, nullptr, 0, 0});
     for (uint32_t k = 0; k < g.num_partitions; ++k) {
         parts[k].first = partition_offset(g.num_nodes, g.num_partitions, k);
@@ -504,7 +506,6 @@ void Engine::step(const uint32_t* edges, uint32_t nb, const uint32_t* bucket, ui
     mark(PHASE_SAMPLE);
     const uint64_t base = mix_seed(mix_seed(m.neg_seed, epoch, bucket_step), batch_in_bucket);
     direct_hi = getenv_direct() ? 2 * nb : 0;
-    static const bool sample_on_step = getenv("EMBER_SAMPLE_ON_STEP") != nullptr;  // A/B
     if (tc_engine() && !wide && !sample_on_step) {
         // The packed gather draws the shared negatives itself (same counter-based stream), so the
         // sampling + keys kernel runs on the helper stream beside it, forked here: after the caller's

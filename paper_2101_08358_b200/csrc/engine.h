@@ -176,6 +176,9 @@ struct Engine {
     cudaStream_t comm = nullptr;
     cudaEvent_t ev_rel_grad = nullptr, ev_rel_done = nullptr;
     bool force_dense = false;  // EMBER_DENSE_RELATIONS=1: that path at world 1 (tests: bit-identical)
+    // A/B switches read per context (tests: bit-identical either way): EMBER_SAMPLE_ON_STEP=1 samples
+    // on the step stream before the gather; EMBER_SEG_WALK=1 the segment kernel visits every run
+    bool sample_on_step = false, seg_walk = false;
     // host-batch path: positives copied on `io` into one of two staging slots, overlapping the
     // previous step; ev_staged[k]: copy into slot k done; ev_consumed[k]: the step reading slot k done
     cudaStream_t io = nullptr, io_out = nullptr;  // host->device batches / device->host losses

@@ -1542,8 +1542,7 @@ void launch_segments(const Engine& E, uint32_t n_slots, const KeySpace& ks, bool
     a.vals_sorted = E.s.vals_sorted;
     a.direct_hi = apply ? E.direct_hi : 0u;
     // the plan's run list is valid when it was built for the same direct-apply threshold
-    static const bool walk = getenv("EMBER_SEG_WALK") != nullptr;  // A/B: every run visited
-    a.act = (!walk && a.direct_hi == E.plan_direct) ? E.s.seg_act : nullptr;
+    a.act = (!E.seg_walk && a.direct_hi == E.plan_direct) ? E.s.seg_act : nullptr;  // (E.seg_walk: A/B)
     a.d = E.dim;
     a.lr = E.m.lr;
     a.eps = E.m.eps;

@@ -310,6 +310,34 @@ def test_relation_first_reduction_bit_identical(graph, monkeypatch, kind, b):
         assert a.tobytes() == b_.tobytes()
 
 
+@pytest.mark.parametrize("switch", ["EMBER_SAMPLE_ON_STEP", "EMBER_SEG_WALK", "EMBER_LONG_FINAL_LATE", "EMBER_DA_L2"])
+def test_step_scheduling_switches_bit_identical(graph, monkeypatch, switch):
+    """The step's scheduling choices leave every parameter bit-identical to their A/B alternative:
+    negatives drawn by the packed gather while k_sample_keys runs on the helper stream (vs sampling
+    on the step stream first), the segment kernel walking only the plan's runs with work (vs every
+    run), k_long_final scheduled once the chunk partials exist (vs after the segment kernel), dA
+    stored with an L2 evict_last policy (vs plain stores) — long segments included (b = 1500)."""
+    edges, off, _ = graph
+    tabs = []
+    for on in (False, True):
+        for sw in ("EMBER_SAMPLE_ON_STEP", "EMBER_SEG_WALK", "EMBER_LONG_FINAL_LATE", "EMBER_DA_L2"):
+            monkeypatch.delenv(sw, raising=False)
+        if on:
+            monkeypatch.setenv(switch, "0" if switch == "EMBER_DA_L2" else "1")
+        tr = make_trainer("distmult", dim=32, b=1500, nt=64, p=2, engine="tc")
+        for step, (i, j) in enumerate([(0, 1), (1, 1), (1, 0), (0, 0)]):
+            bk = i * 2 + j
+            bucket = _dev(edges[off[bk]:off[bk + 1]])
+            n = (off[bk + 1] - off[bk]) // 1500
+            for k in range(min(3, n)):
+                tr.train_batch(bucket, k * 1500, 1500, i, j, epoch=0, bucket_step=step, batch_in_bucket=k)
+        tr.synchronize()
+        tabs.append(host_tables(tr))
+        tr.close()
+    for a, b_ in zip(tabs[0], tabs[1]):
+        assert a.tobytes() == b_.tobytes()
+
+
 def test_host_batch_path_bit_identical(graph):
     """ember_train_batch_host (positives from pinned host memory, double-buffered asynchronous
     copies overlapping the previous step) trains exactly like ember_train_batch."""
