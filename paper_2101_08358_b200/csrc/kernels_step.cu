@@ -512,9 +512,6 @@ __global__ void __launch_bounds__(256, 4) k_chain_rule(const uint32_t* __restric
 // edge's indices, ranks, uniqueness flags and g0 are loaded with its copies (one latency).
 constexpr int CP_ROLES = 7;  // S, T, R, acc_S, acc_T, U (dA dst), W (dA src)
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(tc::smem_addr(smem)), "l"(gmem) : "memory");
-}
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tc::smem_addr(smem)), "l"(gmem) : "memory");
 }
@@ -878,23 +875,6 @@ __device__ __forceinline__ void add4(float4& s, const float4& x) {
     s.w += x.w;
 }
 
-// Sum of rows [0, cnt) (stride d floats) at column block c4, in row order, 4 loads in flight.
-__device__ __forceinline__ float4 sum_rows(const float* base, uint32_t cnt, uint32_t d, uint32_t c4) {
-    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-    uint32_t r = 0;
-    for (; r + 4 <= cnt; r += 4) {
-        const float4 x0 = ldg4(base + (uint64_t)r * d + 4 * c4);
-        const float4 x1 = ldg4(base + (uint64_t)(r + 1) * d + 4 * c4);
-        const float4 x2 = ldg4(base + (uint64_t)(r + 2) * d + 4 * c4);
-        const float4 x3 = ldg4(base + (uint64_t)(r + 3) * d + 4 * c4);
-        add4(s, x0);
-        add4(s, x1);
-        add4(s, x2);
-        add4(s, x3);
-    }
-    for (; r < cnt; ++r) add4(s, ldg4(base + (uint64_t)r * d + 4 * c4));
-    return s;
-}
 
 // Sum of rows [0, cnt) at column blocks c4a and c4b (c4b valid iff hasb), in row order, 4 loads
 // in flight.
@@ -1067,24 +1047,6 @@ __global__ void __launch_bounds__(256, 4) k_segments_pipe(const __grid_constant_
     cp_wait<0>();
 }
 
-// Sum of rows r = r0, r0 + step, ... < cnt at column block c4, 4 loads in flight, in row order.
-__device__ __forceinline__ float4 sum_rows_strided(const float* base, uint32_t r0, uint32_t step, uint32_t cnt,
-                                                   uint32_t d, uint32_t c4) {
-    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-    uint32_t r = r0;
-    for (; r + 3 * step < cnt; r += 4 * step) {
-        const float4 x0 = ldg4(base + (uint64_t)r * d + 4 * c4);
-        const float4 x1 = ldg4(base + (uint64_t)(r + step) * d + 4 * c4);
-        const float4 x2 = ldg4(base + (uint64_t)(r + 2 * step) * d + 4 * c4);
-        const float4 x3 = ldg4(base + (uint64_t)(r + 3 * step) * d + 4 * c4);
-        add4(s, x0);
-        add4(s, x1);
-        add4(s, x2);
-        add4(s, x3);
-    }
-    for (; r < cnt; r += step) add4(s, ldg4(base + (uint64_t)r * d + 4 * c4));
-    return s;
-}
 
 // The same for two column blocks at once (c4a, and c4b when hasb): 8 loads in flight, and per
 // column the same row order (bit-identical to two sum_rows_strided passes).

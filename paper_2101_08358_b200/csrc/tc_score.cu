@@ -183,7 +183,6 @@ __device__ __forceinline__ uint64_t mndesc(const uint8_t* tile, int R, int s, in
     return tc::sdesc(tc::smem_addr(tile) + (uint32_t)(cb0 * R * 16 + s * 256), 128u, (uint32_t)(R * 16));
 }
 
-__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 __device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
     asm volatile(

@@ -169,7 +169,7 @@ double tc_selftest(int device, int mode, int K, int N, uint64_t seed) {
 namespace ember {
 namespace {
 __global__ void __launch_bounds__(128, 1) k_tc_mmabench(int mode, int N, int iters, int nacc, long long* out) {
-    extern __shared__ __align__(1024) uint8_t smem[];
+    extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t bar;
     __shared__ uint32_t tslot;
     const int warp = threadIdx.x / 32;
