@@ -506,7 +506,10 @@ void Engine::step(const uint32_t* edges, uint32_t nb, const uint32_t* bucket, ui
     mark(PHASE_SAMPLE);
     const uint64_t base = mix_seed(mix_seed(m.neg_seed, epoch, bucket_step), batch_in_bucket);
     direct_hi = getenv_direct() ? 2 * nb : 0;
-    if (tc_engine() && !wide && !sample_on_step) {
+    // EMBER_HOST_INLINE=1 (A/B): also for host-staged batches, where it measured slower (0.3229 vs
+    // 0.3031 ms per step of the host-buffer path: the staging waits then sit right before the gather)
+    static const int host_inline = getenv("EMBER_HOST_INLINE") ? atoi(getenv("EMBER_HOST_INLINE")) : 0;
+    if (tc_engine() && !wide && !sample_on_step && (!edges_ready || host_inline)) {
         // The packed gather draws the shared negatives itself (same counter-based stream), so the
         // sampling + keys kernel runs on the helper stream beside it, forked here: after the caller's
         // work on the step stream and the previous step's updates.
