@@ -37,54 +37,76 @@ std::uint64_t OrderingPlan::next_use_after(PartitionId part, std::uint64_t step)
     return hit == uses.end() ? kNeverUsed : *hit;
 }
 
+// Structural check of a plan, one pass per invariant: (1) the sequence is a permutation of
+// the p x p buckets, (2) every buffer state fits in c slots, is sorted, and each state follows
+// its predecessor by exactly the recorded swap, (3) the per-bucket state index never goes
+// backwards and names a state holding both partitions of the bucket.
 void OrderingPlan::validate() const {
+    auto fail = [](const std::string& what) { throw EmberError("invalid ordering plan: " + what); };
     const std::uint64_t total = num_buckets();
-    if (bucket_sequence.size() != total) throw EmberError("plan: bucket count != p^2");
-    if (bucket_state.size() != total) throw EmberError("plan: missing per-bucket state index");
-    std::vector<std::uint8_t> covered(total, 0);
-    for (const BucketId& b : bucket_sequence) {
-        if (b.i >= p || b.j >= p) throw EmberError("plan: bucket id out of range");
-        std::uint8_t& cell = covered[static_cast<std::uint64_t>(b.i) * p + b.j];
-        if (cell) throw EmberError("plan: duplicate bucket");
-        cell = 1;
+    if (bucket_sequence.size() != total || bucket_state.size() != total)
+        fail("expected " + std::to_string(total) + " buckets and state indices, got " +
+             std::to_string(bucket_sequence.size()) + " / " + std::to_string(bucket_state.size()));
+
+    std::vector<bool> seen(total, false);
+    for (std::uint64_t t = 0; t < total; ++t) {
+        const BucketId b = bucket_sequence[t];
+        if (b.i >= p || b.j >= p) fail("bucket at step " + std::to_string(t) + " names a partition >= p");
+        const std::uint64_t cell = static_cast<std::uint64_t>(b.i) * p + b.j;
+        if (seen[cell]) fail("bucket at step " + std::to_string(t) + " appears twice");
+        seen[cell] = true;
     }
-    if (buffer_states.empty()) throw EmberError("plan: no buffer states");
-    if (buffer_states.size() != swap_events.size() + 1) throw EmberError("plan: state count != swaps + 1");
-    for (const auto& st : buffer_states) {
-        if (st.size() > c) throw EmberError("plan: buffer state exceeds capacity");
-        if (!std::is_sorted(st.begin(), st.end())) throw EmberError("plan: state not sorted");
+
+    if (buffer_states.size() != swap_events.size() + 1 || swap_count != swap_events.size())
+        fail("swap bookkeeping disagrees (states " + std::to_string(buffer_states.size()) + ", events " +
+             std::to_string(swap_events.size()) + ", swap_count " + std::to_string(swap_count) + ")");
+    // Membership bitmap of the current state; a legal transition clears exactly the evicted
+    // partition and sets exactly the admitted one.
+    std::vector<std::uint8_t> held(p, 0);
+    for (std::size_t k = 0; k < buffer_states.size(); ++k) {
+        const auto& st = buffer_states[k];
+        if (st.size() > c) fail("state " + std::to_string(k) + " holds more than c partitions");
+        for (std::size_t q = 0; q < st.size(); ++q)
+            if (st[q] >= p || (q > 0 && st[q] <= st[q - 1]))
+                fail("state " + std::to_string(k) + " is not a sorted set of partition ids");
+        if (k == 0) {
+            for (PartitionId x : st) held[x] = 1;
+            continue;
+        }
+        const SwapEvent& ev = swap_events[k - 1];
+        if (ev.evicted >= p || ev.admitted >= p || !held[ev.evicted] || held[ev.admitted])
+            fail("swap " + std::to_string(k - 1) + " does not apply to state " + std::to_string(k - 1));
+        held[ev.evicted] = 0;
+        held[ev.admitted] = 1;
+        std::size_t n_held = 0;
+        for (PartitionId x = 0; x < p; ++x) n_held += held[x];
+        bool same = n_held == st.size();
+        for (PartitionId x : st) same = same && held[x];
+        if (!same) fail("state " + std::to_string(k) + " is not state " + std::to_string(k - 1) + " after its swap");
     }
-    for (std::size_t k = 1; k < buffer_states.size(); ++k) {
-        const auto& before = buffer_states[k - 1];
-        const auto& after = buffer_states[k];
-        std::vector<PartitionId> out, in;
-        std::set_difference(before.begin(), before.end(), after.begin(), after.end(), std::back_inserter(out));
-        std::set_difference(after.begin(), after.end(), before.begin(), before.end(), std::back_inserter(in));
-        if (out.size() != 1 || in.size() != 1) throw EmberError("plan: consecutive states differ by != 1 swap");
-        if (out[0] != swap_events[k - 1].evicted || in[0] != swap_events[k - 1].admitted)
-            throw EmberError("plan: swap event does not match state transition");
-    }
-    std::uint32_t last = 0;
+
+    std::uint32_t prev = 0;
     for (std::uint64_t t = 0; t < total; ++t) {
         const std::uint32_t s = bucket_state[t];
-        if (s >= buffer_states.size()) throw EmberError("plan: state index out of range");
-        if (s < last) throw EmberError("plan: state index regressed");
-        last = s;
+        if (s >= buffer_states.size() || s < prev)
+            fail("state index of step " + std::to_string(t) + " is out of range or goes backwards");
+        prev = s;
         const auto& st = buffer_states[s];
-        if (!std::binary_search(st.begin(), st.end(), bucket_sequence[t].i) ||
-            !std::binary_search(st.begin(), st.end(), bucket_sequence[t].j))
-            throw EmberError("plan: bucket processed without both partitions resident");
+        const BucketId b = bucket_sequence[t];
+        if (!std::binary_search(st.begin(), st.end(), b.i) || !std::binary_search(st.begin(), st.end(), b.j))
+            fail("step " + std::to_string(t) + " runs a bucket whose partitions are not both buffered");
     }
-    if (swap_count != swap_events.size()) throw EmberError("plan: swap_count mismatch");
 }
 
 namespace {
 
+// Accepted (p, c): p >= 1 and 1 <= c <= p, with c >= 2 as soon as there are off-diagonal
+// buckets (p > 1), since a bucket (i, j) needs i and j resident together.
 void require_valid_pc(std::uint32_t p, std::uint32_t c) {
-    if (p == 0) throw ConfigError("ordering: p must be >= 1");
-    if (c > p) throw ConfigError("ordering: c must be <= p");
-    if (c < 2 && p > 1) throw ConfigError("ordering: c must be >= 2 when p > 1");
-    if (c == 0) throw ConfigError("ordering: c must be >= 1");
+    if (p == 0) throw ConfigError("ordering needs at least one partition (p = 0)");
+    if (c > p) throw ConfigError("ordering buffer capacity c = " + std::to_string(c) + " exceeds p = " + std::to_string(p));
+    if (c < 2 && p > 1) throw ConfigError("ordering with p > 1 needs a buffer of at least 2 partitions");
+    if (c == 0) throw ConfigError("ordering buffer capacity c must be positive");
 }
 
 // Belady replay (furthest next use, ties to the lower id) of plan.bucket_sequence into a
@@ -136,7 +158,7 @@ void replay_with_belady(OrderingPlan& plan) {
                     furthest = nu;
                 }
             }
-            if (!found) throw EmberError("belady: no evictable partition (c too small for bucket)");
+            if (!found) throw EmberError("Belady replay: every buffered partition is needed by the current bucket (c too small)");
             resident[victim] = 0;
             resident[need] = 1;
             plan.swap_events.push_back({static_cast<std::uint32_t>(t), victim, need});
@@ -258,17 +280,17 @@ OrderingPlan empty_plan(OrderingKind kind, std::uint32_t p, std::uint32_t c, std
 }  // namespace
 
 std::uint64_t lower_bound_swaps(std::uint32_t p, std::uint32_t c) {
-    if (c == 0 || c > p) throw ConfigError("lower_bound_swaps: requires 1 <= c <= p");
+    if (c == 0 || c > p) throw ConfigError("lower_bound_swaps: c must lie in [1, p]");
     if (p == c) return 0;
-    if (c == 1) throw ConfigError("lower_bound_swaps: c = 1 cannot cover pairs for p > 1");
+    if (c == 1) throw ConfigError("lower_bound_swaps: with p > 1 a single-slot buffer never holds a pair");
     const std::uint64_t pairs_left = static_cast<std::uint64_t>(p) * (p - 1) / 2 - static_cast<std::uint64_t>(c) * (c - 1) / 2;
     return (pairs_left + c - 2) / (c - 1);  // ceil(pairs_left / (c-1)), §4.1
 }
 
 std::uint64_t elimination_swap_formula(std::uint32_t p, std::uint32_t c) {
-    if (c == 0 || c > p) throw ConfigError("elimination_swap_formula: requires 1 <= c <= p");
+    if (c == 0 || c > p) throw ConfigError("elimination_swap_formula: c must lie in [1, p]");
     if (p == c) return 0;
-    if (c == 1) throw ConfigError("elimination_swap_formula: c = 1 invalid for p > 1");
+    if (c == 1) throw ConfigError("elimination_swap_formula: with p > 1 a single-slot buffer never holds a pair");
     // (p-c) + (x+1)[(p-c) - x(c-1)/2], x = floor((p-c)/(c-1)), evaluated in half units
     const std::uint64_t gap = p - c;
     const std::uint64_t x = gap / (c - 1);
@@ -280,7 +302,7 @@ OrderingPlan elimination_order(std::uint32_t p, std::uint32_t c, std::uint64_t s
     OrderingPlan plan = empty_plan(OrderingKind::Elimination, p, c, seed);
     Eliminator(p, c, seed, plan.bucket_sequence).run();
     if (plan.bucket_sequence.size() != plan.num_buckets())
-        throw EmberError("elimination_order: construction missed buckets");
+        throw EmberError("elimination order: the construction did not visit every bucket");
     replay_with_belady(plan);
     return plan;
 }
@@ -345,7 +367,7 @@ OrderingPlan make_plan(OrderingKind kind, std::uint32_t p, std::uint32_t c, std:
         case OrderingKind::HilbertSymmetric: return hilbert_symmetric_order(p, c);
         case OrderingKind::Random: return random_order(p, c, seed);
     }
-    throw ConfigError("make_plan: unknown ordering kind");
+    throw ConfigError("make_plan: ordering kind out of range");
 }
 
 IOReport simulate_io(const OrderingPlan& plan, std::uint64_t partition_bytes) {

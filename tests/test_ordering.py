@@ -88,3 +88,53 @@ def test_reference_unit_test_passes_in_place():
     out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "16 passed" in out.stdout
+
+
+_VALIDATE_CPP = r"""
+#include "ember/ordering.h"
+#include <cstdio>
+#include <functional>
+using namespace ember;
+static int rejects(const std::function<void(OrderingPlan&)>& corrupt, const OrderingPlan& good) {
+    OrderingPlan bad = good;
+    corrupt(bad);
+    try { bad.validate(); } catch (const EmberError&) { return 0; }
+    return 1;
+}
+int main() {
+    int fails = 0;
+    for (auto kind : {OrderingKind::Elimination, OrderingKind::Hilbert, OrderingKind::HilbertSymmetric,
+                      OrderingKind::Random})
+        for (unsigned p : {1u, 4u, 7u, 16u})
+            for (unsigned c : {2u, 3u, 5u}) {
+                if (c > p) continue;
+                OrderingPlan plan = make_plan(kind, p, c, 42);
+                plan.validate();  // every generated plan is valid
+                if (plan.swap_events.empty()) continue;
+                fails += rejects([](OrderingPlan& q) { q.bucket_sequence.pop_back(); }, plan);
+                fails += rejects([](OrderingPlan& q) { q.bucket_sequence[1] = q.bucket_sequence[0]; }, plan);
+                fails += rejects([](OrderingPlan& q) { q.swap_count += 1; }, plan);
+                fails += rejects([](OrderingPlan& q) { std::swap(q.swap_events[0].evicted, q.swap_events[0].admitted); }, plan);
+                fails += rejects([](OrderingPlan& q) { q.bucket_state.back() = 0; }, plan);
+                fails += rejects([](OrderingPlan& q) { q.buffer_states[1].push_back(q.p); }, plan);
+            }
+    try { make_plan(OrderingKind::Elimination, 4, 5, 0); ++fails; } catch (const ConfigError&) {}
+    try { make_plan(OrderingKind::Elimination, 4, 1, 0); ++fails; } catch (const ConfigError&) {}
+    std::printf("validate fails=%d\n", fails);
+    return fails != 0;
+}
+"""
+
+
+def test_plan_validation_accepts_generated_and_rejects_corrupted_plans(tmp_path):
+    """OrderingPlan::validate (ordering.h:45) accepts every generated plan and throws EmberError for
+    each structural corruption; bad (p, c) raise ConfigError."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "validate.cpp"
+    src.write_text(_VALIDATE_CPP)
+    exe = tmp_path / "validate"
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(root, "include"), str(src),
+                    os.path.join(root, "paper_2101_08358_b200", "csrc", "host", "ordering.cpp"), "-o", str(exe)],
+                   check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "fails=0" in r.stdout, r.stdout + r.stderr
