@@ -960,7 +960,9 @@ void launch_contract_tc(Engine& E, uint32_t nb) {
     // free SMs run the helper stream's key sort. Test caps (EMBER_TC_MAXGRID) are used as given.
     constexpr int kSpareSms = 8;
     const int g2 = std::min(items2, gmax);
-    const int grid1 = std::min(items1, t.max_grid == 0 && E.sm_count - g2 <= kSpareSms ? g2 : gmax);
+    static const int rows_grid = getenv("EMBER_TC_ROWS_GRID") ? atoi(getenv("EMBER_TC_ROWS_GRID")) : 0;  // A/B
+    const int grid1 = rows_grid > 0 ? std::min(items1, std::min(rows_grid, gmax))
+                                    : std::min(items1, t.max_grid == 0 && E.sm_count - g2 <= kSpareSms ? g2 : gmax);
     a.arrive = t.arrive;
     a.arrive_base = t.arrive_base[0];
     t.arrive_base[0] += (uint32_t)grid1;
